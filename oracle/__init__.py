@@ -1,0 +1,253 @@
+"""CPU oracle for the BioDynaMo/TeraAgent mechanics hot path (arXiv 2503.10796).
+
+TEST INFRASTRUCTURE ONLY.  Only ``tests/``, ``__graft_entry__.smoke()`` and
+``bench.py``'s ``cpu_baseline`` / ``--impl reference`` leg may import this package.
+The product package ``paper_2503_10796_b200`` never imports it and shares no code
+with it.
+
+The arithmetic lives in plain C (``oracle/oracle.c``; fp64, ``-ffp-contract=off``,
+explicit ``fma`` at the two canonical sites).  This module only marshals numpy
+arrays through ctypes.  Each function cites the passage of PAPER.md it follows in
+the C source.
+
+Parity status per function (DESIGN.md section 4 lists the pins):
+  philox4x32_10        pinned (ATen's philox_engine, a library routine)
+  init_spheres         pinned (exact u53 mapping, moments)
+  neighbor_pairs_*     pinned (brute force on tiny inputs, pure-Python recount)
+  mech_step            pinned (Eq. 4.1 closed forms, antisymmetry, cap, static transparency)
+  sorted_order         pinned (Morton worked example P:4762-4766, sortedness invariants)
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SO = os.path.join(_HERE, "liboracle.so")
+_SRC = [os.path.join(_HERE, "oracle.c")]
+
+CFLAGS = ["-O2", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared", "-std=c11"]
+
+MOVED, GREW, ADDED, STATIC = 1, 2, 4, 8
+NNZ_SHIFT = 4
+
+
+def build(force: bool = False) -> str:
+    """Compile liboracle.so with gcc (no CUDA)."""
+    newest = max(os.path.getmtime(s) for s in _SRC)
+    if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < newest:
+        tmp = _SO + ".tmp"
+        subprocess.check_call(["gcc", *CFLAGS, *_SRC, "-o", tmp, "-lm"])
+        os.replace(tmp, _SO)
+    return _SO
+
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    global _lib
+    if _lib is None:
+        build()
+        L = ctypes.CDLL(_SO)
+        P = ctypes.c_void_p
+        i64 = ctypes.c_int64
+        u64 = ctypes.c_uint64
+        dbl = ctypes.c_double
+        i32 = ctypes.c_int
+        L.orc_philox4x32_10.argtypes = [P, P, P]
+        L.orc_u53.argtypes = [ctypes.c_uint32, ctypes.c_uint32]
+        L.orc_u53.restype = dbl
+        L.orc_u32.argtypes = [ctypes.c_uint32]
+        L.orc_u32.restype = dbl
+        L.orc_init_spheres.argtypes = [i64, i64, u64, dbl, dbl, dbl, i32, P, P, P, P, P, P]
+        L.orc_morton.argtypes = [P, i32, i32]
+        L.orc_morton.restype = u64
+        L.orc_blocked_key.argtypes = [i64, i64, i64, P]
+        L.orc_blocked_key.restype = u64
+        L.orc_grid_geometry.argtypes = [i64, P, P, P, P, dbl, P, P, P, P]
+        L.orc_neighbor_pairs_brute.argtypes = [i64, P, P, P, P, dbl, P, i64]
+        L.orc_neighbor_pairs_brute.restype = i64
+        L.orc_neighbor_pairs_grid.argtypes = [i64, P, P, P, P, P, dbl, P, i64]
+        L.orc_neighbor_pairs_grid.restype = i64
+        L.orc_pair_force.argtypes = [dbl, dbl, dbl, dbl, dbl, P, P]
+        L.orc_pair_force.restype = dbl
+        L.orc_mech_step.argtypes = [i64, P, P, P, P, P, P, P, i64, P, P, P, P, P, P, P]
+        L.orc_sorted_order.argtypes = [i64, P, P, P, P, P, dbl, P, P]
+        _lib = L
+    return _lib
+
+
+def _p(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+def _f64(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def _u32(a):
+    return np.ascontiguousarray(a, dtype=np.uint32)
+
+
+class MechParams(ctypes.Structure):
+    """Mirror of ``orc_mech_params`` (oracle.c)."""
+
+    _fields_ = [
+        ("k", ctypes.c_double),
+        ("gamma", ctypes.c_double),
+        ("dt", ctypes.c_double),
+        ("max_disp", ctypes.c_double),
+        ("force_threshold", ctypes.c_double),
+        ("radius", ctypes.c_double),
+        ("detect_static", ctypes.c_int32),
+        ("boundary", ctypes.c_int32),
+        ("lo", ctypes.c_double * 3),
+        ("hi", ctypes.c_double * 3),
+    ]
+
+
+class Counters(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int64) for n in ("cand", "nbr", "cont", "n_static")]
+
+
+def mech_params(k=2.0, gamma=1.0, dt=0.01, max_disp=3.0, force_threshold=0.0, radius=0.0,
+                detect_static=False, boundary=0, lo=(0.0, 0.0, 0.0), hi=(0.0, 0.0, 0.0)):
+    p = MechParams()
+    p.k, p.gamma, p.dt, p.max_disp = k, gamma, dt, max_disp
+    p.force_threshold, p.radius = force_threshold, radius
+    p.detect_static, p.boundary = int(bool(detect_static)), int(boundary)
+    p.lo[:] = list(lo)
+    p.hi[:] = list(hi)
+    return p
+
+
+# ----------------------------------------------------------------------------------
+def philox4x32_10(ctr, key) -> np.ndarray:
+    c = np.asarray(ctr, dtype=np.uint32).copy()
+    k = np.asarray(key, dtype=np.uint32).copy()
+    out = np.zeros(4, dtype=np.uint32)
+    lib().orc_philox4x32_10(_p(c), _p(k), _p(out))
+    return out
+
+
+def u53(wa: int, wb: int) -> float:
+    return lib().orc_u53(wa, wb)
+
+
+def u32(w: int) -> float:
+    return lib().orc_u32(w)
+
+
+def init_spheres(n, seed, side, d_lo, d_width=0.0, d_random=False, id0=0):
+    """Uniform-in-cube population, per-id Philox (R22/R23/R29).
+
+    Returns dict of numpy arrays x, y, z, d (f64), id, flags (u32)."""
+    s = {k: np.zeros(n, np.float64) for k in ("x", "y", "z", "d")}
+    s["id"] = np.zeros(n, np.uint32)
+    s["flags"] = np.zeros(n, np.uint32)
+    lib().orc_init_spheres(id0, n, seed, side, d_lo, d_width, int(bool(d_random)),
+                           _p(s["x"]), _p(s["y"]), _p(s["z"]), _p(s["d"]),
+                           _p(s["id"]), _p(s["flags"]))
+    return s
+
+
+def morton(coords, bits) -> int:
+    c = np.asarray(coords, dtype=np.uint32)
+    return int(lib().orc_morton(_p(c), len(c), bits))
+
+
+def blocked_key(bx, by, bz, D) -> int:
+    Da = np.asarray(D, dtype=np.int64)
+    return int(lib().orc_blocked_key(bx, by, bz, _p(Da)))
+
+
+def grid_geometry(s, radius=0.0):
+    n = len(s["x"])
+    R = ctypes.c_double()
+    L = ctypes.c_double()
+    o = np.zeros(3, np.float64)
+    D = np.zeros(3, np.int64)
+    lib().orc_grid_geometry(n, _p(_f64(s["x"])), _p(_f64(s["y"])), _p(_f64(s["z"])),
+                            _p(_f64(s["d"])), radius, ctypes.byref(R), ctypes.byref(L),
+                            _p(o), _p(D))
+    return R.value, L.value, o, D
+
+
+def neighbor_pairs_brute(s, R) -> np.ndarray:
+    x, y, z, i = _f64(s["x"]), _f64(s["y"]), _f64(s["z"]), _u32(s["id"])
+    n = len(x)
+    cnt = lib().orc_neighbor_pairs_brute(n, _p(x), _p(y), _p(z), _p(i), R, None, 0)
+    out = np.zeros(max(cnt, 1), np.uint64)
+    lib().orc_neighbor_pairs_brute(n, _p(x), _p(y), _p(z), _p(i), R, _p(out), cnt)
+    return np.sort(out[:cnt])
+
+
+def neighbor_pairs_grid(s, radius=0.0) -> np.ndarray:
+    x, y, z, d, i = (_f64(s["x"]), _f64(s["y"]), _f64(s["z"]), _f64(s["d"]),
+                     _u32(s["id"]))
+    n = len(x)
+    cnt = lib().orc_neighbor_pairs_grid(n, _p(x), _p(y), _p(z), _p(d), _p(i), radius, None, 0)
+    out = np.zeros(max(cnt, 1), np.uint64)
+    lib().orc_neighbor_pairs_grid(n, _p(x), _p(y), _p(z), _p(d), _p(i), radius, _p(out), cnt)
+    return np.sort(out[:cnt])
+
+
+def pair_force(k, gamma, D, ri, rj):
+    """Eq. 4.1/4.2 for one pair at squared distance D: returns (F_N, s, contact)."""
+    c = ctypes.c_int()
+    sc = ctypes.c_double()
+    Fn = lib().orc_pair_force(k, gamma, D, ri, rj, ctypes.byref(c), ctypes.byref(sc))
+    return Fn, sc.value, bool(c.value)
+
+
+def mech_step(s, params: MechParams, sample=None):
+    """One mechanics step (copy semantics).  Returns (out, counters).
+
+    out holds x, y, z, flags and the summed force (m x 3; zero for static agents) for
+    every agent (input order) or for the agents listed in
+    ``sample`` (in that order); d and id are unchanged by a mechanics step."""
+    x, y, z, d = _f64(s["x"]), _f64(s["y"]), _f64(s["z"]), _f64(s["d"])
+    i, f = _u32(s["id"]), _u32(s["flags"])
+    n = len(x)
+    if sample is None:
+        m, idx = n, None
+    else:
+        idx = np.ascontiguousarray(sample, dtype=np.int64)
+        m = len(idx)
+    out = {k: np.zeros(m, np.float64) for k in ("x", "y", "z")}
+    out["flags"] = np.zeros(m, np.uint32)
+    out["force"] = np.zeros((m, 3), np.float64)
+    c = Counters()
+    lib().orc_mech_step(n, _p(x), _p(y), _p(z), _p(d), _p(i), _p(f), ctypes.byref(params), m,
+                        None if idx is None else _p(idx), _p(out["x"]), _p(out["y"]),
+                        _p(out["z"]), _p(out["flags"]), _p(out["force"]), ctypes.byref(c))
+    return out, {k: getattr(c, k) for k in ("cand", "nbr", "cont", "n_static")}
+
+
+def sorted_order(s, radius=0.0):
+    """Input indices in (blocked Morton key, id) order, and the sorted keys."""
+    x, y, z, d, i = (_f64(s["x"]), _f64(s["y"]), _f64(s["z"]), _f64(s["d"]),
+                     _u32(s["id"]))
+    n = len(x)
+    perm = np.zeros(n, np.int64)
+    keys = np.zeros(n, np.uint64)
+    if n:
+        lib().orc_sorted_order(n, _p(x), _p(y), _p(z), _p(d), _p(i), radius, _p(perm), _p(keys))
+    return perm, keys
+
+
+def step_full(s, params: MechParams):
+    """Convenience: one step returning the full new state in the product's output
+    order (sorted by the step's grid), as the GPU library leaves it."""
+    out, cnt = mech_step(s, params)
+    perm, _ = sorted_order(s, params.radius)
+    new = {
+        "x": out["x"][perm], "y": out["y"][perm], "z": out["z"][perm],
+        "d": np.asarray(s["d"], np.float64)[perm], "id": np.asarray(s["id"], np.uint32)[perm],
+        "flags": out["flags"][perm],
+    }
+    return new, cnt

@@ -1,0 +1,520 @@
+/*
+ * oracle.c -- plain, slow, obviously-correct CPU oracle for the BioDynaMo/TeraAgent
+ * mechanics hot path (arXiv 2503.10796, L. Breitwieser, ETH Diss. 30705).
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference leg may load or execute anything under oracle/.
+ * The product path (paper_2503_10796_b200/) never links, imports or calls it, and
+ * this file shares no code, header, table or constant generator with the CUDA path.
+ *
+ * Citations: "P:a-b" = /root/reference/PAPER.md lines a-b (section / equation label
+ * given alongside).  Readings of passages where the paper is silent are numbered
+ * R1..Rn and listed in DESIGN.md section 3 ("Readings").
+ *
+ * Arithmetic: IEEE binary64, round-to-nearest-even, compiled with
+ * -O2 -ffp-contract=off so that the compiler never fuses a*b+c.  fma() is called at
+ * exactly the two canonical sites (squared distance, force accumulation; R9).
+ * sqrt() and '/' are IEEE correctly-rounded.
+ *
+ * Everything here is written for readability, not speed: sorting by qsort, box
+ * lookup by binary search, one agent at a time.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+/* ------------------------------------------------------------------------------ */
+/* Counter-based PRNG: Philox4x32-10 (Salmon et al., SC'11 "Random123").            */
+/* The paper proposes a per-agent counter-based PRNG as its remedy for              */
+/* non-determinism: "Counter-based PRNGs [random123] could be a good choice"        */
+/* (sec. "Reproducibility").  Reading R22: key = seed (lo, hi),        */
+/* counter = (id_lo, id_hi, word2, stream).                                         */
+/* ------------------------------------------------------------------------------ */
+void orc_philox4x32_10(const uint32_t ctr_in[4], const uint32_t key_in[2], uint32_t out[4])
+{
+    uint32_t c0 = ctr_in[0], c1 = ctr_in[1], c2 = ctr_in[2], c3 = ctr_in[3];
+    uint32_t k0 = key_in[0], k1 = key_in[1];
+    for (int round = 0; round < 10; ++round) {
+        if (round > 0) {              /* key schedule: bump by the Weyl constants */
+            k0 += 0x9E3779B9u;
+            k1 += 0xBB67AE85u;
+        }
+        uint64_t p0 = (uint64_t)0xD2511F53u * (uint64_t)c0;
+        uint64_t p1 = (uint64_t)0xCD9E8D57u * (uint64_t)c2;
+        uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0;
+        uint32_t hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
+        uint32_t n0 = hi1 ^ c1 ^ k0;
+        uint32_t n1 = lo1;
+        uint32_t n2 = hi0 ^ c3 ^ k1;
+        uint32_t n3 = lo0;
+        c0 = n0; c1 = n1; c2 = n2; c3 = n3;
+    }
+    out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
+}
+
+/* Philox words -> reals (reading R29).  Both conversions are exact in binary64. */
+double orc_u32(uint32_t w) { return (double)w * 0x1p-32; }
+
+double orc_u53(uint32_t wa, uint32_t wb)
+{
+    double hi = (double)(wa >> 5);   /* 27 bits */
+    double lo = (double)(wb >> 6);   /* 26 bits */
+    return (hi * 67108864.0 + lo) * 0x1p-53;
+}
+
+static void philox_draw(uint64_t seed, uint64_t id, uint32_t word2, uint32_t stream, uint32_t w[4])
+{
+    uint32_t ctr[4] = {(uint32_t)id, (uint32_t)(id >> 32), word2, stream};
+    uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+    orc_philox4x32_10(ctr, key, w);
+}
+
+/* ------------------------------------------------------------------------------ */
+/* Agent flag bits (reading R8/R31).                                                */
+/* ------------------------------------------------------------------------------ */
+enum {
+    ORC_MOVED = 1u << 0,   /* displacement != 0 in the last step                       */
+    ORC_GREW = 1u << 1,    /* diameter increased in the last step                      */
+    ORC_ADDED = 1u << 2,   /* agent created in the last step (initial agents included) */
+    ORC_STATIC = 1u << 3,  /* force skipped in the last step                           */
+    ORC_NNZ_SHIFT = 4,     /* bits 4-5: #nonzero neighbour forces, saturating at 2     */
+};
+
+/* ------------------------------------------------------------------------------ */
+/* Population generation (ModelInitializer): uniform in a cube.        */
+/* x,y from ctr (id, 0xFFFFFFFF, 2); z from (id, 0xFFFFFFFE, 2); a random diameter  */
+/* d = d_lo + d_width*u from (id, 0xFFFFFFFD, 2) (reading R23).                      */
+/* All initial agents carry ORC_ADDED: they "were added" before step 0, so          */
+/* condition (iii) of P:4941-4946 prevents anyone from being static at step 0.      */
+/* ------------------------------------------------------------------------------ */
+void orc_init_spheres(int64_t id0, int64_t n, uint64_t seed, double side,
+                      double d_lo, double d_width, int d_random,
+                      double *x, double *y, double *z, double *d,
+                      uint32_t *id, uint32_t *flags)
+{
+    for (int64_t k = 0; k < n; ++k) {
+        uint64_t a = (uint64_t)(id0 + k);
+        uint32_t w[4];
+        philox_draw(seed, a, 0xFFFFFFFFu, 2u, w);
+        x[k] = orc_u53(w[0], w[1]) * side;
+        y[k] = orc_u53(w[2], w[3]) * side;
+        philox_draw(seed, a, 0xFFFFFFFEu, 2u, w);
+        z[k] = orc_u53(w[0], w[1]) * side;
+        if (d_random) {
+            philox_draw(seed, a, 0xFFFFFFFDu, 2u, w);
+            d[k] = d_lo + d_width * orc_u53(w[0], w[1]);
+        } else {
+            d[k] = d_lo;
+        }
+        id[k] = (uint32_t)a;
+        flags[k] = ORC_ADDED;
+    }
+}
+
+/* ------------------------------------------------------------------------------ */
+/* Morton order (fig:load-balancing-design): interleave the bits of    */
+/* the box coordinates, coordinate 0 (x) in the lowest bit.                          */
+/* ------------------------------------------------------------------------------ */
+uint64_t orc_morton(const uint32_t *coord, int ndim, int bits)
+{
+    uint64_t code = 0;
+    for (int b = 0; b < bits; ++b)
+        for (int a = 0; a < ndim; ++a)
+            code |= (uint64_t)((coord[a] >> b) & 1u) << (b * ndim + a);
+    return code;
+}
+
+/* Blocked Morton key (reading R32): boxes are grouped in 4x4x4 tiles; tiles are    */
+/* numbered row-major (x fastest); inside a tile the 64 boxes follow 3-D Morton.    */
+uint64_t orc_blocked_key(int64_t bx, int64_t by, int64_t bz, const int64_t D[3])
+{
+    int64_t Tx = (D[0] + 3) / 4, Ty = (D[1] + 3) / 4;
+    int64_t tile = ((bz / 4) * Ty + (by / 4)) * Tx + (bx / 4);
+    uint32_t c[3] = {(uint32_t)(bx % 4), (uint32_t)(by % 4), (uint32_t)(bz % 4)};
+    return (uint64_t)tile * 64u + orc_morton(c, 3, 2);
+}
+
+/* ------------------------------------------------------------------------------ */
+/* Uniform grid geometry ("Environment Search"; P:4487-4530 sec:grid).  */
+/* R = largest diameter ("box size ... determined automatically based on the        */
+/* largest agent") unless the caller fixes it; L = R(1+2^-20) (R5);    */
+/* origin = per-axis minimum (open boundary: "space grows to encapsulate all        */
+/* agents"; R12).                                                           */
+/* ------------------------------------------------------------------------------ */
+typedef struct {
+    double R, L, o[3], hi[3];
+    int64_t D[3];
+} orc_grid;
+
+void orc_grid_geometry(int64_t n, const double *x, const double *y, const double *z,
+                       const double *d, double radius, double *out_R, double *out_L,
+                       double out_o[3], int64_t out_D[3])
+{
+    double R = 0.0, lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
+    for (int64_t i = 0; i < n; ++i) {
+        double p[3] = {x[i], y[i], z[i]};
+        for (int a = 0; a < 3; ++a) {
+            if (i == 0 || p[a] < lo[a]) lo[a] = p[a];
+            if (i == 0 || p[a] > hi[a]) hi[a] = p[a];
+        }
+        if (d[i] > R) R = d[i];
+    }
+    if (radius > 0.0) R = radius;
+    double L = R * (1.0 + 0x1p-20);
+    for (int a = 0; a < 3; ++a) {
+        out_o[a] = lo[a];
+        out_D[a] = n > 0 ? (int64_t)floor((hi[a] - lo[a]) / L) + 1 : 0;
+    }
+    *out_R = R;
+    *out_L = L;
+}
+
+static void box_of(const orc_grid *g, double px, double py, double pz, int64_t b[3])
+{
+    b[0] = (int64_t)floor((px - g->o[0]) / g->L);
+    b[1] = (int64_t)floor((py - g->o[1]) / g->L);
+    b[2] = (int64_t)floor((pz - g->o[2]) / g->L);
+}
+
+/* ---- the grid itself: agents sorted by (row-major box index, id) ---------------- */
+typedef struct {
+    int64_t box;   /* (bz*Dy + by)*Dx + bx */
+    uint32_t id;
+    int64_t idx;   /* agent index in the input arrays */
+} orc_entry;
+
+static int cmp_entry(const void *pa, const void *pb)
+{
+    const orc_entry *a = pa, *b = pb;
+    if (a->box != b->box) return a->box < b->box ? -1 : 1;
+    if (a->id != b->id) return a->id < b->id ? -1 : 1;
+    return 0;
+}
+
+typedef struct {
+    orc_grid g;
+    int64_t n;
+    orc_entry *e;  /* n entries sorted by (box, id) */
+} orc_index;
+
+static int64_t lin_box(const orc_grid *g, int64_t bx, int64_t by, int64_t bz)
+{
+    return (bz * g->D[1] + by) * g->D[0] + bx;
+}
+
+static void index_build(orc_index *ix, int64_t n, const double *x, const double *y,
+                        const double *z, const double *d, const uint32_t *id, double radius)
+{
+    ix->n = n;
+    orc_grid_geometry(n, x, y, z, d, radius, &ix->g.R, &ix->g.L, ix->g.o, ix->g.D);
+    ix->e = (orc_entry *)malloc(sizeof(orc_entry) * (size_t)(n > 0 ? n : 1));
+    for (int64_t i = 0; i < n; ++i) {
+        int64_t b[3];
+        box_of(&ix->g, x[i], y[i], z[i], b);
+        ix->e[i].box = lin_box(&ix->g, b[0], b[1], b[2]);
+        ix->e[i].id = id[i];
+        ix->e[i].idx = i;
+    }
+    qsort(ix->e, (size_t)n, sizeof(orc_entry), cmp_entry);
+}
+
+static void index_free(orc_index *ix) { free(ix->e); }
+
+/* [first, last) range of entries in box `box` (binary search) */
+static void box_range(const orc_index *ix, int64_t box, int64_t *first, int64_t *last)
+{
+    int64_t lo = 0, hi = ix->n;
+    while (lo < hi) {
+        int64_t mid = (lo + hi) / 2;
+        if (ix->e[mid].box < box) lo = mid + 1; else hi = mid;
+    }
+    *first = lo;
+    hi = ix->n;
+    while (lo < hi) {
+        int64_t mid = (lo + hi) / 2;
+        if (ix->e[mid].box <= box) lo = mid + 1; else hi = mid;
+    }
+    *last = lo;
+}
+
+/* Squared centre distance in the canonical operation order (R9):
+ * D = fma(dz, dz, fma(dy, dy, dx*dx)) with d* = (own - other). */
+static double sqdist(double dx, double dy, double dz)
+{
+    return fma(dz, dz, fma(dy, dy, dx * dx));
+}
+
+/* ------------------------------------------------------------------------------ */
+/* Neighbour pairs by the plain definition (all pairs; reading R4):                 */
+/* N_i = { j != i : D_ij <= R*R }.  Writes (id_i << 32 | id_j) for every ordered     */
+/* pair, unsorted; returns the count (pairs beyond `cap` are counted, not written). */
+/* ------------------------------------------------------------------------------ */
+int64_t orc_neighbor_pairs_brute(int64_t n, const double *x, const double *y, const double *z,
+                                 const uint32_t *id, double R, uint64_t *pairs, int64_t cap)
+{
+    double R2 = R * R;
+    int64_t cnt = 0;
+    for (int64_t i = 0; i < n; ++i)
+        for (int64_t j = 0; j < n; ++j) {
+            if (j == i) continue;
+            double D = sqdist(x[i] - x[j], y[i] - y[j], z[i] - z[j]);
+            if (D <= R2) {
+                if (cnt < cap) pairs[cnt] = ((uint64_t)id[i] << 32) | id[j];
+                ++cnt;
+            }
+        }
+    return cnt;
+}
+
+/* Same relation enumerated through the uniform grid's 27 boxes. */
+int64_t orc_neighbor_pairs_grid(int64_t n, const double *x, const double *y, const double *z,
+                                const double *d, const uint32_t *id, double radius,
+                                uint64_t *pairs, int64_t cap)
+{
+    orc_index ix;
+    index_build(&ix, n, x, y, z, d, id, radius);
+    double R2 = ix.g.R * ix.g.R;
+    int64_t cnt = 0;
+    for (int64_t i = 0; i < n; ++i) {
+        int64_t b[3];
+        box_of(&ix.g, x[i], y[i], z[i], b);
+        for (int dz = -1; dz <= 1; ++dz)
+            for (int dy = -1; dy <= 1; ++dy)
+                for (int dx = -1; dx <= 1; ++dx) {
+                    int64_t cx = b[0] + dx, cy = b[1] + dy, cz = b[2] + dz;
+                    if (cx < 0 || cy < 0 || cz < 0 || cx >= ix.g.D[0] || cy >= ix.g.D[1] ||
+                        cz >= ix.g.D[2])
+                        continue;
+                    int64_t f, l;
+                    box_range(&ix, lin_box(&ix.g, cx, cy, cz), &f, &l);
+                    for (int64_t s = f; s < l; ++s) {
+                        int64_t j = ix.e[s].idx;
+                        if (j == i) continue;
+                        double D = sqdist(x[i] - x[j], y[i] - y[j], z[i] - z[j]);
+                        if (D <= R2) {
+                            if (cnt < cap) pairs[cnt] = ((uint64_t)id[i] << 32) | id[j];
+                            ++cnt;
+                        }
+                    }
+                }
+    }
+    index_free(&ix);
+    return cnt;
+}
+
+/* ------------------------------------------------------------------------------ */
+/* Pair force, Eq. 4.1 / 4.2 (eq:force, eq:force-radius):               */
+/*   F_N = k*delta - gamma*sqrt(rbar*delta),  rbar = r1*r2/(r1+r2)                   */
+/* delta = r_i + r_j - |x_i - x_j| (R2), force only for delta > 0 (R3) and          */
+/* dist > 0 (R10).  Direction along the centre line, positive = repulsive (R1).     */
+/* Returns F_N, writes s = F_N / dist.                                               */
+/* ------------------------------------------------------------------------------ */
+double orc_pair_force(double k, double gamma, double D, double ri, double rj, int *contact,
+                      double *s_out)
+{
+    double dist = sqrt(D);
+    double delta = (ri + rj) - dist;
+    *contact = 0;
+    *s_out = 0.0;
+    if (!(delta > 0.0 && dist > 0.0)) return 0.0;
+    *contact = 1;
+    double rbar = (ri * rj) / (ri + rj);
+    double Fn = k * delta - gamma * sqrt(rbar * delta);
+    *s_out = Fn / dist;
+    return Fn;
+}
+
+/* ------------------------------------------------------------------------------ */
+/* One mechanics step (MechanicalForcesOp + BoundSpaceOp,  */
+/* with the static-agent skip of sec:static-agents).  Copy (Jacobi)     */
+/* semantics: every read uses the start-of-step state (R11).            */
+/* ------------------------------------------------------------------------------ */
+typedef struct {
+    double k, gamma, dt, max_disp, force_threshold, radius;
+    int32_t detect_static, boundary;  /* boundary: 0 open, 1 closed */
+    double lo[3], hi[3];
+} orc_mech_params;
+
+typedef struct {
+    int64_t cand, nbr, cont, n_static;
+} orc_counters;
+
+static int nnz_of(uint32_t f) { return (int)((f >> ORC_NNZ_SHIFT) & 3u); }
+
+/* Computes the step for agents idx_list[0..m) (all agents when idx_list == NULL;
+ * then m must equal n).  Results are written at position k of the out arrays for
+ * the k-th listed agent. */
+void orc_mech_step(int64_t n, const double *x, const double *y, const double *z,
+                   const double *d, const uint32_t *id, const uint32_t *flags,
+                   const orc_mech_params *p, int64_t m, const int64_t *idx_list,
+                   double *x_out, double *y_out, double *z_out, uint32_t *flags_out,
+                   double *force_out /* nullable: 3*m, the summed force F_i */,
+                   orc_counters *cnt)
+{
+    memset(cnt, 0, sizeof(*cnt));
+    if (n == 0) return;
+    orc_index ix;
+    index_build(&ix, n, x, y, z, d, id, p->radius);
+    const orc_grid *g = &ix.g;
+    double R2 = g->R * g->R;
+    const uint32_t CHANGED = ORC_MOVED | ORC_GREW | ORC_ADDED;
+
+    for (int64_t k = 0; k < m; ++k) {
+        int64_t i = idx_list ? idx_list[k] : k;
+        int64_t b[3];
+        box_of(g, x[i], y[i], z[i], b);
+        double ri = d[i] * 0.5;
+
+        /* (a5) static classification: (i) the agent and none of its
+         * neighbours moved, (ii) no force-increasing change (growth), (iii) no agent
+         * added within the radius, (iv) at most one non-zero neighbour force.  All
+         * facts refer to the last iteration (flags of step t-1); the neighbours are
+         * those within R now (R8). */
+        int is_static = 0;
+        if (p->detect_static && !(flags[i] & CHANGED) && nnz_of(flags[i]) <= 1) {
+            is_static = 1;
+            for (int dz = -1; dz <= 1 && is_static; ++dz)
+                for (int dy = -1; dy <= 1 && is_static; ++dy)
+                    for (int dx = -1; dx <= 1 && is_static; ++dx) {
+                        int64_t cx = b[0] + dx, cy = b[1] + dy, cz = b[2] + dz;
+                        if (cx < 0 || cy < 0 || cz < 0 || cx >= g->D[0] || cy >= g->D[1] ||
+                            cz >= g->D[2])
+                            continue;
+                        int64_t f, l;
+                        box_range(&ix, lin_box(g, cx, cy, cz), &f, &l);
+                        for (int64_t s = f; s < l; ++s) {
+                            int64_t j = ix.e[s].idx;
+                            if (j == i) continue;
+                            double D = sqdist(x[i] - x[j], y[i] - y[j], z[i] - z[j]);
+                            if (D <= R2 && (flags[j] & CHANGED)) {
+                                is_static = 0;
+                                break;
+                            }
+                        }
+                    }
+        }
+
+        double Dx = 0.0, Dy = 0.0, Dz = 0.0;
+        double Fx = 0.0, Fy = 0.0, Fz = 0.0;
+        int nnz;
+        if (is_static) {
+            nnz = nnz_of(flags[i]);  /* carried */
+            cnt->n_static++;
+        } else {
+            /* (a6)+(a7): 27 boxes in (dz, dy, dx) lexicographic order, inside a box
+             * ascending id (R9); sum f_ij = s*(x_i - x_j) with fma. */
+            nnz = 0;
+            for (int dz = -1; dz <= 1; ++dz)
+                for (int dy = -1; dy <= 1; ++dy)
+                    for (int dx = -1; dx <= 1; ++dx) {
+                        int64_t cx = b[0] + dx, cy = b[1] + dy, cz = b[2] + dz;
+                        if (cx < 0 || cy < 0 || cz < 0 || cx >= g->D[0] || cy >= g->D[1] ||
+                            cz >= g->D[2])
+                            continue;
+                        int64_t f, l;
+                        box_range(&ix, lin_box(g, cx, cy, cz), &f, &l);
+                        for (int64_t s = f; s < l; ++s) {
+                            int64_t j = ix.e[s].idx;
+                            if (j == i) continue;
+                            cnt->cand++;
+                            double ex = x[i] - x[j], ey = y[i] - y[j], ez = z[i] - z[j];
+                            double D = sqdist(ex, ey, ez);
+                            if (!(D <= R2)) continue;
+                            cnt->nbr++;
+                            int contact;
+                            double sc;
+                            double Fn = orc_pair_force(p->k, p->gamma, D, ri, d[j] * 0.5,
+                                                       &contact, &sc);
+                            if (!contact) continue;
+                            cnt->cont++;
+                            Fx = fma(sc, ex, Fx);
+                            Fy = fma(sc, ey, Fy);
+                            Fz = fma(sc, ez, Fz);
+                            if (Fn != 0.0 && nnz < 2) ++nnz;
+                        }
+                    }
+            /* (a8) displacement = dt * F (R6); no move unless |F| > threshold (R7,
+             * P:4964-4965); cap |displacement| at max_disp. */
+            double F2 = Fx * Fx + Fy * Fy + Fz * Fz;
+            double tau = p->force_threshold;
+            if (F2 > tau * tau) {
+                Dx = p->dt * Fx;
+                Dy = p->dt * Fy;
+                Dz = p->dt * Fz;
+                double n2 = Dx * Dx + Dy * Dy + Dz * Dz;
+                double mx = p->max_disp;
+                if (n2 > mx * mx) {
+                    double scale = mx / sqrt(n2);
+                    Dx = Dx * scale;
+                    Dy = Dy * scale;
+                    Dz = Dz * scale;
+                }
+            }
+        }
+        double nx = x[i] + Dx, ny = y[i] + Dy, nz = z[i] + Dz;
+        /* (a9) boundary condition (sec:space-boundary): open = no-op (the
+         * grid origin follows the agents, R12); closed = clamp into [lo, hi]. */
+        if (p->boundary == 1) {
+            double *q[3] = {&nx, &ny, &nz};
+            for (int a = 0; a < 3; ++a) {
+                if (*q[a] < p->lo[a]) *q[a] = p->lo[a];
+                if (*q[a] > p->hi[a]) *q[a] = p->hi[a];
+            }
+        }
+        int moved = (Dx != 0.0 || Dy != 0.0 || Dz != 0.0);
+        if (force_out) {
+            force_out[3 * k + 0] = Fx;
+            force_out[3 * k + 1] = Fy;
+            force_out[3 * k + 2] = Fz;
+        }
+        x_out[k] = nx;
+        y_out[k] = ny;
+        z_out[k] = nz;
+        flags_out[k] = (moved ? ORC_MOVED : 0u) | (is_static ? ORC_STATIC : 0u) |
+                       ((uint32_t)nnz << ORC_NNZ_SHIFT);
+    }
+    index_free(&ix);
+}
+
+/* ------------------------------------------------------------------------------ */
+/* The agent order after a step (A12): agents sorted by the blocked     */
+/* Morton key of their box in the step's grid, ascending id inside a box.            */
+/* Writes the permutation (input indices in sorted order) and the keys.              */
+/* ------------------------------------------------------------------------------ */
+typedef struct {
+    uint64_t key;
+    uint32_t id;
+    int64_t idx;
+} orc_kentry;
+
+static int cmp_kentry(const void *pa, const void *pb)
+{
+    const orc_kentry *a = pa, *b = pb;
+    if (a->key != b->key) return a->key < b->key ? -1 : 1;
+    if (a->id != b->id) return a->id < b->id ? -1 : 1;
+    return 0;
+}
+
+void orc_sorted_order(int64_t n, const double *x, const double *y, const double *z,
+                      const double *d, const uint32_t *id, double radius, int64_t *perm,
+                      uint64_t *keys_sorted)
+{
+    if (n == 0) return;
+    orc_grid g;
+    orc_grid_geometry(n, x, y, z, d, radius, &g.R, &g.L, g.o, g.D);
+    orc_kentry *e = (orc_kentry *)malloc(sizeof(orc_kentry) * (size_t)n);
+    for (int64_t i = 0; i < n; ++i) {
+        int64_t b[3];
+        box_of(&g, x[i], y[i], z[i], b);
+        e[i].key = orc_blocked_key(b[0], b[1], b[2], g.D);
+        e[i].id = id[i];
+        e[i].idx = i;
+    }
+    qsort(e, (size_t)n, sizeof(orc_kentry), cmp_kentry);
+    for (int64_t i = 0; i < n; ++i) {
+        perm[i] = e[i].idx;
+        if (keys_sorted) keys_sorted[i] = e[i].key;
+    }
+    free(e);
+}
