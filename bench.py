@@ -1,0 +1,340 @@
+#!/usr/bin/env python
+"""bench.py -- agent-updates/s of the B200 mechanics step (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config cfg2|cfg1|cfg5] [--no-e2e] [--no-cpu-baseline]
+
+One "step" = one pass of the whole hot path over the agents: grid build (a1-a4:
+reduce, keys, histogram, scan, scatter, in-box id order, gather) + mechanics (a5-a9:
+static test, 27-box scan, Eq. 4.1 force, canonical sum, capped displacement) -- all in
+libbdm.so kernels behind the C ABI.  The workload at N=1 is configs[1] (cfg2: 10M
+agents, d ~ U[8,12] um, 50 % volume fraction, static skip on).  Inputs (440 MB of
+SoA) exceed the 126 MB L2, so no flush is needed between steps; the state evolves
+from step to step exactly as the simulation does.
+
+Rank 0 prints ONE JSON line.  --impl reference times the CPU oracle (oracle/, the
+from-scratch reference of this tier) on the host cores instead.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import workloads as W  # noqa: E402
+
+METRIC = "agent-updates/sec per mechanics step (fp64) and % of HBM/fp64 roofline"
+UNIT = "agent-updates/s"
+
+# Algorithmic work per agent-update: bytes the method must move
+# and fp64 pipe instructions the method must issue.
+B_ALG_PER_AGENT = 72.0           # x,y,z,d read (32) + x,y,z write (24) + key/perm (16)
+B_ALG_STATIC_EXTRA = 8.0         # flags read + write with detect_static
+FP64_PER_CAND, FP64_PER_NBR, FP64_PER_CONT, FP64_PER_AGENT = 7.0, 3.0, 60.0, 40.0
+
+
+def _peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            return json.load(f), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+class ClockSampler:
+    """Samples SM clock and throttle reasons (NVML) during the timed region."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+        0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+        0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+        0x100: "display_clock_setting",
+    }
+
+    def __init__(self, device_index: int, period_s: float = 0.02):
+        self.dev = device_index
+        self.period = period_s
+        self.samples = []
+        self.reasons = set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # pragma: no cover - NVML missing
+            self.err = str(e)
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                mask = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if mask & bit and bit != 0x1:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                    "samples": len(self.samples)}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+# ------------------------------------------------------------------ CPU oracle legs
+def oracle_step_rate(cfg_n: int, repeats: int = 1):
+    """Times the oracle (single-threaded C, as it stands) on one full mechanics step of
+    the cfg2 workload at cfg_n agents (same density and diameter mix)."""
+    import oracle
+    cfg = W.cfg2_scaled(cfg_n)
+    s = oracle.init_spheres(cfg.n, cfg.seed, cfg.side, cfg.d_lo, cfg.d_width, cfg.d_random)
+    p = oracle.mech_params(detect_static=True)
+    times = []
+    for _ in range(repeats):
+        t0 = time.perf_counter()
+        out, _ = oracle.mech_step(s, p)
+        times.append(time.perf_counter() - t0)
+        s = dict(s, x=out["x"], y=out["y"], z=out["z"], flags=out["flags"])
+    return cfg.n / statistics.median(times), times
+
+
+def run_reference(args, ws, rank):
+    """--impl reference: the CPU oracle on the host cores (rank 0 only)."""
+    if rank != 0:
+        return
+    import oracle
+    oracle.build()
+    n_sample = 200_000
+    cfg = W.cfg2_scaled(n_sample)
+    s = oracle.init_spheres(cfg.n, cfg.seed, cfg.side, cfg.d_lo, cfg.d_width, cfg.d_random)
+    p = oracle.mech_params(detect_static=True)
+    for _ in range(args.warmup):
+        out, _ = oracle.mech_step(s, p)
+        s = dict(s, x=out["x"], y=out["y"], z=out["z"], flags=out["flags"])
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        out, _ = oracle.mech_step(s, p)
+        s = dict(s, x=out["x"], y=out["y"], z=out["z"], flags=out["flags"])
+    dt = time.perf_counter() - t0
+    value = cfg.n * args.steps / dt
+    sample = (f"each step = one full oracle mechanics step of the cfg2 workload at {n_sample} "
+              f"agents (same density, diameter mix, static skip on)")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": "cfg2 (configs[1]) sample", "agents_per_step": n_sample},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ GPU arm
+def run_ours(args, ws, rank, local):
+    import torch
+    from paper_2503_10796_b200 import Agents, Engine, Params
+
+    if ws > 1:
+        raise SystemExit("multi-GPU slab decomposition is not wired into bench.py yet")
+    torch.cuda.set_device(local)
+    cfg = W.PRESETS[args.config]
+    eng = Engine(local, cfg.n)
+    a = Agents.empty(cfg.n)
+    stream = torch.cuda.Stream()
+    with torch.cuda.stream(stream):
+        eng.init_spheres(a, cfg.n, seed=cfg.seed, side=cfg.side, d_lo=cfg.d_lo,
+                         d_width=cfg.d_width, d_random=cfg.d_random, stream=stream)
+    params = Params(k=cfg.k, gamma=cfg.gamma, dt=cfg.dt, max_displacement=cfg.max_disp,
+                    force_threshold=cfg.force_threshold, detect_static=cfg.detect_static)
+    # first step sizes the grid; reserve slot headroom (+8 tiles/axis) for the growth of
+    # the open-boundary space over the run so no timed step overflows
+    eng.step(a, params, stream=stream)
+    gi = eng.grid_info()
+    T = [(d + 3) // 4 + 8 for d in gi["dims"]]
+    eng.reserve(0, T[0] * T[1] * T[2] * 64)
+    for _ in range(max(args.warmup - 1, 0)):
+        eng.step(a, params, stream=stream)
+    # work counters of a representative step (the last warm-up step)
+    pst = Params(**{**params.__dict__, "collect_stats": True})
+    eng.step(a, pst, stream=stream)
+    st_before = eng.stats()
+
+    K = args.steps
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+           torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = eng.stats()["launches"]
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        start.record(stream)
+        for k in range(K):
+            e0, e1, e2 = ev[k]
+            e0.record(stream)
+            eng.grid_build(a, params.radius, stream=stream)
+            e1.record(stream)
+            eng.mech_step(a, params, stream=stream)
+            e2.record(stream)
+        stop.record(stream)
+        torch.cuda.synchronize()
+    launches = eng.stats()["launches"] - launches0
+    rc = eng.try_sync(stream)
+    if rc != 0:
+        raise SystemExit(f"a timed step failed (bdm status {rc}); rerun")
+    total_ms = start.elapsed_time(stop)
+    grid_ms = [ev[k][0].elapsed_time(ev[k][1]) for k in range(K)]
+    mech_ms = [ev[k][1].elapsed_time(ev[k][2]) for k in range(K)]
+    eng.step(a, pst, stream=stream)
+    st_after = eng.stats()
+    clocks = clk.summary()
+
+    ms_step = total_ms / K
+    value = cfg.n / (ms_step * 1e-3)
+
+    # roofline of the dominant kernel (k_mech): fp64-pipe bound
+    avg = lambda k: 0.5 * (st_before[k] + st_after[k])  # noqa: E731
+    cand, nbr, cont, nstat = avg("cand"), avg("nbr"), avg("cont"), avg("n_static")
+    fp64_per_launch = (FP64_PER_CAND * cand + FP64_PER_NBR * nbr + FP64_PER_CONT * cont +
+                       FP64_PER_AGENT * cfg.n)
+    mech_avg_s = statistics.mean(mech_ms) * 1e-3
+    peaks, peak_src = _peaks()
+    sm_count = torch.cuda.get_device_properties(local).multi_processor_count
+    max_mhz = clocks["sm_max_mhz"] or peaks.get("sm_max_mhz", 1965.0)
+    fp64_peak = sm_count * 64 * max_mhz * 1e6  # fp64 lane-instructions/s at max clock
+    achieved = fp64_per_launch / mech_avg_s
+    b_alg = (B_ALG_PER_AGENT + (B_ALG_STATIC_EXTRA if cfg.detect_static else 0.0)) * cfg.n
+    hbm_peak = peaks["hbm_gbs"] * 1e9
+    t_roof = max(b_alg / hbm_peak, fp64_per_launch / fp64_peak)
+    dfma_meas, _ = eng.peak_dfma()
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": K,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{cfg.name} (configs[1])" if cfg.name == "cfg2" else cfg.name,
+                   "agents": cfg.n, "side_um": cfg.side, "diameter": "U[8,12] um"
+                   if cfg.d_random else f"{cfg.d_lo} um", "detect_static": cfg.detect_static,
+                   "dt": cfg.dt, "max_displacement_um": cfg.max_disp,
+                   "l2": "inputs (44 B/agent SoA) larger than L2; no flush",
+                   "parallelism": f"{ws} GPU"},
+        "roofline": {"bound": "alu", "kernel": "k_mech (a5-a9)",
+                     "achieved": achieved / 1e12, "peak": fp64_peak / 1e12,
+                     "unit": "T fp64-inst/s", "frac": achieved / fp64_peak, "traffic": None,
+                     "peak_source": f"{sm_count} SMs x 64 fp64 lanes x {max_mhz:.0f} MHz "
+                                    f"(guide unit counts, max clock); measured DFMA "
+                                    f"{dfma_meas / 1e12:.2f} T/s",
+                     "work_per_launch": {"cand": cand, "nbr": nbr, "cont": cont,
+                                         "static": nstat, "fp64_inst": fp64_per_launch},
+                     "mech_ms": statistics.mean(mech_ms), "grid_ms": statistics.mean(grid_ms)},
+        "step_roofline": {"t_roof_ms": t_roof * 1e3, "frac": t_roof / (ms_step * 1e-3),
+                          "hbm_term_ms": b_alg / hbm_peak * 1e3,
+                          "fp64_term_ms": fp64_per_launch / fp64_peak * 1e3,
+                          "hbm_peak_gbs": peaks["hbm_gbs"], "hbm_peak_source": peak_src},
+        "clocks": clocks,
+        "gpu_launches": launches,
+    }
+
+    if not args.no_e2e:
+        line["e2e"] = measure_e2e(eng, cfg, params, stream)
+    if not args.no_cpu_baseline and rank == 0 and ws == 1:
+        line["cpu_baseline"] = cpu_baseline()
+    print(json.dumps(line), flush=True)
+
+
+def measure_e2e(eng, cfg, params, stream, steps: int = 3):
+    """Same metric through bdm_step_host: pinned host SoA -> device, step, device -> host,
+    every step inside the timed region."""
+    import torch
+    from paper_2503_10796_b200 import Agents
+    n = cfg.n
+    hin = Agents.empty(n, pin=True)
+    hout = Agents.empty(n, pin=True)
+    dev = Agents.empty(n)
+    eng.init_spheres(dev, n, seed=cfg.seed, side=cfg.side, d_lo=cfg.d_lo, d_width=cfg.d_width,
+                     d_random=cfg.d_random, stream=stream)
+    torch.cuda.synchronize()
+    for k in ("x", "y", "z", "diameter", "id", "flags"):
+        getattr(hin, k).copy_(getattr(dev, k))
+    hin.n = n
+    eng.step_host(hin, hout, dev, params, stream=stream)  # warm-up
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        eng.step_host(hout, hout, dev, params, stream=stream)
+    dt = (time.perf_counter() - t0) / steps
+    b = n * (4 * 8 + 2 * 4)
+    return {"value": n / dt, "unit": UNIT, "h2d_bytes_per_step": b, "d2h_bytes_per_step": b,
+            "ms_per_step": dt * 1e3, "api": "bdm_step_host (C ABI, pinned host buffers)"}
+
+
+def cpu_baseline():
+    import oracle
+    oracle.build()
+    n = 1_000_000
+    value, times = oracle_step_rate(n, repeats=2)
+    return {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"one full oracle step (single-threaded C) of the cfg2 workload at {n} "
+                      f"agents, same density/diameter mix, static skip on; median of "
+                      f"{len(times)} steps ({', '.join(f'{t:.2f}' for t in times)} s)"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="cfg2", choices=sorted(W.PRESETS))
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    ws, rank, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, ws, rank)
+        return
+    run_ours(args, ws, rank, local)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,209 @@
+/*
+ * bdm.h -- C ABI of the B200-native BioDynaMo/TeraAgent mechanics hot path
+ * (arXiv 2503.10796).  Implemented by paper_2503_10796_b200/libbdm.so (sm_100a).
+ *
+ * Citations "P:a-b" are lines of PAPER.md (the thesis' LaTeX source); the section,
+ * equation or algorithm label is given alongside.  "Rn" refers to the numbered
+ * readings in DESIGN.md section 3 (where the paper is silent or ambiguous).
+ *
+ * Conventions for every entry point
+ *   - All agent-array pointers are DEVICE pointers (cudaMalloc / torch CUDA tensors)
+ *     unless the entry point's name ends in _host.  Arrays are structure-of-arrays,
+ *     indexed [0, n), 8-byte aligned; they are owned by the caller.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = the legacy default stream).
+ *     Every call only enqueues work on `stream` unless documented as synchronizing.
+ *   - The library owns its workspace (allocated in bdm_create / grown on demand in
+ *     bdm_grid_build and bdm_reserve); nothing is allocated inside bdm_mech_step.
+ *   - Every call returns a bdm_status; no C++ exception crosses the ABI.
+ *     bdm_last_error() returns a thread-local message for the last failure.
+ *   - Device-side conditions (grid-slot capacity exceeded, non-finite positions)
+ *     are latched in device memory; the kernels of the affected step become no-ops
+ *     (the caller's arrays are left exactly as they were) and bdm_sync() reports
+ *     the condition.  The caller may then bdm_reserve() and re-issue the step.
+ *   - n == 0 is valid and every compute call is a no-op for it.
+ */
+#ifndef BDM_H
+#define BDM_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    BDM_OK = 0,
+    BDM_EINVAL = -1,      /* bad argument (null pointer, n > capacity, radius < 0, ...) */
+    BDM_ECAPACITY = -2,   /* a library or caller capacity is too small; see bdm_last_error */
+    BDM_ECUDA = -3,       /* CUDA runtime error (possibly from an earlier async launch) */
+    BDM_ENCCL = -4,       /* reserved for collective errors */
+    BDM_ENOTFINITE = -5,  /* a position was NaN/Inf */
+    BDM_ENOTIMPL = -6     /* feature not implemented in this build */
+} bdm_status;
+
+/* Agent flag bits (R8, R31; static-agent conditions of P:4941-4946).  Set by a
+ * step, read by the next step. */
+#define BDM_FLAG_MOVED 0x1u   /* displacement != 0 in the last step (condition i)    */
+#define BDM_FLAG_GREW 0x2u    /* diameter increased in the last step (condition ii)  */
+#define BDM_FLAG_ADDED 0x4u   /* created in the last step (condition iii); initial
+                                 agents carry it so nobody is static at step 0     */
+#define BDM_FLAG_STATIC 0x8u  /* the force was skipped in the last step             */
+#define BDM_FLAG_NNZ_SHIFT 4  /* bits 4-5: #non-zero neighbour forces, saturating at
+                                 2 (condition iv)                                   */
+
+/* Structure-of-arrays agent storage (D01/D02 of SURVEY).  Caller-owned
+ * device memory, `capacity` elements each.  A mechanics step reorders all arrays
+ * (agents travel with their id), see bdm_mech_step. */
+typedef struct {
+    int64_t n;            /* live agents                                           */
+    int64_t capacity;     /* allocated elements of every array                     */
+    double *x, *y, *z;    /* centre of mass [um or m]                              */
+    double *diameter;     /* sphere diameter d = 2r                                 */
+    double *volume;       /* nullable (growth/division only)                       */
+    uint32_t *id;         /* immutable global agent id (A50)                       */
+    uint32_t *flags;      /* BDM_FLAG_* bits                                       */
+    uint8_t *state;       /* nullable (SIR only): 0 S, 1 I, 2 R                    */
+} bdm_agents;
+
+/* Parameters of one mechanics step. */
+typedef struct {
+    double k, gamma;           /* Eq. 4.1 coefficients, 2 and 1 in the paper */
+    double dt;                 /* displacement = dt * sum of forces (R6)                    */
+    double max_displacement;   /* cap on |displacement| per step (R6)                       */
+    double force_threshold;    /* move only if |F| > threshold (R7)            */
+    double radius;             /* interaction radius; <= 0: largest diameter  */
+    int32_t detect_static;     /* 1: skip the force of static agents (sec:static-agents)    */
+    int32_t boundary;          /* 0 open (P:2671 (i)), 1 closed = clamp to [lo, hi]        */
+    double lo[3], hi[3];       /* closed-boundary box                                       */
+    uint64_t seed;             /* Philox key for steps that draw random numbers            */
+    uint32_t step;             /* iteration number (Philox counter word)                    */
+    uint32_t collect_stats;    /* 1: count candidates/neighbours/contacts (costs atomics)  */
+} bdm_params;
+
+/* Per-step work counters (sums over the agents of the step). */
+typedef struct {
+    int64_t cand;      /* candidates examined in the 27 boxes (force loop only)     */
+    int64_t nbr;       /* of which within the interaction radius (D <= R^2)         */
+    int64_t cont;      /* of which in contact (overlap delta > 0)                   */
+    int64_t n_static;  /* agents whose force was skipped                           */
+    int64_t n_moved;   /* agents with a non-zero displacement                      */
+    int64_t launches;  /* kernels launched by this context since bdm_create (cumulative,
+                          host-side count; independent of collect_stats)            */
+} bdm_stats;
+
+/* Geometry of the last grid build (a1 of SURVEY section 8(a)). */
+typedef struct {
+    double R, L;             /* interaction radius and box edge L = R(1+2^-20) (R5)  */
+    double origin[3];        /* per-axis minimum of the positions (R12)              */
+    double upper[3];         /* per-axis maximum                                     */
+    int64_t dims[3];         /* boxes per axis                                        */
+    int64_t nslots;          /* blocked-Morton key slots = ceil(dims/4)^3 * 64 (R32)   */
+    int64_t slot_capacity;   /* allocated slots                                       */
+} bdm_grid_info;
+
+typedef struct bdm_ctx *bdm_handle;
+
+/* Create a library context on CUDA device `device` with workspace for up to
+ * `max_agents` agents (grown automatically by bdm_grid_build if exceeded).
+ * Synchronizing.  Errors: BDM_EINVAL (max_agents < 0, bad device), BDM_ECUDA. */
+bdm_status bdm_create(bdm_handle *out, int device, int64_t max_agents);
+
+/* Free the context and its workspace.  Synchronizing.  NULL is a no-op. */
+bdm_status bdm_destroy(bdm_handle h);
+
+/* Thread-local description of the last error ("" if none). */
+const char *bdm_last_error(void);
+
+/* Library version string ("bdm <semver> sm_100a"). */
+const char *bdm_version(void);
+
+/* Uniform-in-cube population (ModelInitializer) with the per-agent
+ * counter-based PRNG the paper proposes: for agent id = id0 + k,
+ * Philox4x32-10 with key = seed and counter (id_lo, id_hi, w, 2) gives
+ * x, y from w = 0xFFFFFFFF, z from w = 0xFFFFFFFE, and, if d_random, the diameter
+ * d = d_lo + d_width * u53 from w = 0xFFFFFFFD (R22, R23, R29); else d = d_lo.
+ * Writes agents [0, n) of `a` (a->n is set to n) with flags = BDM_FLAG_ADDED.
+ * Errors: BDM_EINVAL if n > a->capacity or a required pointer is NULL. */
+bdm_status bdm_init_spheres(bdm_handle h, bdm_agents *a, int64_t id0, int64_t n,
+                            uint64_t seed, double side, double d_lo, double d_width,
+                            int32_t d_random, void *stream);
+
+/* Grid build ("Environment Search" P:2584-2598, sec:grid
+ * P:4487-4530, agent sorting sec:load-balancing P:4720-4838):
+ *   a1  R = radius > 0 ? radius : max_i d_i; L = R(1+2^-20); origin = per-axis min;
+ *       dims = floor((max - origin)/L) + 1                               (R5, R12)
+ *   a2  box b = floor((x - origin)/L); blocked-Morton key (4^3 tiles, row-major
+ *       tiles, 3-D Morton inside, x in the lowest bit)                   (R32)
+ *   a3  box start/length by an exclusive scan of per-slot counts (replaces the
+ *       paper's timestamped array linked list)
+ *   a4  counting sort by key, ascending id inside a box, gather of the SoA into
+ *       the library's sorted workspace.
+ * `ghosts` (nullable) are read-only agents owned by a neighbouring rank (aura,
+ * P:6083-6106); they enter the grid but are never updated.  Not yet supported:
+ * a non-NULL `ghosts` returns BDM_ENOTIMPL.
+ * The first call for a given context synchronizes once to size the slot array;
+ * later calls are asynchronous.  Errors: BDM_EINVAL, BDM_ECUDA. */
+bdm_status bdm_grid_build(bdm_handle h, const bdm_agents *a, const bdm_agents *ghosts,
+                          double radius, void *stream);
+
+/* Mechanics step over the grid of the preceding bdm_grid_build on the same agents
+ * (rows a5-a9: MechanicalForcesOp + BoundSpaceOp; Eq. 4.1/4.2
+ * P:2720-2741; static-agent skip sec:static-agents P:4920-4965).  Copy (Jacobi)
+ * semantics (R11).  For every agent i, in the canonical order of R9
+ * (27 boxes in (dz,dy,dx) lexicographic order, ascending id inside a box):
+ *   D = fma(dz,dz, fma(dy,dy, dx*dx)), (dx,dy,dz) = x_i - x_j; neighbour iff D <= R^2
+ *   dist = sqrt(D); delta = (r_i + r_j) - dist; if delta > 0 and dist > 0:
+ *     rbar = r_i r_j/(r_i + r_j); F_N = k delta - gamma sqrt(rbar delta);
+ *     F_i = fma(F_N/dist, x_i - x_j, F_i) per component
+ *   displacement = dt F_i if |F_i|^2 > threshold^2 else 0, capped at
+ *   max_displacement; x_i += displacement; boundary (open: no-op; closed: clamp).
+ * Static agents (R8) skip the force: displacement 0, nnz carried.
+ * On return (stream order) the caller's arrays x,y,z,diameter,id,flags hold the
+ * new state in the grid's sorted order (key, then id): a permutation of the input.
+ * Errors: BDM_EINVAL (no matching grid build, bad params), BDM_ENOTIMPL
+ * (toroidal boundary), BDM_ECUDA. */
+bdm_status bdm_mech_step(bdm_handle h, bdm_agents *a, const bdm_params *p, void *stream);
+
+/* Convenience: bdm_grid_build(a, NULL, p->radius) then bdm_mech_step(a, p). */
+bdm_status bdm_step(bdm_handle h, bdm_agents *a, const bdm_params *p, void *stream);
+
+/* End-to-end step on HOST arrays (the e2e entry point): copies the n agents of
+ * `host_in` to the device arrays `dev` (host->device), runs bdm_step, copies the
+ * new state back into `host_out` (device->host) and synchronizes `stream`.
+ * host_in may equal host_out.  Host arrays should be pinned for full bandwidth.
+ * Errors: as bdm_step, plus deferred device conditions (as bdm_sync). */
+bdm_status bdm_step_host(bdm_handle h, const bdm_agents *host_in, bdm_agents *host_out,
+                         bdm_agents *dev, const bdm_params *p, void *stream);
+
+/* Synchronize `stream` and report latched device conditions: BDM_ECAPACITY (grid
+ * slots exceeded; bdm_get_grid_info gives the needed nslots), BDM_ENOTFINITE, or a
+ * CUDA error.  Clears the latched condition. */
+bdm_status bdm_sync(bdm_handle h, void *stream);
+
+/* Ensure at least `nslots` grid slots and `max_agents` agents of workspace.
+ * Synchronizing. */
+bdm_status bdm_reserve(bdm_handle h, int64_t max_agents, int64_t nslots);
+
+/* Work counters of the last step issued with collect_stats = 1.  Synchronizes. */
+bdm_status bdm_get_stats(bdm_handle h, bdm_stats *out);
+
+/* Geometry of the last grid build.  Synchronizes. */
+bdm_status bdm_get_grid_info(bdm_handle h, bdm_grid_info *out);
+
+/* Test hook: all ordered neighbour pairs (id_i << 32 | id_j), j != i, D_ij <= R^2
+ * (R = radius > 0 ? radius : max diameter), enumerated through the grid (builds
+ * one, which replaces the grid of any previous bdm_grid_build).  Writes at most
+ * `cap` pairs (unordered) to the device array `pairs` and the total count to
+ * *count_host.  Synchronizing.  Returns BDM_ECAPACITY if count > cap. */
+bdm_status bdm_neighbor_pairs(bdm_handle h, const bdm_agents *a, double radius,
+                              uint64_t *pairs, int64_t cap, int64_t *count_host,
+                              void *stream);
+
+/* Diagnostic: measured fp64 FMA throughput of this GPU (DFMA lane-operations per
+ * second, i.e. half the fp64 FLOP/s) and the SM count.  Synchronizing. */
+bdm_status bdm_peak_dfma(bdm_handle h, double *dfma_per_s, int32_t *sm_count);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BDM_H */

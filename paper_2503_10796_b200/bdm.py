@@ -1,0 +1,326 @@
+"""Thin Python binding of include/bdm.h (libbdm.so, sm_100a).
+
+Argument marshalling only: every step of the hot path runs in the CUDA kernels of
+libbdm.so.  PyTorch provides device memory (CUDA tensors), streams and process
+groups.  There is no CPU fallback: if libbdm.so is missing or no GPU is present the
+calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass, field
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libbdm.so")
+
+BDM_OK, BDM_EINVAL, BDM_ECAPACITY, BDM_ECUDA, BDM_ENCCL, BDM_ENOTFINITE, BDM_ENOTIMPL = (
+    0, -1, -2, -3, -4, -5, -6)
+FLAG_MOVED, FLAG_GREW, FLAG_ADDED, FLAG_STATIC = 1, 2, 4, 8
+NNZ_SHIFT = 4
+
+# Every symbol include/bdm.h declares (checked by tests/test_abi.py).
+EXPORTS = [
+    "bdm_create", "bdm_destroy", "bdm_last_error", "bdm_version", "bdm_init_spheres",
+    "bdm_grid_build", "bdm_mech_step", "bdm_step", "bdm_step_host", "bdm_sync", "bdm_reserve",
+    "bdm_get_stats", "bdm_get_grid_info", "bdm_neighbor_pairs", "bdm_peak_dfma",
+]
+
+
+class BdmError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"bdm status {status}: {msg}")
+        self.status = status
+
+
+class CAgents(ctypes.Structure):
+    _fields_ = [
+        ("n", ctypes.c_int64), ("capacity", ctypes.c_int64),
+        ("x", ctypes.c_void_p), ("y", ctypes.c_void_p), ("z", ctypes.c_void_p),
+        ("diameter", ctypes.c_void_p), ("volume", ctypes.c_void_p),
+        ("id", ctypes.c_void_p), ("flags", ctypes.c_void_p), ("state", ctypes.c_void_p),
+    ]
+
+
+class CParams(ctypes.Structure):
+    _fields_ = [
+        ("k", ctypes.c_double), ("gamma", ctypes.c_double), ("dt", ctypes.c_double),
+        ("max_displacement", ctypes.c_double), ("force_threshold", ctypes.c_double),
+        ("radius", ctypes.c_double), ("detect_static", ctypes.c_int32),
+        ("boundary", ctypes.c_int32), ("lo", ctypes.c_double * 3), ("hi", ctypes.c_double * 3),
+        ("seed", ctypes.c_uint64), ("step", ctypes.c_uint32), ("collect_stats", ctypes.c_uint32),
+    ]
+
+
+class CStats(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int64) for n in ("cand", "nbr", "cont", "n_static", "n_moved",
+                                              "launches")]
+
+
+class CGridInfo(ctypes.Structure):
+    _fields_ = [
+        ("R", ctypes.c_double), ("L", ctypes.c_double), ("origin", ctypes.c_double * 3),
+        ("upper", ctypes.c_double * 3), ("dims", ctypes.c_int64 * 3), ("nslots", ctypes.c_int64),
+        ("slot_capacity", ctypes.c_int64),
+    ]
+
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
+    """dlopen libbdm.so and declare the signatures.  Raises if it is missing."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"{path} is missing: run `python -c 'import __graft_entry__ as g; "
+                          f"g.build()'` (no CPU fallback exists)")
+    L = ctypes.CDLL(path)
+    P, i64, i32, dbl, u64 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_double, ctypes.c_uint64
+    AG = ctypes.POINTER(CAgents)
+    PR = ctypes.POINTER(CParams)
+    sig = {
+        "bdm_create": [ctypes.POINTER(P), ctypes.c_int, i64],
+        "bdm_destroy": [P],
+        "bdm_init_spheres": [P, AG, i64, i64, u64, dbl, dbl, dbl, i32, P],
+        "bdm_grid_build": [P, AG, AG, dbl, P],
+        "bdm_mech_step": [P, AG, PR, P],
+        "bdm_step": [P, AG, PR, P],
+        "bdm_step_host": [P, AG, AG, AG, PR, P],
+        "bdm_sync": [P, P],
+        "bdm_reserve": [P, i64, i64],
+        "bdm_get_stats": [P, ctypes.POINTER(CStats)],
+        "bdm_get_grid_info": [P, ctypes.POINTER(CGridInfo)],
+        "bdm_neighbor_pairs": [P, AG, dbl, P, i64, ctypes.POINTER(i64), P],
+        "bdm_peak_dfma": [P, ctypes.POINTER(dbl), ctypes.POINTER(i32)],
+    }
+    for name, args in sig.items():
+        f = getattr(L, name)
+        f.argtypes = args
+        f.restype = ctypes.c_int
+    L.bdm_last_error.restype = ctypes.c_char_p
+    L.bdm_version.restype = ctypes.c_char_p
+    _lib = L
+    return L
+
+
+def _check(status: int):
+    if status != BDM_OK:
+        raise BdmError(status, load_library().bdm_last_error().decode())
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else ctypes.c_void_p(0)
+
+
+@dataclass
+class Params:
+    """bdm_params.  Defaults: Eq. 4.1 with k = 2, gamma = 1; dt = 0.01 and
+    a 3 um cap (BASELINE configs); threshold 0; R = largest diameter."""
+    k: float = 2.0
+    gamma: float = 1.0
+    dt: float = 0.01
+    max_displacement: float = 3.0
+    force_threshold: float = 0.0
+    radius: float = 0.0
+    detect_static: bool = False
+    boundary: int = 0
+    lo: tuple = (0.0, 0.0, 0.0)
+    hi: tuple = (0.0, 0.0, 0.0)
+    seed: int = 1
+    step: int = 0
+    collect_stats: bool = False
+
+    def c(self) -> CParams:
+        p = CParams()
+        p.k, p.gamma, p.dt = self.k, self.gamma, self.dt
+        p.max_displacement, p.force_threshold, p.radius = (
+            self.max_displacement, self.force_threshold, self.radius)
+        p.detect_static, p.boundary = int(bool(self.detect_static)), int(self.boundary)
+        p.lo[:] = list(self.lo)
+        p.hi[:] = list(self.hi)
+        p.seed, p.step, p.collect_stats = int(self.seed), int(self.step), int(bool(self.collect_stats))
+        return p
+
+
+@dataclass
+class Agents:
+    """SoA agent arrays (torch tensors on one device, or pinned host tensors)."""
+    x: "object"
+    y: "object"
+    z: "object"
+    diameter: "object"
+    id: "object"
+    flags: "object"
+    n: int = 0
+    volume: "object" = None
+    state: "object" = None
+    _c: CAgents = field(default=None, repr=False)
+
+    @staticmethod
+    def empty(capacity: int, device="cuda", pin: bool = False) -> "Agents":
+        import torch
+        kw = dict(device=device) if not pin else dict(pin_memory=True)
+        f64 = lambda: torch.empty(capacity, dtype=torch.float64, **kw)  # noqa: E731
+        u32 = lambda: torch.empty(capacity, dtype=torch.int32, **kw)    # noqa: E731
+        return Agents(f64(), f64(), f64(), f64(), u32(), u32(), 0)
+
+    @property
+    def capacity(self) -> int:
+        return int(self.x.numel())
+
+    def c(self) -> CAgents:
+        a = CAgents()
+        a.n, a.capacity = int(self.n), self.capacity
+        a.x, a.y, a.z, a.diameter = _ptr(self.x), _ptr(self.y), _ptr(self.z), _ptr(self.diameter)
+        a.volume, a.id, a.flags, a.state = (_ptr(self.volume), _ptr(self.id), _ptr(self.flags),
+                                            _ptr(self.state))
+        self._c = a
+        return a
+
+    def numpy(self) -> dict:
+        """Copy of the live agents as numpy arrays (id/flags as uint32)."""
+        import numpy as np
+        n = self.n
+        out = {k: getattr(self, k)[:n].cpu().numpy() for k in ("x", "y", "z", "diameter")}
+        out["d"] = out.pop("diameter")
+        out["id"] = self.id[:n].cpu().numpy().view(np.uint32)
+        out["flags"] = self.flags[:n].cpu().numpy().view(np.uint32)
+        return out
+
+    @staticmethod
+    def from_numpy(s: dict, capacity: int = None, device="cuda") -> "Agents":
+        import numpy as np
+        import torch
+        n = len(s["x"])
+        cap = max(capacity or n, 1)
+        a = Agents.empty(cap, device=device)
+        a.n = n
+        for k, src in (("x", "x"), ("y", "y"), ("z", "z"), ("diameter", "d")):
+            getattr(a, k)[:n].copy_(torch.from_numpy(np.ascontiguousarray(s[src], np.float64)))
+        a.id[:n].copy_(torch.from_numpy(np.ascontiguousarray(s["id"], np.uint32).view(np.int32)))
+        a.flags[:n].copy_(torch.from_numpy(np.ascontiguousarray(s["flags"], np.uint32).view(np.int32)))
+        return a
+
+
+def _stream_ptr(stream):
+    if stream is None:
+        import torch
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+class Engine:
+    """Owns a bdm_handle (library workspace on one device)."""
+
+    def __init__(self, device: int = 0, max_agents: int = 1):
+        self.lib = load_library()
+        h = ctypes.c_void_p()
+        _check(self.lib.bdm_create(ctypes.byref(h), int(device), int(max_agents)))
+        self.h = h
+        self.device = device
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.bdm_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -------------------------------------------------------------- calls of bdm.h
+    def init_spheres(self, agents: Agents, n, seed=1, side=160.0, d_lo=10.0, d_width=0.0,
+                     d_random=False, id0=0, stream=None):
+        ca = agents.c()
+        _check(self.lib.bdm_init_spheres(self.h, ctypes.byref(ca), int(id0), int(n), int(seed),
+                                         float(side), float(d_lo), float(d_width),
+                                         int(bool(d_random)), _stream_ptr(stream)))
+        agents.n = int(n)
+
+    def grid_build(self, agents: Agents, radius: float = 0.0, stream=None):
+        ca = agents.c()
+        _check(self.lib.bdm_grid_build(self.h, ctypes.byref(ca), None, float(radius),
+                                       _stream_ptr(stream)))
+
+    def mech_step(self, agents: Agents, params: Params, stream=None):
+        ca = agents.c()
+        cp = params.c()
+        _check(self.lib.bdm_mech_step(self.h, ctypes.byref(ca), ctypes.byref(cp),
+                                      _stream_ptr(stream)))
+
+    def step(self, agents: Agents, params: Params, stream=None, sync: bool = True,
+             retries: int = 3):
+        """grid build + mechanics step.  With sync=True, checks the latched device
+        conditions and, on a grid-slot overflow, grows the slot array and re-issues the
+        step (the caller's arrays are untouched by an overflowed step)."""
+        for _ in range(retries + 1):
+            self.grid_build(agents, params.radius, stream)
+            self.mech_step(agents, params, stream)
+            if not sync:
+                return
+            st = self.lib.bdm_sync(self.h, _stream_ptr(stream))
+            if st == BDM_ECAPACITY:
+                gi = self.grid_info()
+                _check(self.lib.bdm_reserve(self.h, 0, int(gi["nslots"] * 3 // 2)))
+                continue
+            _check(st)
+            return
+        raise BdmError(BDM_ECAPACITY, "grid slot capacity could not be satisfied")
+
+    def step_host(self, host_in: Agents, host_out: Agents, dev: Agents, params: Params,
+                  stream=None):
+        ci, co, cd, cp = host_in.c(), host_out.c(), dev.c(), params.c()
+        _check(self.lib.bdm_step_host(self.h, ctypes.byref(ci), ctypes.byref(co),
+                                      ctypes.byref(cd), ctypes.byref(cp), _stream_ptr(stream)))
+        host_out.n = host_in.n
+        dev.n = host_in.n
+
+    def sync(self, stream=None):
+        _check(self.lib.bdm_sync(self.h, _stream_ptr(stream)))
+
+    def try_sync(self, stream=None) -> int:
+        return int(self.lib.bdm_sync(self.h, _stream_ptr(stream)))
+
+    def reserve(self, max_agents: int = 0, nslots: int = 0):
+        _check(self.lib.bdm_reserve(self.h, int(max_agents), int(nslots)))
+
+    def stats(self) -> dict:
+        s = CStats()
+        _check(self.lib.bdm_get_stats(self.h, ctypes.byref(s)))
+        return {k: getattr(s, k) for k in ("cand", "nbr", "cont", "n_static", "n_moved",
+                                           "launches")}
+
+    def grid_info(self) -> dict:
+        g = CGridInfo()
+        _check(self.lib.bdm_get_grid_info(self.h, ctypes.byref(g)))
+        return {"R": g.R, "L": g.L, "origin": list(g.origin), "upper": list(g.upper),
+                "dims": list(g.dims), "nslots": g.nslots, "slot_capacity": g.slot_capacity}
+
+    def neighbor_pairs(self, agents: Agents, radius: float = 0.0, stream=None):
+        """Sorted numpy uint64 array of (id_i << 32 | id_j) through the GPU grid."""
+        import numpy as np
+        import torch
+        ca = agents.c()
+        cnt = ctypes.c_int64()
+        cap = 1
+        buf = torch.empty(cap, dtype=torch.int64, device=agents.x.device)
+        st = self.lib.bdm_neighbor_pairs(self.h, ctypes.byref(ca), float(radius), _ptr(buf), cap,
+                                         ctypes.byref(cnt), _stream_ptr(stream))
+        if st == BDM_ECAPACITY and cnt.value > cap:
+            cap = cnt.value
+            buf = torch.empty(cap, dtype=torch.int64, device=agents.x.device)
+            ca = agents.c()
+            st = self.lib.bdm_neighbor_pairs(self.h, ctypes.byref(ca), float(radius), _ptr(buf),
+                                             cap, ctypes.byref(cnt), _stream_ptr(stream))
+        _check(st)
+        return np.sort(buf[:cnt.value].cpu().numpy().view(np.uint64))
+
+    def peak_dfma(self):
+        v = ctypes.c_double()
+        n = ctypes.c_int32()
+        _check(self.lib.bdm_peak_dfma(self.h, ctypes.byref(v), ctypes.byref(n)))
+        return v.value, n.value

@@ -1,0 +1,341 @@
+// bdm_abi.cu -- extern "C" entry points of include/bdm.h: argument checks, workspace
+// management, and the stream-ordered composition of the kernels.
+#include <cuda_runtime.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <string>
+
+#include "bdm_internal.cuh"
+
+namespace bdm {
+
+static thread_local std::string g_err;
+
+void set_error(const std::string &msg) { g_err = msg; }
+
+bdm_status cuda_fail(cudaError_t e, const char *what) {
+    g_err = std::string(what) + ": " + cudaGetErrorString(e);
+    return BDM_ECUDA;
+}
+
+int64_t scan_block_count(int64_t slot_cap);
+
+static bdm_status fail(bdm_status s, const std::string &msg) {
+    g_err = msg;
+    return s;
+}
+
+template <class T>
+static bdm_status dalloc(T **p, int64_t count) {
+    if (*p) cudaFree(*p);
+    *p = nullptr;
+    if (count <= 0) count = 1;
+    cudaError_t e = cudaMalloc((void **)p, (size_t)count * sizeof(T));
+    if (e != cudaSuccess) {
+        *p = nullptr;
+        cudaGetLastError();
+        return fail(BDM_ECAPACITY, std::string("cudaMalloc of ") +
+                                       std::to_string((long long)count * sizeof(T)) +
+                                       " bytes failed: " + cudaGetErrorString(e));
+    }
+    return BDM_OK;
+}
+
+static bdm_status grow_agents(Ctx *c, int64_t n) {
+    if (n <= c->agent_cap) return BDM_OK;
+    BDM_CUDA_TRY(cudaDeviceSynchronize());
+    const int64_t cap = n + n / 8 + 1024;
+    bdm_status s;
+    if ((s = dalloc(&c->key, cap)) || (s = dalloc(&c->rank, cap)) ||
+        (s = dalloc(&c->perm_tmp, cap)) || (s = dalloc(&c->skey, cap)) ||
+        (s = dalloc(&c->sid, cap)) || (s = dalloc(&c->perm, cap)) || (s = dalloc(&c->sx, cap)) ||
+        (s = dalloc(&c->sy, cap)) || (s = dalloc(&c->sz, cap)) || (s = dalloc(&c->sd, cap)) ||
+        (s = dalloc(&c->sidf, cap)) || (s = dalloc(&c->sflags, cap))) {
+        c->agent_cap = 0;
+        return s;
+    }
+    c->agent_cap = cap;
+    c->grid_valid = false;
+    return BDM_OK;
+}
+
+static bdm_status grow_slots(Ctx *c, int64_t nslots) {
+    if (nslots <= c->slot_cap) return BDM_OK;
+    BDM_CUDA_TRY(cudaDeviceSynchronize());
+    bdm_status s;
+    if ((s = dalloc(&c->box_start, nslots + 1))) { c->slot_cap = 0; return s; }
+    const int64_t nb = scan_block_count(nslots);
+    if ((s = dalloc(&c->block_sums, nb + 1))) { c->slot_cap = 0; return s; }
+    c->block_sums_cap = nb + 1;
+    c->slot_cap = nslots;
+    long long cap = nslots;
+    BDM_CUDA_TRY(cudaMemcpy(&c->sc->slot_cap, &cap, sizeof(cap), cudaMemcpyHostToDevice));
+    c->grid_valid = false;
+    return BDM_OK;
+}
+
+static bdm_status check_agents(const bdm_agents *a, bool need_all) {
+    if (!a) return fail(BDM_EINVAL, "agents is NULL");
+    if (a->n < 0 || a->n > a->capacity) return fail(BDM_EINVAL, "n < 0 or n > capacity");
+    if (a->n > 0xFFFFFFFFll - 1) return fail(BDM_EINVAL, "n exceeds 2^32 - 2 agents per context");
+    if (need_all && a->n > 0 &&
+        (!a->x || !a->y || !a->z || !a->diameter || !a->id || !a->flags))
+        return fail(BDM_EINVAL, "a required agent array is NULL");
+    const void *ptrs[] = {a->x, a->y, a->z, a->diameter, a->volume};
+    for (const void *p : ptrs)
+        if (((uintptr_t)p & 7u) != 0) return fail(BDM_EINVAL, "agent array not 8-byte aligned");
+    return BDM_OK;
+}
+
+// Latched device conditions -> status (after a synchronize).
+static bdm_status read_latches(Ctx *c, bool clear) {
+    BDM_CUDA_TRY(cudaMemcpy(c->sc_host, c->sc, sizeof(DevScalars), cudaMemcpyDeviceToHost));
+    bdm_status st = BDM_OK;
+    if (c->sc_host->nonfinite) {
+        st = fail(BDM_ENOTFINITE, "a position or diameter is NaN/Inf");
+    } else if (c->sc_host->overflow) {
+        st = fail(BDM_ECAPACITY, "grid needs " + std::to_string(c->sc_host->nslots) +
+                                     " slots, capacity " + std::to_string(c->slot_cap));
+    }
+    if (clear && st != BDM_OK) {
+        int32_t z[2] = {0, 0};
+        BDM_CUDA_TRY(cudaMemcpy(&c->sc->overflow, z, sizeof(z), cudaMemcpyHostToDevice));
+    }
+    return st;
+}
+
+}  // namespace bdm
+
+using namespace bdm;
+
+extern "C" {
+
+const char *bdm_last_error(void) { return g_err.c_str(); }
+
+const char *bdm_version(void) { return "bdm 0.1.0 sm_100a"; }
+
+bdm_status bdm_create(bdm_handle *out, int device, int64_t max_agents) {
+    if (!out) return fail(BDM_EINVAL, "out is NULL");
+    *out = nullptr;
+    if (max_agents < 0) return fail(BDM_EINVAL, "max_agents < 0");
+    int ndev = 0;
+    BDM_CUDA_TRY(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) return fail(BDM_EINVAL, "bad device index");
+    BDM_CUDA_TRY(cudaSetDevice(device));
+    Ctx *c = new Ctx();
+    c->device = device;
+    cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device);
+    if (cudaMalloc(&c->sc, sizeof(DevScalars)) != cudaSuccess ||
+        cudaMallocHost(&c->sc_host, sizeof(DevScalars)) != cudaSuccess ||
+        cudaMalloc(&c->pair_count, sizeof(unsigned long long)) != cudaSuccess) {
+        cudaGetLastError();
+        delete c;
+        return fail(BDM_ECUDA, "allocation of the context scalars failed");
+    }
+    cudaMemset(c->sc, 0, sizeof(DevScalars));
+    bdm_status s = grow_agents(c, max_agents > 0 ? max_agents : 1);
+    if (s != BDM_OK) {
+        bdm_destroy((bdm_handle)c);
+        return s;
+    }
+    BDM_CUDA_TRY(cudaDeviceSynchronize());
+    *out = (bdm_handle)c;
+    return BDM_OK;
+}
+
+bdm_status bdm_destroy(bdm_handle h) {
+    if (!h) return BDM_OK;
+    Ctx *c = (Ctx *)h;
+    cudaSetDevice(c->device);
+    cudaDeviceSynchronize();
+    void *bufs[] = {c->key, c->rank, c->perm_tmp, c->skey, c->sid, c->perm, c->sx, c->sy,
+                    c->sz, c->sd, c->sidf, c->sflags, c->box_start, c->block_sums,
+                    c->pair_count, c->sc};
+    for (void *p : bufs)
+        if (p) cudaFree(p);
+    if (c->sc_host) cudaFreeHost(c->sc_host);
+    delete c;
+    return BDM_OK;
+}
+
+bdm_status bdm_init_spheres(bdm_handle h, bdm_agents *a, int64_t id0, int64_t n, uint64_t seed,
+                            double side, double d_lo, double d_width, int32_t d_random,
+                            void *stream) {
+    if (!h) return fail(BDM_EINVAL, "handle is NULL");
+    if (!a || n < 0 || n > a->capacity || id0 < 0)
+        return fail(BDM_EINVAL, "bad n / id0 / capacity");
+    if (n > 0 && (!a->x || !a->y || !a->z || !a->diameter || !a->id || !a->flags))
+        return fail(BDM_EINVAL, "a required agent array is NULL");
+    if (!(side > 0.0)) return fail(BDM_EINVAL, "side must be > 0");
+    a->n = n;
+    return launch_init_spheres(a, id0, n, seed, side, d_lo, d_width, d_random,
+                               (cudaStream_t)stream);
+}
+
+bdm_status bdm_grid_build(bdm_handle h, const bdm_agents *a, const bdm_agents *ghosts,
+                          double radius, void *stream) {
+    if (!h) return fail(BDM_EINVAL, "handle is NULL");
+    Ctx *c = (Ctx *)h;
+    bdm_status s = check_agents(a, true);
+    if (s != BDM_OK) return s;
+    if (ghosts && ghosts->n > 0) return fail(BDM_ENOTIMPL, "ghost agents not supported yet");
+    if (radius < 0.0 || radius != radius) return fail(BDM_EINVAL, "radius < 0");
+    cudaStream_t st = (cudaStream_t)stream;
+    c->grid_valid = false;
+    if (a->n == 0) {
+        c->grid_valid = true;
+        c->grid_x = a->x;
+        c->grid_n = 0;
+        return BDM_OK;
+    }
+    if ((s = grow_agents(c, a->n)) != BDM_OK) return s;
+    if ((s = launch_grid_geometry(c, a, radius, st)) != BDM_OK) return s;
+    if (c->slot_cap == 0) {
+        // first build: size the slot array from the actual geometry (one sync),
+        // with room for growth of the open-boundary space (+4 tiles per axis)
+        BDM_CUDA_TRY(cudaStreamSynchronize(st));
+        BDM_CUDA_TRY(cudaMemcpy(c->sc_host, c->sc, sizeof(DevScalars), cudaMemcpyDeviceToHost));
+        if (c->sc_host->nonfinite) {
+            int32_t z[2] = {0, 0};
+            cudaMemcpy(&c->sc->overflow, z, sizeof(z), cudaMemcpyHostToDevice);
+            return fail(BDM_ENOTFINITE, "a position or diameter is NaN/Inf");
+        }
+        const int64_t t0 = c->sc_host->T[0] + 4, t1 = c->sc_host->T[1] + 4,
+                      t2 = c->sc_host->T[2] + 4;
+        if ((s = grow_slots(c, t0 * t1 * t2 * 64)) != BDM_OK) return s;
+        int32_t z[2] = {0, 0};
+        BDM_CUDA_TRY(cudaMemcpy(&c->sc->overflow, z, sizeof(z), cudaMemcpyHostToDevice));
+        if ((s = launch_grid_geometry(c, a, radius, st)) != BDM_OK) return s;
+    }
+    if ((s = launch_grid_sort(c, a, st)) != BDM_OK) return s;
+    c->grid_valid = true;
+    c->grid_x = a->x;
+    c->grid_n = a->n;
+    return BDM_OK;
+}
+
+bdm_status bdm_mech_step(bdm_handle h, bdm_agents *a, const bdm_params *p, void *stream) {
+    if (!h || !p) return fail(BDM_EINVAL, "handle or params is NULL");
+    Ctx *c = (Ctx *)h;
+    bdm_status s = check_agents(a, true);
+    if (s != BDM_OK) return s;
+    if (!c->grid_valid || c->grid_x != a->x || c->grid_n != a->n)
+        return fail(BDM_EINVAL, "bdm_mech_step needs a preceding bdm_grid_build on the same agents");
+    if (p->boundary == 2) return fail(BDM_ENOTIMPL, "toroidal mechanics not implemented");
+    if (p->boundary != 0 && p->boundary != 1) return fail(BDM_EINVAL, "bad boundary");
+    if (!(p->dt >= 0.0) || !(p->max_displacement >= 0.0) || !(p->force_threshold >= 0.0))
+        return fail(BDM_EINVAL, "dt, max_displacement and force_threshold must be >= 0");
+    c->grid_valid = false;  // positions change: the grid is stale afterwards
+    if (a->n == 0) return BDM_OK;
+    return launch_mech(c, a, p, (cudaStream_t)stream);
+}
+
+bdm_status bdm_step(bdm_handle h, bdm_agents *a, const bdm_params *p, void *stream) {
+    if (!p) return fail(BDM_EINVAL, "params is NULL");
+    bdm_status s = bdm_grid_build(h, a, nullptr, p->radius, stream);
+    if (s != BDM_OK) return s;
+    return bdm_mech_step(h, a, p, stream);
+}
+
+bdm_status bdm_step_host(bdm_handle h, const bdm_agents *hin, bdm_agents *hout, bdm_agents *dev,
+                         const bdm_params *p, void *stream) {
+    if (!h || !hin || !hout || !dev || !p) return fail(BDM_EINVAL, "NULL argument");
+    if (hin->n > dev->capacity || hin->n > hout->capacity)
+        return fail(BDM_EINVAL, "n exceeds a capacity");
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t n = (size_t)hin->n;
+    dev->n = hin->n;
+    BDM_CUDA_TRY(cudaMemcpyAsync(dev->x, hin->x, n * 8, cudaMemcpyHostToDevice, st));
+    BDM_CUDA_TRY(cudaMemcpyAsync(dev->y, hin->y, n * 8, cudaMemcpyHostToDevice, st));
+    BDM_CUDA_TRY(cudaMemcpyAsync(dev->z, hin->z, n * 8, cudaMemcpyHostToDevice, st));
+    BDM_CUDA_TRY(cudaMemcpyAsync(dev->diameter, hin->diameter, n * 8, cudaMemcpyHostToDevice, st));
+    BDM_CUDA_TRY(cudaMemcpyAsync(dev->id, hin->id, n * 4, cudaMemcpyHostToDevice, st));
+    BDM_CUDA_TRY(cudaMemcpyAsync(dev->flags, hin->flags, n * 4, cudaMemcpyHostToDevice, st));
+    bdm_status s = bdm_step(h, dev, p, stream);
+    if (s != BDM_OK) return s;
+    hout->n = hin->n;
+    BDM_CUDA_TRY(cudaMemcpyAsync(hout->x, dev->x, n * 8, cudaMemcpyDeviceToHost, st));
+    BDM_CUDA_TRY(cudaMemcpyAsync(hout->y, dev->y, n * 8, cudaMemcpyDeviceToHost, st));
+    BDM_CUDA_TRY(cudaMemcpyAsync(hout->z, dev->z, n * 8, cudaMemcpyDeviceToHost, st));
+    BDM_CUDA_TRY(cudaMemcpyAsync(hout->diameter, dev->diameter, n * 8, cudaMemcpyDeviceToHost, st));
+    BDM_CUDA_TRY(cudaMemcpyAsync(hout->id, dev->id, n * 4, cudaMemcpyDeviceToHost, st));
+    BDM_CUDA_TRY(cudaMemcpyAsync(hout->flags, dev->flags, n * 4, cudaMemcpyDeviceToHost, st));
+    return bdm_sync(h, stream);
+}
+
+bdm_status bdm_sync(bdm_handle h, void *stream) {
+    if (!h) return fail(BDM_EINVAL, "handle is NULL");
+    Ctx *c = (Ctx *)h;
+    BDM_CUDA_TRY(cudaStreamSynchronize((cudaStream_t)stream));
+    BDM_CUDA_TRY(cudaGetLastError());
+    return read_latches(c, true);
+}
+
+bdm_status bdm_reserve(bdm_handle h, int64_t max_agents, int64_t nslots) {
+    if (!h) return fail(BDM_EINVAL, "handle is NULL");
+    Ctx *c = (Ctx *)h;
+    bdm_status s = grow_agents(c, max_agents);
+    if (s != BDM_OK) return s;
+    return grow_slots(c, nslots);
+}
+
+bdm_status bdm_get_stats(bdm_handle h, bdm_stats *out) {
+    if (!h || !out) return fail(BDM_EINVAL, "NULL argument");
+    Ctx *c = (Ctx *)h;
+    BDM_CUDA_TRY(cudaDeviceSynchronize());
+    BDM_CUDA_TRY(cudaMemcpy(c->sc_host, c->sc, sizeof(DevScalars), cudaMemcpyDeviceToHost));
+    out->cand = (int64_t)c->sc_host->stats[0];
+    out->nbr = (int64_t)c->sc_host->stats[1];
+    out->cont = (int64_t)c->sc_host->stats[2];
+    out->n_static = (int64_t)c->sc_host->stats[3];
+    out->n_moved = (int64_t)c->sc_host->stats[4];
+    out->launches = c->launches;
+    return BDM_OK;
+}
+
+bdm_status bdm_get_grid_info(bdm_handle h, bdm_grid_info *out) {
+    if (!h || !out) return fail(BDM_EINVAL, "NULL argument");
+    Ctx *c = (Ctx *)h;
+    BDM_CUDA_TRY(cudaDeviceSynchronize());
+    BDM_CUDA_TRY(cudaMemcpy(c->sc_host, c->sc, sizeof(DevScalars), cudaMemcpyDeviceToHost));
+    const DevScalars &s = *c->sc_host;
+    out->R = s.R;
+    out->L = s.L;
+    for (int a = 0; a < 3; ++a) {
+        out->origin[a] = s.o[a];
+        out->upper[a] = s.hi[a];
+        out->dims[a] = s.dims[a];
+    }
+    out->nslots = s.nslots;
+    out->slot_capacity = c->slot_cap;
+    return BDM_OK;
+}
+
+bdm_status bdm_neighbor_pairs(bdm_handle h, const bdm_agents *a, double radius, uint64_t *pairs,
+                              int64_t cap, int64_t *count_host, void *stream) {
+    if (!h || !count_host) return fail(BDM_EINVAL, "NULL argument");
+    if (cap > 0 && !pairs) return fail(BDM_EINVAL, "pairs is NULL");
+    Ctx *c = (Ctx *)h;
+    bdm_status s = bdm_grid_build(h, a, nullptr, radius, stream);
+    if (s != BDM_OK) return s;
+    c->grid_valid = false;  // the hook consumes the grid
+    *count_host = 0;
+    if (a->n == 0) return BDM_OK;
+    if ((s = launch_pairs(c, a->n, pairs, cap, (cudaStream_t)stream)) != BDM_OK) return s;
+    if ((s = bdm_sync(h, stream)) != BDM_OK) return s;
+    unsigned long long cnt = 0;
+    BDM_CUDA_TRY(cudaMemcpy(&cnt, c->pair_count, sizeof(cnt), cudaMemcpyDeviceToHost));
+    *count_host = (int64_t)cnt;
+    if ((int64_t)cnt > cap) return fail(BDM_ECAPACITY, "more pairs than cap");
+    return BDM_OK;
+}
+
+bdm_status bdm_peak_dfma(bdm_handle h, double *dfma_per_s, int32_t *sm_count) {
+    if (!h || !dfma_per_s || !sm_count) return fail(BDM_EINVAL, "NULL argument");
+    Ctx *c = (Ctx *)h;
+    *sm_count = c->sm_count;
+    return launch_peak_dfma(c->sm_count, dfma_per_s);
+}
+
+}  // extern "C"

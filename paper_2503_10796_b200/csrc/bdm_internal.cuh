@@ -1,0 +1,137 @@
+// bdm_internal.cuh -- shared declarations of the sm_100a implementation of bdm.h.
+//
+// Device helpers (Philox, ordered double encoding, blocked-Morton key) and the
+// library context.  Nothing here is shared with oracle/ (the CPU oracle has its own
+// independent implementation of every formula).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "bdm.h"
+
+namespace bdm {
+
+// ------------------------------------------------------------------ error plumbing
+void set_error(const std::string &msg);
+bdm_status cuda_fail(cudaError_t e, const char *what);
+
+#define BDM_CUDA_TRY(expr)                                              \
+    do {                                                                \
+        cudaError_t e__ = (expr);                                       \
+        if (e__ != cudaSuccess) return ::bdm::cuda_fail(e__, #expr);    \
+    } while (0)
+
+#define BDM_LAUNCH_CHECK(what)                                          \
+    do {                                                                \
+        cudaError_t e__ = cudaGetLastError();                           \
+        if (e__ != cudaSuccess) return ::bdm::cuda_fail(e__, what);     \
+    } while (0)
+
+// ------------------------------------------------------------------ device scalars
+// Written and read only by kernels (no host round trip inside a step).
+struct DevScalars {
+    unsigned long long enc_lo[3], enc_hi[3], enc_dmax;  // ordered encodings (atomics)
+    double R, R2, L;
+    double o[3], hi[3];
+    int32_t dims[3];
+    int32_t T[3];          // tiles per axis = ceil(dims / 4)
+    long long nslots;      // T0*T1*T2*64
+    long long slot_cap;    // allocated slots (host-written)
+    int32_t overflow;      // latched: nslots > slot_cap
+    int32_t nonfinite;     // latched: a position was NaN/Inf
+    unsigned long long stats[5];  // cand, nbr, cont, n_static, n_moved
+};
+
+// ------------------------------------------------------------------ library context
+struct Ctx {
+    int device = 0;
+    int sm_count = 148;
+    int64_t agent_cap = 0;
+    int64_t slot_cap = 0;
+    // per-agent workspace
+    uint32_t *key = nullptr, *rank = nullptr;          // unsorted order
+    uint32_t *perm_tmp = nullptr, *skey = nullptr, *sid = nullptr;  // after scatter
+    uint32_t *perm = nullptr;                          // sorted slot -> input index
+    double *sx = nullptr, *sy = nullptr, *sz = nullptr, *sd = nullptr;  // sorted SoA
+    uint32_t *sidf = nullptr, *sflags = nullptr;
+    // grid
+    uint32_t *box_start = nullptr;  // slot_cap + 1
+    uint32_t *block_sums = nullptr;
+    int64_t block_sums_cap = 0;
+    // misc
+    unsigned long long *pair_count = nullptr;
+    DevScalars *sc = nullptr;       // device
+    DevScalars *sc_host = nullptr;  // pinned mirror
+    // bookkeeping: the grid of the last bdm_grid_build
+    bool grid_valid = false;
+    const double *grid_x = nullptr;
+    int64_t grid_n = 0;
+    int64_t launches = 0;  // kernels launched (host-side count)
+};
+
+// ------------------------------------------------------------------ device helpers
+__device__ inline unsigned long long enc_double(double v) {
+    // monotone map double -> u64 (for atomicMin/atomicMax on doubles)
+    unsigned long long b = (unsigned long long)__double_as_longlong(v);
+    return (b & 0x8000000000000000ull) ? ~b : (b | 0x8000000000000000ull);
+}
+__device__ inline double dec_double(unsigned long long e) {
+    unsigned long long b = (e & 0x8000000000000000ull) ? (e & 0x7FFFFFFFFFFFFFFFull) : ~e;
+    return __longlong_as_double((long long)b);
+}
+
+// Philox4x32-10 (Salmon et al. SC'11), the counter-based generator the paper
+// proposes for order-independent per-agent randomness.
+struct U4 {
+    uint32_t a, b, c, d;
+};
+__device__ inline U4 philox10(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, uint32_t k0,
+                              uint32_t k1) {
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        const uint32_t lo0 = 0xD2511F53u * c0, hi0 = __umulhi(0xD2511F53u, c0);
+        const uint32_t lo1 = 0xCD9E8D57u * c2, hi1 = __umulhi(0xCD9E8D57u, c2);
+        const uint32_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+        c0 = n0;
+        c1 = lo1;
+        c2 = n2;
+        c3 = lo0;
+        k0 += 0x9E3779B9u;
+        k1 += 0xBB67AE85u;
+    }
+    return U4{c0, c1, c2, c3};
+}
+// 53-bit uniform in [0,1) from two words (R29): ((a>>5)*2^26 + (b>>6)) * 2^-53.
+__device__ inline double uniform53(uint32_t a, uint32_t b) {
+    return (double)(((unsigned long long)(a >> 5) << 26) | (unsigned long long)(b >> 6)) *
+           0x1p-53;
+}
+__device__ inline double uniform32(uint32_t w) { return (double)w * 0x1p-32; }
+
+// Blocked-Morton slot of box (bx, by, bz) (R32): 4x4x4 tiles numbered row-major,
+// 6-bit Morton code inside the tile with x in the lowest bit.
+__device__ __forceinline__ uint32_t box_key(int bx, int by, int bz, int T0, int T1) {
+    const uint32_t tile = (uint32_t)(((bz >> 2) * T1 + (by >> 2)) * T0 + (bx >> 2));
+    const uint32_t m = (uint32_t)((bx & 1) | ((by & 1) << 1) | ((bz & 1) << 2) |
+                                  ((bx & 2) << 2) | ((by & 2) << 3) | ((bz & 2) << 4));
+    return tile * 64u + m;
+}
+
+constexpr uint32_t kChanged = BDM_FLAG_MOVED | BDM_FLAG_GREW | BDM_FLAG_ADDED;
+
+// ------------------------------------------------------------------ launchers
+// grid (kernels_grid.cu)
+bdm_status launch_init_spheres(const bdm_agents *a, int64_t id0, int64_t n, uint64_t seed,
+                               double side, double d_lo, double d_width, int d_random,
+                               cudaStream_t st);
+bdm_status launch_grid_geometry(Ctx *c, const bdm_agents *a, double radius, cudaStream_t st);
+bdm_status launch_grid_sort(Ctx *c, const bdm_agents *a, cudaStream_t st);
+// mechanics (kernels_mech.cu)
+bdm_status launch_mech(Ctx *c, bdm_agents *a, const bdm_params *p, cudaStream_t st);
+bdm_status launch_pairs(Ctx *c, int64_t n, uint64_t *pairs, int64_t cap, cudaStream_t st);
+bdm_status launch_peak_dfma(int sm_count, double *dfma_per_s);
+
+}  // namespace bdm

@@ -1,0 +1,362 @@
+// kernels_grid.cu -- population init and the uniform-grid build.
+//
+//   a1  k_reduce + k_setup        exact per-axis min/max and max diameter, then
+//                                 R, L = R(1+2^-20), origin, dims, tiles, nslots
+//   a2  k_key                     box -> blocked-Morton slot, atomic per-slot rank
+//   a3  k_scan_*                  exclusive scan of slot counts -> box_start
+//   a4  k_scatter + k_fix_gather  counting-sort scatter, ascending-id order inside
+//                                 a box, gather of the SoA into the sorted workspace
+//
+// Paper: "Environment Search" P:2584-2598; sec:grid P:4487-4530 (boxes, 27-box
+// search, array-based linked list); sec:load-balancing P:4720-4838 (Morton order,
+// prefix sum over boxes P:4820-4827, copy to the new position P:4829-4835).
+#include <cuda_runtime.h>
+#include <math.h>
+
+#include "bdm_internal.cuh"
+
+namespace bdm {
+
+// ============================================================== population init
+__global__ void k_init_spheres(int64_t id0, int64_t n, uint32_t k0, uint32_t k1, double side,
+                               double d_lo, double d_width, int d_random, double *__restrict__ x,
+                               double *__restrict__ y, double *__restrict__ z,
+                               double *__restrict__ d, uint32_t *__restrict__ id,
+                               uint32_t *__restrict__ flags) {
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        const unsigned long long a = (unsigned long long)(id0 + k);
+        const uint32_t lo = (uint32_t)a, hi = (uint32_t)(a >> 32);
+        const U4 w = philox10(lo, hi, 0xFFFFFFFFu, 2u, k0, k1);
+        x[k] = uniform53(w.a, w.b) * side;
+        y[k] = uniform53(w.c, w.d) * side;
+        const U4 v = philox10(lo, hi, 0xFFFFFFFEu, 2u, k0, k1);
+        z[k] = uniform53(v.a, v.b) * side;
+        if (d_random) {
+            const U4 u = philox10(lo, hi, 0xFFFFFFFDu, 2u, k0, k1);
+            d[k] = d_lo + d_width * uniform53(u.a, u.b);
+        } else {
+            d[k] = d_lo;
+        }
+        id[k] = (uint32_t)a;
+        flags[k] = BDM_FLAG_ADDED;
+    }
+}
+
+bdm_status launch_init_spheres(const bdm_agents *a, int64_t id0, int64_t n, uint64_t seed,
+                               double side, double d_lo, double d_width, int d_random,
+                               cudaStream_t st) {
+    if (n == 0) return BDM_OK;
+    const int threads = 256;
+    const int64_t blocks = (n + threads - 1) / threads;
+    k_init_spheres<<<(unsigned)(blocks < 1184 * 16 ? blocks : 1184 * 16), threads, 0, st>>>(
+        id0, n, (uint32_t)seed, (uint32_t)(seed >> 32), side, d_lo, d_width, d_random, a->x,
+        a->y, a->z, a->diameter, a->id, a->flags);
+    BDM_LAUNCH_CHECK("k_init_spheres");
+    return BDM_OK;
+}
+
+// ============================================================== a1: global scalars
+__global__ void k_reset_scalars(DevScalars *sc) {
+    if (threadIdx.x == 0) {
+        for (int a = 0; a < 3; ++a) {
+            sc->enc_lo[a] = enc_double(INFINITY);
+            sc->enc_hi[a] = enc_double(-INFINITY);
+        }
+        sc->enc_dmax = enc_double(-INFINITY);
+    }
+}
+
+__device__ __forceinline__ double warp_min(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+// Exact min/max (comparisons only): per-thread, warp shuffles, shared memory, one
+// atomic per block on the ordered encodings.
+__global__ void __launch_bounds__(256) k_reduce(int64_t n, const double *__restrict__ x,
+                                                const double *__restrict__ y,
+                                                const double *__restrict__ z,
+                                                const double *__restrict__ d, DevScalars *sc) {
+    double lo0 = INFINITY, lo1 = INFINITY, lo2 = INFINITY;
+    double hi0 = -INFINITY, hi1 = -INFINITY, hi2 = -INFINITY, dm = -INFINITY;
+    bool bad = false;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const double px = x[i], py = y[i], pz = z[i], pd = d[i];
+        bad |= !isfinite(px) || !isfinite(py) || !isfinite(pz) || !isfinite(pd);
+        lo0 = fmin(lo0, px); hi0 = fmax(hi0, px);
+        lo1 = fmin(lo1, py); hi1 = fmax(hi1, py);
+        lo2 = fmin(lo2, pz); hi2 = fmax(hi2, pz);
+        dm = fmax(dm, pd);
+    }
+    lo0 = warp_min(lo0); lo1 = warp_min(lo1); lo2 = warp_min(lo2);
+    hi0 = warp_max(hi0); hi1 = warp_max(hi1); hi2 = warp_max(hi2); dm = warp_max(dm);
+    __shared__ double sh[8][7];
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) {
+        sh[w][0] = lo0; sh[w][1] = lo1; sh[w][2] = lo2;
+        sh[w][3] = hi0; sh[w][4] = hi1; sh[w][5] = hi2; sh[w][6] = dm;
+    }
+    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicExch(&sc->nonfinite, 1);
+    if (threadIdx.x < 7) {
+        const int q = threadIdx.x;
+        double v = sh[0][q];
+        for (int k = 1; k < (int)(blockDim.x >> 5); ++k)
+            v = q < 3 ? fmin(v, sh[k][q]) : fmax(v, sh[k][q]);
+        const unsigned long long e = enc_double(v);
+        if (q < 3) atomicMin(&sc->enc_lo[q], e);
+        else if (q < 6) atomicMax(&sc->enc_hi[q - 3], e);
+        else atomicMax(&sc->enc_dmax, e);
+    }
+}
+
+// R, L, origin, dims, tiles, slot count; latches overflow if the slots do not fit.
+__global__ void k_setup(DevScalars *sc, double radius) {
+    if (threadIdx.x != 0) return;
+    const double R = radius > 0.0 ? radius : dec_double(sc->enc_dmax);
+    const double L = R * (1.0 + 0x1p-20);
+    sc->R = R;
+    sc->R2 = R * R;
+    sc->L = L;
+    long long ns = 64;
+    bool bad = !(L > 0.0) || !isfinite(L);
+    for (int a = 0; a < 3; ++a) {
+        const double lo = dec_double(sc->enc_lo[a]), hi = dec_double(sc->enc_hi[a]);
+        sc->o[a] = lo;
+        sc->hi[a] = hi;
+        const double ext = floor((hi - lo) / L);
+        if (!(ext < 1.0e9)) bad = true;
+        const int dim = bad ? 1 : (int)ext + 1;
+        sc->dims[a] = dim;
+        sc->T[a] = (dim + 3) >> 2;
+        ns *= (long long)sc->T[a];
+        if (ns > (1ll << 40)) bad = true;
+    }
+    sc->nslots = ns;
+    if (bad || ns >= 0xFFFFFFFFll || ns > sc->slot_cap) sc->overflow = 1;
+}
+
+bdm_status launch_grid_geometry(Ctx *c, const bdm_agents *a, double radius, cudaStream_t st) {
+    k_reset_scalars<<<1, 32, 0, st>>>(c->sc);
+    const int64_t n = a->n;
+    int64_t blocks = (n + 255) / 256;
+    const int64_t maxb = (int64_t)c->sm_count * 8;
+    if (blocks > maxb) blocks = maxb;
+    if (blocks < 1) blocks = 1;
+    k_reduce<<<(unsigned)blocks, 256, 0, st>>>(n, a->x, a->y, a->z, a->diameter, c->sc);
+    k_setup<<<1, 32, 0, st>>>(c->sc, radius);
+    c->launches += 3;
+    BDM_LAUNCH_CHECK("grid geometry");
+    return BDM_OK;
+}
+
+// ============================================================== a2: keys + histogram
+__global__ void k_zero_counts(uint32_t *__restrict__ counts, const DevScalars *__restrict__ sc) {
+    if (sc->overflow) return;
+    const long long m = sc->nslots + 1;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < m;
+         i += (long long)gridDim.x * blockDim.x)
+        counts[i] = 0u;
+}
+
+__global__ void __launch_bounds__(256) k_key(int64_t n, const double *__restrict__ x,
+                                             const double *__restrict__ y,
+                                             const double *__restrict__ z,
+                                             const DevScalars *__restrict__ sc,
+                                             uint32_t *__restrict__ key,
+                                             uint32_t *__restrict__ rank,
+                                             uint32_t *__restrict__ counts) {
+    if (sc->overflow) return;
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double L = sc->L;
+    const int bx = (int)floor((x[i] - sc->o[0]) / L);
+    const int by = (int)floor((y[i] - sc->o[1]) / L);
+    const int bz = (int)floor((z[i] - sc->o[2]) / L);
+    const uint32_t k = box_key(bx, by, bz, sc->T[0], sc->T[1]);
+    key[i] = k;
+    rank[i] = atomicAdd(&counts[k], 1u);
+}
+
+// ============================================================== a3: exclusive scan
+// Reduce-then-scan over m = nslots + 1 counts, tiles of 4096 (512 threads x 8).
+constexpr int kScanThreads = 512;
+constexpr int kScanItems = 8;
+constexpr int kScanTile = kScanThreads * kScanItems;
+
+__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v) {
+    const int l = threadIdx.x & 31;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, v, o);
+        if (l >= o) v += t;
+    }
+    return v;
+}
+
+// Block-wide exclusive scan of one value per thread; returns the exclusive prefix and
+// writes the block total to *total.
+__device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t *total) {
+    __shared__ uint32_t wsum[32];
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    const uint32_t inc = warp_incl_scan(v);
+    if (l == 31) wsum[w] = inc;
+    __syncthreads();
+    if (w == 0) {
+        const int nw = blockDim.x >> 5;
+        uint32_t s = l < nw ? wsum[l] : 0u;
+        s = warp_incl_scan(s);
+        wsum[l] = s;  // inclusive prefix over warps
+    }
+    __syncthreads();
+    const uint32_t before = (w > 0 ? wsum[w - 1] : 0u) + inc - v;
+    *total = wsum[(blockDim.x >> 5) - 1];
+    __syncthreads();
+    return before;
+}
+
+__global__ void __launch_bounds__(kScanThreads) k_scan_reduce(const uint32_t *__restrict__ cnt,
+                                                              uint32_t *__restrict__ bsum,
+                                                              const DevScalars *__restrict__ sc) {
+    if (sc->overflow) return;
+    const long long m = sc->nslots + 1;
+    const long long base = (long long)blockIdx.x * kScanTile;
+    if (base >= m) return;
+    uint32_t s = 0;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        const long long i = base + (long long)k * kScanThreads + threadIdx.x;
+        if (i < m) s += cnt[i];
+    }
+    uint32_t tot;
+    block_excl_scan(s, &tot);
+    if (threadIdx.x == 0) bsum[blockIdx.x] = tot;
+}
+
+// One block scans the block sums (exclusive, in place).
+__global__ void __launch_bounds__(1024) k_scan_top(uint32_t *__restrict__ bsum,
+                                                   const DevScalars *__restrict__ sc) {
+    if (sc->overflow) return;
+    const long long m = sc->nslots + 1;
+    const long long nb = (m + kScanTile - 1) / kScanTile;
+    const long long per = (nb + blockDim.x - 1) / blockDim.x;
+    const long long b0 = threadIdx.x * per;
+    uint32_t s = 0;
+    for (long long b = b0; b < b0 + per && b < nb; ++b) s += bsum[b];
+    uint32_t tot;
+    uint32_t run = block_excl_scan(s, &tot);
+    for (long long b = b0; b < b0 + per && b < nb; ++b) {
+        const uint32_t v = bsum[b];
+        bsum[b] = run;
+        run += v;
+    }
+}
+
+__global__ void __launch_bounds__(kScanThreads) k_scan_apply(uint32_t *__restrict__ cnt,
+                                                             const uint32_t *__restrict__ bsum,
+                                                             const DevScalars *__restrict__ sc) {
+    if (sc->overflow) return;
+    const long long m = sc->nslots + 1;
+    const long long base = (long long)blockIdx.x * kScanTile;
+    if (base >= m) return;
+    // thread t owns items base + t*8 .. +7 (contiguous)
+    uint32_t v[kScanItems];
+    const long long i0 = base + (long long)threadIdx.x * kScanItems;
+    uint32_t s = 0;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        v[k] = (i0 + k < m) ? cnt[i0 + k] : 0u;
+        s += v[k];
+    }
+    uint32_t tot;
+    uint32_t run = block_excl_scan(s, &tot) + bsum[blockIdx.x];
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        if (i0 + k < m) cnt[i0 + k] = run;
+        run += v[k];
+    }
+}
+
+// ============================================================== a4: scatter + order + gather
+__global__ void __launch_bounds__(256) k_scatter(int64_t n, const uint32_t *__restrict__ key,
+                                                 const uint32_t *__restrict__ rank,
+                                                 const uint32_t *__restrict__ box_start,
+                                                 const uint32_t *__restrict__ id,
+                                                 uint32_t *__restrict__ perm_tmp,
+                                                 uint32_t *__restrict__ skey,
+                                                 uint32_t *__restrict__ sid,
+                                                 const DevScalars *__restrict__ sc) {
+    if (sc->overflow) return;
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t k = key[i];
+    const uint32_t slot = box_start[k] + rank[i];
+    perm_tmp[slot] = (uint32_t)i;
+    skey[slot] = k;
+    sid[slot] = id[i];
+}
+
+// Slot s of the scatter holds an agent of box k in arbitrary order; its final slot
+// is box_start[k] + #(agents of box k with a smaller id).  Gathers the SoA there.
+__global__ void __launch_bounds__(256) k_fix_gather(
+    int64_t n, const uint32_t *__restrict__ skey, const uint32_t *__restrict__ sid,
+    const uint32_t *__restrict__ perm_tmp, const uint32_t *__restrict__ box_start,
+    const double *__restrict__ x, const double *__restrict__ y, const double *__restrict__ z,
+    const double *__restrict__ d, const uint32_t *__restrict__ flags, double *__restrict__ sx,
+    double *__restrict__ sy, double *__restrict__ sz, double *__restrict__ sd,
+    uint32_t *__restrict__ sidf, uint32_t *__restrict__ sflags, uint32_t *__restrict__ perm,
+    const DevScalars *__restrict__ sc) {
+    if (sc->overflow) return;
+    const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (s >= n) return;
+    const uint32_t k = skey[s];
+    const uint32_t lo = box_start[k], hi = box_start[k + 1];
+    const uint32_t me = sid[s];
+    uint32_t r = 0;
+    for (uint32_t t = lo; t < hi; ++t) r += (sid[t] < me);
+    const uint32_t dst = lo + r;
+    const uint32_t src = perm_tmp[s];
+    sx[dst] = x[src];
+    sy[dst] = y[src];
+    sz[dst] = z[src];
+    sd[dst] = d[src];
+    sidf[dst] = me;
+    sflags[dst] = flags[src];
+    perm[dst] = src;
+}
+
+bdm_status launch_grid_sort(Ctx *c, const bdm_agents *a, cudaStream_t st) {
+    const int64_t n = a->n;
+    const int threads = 256;
+    const unsigned nb = (unsigned)((n + threads - 1) / threads);
+    {
+        int64_t zb = (c->slot_cap + 1 + 1023) / 1024;
+        const int64_t maxb = (int64_t)c->sm_count * 16;
+        if (zb > maxb) zb = maxb;
+        k_zero_counts<<<(unsigned)zb, 1024, 0, st>>>(c->box_start, c->sc);
+    }
+    k_key<<<nb, threads, 0, st>>>(n, a->x, a->y, a->z, c->sc, c->key, c->rank, c->box_start);
+    const unsigned sb = (unsigned)((c->slot_cap + 1 + kScanTile - 1) / kScanTile);
+    k_scan_reduce<<<sb, kScanThreads, 0, st>>>(c->box_start, c->block_sums, c->sc);
+    k_scan_top<<<1, 1024, 0, st>>>(c->block_sums, c->sc);
+    k_scan_apply<<<sb, kScanThreads, 0, st>>>(c->box_start, c->block_sums, c->sc);
+    k_scatter<<<nb, threads, 0, st>>>(n, c->key, c->rank, c->box_start, a->id, c->perm_tmp,
+                                      c->skey, c->sid, c->sc);
+    k_fix_gather<<<nb, threads, 0, st>>>(n, c->skey, c->sid, c->perm_tmp, c->box_start, a->x,
+                                         a->y, a->z, a->diameter, a->flags, c->sx, c->sy, c->sz,
+                                         c->sd, c->sidf, c->sflags, c->perm, c->sc);
+    c->launches += 7;
+    BDM_LAUNCH_CHECK("grid sort");
+    return BDM_OK;
+}
+
+int64_t scan_block_count(int64_t slot_cap) { return (slot_cap + 1 + kScanTile - 1) / kScanTile; }
+
+}  // namespace bdm

@@ -1,0 +1,254 @@
+"""GPU parity: libbdm.so (through the C ABI) against the CPU oracle, same seeded inputs.
+
+Bar (BASELINE.json north_star): neighbour pair sets, ids, order and flags bit-exact;
+fp64 positions within 1e-9 relative -- the canonical summation order and fma sites
+(R9) make them bit-exact, which is what these tests assert first.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+REL_TOL = 1e-9  # north_star tolerance for fp64 positions
+
+
+@pytest.fixture(scope="module")
+def eng():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_2503_10796_b200 import Engine
+    e = Engine(0, 1 << 16)
+    yield e
+    e.close()
+
+
+def gpu_init(eng, cfg, n=None, capacity=None):
+    from paper_2503_10796_b200 import Agents
+    n = cfg.n if n is None else n
+    a = Agents.empty(max(capacity or n, 1))
+    eng.init_spheres(a, n, seed=cfg.seed, side=cfg.side, d_lo=cfg.d_lo, d_width=cfg.d_width,
+                     d_random=cfg.d_random)
+    return a
+
+
+def orc_init(orc, cfg, n=None):
+    n = cfg.n if n is None else n
+    return orc.init_spheres(n, cfg.seed, cfg.side, cfg.d_lo, cfg.d_width, cfg.d_random)
+
+
+def params_pair(orc, cfg, **over):
+    from paper_2503_10796_b200 import Params
+    kw = dict(k=cfg.k, gamma=cfg.gamma, dt=cfg.dt, max_disp=cfg.max_disp,
+              force_threshold=cfg.force_threshold, detect_static=cfg.detect_static)
+    kw.update(over)
+    gp = Params(k=kw["k"], gamma=kw["gamma"], dt=kw["dt"], max_displacement=kw["max_disp"],
+                force_threshold=kw["force_threshold"], detect_static=kw["detect_static"],
+                boundary=kw.get("boundary", 0), lo=kw.get("lo", (0, 0, 0)),
+                hi=kw.get("hi", (0, 0, 0)), collect_stats=True)
+    op = orc.mech_params(k=kw["k"], gamma=kw["gamma"], dt=kw["dt"], max_disp=kw["max_disp"],
+                         force_threshold=kw["force_threshold"],
+                         detect_static=kw["detect_static"], boundary=kw.get("boundary", 0),
+                         lo=kw.get("lo", (0, 0, 0)), hi=kw.get("hi", (0, 0, 0)))
+    return gp, op
+
+
+def assert_state_equal(g, o, what=""):
+    """g: GPU state (sorted order), o: oracle state (oracle's sorted order)."""
+    assert np.array_equal(g["id"], o["id"]), f"{what}: agent order/ids differ"
+    assert np.array_equal(g["flags"], o["flags"]), f"{what}: flags differ"
+    assert np.array_equal(g["d"], o["d"]), f"{what}: diameters differ"
+    for k in ("x", "y", "z"):
+        if not np.array_equal(g[k], o[k]):
+            rel = np.abs(g[k] - o[k]) / np.maximum(np.abs(o[k]), 1e-300)
+            assert rel.max() <= REL_TOL, f"{what}: {k} rel err {rel.max()}"
+            pytest.fail(f"{what}: {k} not bit-exact (max rel {rel.max():.3g}, within 1e-9)")
+
+
+def test_init_bit_exact_vs_oracle(eng, orc):
+    for cfg, n in ((W.CFG1, 4096), (W.CFG2, 100_003)):
+        a = gpu_init(eng, cfg, n)
+        g = a.numpy()
+        o = orc_init(orc, cfg, n)
+        for k in ("x", "y", "z", "d", "id", "flags"):
+            assert np.array_equal(g[k], o[k]), (cfg.name, k)
+
+
+def test_cfg1_trajectory_bit_exact(eng, orc):
+    """configs[0]: 4,096 agents, 10 steps, full state after every step."""
+    cfg = W.CFG1
+    a = gpu_init(eng, cfg)
+    o = orc_init(orc, cfg)
+    gp, op = params_pair(orc, cfg)
+    for t in range(cfg.steps):
+        eng.step(a, gp)
+        st = eng.stats()
+        o, cnt = orc.step_full(o, op)
+        assert_state_equal(a.numpy(), o, f"cfg1 step {t}")
+        for k in ("cand", "nbr", "cont", "n_static"):
+            assert st[k] == cnt[k], (t, k, st[k], cnt[k])
+
+
+def test_neighbor_pairs_equal_bruteforce(eng, orc):
+    from paper_2503_10796_b200 import Agents
+    cfg = W.CFG1
+    o = orc_init(orc, cfg)
+    for t in range(3):
+        a = Agents.from_numpy(o)
+        got = eng.neighbor_pairs(a)
+        want = orc.neighbor_pairs_brute(o, float(o["d"].max()))
+        assert np.array_equal(got, want)
+        o, _ = orc.step_full(o, orc.mech_params())
+    # ragged sizes, several densities, explicit radius
+    for n, side, R in ((1, 10.0, 0.0), (2, 5.0, 0.0), (777, 60.0, 0.0), (5000, 90.0, 7.5)):
+        s = orc.init_spheres(n, 3, side, 8.0, 4.0, True)
+        a = Agents.from_numpy(s)
+        got = eng.neighbor_pairs(a, R)
+        want = orc.neighbor_pairs_brute(s, R if R > 0 else float(s["d"].max()))
+        assert np.array_equal(got, want), n
+
+
+@pytest.mark.parametrize("n", [1, 2, 31, 257, 20_011])
+def test_cfg2_mix_reduced_n_static_on(eng, orc, n):
+    """cfg2 density and diameter mix at reduced N (spans many tiles + a ragged tail)."""
+    cfg = W.cfg2_scaled(n)
+    a = gpu_init(eng, cfg)
+    o = orc_init(orc, cfg)
+    gp, op = params_pair(orc, cfg)
+    for t in range(4):
+        eng.step(a, gp)
+        st = eng.stats()
+        o, cnt = orc.step_full(o, op)
+        assert_state_equal(a.numpy(), o, f"n={n} step {t}")
+        assert (st["cand"], st["nbr"], st["cont"], st["n_static"]) == (
+            cnt["cand"], cnt["nbr"], cnt["cont"], cnt["n_static"])
+
+
+@pytest.mark.parametrize("side,tau", [(160.0, 1e-3), (640.0, 0.0)])
+def test_static_skip_fires_and_matches_oracle(eng, orc, side, tau):
+    """Static skip on: bit-exact vs the oracle, and transparent vs skip off."""
+    cfg = W.CFG1
+    a_on = gpu_init(eng, cfg)
+    eng.init_spheres(a_on, cfg.n, seed=1, side=side, d_lo=10.0)
+    a_off = gpu_init(eng, cfg)
+    eng.init_spheres(a_off, cfg.n, seed=1, side=side, d_lo=10.0)
+    o = orc.init_spheres(cfg.n, 1, side, 10.0)
+    gp_on, op_on = params_pair(orc, cfg, detect_static=True, force_threshold=tau)
+    gp_off, _ = params_pair(orc, cfg, detect_static=False, force_threshold=tau)
+    n_static = 0
+    for t in range(8):
+        eng.step(a_on, gp_on)
+        n_static += eng.stats()["n_static"]
+        eng.step(a_off, gp_off)
+        o, _ = orc.step_full(o, op_on)
+        g_on = a_on.numpy()
+        assert_state_equal(g_on, o, f"static on step {t}")
+        g_off = a_off.numpy()
+        assert np.array_equal(g_on["id"], g_off["id"])
+        for k in ("x", "y", "z"):
+            assert np.array_equal(g_on[k], g_off[k])
+    assert n_static > 100
+
+
+def test_edge_cases(eng, orc):
+    from paper_2503_10796_b200 import Agents, Params
+    # n = 0: valid no-op
+    a = Agents.empty(4)
+    a.n = 0
+    eng.step(a, Params())
+    # all agents in one box; coincident centres (dist = 0 contributes nothing, R10)
+    s = {"x": np.array([1.0, 1.0, 1.5, 2.0]), "y": np.array([0.0, 0.0, 0.5, 0.25]),
+         "z": np.zeros(4), "d": np.full(4, 10.0), "id": np.arange(4, dtype=np.uint32),
+         "flags": np.full(4, 4, np.uint32)}
+    a = Agents.from_numpy(s)
+    gp, op = params_pair(orc, W.CFG1)
+    eng.step(a, gp)
+    o, _ = orc.step_full(s, op)
+    assert_state_equal(a.numpy(), o, "one box")
+    # heavy overlap with a large dt: the 3 um cap binds (R6)
+    s = orc.init_spheres(3000, 2, 40.0, 10.0)
+    a = Agents.from_numpy(s)
+    gp, op = params_pair(orc, W.CFG1, dt=1.0)
+    eng.step(a, gp)
+    o, _ = orc.step_full(s, op)
+    assert_state_equal(a.numpy(), o, "cap")
+    # closed boundary (clamp into [lo, hi])
+    s = orc.init_spheres(2000, 4, 50.0, 10.0)
+    a = Agents.from_numpy(s)
+    gp, op = params_pair(orc, W.CFG1, dt=1.0, boundary=1, lo=(5, 5, 5), hi=(45, 45, 45))
+    eng.step(a, gp)
+    o, _ = orc.step_full(s, op)
+    assert_state_equal(a.numpy(), o, "closed")
+
+
+def test_capacity_overflow_is_recovered(eng, orc):
+    """An agent far outside the first grid's extent exceeds the slot capacity; the
+    overflowed step is a no-op and the binding grows the slots and re-issues it."""
+    from paper_2503_10796_b200 import Agents, Engine
+    e = Engine(0, 16)
+    s = orc.init_spheres(500, 5, 50.0, 10.0)
+    a = Agents.from_numpy(s)
+    gp, op = params_pair(orc, W.CFG1)
+    e.step(a, gp)
+    s1, _ = orc.step_full(s, op)
+    s1 = {k: v.copy() for k, v in s1.items()}
+    s1["x"][0] += 5000.0
+    a = Agents.from_numpy(s1)
+    e.step(a, gp)
+    o, _ = orc.step_full(s1, op)
+    assert_state_equal(a.numpy(), o, "after regrow")
+    e.close()
+
+
+def test_step_host_equals_device_step(eng, orc):
+    import torch
+    from paper_2503_10796_b200 import Agents
+    cfg = W.cfg2_scaled(50_000)
+    o = orc_init(orc, cfg)
+    hin = Agents.empty(cfg.n, pin=True)
+    hout = Agents.empty(cfg.n, pin=True)
+    for k, src in (("x", "x"), ("y", "y"), ("z", "z"), ("diameter", "d")):
+        getattr(hin, k).copy_(torch.from_numpy(o[src]))
+    hin.id.copy_(torch.from_numpy(o["id"].view(np.int32)))
+    hin.flags.copy_(torch.from_numpy(o["flags"].view(np.int32)))
+    hin.n = cfg.n
+    dev = Agents.empty(cfg.n)
+    gp, op = params_pair(orc, cfg)
+    eng.step_host(hin, hout, dev, gp)
+    want, _ = orc.step_full(o, op)
+    got = {"x": hout.x.numpy(), "y": hout.y.numpy(), "z": hout.z.numpy(),
+           "d": hout.diameter.numpy(), "id": hout.id.numpy().view(np.uint32),
+           "flags": hout.flags.numpy().view(np.uint32)}
+    assert_state_equal(got, want, "step_host")
+
+
+@pytest.mark.slow
+def test_cfg2_full_size_teacher_forced(eng, orc):
+    """configs[1] at full size (10M agents), the bench's launch configuration: after
+    steps 0 and 1, 100k sampled agents recomputed by the oracle from the GPU's input
+    state (teacher forcing) must match bit-exactly."""
+    import torch
+    cfg = W.CFG2
+    a = gpu_init(eng, cfg)
+    gp, op = params_pair(orc, cfg)
+    rng = np.random.default_rng(0)
+    for t in range(2):
+        before = a.numpy()
+        eng.step(a, gp)
+        after = a.numpy()
+        sample = rng.choice(cfg.n, 100_000, replace=False)
+        out, cnt = orc.mech_step(before, op, sample=sample)
+        pos = {int(i): k for k, i in enumerate(after["id"])}
+        idx = np.array([pos[int(before["id"][i])] for i in sample])
+        for k in ("x", "y", "z", "flags"):
+            g = after[k][idx]
+            assert np.array_equal(g, out[k]), (t, k)
+        # the order is the oracle's sorted order of the input state
+        perm, _ = orc.sorted_order(before)
+        assert np.array_equal(after["id"], before["id"][perm])
+        del before, after
+        torch.cuda.empty_cache()

@@ -1,0 +1,62 @@
+"""Workload presets (BASELINE.json configs) shared by tests, bench.py and smoke().
+
+Pure configuration: sizes, parameters, seeds and the cube side that gives the stated
+volume fraction.  It holds none of the method's arithmetic (no force, no grid, no
+RNG); each side (oracle/ and the CUDA library) generates the population itself from
+the per-id Philox recipe of DESIGN.md section 5.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, asdict
+
+
+def side_for_fraction(n: int, mean_d3: float, phi: float) -> float:
+    """Cube side such that n spheres with E[d^3] = mean_d3 fill a volume fraction phi."""
+    return (n * (math.pi / 6.0) * mean_d3 / phi) ** (1.0 / 3.0)
+
+
+@dataclass(frozen=True)
+class MechConfig:
+    name: str
+    n: int
+    side: float
+    d_lo: float
+    d_width: float          # d = d_lo + d_width*u (d_random) else d = d_lo
+    d_random: bool
+    steps: int
+    detect_static: bool
+    seed: int = 1
+    dt: float = 0.01
+    max_disp: float = 3.0
+    k: float = 2.0
+    gamma: float = 1.0
+    force_threshold: float = 0.0
+
+    def to_dict(self):
+        return asdict(self)
+
+
+# configs[0]: 4,096 spheres, d = 10 um, 160 um cube, R = max d, dt = 0.01, cap 3 um,
+# 10 steps, seed 1, mechanics only (static skip off; R25).
+CFG1 = MechConfig("cfg1", 4096, 160.0, 10.0, 0.0, False, 10, False)
+
+# configs[1]: 10M spheres, d ~ U[8,12] um (E[d^3] = 1040 um^3), cube for 50 % volume
+# fraction (side 2216.6 um), static-agent skip on, 100 steps on 1 GPU.
+CFG2_MEAN_D3 = (12.0**4 - 8.0**4) / (4.0 * 4.0)
+CFG2 = MechConfig("cfg2", 10_000_000, side_for_fraction(10_000_000, CFG2_MEAN_D3, 0.5),
+                  8.0, 4.0, True, 100, True)
+
+
+def cfg2_scaled(n: int) -> MechConfig:
+    """cfg2's density and diameter mix at a smaller agent count (parity-test size)."""
+    return MechConfig(f"cfg2@{n}", n, side_for_fraction(n, CFG2_MEAN_D3, 0.5), 8.0, 4.0, True,
+                      100, True)
+
+
+# configs[4]: 1.7B spheres, d = 10 um, 50 % volume fraction (side 12,119.7 um),
+# x-slab decomposition over 1/2/4/8 GPUs, 10 steps.
+CFG5 = MechConfig("cfg5", 1_700_000_000, side_for_fraction(1_700_000_000, 1000.0, 0.5),
+                  10.0, 0.0, False, 10, False)
+
+PRESETS = {"cfg1": CFG1, "cfg2": CFG2, "cfg5": CFG5}
