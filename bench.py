@@ -179,6 +179,7 @@ def run_ours(args, ws, rank, local):
     torch.cuda.set_device(local)
     cfg = W.PRESETS[args.config]
     eng = Engine(local, cfg.n)
+    eng.set_option("mech_kernel", args.mech_kernel)
     a = Agents.empty(cfg.n)
     stream = torch.cuda.Stream()
     with torch.cuda.stream(stream):
@@ -327,6 +328,7 @@ def main():
     ap.add_argument("--config", default="cfg2", choices=sorted(W.PRESETS))
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--mech-kernel", type=int, default=0, help="0 tile kernel, 1 reference")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     ws, rank, local = dist_env()

@@ -199,6 +199,13 @@ bdm_status bdm_neighbor_pairs(bdm_handle h, const bdm_agents *a, double radius,
                               uint64_t *pairs, int64_t cap, int64_t *count_host,
                               void *stream);
 
+/* Tuning/diagnostic options (host-side, take effect at the next launch):
+ *   "mech_kernel"  0 (default) tile kernel: CTA per 4x4x4-box tile with the halo staged
+ *                  in shared memory and a lane-parallel pair queue;
+ *                  1 per-agent reference kernel reading neighbours from global memory.
+ * Both produce bit-identical results.  Errors: BDM_EINVAL for an unknown name/value. */
+bdm_status bdm_set_option(bdm_handle h, const char *name, int64_t value);
+
 /* Diagnostic: measured fp64 FMA throughput of this GPU (DFMA lane-operations per
  * second, i.e. half the fp64 FLOP/s) and the SM count.  Synchronizing. */
 bdm_status bdm_peak_dfma(bdm_handle h, double *dfma_per_s, int32_t *sm_count);

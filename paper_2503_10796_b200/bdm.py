@@ -24,6 +24,7 @@ EXPORTS = [
     "bdm_create", "bdm_destroy", "bdm_last_error", "bdm_version", "bdm_init_spheres",
     "bdm_grid_build", "bdm_mech_step", "bdm_step", "bdm_step_host", "bdm_sync", "bdm_reserve",
     "bdm_get_stats", "bdm_get_grid_info", "bdm_neighbor_pairs", "bdm_peak_dfma",
+    "bdm_set_option",
 ]
 
 
@@ -94,6 +95,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "bdm_get_grid_info": [P, ctypes.POINTER(CGridInfo)],
         "bdm_neighbor_pairs": [P, AG, dbl, P, i64, ctypes.POINTER(i64), P],
         "bdm_peak_dfma": [P, ctypes.POINTER(dbl), ctypes.POINTER(i32)],
+        "bdm_set_option": [P, ctypes.c_char_p, i64],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -318,6 +320,9 @@ class Engine:
                                              cap, ctypes.byref(cnt), _stream_ptr(stream))
         _check(st)
         return np.sort(buf[:cnt.value].cpu().numpy().view(np.uint64))
+
+    def set_option(self, name: str, value: int):
+        _check(self.lib.bdm_set_option(self.h, name.encode(), int(value)))
 
     def peak_dfma(self):
         v = ctypes.c_double()

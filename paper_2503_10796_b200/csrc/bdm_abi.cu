@@ -331,6 +331,17 @@ bdm_status bdm_neighbor_pairs(bdm_handle h, const bdm_agents *a, double radius, 
     return BDM_OK;
 }
 
+bdm_status bdm_set_option(bdm_handle h, const char *name, int64_t value) {
+    if (!h || !name) return fail(BDM_EINVAL, "NULL argument");
+    Ctx *c = (Ctx *)h;
+    if (strcmp(name, "mech_kernel") == 0) {
+        if (value < 0 || value > 1) return fail(BDM_EINVAL, "mech_kernel must be 0 or 1");
+        c->mech_kernel = (int)value;
+        return BDM_OK;
+    }
+    return fail(BDM_EINVAL, std::string("unknown option ") + name);
+}
+
 bdm_status bdm_peak_dfma(bdm_handle h, double *dfma_per_s, int32_t *sm_count) {
     if (!h || !dfma_per_s || !sm_count) return fail(BDM_EINVAL, "NULL argument");
     Ctx *c = (Ctx *)h;

@@ -70,6 +70,7 @@ struct Ctx {
     const double *grid_x = nullptr;
     int64_t grid_n = 0;
     int64_t launches = 0;  // kernels launched (host-side count)
+    int mech_kernel = 0;   // option "mech_kernel": 0 tile kernel, 1 per-agent reference kernel
 };
 
 // ------------------------------------------------------------------ device helpers

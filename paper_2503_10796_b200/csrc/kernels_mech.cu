@@ -44,140 +44,401 @@ __device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v)
     return v;
 }
 
+// Grid scalars of the current step, read once per thread/CTA.
+struct GridView {
+    double L, R2, o0, o1, o2;
+    int D0, D1, D2, T0, T1, T2;
+};
+__device__ __forceinline__ GridView load_grid(const DevScalars *__restrict__ sc) {
+    GridView g;
+    g.L = sc->L; g.R2 = sc->R2; g.o0 = sc->o[0]; g.o1 = sc->o[1]; g.o2 = sc->o[2];
+    g.D0 = sc->dims[0]; g.D1 = sc->dims[1]; g.D2 = sc->dims[2];
+    g.T0 = sc->T[0]; g.T1 = sc->T[1]; g.T2 = sc->T[2];
+    return g;
+}
+
+struct Counts {
+    uint32_t cand = 0, nbr = 0, cont = 0, stat = 0, moved = 0;
+};
+
+// a8 + a9 + write-back for one agent (shared by both kernels).
+__device__ __forceinline__ void finish_agent(const MechArgs &A, int64_t s, double xi, double yi,
+                                             double zi, double Fx, double Fy, double Fz,
+                                             bool is_static, int nnz, Counts &c) {
+    double Dx = 0.0, Dy = 0.0, Dz = 0.0;
+    if (!is_static) {
+        const double F2 = Fx * Fx + Fy * Fy + Fz * Fz;
+        if (F2 > A.tau * A.tau) {
+            Dx = A.dt * Fx;
+            Dy = A.dt * Fy;
+            Dz = A.dt * Fz;
+            const double n2 = Dx * Dx + Dy * Dy + Dz * Dz;
+            if (n2 > A.max_disp * A.max_disp) {
+                const double scale = A.max_disp / sqrt(n2);
+                Dx = Dx * scale;
+                Dy = Dy * scale;
+                Dz = Dz * scale;
+            }
+        }
+    }
+    double nx = xi + Dx, ny = yi + Dy, nz = zi + Dz;
+    if (A.boundary == 1) {
+        nx = nx < A.lo0 ? A.lo0 : (nx > A.hi0 ? A.hi0 : nx);
+        ny = ny < A.lo1 ? A.lo1 : (ny > A.hi1 ? A.hi1 : ny);
+        nz = nz < A.lo2 ? A.lo2 : (nz > A.hi2 ? A.hi2 : nz);
+    }
+    const bool moved = (Dx != 0.0 || Dy != 0.0 || Dz != 0.0);
+    c.moved += moved ? 1u : 0u;
+    c.stat += is_static ? 1u : 0u;
+    A.ox[s] = nx;
+    A.oy[s] = ny;
+    A.oz[s] = nz;
+    A.od[s] = A.sd[s];
+    A.oid[s] = A.sid[s];
+    A.oflags[s] = (moved ? BDM_FLAG_MOVED : 0u) | (is_static ? BDM_FLAG_STATIC : 0u) |
+                  ((uint32_t)nnz << BDM_FLAG_NNZ_SHIFT);
+}
+
+// The whole step for agent s of the sorted order, reading neighbours from global
+// memory (the reference formulation; used by k_mech and as the tile kernel's
+// fallback for over-full tiles).
+__device__ void mech_agent_global(const MechArgs &A, const GridView &g, int64_t s, Counts &c) {
+    const double xi = A.sx[s], yi = A.sy[s], zi = A.sz[s], di = A.sd[s];
+    const uint32_t fi = A.sflags[s];
+    const double ri = di * 0.5;
+    const int bx = (int)floor((xi - g.o0) / g.L);
+    const int by = (int)floor((yi - g.o1) / g.L);
+    const int bz = (int)floor((zi - g.o2) / g.L);
+    const int nnz_in = (int)((fi >> BDM_FLAG_NNZ_SHIFT) & 3u);
+
+    // ---- a5: static classification (pull test over the neighbours' flags)
+    bool is_static = false;
+    if (A.detect_static && !(fi & kChanged) && nnz_in <= 1) {
+        is_static = true;
+        for (int dz = -1; dz <= 1 && is_static; ++dz) {
+            const int cz = bz + dz;
+            if (cz < 0 || cz >= g.D2) continue;
+            for (int dy = -1; dy <= 1 && is_static; ++dy) {
+                const int cy = by + dy;
+                if (cy < 0 || cy >= g.D1) continue;
+                for (int dx = -1; dx <= 1 && is_static; ++dx) {
+                    const int cx = bx + dx;
+                    if (cx < 0 || cx >= g.D0) continue;
+                    const uint32_t key = box_key(cx, cy, cz, g.T0, g.T1);
+                    const uint32_t b0 = A.box_start[key], b1 = A.box_start[key + 1];
+                    for (uint32_t t = b0; t < b1; ++t) {
+                        if (t == (uint32_t)s) continue;
+                        const double ex = xi - A.sx[t], ey = yi - A.sy[t], ez = zi - A.sz[t];
+                        const double D = fma(ez, ez, fma(ey, ey, ex * ex));
+                        if (D <= g.R2 && (A.sflags[t] & kChanged)) {
+                            is_static = false;
+                            break;
+                        }
+                    }
+                }
+            }
+        }
+    }
+    double Fx = 0.0, Fy = 0.0, Fz = 0.0;
+    int nnz = nnz_in;
+    if (!is_static) {
+        // ---- a6 + a7: canonical order (dz, dy, dx), ascending id in a box
+        nnz = 0;
+        for (int dz = -1; dz <= 1; ++dz) {
+            const int cz = bz + dz;
+            if (cz < 0 || cz >= g.D2) continue;
+            for (int dy = -1; dy <= 1; ++dy) {
+                const int cy = by + dy;
+                if (cy < 0 || cy >= g.D1) continue;
+                for (int dx = -1; dx <= 1; ++dx) {
+                    const int cx = bx + dx;
+                    if (cx < 0 || cx >= g.D0) continue;
+                    const uint32_t key = box_key(cx, cy, cz, g.T0, g.T1);
+                    const uint32_t b0 = A.box_start[key], b1 = A.box_start[key + 1];
+                    for (uint32_t t = b0; t < b1; ++t) {
+                        if (t == (uint32_t)s) continue;
+                        ++c.cand;
+                        const double ex = xi - A.sx[t], ey = yi - A.sy[t], ez = zi - A.sz[t];
+                        const double D = fma(ez, ez, fma(ey, ey, ex * ex));
+                        if (!(D <= g.R2)) continue;
+                        ++c.nbr;
+                        const double dist = sqrt(D);
+                        const double rj = A.sd[t] * 0.5;
+                        const double delta = (ri + rj) - dist;
+                        if (!(delta > 0.0 && dist > 0.0)) continue;
+                        ++c.cont;
+                        const double rbar = (ri * rj) / (ri + rj);
+                        const double Fn = A.k * delta - A.gamma * sqrt(rbar * delta);
+                        const double sc_ = Fn / dist;
+                        Fx = fma(sc_, ex, Fx);
+                        Fy = fma(sc_, ey, Fy);
+                        Fz = fma(sc_, ez, Fz);
+                        if (Fn != 0.0 && nnz < 2) ++nnz;
+                    }
+                }
+            }
+        }
+    }
+    finish_agent(A, s, xi, yi, zi, Fx, Fy, Fz, is_static, nnz, c);
+}
+
+template <bool kStats>
+__device__ __forceinline__ void flush_counts(const Counts &c, DevScalars *sc) {
+    if (!kStats) return;
+    const unsigned long long a = warp_sum_u64(c.cand), b = warp_sum_u64(c.nbr),
+                             d = warp_sum_u64(c.cont), e = warp_sum_u64(c.stat),
+                             f = warp_sum_u64(c.moved);
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(&sc->stats[0], a);
+        atomicAdd(&sc->stats[1], b);
+        atomicAdd(&sc->stats[2], d);
+        atomicAdd(&sc->stats[3], e);
+        atomicAdd(&sc->stats[4], f);
+    }
+}
+
+// Thread per agent over global memory (reference formulation).
 template <bool kStats>
 __global__ void __launch_bounds__(256) k_mech(MechArgs A, DevScalars *__restrict__ sc) {
     if (sc->overflow) return;
+    const GridView g = load_grid(sc);
+    Counts c;
     const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    const bool live = s < A.n;
-    uint32_t c_cand = 0, c_nbr = 0, c_cont = 0, c_static = 0, c_moved = 0;
-    if (live) {
-        const double L = sc->L, R2 = sc->R2;
-        const double o0 = sc->o[0], o1 = sc->o[1], o2 = sc->o[2];
-        const int D0 = sc->dims[0], D1 = sc->dims[1], D2 = sc->dims[2];
-        const int T0 = sc->T[0], T1 = sc->T[1];
-        const double xi = A.sx[s], yi = A.sy[s], zi = A.sz[s], di = A.sd[s];
-        const uint32_t fi = A.sflags[s];
-        const double ri = di * 0.5;
-        const int bx = (int)floor((xi - o0) / L);
-        const int by = (int)floor((yi - o1) / L);
-        const int bz = (int)floor((zi - o2) / L);
-        const int nnz_in = (int)((fi >> BDM_FLAG_NNZ_SHIFT) & 3u);
+    if (s < A.n) mech_agent_global(A, g, s, c);
+    flush_counts<kStats>(c, sc);
+}
 
-        // ---- a5: static classification (pull test over the neighbours' flags)
-        bool is_static = false;
-        if (A.detect_static && !(fi & kChanged) && nnz_in <= 1) {
-            is_static = true;
-            for (int dz = -1; dz <= 1 && is_static; ++dz) {
-                const int cz = bz + dz;
-                if (cz < 0 || cz >= D2) continue;
-                for (int dy = -1; dy <= 1 && is_static; ++dy) {
-                    const int cy = by + dy;
-                    if (cy < 0 || cy >= D1) continue;
-                    for (int dx = -1; dx <= 1 && is_static; ++dx) {
-                        const int cx = bx + dx;
-                        if (cx < 0 || cx >= D0) continue;
-                        const uint32_t key = box_key(cx, cy, cz, T0, T1);
-                        const uint32_t b0 = A.box_start[key], b1 = A.box_start[key + 1];
-                        for (uint32_t t = b0; t < b1; ++t) {
-                            if (t == (uint32_t)s) continue;
-                            const double ex = xi - A.sx[t], ey = yi - A.sy[t], ez = zi - A.sz[t];
-                            const double D = fma(ez, ez, fma(ey, ey, ex * ex));
-                            if (D <= R2 && (A.sflags[t] & kChanged)) {
-                                is_static = false;
-                                break;
+// ============================================================== tile kernel
+// One CTA per 4x4x4-box tile (persistent, strided over tiles).  The 6x6x6 boxes of
+// the tile and its one-box halo are staged in shared memory in row-major box order
+// (z, y, x), ids ascending inside a box.  In that order an agent's 27 neighbour boxes
+// form 9 contiguous runs (one per (dz, dy)), visited in exactly the canonical order
+// of R9, and "canonical order" == "ascending staged index".
+//   phase 1  each lane scans its 9 runs (exact fp64 test D <= R^2) and appends its
+//            neighbours to a warp queue (and remembers their queue slots in order)
+//   phase 2  the warp evaluates Eq. 4.1 for the queued pairs lane-parallel (the
+//            sqrt/div-heavy part, no divergence between agents)
+//   phase 3  each lane accumulates its own contacts in canonical order with fma
+constexpr int kTileThreads = 128;
+constexpr int kTileWarps = kTileThreads / 32;
+constexpr int kMMax = 512;   // staged agents per CTA (6^3 boxes)
+constexpr int kQCap = 448;   // neighbour pairs queued per warp
+constexpr int kKMax = 24;    // neighbours per agent in the queue
+
+struct TileSmem {
+    uint32_t start[216];
+    uint32_t off[217];
+    double X[kMMax], Y[kMMax], Z[kMMax], Rr[kMMax];
+    uint32_t F[kMMax];
+    double qv[kTileWarps][kQCap];
+    uint32_t qm[kTileWarps][kQCap];
+    uint16_t lidx[kTileWarps][kKMax][32];
+    uint16_t mi[kTileWarps][32];
+    uint8_t stat[kTileWarps][32];
+    int qcnt[kTileWarps];
+};
+
+__device__ __forceinline__ int warp_append(int *counter) {
+    const unsigned act = __activemask();
+    const int lane = threadIdx.x & 31;
+    const int leader = __ffs(act) - 1;
+    int base = 0;
+    if (lane == leader) base = atomicAdd(counter, __popc(act));
+    base = __shfl_sync(act, base, leader);
+    return base + __popc(act & ((1u << lane) - 1u));
+}
+
+template <bool kStats>
+__global__ void __launch_bounds__(kTileThreads) k_mech_tile(MechArgs A, DevScalars *__restrict__ sc) {
+    if (sc->overflow) return;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    TileSmem &S = *reinterpret_cast<TileSmem *>(smem_raw);
+    const GridView g = load_grid(sc);
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const long long ntiles = (long long)g.T0 * g.T1 * g.T2;
+    Counts c;
+
+    for (long long t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int tx = (int)(t % g.T0), ty = (int)((t / g.T0) % g.T1), tz = (int)(t / ((long long)g.T0 * g.T1));
+        const int bx0 = 4 * tx - 1, by0 = 4 * ty - 1, bz0 = 4 * tz - 1;
+        const uint32_t g0 = A.box_start[(uint32_t)t * 64u], g1 = A.box_start[(uint32_t)t * 64u + 64u];
+        const int nc = (int)(g1 - g0);
+        if (nc == 0) continue;  // uniform across the CTA
+        // ---- box table of the 6^3 region (out-of-grid boxes are empty)
+        for (int lb = tid; lb < 216; lb += kTileThreads) {
+            const int gx = bx0 + lb % 6, gy = by0 + (lb / 6) % 6, gz = bz0 + lb / 36;
+            uint32_t st = 0, cnt = 0;
+            if (gx >= 0 && gy >= 0 && gz >= 0 && gx < g.D0 && gy < g.D1 && gz < g.D2) {
+                const uint32_t key = box_key(gx, gy, gz, g.T0, g.T1);
+                st = A.box_start[key];
+                cnt = A.box_start[key + 1] - st;
+            }
+            S.start[lb] = st;
+            S.off[lb] = cnt;
+        }
+        __syncthreads();
+        if (w == 0) {  // exclusive scan of the 216 counts (7 per lane)
+            uint32_t v[7], sum = 0;
+#pragma unroll
+            for (int k = 0; k < 7; ++k) {
+                const int lb = lane * 7 + k;
+                v[k] = lb < 216 ? S.off[lb] : 0u;
+                sum += v[k];
+            }
+            uint32_t inc = sum;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+                if (lane >= o) inc += y;
+            }
+            uint32_t run = inc - sum;
+#pragma unroll
+            for (int k = 0; k < 7; ++k) {
+                const int lb = lane * 7 + k;
+                if (lb <= 216) S.off[lb] = run;
+                run += v[k];
+            }
+        }
+        __syncthreads();
+        const int M = (int)S.off[216];
+        if (M > kMMax) {
+            // over-full tile: reference formulation straight from global memory
+            for (int k = tid; k < nc; k += kTileThreads) mech_agent_global(A, g, g0 + k, c);
+            __syncthreads();
+            continue;
+        }
+        // ---- stage the region (row-major boxes, ascending id inside a box)
+        for (int m = tid; m < M; m += kTileThreads) {
+            int lo = 0, hi = 216;  // last lb with off[lb] <= m
+            while (hi - lo > 1) {
+                const int mid = (lo + hi) >> 1;
+                if (S.off[mid] <= (uint32_t)m) lo = mid; else hi = mid;
+            }
+            const uint32_t gi = S.start[lo] + ((uint32_t)m - S.off[lo]);
+            S.X[m] = A.sx[gi];
+            S.Y[m] = A.sy[gi];
+            S.Z[m] = A.sz[gi];
+            S.Rr[m] = A.sd[gi] * 0.5;
+            S.F[m] = A.sflags[gi];
+        }
+        if (tid < kTileWarps) S.qcnt[tid] = 0;
+        __syncthreads();
+
+        for (int base = 0; base < nc; base += kTileThreads) {
+            const int k = base + tid;
+            const bool active = k < nc;
+            if (base + w * 32 >= nc) break;  // warp-uniform: no agent left for this warp
+            // ---- own agent
+            int mi = 0, lbi = 0, lcount = 0;
+            double xi = 0.0, yi = 0.0, zi = 0.0;
+            uint32_t fi = 0;
+            bool cand_static = false, changed_nb = false, ovf = false;
+            uint32_t my_cand = 0;
+            if (active) {
+                const uint32_t gk = g0 + (uint32_t)k;
+                xi = A.sx[gk]; yi = A.sy[gk]; zi = A.sz[gk];
+                const int lx = (int)floor((xi - g.o0) / g.L) - bx0;
+                const int ly = (int)floor((yi - g.o1) / g.L) - by0;
+                const int lz = (int)floor((zi - g.o2) / g.L) - bz0;
+                lbi = (lz * 6 + ly) * 6 + lx;
+                mi = (int)(S.off[lbi] + (gk - S.start[lbi]));
+                fi = S.F[mi];
+                cand_static = A.detect_static && !(fi & kChanged) &&
+                              ((fi >> BDM_FLAG_NNZ_SHIFT) & 3u) <= 1u;
+                // ---- phase 1: 9 runs in canonical order, exact fp64 radius test
+                const double R2 = g.R2;
+#pragma unroll 1
+                for (int r = 0; r < 9; ++r) {
+                    const int lb0 = lbi + ((r / 3 - 1) * 6 + (r % 3 - 1)) * 6 - 1;
+                    const int mend = (int)S.off[lb0 + 3];
+                    for (int m = (int)S.off[lb0]; m < mend; ++m) {
+                        if (m == mi) continue;
+                        ++my_cand;
+                        const double ex = xi - S.X[m], ey = yi - S.Y[m], ez = zi - S.Z[m];
+                        const double D = fma(ez, ez, fma(ey, ey, ex * ex));
+                        if (D <= R2) {
+                            changed_nb |= (S.F[m] & kChanged) != 0u;
+                            const int pos = warp_append(&S.qcnt[w]);
+                            if (pos < kQCap && lcount < kKMax) {
+                                S.qv[w][pos] = D;
+                                S.qm[w][pos] = (uint32_t)m | ((uint32_t)lane << 16);
+                                S.lidx[w][lcount][lane] = (uint16_t)pos;
+                            } else {
+                                ovf = true;
                             }
+                            ++lcount;
                         }
                     }
                 }
             }
-        }
-
-        double Dx = 0.0, Dy = 0.0, Dz = 0.0;
-        int nnz = nnz_in;
-        if (is_static) {
-            c_static = 1;
-        } else {
-            // ---- a6 + a7: canonical order (dz, dy, dx), ascending id in a box
-            double Fx = 0.0, Fy = 0.0, Fz = 0.0;
-            nnz = 0;
-            for (int dz = -1; dz <= 1; ++dz) {
-                const int cz = bz + dz;
-                if (cz < 0 || cz >= D2) continue;
-                for (int dy = -1; dy <= 1; ++dy) {
-                    const int cy = by + dy;
-                    if (cy < 0 || cy >= D1) continue;
-                    for (int dx = -1; dx <= 1; ++dx) {
-                        const int cx = bx + dx;
-                        if (cx < 0 || cx >= D0) continue;
-                        const uint32_t key = box_key(cx, cy, cz, T0, T1);
-                        const uint32_t b0 = A.box_start[key], b1 = A.box_start[key + 1];
-                        for (uint32_t t = b0; t < b1; ++t) {
-                            if (t == (uint32_t)s) continue;
-                            if (kStats) ++c_cand;
-                            const double ex = xi - A.sx[t], ey = yi - A.sy[t], ez = zi - A.sz[t];
-                            const double D = fma(ez, ez, fma(ey, ey, ex * ex));
-                            if (!(D <= R2)) continue;
-                            if (kStats) ++c_nbr;
-                            const double dist = sqrt(D);
-                            const double rj = A.sd[t] * 0.5;
-                            const double delta = (ri + rj) - dist;
-                            if (!(delta > 0.0 && dist > 0.0)) continue;
-                            if (kStats) ++c_cont;
+            const bool is_static = active && cand_static && !changed_nb;
+            S.mi[w][lane] = (uint16_t)mi;
+            S.stat[w][lane] = is_static ? 1 : 0;
+            const bool wovf = __any_sync(0xffffffffu, ovf);
+            __syncwarp();
+            if (wovf) {
+                // queue overflow: this warp's agents take the reference path
+                if (active) mech_agent_global(A, g, g0 + k, c);
+            } else {
+                // ---- phase 2: Eq. 4.1/4.2 for the queued pairs, lane-parallel
+                const int qn = S.qcnt[w];
+                for (int p = lane; p < qn; p += 32) {
+                    const uint32_t meta = S.qm[w][p];
+                    const int m = (int)(meta & 0xFFFFu), owner = (int)(meta >> 16);
+                    uint32_t code = 0;
+                    double sc_ = 0.0;
+                    if (!S.stat[w][owner]) {
+                        const double D = S.qv[w][p];
+                        const double ri = S.Rr[S.mi[w][owner]], rj = S.Rr[m];
+                        const double dist = sqrt(D);
+                        const double delta = (ri + rj) - dist;
+                        if (delta > 0.0 && dist > 0.0) {
                             const double rbar = (ri * rj) / (ri + rj);
                             const double Fn = A.k * delta - A.gamma * sqrt(rbar * delta);
-                            const double sc_ = Fn / dist;
+                            sc_ = Fn / dist;
+                            code = 1u | (Fn != 0.0 ? 2u : 0u);
+                        }
+                    }
+                    S.qv[w][p] = sc_;
+                    S.qm[w][p] = meta | (code << 24);
+                }
+                __syncwarp();
+                // ---- phase 3: ordered accumulation of the own contacts
+                if (active) {
+                    double Fx = 0.0, Fy = 0.0, Fz = 0.0;
+                    int nnz = 0;
+                    uint32_t my_cont = 0;
+                    for (int j = 0; j < lcount; ++j) {
+                        const int p = S.lidx[w][j][lane];
+                        const uint32_t meta = S.qm[w][p];
+                        if (meta & (1u << 24)) {
+                            const int m = (int)(meta & 0xFFFFu);
+                            const double sc_ = S.qv[w][p];
+                            const double ex = xi - S.X[m], ey = yi - S.Y[m], ez = zi - S.Z[m];
                             Fx = fma(sc_, ex, Fx);
                             Fy = fma(sc_, ey, Fy);
                             Fz = fma(sc_, ez, Fz);
-                            if (Fn != 0.0 && nnz < 2) ++nnz;
+                            ++my_cont;
+                            if ((meta & (1u << 25)) && nnz < 2) ++nnz;
                         }
                     }
+                    if (!is_static) {
+                        c.cand += my_cand;
+                        c.nbr += (uint32_t)lcount;
+                        c.cont += my_cont;
+                    } else {
+                        nnz = (int)((fi >> BDM_FLAG_NNZ_SHIFT) & 3u);
+                    }
+                    finish_agent(A, g0 + k, xi, yi, zi, Fx, Fy, Fz, is_static, nnz, c);
                 }
             }
-            // ---- a8: displacement, threshold, cap
-            const double F2 = Fx * Fx + Fy * Fy + Fz * Fz;
-            if (F2 > A.tau * A.tau) {
-                Dx = A.dt * Fx;
-                Dy = A.dt * Fy;
-                Dz = A.dt * Fz;
-                const double n2 = Dx * Dx + Dy * Dy + Dz * Dz;
-                if (n2 > A.max_disp * A.max_disp) {
-                    const double scale = A.max_disp / sqrt(n2);
-                    Dx = Dx * scale;
-                    Dy = Dy * scale;
-                    Dz = Dz * scale;
-                }
-            }
+            __syncwarp();
+            if (lane == 0) S.qcnt[w] = 0;
+            __syncwarp();
         }
-        double nx = xi + Dx, ny = yi + Dy, nz = zi + Dz;
-        // ---- a9: boundary
-        if (A.boundary == 1) {
-            nx = nx < A.lo0 ? A.lo0 : (nx > A.hi0 ? A.hi0 : nx);
-            ny = ny < A.lo1 ? A.lo1 : (ny > A.hi1 ? A.hi1 : ny);
-            nz = nz < A.lo2 ? A.lo2 : (nz > A.hi2 ? A.hi2 : nz);
-        }
-        const bool moved = (Dx != 0.0 || Dy != 0.0 || Dz != 0.0);
-        c_moved = moved ? 1u : 0u;
-        A.ox[s] = nx;
-        A.oy[s] = ny;
-        A.oz[s] = nz;
-        A.od[s] = di;
-        A.oid[s] = A.sid[s];
-        A.oflags[s] = (moved ? BDM_FLAG_MOVED : 0u) | (is_static ? BDM_FLAG_STATIC : 0u) |
-                      ((uint32_t)nnz << BDM_FLAG_NNZ_SHIFT);
+        __syncthreads();  // before the next tile overwrites the staged region
     }
-    if (kStats) {
-        const unsigned long long a = warp_sum_u64(c_cand), b = warp_sum_u64(c_nbr),
-                                 c = warp_sum_u64(c_cont), d = warp_sum_u64(c_static),
-                                 e = warp_sum_u64(c_moved);
-        if ((threadIdx.x & 31) == 0) {
-            atomicAdd(&sc->stats[0], a);
-            atomicAdd(&sc->stats[1], b);
-            atomicAdd(&sc->stats[2], c);
-            atomicAdd(&sc->stats[3], d);
-            atomicAdd(&sc->stats[4], e);
-        }
-    }
+    flush_counts<kStats>(c, sc);
 }
 
 bdm_status launch_mech(Ctx *c, bdm_agents *a, const bdm_params *p, cudaStream_t st) {
@@ -191,12 +452,30 @@ bdm_status launch_mech(Ctx *c, bdm_agents *a, const bdm_params *p, cudaStream_t 
     A.detect_static = p->detect_static; A.boundary = p->boundary;
     A.lo0 = p->lo[0]; A.lo1 = p->lo[1]; A.lo2 = p->lo[2];
     A.hi0 = p->hi[0]; A.hi1 = p->hi[1]; A.hi2 = p->hi[2];
-    const unsigned nb = (unsigned)((a->n + 255) / 256);
-    if (p->collect_stats) {
+    if (p->collect_stats)
         BDM_CUDA_TRY(cudaMemsetAsync(c->sc->stats, 0, sizeof(c->sc->stats), st));
-        k_mech<true><<<nb, 256, 0, st>>>(A, c->sc);
+    const bool tile = c->mech_kernel != 1;
+    if (tile) {
+        static bool attr_set = false;
+        const int smem = (int)sizeof(TileSmem);
+        if (!attr_set) {
+            BDM_CUDA_TRY(cudaFuncSetAttribute(k_mech_tile<true>,
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+            BDM_CUDA_TRY(cudaFuncSetAttribute(k_mech_tile<false>,
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+            attr_set = true;
+        }
+        int per_sm = 0;
+        BDM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+            &per_sm, k_mech_tile<false>, kTileThreads, smem));
+        if (per_sm < 1) per_sm = 1;
+        const unsigned grid = (unsigned)(c->sm_count * per_sm);
+        if (p->collect_stats) k_mech_tile<true><<<grid, kTileThreads, smem, st>>>(A, c->sc);
+        else k_mech_tile<false><<<grid, kTileThreads, smem, st>>>(A, c->sc);
     } else {
-        k_mech<false><<<nb, 256, 0, st>>>(A, c->sc);
+        const unsigned nb = (unsigned)((a->n + 255) / 256);
+        if (p->collect_stats) k_mech<true><<<nb, 256, 0, st>>>(A, c->sc);
+        else k_mech<false><<<nb, 256, 0, st>>>(A, c->sc);
     }
     c->launches += 1;
     BDM_LAUNCH_CHECK("k_mech");

@@ -16,13 +16,15 @@ pytestmark = pytest.mark.gpu
 REL_TOL = 1e-9  # north_star tolerance for fp64 positions
 
 
-@pytest.fixture(scope="module")
-def eng():
+@pytest.fixture(scope="module", params=[0, 1], ids=["tile", "reference"])
+def eng(request):
+    """Both mechanics kernels: the tile kernel (default) and the per-agent reference."""
     import torch
     if not torch.cuda.is_available():
         pytest.skip("no GPU")
     from paper_2503_10796_b200 import Engine
     e = Engine(0, 1 << 16)
+    e.set_option("mech_kernel", request.param)
     yield e
     e.close()
 
@@ -190,6 +192,7 @@ def test_capacity_overflow_is_recovered(eng, orc):
     overflowed step is a no-op and the binding grows the slots and re-issues it."""
     from paper_2503_10796_b200 import Agents, Engine
     e = Engine(0, 16)
+    e.set_option("mech_kernel", eng.lib and 0)
     s = orc.init_spheres(500, 5, 50.0, 10.0)
     a = Agents.from_numpy(s)
     gp, op = params_pair(orc, W.CFG1)
