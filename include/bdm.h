@@ -203,7 +203,9 @@ bdm_status bdm_neighbor_pairs(bdm_handle h, const bdm_agents *a, double radius,
  *   "mech_kernel"  0 (default) tile kernel: CTA per 4x4x4-box tile with the halo staged
  *                  in shared memory and a lane-parallel pair queue;
  *                  1 per-agent reference kernel reading neighbours from global memory.
- * Both produce bit-identical results.  Errors: BDM_EINVAL for an unknown name/value. */
+ *   "prefilter"    1 (default) / 0: conservative fp32 candidate test in the tile kernel
+ *                  (never rejects a neighbour; the exact fp64 test decides).
+ * All settings produce bit-identical results.  Errors: BDM_EINVAL for an unknown name/value. */
 bdm_status bdm_set_option(bdm_handle h, const char *name, int64_t value);
 
 /* Diagnostic: measured fp64 FMA throughput of this GPU (DFMA lane-operations per

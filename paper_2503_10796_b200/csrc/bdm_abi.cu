@@ -339,6 +339,11 @@ bdm_status bdm_set_option(bdm_handle h, const char *name, int64_t value) {
         c->mech_kernel = (int)value;
         return BDM_OK;
     }
+    if (strcmp(name, "prefilter") == 0) {
+        if (value < 0 || value > 1) return fail(BDM_EINVAL, "prefilter must be 0 or 1");
+        c->prefilter = (int)value;
+        return BDM_OK;
+    }
     return fail(BDM_EINVAL, std::string("unknown option ") + name);
 }
 

@@ -71,6 +71,7 @@ struct Ctx {
     int64_t grid_n = 0;
     int64_t launches = 0;  // kernels launched (host-side count)
     int mech_kernel = 0;   // option "mech_kernel": 0 tile kernel, 1 per-agent reference kernel
+    int prefilter = 1;     // option "prefilter": fp32 conservative candidate test in the tile kernel
 };
 
 // ------------------------------------------------------------------ device helpers

@@ -102,7 +102,8 @@ __device__ __forceinline__ void finish_agent(const MechArgs &A, int64_t s, doubl
 // The whole step for agent s of the sorted order, reading neighbours from global
 // memory (the reference formulation; used by k_mech and as the tile kernel's
 // fallback for over-full tiles).
-__device__ void mech_agent_global(const MechArgs &A, const GridView &g, int64_t s, Counts &c) {
+__device__ __forceinline__ void mech_agent_global(const MechArgs &A, const GridView &g, int64_t s,
+                                                  Counts &c) {
     const double xi = A.sx[s], yi = A.sy[s], zi = A.sz[s], di = A.sd[s];
     const uint32_t fi = A.sflags[s];
     const double ri = di * 0.5;
@@ -213,55 +214,110 @@ __global__ void __launch_bounds__(256) k_mech(MechArgs A, DevScalars *__restrict
 // the tile and its one-box halo are staged in shared memory in row-major box order
 // (z, y, x), ids ascending inside a box.  In that order an agent's 27 neighbour boxes
 // form 9 contiguous runs (one per (dz, dy)), visited in exactly the canonical order
-// of R9, and "canonical order" == "ascending staged index".
-//   phase 1  each lane scans its 9 runs (exact fp64 test D <= R^2) and appends its
-//            neighbours to a warp queue (and remembers their queue slots in order)
-//   phase 2  the warp evaluates Eq. 4.1 for the queued pairs lane-parallel (the
-//            sqrt/div-heavy part, no divergence between agents)
-//   phase 3  each lane accumulates its own contacts in canonical order with fma
+// of R9, so "canonical order" == "ascending staged index".
+// The tile's agents are split over ceil(nc/32) warps in equal contiguous shares.
+// Per warp batch (<= 32 agents, one per lane):
+//   phase 1  each lane walks its (non-empty) runs as one flattened loop; the loop trip
+//            count is the warp maximum and the run advance is predicated, so lanes stay
+//            converged.  The test is a conservative fp32 distance check on
+//            region-relative coordinates (never rejects a true neighbour, see below);
+//            survivors go to the lane's own list (no atomics)
+//   phase 2  the lane lists are concatenated in lane order (warp scan); lane-parallel
+//            over the pairs: the exact fp64 test D <= R^2 (R4, R9) decides the
+//            neighbour set, Eq. 4.1/4.2 gives s = F_N/dist (sqrt/div heavy part)
+//   phase 3  each lane accumulates its own pairs in canonical order with fma
+// The prefilter: xr = fl32(x - X0) with X0 the region corner, |x - X0| <= 6L, so each
+// relative coordinate carries <= 2^-24*6L error and a true neighbour (D <= R^2) has
+// D32 <= R^2 (1 + 2.6e-6) for L = R(1+2^-20); the threshold R^2 (1 + 2^-12) has a 90x
+// margin.  Needs |coordinates| / L < 2^30 (checked on device; else the candidate test
+// is done in fp64 directly).
 constexpr int kTileThreads = 128;
 constexpr int kTileWarps = kTileThreads / 32;
-constexpr int kMMax = 512;   // staged agents per CTA (6^3 boxes)
-constexpr int kQCap = 448;   // neighbour pairs queued per warp
-constexpr int kKMax = 24;    // neighbours per agent in the queue
+constexpr int kMMax = 448;   // staged agents per CTA (6^3 boxes)
+constexpr int kQCap = 352;   // surviving pairs per warp batch
+constexpr int kKMax = 24;    // survivors per agent
+constexpr uint32_t kCodeNbr = 1u << 24, kCodeContact = 1u << 25, kCodeNonzero = 1u << 26;
 
 struct TileSmem {
     uint32_t start[216];
     uint32_t off[217];
+    float4 P[kMMax];                        // fp32 region-relative x, y, z
     double X[kMMax], Y[kMMax], Z[kMMax], Rr[kMMax];
     uint32_t F[kMMax];
-    double qv[kTileWarps][kQCap];
-    uint32_t qm[kTileWarps][kQCap];
-    uint16_t lidx[kTileWarps][kKMax][32];
-    uint16_t mi[kTileWarps][32];
-    uint8_t stat[kTileWarps][32];
-    int qcnt[kTileWarps];
+    uint8_t mbox[kMMax];                    // staged index -> local box
+    struct Warp {
+        double qs[kQCap];                  // s = F_N / dist per pair
+        uint32_t pr[kQCap];                // m | agent << 16 | codes
+        uint32_t run[9][32];               // per lane: non-empty runs (start | end << 16)
+        uint16_t lst[kKMax][32];           // per lane: survivors (staged index)
+        uint16_t mi[32];                   // agent -> staged index
+        uint8_t chg[32];                   // agent saw a changed neighbour
+    } W[kTileWarps];
 };
 
-__device__ __forceinline__ int warp_append(int *counter) {
-    const unsigned act = __activemask();
-    const int lane = threadIdx.x & 31;
-    const int leader = __ffs(act) - 1;
-    int base = 0;
-    if (lane == leader) base = atomicAdd(counter, __popc(act));
-    base = __shfl_sync(act, base, leader);
-    return base + __popc(act & ((1u << lane) - 1u));
+template <bool kPF>
+__device__ __forceinline__ int phase1(const TileSmem &S, TileSmem::Warp &Wp, int lane, int mi,
+                                      double xi, double yi, double zi, int ca, int nr,
+                                      int cmax, float R2f, double R2) {
+    // Walks the lane's non-empty runs.  The next run is prefetched into a register, so
+    // the loop-carried chain is only m -> (m == e) -> select; a lane past its last
+    // candidate parks on its own index (masked by it < ca).
+    int cnt = 0, j = 1;
+    const uint32_t v0 = Wp.run[0][lane];
+    uint32_t nxt = Wp.run[1][lane];
+    int m = nr > 0 ? (int)(v0 & 0xFFFFu) : mi, e = nr > 0 ? (int)(v0 >> 16) : mi + 1;
+    const float4 pi = S.P[mi];
+#pragma unroll 2
+    for (int it = 0; it < cmax; ++it) {
+        bool pass;
+        if (kPF) {
+            const float4 q = S.P[m];
+            const float ex = pi.x - q.x, ey = pi.y - q.y, ez = pi.z - q.z;
+            pass = fmaf(ez, ez, fmaf(ey, ey, ex * ex)) <= R2f;
+        } else {
+            const double ex = xi - S.X[m], ey = yi - S.Y[m], ez = zi - S.Z[m];
+            pass = fma(ez, ez, fma(ey, ey, ex * ex)) <= R2;
+        }
+        pass = pass && (m != mi) && (it < ca);
+        // branch-free append: the slot at cnt is scratch until committed
+        Wp.lst[cnt < kKMax ? cnt : kKMax - 1][lane] = (uint16_t)m;
+        cnt += pass ? 1 : 0;
+        // branch-free run advance: next run from the prefetch register, or park
+        ++m;
+        const bool at_end = (m == e), more = j < nr;
+        const int mn = more ? (int)(nxt & 0xFFFFu) : mi;
+        const int en = more ? (int)(nxt >> 16) : mi + 1;
+        m = at_end ? mn : m;
+        e = at_end ? en : e;
+        j += at_end ? 1 : 0;
+        nxt = Wp.run[j < 9 ? j : 8][lane];
+    }
+    return cnt;
 }
 
 template <bool kStats>
-__global__ void __launch_bounds__(kTileThreads) k_mech_tile(MechArgs A, DevScalars *__restrict__ sc) {
+__global__ void __launch_bounds__(kTileThreads, 4) k_mech_tile(MechArgs A, DevScalars *__restrict__ sc,
+                                                            int allow_prefilter) {
     if (sc->overflow) return;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     TileSmem &S = *reinterpret_cast<TileSmem *>(smem_raw);
     const GridView g = load_grid(sc);
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    TileSmem::Warp &Wp = S.W[w];
     const long long ntiles = (long long)g.T0 * g.T1 * g.T2;
+    const float R2f = (float)(g.R2 * (1.0 + 0x1p-12));
+    // prefilter precondition |coordinates| / L < 2^30 (uniform over the grid)
+    const double amax = fmax(fmax(fmax(fabs(g.o0), fabs(g.o1)), fmax(fabs(g.o2), fabs(sc->hi[0]))),
+                             fmax(fabs(sc->hi[1]), fabs(sc->hi[2])));
+    const bool use_pf = allow_prefilter && amax < 0x1p30 * g.L;
     Counts c;
 
     for (long long t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        const int tx = (int)(t % g.T0), ty = (int)((t / g.T0) % g.T1), tz = (int)(t / ((long long)g.T0 * g.T1));
+        const int tx = (int)(t % g.T0), ty = (int)((t / g.T0) % g.T1);
+        const int tz = (int)(t / ((long long)g.T0 * g.T1));
         const int bx0 = 4 * tx - 1, by0 = 4 * ty - 1, bz0 = 4 * tz - 1;
-        const uint32_t g0 = A.box_start[(uint32_t)t * 64u], g1 = A.box_start[(uint32_t)t * 64u + 64u];
+        const uint32_t g0 = A.box_start[(uint32_t)t * 64u];
+        const uint32_t g1 = A.box_start[(uint32_t)t * 64u + 64u];
         const int nc = (int)(g1 - g0);
         if (nc == 0) continue;  // uniform across the CTA
         // ---- box table of the 6^3 region (out-of-grid boxes are empty)
@@ -307,138 +363,185 @@ __global__ void __launch_bounds__(kTileThreads) k_mech_tile(MechArgs A, DevScala
             __syncthreads();
             continue;
         }
-        // ---- stage the region (row-major boxes, ascending id inside a box)
-        for (int m = tid; m < M; m += kTileThreads) {
-            int lo = 0, hi = 216;  // last lb with off[lb] <= m
-            while (hi - lo > 1) {
-                const int mid = (lo + hi) >> 1;
-                if (S.off[mid] <= (uint32_t)m) lo = mid; else hi = mid;
-            }
-            const uint32_t gi = S.start[lo] + ((uint32_t)m - S.off[lo]);
-            S.X[m] = A.sx[gi];
-            S.Y[m] = A.sy[gi];
-            S.Z[m] = A.sz[gi];
-            S.Rr[m] = A.sd[gi] * 0.5;
-            S.F[m] = A.sflags[gi];
+        // ---- stage the region box by box (row-major boxes, ascending id in a box)
+        const double X0 = g.o0 + (double)bx0 * g.L, Y0 = g.o1 + (double)by0 * g.L,
+                     Z0 = g.o2 + (double)bz0 * g.L;
+        for (int lb = tid; lb < 216; lb += kTileThreads)  // staged index -> its box
+            for (uint32_t m = S.off[lb]; m < S.off[lb + 1]; ++m) S.mbox[m] = (uint8_t)lb;
+        __syncthreads();
+        for (int m = tid; m < M; m += kTileThreads) {  // converged, independent loads
+            const int lb = S.mbox[m];
+            const uint32_t gi = S.start[lb] + ((uint32_t)m - S.off[lb]);
+            const double x = A.sx[gi], y = A.sy[gi], z = A.sz[gi], d = A.sd[gi];
+            const uint32_t f = A.sflags[gi];
+            S.X[m] = x;
+            S.Y[m] = y;
+            S.Z[m] = z;
+            S.Rr[m] = d * 0.5;
+            S.F[m] = f;
+            S.P[m] = make_float4((float)(x - X0), (float)(y - Y0), (float)(z - Z0), 0.f);
         }
-        if (tid < kTileWarps) S.qcnt[tid] = 0;
         __syncthreads();
 
-        for (int base = 0; base < nc; base += kTileThreads) {
-            const int k = base + tid;
-            const bool active = k < nc;
-            if (base + w * 32 >= nc) break;  // warp-uniform: no agent left for this warp
-            // ---- own agent
-            int mi = 0, lbi = 0, lcount = 0;
-            double xi = 0.0, yi = 0.0, zi = 0.0;
+        // ceil(nc/32) warps share the tile's agents equally (contiguous, <= 32 each)
+        const int nw = min(kTileWarps, (nc + 31) >> 5);
+        const int share = (nc + nw - 1) / nw;
+        const int wlo = w < nw ? min(nc, w * share) : nc;
+        const int whi = w < nw ? min(nc, wlo + share) : nc;
+        for (int base = wlo; base < whi; base += 32) {  // warp-uniform
+            const int na = min(32, whi - base);
+            const int k = base + lane;
+            const bool active = lane < na;
+            // ---- own agent: staged index, runs, candidate count
+            int mi = 0, ca = 0, nr = 0;
             uint32_t fi = 0;
-            bool cand_static = false, changed_nb = false, ovf = false;
-            uint32_t my_cand = 0;
+            double xi = 0.0, yi = 0.0, zi = 0.0;
+            bool cand_static = false;
             if (active) {
                 const uint32_t gk = g0 + (uint32_t)k;
-                xi = A.sx[gk]; yi = A.sy[gk]; zi = A.sz[gk];
+                xi = A.sx[gk];
+                yi = A.sy[gk];
+                zi = A.sz[gk];
                 const int lx = (int)floor((xi - g.o0) / g.L) - bx0;
                 const int ly = (int)floor((yi - g.o1) / g.L) - by0;
                 const int lz = (int)floor((zi - g.o2) / g.L) - bz0;
-                lbi = (lz * 6 + ly) * 6 + lx;
+                const int lbi = (lz * 6 + ly) * 6 + lx;
                 mi = (int)(S.off[lbi] + (gk - S.start[lbi]));
                 fi = S.F[mi];
                 cand_static = A.detect_static && !(fi & kChanged) &&
                               ((fi >> BDM_FLAG_NNZ_SHIFT) & 3u) <= 1u;
-                // ---- phase 1: 9 runs in canonical order, exact fp64 radius test
-                const double R2 = g.R2;
-#pragma unroll 1
+#pragma unroll
                 for (int r = 0; r < 9; ++r) {
-                    const int lb0 = lbi + ((r / 3 - 1) * 6 + (r % 3 - 1)) * 6 - 1;
-                    const int mend = (int)S.off[lb0 + 3];
-                    for (int m = (int)S.off[lb0]; m < mend; ++m) {
-                        if (m == mi) continue;
-                        ++my_cand;
-                        const double ex = xi - S.X[m], ey = yi - S.Y[m], ez = zi - S.Z[m];
-                        const double D = fma(ez, ez, fma(ey, ey, ex * ex));
-                        if (D <= R2) {
-                            changed_nb |= (S.F[m] & kChanged) != 0u;
-                            const int pos = warp_append(&S.qcnt[w]);
-                            if (pos < kQCap && lcount < kKMax) {
-                                S.qv[w][pos] = D;
-                                S.qm[w][pos] = (uint32_t)m | ((uint32_t)lane << 16);
-                                S.lidx[w][lcount][lane] = (uint16_t)pos;
-                            } else {
-                                ovf = true;
-                            }
-                            ++lcount;
-                        }
+                    const int lb0 = lbi - 43 + (r / 3) * 36 + (r % 3) * 6;
+                    const uint32_t rs = S.off[lb0], re = S.off[lb0 + 3];
+                    if (re > rs) {
+                        Wp.run[nr][lane] = rs | (re << 16);
+                        ++nr;
+                        ca += (int)(re - rs);
                     }
                 }
-            }
-            const bool is_static = active && cand_static && !changed_nb;
-            S.mi[w][lane] = (uint16_t)mi;
-            S.stat[w][lane] = is_static ? 1 : 0;
-            const bool wovf = __any_sync(0xffffffffu, ovf);
-            __syncwarp();
-            if (wovf) {
-                // queue overflow: this warp's agents take the reference path
-                if (active) mech_agent_global(A, g, g0 + k, c);
+                Wp.mi[lane] = (uint16_t)mi;
+                Wp.chg[lane] = 0;
             } else {
-                // ---- phase 2: Eq. 4.1/4.2 for the queued pairs, lane-parallel
-                const int qn = S.qcnt[w];
-                for (int p = lane; p < qn; p += 32) {
-                    const uint32_t meta = S.qm[w][p];
-                    const int m = (int)(meta & 0xFFFFu), owner = (int)(meta >> 16);
-                    uint32_t code = 0;
-                    double sc_ = 0.0;
-                    if (!S.stat[w][owner]) {
-                        const double D = S.qv[w][p];
-                        const double ri = S.Rr[S.mi[w][owner]], rj = S.Rr[m];
+                Wp.run[0][lane] = 0u;
+            }
+            const int cmax = __reduce_max_sync(0xffffffffu, ca);
+            __syncwarp();
+            // ---- phase 1: flattened, converged walk over the runs
+            const int cnt = use_pf ? phase1<true>(S, Wp, lane, mi, xi, yi, zi, ca, nr, cmax, R2f, g.R2)
+                                   : phase1<false>(S, Wp, lane, mi, xi, yi, zi, ca, nr, cmax, R2f, g.R2);
+            // ---- concatenate the lane lists (lane order = agent-major canonical order)
+            int cincl = cnt;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, cincl, o);
+                if (lane >= o) cincl += y;
+            }
+            const int my_off = cincl - cnt;
+            const int total = __shfl_sync(0xffffffffu, cincl, 31);
+            const bool wovf = __any_sync(0xffffffffu, cnt > kKMax) || total > kQCap;
+            if (wovf) {
+                // list overflow: this warp batch takes the reference path
+                if (active) mech_agent_global(A, g, g0 + k, c);
+                __syncwarp();
+                continue;
+            }
+            for (int jj = 0; jj < cnt; ++jj)
+                Wp.pr[my_off + jj] = (uint32_t)Wp.lst[jj][lane] | ((uint32_t)lane << 16);
+            __syncwarp();
+            const bool any_cs = __any_sync(0xffffffffu, cand_static);
+            // ---- phase 2a (only if an agent may be static): exact test + neighbour flags
+            if (any_cs) {
+                for (int p = lane; p < total; p += 32) {
+                    const uint32_t e = Wp.pr[p];
+                    const int m = (int)(e & 0xFFFFu), owner = (int)((e >> 16) & 0xFFu);
+                    const int mo = Wp.mi[owner];
+                    const double ex = S.X[mo] - S.X[m], ey = S.Y[mo] - S.Y[m], ez = S.Z[mo] - S.Z[m];
+                    const double D = fma(ez, ez, fma(ey, ey, ex * ex));
+                    if (D <= g.R2 && (S.F[m] & kChanged)) Wp.chg[owner] = 1;
+                }
+                __syncwarp();
+            }
+            const bool is_static = active && cand_static && !Wp.chg[lane];
+            const unsigned stat_mask = __ballot_sync(0xffffffffu, is_static);
+            // ---- phase 2: exact test and Eq. 4.1/4.2 for the pairs, lane-parallel
+            for (int p = lane; p < total; p += 32) {
+                const uint32_t e = Wp.pr[p];
+                const int m = (int)(e & 0xFFFFu), owner = (int)((e >> 16) & 0xFFu);
+                const int mo = Wp.mi[owner];
+                const double ex = S.X[mo] - S.X[m], ey = S.Y[mo] - S.Y[m], ez = S.Z[mo] - S.Z[m];
+                const double D = fma(ez, ez, fma(ey, ey, ex * ex));
+                double sc_ = 0.0;
+                uint32_t code = 0;
+                if (D <= g.R2) {
+                    code = kCodeNbr;
+                    if (!((stat_mask >> owner) & 1u)) {
+                        const double ri = S.Rr[mo], rj = S.Rr[m];
                         const double dist = sqrt(D);
                         const double delta = (ri + rj) - dist;
                         if (delta > 0.0 && dist > 0.0) {
                             const double rbar = (ri * rj) / (ri + rj);
                             const double Fn = A.k * delta - A.gamma * sqrt(rbar * delta);
                             sc_ = Fn / dist;
-                            code = 1u | (Fn != 0.0 ? 2u : 0u);
+                            code |= kCodeContact | (Fn != 0.0 ? kCodeNonzero : 0u);
                         }
                     }
-                    S.qv[w][p] = sc_;
-                    S.qm[w][p] = meta | (code << 24);
                 }
-                __syncwarp();
-                // ---- phase 3: ordered accumulation of the own contacts
-                if (active) {
-                    double Fx = 0.0, Fy = 0.0, Fz = 0.0;
-                    int nnz = 0;
-                    uint32_t my_cont = 0;
-                    for (int j = 0; j < lcount; ++j) {
-                        const int p = S.lidx[w][j][lane];
-                        const uint32_t meta = S.qm[w][p];
-                        if (meta & (1u << 24)) {
-                            const int m = (int)(meta & 0xFFFFu);
-                            const double sc_ = S.qv[w][p];
-                            const double ex = xi - S.X[m], ey = yi - S.Y[m], ez = zi - S.Z[m];
-                            Fx = fma(sc_, ex, Fx);
-                            Fy = fma(sc_, ey, Fy);
-                            Fz = fma(sc_, ez, Fz);
-                            ++my_cont;
-                            if ((meta & (1u << 25)) && nnz < 2) ++nnz;
-                        }
-                    }
-                    if (!is_static) {
-                        c.cand += my_cand;
-                        c.nbr += (uint32_t)lcount;
-                        c.cont += my_cont;
-                    } else {
-                        nnz = (int)((fi >> BDM_FLAG_NNZ_SHIFT) & 3u);
-                    }
-                    finish_agent(A, g0 + k, xi, yi, zi, Fx, Fy, Fz, is_static, nnz, c);
-                }
+                Wp.qs[p] = sc_;
+                Wp.pr[p] = e | code;
             }
             __syncwarp();
-            if (lane == 0) S.qcnt[w] = 0;
+            // ---- phase 3: ordered accumulation of the own pairs
+            if (active) {
+                double Fx = 0.0, Fy = 0.0, Fz = 0.0;
+                int nnz = 0;
+                uint32_t my_nbr = 0, my_cont = 0;
+                for (int jj = my_off; jj < my_off + cnt; ++jj) {
+                    const uint32_t e = Wp.pr[jj];
+                    my_nbr += (e & kCodeNbr) ? 1u : 0u;
+                    if (e & kCodeContact) {
+                        const int m = (int)(e & 0xFFFFu);
+                        const double sc_ = Wp.qs[jj];
+                        const double ex = xi - S.X[m], ey = yi - S.Y[m], ez = zi - S.Z[m];
+                        Fx = fma(sc_, ex, Fx);
+                        Fy = fma(sc_, ey, Fy);
+                        Fz = fma(sc_, ez, Fz);
+                        ++my_cont;
+                        if ((e & kCodeNonzero) && nnz < 2) ++nnz;
+                    }
+                }
+                if (!is_static) {
+                    c.cand += (uint32_t)(ca - 1);
+                    c.nbr += my_nbr;
+                    c.cont += my_cont;
+                } else {
+                    nnz = (int)((fi >> BDM_FLAG_NNZ_SHIFT) & 3u);
+                }
+                finish_agent(A, g0 + k, xi, yi, zi, Fx, Fy, Fz, is_static, nnz, c);
+            }
             __syncwarp();
         }
         __syncthreads();  // before the next tile overwrites the staged region
     }
     flush_counts<kStats>(c, sc);
+}
+
+template <bool kStats>
+static bdm_status launch_tile(Ctx *c, const MechArgs &A, cudaStream_t st) {
+    static bool attr_set = false;
+    static int per_sm = 0;
+    const int smem = (int)sizeof(TileSmem);
+    if (!attr_set) {
+        BDM_CUDA_TRY(cudaFuncSetAttribute(k_mech_tile<kStats>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        BDM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mech_tile<kStats>,
+                                                                   kTileThreads, smem));
+        if (per_sm < 1) per_sm = 1;
+        attr_set = true;
+    }
+    k_mech_tile<kStats><<<(unsigned)(c->sm_count * per_sm), kTileThreads, smem, st>>>(
+        A, c->sc, c->prefilter);
+    return BDM_OK;
 }
 
 bdm_status launch_mech(Ctx *c, bdm_agents *a, const bdm_params *p, cudaStream_t st) {
@@ -456,22 +559,9 @@ bdm_status launch_mech(Ctx *c, bdm_agents *a, const bdm_params *p, cudaStream_t 
         BDM_CUDA_TRY(cudaMemsetAsync(c->sc->stats, 0, sizeof(c->sc->stats), st));
     const bool tile = c->mech_kernel != 1;
     if (tile) {
-        static bool attr_set = false;
-        const int smem = (int)sizeof(TileSmem);
-        if (!attr_set) {
-            BDM_CUDA_TRY(cudaFuncSetAttribute(k_mech_tile<true>,
-                                              cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-            BDM_CUDA_TRY(cudaFuncSetAttribute(k_mech_tile<false>,
-                                              cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-            attr_set = true;
-        }
-        int per_sm = 0;
-        BDM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-            &per_sm, k_mech_tile<false>, kTileThreads, smem));
-        if (per_sm < 1) per_sm = 1;
-        const unsigned grid = (unsigned)(c->sm_count * per_sm);
-        if (p->collect_stats) k_mech_tile<true><<<grid, kTileThreads, smem, st>>>(A, c->sc);
-        else k_mech_tile<false><<<grid, kTileThreads, smem, st>>>(A, c->sc);
+        const bdm_status s = p->collect_stats ? launch_tile<true>(c, A, st)
+                                              : launch_tile<false>(c, A, st);
+        if (s != BDM_OK) return s;
     } else {
         const unsigned nb = (unsigned)((a->n + 255) / 256);
         if (p->collect_stats) k_mech<true><<<nb, 256, 0, st>>>(A, c->sc);
