@@ -77,6 +77,11 @@ def lib() -> ctypes.CDLL:
         L.orc_pair_force.restype = dbl
         L.orc_mech_step.argtypes = [i64, P, P, P, P, P, P, P, i64, P, P, P, P, P, P, P]
         L.orc_sorted_order.argtypes = [i64, P, P, P, P, P, dbl, P, P]
+        L.orc_cbrt_det.argtypes = [dbl]
+        L.orc_cbrt_det.restype = dbl
+        L.orc_division_axis.argtypes = [u64, u64, ctypes.c_uint32, P]
+        L.orc_grow_divide.argtypes = [i64, P, P, P, P, P, P, P, i64, dbl, dbl, u64, ctypes.c_uint32]
+        L.orc_grow_divide.restype = i64
         _lib = L
     return _lib
 
@@ -251,3 +256,56 @@ def step_full(s, params: MechParams):
         "flags": out["flags"][perm],
     }
     return new, cnt
+
+
+# ---------------------------------------------------------------- growth + division (cfg3)
+V_MAX_CFG3 = (3.141592653589793 / 6.0) * 1728.0   # (M_PI/6.0)*1728.0: d = 12 um
+
+
+def cbrt_det(v: float) -> float:
+    """R28 deterministic cube root (8 Newton steps from a power-of-two start)."""
+    return lib().orc_cbrt_det(v)
+
+
+def division_axis(seed: int, agent_id: int, step: int) -> np.ndarray:
+    u = np.zeros(3, np.float64)
+    lib().orc_division_axis(seed, agent_id, step, _p(u))
+    return u
+
+
+def init_volumes(s):
+    """V = (M_PI/6.0)*(d*d*d) per agent (R28 companion, exact op order)."""
+    d = np.asarray(s["d"], np.float64)
+    return (np.pi / 6.0) * (d * d * d)
+
+
+def grow_divide(s, growth, v_max, seed, step):
+    """Growth/division pass (Alg. 4 control flow + Cell::Divide, R13-R15).  s holds x,
+    y, z, d, vol, id, flags (post-mechanics); returns a new dict with daughters
+    appended at n + rank (rank among dividers in id order)."""
+    n = len(s["x"])
+    ndiv = int(np.count_nonzero(~(np.asarray(s["vol"]) < v_max)))
+    cap = n + ndiv
+    out = {}
+    for k in ("x", "y", "z", "d", "vol"):
+        a = np.zeros(max(cap, 1), np.float64)
+        a[:n] = s[k]
+        out[k] = a
+    for k in ("id", "flags"):
+        a = np.zeros(max(cap, 1), np.uint32)
+        a[:n] = s[k]
+        out[k] = a
+    r = lib().orc_grow_divide(n, _p(out["x"]), _p(out["y"]), _p(out["z"]), _p(out["d"]),
+                              _p(out["vol"]), _p(out["id"]), _p(out["flags"]), cap, growth,
+                              v_max, seed, step)
+    assert r == cap, (r, cap)
+    return {k: v[:cap] for k, v in out.items()}
+
+
+def cfg3_step(s, params: MechParams, growth, v_max, seed, step):
+    """One cfg3 step (R15, R27): mechanics on the snapshot (static skip per params),
+    then growth/division at the post-mechanics positions.  Input/output in any order."""
+    out, cnt = mech_step(s, params)
+    post = {"x": out["x"], "y": out["y"], "z": out["z"], "d": s["d"], "vol": s["vol"],
+            "id": s["id"], "flags": out["flags"]}
+    return grow_divide(post, growth, v_max, seed, step), cnt

@@ -19,7 +19,11 @@
  * Everything here is written for readability, not speed: sorting by qsort, box
  * lookup by binary search, one agent at a time.
  */
+#define _USE_MATH_DEFINES
 #include <math.h>
+#ifndef M_PI
+#define M_PI 3.14159265358979323846
+#endif
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
@@ -517,4 +521,118 @@ void orc_sorted_order(int64_t n, const double *x, const double *y, const double 
         if (keys_sorted) keys_sorted[i] = e[i].key;
     }
     free(e);
+}
+
+/* ------------------------------------------------------------------------------ */
+/* Growth and division (cfg3): Alg. 4 control flow "grow if d < max, else divide"   */
+/* (algo:tumor_growth_module) with division probability 1; Cell::Divide */
+/* splits the volume by the volume ratio and places the daughter along the division */
+/* axis; additions become visible at the next iteration (*/
+/* P:4538-4544).  Readings R13-R15, R28.                                 */
+/* ------------------------------------------------------------------------------ */
+
+/* R28: deterministic cube root.  v = m 2^e (frexp, m in [0.5,1)); start y = 2^k with
+ * k = floor((e+1)/3); exactly 8 Newton steps y <- (2y + v/(y*y))/3, no fma. */
+double orc_cbrt_det(double v)
+{
+    if (!(v > 0.0)) return 0.0;
+    int e;
+    (void)frexp(v, &e);
+    int num = e + 1;
+    int k = num >= 0 ? num / 3 : -((-num + 2) / 3); /* mathematical floor(num/3) */
+    double y = ldexp(1.0, k);
+    for (int it = 0; it < 8; ++it) {
+        double yy = y * y;
+        double q = v / yy;
+        double t = 2.0 * y + q;
+        y = t / 3.0;
+    }
+    return y;
+}
+
+/* R13: division axis uniform on the sphere by rejection in the unit ball.  Try k uses
+ * Philox counter (id, step, 3 + 4k): v_a = 2 u32(w_a) - 1 (a = 0,1,2); accept if
+ * 0 < v.v <= 1, u = v / sqrt(v.v); after 16 rejected tries the axis is +x. */
+void orc_division_axis(uint64_t seed, uint64_t id, uint32_t step, double u[3])
+{
+    for (uint32_t k = 0; k < 16; ++k) {
+        uint32_t w[4];
+        philox_draw(seed, id, step, 3u + 4u * k, w);
+        double vx = 2.0 * orc_u32(w[0]) - 1.0;
+        double vy = 2.0 * orc_u32(w[1]) - 1.0;
+        double vz = 2.0 * orc_u32(w[2]) - 1.0;
+        double n2 = vx * vx + vy * vy + vz * vz;
+        if (n2 > 0.0 && n2 <= 1.0) {
+            double n = sqrt(n2);
+            u[0] = vx / n;
+            u[1] = vy / n;
+            u[2] = vz / n;
+            return;
+        }
+    }
+    u[0] = 1.0;
+    u[1] = 0.0;
+    u[2] = 0.0;
+}
+
+/* One growth/division pass over n agents that already carry their post-mechanics
+ * positions (R15: growth and division read the start-of-step volume V).  For every
+ * agent in ascending id order:
+ *   V < v_max:  V += growth; d = 2 cbrt_det(V C), C = 0.75/M_PI; flag GREW if d grew
+ *   else:       V <- V/2 for mother and daughter (volume ratio 0.5, exact),
+ *               r' = cbrt_det(V' C), d' = 2r', axis u (R13),
+ *               mother at x - r'u (flag MOVED, its diameter shrank),
+ *               daughter at x + r'u (flag ADDED), id = n + rank among dividers by id,
+ *               appended at index n + rank.
+ * Arrays must have room for the daughters; returns the new agent count.
+ * Input arrays may be in any order; ids must be exactly 0..n-1. */
+int64_t orc_grow_divide(int64_t n, double *x, double *y, double *z, double *d, double *vol,
+                        uint32_t *id, uint32_t *flags, int64_t capacity, double growth,
+                        double v_max, uint64_t seed, uint32_t step)
+{
+    const double C = 0.75 / M_PI;
+    int64_t *by_id = (int64_t *)malloc(sizeof(int64_t) * (size_t)(n > 0 ? n : 1));
+    for (int64_t i = 0; i < n; ++i) by_id[id[i]] = i;
+    int64_t ndiv = 0;
+    for (int64_t k = 0; k < n; ++k)
+        if (!(vol[by_id[k]] < v_max)) ++ndiv;
+    if (n + ndiv > capacity) {
+        free(by_id);
+        return -(n + ndiv);
+    }
+    int64_t rank = 0;
+    for (int64_t k = 0; k < n; ++k) {      /* ascending id */
+        int64_t i = by_id[k];
+        double V = vol[i];
+        if (V < v_max) {
+            double Vn = V + growth;
+            double dn = 2.0 * orc_cbrt_det(Vn * C);
+            if (dn > d[i]) flags[i] |= ORC_GREW;
+            vol[i] = Vn;
+            d[i] = dn;
+        } else {
+            double Vh = V * 0.5;
+            double r = orc_cbrt_det(Vh * C);
+            double u[3];
+            orc_division_axis(seed, id[i], step, u);
+            int64_t j = n + rank;
+            double px = x[i], py = y[i], pz = z[i];
+            x[i] = px - r * u[0];
+            y[i] = py - r * u[1];
+            z[i] = pz - r * u[2];
+            x[j] = px + r * u[0];
+            y[j] = py + r * u[1];
+            z[j] = pz + r * u[2];
+            vol[i] = Vh;
+            vol[j] = Vh;
+            d[i] = 2.0 * r;
+            d[j] = 2.0 * r;
+            flags[i] |= ORC_MOVED;
+            flags[j] = ORC_ADDED;
+            id[j] = (uint32_t)(n + rank);
+            ++rank;
+        }
+    }
+    free(by_id);
+    return n + ndiv;
 }
