@@ -175,6 +175,24 @@ bdm_status bdm_step(bdm_handle h, bdm_agents *a, const bdm_params *p, void *stre
 bdm_status bdm_step_host(bdm_handle h, const bdm_agents *host_in, bdm_agents *host_out,
                          bdm_agents *dev, const bdm_params *p, void *stream);
 
+/* Growth and division with add-compaction (Alg. 4 control flow
+ * "grow while below the maximum size, else divide", with division
+ * probability 1; Cell::Divide; parallel addition).  Reads
+ * the start-of-step volume (R15) of every agent i in [0, n):
+ *   V < v_max:  V += growth; d = 2 cbrt_det(V * 0.75/pi) (R28); GREW if d increased
+ *   else:       V/2 for mother and daughter, r' = cbrt_det(V/2 * 0.75/pi), axis u from
+ *               Philox(seed, id, p->step, stream 3 + 4k) by rejection (R13); mother
+ *               at x - r'u (MOVED), daughter at x + r'u (ADDED) with id n + rank and
+ *               stored at index n + rank, rank = position among the dividers in id
+ *               order.  Requires volume != NULL and ids exactly 0..n-1.
+ * Usually called right after bdm_mech_step (positions are post-mechanics).  Writes
+ * the new count to *n_out_host (pinned host memory, asynchronously; valid after the
+ * stream synchronizes); a->n is NOT updated.  If n + #dividers > capacity nothing is
+ * modified, *n_out_host = -(required capacity) and bdm_sync reports BDM_ECAPACITY.
+ * Errors: BDM_EINVAL (no volume array, growth < 0, v_max <= 0). */
+bdm_status bdm_grow_divide(bdm_handle h, bdm_agents *a, const bdm_params *p, double growth,
+                           double v_max, int64_t *n_out_host, void *stream);
+
 /* Synchronize `stream` and report latched device conditions: BDM_ECAPACITY (grid
  * slots exceeded; bdm_get_grid_info gives the needed nslots), BDM_ENOTFINITE, or a
  * CUDA error.  Clears the latched condition. */

@@ -24,7 +24,7 @@ EXPORTS = [
     "bdm_create", "bdm_destroy", "bdm_last_error", "bdm_version", "bdm_init_spheres",
     "bdm_grid_build", "bdm_mech_step", "bdm_step", "bdm_step_host", "bdm_sync", "bdm_reserve",
     "bdm_get_stats", "bdm_get_grid_info", "bdm_neighbor_pairs", "bdm_peak_dfma",
-    "bdm_set_option",
+    "bdm_set_option", "bdm_grow_divide",
 ]
 
 
@@ -96,6 +96,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "bdm_neighbor_pairs": [P, AG, dbl, P, i64, ctypes.POINTER(i64), P],
         "bdm_peak_dfma": [P, ctypes.POINTER(dbl), ctypes.POINTER(i32)],
         "bdm_set_option": [P, ctypes.c_char_p, i64],
+        "bdm_grow_divide": [P, AG, PR, dbl, dbl, P, P],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -161,12 +162,18 @@ class Agents:
     _c: CAgents = field(default=None, repr=False)
 
     @staticmethod
-    def empty(capacity: int, device="cuda", pin: bool = False) -> "Agents":
+    def empty(capacity: int, device="cuda", pin: bool = False, volume: bool = False,
+              state: bool = False) -> "Agents":
         import torch
         kw = dict(device=device) if not pin else dict(pin_memory=True)
         f64 = lambda: torch.empty(capacity, dtype=torch.float64, **kw)  # noqa: E731
         u32 = lambda: torch.empty(capacity, dtype=torch.int32, **kw)    # noqa: E731
-        return Agents(f64(), f64(), f64(), f64(), u32(), u32(), 0)
+        a = Agents(f64(), f64(), f64(), f64(), u32(), u32(), 0)
+        if volume:
+            a.volume = f64()
+        if state:
+            a.state = torch.zeros(capacity, dtype=torch.uint8, **kw)
+        return a
 
     @property
     def capacity(self) -> int:
@@ -189,6 +196,10 @@ class Agents:
         out["d"] = out.pop("diameter")
         out["id"] = self.id[:n].cpu().numpy().view(np.uint32)
         out["flags"] = self.flags[:n].cpu().numpy().view(np.uint32)
+        if self.volume is not None:
+            out["vol"] = self.volume[:n].cpu().numpy()
+        if self.state is not None:
+            out["state"] = self.state[:n].cpu().numpy()
         return out
 
     @staticmethod
@@ -203,6 +214,12 @@ class Agents:
             getattr(a, k)[:n].copy_(torch.from_numpy(np.ascontiguousarray(s[src], np.float64)))
         a.id[:n].copy_(torch.from_numpy(np.ascontiguousarray(s["id"], np.uint32).view(np.int32)))
         a.flags[:n].copy_(torch.from_numpy(np.ascontiguousarray(s["flags"], np.uint32).view(np.int32)))
+        if "vol" in s:
+            a.volume = torch.zeros(cap, dtype=torch.float64, device=device)
+            a.volume[:n].copy_(torch.from_numpy(np.ascontiguousarray(s["vol"], np.float64)))
+        if "state" in s:
+            a.state = torch.zeros(cap, dtype=torch.uint8, device=device)
+            a.state[:n].copy_(torch.from_numpy(np.ascontiguousarray(s["state"], np.uint8)))
         return a
 
 
@@ -272,6 +289,29 @@ class Engine:
             _check(st)
             return
         raise BdmError(BDM_ECAPACITY, "grid slot capacity could not be satisfied")
+
+    def grow_divide(self, agents: Agents, params: Params, growth: float, v_max: float,
+                    stream=None) -> int:
+        """bdm_grow_divide; synchronizes, updates agents.n and returns it.  Raises
+        BdmError(BDM_ECAPACITY) if the arrays cannot hold the daughters."""
+        import torch
+        if not hasattr(self, "_n_out"):
+            self._n_out = torch.zeros(1, dtype=torch.int64, pin_memory=True)
+        ca = agents.c()
+        cp = params.c()
+        _check(self.lib.bdm_grow_divide(self.h, ctypes.byref(ca), ctypes.byref(cp), float(growth),
+                                        float(v_max), ctypes.c_void_p(self._n_out.data_ptr()),
+                                        _stream_ptr(stream)))
+        self.sync(stream)
+        agents.n = int(self._n_out[0])
+        return agents.n
+
+    def cfg3_step(self, agents: Agents, params: Params, growth: float, v_max: float,
+                  stream=None) -> int:
+        """One proliferation step (R15): grid + mechanics on the snapshot, then
+        growth/division at the post-mechanics positions."""
+        self.step(agents, params, stream=stream)
+        return self.grow_divide(agents, params, growth, v_max, stream=stream)
 
     def step_host(self, host_in: Agents, host_out: Agents, dev: Agents, params: Params,
                   stream=None):

@@ -2,6 +2,7 @@
 // management, and the stream-ordered composition of the kernels.
 #include <cuda_runtime.h>
 #include <stdio.h>
+#include <math.h>
 #include <string.h>
 
 #include <string>
@@ -51,12 +52,19 @@ static bdm_status grow_agents(Ctx *c, int64_t n) {
         (s = dalloc(&c->perm_tmp, cap)) || (s = dalloc(&c->skey, cap)) ||
         (s = dalloc(&c->sid, cap)) || (s = dalloc(&c->perm, cap)) || (s = dalloc(&c->sx, cap)) ||
         (s = dalloc(&c->sy, cap)) || (s = dalloc(&c->sz, cap)) || (s = dalloc(&c->sd, cap)) ||
-        (s = dalloc(&c->sidf, cap)) || (s = dalloc(&c->sflags, cap))) {
+        (s = dalloc(&c->sidf, cap)) || (s = dalloc(&c->sflags, cap)) ||
+        (s = dalloc(&c->svol, cap)) || (s = dalloc(&c->div_rank, cap + 1))) {
         c->agent_cap = 0;
         return s;
     }
     c->agent_cap = cap;
     c->grid_valid = false;
+    // the scan block sums serve both the slot scan and the agent-indexed scans
+    const int64_t nb = scan_block_count(cap > c->slot_cap ? cap : c->slot_cap) + 1;
+    if (nb > c->block_sums_cap) {
+        if ((s = dalloc(&c->block_sums, nb))) return s;
+        c->block_sums_cap = nb;
+    }
     return BDM_OK;
 }
 
@@ -65,9 +73,11 @@ static bdm_status grow_slots(Ctx *c, int64_t nslots) {
     BDM_CUDA_TRY(cudaDeviceSynchronize());
     bdm_status s;
     if ((s = dalloc(&c->box_start, nslots + 1))) { c->slot_cap = 0; return s; }
-    const int64_t nb = scan_block_count(nslots);
-    if ((s = dalloc(&c->block_sums, nb + 1))) { c->slot_cap = 0; return s; }
-    c->block_sums_cap = nb + 1;
+    const int64_t nb = scan_block_count(nslots > c->agent_cap ? nslots : c->agent_cap) + 1;
+    if (nb > c->block_sums_cap) {
+        if ((s = dalloc(&c->block_sums, nb))) { c->slot_cap = 0; return s; }
+        c->block_sums_cap = nb;
+    }
     c->slot_cap = nslots;
     long long cap = nslots;
     BDM_CUDA_TRY(cudaMemcpy(&c->sc->slot_cap, &cap, sizeof(cap), cudaMemcpyHostToDevice));
@@ -94,6 +104,8 @@ static bdm_status read_latches(Ctx *c, bool clear) {
     bdm_status st = BDM_OK;
     if (c->sc_host->nonfinite) {
         st = fail(BDM_ENOTFINITE, "a position or diameter is NaN/Inf");
+    } else if (c->sc_host->overflow == 2) {
+        st = fail(BDM_ECAPACITY, "agent capacity too small for the daughters of this step");
     } else if (c->sc_host->overflow) {
         st = fail(BDM_ECAPACITY, "grid needs " + std::to_string(c->sc_host->nslots) +
                                      " slots, capacity " + std::to_string(c->slot_cap));
@@ -128,7 +140,8 @@ bdm_status bdm_create(bdm_handle *out, int device, int64_t max_agents) {
     cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device);
     if (cudaMalloc(&c->sc, sizeof(DevScalars)) != cudaSuccess ||
         cudaMallocHost(&c->sc_host, sizeof(DevScalars)) != cudaSuccess ||
-        cudaMalloc(&c->pair_count, sizeof(unsigned long long)) != cudaSuccess) {
+        cudaMalloc(&c->pair_count, sizeof(unsigned long long)) != cudaSuccess ||
+        cudaMalloc(&c->n_new, sizeof(long long)) != cudaSuccess) {
         cudaGetLastError();
         delete c;
         return fail(BDM_ECUDA, "allocation of the context scalars failed");
@@ -150,8 +163,8 @@ bdm_status bdm_destroy(bdm_handle h) {
     cudaSetDevice(c->device);
     cudaDeviceSynchronize();
     void *bufs[] = {c->key, c->rank, c->perm_tmp, c->skey, c->sid, c->perm, c->sx, c->sy,
-                    c->sz, c->sd, c->sidf, c->sflags, c->box_start, c->block_sums,
-                    c->pair_count, c->sc};
+                    c->sz, c->sd, c->sidf, c->sflags, c->svol, c->div_rank, c->box_start,
+                    c->block_sums, c->pair_count, c->n_new, c->sc};
     for (void *p : bufs)
         if (p) cudaFree(p);
     if (c->sc_host) cudaFreeHost(c->sc_host);
@@ -262,6 +275,21 @@ bdm_status bdm_step_host(bdm_handle h, const bdm_agents *hin, bdm_agents *hout, 
     BDM_CUDA_TRY(cudaMemcpyAsync(hout->id, dev->id, n * 4, cudaMemcpyDeviceToHost, st));
     BDM_CUDA_TRY(cudaMemcpyAsync(hout->flags, dev->flags, n * 4, cudaMemcpyDeviceToHost, st));
     return bdm_sync(h, stream);
+}
+
+bdm_status bdm_grow_divide(bdm_handle h, bdm_agents *a, const bdm_params *p, double growth,
+                           double v_max, int64_t *n_out_host, void *stream) {
+    if (!h || !p || !n_out_host) return fail(BDM_EINVAL, "NULL argument");
+    Ctx *c = (Ctx *)h;
+    bdm_status s = check_agents(a, true);
+    if (s != BDM_OK) return s;
+    if (!a->volume) return fail(BDM_EINVAL, "growth/division needs the volume array");
+    if (!(growth >= 0.0) || !(v_max > 0.0)) return fail(BDM_EINVAL, "growth < 0 or v_max <= 0");
+    if ((s = grow_agents(c, a->n)) != BDM_OK) return s;
+    c->grid_valid = false;
+    const double vol_to_r3 = 0.75 / M_PI;  // r^3 = V * 0.75/pi, computed once (R28)
+    return launch_grow_divide(c, a, growth, v_max, vol_to_r3, p->seed, p->step,
+                              (long long *)n_out_host, (cudaStream_t)stream);
 }
 
 bdm_status bdm_sync(bdm_handle h, void *stream) {

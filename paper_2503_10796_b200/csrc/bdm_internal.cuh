@@ -57,6 +57,9 @@ struct Ctx {
     uint32_t *perm = nullptr;                          // sorted slot -> input index
     double *sx = nullptr, *sy = nullptr, *sz = nullptr, *sd = nullptr;  // sorted SoA
     uint32_t *sidf = nullptr, *sflags = nullptr;
+    double *svol = nullptr;                            // sorted volume (when present)
+    uint32_t *div_rank = nullptr;                      // growth/division: flag -> rank by id
+    long long *n_new = nullptr;                        // growth/division: new agent count
     // grid
     uint32_t *box_start = nullptr;  // slot_cap + 1
     uint32_t *block_sums = nullptr;
@@ -135,5 +138,10 @@ bdm_status launch_grid_sort(Ctx *c, const bdm_agents *a, cudaStream_t st);
 bdm_status launch_mech(Ctx *c, bdm_agents *a, const bdm_params *p, cudaStream_t st);
 bdm_status launch_pairs(Ctx *c, int64_t n, uint64_t *pairs, int64_t cap, cudaStream_t st);
 bdm_status launch_peak_dfma(int sm_count, double *dfma_per_s);
+// generic exclusive scan of m u32 values in place (kernels_grid.cu)
+bdm_status launch_scan_u32(Ctx *c, uint32_t *data, long long m, cudaStream_t st);
+// growth + division (kernels_divide.cu)
+bdm_status launch_grow_divide(Ctx *c, bdm_agents *a, double growth, double v_max, double vol_to_r3,
+                              uint64_t seed, uint32_t step, long long *n_new_host, cudaStream_t st);
 
 }  // namespace bdm

@@ -222,11 +222,17 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t *total)
     return before;
 }
 
+// m = nslots + 1 from the device scalars (grid scan) or the explicit m_host (sc == nullptr)
+__device__ __forceinline__ long long scan_len(const DevScalars *__restrict__ sc, long long m_host) {
+    return sc ? sc->nslots + 1 : m_host;
+}
+
 __global__ void __launch_bounds__(kScanThreads) k_scan_reduce(const uint32_t *__restrict__ cnt,
                                                               uint32_t *__restrict__ bsum,
-                                                              const DevScalars *__restrict__ sc) {
-    if (sc->overflow) return;
-    const long long m = sc->nslots + 1;
+                                                              const DevScalars *__restrict__ sc,
+                                                              long long m_host) {
+    if (sc && sc->overflow) return;
+    const long long m = scan_len(sc, m_host);
     const long long base = (long long)blockIdx.x * kScanTile;
     if (base >= m) return;
     uint32_t s = 0;
@@ -242,9 +248,10 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_reduce(const uint32_t *__
 
 // One block scans the block sums (exclusive, in place).
 __global__ void __launch_bounds__(1024) k_scan_top(uint32_t *__restrict__ bsum,
-                                                   const DevScalars *__restrict__ sc) {
-    if (sc->overflow) return;
-    const long long m = sc->nslots + 1;
+                                                   const DevScalars *__restrict__ sc,
+                                                   long long m_host) {
+    if (sc && sc->overflow) return;
+    const long long m = scan_len(sc, m_host);
     const long long nb = (m + kScanTile - 1) / kScanTile;
     const long long per = (nb + blockDim.x - 1) / blockDim.x;
     const long long b0 = threadIdx.x * per;
@@ -261,9 +268,10 @@ __global__ void __launch_bounds__(1024) k_scan_top(uint32_t *__restrict__ bsum,
 
 __global__ void __launch_bounds__(kScanThreads) k_scan_apply(uint32_t *__restrict__ cnt,
                                                              const uint32_t *__restrict__ bsum,
-                                                             const DevScalars *__restrict__ sc) {
-    if (sc->overflow) return;
-    const long long m = sc->nslots + 1;
+                                                             const DevScalars *__restrict__ sc,
+                                                             long long m_host) {
+    if (sc && sc->overflow) return;
+    const long long m = scan_len(sc, m_host);
     const long long base = (long long)blockIdx.x * kScanTile;
     if (base >= m) return;
     // thread t owns items base + t*8 .. +7 (contiguous)
@@ -312,7 +320,7 @@ __global__ void __launch_bounds__(256) k_fix_gather(
     const double *__restrict__ d, const uint32_t *__restrict__ flags, double *__restrict__ sx,
     double *__restrict__ sy, double *__restrict__ sz, double *__restrict__ sd,
     uint32_t *__restrict__ sidf, uint32_t *__restrict__ sflags, uint32_t *__restrict__ perm,
-    const DevScalars *__restrict__ sc) {
+    const double *__restrict__ vol, double *__restrict__ svol, const DevScalars *__restrict__ sc) {
     if (sc->overflow) return;
     const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (s >= n) return;
@@ -330,6 +338,7 @@ __global__ void __launch_bounds__(256) k_fix_gather(
     sidf[dst] = me;
     sflags[dst] = flags[src];
     perm[dst] = src;
+    if (vol) svol[dst] = vol[src];
 }
 
 bdm_status launch_grid_sort(Ctx *c, const bdm_agents *a, cudaStream_t st) {
@@ -344,19 +353,37 @@ bdm_status launch_grid_sort(Ctx *c, const bdm_agents *a, cudaStream_t st) {
     }
     k_key<<<nb, threads, 0, st>>>(n, a->x, a->y, a->z, c->sc, c->key, c->rank, c->box_start);
     const unsigned sb = (unsigned)((c->slot_cap + 1 + kScanTile - 1) / kScanTile);
-    k_scan_reduce<<<sb, kScanThreads, 0, st>>>(c->box_start, c->block_sums, c->sc);
-    k_scan_top<<<1, 1024, 0, st>>>(c->block_sums, c->sc);
-    k_scan_apply<<<sb, kScanThreads, 0, st>>>(c->box_start, c->block_sums, c->sc);
+    k_scan_reduce<<<sb, kScanThreads, 0, st>>>(c->box_start, c->block_sums, c->sc, 0);
+    k_scan_top<<<1, 1024, 0, st>>>(c->block_sums, c->sc, 0);
+    k_scan_apply<<<sb, kScanThreads, 0, st>>>(c->box_start, c->block_sums, c->sc, 0);
     k_scatter<<<nb, threads, 0, st>>>(n, c->key, c->rank, c->box_start, a->id, c->perm_tmp,
                                       c->skey, c->sid, c->sc);
     k_fix_gather<<<nb, threads, 0, st>>>(n, c->skey, c->sid, c->perm_tmp, c->box_start, a->x,
                                          a->y, a->z, a->diameter, a->flags, c->sx, c->sy, c->sz,
-                                         c->sd, c->sidf, c->sflags, c->perm, c->sc);
+                                         c->sd, c->sidf, c->sflags, c->perm, a->volume, c->svol,
+                                         c->sc);
     c->launches += 7;
     BDM_LAUNCH_CHECK("grid sort");
     return BDM_OK;
 }
 
 int64_t scan_block_count(int64_t slot_cap) { return (slot_cap + 1 + kScanTile - 1) / kScanTile; }
+
+// Exclusive scan of m values in place (block sums in the context's scan buffer, which
+// bdm_reserve / grow_agents size for max(slots, agents) + 1 entries).
+bdm_status launch_scan_u32(Ctx *c, uint32_t *data, long long m, cudaStream_t st) {
+    if (m <= 0) return BDM_OK;
+    const unsigned sb = (unsigned)((m + kScanTile - 1) / kScanTile);
+    if ((int64_t)sb + 1 > c->block_sums_cap) {
+        set_error("scan buffer too small");
+        return BDM_ECAPACITY;
+    }
+    k_scan_reduce<<<sb, kScanThreads, 0, st>>>(data, c->block_sums, nullptr, m);
+    k_scan_top<<<1, 1024, 0, st>>>(c->block_sums, nullptr, m);
+    k_scan_apply<<<sb, kScanThreads, 0, st>>>(data, c->block_sums, nullptr, m);
+    c->launches += 3;
+    BDM_LAUNCH_CHECK("scan");
+    return BDM_OK;
+}
 
 }  // namespace bdm

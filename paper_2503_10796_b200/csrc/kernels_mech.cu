@@ -33,6 +33,8 @@ struct MechArgs {
     double *__restrict__ od;
     uint32_t *__restrict__ oid;
     uint32_t *__restrict__ oflags;
+    const double *__restrict__ svol;  // nullable: volume travels with the agents
+    double *__restrict__ ovol;
     double k, gamma, dt, max_disp, tau;
     int detect_static, boundary;
     double lo0, lo1, lo2, hi0, hi1, hi2;
@@ -95,6 +97,7 @@ __device__ __forceinline__ void finish_agent(const MechArgs &A, int64_t s, doubl
     A.oz[s] = nz;
     A.od[s] = A.sd[s];
     A.oid[s] = A.sid[s];
+    if (A.ovol) A.ovol[s] = A.svol[s];
     A.oflags[s] = (moved ? BDM_FLAG_MOVED : 0u) | (is_static ? BDM_FLAG_STATIC : 0u) |
                   ((uint32_t)nnz << BDM_FLAG_NNZ_SHIFT);
 }
@@ -249,7 +252,7 @@ struct TileSmem {
         double qs[kQCap];                  // s = F_N / dist per pair
         uint32_t pr[kQCap];                // m | agent << 16 | codes
         uint32_t run[9][32];               // per lane: non-empty runs (start | end << 16)
-        uint16_t lst[kKMax][32];           // per lane: survivors (staged index)
+        uint16_t lst[kKMax + 1][32];       // per lane: survivors (+1 scratch slot)
         uint16_t mi[32];                   // agent -> staged index
         uint8_t chg[32];                   // agent saw a changed neighbour
     } W[kTileWarps];
@@ -279,8 +282,9 @@ __device__ __forceinline__ int phase1(const TileSmem &S, TileSmem::Warp &Wp, int
             pass = fma(ez, ez, fma(ey, ey, ex * ex)) <= R2;
         }
         pass = pass && (m != mi) && (it < ca);
-        // branch-free append: the slot at cnt is scratch until committed
-        Wp.lst[cnt < kKMax ? cnt : kKMax - 1][lane] = (uint16_t)m;
+        // branch-free append: the slot at cnt is scratch until committed (slot kKMax is
+        // a spare, so a full list is never overwritten; cnt > kKMax means overflow)
+        Wp.lst[cnt < kKMax ? cnt : kKMax][lane] = (uint16_t)m;
         cnt += pass ? 1 : 0;
         // branch-free run advance: next run from the prefetch register, or park
         ++m;
@@ -550,6 +554,8 @@ bdm_status launch_mech(Ctx *c, bdm_agents *a, const bdm_params *p, cudaStream_t 
     A.sx = c->sx; A.sy = c->sy; A.sz = c->sz; A.sd = c->sd;
     A.sid = c->sidf; A.sflags = c->sflags; A.box_start = c->box_start;
     A.ox = a->x; A.oy = a->y; A.oz = a->z; A.od = a->diameter; A.oid = a->id; A.oflags = a->flags;
+    A.svol = a->volume ? c->svol : nullptr;
+    A.ovol = a->volume;
     A.k = p->k; A.gamma = p->gamma; A.dt = p->dt; A.max_disp = p->max_displacement;
     A.tau = p->force_threshold;
     A.detect_static = p->detect_static; A.boundary = p->boundary;

@@ -1,0 +1,86 @@
+"""GPU parity for growth + division (cfg3) through the C ABI."""
+import math
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+V_MAX = (math.pi / 6.0) * 1728.0
+GROWTH = 400.0
+
+
+@pytest.fixture(scope="module")
+def eng():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_2503_10796_b200 import Engine
+    e = Engine(0, 1 << 16)
+    yield e
+    e.close()
+
+
+def by_id(s):
+    order = np.argsort(s["id"], kind="stable")
+    return {k: np.asarray(v)[order] for k, v in s.items()}
+
+
+def assert_same(g, o, what):
+    g, o = by_id(g), by_id(o)
+    assert len(g["id"]) == len(o["id"]), what
+    for k in ("id", "flags", "d", "vol", "x", "y", "z"):
+        assert np.array_equal(g[k], o[k]), (what, k)
+
+
+def _start(orc, n, side):
+    s = orc.init_spheres(n, 1, side, 8.0)
+    s["vol"] = orc.init_volumes(s)
+    return s
+
+
+@pytest.mark.parametrize("n,steps", [(1, 6), (257, 10), (2000, 12)])
+def test_cfg3_reduced_trajectory(eng, orc, n, steps):
+    """cfg3 density (1M per mm^3) at reduced N; every step bit-exact by id."""
+    from paper_2503_10796_b200 import Agents, Params
+    side = 1000.0 * (n / 1e6) ** (1 / 3)
+    o = _start(orc, n, side)
+    a = Agents.from_numpy(o, capacity=n * 2 ** (steps // 2 + 2))
+    gp = Params(seed=1, collect_stats=True)
+    op = orc.mech_params()
+    for t in range(steps):
+        gp.step = t
+        eng.cfg3_step(a, gp, GROWTH, V_MAX)
+        o, _ = orc.cfg3_step(o, op, GROWTH, V_MAX, 1, t)
+        assert_same(a.numpy(), o, f"n={n} step {t}")
+
+
+def test_grow_divide_capacity_error_leaves_state(eng, orc):
+    from paper_2503_10796_b200 import Agents, BdmError, Params
+    o = _start(orc, 100, 50.0)
+    o["vol"][:] = 1000.0                     # everyone divides
+    a = Agents.from_numpy(o, capacity=150)   # room for 50 daughters only
+    before = a.numpy()
+    with pytest.raises(BdmError) as ei:
+        eng.grow_divide(a, Params(seed=1), GROWTH, V_MAX)
+    assert ei.value.status == -2
+    after = a.numpy()
+    for k in before:
+        assert np.array_equal(before[k], after[k]), k
+    assert a.n == 100 or a.n == -200
+
+
+@pytest.mark.slow
+def test_cfg3_full_size_first_steps(eng, orc):
+    """configs[2] at full size (1M agents): steps 1-4 (population 1M -> 2M) bit-exact."""
+    from paper_2503_10796_b200 import Agents, Params
+    o = _start(orc, 1_000_000, 1000.0)
+    a = Agents.from_numpy(o, capacity=2_100_000)
+    gp = Params(seed=1)
+    op = orc.mech_params()
+    for t in range(4):
+        gp.step = t
+        eng.cfg3_step(a, gp, GROWTH, V_MAX)
+        o, _ = orc.cfg3_step(o, op, GROWTH, V_MAX, 1, t)
+        assert_same(a.numpy(), o, f"full step {t}")
+    assert a.n == 2_000_000

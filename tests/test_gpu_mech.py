@@ -187,6 +187,29 @@ def test_edge_cases(eng, orc):
     assert_state_equal(a.numpy(), o, "closed")
 
 
+@pytest.mark.parametrize("k", [23, 24, 25, 40, 90])
+def test_crowded_neighbourhoods(eng, orc, k):
+    """An agent with exactly k agents inside its radius (around the per-agent list
+    capacity of the tile kernel and beyond): bit-exact vs the oracle."""
+    from paper_2503_10796_b200 import Agents
+    rng = np.random.default_rng(k)
+    # k neighbours inside a ball of radius 9 (R = 10) around the origin + sparse others
+    v = rng.normal(size=(k, 3))
+    v *= (rng.uniform(0.2, 0.9, k) ** (1 / 3) * 9.0 / np.linalg.norm(v, axis=1))[:, None]
+    far = rng.uniform(-60, 60, (300, 3))
+    pts = np.vstack([[0, 0, 0], v, far])
+    n = len(pts)
+    s = {"x": pts[:, 0].copy(), "y": pts[:, 1].copy(), "z": pts[:, 2].copy(),
+         "d": np.full(n, 10.0), "id": np.arange(n, dtype=np.uint32),
+         "flags": np.full(n, 4, np.uint32)}
+    gp, op = params_pair(orc, W.CFG1)
+    a = Agents.from_numpy(s)
+    for t in range(2):
+        eng.step(a, gp)
+        s, _ = orc.step_full(s, op)
+        assert_state_equal(a.numpy(), s, f"k={k} step {t}")
+
+
 def test_capacity_overflow_is_recovered(eng, orc):
     """An agent far outside the first grid's extent exceeds the slot capacity; the
     overflowed step is a no-op and the binding grows the slots and re-issues it."""
