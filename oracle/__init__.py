@@ -82,6 +82,11 @@ def lib() -> ctypes.CDLL:
         L.orc_division_axis.argtypes = [u64, u64, ctypes.c_uint32, P]
         L.orc_grow_divide.argtypes = [i64, P, P, P, P, P, P, P, i64, dbl, dbl, u64, ctypes.c_uint32]
         L.orc_grow_divide.restype = i64
+        L.orc_wrap.argtypes = [dbl, dbl]
+        L.orc_wrap.restype = dbl
+        L.orc_sir_step.argtypes = [i64, P, P, P, P, P, dbl, dbl, dbl, dbl, u64, ctypes.c_uint32, P]
+        L.orc_sir_step.restype = i64
+        L.orc_init_sir.argtypes = [i64, u64, dbl, i64, P, P, P, P, P]
         _lib = L
     return _lib
 
@@ -309,3 +314,36 @@ def cfg3_step(s, params: MechParams, growth, v_max, seed, step):
     post = {"x": out["x"], "y": out["y"], "z": out["z"], "d": s["d"], "vol": s["vol"],
             "id": s["id"], "flags": out["flags"]}
     return grow_divide(post, growth, v_max, seed, step), cnt
+
+
+# ---------------------------------------------------------------- SIR epidemiology (cfg4)
+S_, I_, R_ = 0, 1, 2
+
+
+def wrap(el: float, max_bound: float) -> float:
+    """Alg. 9 toroidal wrap, literal (R20)."""
+    return lib().orc_wrap(el, max_bound)
+
+
+def init_sir(n, seed, side, n_infected):
+    s = {k: np.zeros(n, np.float64) for k in ("x", "y", "z")}
+    s["state"] = np.zeros(n, np.uint8)
+    s["id"] = np.zeros(n, np.uint32)
+    lib().orc_init_sir(n, seed, side, n_infected, _p(s["x"]), _p(s["y"]), _p(s["z"]),
+                       _p(s["state"]), _p(s["id"]))
+    return s
+
+
+def sir_step(s, side, radius, p_inf, p_rec, seed, step):
+    """Algorithms 7-9 (R16-R20, R22) on a copy of s; returns (new state, counts, new
+    infections)."""
+    out = {k: np.array(v, copy=True) for k, v in s.items()}
+    n = len(out["x"])
+    for k in ("x", "y", "z"):
+        out[k] = np.ascontiguousarray(out[k], np.float64)
+    out["state"] = np.ascontiguousarray(out["state"], np.uint8)
+    ids = np.ascontiguousarray(out["id"], np.uint32)
+    counts = np.zeros(3, np.int64)
+    ni = lib().orc_sir_step(n, _p(out["x"]), _p(out["y"]), _p(out["z"]), _p(out["state"]),
+                            _p(ids), side, radius, p_inf, p_rec, seed, step, _p(counts))
+    return out, counts, ni

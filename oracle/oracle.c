@@ -636,3 +636,165 @@ int64_t orc_grow_divide(int64_t n, double *x, double *y, double *z, double *d, d
     free(by_id);
     return n + ndiv;
 }
+
+/* ------------------------------------------------------------------------------ */
+/* SIR epidemiology step (cfg4): Algorithms 7-9 (algo:infection P:3220-3249,        */
+/* algo:recovery P:3251-3270, algo:random-movement P:3272-3303).  Readings:          */
+/*   R16  movement v = 2u - 1 per axis, capped: if v.v > 1 then v = v / sqrt(v.v)   */
+/*   R17  draws compared with '<' (u = w 2^-32)                                      */
+/*   R18  order infection -> recovery -> movement; neighbours' states and positions  */
+/*        from the start-of-step snapshot; own state updated in sequence             */
+/*   R19  periodic neighbour search with minimum-image differences                    */
+/*   R20  Alg. 9 wrap taken literally: el = fmod(el, max); if el < 0: el = max + el   */
+/*   R22  Philox counter (id, step, 0) -> movement w0..w2 + infection w3;             */
+/*        (id, step, 1) -> recovery w0                                              */
+/* No fused multiply-add anywhere (BASELINE: "FMA contraction off").                 */
+/* ------------------------------------------------------------------------------ */
+enum { ORC_S = 0, ORC_I = 1, ORC_R = 2 };
+
+double orc_wrap(double el, double max_bound)
+{
+    el = fmod(el, max_bound);
+    if (el < 0.0) el = max_bound + el;
+    return el;
+}
+
+static double min_image(double d, double side)
+{
+    double half = side * 0.5;
+    if (d > half) d = d - side;
+    else if (d < -half) d = d + side;
+    return d;
+}
+
+typedef struct {
+    int64_t key;   /* (bz*D + by)*D + bx */
+    int64_t idx;
+} orc_kv;
+
+static int cmp_kv(const void *pa, const void *pb)
+{
+    const orc_kv *a = pa, *b = pb;
+    if (a->key != b->key) return a->key < b->key ? -1 : 1;
+    return a->idx < b->idx ? -1 : (a->idx > b->idx);
+}
+
+static int64_t sir_box(double v, double L, int64_t D)
+{
+    int64_t b = (int64_t)floor(v / L);
+    if (b < 0) b = 0;
+    if (b > D - 1) b = D - 1;
+    return b;
+}
+
+/* Updates x, y, z, state in place for n agents in a periodic cube [0, side)^3 with
+ * D = floor(side / radius) boxes of edge L = side / D per axis (needs D >= 3).
+ * counts[0..2] receives S, I, R after the step; returns the number of new infections. */
+int64_t orc_sir_step(int64_t n, double *x, double *y, double *z, uint8_t *state,
+                     const uint32_t *id, double side, double radius, double p_inf,
+                     double p_rec, uint64_t seed, uint32_t step, int64_t counts[3])
+{
+    int64_t D = (int64_t)floor(side / radius);
+    double L = side / (double)D;
+    double R2 = radius * radius;
+    double *x0 = malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
+    double *y0 = malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
+    double *z0 = malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
+    uint8_t *s0 = malloc((size_t)(n > 0 ? n : 1));
+    memcpy(x0, x, sizeof(double) * (size_t)n);
+    memcpy(y0, y, sizeof(double) * (size_t)n);
+    memcpy(z0, z, sizeof(double) * (size_t)n);
+    memcpy(s0, state, (size_t)n);
+    /* index of the infected agents of the snapshot, sorted by box */
+    int64_t ni = 0;
+    for (int64_t i = 0; i < n; ++i) ni += (s0[i] == ORC_I);
+    orc_kv *inf = malloc(sizeof(orc_kv) * (size_t)(ni > 0 ? ni : 1));
+    ni = 0;
+    for (int64_t i = 0; i < n; ++i)
+        if (s0[i] == ORC_I) {
+            int64_t bx = sir_box(x0[i], L, D), by = sir_box(y0[i], L, D), bz = sir_box(z0[i], L, D);
+            inf[ni].key = (bz * D + by) * D + bx;
+            inf[ni].idx = i;
+            ++ni;
+        }
+    qsort(inf, (size_t)ni, sizeof(orc_kv), cmp_kv);
+
+    int64_t new_inf = 0;
+    counts[0] = counts[1] = counts[2] = 0;
+    for (int64_t i = 0; i < n; ++i) {
+        uint32_t w[4];
+        philox_draw(seed, id[i], step, 0u, w);
+        uint8_t st = s0[i];
+        /* Alg. 7: a susceptible agent, with probability p_inf, becomes infected if an
+         * infected agent is within the infection radius */
+        if (st == ORC_S && orc_u32(w[3]) < p_inf) {
+            int64_t bx = sir_box(x0[i], L, D), by = sir_box(y0[i], L, D), bz = sir_box(z0[i], L, D);
+            int found = 0;
+            for (int dz = -1; dz <= 1 && !found; ++dz)
+                for (int dy = -1; dy <= 1 && !found; ++dy)
+                    for (int dx = -1; dx <= 1 && !found; ++dx) {
+                        int64_t cx = ((bx + dx) % D + D) % D, cy = ((by + dy) % D + D) % D,
+                                cz = ((bz + dz) % D + D) % D;
+                        int64_t key = (cz * D + cy) * D + cx;
+                        int64_t lo = 0, hi = ni;
+                        while (lo < hi) {
+                            int64_t mid = (lo + hi) / 2;
+                            if (inf[mid].key < key) lo = mid + 1; else hi = mid;
+                        }
+                        for (int64_t s = lo; s < ni && inf[s].key == key; ++s) {
+                            int64_t j = inf[s].idx;
+                            double ex = min_image(x0[i] - x0[j], side);
+                            double ey = min_image(y0[i] - y0[j], side);
+                            double ez = min_image(z0[i] - z0[j], side);
+                            double Dd = ex * ex + ey * ey + ez * ez;
+                            if (Dd <= R2) { found = 1; break; }
+                        }
+                    }
+            if (found) {
+                st = ORC_I;
+                ++new_inf;
+            }
+        }
+        /* Alg. 8: an infected agent recovers with probability p_rec */
+        if (st == ORC_I) {
+            uint32_t wr[4];
+            philox_draw(seed, id[i], step, 1u, wr);
+            if (orc_u32(wr[0]) < p_rec) st = ORC_R;
+        }
+        state[i] = st;
+        counts[st] += 1;
+        /* Alg. 9: random movement, capped at unit length (R16), toroidal wrap (R20) */
+        double vx = 2.0 * orc_u32(w[0]) - 1.0;
+        double vy = 2.0 * orc_u32(w[1]) - 1.0;
+        double vz = 2.0 * orc_u32(w[2]) - 1.0;
+        double v2 = vx * vx + vy * vy + vz * vz;
+        if (v2 > 1.0) {
+            double nv = sqrt(v2);
+            vx = vx / nv;
+            vy = vy / nv;
+            vz = vz / nv;
+        }
+        x[i] = orc_wrap(x0[i] + vx, side);
+        y[i] = orc_wrap(y0[i] + vy, side);
+        z[i] = orc_wrap(z0[i] + vz, side);
+    }
+    free(x0); free(y0); free(z0); free(s0); free(inf);
+    return new_inf;
+}
+
+/* Population for cfg4: uniform in [0, side)^3 (same per-id recipe as the spheres),
+ * ids < n_infected start infected (R21), all others susceptible. */
+void orc_init_sir(int64_t n, uint64_t seed, double side, int64_t n_infected, double *x,
+                  double *y, double *z, uint8_t *state, uint32_t *id)
+{
+    for (int64_t k = 0; k < n; ++k) {
+        uint32_t w[4];
+        philox_draw(seed, (uint64_t)k, 0xFFFFFFFFu, 2u, w);
+        x[k] = orc_u53(w[0], w[1]) * side;
+        y[k] = orc_u53(w[2], w[3]) * side;
+        philox_draw(seed, (uint64_t)k, 0xFFFFFFFEu, 2u, w);
+        z[k] = orc_u53(w[0], w[1]) * side;
+        id[k] = (uint32_t)k;
+        state[k] = (k < n_infected) ? ORC_I : ORC_S;
+    }
+}
