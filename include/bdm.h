@@ -193,6 +193,23 @@ bdm_status bdm_step_host(bdm_handle h, const bdm_agents *host_in, bdm_agents *ho
 bdm_status bdm_grow_divide(bdm_handle h, bdm_agents *a, const bdm_params *p, double growth,
                            double v_max, int64_t *n_out_host, void *stream);
 
+/* SIR epidemiology step (Algorithms 7-9) on point
+ * agents (x, y, z, state; id nullable = index) in the periodic cube [0, side)^3, in
+ * place.  For every agent, from the start-of-step snapshot (R16-R22):
+ *   w = Philox(seed, (id, p->step, 0)); if S and u32(w3) < p_inf and an agent that was
+ *   infected at the start of the step lies within `radius` (minimum image): I;
+ *   if I and u32(Philox(seed, (id, p->step, 1)).w0) < p_rec: R;
+ *   v = 2 u32(w0..w2) - 1, v /= |v| if |v| > 1; x = wrap(x + v) with Alg. 9's
+ *   el = fmod(el, side); if el < 0: el = side + el.
+ * No fused multiply-add.  Needs side/radius >= 3.  If counts_host (pinned, 4 int64)
+ * is non-NULL it receives S, I, R after the step and the number of new infections
+ * (asynchronously).  The infected index holds up to max(65536, n/16) agents (option
+ * "sir_index_capacity"); beyond that the step is a no-op and bdm_sync reports
+ * BDM_ECAPACITY.  Errors: BDM_EINVAL. */
+bdm_status bdm_sir_step(bdm_handle h, bdm_agents *a, const bdm_params *p, double side,
+                        double radius, double p_inf, double p_rec, int64_t *counts_host,
+                        void *stream);
+
 /* Synchronize `stream` and report latched device conditions: BDM_ECAPACITY (grid
  * slots exceeded; bdm_get_grid_info gives the needed nslots), BDM_ENOTFINITE, or a
  * CUDA error.  Clears the latched condition. */
@@ -221,6 +238,7 @@ bdm_status bdm_neighbor_pairs(bdm_handle h, const bdm_agents *a, double radius,
  *   "mech_kernel"  0 (default) tile kernel: CTA per 4x4x4-box tile with the halo staged
  *                  in shared memory and a lane-parallel pair queue;
  *                  1 per-agent reference kernel reading neighbours from global memory.
+ *   "sir_index_capacity"  infected agents the SIR index holds (0 = max(65536, n/16)).
  *   "prefilter"    1 (default) / 0: conservative fp32 candidate test in the tile kernel
  *                  (never rejects a neighbour; the exact fp64 test decides).
  * All settings produce bit-identical results.  Errors: BDM_EINVAL for an unknown name/value. */

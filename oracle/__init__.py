@@ -87,6 +87,9 @@ def lib() -> ctypes.CDLL:
         L.orc_sir_step.argtypes = [i64, P, P, P, P, P, dbl, dbl, dbl, dbl, u64, ctypes.c_uint32, P]
         L.orc_sir_step.restype = i64
         L.orc_init_sir.argtypes = [i64, u64, dbl, i64, P, P, P, P, P]
+        L.orc_sir_step_sample.argtypes = [i64, P, P, P, P, P, dbl, dbl, dbl, dbl, u64,
+                                          ctypes.c_uint32, i64, P, P, P, P, P, P]
+        L.orc_sir_step_sample.restype = i64
         _lib = L
     return _lib
 
@@ -346,4 +349,20 @@ def sir_step(s, side, radius, p_inf, p_rec, seed, step):
     counts = np.zeros(3, np.int64)
     ni = lib().orc_sir_step(n, _p(out["x"]), _p(out["y"]), _p(out["z"]), _p(out["state"]),
                             _p(ids), side, radius, p_inf, p_rec, seed, step, _p(counts))
+    return out, counts, ni
+
+
+def sir_step_sample(s, side, radius, p_inf, p_rec, seed, step, sample):
+    """SIR step for the listed agents only (full snapshot for the infected index)."""
+    x, y, z = _f64(s["x"]), _f64(s["y"]), _f64(s["z"])
+    st = np.ascontiguousarray(s["state"], np.uint8)
+    ids = _u32(s["id"])
+    idx = np.ascontiguousarray(sample, np.int64)
+    m = len(idx)
+    out = {k: np.zeros(m, np.float64) for k in ("x", "y", "z")}
+    out["state"] = np.zeros(m, np.uint8)
+    counts = np.zeros(3, np.int64)
+    ni = lib().orc_sir_step_sample(len(x), _p(x), _p(y), _p(z), _p(st), _p(ids), side, radius,
+                                   p_inf, p_rec, seed, step, m, _p(idx), _p(out["x"]),
+                                   _p(out["y"]), _p(out["z"]), _p(out["state"]), _p(counts))
     return out, counts, ni

@@ -690,21 +690,44 @@ static int64_t sir_box(double v, double L, int64_t D)
 /* Updates x, y, z, state in place for n agents in a periodic cube [0, side)^3 with
  * D = floor(side / radius) boxes of edge L = side / D per axis (needs D >= 3).
  * counts[0..2] receives S, I, R after the step; returns the number of new infections. */
+/* Sampled form: computes the step for the m agents idx[0..m) (NULL: all, m = n) from
+ * the full snapshot (x, y, z, state) and writes their new values to the out arrays
+ * (position k for the k-th listed agent).  Inputs are not modified. */
+int64_t orc_sir_step_sample(int64_t n, const double *x, const double *y, const double *z,
+                            const uint8_t *state, const uint32_t *id, double side,
+                            double radius, double p_inf, double p_rec, uint64_t seed,
+                            uint32_t step, int64_t m, const int64_t *idx, double *ox,
+                            double *oy, double *oz, uint8_t *ostate, int64_t counts[3]);
+
 int64_t orc_sir_step(int64_t n, double *x, double *y, double *z, uint8_t *state,
                      const uint32_t *id, double side, double radius, double p_inf,
                      double p_rec, uint64_t seed, uint32_t step, int64_t counts[3])
 {
+    double *ox = malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
+    double *oy = malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
+    double *oz = malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
+    uint8_t *os = malloc((size_t)(n > 0 ? n : 1));
+    int64_t r = orc_sir_step_sample(n, x, y, z, state, id, side, radius, p_inf, p_rec, seed,
+                                    step, n, NULL, ox, oy, oz, os, counts);
+    memcpy(x, ox, sizeof(double) * (size_t)n);
+    memcpy(y, oy, sizeof(double) * (size_t)n);
+    memcpy(z, oz, sizeof(double) * (size_t)n);
+    memcpy(state, os, (size_t)n);
+    free(ox); free(oy); free(oz); free(os);
+    return r;
+}
+
+int64_t orc_sir_step_sample(int64_t n, const double *x, const double *y, const double *z,
+                            const uint8_t *state, const uint32_t *id, double side,
+                            double radius, double p_inf, double p_rec, uint64_t seed,
+                            uint32_t step, int64_t m, const int64_t *idx, double *ox,
+                            double *oy, double *oz, uint8_t *ostate, int64_t counts[3])
+{
     int64_t D = (int64_t)floor(side / radius);
     double L = side / (double)D;
     double R2 = radius * radius;
-    double *x0 = malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
-    double *y0 = malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
-    double *z0 = malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
-    uint8_t *s0 = malloc((size_t)(n > 0 ? n : 1));
-    memcpy(x0, x, sizeof(double) * (size_t)n);
-    memcpy(y0, y, sizeof(double) * (size_t)n);
-    memcpy(z0, z, sizeof(double) * (size_t)n);
-    memcpy(s0, state, (size_t)n);
+    const double *x0 = x, *y0 = y, *z0 = z;   /* the snapshot (inputs are read-only) */
+    const uint8_t *s0 = state;
     /* index of the infected agents of the snapshot, sorted by box */
     int64_t ni = 0;
     for (int64_t i = 0; i < n; ++i) ni += (s0[i] == ORC_I);
@@ -721,7 +744,8 @@ int64_t orc_sir_step(int64_t n, double *x, double *y, double *z, uint8_t *state,
 
     int64_t new_inf = 0;
     counts[0] = counts[1] = counts[2] = 0;
-    for (int64_t i = 0; i < n; ++i) {
+    for (int64_t k = 0; k < m; ++k) {
+        int64_t i = idx ? idx[k] : k;
         uint32_t w[4];
         philox_draw(seed, id[i], step, 0u, w);
         uint8_t st = s0[i];
@@ -761,7 +785,7 @@ int64_t orc_sir_step(int64_t n, double *x, double *y, double *z, uint8_t *state,
             philox_draw(seed, id[i], step, 1u, wr);
             if (orc_u32(wr[0]) < p_rec) st = ORC_R;
         }
-        state[i] = st;
+        ostate[k] = st;
         counts[st] += 1;
         /* Alg. 9: random movement, capped at unit length (R16), toroidal wrap (R20) */
         double vx = 2.0 * orc_u32(w[0]) - 1.0;
@@ -774,11 +798,11 @@ int64_t orc_sir_step(int64_t n, double *x, double *y, double *z, uint8_t *state,
             vy = vy / nv;
             vz = vz / nv;
         }
-        x[i] = orc_wrap(x0[i] + vx, side);
-        y[i] = orc_wrap(y0[i] + vy, side);
-        z[i] = orc_wrap(z0[i] + vz, side);
+        ox[k] = orc_wrap(x0[i] + vx, side);
+        oy[k] = orc_wrap(y0[i] + vy, side);
+        oz[k] = orc_wrap(z0[i] + vz, side);
     }
-    free(x0); free(y0); free(z0); free(s0); free(inf);
+    free(inf);
     return new_inf;
 }
 

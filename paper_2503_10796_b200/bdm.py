@@ -24,7 +24,7 @@ EXPORTS = [
     "bdm_create", "bdm_destroy", "bdm_last_error", "bdm_version", "bdm_init_spheres",
     "bdm_grid_build", "bdm_mech_step", "bdm_step", "bdm_step_host", "bdm_sync", "bdm_reserve",
     "bdm_get_stats", "bdm_get_grid_info", "bdm_neighbor_pairs", "bdm_peak_dfma",
-    "bdm_set_option", "bdm_grow_divide",
+    "bdm_set_option", "bdm_grow_divide", "bdm_sir_step",
 ]
 
 
@@ -97,6 +97,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "bdm_peak_dfma": [P, ctypes.POINTER(dbl), ctypes.POINTER(i32)],
         "bdm_set_option": [P, ctypes.c_char_p, i64],
         "bdm_grow_divide": [P, AG, PR, dbl, dbl, P, P],
+        "bdm_sir_step": [P, AG, PR, dbl, dbl, dbl, dbl, P, P],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -194,8 +195,10 @@ class Agents:
         n = self.n
         out = {k: getattr(self, k)[:n].cpu().numpy() for k in ("x", "y", "z", "diameter")}
         out["d"] = out.pop("diameter")
-        out["id"] = self.id[:n].cpu().numpy().view(np.uint32)
-        out["flags"] = self.flags[:n].cpu().numpy().view(np.uint32)
+        if self.id is not None:
+            out["id"] = self.id[:n].cpu().numpy().view(np.uint32)
+        if self.flags is not None:
+            out["flags"] = self.flags[:n].cpu().numpy().view(np.uint32)
         if self.volume is not None:
             out["vol"] = self.volume[:n].cpu().numpy()
         if self.state is not None:
@@ -305,6 +308,31 @@ class Engine:
         self.sync(stream)
         agents.n = int(self._n_out[0])
         return agents.n
+
+    def sir_step(self, agents: Agents, params: Params, side: float, radius: float,
+                 p_inf: float, p_rec: float, stream=None, sync: bool = True):
+        """bdm_sir_step.  With sync=True returns the counts (S, I, R, new infections); if
+        the infected index was too small (the step is then a no-op) it is enlarged to n
+        and the step re-issued."""
+        import torch
+        if not hasattr(self, "_sir_counts"):
+            self._sir_counts = torch.zeros(4, dtype=torch.int64, pin_memory=True)
+        for attempt in range(2):
+            ca = agents.c()
+            cp = params.c()
+            _check(self.lib.bdm_sir_step(self.h, ctypes.byref(ca), ctypes.byref(cp), float(side),
+                                         float(radius), float(p_inf), float(p_rec),
+                                         ctypes.c_void_p(self._sir_counts.data_ptr()),
+                                         _stream_ptr(stream)))
+            if not sync:
+                return None
+            st = self.lib.bdm_sync(self.h, _stream_ptr(stream))
+            if st == BDM_ECAPACITY and attempt == 0 and getattr(self, "_sir_autogrow", True):
+                self.set_option("sir_index_capacity", max(int(agents.n), 1))
+                continue
+            _check(st)
+            return [int(v) for v in self._sir_counts]
+        return None
 
     def cfg3_step(self, agents: Agents, params: Params, growth: float, v_max: float,
                   stream=None) -> int:

@@ -15,7 +15,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 SO = os.path.join(HERE, "libbdm.so")
-SOURCES = ["bdm_abi.cu", "kernels_grid.cu", "kernels_mech.cu", "kernels_divide.cu"]
+SOURCES = ["bdm_abi.cu", "kernels_grid.cu", "kernels_mech.cu", "kernels_divide.cu",
+           "kernels_sir.cu"]
 HEADERS = ["bdm_internal.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 

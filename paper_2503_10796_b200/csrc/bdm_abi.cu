@@ -104,6 +104,8 @@ static bdm_status read_latches(Ctx *c, bool clear) {
     bdm_status st = BDM_OK;
     if (c->sc_host->nonfinite) {
         st = fail(BDM_ENOTFINITE, "a position or diameter is NaN/Inf");
+    } else if (c->sc_host->overflow == 3) {
+        st = fail(BDM_ECAPACITY, "SIR infected index too small (raise option sir_index_capacity)");
     } else if (c->sc_host->overflow == 2) {
         st = fail(BDM_ECAPACITY, "agent capacity too small for the daughters of this step");
     } else if (c->sc_host->overflow) {
@@ -167,6 +169,10 @@ bdm_status bdm_destroy(bdm_handle h) {
                     c->block_sums, c->pair_count, c->n_new, c->sc};
     for (void *p : bufs)
         if (p) cudaFree(p);
+    void *sbufs[] = {c->sir.keys, c->sir.heads, c->sir.next, c->sir.bitmap, c->sir.ix, c->sir.iy,
+                     c->sir.iz, c->sir.misc};
+    for (void *q : sbufs)
+        if (q) cudaFree(q);
     if (c->sc_host) cudaFreeHost(c->sc_host);
     delete c;
     return BDM_OK;
@@ -292,6 +298,22 @@ bdm_status bdm_grow_divide(bdm_handle h, bdm_agents *a, const bdm_params *p, dou
                               (long long *)n_out_host, (cudaStream_t)stream);
 }
 
+bdm_status bdm_sir_step(bdm_handle h, bdm_agents *a, const bdm_params *p, double side,
+                        double radius, double p_inf, double p_rec, int64_t *counts_host,
+                        void *stream) {
+    if (!h || !p || !a) return fail(BDM_EINVAL, "NULL argument");
+    Ctx *c = (Ctx *)h;
+    if (a->n < 0 || a->n > a->capacity) return fail(BDM_EINVAL, "n < 0 or n > capacity");
+    if (a->n > 0 && (!a->x || !a->y || !a->z || !a->state))
+        return fail(BDM_EINVAL, "SIR needs x, y, z and state");
+    if (!(side > 0.0) || !(radius > 0.0)) return fail(BDM_EINVAL, "side and radius must be > 0");
+    if (!(p_inf >= 0.0 && p_inf <= 1.0) || !(p_rec >= 0.0 && p_rec <= 1.0))
+        return fail(BDM_EINVAL, "probabilities must be in [0, 1]");
+    c->grid_valid = false;
+    return launch_sir_step(c, a, p, side, radius, p_inf, p_rec, (long long *)counts_host,
+                           (cudaStream_t)stream);
+}
+
 bdm_status bdm_sync(bdm_handle h, void *stream) {
     if (!h) return fail(BDM_EINVAL, "handle is NULL");
     Ctx *c = (Ctx *)h;
@@ -365,6 +387,11 @@ bdm_status bdm_set_option(bdm_handle h, const char *name, int64_t value) {
     if (strcmp(name, "mech_kernel") == 0) {
         if (value < 0 || value > 1) return fail(BDM_EINVAL, "mech_kernel must be 0 or 1");
         c->mech_kernel = (int)value;
+        return BDM_OK;
+    }
+    if (strcmp(name, "sir_index_capacity") == 0) {
+        if (value < 0) return fail(BDM_EINVAL, "sir_index_capacity must be >= 0");
+        c->sir.icap_override = value;
         return BDM_OK;
     }
     if (strcmp(name, "prefilter") == 0) {

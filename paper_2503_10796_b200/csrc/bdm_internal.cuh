@@ -45,6 +45,16 @@ struct DevScalars {
     unsigned long long stats[5];  // cand, nbr, cont, n_static, n_moved
 };
 
+// SIR workspace (kernels_sir.cu), allocated on first use
+struct SirWs {
+    unsigned long long *keys = nullptr;
+    uint32_t *heads = nullptr, *next = nullptr, *bitmap = nullptr;
+    double *ix = nullptr, *iy = nullptr, *iz = nullptr;
+    void *misc = nullptr;   // infected count + 4 counters
+    int64_t icap = 0, tsize = 0, bwords = 0;
+    int64_t icap_override = 0;
+};
+
 // ------------------------------------------------------------------ library context
 struct Ctx {
     int device = 0;
@@ -75,6 +85,7 @@ struct Ctx {
     int64_t launches = 0;  // kernels launched (host-side count)
     int mech_kernel = 0;   // option "mech_kernel": 0 tile kernel, 1 per-agent reference kernel
     int prefilter = 1;     // option "prefilter": fp32 conservative candidate test in the tile kernel
+    SirWs sir;
 };
 
 // ------------------------------------------------------------------ device helpers
@@ -140,6 +151,9 @@ bdm_status launch_pairs(Ctx *c, int64_t n, uint64_t *pairs, int64_t cap, cudaStr
 bdm_status launch_peak_dfma(int sm_count, double *dfma_per_s);
 // generic exclusive scan of m u32 values in place (kernels_grid.cu)
 bdm_status launch_scan_u32(Ctx *c, uint32_t *data, long long m, cudaStream_t st);
+// SIR (kernels_sir.cu)
+bdm_status launch_sir_step(Ctx *c, bdm_agents *a, const bdm_params *p, double side, double radius,
+                           double p_inf, double p_rec, long long *counts_host, cudaStream_t st);
 // growth + division (kernels_divide.cu)
 bdm_status launch_grow_divide(Ctx *c, bdm_agents *a, double growth, double v_max, double vol_to_r3,
                               uint64_t seed, uint32_t step, long long *n_new_host, cudaStream_t st);

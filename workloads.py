@@ -59,4 +59,39 @@ def cfg2_scaled(n: int) -> MechConfig:
 CFG5 = MechConfig("cfg5", 1_700_000_000, side_for_fraction(1_700_000_000, 1000.0, 0.5),
                   10.0, 0.0, False, 10, False)
 
-PRESETS = {"cfg1": CFG1, "cfg2": CFG2, "cfg5": CFG5}
+# configs[2]: cell proliferation, 1M spheres d = 8 um in a 1 mm cube, +400 um^3 per
+# step, divide at d = 12 um (V >= (M_PI/6)*1728), mechanics each step, 20 steps.
+CFG3 = MechConfig("cfg3", 1_000_000, 1000.0, 8.0, 0.0, False, 20, False)
+CFG3_GROWTH = 400.0
+CFG3_V_MAX = (math.pi / 6.0) * 1728.0
+
+
+@dataclass(frozen=True)
+class SirConfig:
+    name: str
+    n: int
+    side: float           # periodic cube edge [m]
+    radius: float         # infection radius [m]
+    p_inf: float
+    p_rec: float
+    n_infected: int       # ids < n_infected start infected (R21)
+    steps: int
+    seed: int = 1
+
+    def to_dict(self):
+        return asdict(self)
+
+
+# configs[3]: 100M point agents in a periodic 10 km cube, radius 2 m, p_inf 0.1,
+# p_rec 0.01, 0.1 % initially infected, 200 steps.
+CFG4 = SirConfig("cfg4", 100_000_000, 10_000.0, 2.0, 0.1, 0.01, 100_000, 200)
+
+
+def cfg4_scaled(n: int, side: float = None) -> SirConfig:
+    """cfg4's parameters at n agents (default: cfg4's density)."""
+    if side is None:
+        side = CFG4.side * (n / CFG4.n) ** (1.0 / 3.0)
+    return SirConfig(f"cfg4@{n}", n, side, 2.0, 0.1, 0.01, max(1, n // 1000), 200)
+
+
+PRESETS = {"cfg1": CFG1, "cfg2": CFG2, "cfg3": CFG3, "cfg4": CFG4, "cfg5": CFG5}
