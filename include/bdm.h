@@ -139,8 +139,10 @@ bdm_status bdm_init_spheres(bdm_handle h, bdm_agents *a, int64_t id0, int64_t n,
  *   a4  counting sort by key, ascending id inside a box, gather of the SoA into
  *       the library's sorted workspace.
  * `ghosts` (nullable) are read-only agents owned by a neighbouring rank (aura,
- * P:6083-6106); they enter the grid but are never updated.  Not yet supported:
- * a non-NULL `ghosts` returns BDM_ENOTIMPL.
+ * P:6083-6106): they enter the grid (and the canonical order) but are never
+ * updated; the following bdm_mech_step writes only the local agents.
+ * With a frame set by bdm_set_frame, the origin and R come from the frame (the
+ * global grid of a multi-GPU run) and only the lattice extent is local.
  * The first call for a given context synchronizes once to size the slot array;
  * later calls are asynchronous.  Errors: BDM_EINVAL, BDM_ECUDA. */
 bdm_status bdm_grid_build(bdm_handle h, const bdm_agents *a, const bdm_agents *ghosts,
@@ -209,6 +211,39 @@ bdm_status bdm_grow_divide(bdm_handle h, bdm_agents *a, const bdm_params *p, dou
 bdm_status bdm_sir_step(bdm_handle h, bdm_agents *a, const bdm_params *p, double side,
                         double radius, double p_inf, double p_rec, int64_t *counts_host,
                         void *stream);
+
+/* ---- multi-GPU x-slabs (TeraAgent partitioning P:6058-6081, aura
+ * P:6083-6106, migration P:6116-6126).  The transport between ranks is the
+ * caller's (torch.distributed over NCCL in paper_2503_10796_b200/slabs.py); these
+ * calls are the device side: the global frame, packing and appending. */
+#define BDM_PACK_MIGRATE 1  /* x < lo -> left, x >= hi -> right; leavers removed        */
+#define BDM_PACK_AURA 2     /* x < lo + margin -> left, x >= hi - margin -> right; copy */
+
+/* Local frame of `a`: frame_dev[0..2] = exact per-axis minimum of x, y, z and
+ * frame_dev[3] = -(largest diameter) (device memory, 4 doubles).  An element-wise
+ * MIN all-reduce of the ranks' frames gives the global frame (R12: origin = minimum
+ * corner, R = largest diameter).  n == 0 gives (+inf, +inf, +inf, +inf). */
+bdm_status bdm_local_frame(bdm_handle h, const bdm_agents *a, double *frame_dev, void *stream);
+
+/* Use the global frame at frame_dev (device, 4 doubles as above; must stay valid) for
+ * subsequent grid builds, or NULL to return to the local frame (single GPU). */
+bdm_status bdm_set_frame(bdm_handle h, const double *frame_dev);
+
+/* Pack agents of `a` for the slab [lo, hi) into the caller's send buffers
+ * to_left / to_right (device SoA; x, y, z, diameter, id, flags, volume if both have
+ * it), order preserving.  BDM_PACK_MIGRATE: x < lo -> left, x >= hi -> right, and the
+ * leavers are removed from `a` by an order-preserving compaction.  BDM_PACK_AURA:
+ * x < lo + margin -> left, x >= hi - margin -> right (copies; `a` unchanged).
+ * counts_host (pinned, 3 int64, asynchronous) receives #left, #right, #remaining;
+ * to_left->n, to_right->n and a->n are NOT updated.  If a send buffer is too small
+ * nothing is modified, the counts are negated and bdm_sync reports BDM_ECAPACITY. */
+bdm_status bdm_pack_slab(bdm_handle h, bdm_agents *a, double lo, double hi, double margin,
+                         int32_t what, bdm_agents *to_left, bdm_agents *to_right,
+                         int64_t *counts_host, void *stream);
+
+/* Append src[0, src->n) at dst[dst->n, ...) (device to device) and add src->n to
+ * dst->n.  Errors: BDM_ECAPACITY if dst->n + src->n > dst->capacity. */
+bdm_status bdm_append(bdm_handle h, bdm_agents *dst, const bdm_agents *src, void *stream);
 
 /* Synchronize `stream` and report latched device conditions: BDM_ECAPACITY (grid
  * slots exceeded; bdm_get_grid_info gives the needed nslots), BDM_ENOTFINITE, or a

@@ -120,6 +120,9 @@ class MechParams(ctypes.Structure):
         ("boundary", ctypes.c_int32),
         ("lo", ctypes.c_double * 3),
         ("hi", ctypes.c_double * 3),
+        ("use_frame", ctypes.c_int32),
+        ("pad_", ctypes.c_int32),
+        ("frame", ctypes.c_double * 4),
     ]
 
 
@@ -128,8 +131,13 @@ class Counters(ctypes.Structure):
 
 
 def mech_params(k=2.0, gamma=1.0, dt=0.01, max_disp=3.0, force_threshold=0.0, radius=0.0,
-                detect_static=False, boundary=0, lo=(0.0, 0.0, 0.0), hi=(0.0, 0.0, 0.0)):
+                detect_static=False, boundary=0, lo=(0.0, 0.0, 0.0), hi=(0.0, 0.0, 0.0),
+                frame=None):
+    """frame: optional global grid frame (o_x, o_y, o_z, R) of a partitioned run."""
     p = MechParams()
+    if frame is not None:
+        p.use_frame = 1
+        p.frame[:] = [float(v) for v in frame]
     p.k, p.gamma, p.dt, p.max_disp = k, gamma, dt, max_disp
     p.force_threshold, p.radius = force_threshold, radius
     p.detect_static, p.boundary = int(bool(detect_static)), int(boundary)

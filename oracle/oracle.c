@@ -207,11 +207,29 @@ static int64_t lin_box(const orc_grid *g, int64_t bx, int64_t by, int64_t bz)
     return (bz * g->D[1] + by) * g->D[0] + bx;
 }
 
+/* frame (nullable): a global grid frame (o[3], R) shared by the ranks of a
+ * partitioned run: the origin and R come from it, the box count from the
+ * agents' extent measured from that origin. */
 static void index_build(orc_index *ix, int64_t n, const double *x, const double *y,
-                        const double *z, const double *d, const uint32_t *id, double radius)
+                        const double *z, const double *d, const uint32_t *id, double radius,
+                        const double *frame)
 {
     ix->n = n;
     orc_grid_geometry(n, x, y, z, d, radius, &ix->g.R, &ix->g.L, ix->g.o, ix->g.D);
+    if (frame) {
+        double R = radius > 0.0 ? radius : frame[3];
+        double L = R * (1.0 + 0x1p-20);
+        ix->g.R = R;
+        ix->g.L = L;
+        for (int a = 0; a < 3; ++a) {
+            double hi = frame[a];
+            const double *p = a == 0 ? x : a == 1 ? y : z;
+            for (int64_t i = 0; i < n; ++i)
+                if (p[i] > hi) hi = p[i];
+            ix->g.o[a] = frame[a];
+            ix->g.D[a] = (int64_t)floor((hi - frame[a]) / L) + 1;
+        }
+    }
     ix->e = (orc_entry *)malloc(sizeof(orc_entry) * (size_t)(n > 0 ? n : 1));
     for (int64_t i = 0; i < n; ++i) {
         int64_t b[3];
@@ -277,7 +295,7 @@ int64_t orc_neighbor_pairs_grid(int64_t n, const double *x, const double *y, con
                                 uint64_t *pairs, int64_t cap)
 {
     orc_index ix;
-    index_build(&ix, n, x, y, z, d, id, radius);
+    index_build(&ix, n, x, y, z, d, id, radius, NULL);
     double R2 = ix.g.R * ix.g.R;
     int64_t cnt = 0;
     for (int64_t i = 0; i < n; ++i) {
@@ -338,6 +356,8 @@ typedef struct {
     double k, gamma, dt, max_disp, force_threshold, radius;
     int32_t detect_static, boundary;  /* boundary: 0 open, 1 closed */
     double lo[3], hi[3];
+    int32_t use_frame, pad_;          /* 1: grid frame below instead of the agents' own */
+    double frame[4];                  /* o[3], R (global frame)            */
 } orc_mech_params;
 
 typedef struct {
@@ -359,7 +379,7 @@ void orc_mech_step(int64_t n, const double *x, const double *y, const double *z,
     memset(cnt, 0, sizeof(*cnt));
     if (n == 0) return;
     orc_index ix;
-    index_build(&ix, n, x, y, z, d, id, p->radius);
+    index_build(&ix, n, x, y, z, d, id, p->radius, p->use_frame ? p->frame : NULL);
     const orc_grid *g = &ix.g;
     double R2 = g->R * g->R;
     const uint32_t CHANGED = ORC_MOVED | ORC_GREW | ORC_ADDED;

@@ -24,8 +24,10 @@ EXPORTS = [
     "bdm_create", "bdm_destroy", "bdm_last_error", "bdm_version", "bdm_init_spheres",
     "bdm_grid_build", "bdm_mech_step", "bdm_step", "bdm_step_host", "bdm_sync", "bdm_reserve",
     "bdm_get_stats", "bdm_get_grid_info", "bdm_neighbor_pairs", "bdm_peak_dfma",
-    "bdm_set_option", "bdm_grow_divide", "bdm_sir_step",
+    "bdm_set_option", "bdm_grow_divide", "bdm_sir_step", "bdm_local_frame", "bdm_set_frame",
+    "bdm_pack_slab", "bdm_append",
 ]
+PACK_MIGRATE, PACK_AURA = 1, 2
 
 
 class BdmError(RuntimeError):
@@ -98,6 +100,10 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "bdm_set_option": [P, ctypes.c_char_p, i64],
         "bdm_grow_divide": [P, AG, PR, dbl, dbl, P, P],
         "bdm_sir_step": [P, AG, PR, dbl, dbl, dbl, dbl, P, P],
+        "bdm_local_frame": [P, AG, P, P],
+        "bdm_set_frame": [P, P],
+        "bdm_pack_slab": [P, AG, dbl, dbl, dbl, i32, AG, AG, P, P],
+        "bdm_append": [P, AG, AG, P],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -263,12 +269,51 @@ class Engine:
                                          int(bool(d_random)), _stream_ptr(stream)))
         agents.n = int(n)
 
-    def grid_build(self, agents: Agents, radius: float = 0.0, stream=None):
+    def grid_build(self, agents: Agents, radius: float = 0.0, stream=None, ghosts=None):
         ca = agents.c()
-        _check(self.lib.bdm_grid_build(self.h, ctypes.byref(ca), None, float(radius),
-                                       _stream_ptr(stream)))
+        cg = ghosts.c() if ghosts is not None else None
+        _check(self.lib.bdm_grid_build(self.h, ctypes.byref(ca),
+                                       ctypes.byref(cg) if cg is not None else None,
+                                       float(radius), _stream_ptr(stream)))
+
+    # -------------------------------------------------------------- x-slab device side
+    def local_frame(self, agents: Agents, out, stream=None):
+        """bdm_local_frame into the device tensor `out` (4 float64)."""
+        ca = agents.c()
+        _check(self.lib.bdm_local_frame(self.h, ctypes.byref(ca), _ptr(out), _stream_ptr(stream)))
+
+    def set_frame(self, frame):
+        """bdm_set_frame (device tensor of 4 float64, kept alive by the caller) or None."""
+        self._frame_ref = frame
+        _check(self.lib.bdm_set_frame(self.h, _ptr(frame) if frame is not None else None))
+
+    def pack_slab(self, agents: Agents, lo: float, hi: float, margin: float, what: int,
+                  to_left: Agents, to_right: Agents, stream=None):
+        """bdm_pack_slab; synchronizes; sets to_left.n, to_right.n (and agents.n for a
+        migration); returns (n_left, n_right)."""
+        import torch
+        if not hasattr(self, "_pack_counts"):
+            self._pack_counts = torch.zeros(3, dtype=torch.int64, pin_memory=True)
+        ca, cl, cr = agents.c(), to_left.c(), to_right.c()
+        _check(self.lib.bdm_pack_slab(self.h, ctypes.byref(ca), float(lo), float(hi),
+                                      float(margin), int(what), ctypes.byref(cl),
+                                      ctypes.byref(cr), ctypes.c_void_p(self._pack_counts.data_ptr()),
+                                      _stream_ptr(stream)))
+        self.sync(stream)
+        nl, nr, rem = (int(v) for v in self._pack_counts)
+        to_left.n, to_right.n = nl, nr
+        if what == PACK_MIGRATE:
+            agents.n = rem
+        return nl, nr
+
+    def append(self, dst: Agents, src: Agents, stream=None):
+        cd, cs = dst.c(), src.c()
+        _check(self.lib.bdm_append(self.h, ctypes.byref(cd), ctypes.byref(cs), _stream_ptr(stream)))
+        dst.n = int(cd.n)
 
     def mech_step(self, agents: Agents, params: Params, stream=None):
+        """bdm_mech_step over the grid of the preceding grid_build (locals only are
+        written)."""
         ca = agents.c()
         cp = params.c()
         _check(self.lib.bdm_mech_step(self.h, ctypes.byref(ca), ctypes.byref(cp),

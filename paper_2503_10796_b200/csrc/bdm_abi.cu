@@ -53,7 +53,9 @@ static bdm_status grow_agents(Ctx *c, int64_t n) {
         (s = dalloc(&c->sid, cap)) || (s = dalloc(&c->perm, cap)) || (s = dalloc(&c->sx, cap)) ||
         (s = dalloc(&c->sy, cap)) || (s = dalloc(&c->sz, cap)) || (s = dalloc(&c->sd, cap)) ||
         (s = dalloc(&c->sidf, cap)) || (s = dalloc(&c->sflags, cap)) ||
-        (s = dalloc(&c->svol, cap)) || (s = dalloc(&c->div_rank, cap + 1))) {
+        (s = dalloc(&c->svol, cap)) || (s = dalloc(&c->div_rank, cap + 1)) ||
+        (s = dalloc(&c->lrank, cap + 1)) || (s = dalloc(&c->cls, cap + 1)) ||
+        (s = dalloc(&c->cls2, cap + 1))) {
         c->agent_cap = 0;
         return s;
     }
@@ -104,6 +106,8 @@ static bdm_status read_latches(Ctx *c, bool clear) {
     bdm_status st = BDM_OK;
     if (c->sc_host->nonfinite) {
         st = fail(BDM_ENOTFINITE, "a position or diameter is NaN/Inf");
+    } else if (c->sc_host->overflow == 4) {
+        st = fail(BDM_ECAPACITY, "slab send buffer too small");
     } else if (c->sc_host->overflow == 3) {
         st = fail(BDM_ECAPACITY, "SIR infected index too small (raise option sir_index_capacity)");
     } else if (c->sc_host->overflow == 2) {
@@ -143,7 +147,8 @@ bdm_status bdm_create(bdm_handle *out, int device, int64_t max_agents) {
     if (cudaMalloc(&c->sc, sizeof(DevScalars)) != cudaSuccess ||
         cudaMallocHost(&c->sc_host, sizeof(DevScalars)) != cudaSuccess ||
         cudaMalloc(&c->pair_count, sizeof(unsigned long long)) != cudaSuccess ||
-        cudaMalloc(&c->n_new, sizeof(long long)) != cudaSuccess) {
+        cudaMalloc(&c->n_new, sizeof(long long)) != cudaSuccess ||
+        cudaMalloc(&c->pack_counts, 16 * sizeof(long long)) != cudaSuccess) {
         cudaGetLastError();
         delete c;
         return fail(BDM_ECUDA, "allocation of the context scalars failed");
@@ -166,7 +171,8 @@ bdm_status bdm_destroy(bdm_handle h) {
     cudaDeviceSynchronize();
     void *bufs[] = {c->key, c->rank, c->perm_tmp, c->skey, c->sid, c->perm, c->sx, c->sy,
                     c->sz, c->sd, c->sidf, c->sflags, c->svol, c->div_rank, c->box_start,
-                    c->block_sums, c->pair_count, c->n_new, c->sc};
+                    c->block_sums, c->pair_count, c->n_new, c->lrank, c->cls, c->cls2,
+                    c->pack_counts, c->sc};
     for (void *p : bufs)
         if (p) cudaFree(p);
     void *sbufs[] = {c->sir.keys, c->sir.heads, c->sir.next, c->sir.bitmap, c->sir.ix, c->sir.iy,
@@ -198,18 +204,21 @@ bdm_status bdm_grid_build(bdm_handle h, const bdm_agents *a, const bdm_agents *g
     Ctx *c = (Ctx *)h;
     bdm_status s = check_agents(a, true);
     if (s != BDM_OK) return s;
-    if (ghosts && ghosts->n > 0) return fail(BDM_ENOTIMPL, "ghost agents not supported yet");
+    if (ghosts && ghosts->n > 0 && (s = check_agents(ghosts, true)) != BDM_OK) return s;
+    const bdm_agents *g = (ghosts && ghosts->n > 0) ? ghosts : nullptr;
     if (radius < 0.0 || radius != radius) return fail(BDM_EINVAL, "radius < 0");
     cudaStream_t st = (cudaStream_t)stream;
     c->grid_valid = false;
+    const int64_t ntot = a->n + (g ? g->n : 0);
     if (a->n == 0) {
         c->grid_valid = true;
         c->grid_x = a->x;
         c->grid_n = 0;
+        c->grid_ng = 0;
         return BDM_OK;
     }
-    if ((s = grow_agents(c, a->n)) != BDM_OK) return s;
-    if ((s = launch_grid_geometry(c, a, radius, st)) != BDM_OK) return s;
+    if ((s = grow_agents(c, ntot)) != BDM_OK) return s;
+    if ((s = launch_grid_geometry(c, a, g, radius, st)) != BDM_OK) return s;
     if (c->slot_cap == 0) {
         // first build: size the slot array from the actual geometry (one sync),
         // with room for growth of the open-boundary space (+4 tiles per axis)
@@ -225,12 +234,13 @@ bdm_status bdm_grid_build(bdm_handle h, const bdm_agents *a, const bdm_agents *g
         if ((s = grow_slots(c, t0 * t1 * t2 * 64)) != BDM_OK) return s;
         int32_t z[2] = {0, 0};
         BDM_CUDA_TRY(cudaMemcpy(&c->sc->overflow, z, sizeof(z), cudaMemcpyHostToDevice));
-        if ((s = launch_grid_geometry(c, a, radius, st)) != BDM_OK) return s;
+        if ((s = launch_grid_geometry(c, a, g, radius, st)) != BDM_OK) return s;
     }
-    if ((s = launch_grid_sort(c, a, st)) != BDM_OK) return s;
+    if ((s = launch_grid_sort(c, a, g, st)) != BDM_OK) return s;
     c->grid_valid = true;
     c->grid_x = a->x;
     c->grid_n = a->n;
+    c->grid_ng = g ? g->n : 0;
     return BDM_OK;
 }
 
@@ -247,7 +257,11 @@ bdm_status bdm_mech_step(bdm_handle h, bdm_agents *a, const bdm_params *p, void 
         return fail(BDM_EINVAL, "dt, max_displacement and force_threshold must be >= 0");
     c->grid_valid = false;  // positions change: the grid is stale afterwards
     if (a->n == 0) return BDM_OK;
-    return launch_mech(c, a, p, (cudaStream_t)stream);
+    // the kernels sweep locals + ghosts of the build; outputs go to the locals only
+    bdm_agents all = *a;
+    all.n = a->n + c->grid_ng;
+    const bdm_status s2 = launch_mech(c, &all, p, (cudaStream_t)stream);
+    return s2;
 }
 
 bdm_status bdm_step(bdm_handle h, bdm_agents *a, const bdm_params *p, void *stream) {
@@ -312,6 +326,55 @@ bdm_status bdm_sir_step(bdm_handle h, bdm_agents *a, const bdm_params *p, double
     c->grid_valid = false;
     return launch_sir_step(c, a, p, side, radius, p_inf, p_rec, (long long *)counts_host,
                            (cudaStream_t)stream);
+}
+
+bdm_status bdm_local_frame(bdm_handle h, const bdm_agents *a, double *frame_dev, void *stream) {
+    if (!h || !a || !frame_dev) return fail(BDM_EINVAL, "NULL argument");
+    bdm_status s = check_agents(a, true);
+    if (s != BDM_OK) return s;
+    return launch_local_frame((Ctx *)h, a, frame_dev, (cudaStream_t)stream);
+}
+
+bdm_status bdm_set_frame(bdm_handle h, const double *frame_dev) {
+    if (!h) return fail(BDM_EINVAL, "handle is NULL");
+    Ctx *c = (Ctx *)h;
+    c->frame = frame_dev;
+    c->grid_valid = false;
+    return BDM_OK;
+}
+
+bdm_status bdm_pack_slab(bdm_handle h, bdm_agents *a, double lo, double hi, double margin,
+                         int32_t what, bdm_agents *to_left, bdm_agents *to_right,
+                         int64_t *counts_host, void *stream) {
+    if (!h || !a || !to_left || !to_right || !counts_host) return fail(BDM_EINVAL, "NULL argument");
+    if (what != BDM_PACK_MIGRATE && what != BDM_PACK_AURA) return fail(BDM_EINVAL, "bad what");
+    if (!(lo <= hi) || !(margin >= 0.0)) return fail(BDM_EINVAL, "need lo <= hi and margin >= 0");
+    Ctx *c = (Ctx *)h;
+    bdm_status s = check_agents(a, true);
+    if (s != BDM_OK) return s;
+    if ((s = grow_agents(c, a->n)) != BDM_OK) return s;
+    c->grid_valid = false;  // the migration compaction uses the sorted workspace
+    return launch_pack_slab(c, a, lo, hi, margin, what, to_left, to_right,
+                            (long long *)counts_host, (cudaStream_t)stream);
+}
+
+bdm_status bdm_append(bdm_handle h, bdm_agents *dst, const bdm_agents *src, void *stream) {
+    if (!h || !dst || !src) return fail(BDM_EINVAL, "NULL argument");
+    if (src->n < 0 || dst->n < 0) return fail(BDM_EINVAL, "negative n");
+    if (dst->n + src->n > dst->capacity) return fail(BDM_ECAPACITY, "append exceeds capacity");
+    if (src->n == 0) return BDM_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t n = (size_t)src->n, o = (size_t)dst->n;
+    BDM_CUDA_TRY(cudaMemcpyAsync(dst->x + o, src->x, n * 8, cudaMemcpyDeviceToDevice, st));
+    BDM_CUDA_TRY(cudaMemcpyAsync(dst->y + o, src->y, n * 8, cudaMemcpyDeviceToDevice, st));
+    BDM_CUDA_TRY(cudaMemcpyAsync(dst->z + o, src->z, n * 8, cudaMemcpyDeviceToDevice, st));
+    BDM_CUDA_TRY(cudaMemcpyAsync(dst->diameter + o, src->diameter, n * 8, cudaMemcpyDeviceToDevice, st));
+    BDM_CUDA_TRY(cudaMemcpyAsync(dst->id + o, src->id, n * 4, cudaMemcpyDeviceToDevice, st));
+    BDM_CUDA_TRY(cudaMemcpyAsync(dst->flags + o, src->flags, n * 4, cudaMemcpyDeviceToDevice, st));
+    if (dst->volume && src->volume)
+        BDM_CUDA_TRY(cudaMemcpyAsync(dst->volume + o, src->volume, n * 8, cudaMemcpyDeviceToDevice, st));
+    dst->n += src->n;
+    return BDM_OK;
 }
 
 bdm_status bdm_sync(bdm_handle h, void *stream) {

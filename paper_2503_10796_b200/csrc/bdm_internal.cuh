@@ -43,6 +43,8 @@ struct DevScalars {
     int32_t overflow;      // latched: nslots > slot_cap
     int32_t nonfinite;     // latched: a position was NaN/Inf
     unsigned long long stats[5];  // cand, nbr, cont, n_static, n_moved
+    int32_t boff[3];       // lattice offset: box index = floor((x - o)/L) - boff (R12, 8(e))
+    int32_t pad_;
 };
 
 // SIR workspace (kernels_sir.cu), allocated on first use
@@ -82,6 +84,12 @@ struct Ctx {
     bool grid_valid = false;
     const double *grid_x = nullptr;
     int64_t grid_n = 0;
+    int64_t grid_ng = 0;               // ghosts in the last grid build
+    uint32_t *lrank = nullptr;         // sorted slot -> output index of local agents
+    const double *frame = nullptr;     // device: global (o[3], -dmax) or NULL (local frame)
+    uint32_t *cls = nullptr;           // slab packing: per-agent class / scan scratch
+    uint32_t *cls2 = nullptr;
+    long long *pack_counts = nullptr;  // device: left, right, remaining
     int64_t launches = 0;  // kernels launched (host-side count)
     int mech_kernel = 0;   // option "mech_kernel": 0 tile kernel, 1 per-agent reference kernel
     int prefilter = 1;     // option "prefilter": fp32 conservative candidate test in the tile kernel
@@ -137,14 +145,21 @@ __device__ __forceinline__ uint32_t box_key(int bx, int by, int bz, int T0, int 
 }
 
 constexpr uint32_t kChanged = BDM_FLAG_MOVED | BDM_FLAG_GREW | BDM_FLAG_ADDED;
+constexpr uint32_t kGhost = 1u << 31;  // internal sorted-workspace flag: aura (ghost) agent
 
 // ------------------------------------------------------------------ launchers
 // grid (kernels_grid.cu)
 bdm_status launch_init_spheres(const bdm_agents *a, int64_t id0, int64_t n, uint64_t seed,
                                double side, double d_lo, double d_width, int d_random,
                                cudaStream_t st);
-bdm_status launch_grid_geometry(Ctx *c, const bdm_agents *a, double radius, cudaStream_t st);
-bdm_status launch_grid_sort(Ctx *c, const bdm_agents *a, cudaStream_t st);
+bdm_status launch_grid_geometry(Ctx *c, const bdm_agents *a, const bdm_agents *g, double radius,
+                                cudaStream_t st);
+bdm_status launch_grid_sort(Ctx *c, const bdm_agents *a, const bdm_agents *g, cudaStream_t st);
+// slabs (kernels_slab.cu)
+bdm_status launch_local_frame(Ctx *c, const bdm_agents *a, double *frame_dev, cudaStream_t st);
+bdm_status launch_pack_slab(Ctx *c, bdm_agents *a, double lo, double hi, double margin, int what,
+                            bdm_agents *to_left, bdm_agents *to_right, long long *counts_host,
+                            cudaStream_t st);
 // mechanics (kernels_mech.cu)
 bdm_status launch_mech(Ctx *c, bdm_agents *a, const bdm_params *p, cudaStream_t st);
 bdm_status launch_pairs(Ctx *c, int64_t n, uint64_t *pairs, int64_t cap, cudaStream_t st);

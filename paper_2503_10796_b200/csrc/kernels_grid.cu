@@ -118,9 +118,12 @@ __global__ void __launch_bounds__(256) k_reduce(int64_t n, const double *__restr
 }
 
 // R, L, origin, dims, tiles, slot count; latches overflow if the slots do not fit.
-__global__ void k_setup(DevScalars *sc, double radius) {
+// With a global frame (multi-GPU, 8(e)) the origin and R come from the frame (the
+// all-reduced minimum corner and largest diameter of every rank) and the local
+// extent only fixes the lattice offset and dims.
+__global__ void k_setup(DevScalars *sc, double radius, const double *__restrict__ frame) {
     if (threadIdx.x != 0) return;
-    const double R = radius > 0.0 ? radius : dec_double(sc->enc_dmax);
+    const double R = radius > 0.0 ? radius : (frame ? -frame[3] : dec_double(sc->enc_dmax));
     const double L = R * (1.0 + 0x1p-20);
     sc->R = R;
     sc->R2 = R * R;
@@ -129,10 +132,13 @@ __global__ void k_setup(DevScalars *sc, double radius) {
     bool bad = !(L > 0.0) || !isfinite(L);
     for (int a = 0; a < 3; ++a) {
         const double lo = dec_double(sc->enc_lo[a]), hi = dec_double(sc->enc_hi[a]);
-        sc->o[a] = lo;
+        const double o = frame ? frame[a] : lo;
+        sc->o[a] = o;
         sc->hi[a] = hi;
-        const double ext = floor((hi - lo) / L);
-        if (!(ext < 1.0e9)) bad = true;
+        const double b0 = frame ? floor((lo - o) / L) : 0.0;
+        const double ext = floor((hi - o) / L) - b0;
+        if (!(ext < 1.0e9) || !(b0 >= 0.0 && b0 < 2.0e9)) bad = true;
+        sc->boff[a] = bad ? 0 : (int)b0;
         const int dim = bad ? 1 : (int)ext + 1;
         sc->dims[a] = dim;
         sc->T[a] = (dim + 3) >> 2;
@@ -143,16 +149,20 @@ __global__ void k_setup(DevScalars *sc, double radius) {
     if (bad || ns >= 0xFFFFFFFFll || ns > sc->slot_cap) sc->overflow = 1;
 }
 
-bdm_status launch_grid_geometry(Ctx *c, const bdm_agents *a, double radius, cudaStream_t st) {
+bdm_status launch_grid_geometry(Ctx *c, const bdm_agents *a, const bdm_agents *g, double radius,
+                                cudaStream_t st) {
     k_reset_scalars<<<1, 32, 0, st>>>(c->sc);
-    const int64_t n = a->n;
-    int64_t blocks = (n + 255) / 256;
-    const int64_t maxb = (int64_t)c->sm_count * 8;
-    if (blocks > maxb) blocks = maxb;
-    if (blocks < 1) blocks = 1;
-    k_reduce<<<(unsigned)blocks, 256, 0, st>>>(n, a->x, a->y, a->z, a->diameter, c->sc);
-    k_setup<<<1, 32, 0, st>>>(c->sc, radius);
-    c->launches += 3;
+    const bdm_agents *sets[2] = {a, g};
+    for (const bdm_agents *s : sets) {
+        if (!s || s->n == 0) continue;
+        int64_t blocks = (s->n + 255) / 256;
+        const int64_t maxb = (int64_t)c->sm_count * 8;
+        if (blocks > maxb) blocks = maxb;
+        k_reduce<<<(unsigned)blocks, 256, 0, st>>>(s->n, s->x, s->y, s->z, s->diameter, c->sc);
+        c->launches += 1;
+    }
+    k_setup<<<1, 32, 0, st>>>(c->sc, radius, c->frame);
+    c->launches += 2;
     BDM_LAUNCH_CHECK("grid geometry");
     return BDM_OK;
 }
@@ -166,20 +176,29 @@ __global__ void k_zero_counts(uint32_t *__restrict__ counts, const DevScalars *_
         counts[i] = 0u;
 }
 
-__global__ void __launch_bounds__(256) k_key(int64_t n, const double *__restrict__ x,
-                                             const double *__restrict__ y,
-                                             const double *__restrict__ z,
-                                             const DevScalars *__restrict__ sc,
+// Agents [0, nl) are local, [nl, nl + ng) are the ghosts (aura) of this build.
+struct Src {
+    int64_t nl, ng;
+    const double *__restrict__ x, *__restrict__ y, *__restrict__ z, *__restrict__ d, *__restrict__ vol;
+    const uint32_t *__restrict__ id, *__restrict__ flags;
+    const double *__restrict__ gx, *__restrict__ gy, *__restrict__ gz, *__restrict__ gd;
+    const uint32_t *__restrict__ gid, *__restrict__ gflags;
+};
+
+__global__ void __launch_bounds__(256) k_key(Src S, const DevScalars *__restrict__ sc,
                                              uint32_t *__restrict__ key,
                                              uint32_t *__restrict__ rank,
                                              uint32_t *__restrict__ counts) {
     if (sc->overflow) return;
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= n) return;
+    if (i >= S.nl + S.ng) return;
+    const bool gh = i >= S.nl;
+    const int64_t j = gh ? i - S.nl : i;
+    const double px = gh ? S.gx[j] : S.x[j], py = gh ? S.gy[j] : S.y[j], pz = gh ? S.gz[j] : S.z[j];
     const double L = sc->L;
-    const int bx = (int)floor((x[i] - sc->o[0]) / L);
-    const int by = (int)floor((y[i] - sc->o[1]) / L);
-    const int bz = (int)floor((z[i] - sc->o[2]) / L);
+    const int bx = (int)floor((px - sc->o[0]) / L) - sc->boff[0];
+    const int by = (int)floor((py - sc->o[1]) / L) - sc->boff[1];
+    const int bz = (int)floor((pz - sc->o[2]) / L) - sc->boff[2];
     const uint32_t k = box_key(bx, by, bz, sc->T[0], sc->T[1]);
     key[i] = k;
     rank[i] = atomicAdd(&counts[k], 1u);
@@ -293,37 +312,41 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_apply(uint32_t *__restric
 }
 
 // ============================================================== a4: scatter + order + gather
-__global__ void __launch_bounds__(256) k_scatter(int64_t n, const uint32_t *__restrict__ key,
+__global__ void __launch_bounds__(256) k_scatter(Src S, const uint32_t *__restrict__ key,
                                                  const uint32_t *__restrict__ rank,
                                                  const uint32_t *__restrict__ box_start,
-                                                 const uint32_t *__restrict__ id,
                                                  uint32_t *__restrict__ perm_tmp,
                                                  uint32_t *__restrict__ skey,
                                                  uint32_t *__restrict__ sid,
                                                  const DevScalars *__restrict__ sc) {
     if (sc->overflow) return;
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= n) return;
+    if (i >= S.nl + S.ng) return;
     const uint32_t k = key[i];
     const uint32_t slot = box_start[k] + rank[i];
     perm_tmp[slot] = (uint32_t)i;
     skey[slot] = k;
-    sid[slot] = id[i];
+    sid[slot] = i >= S.nl ? S.gid[i - S.nl] : S.id[i];
 }
 
 // Slot s of the scatter holds an agent of box k in arbitrary order; its final slot
 // is box_start[k] + #(agents of box k with a smaller id).  Gathers the SoA there.
+// Ghosts are marked with kGhost in the sorted flags; with ghosts, lflag[dst] = 1 for
+// local agents (scanned afterwards into their output index).
 __global__ void __launch_bounds__(256) k_fix_gather(
-    int64_t n, const uint32_t *__restrict__ skey, const uint32_t *__restrict__ sid,
+    Src S, const uint32_t *__restrict__ skey, const uint32_t *__restrict__ sid,
     const uint32_t *__restrict__ perm_tmp, const uint32_t *__restrict__ box_start,
-    const double *__restrict__ x, const double *__restrict__ y, const double *__restrict__ z,
-    const double *__restrict__ d, const uint32_t *__restrict__ flags, double *__restrict__ sx,
-    double *__restrict__ sy, double *__restrict__ sz, double *__restrict__ sd,
-    uint32_t *__restrict__ sidf, uint32_t *__restrict__ sflags, uint32_t *__restrict__ perm,
-    const double *__restrict__ vol, double *__restrict__ svol, const DevScalars *__restrict__ sc) {
+    double *__restrict__ sx, double *__restrict__ sy, double *__restrict__ sz,
+    double *__restrict__ sd, uint32_t *__restrict__ sidf, uint32_t *__restrict__ sflags,
+    uint32_t *__restrict__ perm, double *__restrict__ svol, uint32_t *__restrict__ lflag,
+    const DevScalars *__restrict__ sc) {
     if (sc->overflow) return;
     const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (s >= n) return;
+    const int64_t n = S.nl + S.ng;
+    if (s >= n) {
+        if (s == n && lflag) lflag[n] = 0u;
+        return;
+    }
     const uint32_t k = skey[s];
     const uint32_t lo = box_start[k], hi = box_start[k + 1];
     const uint32_t me = sid[s];
@@ -331,18 +354,38 @@ __global__ void __launch_bounds__(256) k_fix_gather(
     for (uint32_t t = lo; t < hi; ++t) r += (sid[t] < me);
     const uint32_t dst = lo + r;
     const uint32_t src = perm_tmp[s];
-    sx[dst] = x[src];
-    sy[dst] = y[src];
-    sz[dst] = z[src];
-    sd[dst] = d[src];
+    if ((int64_t)src < S.nl) {
+        sx[dst] = S.x[src];
+        sy[dst] = S.y[src];
+        sz[dst] = S.z[src];
+        sd[dst] = S.d[src];
+        sflags[dst] = S.flags[src];
+        if (S.vol) svol[dst] = S.vol[src];
+        if (lflag) lflag[dst] = 1u;
+    } else {
+        const int64_t j = (int64_t)src - S.nl;
+        sx[dst] = S.gx[j];
+        sy[dst] = S.gy[j];
+        sz[dst] = S.gz[j];
+        sd[dst] = S.gd[j];
+        sflags[dst] = S.gflags[j] | kGhost;
+        if (S.vol) svol[dst] = 0.0;
+        lflag[dst] = 0u;
+    }
     sidf[dst] = me;
-    sflags[dst] = flags[src];
     perm[dst] = src;
-    if (vol) svol[dst] = vol[src];
 }
 
-bdm_status launch_grid_sort(Ctx *c, const bdm_agents *a, cudaStream_t st) {
-    const int64_t n = a->n;
+bdm_status launch_grid_sort(Ctx *c, const bdm_agents *a, const bdm_agents *g, cudaStream_t st) {
+    Src S;
+    S.nl = a->n;
+    S.ng = g ? g->n : 0;
+    S.x = a->x; S.y = a->y; S.z = a->z; S.d = a->diameter; S.vol = a->volume;
+    S.id = a->id; S.flags = a->flags;
+    S.gx = g ? g->x : nullptr; S.gy = g ? g->y : nullptr; S.gz = g ? g->z : nullptr;
+    S.gd = g ? g->diameter : nullptr; S.gid = g ? g->id : nullptr;
+    S.gflags = g ? g->flags : nullptr;
+    const int64_t n = S.nl + S.ng;
     const int threads = 256;
     const unsigned nb = (unsigned)((n + threads - 1) / threads);
     {
@@ -351,19 +394,20 @@ bdm_status launch_grid_sort(Ctx *c, const bdm_agents *a, cudaStream_t st) {
         if (zb > maxb) zb = maxb;
         k_zero_counts<<<(unsigned)zb, 1024, 0, st>>>(c->box_start, c->sc);
     }
-    k_key<<<nb, threads, 0, st>>>(n, a->x, a->y, a->z, c->sc, c->key, c->rank, c->box_start);
+    k_key<<<nb, threads, 0, st>>>(S, c->sc, c->key, c->rank, c->box_start);
     const unsigned sb = (unsigned)((c->slot_cap + 1 + kScanTile - 1) / kScanTile);
     k_scan_reduce<<<sb, kScanThreads, 0, st>>>(c->box_start, c->block_sums, c->sc, 0);
     k_scan_top<<<1, 1024, 0, st>>>(c->block_sums, c->sc, 0);
     k_scan_apply<<<sb, kScanThreads, 0, st>>>(c->box_start, c->block_sums, c->sc, 0);
-    k_scatter<<<nb, threads, 0, st>>>(n, c->key, c->rank, c->box_start, a->id, c->perm_tmp,
-                                      c->skey, c->sid, c->sc);
-    k_fix_gather<<<nb, threads, 0, st>>>(n, c->skey, c->sid, c->perm_tmp, c->box_start, a->x,
-                                         a->y, a->z, a->diameter, a->flags, c->sx, c->sy, c->sz,
-                                         c->sd, c->sidf, c->sflags, c->perm, a->volume, c->svol,
-                                         c->sc);
+    k_scatter<<<nb, threads, 0, st>>>(S, c->key, c->rank, c->box_start, c->perm_tmp, c->skey,
+                                      c->sid, c->sc);
+    uint32_t *lflag = S.ng > 0 ? c->lrank : nullptr;
+    k_fix_gather<<<(unsigned)((n + 1 + threads - 1) / threads), threads, 0, st>>>(
+        S, c->skey, c->sid, c->perm_tmp, c->box_start, c->sx, c->sy, c->sz, c->sd, c->sidf,
+        c->sflags, c->perm, c->svol, lflag, c->sc);
     c->launches += 7;
     BDM_LAUNCH_CHECK("grid sort");
+    if (S.ng > 0) return launch_scan_u32(c, c->lrank, n + 1, st);  // output index of locals
     return BDM_OK;
 }
 

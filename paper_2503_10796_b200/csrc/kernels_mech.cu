@@ -33,6 +33,7 @@ struct MechArgs {
     double *__restrict__ od;
     uint32_t *__restrict__ oid;
     uint32_t *__restrict__ oflags;
+    const uint32_t *__restrict__ lrank;  // nullable: output index of sorted local slots (ghosts)
     const double *__restrict__ svol;  // nullable: volume travels with the agents
     double *__restrict__ ovol;
     double k, gamma, dt, max_disp, tau;
@@ -50,10 +51,12 @@ __device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v)
 struct GridView {
     double L, R2, o0, o1, o2;
     int D0, D1, D2, T0, T1, T2;
+    int b0, b1, b2;  // lattice offset (global frame, 8(e))
 };
 __device__ __forceinline__ GridView load_grid(const DevScalars *__restrict__ sc) {
     GridView g;
     g.L = sc->L; g.R2 = sc->R2; g.o0 = sc->o[0]; g.o1 = sc->o[1]; g.o2 = sc->o[2];
+    g.b0 = sc->boff[0]; g.b1 = sc->boff[1]; g.b2 = sc->boff[2];
     g.D0 = sc->dims[0]; g.D1 = sc->dims[1]; g.D2 = sc->dims[2];
     g.T0 = sc->T[0]; g.T1 = sc->T[1]; g.T2 = sc->T[2];
     return g;
@@ -63,10 +66,12 @@ struct Counts {
     uint32_t cand = 0, nbr = 0, cont = 0, stat = 0, moved = 0;
 };
 
-// a8 + a9 + write-back for one agent (shared by both kernels).
+// a8 + a9 + write-back for one agent (shared by both kernels); s is the sorted slot,
+// the output goes to lrank[s] when ghosts are present.
 __device__ __forceinline__ void finish_agent(const MechArgs &A, int64_t s, double xi, double yi,
                                              double zi, double Fx, double Fy, double Fz,
                                              bool is_static, int nnz, Counts &c) {
+    const int64_t o = A.lrank ? (int64_t)A.lrank[s] : s;
     double Dx = 0.0, Dy = 0.0, Dz = 0.0;
     if (!is_static) {
         const double F2 = Fx * Fx + Fy * Fy + Fz * Fz;
@@ -92,13 +97,13 @@ __device__ __forceinline__ void finish_agent(const MechArgs &A, int64_t s, doubl
     const bool moved = (Dx != 0.0 || Dy != 0.0 || Dz != 0.0);
     c.moved += moved ? 1u : 0u;
     c.stat += is_static ? 1u : 0u;
-    A.ox[s] = nx;
-    A.oy[s] = ny;
-    A.oz[s] = nz;
-    A.od[s] = A.sd[s];
-    A.oid[s] = A.sid[s];
-    if (A.ovol) A.ovol[s] = A.svol[s];
-    A.oflags[s] = (moved ? BDM_FLAG_MOVED : 0u) | (is_static ? BDM_FLAG_STATIC : 0u) |
+    A.ox[o] = nx;
+    A.oy[o] = ny;
+    A.oz[o] = nz;
+    A.od[o] = A.sd[s];
+    A.oid[o] = A.sid[s];
+    if (A.ovol) A.ovol[o] = A.svol[s];
+    A.oflags[o] = (moved ? BDM_FLAG_MOVED : 0u) | (is_static ? BDM_FLAG_STATIC : 0u) |
                   ((uint32_t)nnz << BDM_FLAG_NNZ_SHIFT);
 }
 
@@ -107,12 +112,13 @@ __device__ __forceinline__ void finish_agent(const MechArgs &A, int64_t s, doubl
 // fallback for over-full tiles).
 __device__ __forceinline__ void mech_agent_global(const MechArgs &A, const GridView &g, int64_t s,
                                                   Counts &c) {
-    const double xi = A.sx[s], yi = A.sy[s], zi = A.sz[s], di = A.sd[s];
     const uint32_t fi = A.sflags[s];
+    if (fi & kGhost) return;  // aura agents are read-only
+    const double xi = A.sx[s], yi = A.sy[s], zi = A.sz[s], di = A.sd[s];
     const double ri = di * 0.5;
-    const int bx = (int)floor((xi - g.o0) / g.L);
-    const int by = (int)floor((yi - g.o1) / g.L);
-    const int bz = (int)floor((zi - g.o2) / g.L);
+    const int bx = (int)floor((xi - g.o0) / g.L) - g.b0;
+    const int by = (int)floor((yi - g.o1) / g.L) - g.b1;
+    const int bz = (int)floor((zi - g.o2) / g.L) - g.b2;
     const int nnz_in = (int)((fi >> BDM_FLAG_NNZ_SHIFT) & 3u);
 
     // ---- a5: static classification (pull test over the neighbours' flags)
@@ -368,8 +374,8 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_mech_tile(MechArgs A, DevSc
             continue;
         }
         // ---- stage the region box by box (row-major boxes, ascending id in a box)
-        const double X0 = g.o0 + (double)bx0 * g.L, Y0 = g.o1 + (double)by0 * g.L,
-                     Z0 = g.o2 + (double)bz0 * g.L;
+        const double X0 = g.o0 + (double)(bx0 + g.b0) * g.L, Y0 = g.o1 + (double)(by0 + g.b1) * g.L,
+                     Z0 = g.o2 + (double)(bz0 + g.b2) * g.L;
         for (int lb = tid; lb < 216; lb += kTileThreads)  // staged index -> its box
             for (uint32_t m = S.off[lb]; m < S.off[lb + 1]; ++m) S.mbox[m] = (uint8_t)lb;
         __syncthreads();
@@ -395,7 +401,7 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_mech_tile(MechArgs A, DevSc
         for (int base = wlo; base < whi; base += 32) {  // warp-uniform
             const int na = min(32, whi - base);
             const int k = base + lane;
-            const bool active = lane < na;
+            const bool active = lane < na && !(A.sflags[g0 + (uint32_t)k] & kGhost);
             // ---- own agent: staged index, runs, candidate count
             int mi = 0, ca = 0, nr = 0;
             uint32_t fi = 0;
@@ -406,9 +412,9 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_mech_tile(MechArgs A, DevSc
                 xi = A.sx[gk];
                 yi = A.sy[gk];
                 zi = A.sz[gk];
-                const int lx = (int)floor((xi - g.o0) / g.L) - bx0;
-                const int ly = (int)floor((yi - g.o1) / g.L) - by0;
-                const int lz = (int)floor((zi - g.o2) / g.L) - bz0;
+                const int lx = (int)floor((xi - g.o0) / g.L) - g.b0 - bx0;
+                const int ly = (int)floor((yi - g.o1) / g.L) - g.b1 - by0;
+                const int lz = (int)floor((zi - g.o2) / g.L) - g.b2 - bz0;
                 const int lbi = (lz * 6 + ly) * 6 + lx;
                 mi = (int)(S.off[lbi] + (gk - S.start[lbi]));
                 fi = S.F[mi];
@@ -555,6 +561,7 @@ bdm_status launch_mech(Ctx *c, bdm_agents *a, const bdm_params *p, cudaStream_t 
     A.sid = c->sidf; A.sflags = c->sflags; A.box_start = c->box_start;
     A.ox = a->x; A.oy = a->y; A.oz = a->z; A.od = a->diameter; A.oid = a->id; A.oflags = a->flags;
     A.svol = a->volume ? c->svol : nullptr;
+    A.lrank = c->grid_ng > 0 ? c->lrank : nullptr;
     A.ovol = a->volume;
     A.k = p->k; A.gamma = p->gamma; A.dt = p->dt; A.max_disp = p->max_displacement;
     A.tau = p->force_threshold;
@@ -592,9 +599,9 @@ __global__ void __launch_bounds__(256) k_pairs(int64_t n, const double *__restri
     if (s >= n) return;
     const double L = sc->L, R2 = sc->R2;
     const double xi = sx[s], yi = sy[s], zi = sz[s];
-    const int bx = (int)floor((xi - sc->o[0]) / L);
-    const int by = (int)floor((yi - sc->o[1]) / L);
-    const int bz = (int)floor((zi - sc->o[2]) / L);
+    const int bx = (int)floor((xi - sc->o[0]) / L) - sc->boff[0];
+    const int by = (int)floor((yi - sc->o[1]) / L) - sc->boff[1];
+    const int bz = (int)floor((zi - sc->o[2]) / L) - sc->boff[2];
     const uint64_t me = (uint64_t)sid[s] << 32;
     for (int dz = -1; dz <= 1; ++dz)
         for (int dy = -1; dy <= 1; ++dy)
