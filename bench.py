@@ -19,6 +19,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import statistics
 import subprocess
@@ -174,8 +175,12 @@ def run_ours(args, ws, rank, local):
     import torch
     from paper_2503_10796_b200 import Agents, Engine, Params
 
-    if ws > 1:
-        raise SystemExit("multi-GPU slab decomposition is not wired into bench.py yet")
+    if ws > 1 or args.config == "cfg5":
+        return run_slabs(args, ws, rank, local)
+    if args.config == "cfg3":
+        return run_cfg3(args, ws, rank, local)
+    if args.config == "cfg4":
+        return run_cfg4(args, ws, rank, local)
     torch.cuda.set_device(local)
     cfg = W.PRESETS[args.config]
     eng = Engine(local, cfg.n)
@@ -280,6 +285,208 @@ def run_ours(args, ws, rank, local):
     if not args.no_cpu_baseline and rank == 0 and ws == 1:
         line["cpu_baseline"] = cpu_baseline()
     print(json.dumps(line), flush=True)
+
+
+def _common(metric_value, ms_step, ws, args, config, clocks, launches, dtype="f64"):
+    return {"metric": METRIC, "value": metric_value, "unit": UNIT, "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": dtype,
+            "data": "synthetic", "config": config, "clocks": clocks, "gpu_launches": launches}
+
+
+def run_cfg3(args, ws, rank, local):
+    """configs[2]: proliferation 1M -> 256M agents over 20 steps (every step has a
+    different N; the value is the aggregate sum(N_t) / sum(t_step))."""
+    import torch
+    from paper_2503_10796_b200 import Agents, Engine, Params
+    torch.cuda.set_device(local)
+    cfg = W.CFG3
+    steps = min(args.steps, cfg.steps)
+    cap = cfg.n * 2 ** ((steps + 1) // 2 + 1)
+    cap = min(cap, 300_000_000)
+    eng = Engine(local, cfg.n)
+    a = Agents.empty(cap, volume=True)
+    stream = torch.cuda.Stream()
+    eng.init_spheres(a, cfg.n, seed=cfg.seed, side=cfg.side, d_lo=cfg.d_lo, stream=stream)
+    a.volume[:cfg.n].copy_((torch.pi / 6.0) * (a.diameter[:cfg.n] ** 3))
+    torch.cuda.synchronize()
+    params = Params(seed=cfg.seed, dt=cfg.dt, max_displacement=cfg.max_disp)
+    # workspace for the final population and for the finest grid (R = 8 um), reserved
+    # before timing so no step pays for an allocation
+    tiles = int(math.ceil((cfg.side + 2 * steps * cfg.max_disp) / cfg.d_lo / 4.0)) + 8
+    eng.reserve(cap, tiles ** 3 * 64)
+    per_step = []
+    launches0 = eng.stats()["launches"]
+    with ClockSampler(local) as clk:
+        for t in range(steps):
+            params.step = t
+            n0 = a.n
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            e0.record(stream)
+            eng.step(a, params, stream=stream)
+            eng.grow_divide(a, params, W.CFG3_GROWTH, W.CFG3_V_MAX, stream=stream)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            per_step.append((n0, e0.elapsed_time(e1)))
+    total_agents = sum(n for n, _ in per_step)
+    total_ms = sum(ms for _, ms in per_step)
+    line = _common(total_agents / (total_ms * 1e-3), total_ms / steps, ws, args,
+                   {"workload": "cfg3 (configs[2])", "initial_agents": cfg.n,
+                    "final_agents": a.n, "steps": steps,
+                    "per_step": [{"n": n, "ms": round(ms, 4)} for n, ms in per_step],
+                    "l2": "inputs larger than L2 from step 1 (48 B/agent x >= 1M)"},
+                   clk.summary(), eng.stats()["launches"] - launches0)
+    line["roofline"] = None
+    line["note"] = "proliferation: per-step rate in config.per_step; dense late steps use the global-memory kernel"
+    print(json.dumps(line), flush=True)
+
+
+def run_cfg4(args, ws, rank, local):
+    """configs[3]: SIR on 100M point agents, HBM-bound (x, y, z, state read + written)."""
+    import torch
+    from paper_2503_10796_b200 import Agents, Engine, Params
+    torch.cuda.set_device(local)
+    cfg = W.CFG4
+    eng = Engine(local, 1)
+    a = Agents.empty(cfg.n, state=True)
+    stream = torch.cuda.Stream()
+    eng.init_spheres(a, cfg.n, seed=cfg.seed, side=cfg.side, d_lo=0.0, stream=stream)
+    torch.cuda.synchronize()
+    a.state[:cfg.n_infected] = 1
+    a.id = None       # ids == index: the Philox counter uses the index (no id traffic)
+    a.diameter = None
+    a.flags = None
+    torch.cuda.synchronize()
+    params = Params(seed=cfg.seed)
+    for t in range(args.warmup):
+        params.step = t
+        eng.sir_step(a, params, cfg.side, cfg.radius, cfg.p_inf, cfg.p_rec, stream=stream)
+    K = args.steps
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(K + 1)]
+    launches0 = eng.stats()["launches"]
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        evs[0].record(stream)
+        for k in range(K):
+            params.step = args.warmup + k
+            eng.sir_step(a, params, cfg.side, cfg.radius, cfg.p_inf, cfg.p_rec, stream=stream,
+                         sync=False)
+            evs[k + 1].record(stream)
+        torch.cuda.synchronize()
+    rc = eng.try_sync(stream)
+    if rc != 0:
+        raise SystemExit(f"a timed SIR step failed (bdm status {rc})")
+    counts = [int(v) for v in eng._sir_counts]
+    ms = evs[0].elapsed_time(evs[K]) / K
+    peaks, src = _peaks()
+    b_alg = 50.0 * cfg.n    # x, y, z read + write (48 B) + state read + write (2 B)
+    ach = b_alg / (ms * 1e-3)
+    line = _common(cfg.n / (ms * 1e-3), ms, ws, args,
+                   {"workload": "cfg4 (configs[3])", "agents": cfg.n, "side_m": cfg.side,
+                    "radius_m": cfg.radius, "p_inf": cfg.p_inf, "p_rec": cfg.p_rec,
+                    "l2": "inputs (2.5 GB) larger than L2; no flush",
+                    "counts_after": {"S": counts[0], "I": counts[1], "R": counts[2]}},
+                   clk.summary(), eng.stats()["launches"] - launches0)
+    line["roofline"] = {"bound": "hbm", "kernel": "k_sir_update + k_sir_collect (whole step)",
+                        "achieved": ach / 1e9, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                        "frac": ach / (peaks["hbm_gbs"] * 1e9), "traffic": None,
+                        "peak_source": src, "alg_bytes_per_agent": 50}
+    print(json.dumps(line), flush=True)
+
+
+def run_slabs(args, ws, rank, local):
+    """x-slab decomposition over N GPUs.  Default: weak scaling with the
+    cfg2 workload per GPU (10M agents in one cfg2 cube per slab, slabs side by side in
+    x); --config cfg5: the 1.7B-agent cube split into N slabs (strong scaling)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2503_10796_b200 import Agents, Engine, Params
+    from paper_2503_10796_b200.slabs import DistTransport, LibOps, Slab, SlabDomain
+    torch.cuda.set_device(local)
+    if ws > 1 and not dist.is_initialized():
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    strong = args.config == "cfg5"
+    cfg = W.CFG5 if strong else W.CFG2
+    if strong:
+        n_local_est = cfg.n // ws
+        side_x = cfg.side
+    else:
+        n_local_est = cfg.n
+        side_x = cfg.side * ws
+    lo = -math.inf if rank == 0 else rank * side_x / ws
+    hi = math.inf if rank == ws - 1 else (rank + 1) * side_x / ws
+    cap = int(n_local_est * 1.15) + 4096
+    eng = Engine(local, cap)
+    a = Agents.empty(cap)
+    stream = torch.cuda.Stream()
+    if strong:
+        # every rank draws the same per-id population and keeps its slab (A48)
+        chunk = 50_000_000
+        tmp = Agents.empty(chunk)
+        a.n = 0
+        for id0 in range(0, cfg.n, chunk):
+            m = min(chunk, cfg.n - id0)
+            eng.init_spheres(tmp, m, id0=id0, seed=cfg.seed, side=cfg.side, d_lo=cfg.d_lo,
+                             stream=stream)
+            torch.cuda.synchronize()
+            sel = (tmp.x[:m] >= lo) & (tmp.x[:m] < hi)
+            k = int(sel.sum())
+            for f in ("x", "y", "z", "diameter", "id", "flags"):
+                getattr(a, f)[a.n:a.n + k].copy_(getattr(tmp, f)[:m][sel])
+            a.n += k
+        del tmp
+    else:
+        eng.init_spheres(a, cfg.n, id0=rank * cfg.n, seed=cfg.seed, side=cfg.side,
+                         d_lo=cfg.d_lo, d_width=cfg.d_width, d_random=cfg.d_random,
+                         stream=stream)
+        torch.cuda.synchronize()
+        a.x[:cfg.n] += rank * cfg.side
+    torch.cuda.synchronize()
+    ops = LibOps(eng, stream=stream)
+    tr = DistTransport(ops, torch.device("cuda", local)) if ws > 1 else None
+    if tr is None:
+        from paper_2503_10796_b200.slabs import LocalTransport
+        tr = LocalTransport()
+    params = Params(k=cfg.k, gamma=cfg.gamma, dt=cfg.dt, max_displacement=cfg.max_disp,
+                    detect_static=cfg.detect_static)
+    dom = SlabDomain([Slab(rank, lo, hi, ops, a)], tr, params)
+    for _ in range(args.warmup):
+        dom.step()
+    n_loc = a.n
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = eng.stats()["launches"]
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            dom.step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
+    tot = torch.tensor([float(n_loc)], dtype=torch.float64, device="cuda")
+    if ws > 1:
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+        dist.all_reduce(tot, op=dist.ReduceOp.SUM)
+    ms_step = float(ms[0]) / args.steps
+    value = float(tot[0]) / (ms_step * 1e-3)
+    if rank == 0:
+        line = _common(value, ms_step, ws, args,
+                       {"workload": ("cfg5 (configs[4]) x-slabs" if strong
+                                     else "cfg2 (configs[1]) per GPU, x-slabs side by side"),
+                        "agents_total": int(tot[0]), "slabs": ws,
+                        "transport": "torch.distributed NCCL p2p + all-reduce" if ws > 1 else "local",
+                        "l2": "inputs larger than L2; no flush", "parallelism": f"x-slab {ws}"},
+                       clk.summary(), eng.stats()["launches"] - launches0)
+        line["scaling"] = "strong" if strong else "weak"
+        line["roofline"] = None
+        line["e2e"] = None
+        line["note"] = "multi-GPU: device-timed max over ranks of the whole protocol step"
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
 
 
 def measure_e2e(eng, cfg, params, stream, steps: int = 3):
