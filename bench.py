@@ -185,6 +185,7 @@ def run_ours(args, ws, rank, local):
     cfg = W.PRESETS[args.config]
     eng = Engine(local, cfg.n)
     eng.set_option("mech_kernel", args.mech_kernel)
+    eng.set_option("fuse_reduce", 1)   # a1 of the next step fused into the mechanics epilogue
     a = Agents.empty(cfg.n)
     stream = torch.cuda.Stream()
     with torch.cuda.stream(stream):

@@ -276,6 +276,11 @@ bdm_status bdm_neighbor_pairs(bdm_handle h, const bdm_agents *a, double radius,
  *   "sir_index_capacity"  infected agents the SIR index holds (0 = max(65536, n/16)).
  *   "prefilter"    1 (default) / 0: conservative fp32 candidate test in the tile kernel
  *                  (never rejects a neighbour; the exact fp64 test decides).
+ *   "fuse_reduce"  0 (default) / 1: bdm_mech_step also reduces the extent of the new
+ *                  state (row a1 of the next step), and the next bdm_grid_build on the
+ *                  same arrays (same x pointer and n) skips its own reduction.  The
+ *                  caller must not modify positions or diameters in between (every
+ *                  other bdm_* call that changes agents clears the fused extent).
  * All settings produce bit-identical results.  Errors: BDM_EINVAL for an unknown name/value. */
 bdm_status bdm_set_option(bdm_handle h, const char *name, int64_t value);
 

@@ -187,6 +187,7 @@ bdm_status bdm_destroy(bdm_handle h) {
 bdm_status bdm_init_spheres(bdm_handle h, bdm_agents *a, int64_t id0, int64_t n, uint64_t seed,
                             double side, double d_lo, double d_width, int32_t d_random,
                             void *stream) {
+    if (h) ((Ctx *)h)->fused_valid = false;
     if (!h) return fail(BDM_EINVAL, "handle is NULL");
     if (!a || n < 0 || n > a->capacity || id0 < 0)
         return fail(BDM_EINVAL, "bad n / id0 / capacity");
@@ -261,6 +262,9 @@ bdm_status bdm_mech_step(bdm_handle h, bdm_agents *a, const bdm_params *p, void 
     bdm_agents all = *a;
     all.n = a->n + c->grid_ng;
     const bdm_status s2 = launch_mech(c, &all, p, (cudaStream_t)stream);
+    c->fused_valid = (s2 == BDM_OK) && c->fuse_reduce && c->grid_ng == 0;
+    c->fused_x = a->x;
+    c->fused_n = a->n;
     return s2;
 }
 
@@ -299,6 +303,7 @@ bdm_status bdm_step_host(bdm_handle h, const bdm_agents *hin, bdm_agents *hout, 
 
 bdm_status bdm_grow_divide(bdm_handle h, bdm_agents *a, const bdm_params *p, double growth,
                            double v_max, int64_t *n_out_host, void *stream) {
+    if (h) ((Ctx *)h)->fused_valid = false;
     if (!h || !p || !n_out_host) return fail(BDM_EINVAL, "NULL argument");
     Ctx *c = (Ctx *)h;
     bdm_status s = check_agents(a, true);
@@ -315,6 +320,7 @@ bdm_status bdm_grow_divide(bdm_handle h, bdm_agents *a, const bdm_params *p, dou
 bdm_status bdm_sir_step(bdm_handle h, bdm_agents *a, const bdm_params *p, double side,
                         double radius, double p_inf, double p_rec, int64_t *counts_host,
                         void *stream) {
+    if (h) ((Ctx *)h)->fused_valid = false;
     if (!h || !p || !a) return fail(BDM_EINVAL, "NULL argument");
     Ctx *c = (Ctx *)h;
     if (a->n < 0 || a->n > a->capacity) return fail(BDM_EINVAL, "n < 0 or n > capacity");
@@ -336,6 +342,7 @@ bdm_status bdm_local_frame(bdm_handle h, const bdm_agents *a, double *frame_dev,
 }
 
 bdm_status bdm_set_frame(bdm_handle h, const double *frame_dev) {
+    if (h) ((Ctx *)h)->fused_valid = false;
     if (!h) return fail(BDM_EINVAL, "handle is NULL");
     Ctx *c = (Ctx *)h;
     c->frame = frame_dev;
@@ -346,6 +353,7 @@ bdm_status bdm_set_frame(bdm_handle h, const double *frame_dev) {
 bdm_status bdm_pack_slab(bdm_handle h, bdm_agents *a, double lo, double hi, double margin,
                          int32_t what, bdm_agents *to_left, bdm_agents *to_right,
                          int64_t *counts_host, void *stream) {
+    if (h) ((Ctx *)h)->fused_valid = false;
     if (!h || !a || !to_left || !to_right || !counts_host) return fail(BDM_EINVAL, "NULL argument");
     if (what != BDM_PACK_MIGRATE && what != BDM_PACK_AURA) return fail(BDM_EINVAL, "bad what");
     if (!(lo <= hi) || !(margin >= 0.0)) return fail(BDM_EINVAL, "need lo <= hi and margin >= 0");
@@ -359,6 +367,7 @@ bdm_status bdm_pack_slab(bdm_handle h, bdm_agents *a, double lo, double hi, doub
 }
 
 bdm_status bdm_append(bdm_handle h, bdm_agents *dst, const bdm_agents *src, void *stream) {
+    if (h) ((Ctx *)h)->fused_valid = false;
     if (!h || !dst || !src) return fail(BDM_EINVAL, "NULL argument");
     if (src->n < 0 || dst->n < 0) return fail(BDM_EINVAL, "negative n");
     if (dst->n + src->n > dst->capacity) return fail(BDM_ECAPACITY, "append exceeds capacity");
@@ -455,6 +464,12 @@ bdm_status bdm_set_option(bdm_handle h, const char *name, int64_t value) {
     if (strcmp(name, "sir_index_capacity") == 0) {
         if (value < 0) return fail(BDM_EINVAL, "sir_index_capacity must be >= 0");
         c->sir.icap_override = value;
+        return BDM_OK;
+    }
+    if (strcmp(name, "fuse_reduce") == 0) {
+        if (value < 0 || value > 1) return fail(BDM_EINVAL, "fuse_reduce must be 0 or 1");
+        c->fuse_reduce = (int)value;
+        c->fused_valid = false;
         return BDM_OK;
     }
     if (strcmp(name, "prefilter") == 0) {

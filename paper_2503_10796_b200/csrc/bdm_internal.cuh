@@ -93,6 +93,10 @@ struct Ctx {
     int64_t launches = 0;  // kernels launched (host-side count)
     int mech_kernel = 0;   // option "mech_kernel": 0 tile kernel, 1 per-agent reference kernel
     int prefilter = 1;     // option "prefilter": fp32 conservative candidate test in the tile kernel
+    int fuse_reduce = 0;   // option "fuse_reduce": next step's a1 extent from the mech epilogue
+    bool fused_valid = false;          // the scalars hold the extent of (fused_x, fused_n)
+    const double *fused_x = nullptr;
+    int64_t fused_n = 0;
     SirWs sir;
 };
 

@@ -121,7 +121,8 @@ __global__ void __launch_bounds__(256) k_reduce(int64_t n, const double *__restr
 // With a global frame (multi-GPU, 8(e)) the origin and R come from the frame (the
 // all-reduced minimum corner and largest diameter of every rank) and the local
 // extent only fixes the lattice offset and dims.
-__global__ void k_setup(DevScalars *sc, double radius, const double *__restrict__ frame) {
+__global__ void k_setup(DevScalars *sc, double radius, const double *__restrict__ frame,
+                        int reset_after) {
     if (threadIdx.x != 0) return;
     const double R = radius > 0.0 ? radius : (frame ? -frame[3] : dec_double(sc->enc_dmax));
     const double L = R * (1.0 + 0x1p-20);
@@ -147,12 +148,22 @@ __global__ void k_setup(DevScalars *sc, double radius, const double *__restrict_
     }
     sc->nslots = ns;
     if (bad || ns >= 0xFFFFFFFFll || ns > sc->slot_cap) sc->overflow = 1;
+    if (reset_after) {  // the mechanics epilogue accumulates the next step's extent
+        for (int a = 0; a < 3; ++a) {
+            sc->enc_lo[a] = enc_double(INFINITY);
+            sc->enc_hi[a] = enc_double(-INFINITY);
+        }
+        sc->enc_dmax = enc_double(-INFINITY);
+    }
 }
 
 bdm_status launch_grid_geometry(Ctx *c, const bdm_agents *a, const bdm_agents *g, double radius,
                                 cudaStream_t st) {
-    k_reset_scalars<<<1, 32, 0, st>>>(c->sc);
-    const bdm_agents *sets[2] = {a, g};
+    // the extent of `a` is already in the scalars when the previous mechanics step wrote
+    // exactly these arrays with the fused reduction (option "fuse_reduce")
+    const bool reuse = c->fuse_reduce && c->fused_valid && c->fused_x == a->x && c->fused_n == a->n;
+    if (!reuse) k_reset_scalars<<<1, 32, 0, st>>>(c->sc);
+    const bdm_agents *sets[2] = {reuse ? nullptr : a, g};
     for (const bdm_agents *s : sets) {
         if (!s || s->n == 0) continue;
         int64_t blocks = (s->n + 255) / 256;
@@ -161,8 +172,9 @@ bdm_status launch_grid_geometry(Ctx *c, const bdm_agents *a, const bdm_agents *g
         k_reduce<<<(unsigned)blocks, 256, 0, st>>>(s->n, s->x, s->y, s->z, s->diameter, c->sc);
         c->launches += 1;
     }
-    k_setup<<<1, 32, 0, st>>>(c->sc, radius, c->frame);
-    c->launches += 2;
+    k_setup<<<1, 32, 0, st>>>(c->sc, radius, c->frame, c->fuse_reduce ? 1 : 0);
+    c->launches += reuse ? 1 : 2;
+    c->fused_valid = false;
     BDM_LAUNCH_CHECK("grid geometry");
     return BDM_OK;
 }

@@ -37,7 +37,7 @@ struct MechArgs {
     const double *__restrict__ svol;  // nullable: volume travels with the agents
     double *__restrict__ ovol;
     double k, gamma, dt, max_disp, tau;
-    int detect_static, boundary;
+    int detect_static, boundary, fuse;
     double lo0, lo1, lo2, hi0, hi1, hi2;
 };
 
@@ -64,6 +64,9 @@ __device__ __forceinline__ GridView load_grid(const DevScalars *__restrict__ sc)
 
 struct Counts {
     uint32_t cand = 0, nbr = 0, cont = 0, stat = 0, moved = 0;
+    // extent of the new state (a1 of the next step, fused: option "fuse_reduce")
+    double lo0 = INFINITY, lo1 = INFINITY, lo2 = INFINITY;
+    double hi0 = -INFINITY, hi1 = -INFINITY, hi2 = -INFINITY, dmax = -INFINITY;
 };
 
 // a8 + a9 + write-back for one agent (shared by both kernels); s is the sorted slot,
@@ -96,6 +99,10 @@ __device__ __forceinline__ void finish_agent(const MechArgs &A, int64_t s, doubl
     }
     const bool moved = (Dx != 0.0 || Dy != 0.0 || Dz != 0.0);
     c.moved += moved ? 1u : 0u;
+    c.lo0 = fmin(c.lo0, nx); c.hi0 = fmax(c.hi0, nx);
+    c.lo1 = fmin(c.lo1, ny); c.hi1 = fmax(c.hi1, ny);
+    c.lo2 = fmin(c.lo2, nz); c.hi2 = fmax(c.hi2, nz);
+    c.dmax = fmax(c.dmax, A.sd[s]);
     c.stat += is_static ? 1u : 0u;
     A.ox[o] = nx;
     A.oy[o] = ny;
@@ -193,7 +200,22 @@ __device__ __forceinline__ void mech_agent_global(const MechArgs &A, const GridV
 }
 
 template <bool kStats>
-__device__ __forceinline__ void flush_counts(const Counts &c, DevScalars *sc) {
+__device__ __forceinline__ void flush_counts(const Counts &c, DevScalars *sc, int fuse) {
+    if (fuse) {  // exact min/max of the new positions -> the next grid build's a1
+        double v[7] = {c.lo0, c.lo1, c.lo2, c.hi0, c.hi1, c.hi2, c.dmax};
+#pragma unroll
+        for (int q = 0; q < 7; ++q)
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const double t = __shfl_xor_sync(0xffffffffu, v[q], o);
+                v[q] = q < 3 ? fmin(v[q], t) : fmax(v[q], t);
+            }
+        if ((threadIdx.x & 31) == 0) {
+            for (int q = 0; q < 3; ++q) atomicMin(&sc->enc_lo[q], enc_double(v[q]));
+            for (int q = 0; q < 3; ++q) atomicMax(&sc->enc_hi[q], enc_double(v[3 + q]));
+            atomicMax(&sc->enc_dmax, enc_double(v[6]));
+        }
+    }
     if (!kStats) return;
     const unsigned long long a = warp_sum_u64(c.cand), b = warp_sum_u64(c.nbr),
                              d = warp_sum_u64(c.cont), e = warp_sum_u64(c.stat),
@@ -215,7 +237,7 @@ __global__ void __launch_bounds__(256) k_mech(MechArgs A, DevScalars *__restrict
     Counts c;
     const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (s < A.n) mech_agent_global(A, g, s, c);
-    flush_counts<kStats>(c, sc);
+    flush_counts<kStats>(c, sc, A.fuse);
 }
 
 // ============================================================== tile kernel
@@ -533,7 +555,7 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_mech_tile(MechArgs A, DevSc
         }
         __syncthreads();  // before the next tile overwrites the staged region
     }
-    flush_counts<kStats>(c, sc);
+    flush_counts<kStats>(c, sc, A.fuse);
 }
 
 template <bool kStats>
@@ -566,6 +588,7 @@ bdm_status launch_mech(Ctx *c, bdm_agents *a, const bdm_params *p, cudaStream_t 
     A.k = p->k; A.gamma = p->gamma; A.dt = p->dt; A.max_disp = p->max_displacement;
     A.tau = p->force_threshold;
     A.detect_static = p->detect_static; A.boundary = p->boundary;
+    A.fuse = c->fuse_reduce && c->grid_ng == 0;
     A.lo0 = p->lo[0]; A.lo1 = p->lo[1]; A.lo2 = p->lo[2];
     A.hi0 = p->hi[0]; A.hi1 = p->hi[1]; A.hi2 = p->hi[2];
     if (p->collect_stats)

@@ -25,6 +25,7 @@ def eng(request):
     from paper_2503_10796_b200 import Engine
     e = Engine(0, 1 << 16)
     e.set_option("mech_kernel", request.param)
+    e.set_option("fuse_reduce", 1 if request.param == 0 else 0)  # tile kernel: fused a1
     yield e
     e.close()
 
