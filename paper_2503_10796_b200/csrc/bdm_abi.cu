@@ -116,6 +116,7 @@ static bdm_status read_latches(Ctx *c, bool clear) {
         st = fail(BDM_ECAPACITY, "grid needs " + std::to_string(c->sc_host->nslots) +
                                      " slots, capacity " + std::to_string(c->slot_cap));
     }
+    if (st != BDM_OK) c->fused_valid = false;  // a skipped step leaves no fused extent
     if (clear && st != BDM_OK) {
         int32_t z[2] = {0, 0};
         BDM_CUDA_TRY(cudaMemcpy(&c->sc->overflow, z, sizeof(z), cudaMemcpyHostToDevice));
