@@ -50,7 +50,9 @@ struct DevScalars {
 // SIR workspace (kernels_sir.cu), allocated on first use
 struct SirWs {
     unsigned long long *keys = nullptr;
-    uint32_t *heads = nullptr, *next = nullptr, *bitmap = nullptr;
+    unsigned long long *heads = nullptr;
+    uint32_t *next = nullptr, *bitmap = nullptr;
+    unsigned long long stamp = 0;
     double *ix = nullptr, *iy = nullptr, *iz = nullptr;
     void *misc = nullptr;   // infected count + 4 counters
     int64_t icap = 0, tsize = 0, bwords = 0;

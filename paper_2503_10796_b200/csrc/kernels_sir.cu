@@ -23,8 +23,11 @@
 namespace bdm {
 
 constexpr int kCoarse = 16;                  // fine boxes per coarse block (per axis)
-constexpr unsigned long long kEmpty = ~0ull;
 constexpr uint32_t kNone = 0xFFFFFFFFu;
+// Hash slots carry the step stamp in their upper 24 bits, so the table never needs
+// clearing: a slot whose stamp is not the current one is empty.  Box keys need
+// <= 39 bits (D <= 8192).
+constexpr int kStampShift = 40;
 
 struct SirArgs {
     int64_t n;
@@ -34,11 +37,13 @@ struct SirArgs {
     uint8_t *__restrict__ state;
     const uint32_t *__restrict__ id;  // nullable: id = index
     double side, L, R2, half, p_inf, p_rec;
-    int D, B;                         // fine boxes / coarse blocks per axis
+    double Rq, invC;                  // coarse test: padded radius, 1 / (16 L)
+    int D, B, cf;                     // fine boxes / coarse blocks per axis; boxes per block
     uint32_t k0, k1, step;
     // infected index
-    unsigned long long *__restrict__ keys;
-    uint32_t *__restrict__ heads;
+    unsigned long long *__restrict__ keys;   // stamp << 40 | box key
+    unsigned long long *__restrict__ heads;  // stamp << 32 | first infected slot
+    unsigned long long stamp;                // 1 .. 2^24-1
     uint32_t *__restrict__ next;
     double *__restrict__ ix;
     double *__restrict__ iy;
@@ -67,9 +72,31 @@ __device__ __forceinline__ double min_image(double d, double side, double half) 
     return d;
 }
 
+__device__ void sir_insert(const SirArgs &A, int64_t i, DevScalars *__restrict__ sc);
+
+// 16 states per thread (one 16-byte load when aligned); inserts the infected ones.
 __global__ void __launch_bounds__(256) k_sir_collect(SirArgs A, DevScalars *__restrict__ sc) {
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= A.n || A.state[i] != 1) return;
+    const int64_t base = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * 16;
+    if (base >= A.n) return;
+    if (base + 16 <= A.n && (((uintptr_t)(A.state + base)) & 15u) == 0) {
+        const uint4 v = *reinterpret_cast<const uint4 *>(A.state + base);
+        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const uint32_t x = w[q];
+            // any byte == 1 (infected)?  (bytes are 0, 1 or 2)
+            if (((x & 0x01010101u)) == 0u) continue;
+#pragma unroll
+            for (int b = 0; b < 4; ++b)
+                if (((x >> (8 * b)) & 0xFFu) == 1u) sir_insert(A, base + 4 * q + b, sc);
+        }
+    } else {
+        for (int64_t i = base; i < A.n && i < base + 16; ++i)
+            if (A.state[i] == 1) sir_insert(A, i, sc);
+    }
+}
+
+__device__ void sir_insert(const SirArgs &A, int64_t i, DevScalars *__restrict__ sc) {
     const uint32_t slot = atomicAdd(A.icount, 1u);
     if (slot >= A.icap) {
         sc->overflow = 3;  // infected index too small: the update is skipped
@@ -82,56 +109,87 @@ __global__ void __launch_bounds__(256) k_sir_collect(SirArgs A, DevScalars *__re
     const int bx = sir_box(px, A.L, A.D), by = sir_box(py, A.L, A.D), bz = sir_box(pz, A.L, A.D);
     const unsigned long long key =
         ((unsigned long long)bz * A.D + (unsigned long long)by) * A.D + (unsigned long long)bx;
+    const unsigned long long skey = (A.stamp << kStampShift) | key;
     unsigned long long h = box_hash(key, A.tbits);
     for (;;) {
-        const unsigned long long prev = atomicCAS(&A.keys[h], kEmpty, key);
-        if (prev == kEmpty || prev == key) break;
+        unsigned long long cur = A.keys[h];
+        if (cur == skey) break;                       // box already present this step
+        if ((cur >> kStampShift) != A.stamp) {        // stale slot: try to claim it
+            const unsigned long long prev = atomicCAS(&A.keys[h], cur, skey);
+            if (prev == cur || prev == skey) break;
+            if ((prev >> kStampShift) != A.stamp) continue;  // lost to another stale write
+        }
         h = (h + 1) & A.tmask;
     }
-    A.next[slot] = atomicExch(&A.heads[h], slot);
-    const uint32_t cb = (uint32_t)(((bz / kCoarse) * A.B + (by / kCoarse)) * A.B + (bx / kCoarse));
+    const unsigned long long old = atomicExch(&A.heads[h], (A.stamp << 32) | slot);
+    A.next[slot] = ((old >> 32) == A.stamp) ? (uint32_t)old : kNone;
+    const uint32_t cb = (uint32_t)(((bz / A.cf) * A.B + (by / A.cf)) * A.B + (bx / A.cf));
     atomicOr(&A.bitmap[cb >> 5], 1u << (cb & 31u));
 }
 
-// Distinct coarse blocks among those of the fine boxes b-1, b, b+1 (periodic): 1-3.
-__device__ __forceinline__ int coarse_set(int b, int D, int c[3]) {
-    const int lo = ((b - 1 + D) % D) / kCoarse, mid = b / kCoarse, hi = ((b + 1) % D) / kCoarse;
-    int n = 0;
-    c[n++] = mid;
-    if (lo != mid) c[n++] = lo;
-    if (hi != mid && hi != lo) c[n++] = hi;
-    return n;
+// Conservative coarse test: the coarse blocks (cf^3 fine boxes, edge C = cf L, cf = 16)
+// that intersect [p - R', p + R'] per axis, R' = R(1 + 2^-20) + 2^-30 C, computed with
+// a multiplication (no exactness needed: every fine box within R of p lies in one of
+// them, since 2R' < C) and wrapped periodically by comparison.  D is a multiple of cf
+// (the GPU's own fine lattice, L = side/D >= R), so every block is complete; for
+// D < 32 a single block covers the space.
+__device__ __forceinline__ int coarse_range(double p, double Rq, double invC, int B, int c[2]) {
+    int lo = (int)floor((p - Rq) * invC), hi = (int)floor((p + Rq) * invC);
+    lo = lo < 0 ? lo + B : (lo >= B ? lo - B : lo);
+    hi = hi < 0 ? hi + B : (hi >= B ? hi - B : hi);
+    c[0] = lo;
+    c[1] = hi;
+    return lo == hi ? 1 : 2;
 }
 
-__device__ __forceinline__ bool coarse_hit(const SirArgs &A, int bx, int by, int bz) {
-    int cx[3], cy[3], cz[3];
-    const int nx = coarse_set(bx, A.D, cx), ny = coarse_set(by, A.D, cy), nz = coarse_set(bz, A.D, cz);
-    for (int a = 0; a < nz; ++a)
-        for (int b = 0; b < ny; ++b)
-            for (int c = 0; c < nx; ++c) {
-                const uint32_t cb = (uint32_t)((cz[a] * A.B + cy[b]) * A.B + cx[c]);
-                if (A.bitmap[cb >> 5] & (1u << (cb & 31u))) return true;
+__device__ __forceinline__ bool coarse_hit(const SirArgs &A, double px, double py, double pz) {
+    int cx[2], cy[2], cz[2];
+    const int nx = coarse_range(px, A.Rq, A.invC, A.B, cx);
+    const int ny = coarse_range(py, A.Rq, A.invC, A.B, cy);
+    const int nz = coarse_range(pz, A.Rq, A.invC, A.B, cz);
+    bool hit = false;
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int b = 0; b < 2; ++b)
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                if (a < nz && b < ny && q < nx) {
+                    const uint32_t cb = (uint32_t)((cz[a] * A.B + cy[b]) * A.B + cx[q]);
+                    hit |= (A.bitmap[cb >> 5] >> (cb & 31u)) & 1u;
+                }
             }
-    return false;
+    return hit;
 }
 
-__device__ bool infected_within(const SirArgs &A, double px, double py, double pz) {
+__device__ __noinline__ bool infected_fine(const SirArgs &A, double px, double py, double pz);
+
+__device__ __forceinline__ bool infected_within(const SirArgs &A, double px, double py, double pz) {
+    if (!coarse_hit(A, px, py, pz)) return false;
+    return infected_fine(A, px, py, pz);
+}
+
+// Exact search of the 27 fine boxes (same box formula as the index), minimum image.
+__device__ __noinline__ bool infected_fine(const SirArgs &A, double px, double py, double pz) {
     const int bx = sir_box(px, A.L, A.D), by = sir_box(py, A.L, A.D), bz = sir_box(pz, A.L, A.D);
-    if (!coarse_hit(A, bx, by, bz)) return false;
     const int D = A.D;
     for (int dz = -1; dz <= 1; ++dz)
         for (int dy = -1; dy <= 1; ++dy)
             for (int dx = -1; dx <= 1; ++dx) {
-                const int cx = (bx + dx + D) % D, cy = (by + dy + D) % D, cz = (bz + dz + D) % D;
+                int cx = bx + dx, cy = by + dy, cz = bz + dz;
+                cx = cx < 0 ? cx + D : (cx >= D ? cx - D : cx);
+                cy = cy < 0 ? cy + D : (cy >= D ? cy - D : cy);
+                cz = cz < 0 ? cz + D : (cz >= D ? cz - D : cz);
                 const unsigned long long key =
                     ((unsigned long long)cz * D + (unsigned long long)cy) * D + (unsigned long long)cx;
+                const unsigned long long skey = (A.stamp << kStampShift) | key;
                 unsigned long long h = box_hash(key, A.tbits);
                 uint32_t head = kNone;
                 for (;;) {
                     const unsigned long long k = A.keys[h];
-                    if (k == kEmpty) break;
-                    if (k == key) {
-                        head = A.heads[h];
+                    if ((k >> kStampShift) != A.stamp) break;  // empty this step
+                    if (k == skey) {
+                        head = (uint32_t)A.heads[h];
                         break;
                     }
                     h = (h + 1) & A.tmask;
@@ -147,13 +205,20 @@ __device__ bool infected_within(const SirArgs &A, double px, double py, double p
     return false;
 }
 
+// Alg. 9 wrap: el = fmod(el, max); if el < 0: el = max + el (R20, literal).  For
+// -max < el < 2 max, fmod is exact and equals el or el - max (Sterbenz: el - max is
+// exact for max <= el <= 2 max), so the fast path is bit-identical to fmod.
 __device__ __forceinline__ double wrap_alg9(double el, double max_bound) {
-    el = fmod(el, max_bound);
-    if (el < 0.0) el = max_bound + el;
-    return el;
+    double r;
+    if (el >= 0.0 && el < max_bound) r = el;
+    else if (el >= max_bound && el <= 2.0 * max_bound) r = el - max_bound;
+    else if (el < 0.0 && el > -max_bound) r = el;
+    else r = fmod(el, max_bound);
+    if (r < 0.0) r = max_bound + r;
+    return r;
 }
 
-__global__ void __launch_bounds__(256) k_sir_update(SirArgs A, DevScalars *__restrict__ sc) {
+__global__ void __launch_bounds__(256, 3) k_sir_update(SirArgs A, DevScalars *__restrict__ sc) {
     if (sc->overflow) return;
     unsigned long long cs = 0, ci = 0, cr = 0, cn = 0;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < A.n;
@@ -181,11 +246,13 @@ __global__ void __launch_bounds__(256) k_sir_update(SirArgs A, DevScalars *__res
         double vy = 2.0 * uniform32(w.b) - 1.0;
         double vz = 2.0 * uniform32(w.c) - 1.0;
         const double v2 = vx * vx + vy * vy + vz * vz;
-        if (v2 > 1.0) {
+        {   // computed by every lane (no divergence), selected where v.v > 1
             const double nv = sqrt(v2);
-            vx = vx / nv;
-            vy = vy / nv;
-            vz = vz / nv;
+            const bool cap = v2 > 1.0;
+            const double qx = vx / nv, qy = vy / nv, qz = vz / nv;
+            vx = cap ? qx : vx;
+            vy = cap ? qy : vy;
+            vz = cap ? qz : vz;
         }
         A.x[i] = wrap_alg9(px + vx, A.side);
         A.y[i] = wrap_alg9(py + vy, A.side);
@@ -219,7 +286,11 @@ static int next_pow2_bits(int64_t v) {
 bdm_status launch_sir_step(Ctx *c, bdm_agents *a, const bdm_params *p, double side, double radius,
                            double p_inf, double p_rec, long long *counts_host, cudaStream_t st) {
     SirWs &W = c->sir;
-    const int D = (int)floor(side / radius);
+    const int D0 = (int)floor(side / radius);
+    // the GPU's fine lattice: L = side/D >= R, D a multiple of kCoarse when large (the
+    // box size does not enter any result: the infection test is exact for any L >= R)
+    const int D = D0 >= 2 * kCoarse ? D0 - D0 % kCoarse : D0;
+    const int cf = D0 >= 2 * kCoarse ? kCoarse : (D0 > 0 ? D0 : 1);
     if (D < 3) {
         set_error("SIR needs side / radius >= 3 boxes per axis");
         return BDM_EINVAL;
@@ -228,7 +299,7 @@ bdm_status launch_sir_step(Ctx *c, bdm_agents *a, const bdm_params *p, double si
         set_error("SIR grid too large");
         return BDM_EINVAL;
     }
-    const int B = (D + kCoarse - 1) / kCoarse;
+    const int B = D / cf;
     const int64_t want_icap = a->n / 16 > 65536 ? a->n / 16 : 65536;
     const int64_t icap = W.icap_override > 0 ? W.icap_override : want_icap;
     const int tbits = next_pow2_bits(2 * icap);
@@ -236,16 +307,16 @@ bdm_status launch_sir_step(Ctx *c, bdm_agents *a, const bdm_params *p, double si
     const int64_t bwords = ((int64_t)B * B * B + 31) / 32;
     if (icap > W.icap || tsize > W.tsize || bwords > W.bwords) {
         BDM_CUDA_TRY(cudaStreamSynchronize(st));
-        void *old[] = {W.keys, W.heads, W.next, W.ix, W.iy, W.iz, W.bitmap};
+        void *old[] = {W.keys, W.heads, W.next, W.ix, W.iy, W.iz, W.bitmap, W.misc};
         for (void *q : old)
             if (q) cudaFree(q);
         W = SirWs{};
         if (cudaMalloc(&W.keys, tsize * 8) != cudaSuccess ||
-            cudaMalloc(&W.heads, tsize * 4) != cudaSuccess ||
+            cudaMalloc(&W.heads, tsize * 8) != cudaSuccess ||
             cudaMalloc(&W.next, icap * 4) != cudaSuccess || cudaMalloc(&W.ix, icap * 8) != cudaSuccess ||
             cudaMalloc(&W.iy, icap * 8) != cudaSuccess || cudaMalloc(&W.iz, icap * 8) != cudaSuccess ||
             cudaMalloc(&W.bitmap, bwords * 4) != cudaSuccess ||
-            (!W.misc && cudaMalloc(&W.misc, 64) != cudaSuccess)) {
+            cudaMalloc(&W.misc, 64) != cudaSuccess) {
             cudaGetLastError();
             set_error("SIR workspace allocation failed");
             return BDM_ECAPACITY;
@@ -253,6 +324,15 @@ bdm_status launch_sir_step(Ctx *c, bdm_agents *a, const bdm_params *p, double si
         W.icap = icap;
         W.tsize = tsize;
         W.bwords = bwords;
+        // fresh table: stamp 0 marks every slot empty
+        BDM_CUDA_TRY(cudaMemsetAsync(W.keys, 0, tsize * 8, st));
+        BDM_CUDA_TRY(cudaMemsetAsync(W.heads, 0, tsize * 8, st));
+        W.stamp = 0;
+    }
+    if (++W.stamp >= (1ull << 24)) {  // stamp wrap: clear once and restart
+        BDM_CUDA_TRY(cudaMemsetAsync(W.keys, 0, W.tsize * 8, st));
+        BDM_CUDA_TRY(cudaMemsetAsync(W.heads, 0, W.tsize * 8, st));
+        W.stamp = 1;
     }
     if (!W.misc) BDM_CUDA_TRY(cudaMalloc(&W.misc, 64));
     SirArgs A;
@@ -260,6 +340,9 @@ bdm_status launch_sir_step(Ctx *c, bdm_agents *a, const bdm_params *p, double si
     A.x = a->x; A.y = a->y; A.z = a->z; A.state = a->state; A.id = a->id;
     A.side = side;
     A.L = side / (double)D;
+    A.cf = cf;
+    A.invC = 1.0 / (A.L * (double)cf);
+    A.Rq = radius * (1.0 + 0x1p-20) + A.L * (double)cf * 0x1p-30;
     A.R2 = radius * radius;
     A.half = side * 0.5;
     A.p_inf = p_inf;
@@ -269,7 +352,8 @@ bdm_status launch_sir_step(Ctx *c, bdm_agents *a, const bdm_params *p, double si
     A.k0 = (uint32_t)p->seed;
     A.k1 = (uint32_t)(p->seed >> 32);
     A.step = p->step;
-    A.keys = W.keys; A.heads = W.heads; A.next = W.next;
+    A.keys = W.keys; A.heads = (unsigned long long *)W.heads; A.next = W.next;
+    A.stamp = W.stamp;
     A.ix = W.ix; A.iy = W.iy; A.iz = W.iz;
     A.bitmap = W.bitmap;
     A.icount = (uint32_t *)W.misc;
@@ -277,12 +361,10 @@ bdm_status launch_sir_step(Ctx *c, bdm_agents *a, const bdm_params *p, double si
     A.icap = (uint32_t)W.icap;
     A.tbits = tbits;
     A.tmask = (unsigned long long)(tsize - 1);
-    BDM_CUDA_TRY(cudaMemsetAsync(W.keys, 0xFF, tsize * 8, st));
-    BDM_CUDA_TRY(cudaMemsetAsync(W.heads, 0xFF, tsize * 4, st));
     BDM_CUDA_TRY(cudaMemsetAsync(W.bitmap, 0, ((int64_t)B * B * B + 31) / 32 * 4, st));
     BDM_CUDA_TRY(cudaMemsetAsync(W.misc, 0, 64, st));
     if (a->n > 0) {
-        const unsigned nb = (unsigned)((a->n + 255) / 256);
+        const unsigned nb = (unsigned)(((a->n + 15) / 16 + 255) / 256);
         k_sir_collect<<<nb, 256, 0, st>>>(A, c->sc);
         int64_t ub = (a->n + 255) / 256;
         const int64_t maxb = (int64_t)c->sm_count * 16;
