@@ -558,6 +558,412 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_mech_tile(MechArgs A, DevSc
     flush_counts<kStats>(c, sc, A.fuse);
 }
 
+// ============================================================== tile kernel v2
+// Same tile/region staging and the same canonical order as k_mech_tile; what changes
+// is how the work is issued:
+//   phase 1  the conservative fp32 candidate test runs on PAIRS of consecutive staged
+//            agents with packed f32x2 arithmetic (FADD2/FMUL2/FFMA2): the region is
+//            staged a second time as (x_m, x_m+1, y_m, y_m+1), (z_m, z_m+1), so a pair
+//            is one LDS.128 + one LDS.64.  Runs of odd length mask the second slot.
+//            Corner runs (dy != 0 and dz != 0) whose row is farther than R from the
+//            agent in (y, z) are not walked (conservative fp32 gap test).  A lane past
+//            its last run parks on a sentinel pair (coordinates 1e30) that never passes.
+//   phase 2a lane-parallel over the warp's survivors: exact fp64 test D <= R^2 (R4, R9),
+//            dist = sqrt(D), delta; contacts are compacted (ballot prefix) into a
+//            contact queue that keeps the agent-major canonical order
+//   phase 2b lane-parallel over the compacted contacts: Eq. 4.1/4.2, s = F_N / dist
+//            (the divisions and the second sqrt run with every lane busy)
+//   phase 3  each lane walks only its own contacts, in canonical order, with fma
+constexpr int kT2Threads = 128;
+constexpr int kT2Warps = kT2Threads / 32;
+constexpr int kM2Max = 448;   // staged agents per CTA
+constexpr int kK2Max = 24;    // fp32 survivors per agent
+constexpr int kQ2Cap = 320;   // survivors per warp batch
+constexpr int kC2Cap = 160;   // contacts per warp batch
+constexpr float kSentinel = 1e30f;
+
+struct Tile2Smem {
+    uint32_t start[216];
+    uint32_t off[217];
+    float4 XY[kM2Max + 2];                  // (x_m, x_m+1, y_m, y_m+1), region-relative fp32
+    float2 ZZ[kM2Max + 2];                  // (z_m, z_m+1)
+    double X[kM2Max], Y[kM2Max], Z[kM2Max], Rr[kM2Max];
+    uint32_t F[kM2Max];
+    uint8_t mbox[kM2Max];
+    struct Warp {
+        uint32_t run[9][32];                // per lane: walked runs (start | end << 16)
+        uint16_t lst[kK2Max + 2][32];       // per lane: survivors (+ scratch rows)
+        uint32_t pr[kQ2Cap];                // m | owner << 16 | codes
+        uint16_t cpre[kQ2Cap + 1];          // contacts before survivor p
+        uint16_t cp[kC2Cap];                // contact -> survivor index
+        double cdist[kC2Cap], cdelta[kC2Cap], cs[kC2Cap];
+        uint16_t mi[32];
+        uint8_t chg[32];
+        uint8_t cnz[kC2Cap];
+    } W[kT2Warps];
+};
+
+__device__ __forceinline__ unsigned long long pk2(float a, float b) {
+    unsigned long long r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ void up2(unsigned long long v, float &a, float &b) {
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+}
+// squared fp32 distances of (px,py,pz) to the staged pair (m, m+1): fl(fl(dz*dz + fl(dy*dy
+// + fl(dx*dx)))) per element with fma, exactly like the scalar prefilter of k_mech_tile
+__device__ __forceinline__ void dist2_pair(unsigned long long pxx, unsigned long long pyy,
+                                           unsigned long long pzz, float4 q, float2 qz,
+                                           float &d0, float &d1) {
+    unsigned long long ex, ey, ez, d;
+    const unsigned long long qx = pk2(q.x, q.y), qy = pk2(q.z, q.w), qzz = pk2(qz.x, qz.y);
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(ex) : "l"(pxx), "l"(qx));
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(ey) : "l"(pyy), "l"(qy));
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(ez) : "l"(pzz), "l"(qzz));
+    asm("mul.rn.f32x2 %0, %1, %1;" : "=l"(d) : "l"(ex));
+    asm("fma.rn.f32x2 %0, %1, %1, %2;" : "=l"(d) : "l"(ey), "l"(d));
+    asm("fma.rn.f32x2 %0, %1, %1, %2;" : "=l"(d) : "l"(ez), "l"(d));
+    up2(d, d0, d1);
+}
+
+template <bool kStats>
+__global__ void __launch_bounds__(kT2Threads, 3) k_mech_tile2(MechArgs A, DevScalars *__restrict__ sc,
+                                                             int allow_prefilter) {
+    if (sc->overflow) return;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    Tile2Smem &S = *reinterpret_cast<Tile2Smem *>(smem_raw);
+    const GridView g = load_grid(sc);
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    Tile2Smem::Warp &Wp = S.W[w];
+    const long long ntiles = (long long)g.T0 * g.T1 * g.T2;
+    const float R2f = (float)(g.R2 * (1.0 + 0x1p-12));
+    const float Lf = (float)g.L;
+    const double amax = fmax(fmax(fmax(fabs(g.o0), fabs(g.o1)), fmax(fabs(g.o2), fabs(sc->hi[0]))),
+                             fmax(fabs(sc->hi[1]), fabs(sc->hi[2])));
+    const bool use_pf = allow_prefilter && amax < 0x1p30 * g.L;
+    const unsigned lt_mask = (1u << lane) - 1u;
+    Counts c;
+
+    for (long long t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int tx = (int)(t % g.T0), ty = (int)((t / g.T0) % g.T1);
+        const int tz = (int)(t / ((long long)g.T0 * g.T1));
+        const int bx0 = 4 * tx - 1, by0 = 4 * ty - 1, bz0 = 4 * tz - 1;
+        const uint32_t g0 = A.box_start[(uint32_t)t * 64u];
+        const uint32_t g1 = A.box_start[(uint32_t)t * 64u + 64u];
+        const int nc = (int)(g1 - g0);
+        if (nc == 0) continue;  // uniform across the CTA
+        if (!use_pf) {  // |coordinates| / L >= 2^30: reference formulation for the tile
+            for (int k = tid; k < nc; k += kT2Threads) mech_agent_global(A, g, g0 + k, c);
+            continue;
+        }
+        // ---- box table of the 6^3 region (out-of-grid boxes are empty)
+        for (int lb = tid; lb < 216; lb += kT2Threads) {
+            const int gx = bx0 + lb % 6, gy = by0 + (lb / 6) % 6, gz = bz0 + lb / 36;
+            uint32_t st = 0, cnt = 0;
+            if (gx >= 0 && gy >= 0 && gz >= 0 && gx < g.D0 && gy < g.D1 && gz < g.D2) {
+                const uint32_t key = box_key(gx, gy, gz, g.T0, g.T1);
+                st = A.box_start[key];
+                cnt = A.box_start[key + 1] - st;
+            }
+            S.start[lb] = st;
+            S.off[lb] = cnt;
+        }
+        __syncthreads();
+        if (w == 0) {  // exclusive scan of the 216 counts (7 per lane)
+            uint32_t v[7], sum = 0;
+#pragma unroll
+            for (int k = 0; k < 7; ++k) {
+                const int lb = lane * 7 + k;
+                v[k] = lb < 216 ? S.off[lb] : 0u;
+                sum += v[k];
+            }
+            uint32_t inc = sum;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+                if (lane >= o) inc += y;
+            }
+            uint32_t run = inc - sum;
+#pragma unroll
+            for (int k = 0; k < 7; ++k) {
+                const int lb = lane * 7 + k;
+                if (lb <= 216) S.off[lb] = run;
+                run += v[k];
+            }
+        }
+        __syncthreads();
+        const int M = (int)S.off[216];
+        if (M > kM2Max) {
+            for (int k = tid; k < nc; k += kT2Threads) mech_agent_global(A, g, g0 + k, c);
+            __syncthreads();
+            continue;
+        }
+        // ---- stage the region (row-major boxes, ascending id in a box)
+        const double X0 = g.o0 + (double)(bx0 + g.b0) * g.L, Y0 = g.o1 + (double)(by0 + g.b1) * g.L,
+                     Z0 = g.o2 + (double)(bz0 + g.b2) * g.L;
+        for (int lb = tid; lb < 216; lb += kT2Threads)
+            for (uint32_t m = S.off[lb]; m < S.off[lb + 1]; ++m) S.mbox[m] = (uint8_t)lb;
+        __syncthreads();
+        float *xy = reinterpret_cast<float *>(S.XY);
+        float *zz = reinterpret_cast<float *>(S.ZZ);
+        for (int m = tid; m < M; m += kT2Threads) {
+            const int lb = S.mbox[m];
+            const uint32_t gi = S.start[lb] + ((uint32_t)m - S.off[lb]);
+            const double x = A.sx[gi], y = A.sy[gi], z = A.sz[gi], d = A.sd[gi];
+            S.X[m] = x;
+            S.Y[m] = y;
+            S.Z[m] = z;
+            S.Rr[m] = d * 0.5;
+            S.F[m] = A.sflags[gi];
+            const float xr = (float)(x - X0), yr = (float)(y - Y0), zr = (float)(z - Z0);
+            xy[4 * m + 0] = xr;
+            xy[4 * m + 2] = yr;
+            zz[2 * m + 0] = zr;
+            if (m > 0) {
+                xy[4 * (m - 1) + 1] = xr;
+                xy[4 * (m - 1) + 3] = yr;
+                zz[2 * (m - 1) + 1] = zr;
+            }
+        }
+        if (tid == 0) {  // sentinel pair at M (and the upper half of M - 1)
+            S.XY[M] = make_float4(kSentinel, kSentinel, kSentinel, kSentinel);
+            S.ZZ[M] = make_float2(kSentinel, kSentinel);
+            if (M > 0) {
+                xy[4 * (M - 1) + 1] = kSentinel;
+                xy[4 * (M - 1) + 3] = kSentinel;
+                zz[2 * (M - 1) + 1] = kSentinel;
+            }
+        }
+        __syncthreads();
+
+        const int nw = min(kT2Warps, (nc + 31) >> 5);
+        const int share = (nc + nw - 1) / nw;
+        const int wlo = w < nw ? min(nc, w * share) : nc;
+        const int whi = w < nw ? min(nc, wlo + share) : nc;
+        for (int base = wlo; base < whi; base += 32) {  // warp-uniform
+            const int na = min(32, whi - base);
+            const int k = base + lane;
+            const bool active = lane < na && !(A.sflags[g0 + (uint32_t)k] & kGhost);
+            int mi = M, ca = 0, nr = 0, npair = 0;
+            uint32_t fi = 0;
+            double xi = 0.0, yi = 0.0, zi = 0.0;
+            bool cand_static = false;
+            float pxr = 0.f, pyr = 0.f, pzr = 0.f;
+            if (active) {
+                const uint32_t gk = g0 + (uint32_t)k;
+                xi = A.sx[gk];
+                yi = A.sy[gk];
+                zi = A.sz[gk];
+                const int lx = (int)floor((xi - g.o0) / g.L) - g.b0 - bx0;
+                const int ly = (int)floor((yi - g.o1) / g.L) - g.b1 - by0;
+                const int lz = (int)floor((zi - g.o2) / g.L) - g.b2 - bz0;
+                const int lbi = (lz * 6 + ly) * 6 + lx;
+                mi = (int)(S.off[lbi] + (gk - S.start[lbi]));
+                fi = S.F[mi];
+                cand_static = A.detect_static && !(fi & kChanged) &&
+                              ((fi >> BDM_FLAG_NNZ_SHIFT) & 3u) <= 1u;
+                const float4 q = S.XY[mi];
+                pxr = q.x;
+                pyr = q.z;
+                pzr = S.ZZ[mi].x;
+                // (y, z) gaps to the faces of the own box, for the corner-run test
+                const float gyl = pyr - (float)ly * Lf, gyh = (float)(ly + 1) * Lf - pyr;
+                const float gzl = pzr - (float)lz * Lf, gzh = (float)(lz + 1) * Lf - pzr;
+#pragma unroll
+                for (int r = 0; r < 9; ++r) {
+                    const int dzi = r / 3, dyi = r % 3;
+                    const int lb0 = lbi - 43 + dzi * 36 + dyi * 6;
+                    const uint32_t rs = S.off[lb0], re = S.off[lb0 + 3];
+                    ca += (int)(re - rs);
+                    bool walk = re > rs;
+                    if (dzi != 1 && dyi != 1) {
+                        const float gy = dyi == 0 ? gyl : gyh, gz = dzi == 0 ? gzl : gzh;
+                        walk = walk && fmaf(gz, gz, gy * gy) <= R2f;
+                    }
+                    if (walk) {
+                        Wp.run[nr][lane] = rs | (re << 16);
+                        ++nr;
+                        npair += (int)((re - rs + 1) >> 1);
+                    }
+                }
+                Wp.mi[lane] = (uint16_t)mi;
+                Wp.chg[lane] = 0;
+            }
+            const int cmax = __reduce_max_sync(0xffffffffu, npair);
+            __syncwarp();
+            // ---- phase 1: packed pair walk over the runs
+            int cnt = 0;
+            {
+                const unsigned long long pxx = pk2(pxr, pxr), pyy = pk2(pyr, pyr), pzz = pk2(pzr, pzr);
+                const uint32_t v0 = nr > 0 ? Wp.run[0][lane] : 0u;
+                int m = nr > 0 ? (int)(v0 & 0xFFFFu) : M, e = nr > 0 ? (int)(v0 >> 16) : M + 2;
+                int j = 1;
+                uint32_t nxt = Wp.run[1][lane];
+#pragma unroll 2
+                for (int it = 0; it < cmax; ++it) {
+                    const float4 q = S.XY[m];
+                    const float2 qz = S.ZZ[m];
+                    float d0, d1;
+                    dist2_pair(pxx, pyy, pzz, q, qz, d0, d1);
+                    const bool p0 = d0 <= R2f;
+                    const bool p1 = (d1 <= R2f) && (m + 1 < e);
+                    Wp.lst[cnt < kK2Max ? cnt : kK2Max][lane] = (uint16_t)m;
+                    cnt += p0 ? 1 : 0;
+                    Wp.lst[cnt < kK2Max ? cnt : kK2Max][lane] = (uint16_t)(m + 1);
+                    cnt += p1 ? 1 : 0;
+                    m += 2;
+                    const bool at_end = m >= e, more = j < nr;
+                    const int mn = more ? (int)(nxt & 0xFFFFu) : M;
+                    const int en = more ? (int)(nxt >> 16) : M + 2;
+                    m = at_end ? mn : m;
+                    e = at_end ? en : e;
+                    j += at_end ? 1 : 0;
+                    nxt = Wp.run[j < 9 ? j : 8][lane];
+                }
+            }
+            // ---- concatenate the lane lists (lane order = agent-major canonical order)
+            int cincl = cnt;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, cincl, o);
+                if (lane >= o) cincl += y;
+            }
+            const int my_off = cincl - cnt;
+            const int total = __shfl_sync(0xffffffffu, cincl, 31);
+            if (__any_sync(0xffffffffu, cnt > kK2Max) || total > kQ2Cap) {
+                if (active) mech_agent_global(A, g, g0 + k, c);
+                __syncwarp();
+                continue;
+            }
+            for (int jj = 0; jj < cnt; ++jj)
+                Wp.pr[my_off + jj] = (uint32_t)Wp.lst[jj][lane] | ((uint32_t)lane << 16);
+            __syncwarp();
+            const bool any_cs = __any_sync(0xffffffffu, cand_static);
+            if (any_cs) {  // static pull test: exact test + neighbour flags
+                for (int p = lane; p < total; p += 32) {
+                    const uint32_t e = Wp.pr[p];
+                    const int m = (int)(e & 0xFFFFu), owner = (int)((e >> 16) & 0xFFu);
+                    const int mo = Wp.mi[owner];
+                    if (m == mo) continue;
+                    const double ex = S.X[mo] - S.X[m], ey = S.Y[mo] - S.Y[m], ez = S.Z[mo] - S.Z[m];
+                    const double D = fma(ez, ez, fma(ey, ey, ex * ex));
+                    if (D <= g.R2 && (S.F[m] & kChanged)) Wp.chg[owner] = 1;
+                }
+                __syncwarp();
+            }
+            const bool is_static = active && cand_static && !Wp.chg[lane];
+            const unsigned stat_mask = __ballot_sync(0xffffffffu, is_static);
+            // ---- phase 2a: exact test, dist, delta; contacts compacted in order
+            int cbase = 0;
+            for (int p0 = 0; p0 < total; p0 += 32) {  // warp-uniform
+                const int p = p0 + lane;
+                bool contact = false;
+                double dist = 0.0, delta = 0.0;
+                uint32_t e = 0;
+                if (p < total) {
+                    e = Wp.pr[p];
+                    const int m = (int)(e & 0xFFFFu), owner = (int)((e >> 16) & 0xFFu);
+                    const int mo = Wp.mi[owner];
+                    const double ex = S.X[mo] - S.X[m], ey = S.Y[mo] - S.Y[m], ez = S.Z[mo] - S.Z[m];
+                    const double D = fma(ez, ez, fma(ey, ey, ex * ex));
+                    if (D <= g.R2 && m != mo) {
+                        e |= kCodeNbr;
+                        if (!((stat_mask >> owner) & 1u)) {
+                            dist = sqrt(D);
+                            delta = (S.Rr[mo] + S.Rr[m]) - dist;
+                            contact = delta > 0.0 && dist > 0.0;
+                        }
+                    }
+                }
+                const unsigned cb = __ballot_sync(0xffffffffu, contact);
+                const int cidx = cbase + __popc(cb & lt_mask);
+                if (p < total) {
+                    Wp.cpre[p] = (uint16_t)cidx;
+                    Wp.pr[p] = e | (contact ? kCodeContact : 0u);
+                    if (contact && cidx < kC2Cap) {
+                        Wp.cp[cidx] = (uint16_t)p;
+                        Wp.cdist[cidx] = dist;
+                        Wp.cdelta[cidx] = delta;
+                    }
+                }
+                cbase += __popc(cb);
+            }
+            if (cbase > kC2Cap) {  // contact queue overflow: reference path for this batch
+                __syncwarp();
+                if (active) mech_agent_global(A, g, g0 + k, c);
+                __syncwarp();
+                continue;
+            }
+            if (lane == 0) Wp.cpre[total] = (uint16_t)cbase;
+            __syncwarp();
+            // ---- phase 2b: Eq. 4.1/4.2 over the compacted contacts
+            for (int q = lane; q < cbase; q += 32) {
+                const uint32_t e = Wp.pr[Wp.cp[q]];
+                const int m = (int)(e & 0xFFFFu), owner = (int)((e >> 16) & 0xFFu);
+                const int mo = Wp.mi[owner];
+                const double ri = S.Rr[mo], rj = S.Rr[m];
+                const double delta = Wp.cdelta[q], dist = Wp.cdist[q];
+                const double rbar = (ri * rj) / (ri + rj);
+                const double Fn = A.k * delta - A.gamma * sqrt(rbar * delta);
+                Wp.cs[q] = Fn / dist;
+                Wp.cnz[q] = Fn != 0.0 ? 1 : 0;
+            }
+            __syncwarp();
+            // ---- phase 3: ordered accumulation of the own contacts
+            if (active) {
+                double Fx = 0.0, Fy = 0.0, Fz = 0.0;
+                int nnz = 0;
+                const int q0 = Wp.cpre[my_off], q1 = Wp.cpre[my_off + cnt];
+                for (int q = q0; q < q1; ++q) {
+                    const int m = (int)(Wp.pr[Wp.cp[q]] & 0xFFFFu);
+                    const double s_ = Wp.cs[q];
+                    const double ex = xi - S.X[m], ey = yi - S.Y[m], ez = zi - S.Z[m];
+                    Fx = fma(s_, ex, Fx);
+                    Fy = fma(s_, ey, Fy);
+                    Fz = fma(s_, ez, Fz);
+                    nnz += Wp.cnz[q];
+                }
+                nnz = nnz < 2 ? nnz : 2;
+                if (!is_static) {
+                    if (kStats) {
+                        uint32_t my_nbr = 0;
+                        for (int jj = my_off; jj < my_off + cnt; ++jj)
+                            my_nbr += (Wp.pr[jj] & kCodeNbr) ? 1u : 0u;
+                        c.cand += (uint32_t)(ca - 1);
+                        c.nbr += my_nbr;
+                        c.cont += (uint32_t)(q1 - q0);
+                    }
+                } else {
+                    nnz = (int)((fi >> BDM_FLAG_NNZ_SHIFT) & 3u);
+                }
+                finish_agent(A, g0 + k, xi, yi, zi, Fx, Fy, Fz, is_static, nnz, c);
+            }
+            __syncwarp();
+        }
+        __syncthreads();
+    }
+    flush_counts<kStats>(c, sc, A.fuse);
+}
+
+template <bool kStats>
+static bdm_status launch_tile2(Ctx *c, const MechArgs &A, cudaStream_t st) {
+    static bool attr_set = false;
+    static int per_sm = 0;
+    const int smem = (int)sizeof(Tile2Smem);
+    if (!attr_set) {
+        BDM_CUDA_TRY(cudaFuncSetAttribute(k_mech_tile2<kStats>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        BDM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mech_tile2<kStats>,
+                                                                   kT2Threads, smem));
+        if (per_sm < 1) per_sm = 1;
+        attr_set = true;
+    }
+    k_mech_tile2<kStats><<<(unsigned)(c->sm_count * per_sm), kT2Threads, smem, st>>>(
+        A, c->sc, c->prefilter);
+    return BDM_OK;
+}
+
 template <bool kStats>
 static bdm_status launch_tile(Ctx *c, const MechArgs &A, cudaStream_t st) {
     static bool attr_set = false;
@@ -593,8 +999,11 @@ bdm_status launch_mech(Ctx *c, bdm_agents *a, const bdm_params *p, cudaStream_t 
     A.hi0 = p->hi[0]; A.hi1 = p->hi[1]; A.hi2 = p->hi[2];
     if (p->collect_stats)
         BDM_CUDA_TRY(cudaMemsetAsync(c->sc->stats, 0, sizeof(c->sc->stats), st));
-    const bool tile = c->mech_kernel != 1;
-    if (tile) {
+    if (c->mech_kernel == 0) {
+        const bdm_status s = p->collect_stats ? launch_tile2<true>(c, A, st)
+                                              : launch_tile2<false>(c, A, st);
+        if (s != BDM_OK) return s;
+    } else if (c->mech_kernel == 2) {
         const bdm_status s = p->collect_stats ? launch_tile<true>(c, A, st)
                                               : launch_tile<false>(c, A, st);
         if (s != BDM_OK) return s;
