@@ -271,8 +271,11 @@ bdm_status bdm_neighbor_pairs(bdm_handle h, const bdm_agents *a, double radius,
 
 /* Tuning/diagnostic options (host-side, take effect at the next launch):
  *   "mech_kernel"  0 (default) tile kernel: CTA per 4x4x4-box tile with the halo staged
- *                  in shared memory and a lane-parallel pair queue;
- *                  1 per-agent reference kernel reading neighbours from global memory.
+ *                  in shared memory, trimmed candidate runs and a lane-parallel contact
+ *                  queue (5 CTAs per SM);
+ *                  1 per-agent reference kernel reading neighbours from global memory;
+ *                  2 the first tile kernel (per-lane pair lists, no run trimming);
+ *                  3 the kernel of 0 compiled for 4 CTAs per SM (no register spills).
  *   "sir_index_capacity"  infected agents the SIR index holds (0 = max(65536, n/16)).
  *   "prefilter"    1 (default) / 0: conservative fp32 candidate test in the tile kernel
  *                  (never rejects a neighbour; the exact fp64 test decides).

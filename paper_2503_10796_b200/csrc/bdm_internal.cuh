@@ -44,7 +44,8 @@ struct DevScalars {
     int32_t nonfinite;     // latched: a position was NaN/Inf
     unsigned long long stats[5];  // cand, nbr, cont, n_static, n_moved
     int32_t boff[3];       // lattice offset: box index = floor((x - o)/L) - boff (R12, 8(e))
-    int32_t pad_;
+    int32_t has_frame;     // the origin came from a global frame (multi-GPU)
+    double dmax_prev;      // max diameter of the grid build's input (the step keeps it)
 };
 
 // SIR workspace (kernels_sir.cu), allocated on first use

@@ -148,6 +148,8 @@ __global__ void k_setup(DevScalars *sc, double radius, const double *__restrict_
     }
     sc->nslots = ns;
     if (bad || ns >= 0xFFFFFFFFll || ns > sc->slot_cap) sc->overflow = 1;
+    sc->has_frame = frame ? 1 : 0;
+    sc->dmax_prev = dec_double(sc->enc_dmax);
     if (reset_after) {  // the mechanics epilogue accumulates the next step's extent
         for (int a = 0; a < 3; ++a) {
             sc->enc_lo[a] = enc_double(INFINITY);

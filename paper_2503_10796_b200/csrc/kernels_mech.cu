@@ -25,6 +25,7 @@ struct MechArgs {
     const double *__restrict__ sz;
     const double *__restrict__ sd;
     const uint32_t *__restrict__ sid;
+    const uint32_t *__restrict__ skey;  // sorted blocked-Morton key (box of each sorted slot)
     const uint32_t *__restrict__ sflags;
     const uint32_t *__restrict__ box_start;
     double *__restrict__ ox;
@@ -558,125 +559,387 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_mech_tile(MechArgs A, DevSc
     flush_counts<kStats>(c, sc, A.fuse);
 }
 
-// ============================================================== tile kernel v2
-// Same tile/region staging and the same canonical order as k_mech_tile; what changes
-// is how the work is issued:
-//   phase 1  the conservative fp32 candidate test runs on PAIRS of consecutive staged
-//            agents with packed f32x2 arithmetic (FADD2/FMUL2/FFMA2): the region is
-//            staged a second time as (x_m, x_m+1, y_m, y_m+1), (z_m, z_m+1), so a pair
-//            is one LDS.128 + one LDS.64.  Runs of odd length mask the second slot.
-//            Corner runs (dy != 0 and dz != 0) whose row is farther than R from the
-//            agent in (y, z) are not walked (conservative fp32 gap test).  A lane past
-//            its last run parks on a sentinel pair (coordinates 1e30) that never passes.
+// ============================================================== tile kernel v6
+// Same region staging and the same canonical order as k_mech_tile;
+// what changes is the cost per agent and per candidate, and the register budget:
+//   tile     the 6^3-box region table (box_start lookups, 2 per thread), one warp scan,
+//            staged index -> box and tile agent -> staged index maps, then the region
+//            agents (fp64 x, y, z, r, flags + an fp32 region-relative copy)
+//   batches  a tile's n agents are split into max(min(4, n), ceil(n/32)) equal batches
+//            (<= 32 agents, one per lane); warp w takes batches w, w+4, ...
+//   setup    the agent's staged index and box come from the tile map (no global key
+//            load, no fp64 divisions); each of the 9 (dz, dy) runs is trimmed box by
+//            box with a conservative fp32 test of the agent's distance to the box (a box
+//            farther than R cannot hold a neighbour, ~25 % of the 27-box candidates);
+//            the slot after the last run holds a sentinel run whose staged agent sits
+//            at 1e30, so the walk needs no bounds test
+//   phase 1  flattened, branch-free walk over the trimmed runs, conservative fp32
+//            distance test, survivors to the lane's own list
 //   phase 2a lane-parallel over the warp's survivors: exact fp64 test D <= R^2 (R4, R9),
-//            dist = sqrt(D), delta; contacts are compacted (ballot prefix) into a
-//            contact queue that keeps the agent-major canonical order
-//   phase 2b lane-parallel over the compacted contacts: Eq. 4.1/4.2, s = F_N / dist
-//            (the divisions and the second sqrt run with every lane busy)
-//   phase 3  each lane walks only its own contacts, in canonical order, with fma
-constexpr int kT2Threads = 128;
-constexpr int kT2Warps = kT2Threads / 32;
-constexpr int kM2Max = 448;   // staged agents per CTA
-constexpr int kK2Max = 24;    // fp32 survivors per agent
-constexpr int kQ2Cap = 320;   // survivors per warp batch
-constexpr int kC2Cap = 160;   // contacts per warp batch
+//            neighbour flags for the static pull test (a5), and a conservative contact
+//            pre-test D < (r_i + r_j)^2 (1 + 2^-30); candidates are compacted (ballot
+//            prefix) into a contact queue that keeps the agent-major canonical order
+//   phase 2b lane-parallel over the queue: dist = sqrt(D), delta > 0 (exact), Eq. 4.1/4.2,
+//            s = F_N / dist
+//   phase 3  each lane accumulates only its own contacts, in canonical order, with fma
+// Registers: the grid scalars live in shared memory and the fused extent / work counters
+// are reduced per batch into per-warp shared accumulators, so nothing fp64 stays live
+// across batches (96 registers, 5 CTAs per SM).
+// The fp32 prefilter: xr = fl32(x - X0) with X0 the region corner, |x - X0| <= 6L, so a
+// true neighbour (D <= R^2) has D32 <= R^2 (1 + 2.6e-6) for L = R(1+2^-20); the
+// threshold R^2 (1 + 2^-12) has a 90x margin, and the box-trimming gaps carry <= 1e-6 L
+// error against the same margin.  Needs |coordinates| / L < 2^30 (checked; else the
+// tile takes the reference formulation).
+constexpr int kT6Threads = 128;
+constexpr int kT6Warps = kT6Threads / 32;
+constexpr int kM6Max = 416;   // staged agents per region (6^3 boxes; mean ~343, sd ~19 at cfg2)
+constexpr int kK6Max = 20;    // fp32 survivors per agent (its own index included)
+constexpr int kQ6Cap = 320;   // survivors per batch (<= 32 agents, mean ~7.6 each)
+constexpr int kC6Cap = 192;   // contact candidates per batch (mean ~3.9 per agent)
+constexpr uint32_t kNbrBit = 1u << 23;
 constexpr float kSentinel = 1e30f;
 
-struct Tile2Smem {
+struct Warp6 {
+    uint32_t pr[kQ6Cap];                    // survivor: m | mo << 9 | owner << 18 | kNbrBit
+    uint16_t cpre[kQ6Cap + 2];              // contact candidates before survivor p
+    union {
+        struct {
+            uint32_t run[10][32];           // per lane: trimmed runs (start | end << 16)
+            uint16_t lst[kK6Max + 1][32];   // per lane: survivors (+ scratch row)
+        } a;
+        struct {
+            double cq[kC6Cap];              // D, then s = F_N / dist
+            uint32_t ce[kC6Cap];            // the survivor entry of the queue slot
+            uint8_t cf[kC6Cap];             // bit1 contact, bit0 F_N != 0
+        } b;
+    } u;
+    double ext[7];                          // fused extent: lo x,y,z, hi x,y,z, max d
+    unsigned long long cnt[5];              // cand, nbr, cont, static, moved
+    uint8_t chg[32];                        // agent saw a changed neighbour (a5)
+};
+struct Tile6Smem {
+    GridView g;
+    float R2f, Lf;
+    int use_pf, edge_only;                  // edge_only: fused extent from boundary tiles only
+    int lo_box[3], hi_box[3];               // boxes that can hold a new extremum (see below)
     uint32_t start[216];
-    uint32_t off[217];
-    float4 XY[kM2Max + 2];                  // (x_m, x_m+1, y_m, y_m+1), region-relative fp32
-    float2 ZZ[kM2Max + 2];                  // (z_m, z_m+1)
-    double X[kM2Max], Y[kM2Max], Z[kM2Max], Rr[kM2Max];
-    uint32_t F[kM2Max];
-    uint8_t mbox[kM2Max];
-    struct Warp {
-        uint32_t run[9][32];                // per lane: walked runs (start | end << 16)
-        uint16_t lst[kK2Max + 2][32];       // per lane: survivors (+ scratch rows)
-        uint32_t pr[kQ2Cap];                // m | owner << 16 | codes
-        uint16_t cpre[kQ2Cap + 1];          // contacts before survivor p
-        uint16_t cp[kC2Cap];                // contact -> survivor index
-        double cdist[kC2Cap], cdelta[kC2Cap], cs[kC2Cap];
-        uint16_t mi[32];
-        uint8_t chg[32];
-        uint8_t cnz[kC2Cap];
-    } W[kT2Warps];
+    uint32_t off[220];
+    float4 P[kM6Max + 1];                   // fp32 region-relative x, y, z (+ sentinel)
+    double X[kM6Max], Y[kM6Max], Z[kM6Max], Rr[kM6Max];
+    uint32_t F[kM6Max];
+    uint32_t kmi[kM6Max];                   // tile agent k -> staged index | region box << 9
+    uint8_t mbox[kM6Max];                   // staged index -> region box
+    Warp6 W[kT6Warps];
 };
 
-__device__ __forceinline__ unsigned long long pk2(float a, float b) {
-    unsigned long long r;
-    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
-    return r;
-}
-__device__ __forceinline__ void up2(unsigned long long v, float &a, float &b) {
-    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
-}
-// squared fp32 distances of (px,py,pz) to the staged pair (m, m+1): fl(fl(dz*dz + fl(dy*dy
-// + fl(dx*dx)))) per element with fma, exactly like the scalar prefilter of k_mech_tile
-__device__ __forceinline__ void dist2_pair(unsigned long long pxx, unsigned long long pyy,
-                                           unsigned long long pzz, float4 q, float2 qz,
-                                           float &d0, float &d1) {
-    unsigned long long ex, ey, ez, d;
-    const unsigned long long qx = pk2(q.x, q.y), qy = pk2(q.z, q.w), qzz = pk2(qz.x, qz.y);
-    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(ex) : "l"(pxx), "l"(qx));
-    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(ey) : "l"(pyy), "l"(qy));
-    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(ez) : "l"(pzz), "l"(qzz));
-    asm("mul.rn.f32x2 %0, %1, %1;" : "=l"(d) : "l"(ex));
-    asm("fma.rn.f32x2 %0, %1, %1, %2;" : "=l"(d) : "l"(ey), "l"(d));
-    asm("fma.rn.f32x2 %0, %1, %1, %2;" : "=l"(d) : "l"(ez), "l"(d));
-    up2(d, d0, d1);
+// Merges one batch's counters into the warp's shared accumulators (lane 0 writes).
+// `sides` selects which of the 7 extent values (lo x,y,z, hi x,y,z, max d) this batch
+// can change (uniform over the warp; see k_mech_tile6).
+template <bool kStats>
+__device__ __forceinline__ void merge_counts(const Counts &c, Warp6 &Wp, int sides, int lane) {
+    if (sides) {
+        const double v0[7] = {c.lo0, c.lo1, c.lo2, c.hi0, c.hi1, c.hi2, c.dmax};
+#pragma unroll
+        for (int q = 0; q < 7; ++q) {
+            if (!((sides >> q) & 1)) continue;
+            double v = v0[q];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const double t = __shfl_xor_sync(0xffffffffu, v, o);
+                v = q < 3 ? fmin(v, t) : fmax(v, t);
+            }
+            if (lane == 0) Wp.ext[q] = q < 3 ? fmin(Wp.ext[q], v) : fmax(Wp.ext[q], v);
+        }
+    }
+    if (kStats) {
+        const unsigned long long a = warp_sum_u64(c.cand), b = warp_sum_u64(c.nbr),
+                                 d = warp_sum_u64(c.cont), e = warp_sum_u64(c.stat),
+                                 f = warp_sum_u64(c.moved);
+        if (lane == 0) {
+            Wp.cnt[0] += a;
+            Wp.cnt[1] += b;
+            Wp.cnt[2] += d;
+            Wp.cnt[3] += e;
+            Wp.cnt[4] += f;
+        }
+    }
+    __syncwarp();
 }
 
+// Eq. 4.1/4.2 for one contact candidate: s = F_N / dist and its flags
+__device__ __forceinline__ void contact_force6(const MechArgs &A, const Tile6Smem &S, double D,
+                                               uint32_t e, unsigned stat_mask, double &s_,
+                                               uint8_t &fl) {
+    const int m = (int)(e & 511u), mo = (int)((e >> 9) & 511u);
+    s_ = 0.0;
+    fl = 0;
+    if (!((stat_mask >> ((e >> 18) & 31u)) & 1u)) {
+        const double dist = sqrt(D);
+        const double ri = S.Rr[mo], rj = S.Rr[m];
+        const double delta = (ri + rj) - dist;
+        if (delta > 0.0) {
+            const double rbar = (ri * rj) / (ri + rj);
+            const double Fn = A.k * delta - A.gamma * sqrt(rbar * delta);
+            s_ = Fn / dist;
+            fl = (uint8_t)(2u | (Fn != 0.0 ? 1u : 0u));
+        }
+    }
+}
+
+// One batch of <= 32 agents of the staged tile (lane = tile agent klo + lane).
 template <bool kStats>
-__global__ void __launch_bounds__(kT2Threads, 3) k_mech_tile2(MechArgs A, DevScalars *__restrict__ sc,
-                                                             int allow_prefilter) {
+__device__ __forceinline__ void tile6_batch(const MechArgs &A, const Tile6Smem &S, Warp6 &Wp,
+                                            int lane, uint32_t g0, int klo, int na, int M,
+                                            int sides) {
+    const unsigned lt_mask = (1u << lane) - 1u;
+    const float R2f = S.R2f, Lf = S.Lf;
+    const int k = klo + lane;
+    const uint32_t gk = g0 + (uint32_t)k;
+    int mi = M, nr = 0, walk = 0, ca = 0;
+    uint32_t fi = 0;
+    bool active = false, cand_static = false;
+    // an inactive lane walks only the sentinel run; its own point is at -1e30 so the
+    // squared fp32 distance overflows to +inf and never passes
+    float4 pi = make_float4(-kSentinel, -kSentinel, -kSentinel, 0.f);
+    if (lane < na) {
+        const uint32_t km = S.kmi[k];
+        mi = (int)(km & 511u);
+        const int lbi = (int)(km >> 9);
+        fi = S.F[mi];
+        active = !(fi & kGhost);
+        if (active) {
+            cand_static = A.detect_static && !(fi & kChanged) && ((fi >> BDM_FLAG_NNZ_SHIFT) & 3u) <= 1u;
+            pi = S.P[mi];
+            const int lx = lbi % 6, ly = (lbi / 6) % 6, lz = lbi / 36;
+            // squared gaps to the faces of the own box (fp32, conservative, see above)
+            const float glx = pi.x - (float)lx * Lf, ghx = (float)(lx + 1) * Lf - pi.x;
+            const float gly = pi.y - (float)ly * Lf, ghy = (float)(ly + 1) * Lf - pi.y;
+            const float glz = pi.z - (float)lz * Lf, ghz = (float)(lz + 1) * Lf - pi.z;
+            const float gx2l = glx * glx, gx2h = ghx * ghx;
+            const float gy2[3] = {gly * gly, 0.f, ghy * ghy};
+            const float gz2[3] = {glz * glz, 0.f, ghz * ghz};
+#pragma unroll
+            for (int r = 0; r < 9; ++r) {
+                const int dzi = r / 3, dyi = r % 3;
+                const int row = lbi - 43 + dzi * 36 + dyi * 6;  // box (lx-1, ly-1+dyi, lz-1+dzi)
+                if (kStats) ca += (int)(S.off[row + 3] - S.off[row]);
+                const float b2 = gz2[dzi] + gy2[dyi];
+                if (b2 <= R2f) {
+                    const int xs = (b2 + gx2l <= R2f) ? 0 : 1;
+                    const int xe = (b2 + gx2h <= R2f) ? 3 : 2;
+                    const uint32_t rs = S.off[row + xs], re = S.off[row + xe];
+                    if (re > rs) {
+                        Wp.u.a.run[nr][lane] = rs | (re << 16);
+                        ++nr;
+                        walk += (int)(re - rs);
+                    }
+                }
+            }
+        }
+    }
+    // sentinel run [M, 0xFFFF): after its last real run a lane walks on past M, its
+    // loads clamped to the sentinel agent P[M] (at 1e30, never passes), and never
+    // advances again
+    Wp.u.a.run[nr][lane] = (uint32_t)M | (0xFFFFu << 16);
+    Wp.chg[lane] = 0;
+    const int cmax = __reduce_max_sync(0xffffffffu, walk);
+    const bool any_cs = __any_sync(0xffffffffu, cand_static);
+    __syncwarp();
+    // ---- phase 1: flattened, branch-free walk over the trimmed runs
+    int cnt = 0;
+    {
+        uint16_t *lrow = &Wp.u.a.lst[0][lane];
+        const uint32_t *rrow = &Wp.u.a.run[0][lane];
+        uint32_t cur = rrow[0];
+        int m = (int)(cur & 0xFFFFu), e = (int)(cur >> 16);
+        const uint32_t *rp = rrow + 32;   // next run (row nr + 1 <= 10 is never consumed)
+        uint32_t nxt = *rp;
+#pragma unroll 2
+        for (int it = 0; it < cmax; ++it) {
+            const float4 q = S.P[min(m, M)];
+            const float ex = pi.x - q.x, ey = pi.y - q.y, ez = pi.z - q.z;
+            const bool pass = fmaf(ez, ez, fmaf(ey, ey, ex * ex)) <= R2f;
+            lrow[32 * cnt] = (uint16_t)m;
+            cnt = min(cnt + (pass ? 1 : 0), kK6Max);
+            ++m;
+            const bool adv = (m == e);
+            m = adv ? (int)(nxt & 0xFFFFu) : m;
+            e = adv ? (int)(nxt >> 16) : e;
+            rp += adv ? 32 : 0;
+            nxt = *rp;
+        }
+    }
+    // a full list (cnt == kK6Max) may have lost survivors: the batch takes the
+    // reference path (kK6Max - 1 survivors + self is far above the mean 7.6)
+    int cincl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, cincl, o);
+        if (lane >= o) cincl += y;
+    }
+    const int my_off = cincl - cnt;
+    const int total = __shfl_sync(0xffffffffu, cincl, 31);
+    Counts c;
+    bool done = false;
+    if (__any_sync(0xffffffffu, cnt >= kK6Max) || total > kQ6Cap) {
+        if (active) mech_agent_global(A, S.g, gk, c);
+        done = true;
+    }
+    if (!done) {
+        const uint32_t tag = ((uint32_t)mi << 9) | ((uint32_t)lane << 18);
+        for (int jj = 0; jj < cnt; ++jj) Wp.pr[my_off + jj] = (uint32_t)Wp.u.a.lst[jj][lane] | tag;
+        __syncwarp();
+        // ---- phase 2a: exact test, static flags, contact pre-test, compaction
+        const double R2 = S.g.R2;
+        int cbase = 0;
+        for (int p0 = 0; p0 < total; p0 += 32) {  // warp-uniform
+            const int p = p0 + lane;
+            bool cc = false;
+            double D = 0.0;
+            uint32_t e = 0;
+            if (p < total) {
+                e = Wp.pr[p];
+                const int m = (int)(e & 511u), mo = (int)((e >> 9) & 511u);
+                const double ex = S.X[mo] - S.X[m], ey = S.Y[mo] - S.Y[m], ez = S.Z[mo] - S.Z[m];
+                D = fma(ez, ez, fma(ey, ey, ex * ex));
+                if (D <= R2 && m != mo) {
+                    e |= kNbrBit;
+                    if (kStats) Wp.pr[p] = e;
+                    if (any_cs && (S.F[m] & kChanged)) Wp.chg[(e >> 18) & 31u] = 1;
+                    const double s2 = S.Rr[mo] + S.Rr[m];
+                    cc = D > 0.0 && D < (s2 * s2) * (1.0 + 0x1p-30);
+                }
+            }
+            const unsigned cb = __ballot_sync(0xffffffffu, cc);
+            const int cidx = cbase + __popc(cb & lt_mask);
+            if (p < total) Wp.cpre[p] = (uint16_t)cidx;
+            if (cc && cidx < kC6Cap) {
+                Wp.u.b.cq[cidx] = D;
+                Wp.u.b.ce[cidx] = e;
+            }
+            cbase += __popc(cb);
+        }
+        if (cbase > kC6Cap) {  // contact queue overflow: reference path for this batch
+            __syncwarp();
+            if (active) mech_agent_global(A, S.g, gk, c);
+            done = true;
+        }
+        if (!done) {
+            if (lane == 0) Wp.cpre[total] = (uint16_t)cbase;
+            __syncwarp();
+            const bool is_static = cand_static && !Wp.chg[lane];
+            const unsigned stat_mask = __ballot_sync(0xffffffffu, is_static);
+            // ---- phase 2b: Eq. 4.1/4.2 over the compacted contact candidates
+            for (int q = lane; q < cbase; q += 32) {
+                double s_;
+                uint8_t fl;
+                contact_force6(A, S, Wp.u.b.cq[q], Wp.u.b.ce[q], stat_mask, s_, fl);
+                Wp.u.b.cq[q] = s_;
+                Wp.u.b.cf[q] = fl;
+            }
+            __syncwarp();
+            // ---- phase 3: ordered accumulation of the own contacts
+            if (active) {
+                const double xi = S.X[mi], yi = S.Y[mi], zi = S.Z[mi];
+                double Fx = 0.0, Fy = 0.0, Fz = 0.0;
+                int nnz = 0;
+                uint32_t my_cont = 0;
+                const int q0 = Wp.cpre[my_off], q1 = Wp.cpre[my_off + cnt];
+                for (int q = q0; q < q1; ++q) {
+                    const uint32_t fl = Wp.u.b.cf[q];
+                    if (fl & 2u) {
+                        const int m = (int)(Wp.u.b.ce[q] & 511u);
+                        const double s_ = Wp.u.b.cq[q];
+                        Fx = fma(s_, xi - S.X[m], Fx);
+                        Fy = fma(s_, yi - S.Y[m], Fy);
+                        Fz = fma(s_, zi - S.Z[m], Fz);
+                        nnz += (int)(fl & 1u);
+                        ++my_cont;
+                    }
+                }
+                nnz = nnz < 2 ? nnz : 2;
+                if (!is_static) {
+                    if (kStats) {
+                        uint32_t my_nbr = 0;
+                        for (int jj = my_off; jj < my_off + cnt; ++jj)
+                            my_nbr += (Wp.pr[jj] & kNbrBit) ? 1u : 0u;
+                        c.cand += (uint32_t)(ca - 1);
+                        c.nbr += my_nbr;
+                        c.cont += my_cont;
+                    }
+                } else {
+                    nnz = (int)((fi >> BDM_FLAG_NNZ_SHIFT) & 3u);
+                }
+                finish_agent(A, gk, xi, yi, zi, Fx, Fy, Fz, is_static, nnz, c);
+            }
+        }
+    }
+    merge_counts<kStats>(c, Wp, sides, lane);
+}
+
+template <bool kStats, int kMinBlocks>
+__global__ void __launch_bounds__(kT6Threads, kMinBlocks) k_mech_tile6(MechArgs A, DevScalars *__restrict__ sc,
+                                                                      int allow_prefilter) {
     if (sc->overflow) return;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    Tile2Smem &S = *reinterpret_cast<Tile2Smem *>(smem_raw);
-    const GridView g = load_grid(sc);
+    Tile6Smem &S = *reinterpret_cast<Tile6Smem *>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-    Tile2Smem::Warp &Wp = S.W[w];
-    const long long ntiles = (long long)g.T0 * g.T1 * g.T2;
-    const float R2f = (float)(g.R2 * (1.0 + 0x1p-12));
-    const float Lf = (float)g.L;
-    const double amax = fmax(fmax(fmax(fabs(g.o0), fabs(g.o1)), fmax(fabs(g.o2), fabs(sc->hi[0]))),
-                             fmax(fabs(sc->hi[1]), fabs(sc->hi[2])));
-    const bool use_pf = allow_prefilter && amax < 0x1p30 * g.L;
-    const unsigned lt_mask = (1u << lane) - 1u;
-    Counts c;
-
-    for (long long t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        const int tx = (int)(t % g.T0), ty = (int)((t / g.T0) % g.T1);
-        const int tz = (int)(t / ((long long)g.T0 * g.T1));
-        const int bx0 = 4 * tx - 1, by0 = 4 * ty - 1, bz0 = 4 * tz - 1;
-        const uint32_t g0 = A.box_start[(uint32_t)t * 64u];
-        const uint32_t g1 = A.box_start[(uint32_t)t * 64u + 64u];
-        const int nc = (int)(g1 - g0);
-        if (nc == 0) continue;  // uniform across the CTA
-        if (!use_pf) {  // |coordinates| / L >= 2^30: reference formulation for the tile
-            for (int k = tid; k < nc; k += kT2Threads) mech_agent_global(A, g, g0 + k, c);
-            continue;
+    if (tid == 0) {
+        const GridView g = load_grid(sc);
+        S.g = g;
+        S.R2f = (float)(g.R2 * (1.0 + 0x1p-12));
+        S.Lf = (float)g.L;
+        const double amax = fmax(fmax(fmax(fabs(g.o0), fabs(g.o1)), fmax(fabs(g.o2), fabs(sc->hi[0]))),
+                                 fmax(fabs(sc->hi[1]), fabs(sc->hi[2])));
+        S.use_pf = allow_prefilter && amax < 0x1p30 * g.L;
+        // Fused extent (a1 of the next step).  Every displacement is at most max_disp
+        // (cap, P:7911-7912 reading R6), so an agent with x > lo + 2 max_disp ends right of
+        // the agent that held the minimum and cannot be the new minimum (likewise for
+        // the maximum); the diameters do not change in this step.  Only tiles holding
+        // boxes within 2 max_disp (+1 box for rounding) of the old extent reduce it.
+        const double md = A.max_disp;
+        S.edge_only = A.fuse && !sc->has_frame && md >= 0.0 && 2.0 * md < 0x1p20 * g.L;
+        if (S.edge_only) {
+            const double ov[3] = {g.o0, g.o1, g.o2};
+            for (int a = 0; a < 3; ++a) {
+                S.lo_box[a] = (int)floor(2.0 * md / g.L) + 1;
+                S.hi_box[a] = (int)floor((sc->hi[a] - 2.0 * md - ov[a]) / g.L) - 1;
+            }
+            if (blockIdx.x == 0) atomicMax(&sc->enc_dmax, enc_double(sc->dmax_prev));
         }
+    }
+    if (lane < 7) S.W[w].ext[lane] = lane < 3 ? INFINITY : -INFINITY;
+    if (lane < 5) S.W[w].cnt[lane] = 0ull;
+    __syncthreads();
+    const int ntiles = S.g.T0 * S.g.T1 * S.g.T2;  // < 2^26 (nslots < 2^32)
+
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const uint32_t g0 = A.box_start[(uint32_t)t * 64u];
+        const int nc = (int)(A.box_start[(uint32_t)t * 64u + 64u] - g0);
+        if (nc == 0) continue;  // uniform across the CTA
+        const int T0 = S.g.T0, T1 = S.g.T1;
+        const int tx = t % T0, ty = (t / T0) % T1, tz = t / (T0 * T1);
+        const int bx0 = 4 * tx - 1, by0 = 4 * ty - 1, bz0 = 4 * tz - 1;
         // ---- box table of the 6^3 region (out-of-grid boxes are empty)
-        for (int lb = tid; lb < 216; lb += kT2Threads) {
+        for (int lb = tid; lb < 216; lb += kT6Threads) {
             const int gx = bx0 + lb % 6, gy = by0 + (lb / 6) % 6, gz = bz0 + lb / 36;
-            uint32_t st = 0, cnt = 0;
-            if (gx >= 0 && gy >= 0 && gz >= 0 && gx < g.D0 && gy < g.D1 && gz < g.D2) {
-                const uint32_t key = box_key(gx, gy, gz, g.T0, g.T1);
+            uint32_t st = 0, cn = 0;
+            if (gx >= 0 && gy >= 0 && gz >= 0 && gx < S.g.D0 && gy < S.g.D1 && gz < S.g.D2) {
+                const uint32_t key = box_key(gx, gy, gz, T0, T1);
                 st = A.box_start[key];
-                cnt = A.box_start[key + 1] - st;
+                cn = A.box_start[key + 1] - st;
             }
             S.start[lb] = st;
-            S.off[lb] = cnt;
+            S.off[lb] = cn;
         }
         __syncthreads();
         if (w == 0) {  // exclusive scan of the 216 counts (7 per lane)
             uint32_t v[7], sum = 0;
 #pragma unroll
-            for (int k = 0; k < 7; ++k) {
-                const int lb = lane * 7 + k;
-                v[k] = lb < 216 ? S.off[lb] : 0u;
-                sum += v[k];
+            for (int q = 0; q < 7; ++q) {
+                const int lb = lane * 7 + q;
+                v[q] = lb < 216 ? S.off[lb] : 0u;
+                sum += v[q];
             }
             uint32_t inc = sum;
 #pragma unroll
@@ -686,280 +949,97 @@ __global__ void __launch_bounds__(kT2Threads, 3) k_mech_tile2(MechArgs A, DevSca
             }
             uint32_t run = inc - sum;
 #pragma unroll
-            for (int k = 0; k < 7; ++k) {
-                const int lb = lane * 7 + k;
+            for (int q = 0; q < 7; ++q) {
+                const int lb = lane * 7 + q;
                 if (lb <= 216) S.off[lb] = run;
-                run += v[k];
+                run += v[q];
             }
         }
         __syncthreads();
         const int M = (int)S.off[216];
-        if (M > kM2Max) {
-            for (int k = tid; k < nc; k += kT2Threads) mech_agent_global(A, g, g0 + k, c);
+        if (M > kM6Max || !S.use_pf) {
+            // over-full region or |coordinates| / L >= 2^30: reference formulation
+            for (int k0 = 32 * w; k0 < nc; k0 += kT6Threads) {
+                Counts c;
+                if (k0 + lane < nc) mech_agent_global(A, S.g, g0 + k0 + lane, c);
+                merge_counts<kStats>(c, S.W[w], A.fuse ? 0x7F : 0, lane);
+            }
             __syncthreads();
             continue;
         }
+        // ---- staged index -> box, tile agent -> staged index
+        for (int lb = tid; lb < 216; lb += kT6Threads) {
+            const uint32_t o = S.off[lb], n = S.off[lb + 1] - o;
+            const int lx = lb % 6, ly = (lb / 6) % 6, lz = lb / 36;
+            const bool inner = lx >= 1 && lx <= 4 && ly >= 1 && ly <= 4 && lz >= 1 && lz <= 4;
+            const uint32_t kb = S.start[lb] - g0;
+            for (uint32_t u = 0; u < n; ++u) {
+                S.mbox[o + u] = (uint8_t)lb;
+                if (inner) S.kmi[kb + u] = (o + u) | ((uint32_t)lb << 9);
+            }
+        }
+        __syncthreads();
         // ---- stage the region (row-major boxes, ascending id in a box)
-        const double X0 = g.o0 + (double)(bx0 + g.b0) * g.L, Y0 = g.o1 + (double)(by0 + g.b1) * g.L,
-                     Z0 = g.o2 + (double)(bz0 + g.b2) * g.L;
-        for (int lb = tid; lb < 216; lb += kT2Threads)
-            for (uint32_t m = S.off[lb]; m < S.off[lb + 1]; ++m) S.mbox[m] = (uint8_t)lb;
-        __syncthreads();
-        float *xy = reinterpret_cast<float *>(S.XY);
-        float *zz = reinterpret_cast<float *>(S.ZZ);
-        for (int m = tid; m < M; m += kT2Threads) {
-            const int lb = S.mbox[m];
-            const uint32_t gi = S.start[lb] + ((uint32_t)m - S.off[lb]);
-            const double x = A.sx[gi], y = A.sy[gi], z = A.sz[gi], d = A.sd[gi];
-            S.X[m] = x;
-            S.Y[m] = y;
-            S.Z[m] = z;
-            S.Rr[m] = d * 0.5;
-            S.F[m] = A.sflags[gi];
-            const float xr = (float)(x - X0), yr = (float)(y - Y0), zr = (float)(z - Z0);
-            xy[4 * m + 0] = xr;
-            xy[4 * m + 2] = yr;
-            zz[2 * m + 0] = zr;
-            if (m > 0) {
-                xy[4 * (m - 1) + 1] = xr;
-                xy[4 * (m - 1) + 3] = yr;
-                zz[2 * (m - 1) + 1] = zr;
+        {
+            const double L = S.g.L;
+            const double X0 = S.g.o0 + (double)(bx0 + S.g.b0) * L, Y0 = S.g.o1 + (double)(by0 + S.g.b1) * L,
+                         Z0 = S.g.o2 + (double)(bz0 + S.g.b2) * L;
+            for (int m = tid; m < M; m += kT6Threads) {
+                const int lb = S.mbox[m];
+                const uint32_t gi = S.start[lb] + ((uint32_t)m - S.off[lb]);
+                const double x = A.sx[gi], y = A.sy[gi], z = A.sz[gi], d = A.sd[gi];
+                S.X[m] = x;
+                S.Y[m] = y;
+                S.Z[m] = z;
+                S.Rr[m] = d * 0.5;
+                S.F[m] = A.sflags[gi];
+                S.P[m] = make_float4((float)(x - X0), (float)(y - Y0), (float)(z - Z0), 0.f);
             }
         }
-        if (tid == 0) {  // sentinel pair at M (and the upper half of M - 1)
-            S.XY[M] = make_float4(kSentinel, kSentinel, kSentinel, kSentinel);
-            S.ZZ[M] = make_float2(kSentinel, kSentinel);
-            if (M > 0) {
-                xy[4 * (M - 1) + 1] = kSentinel;
-                xy[4 * (M - 1) + 3] = kSentinel;
-                zz[2 * (M - 1) + 1] = kSentinel;
-            }
-        }
+        if (tid == 0) S.P[M] = make_float4(kSentinel, kSentinel, kSentinel, 0.f);
         __syncthreads();
-
-        const int nw = min(kT2Warps, (nc + 31) >> 5);
-        const int share = (nc + nw - 1) / nw;
-        const int wlo = w < nw ? min(nc, w * share) : nc;
-        const int whi = w < nw ? min(nc, wlo + share) : nc;
-        for (int base = wlo; base < whi; base += 32) {  // warp-uniform
-            const int na = min(32, whi - base);
-            const int k = base + lane;
-            const bool active = lane < na && !(A.sflags[g0 + (uint32_t)k] & kGhost);
-            int mi = M, ca = 0, nr = 0, npair = 0;
-            uint32_t fi = 0;
-            double xi = 0.0, yi = 0.0, zi = 0.0;
-            bool cand_static = false;
-            float pxr = 0.f, pyr = 0.f, pzr = 0.f;
-            if (active) {
-                const uint32_t gk = g0 + (uint32_t)k;
-                xi = A.sx[gk];
-                yi = A.sy[gk];
-                zi = A.sz[gk];
-                const int lx = (int)floor((xi - g.o0) / g.L) - g.b0 - bx0;
-                const int ly = (int)floor((yi - g.o1) / g.L) - g.b1 - by0;
-                const int lz = (int)floor((zi - g.o2) / g.L) - g.b2 - bz0;
-                const int lbi = (lz * 6 + ly) * 6 + lx;
-                mi = (int)(S.off[lbi] + (gk - S.start[lbi]));
-                fi = S.F[mi];
-                cand_static = A.detect_static && !(fi & kChanged) &&
-                              ((fi >> BDM_FLAG_NNZ_SHIFT) & 3u) <= 1u;
-                const float4 q = S.XY[mi];
-                pxr = q.x;
-                pyr = q.z;
-                pzr = S.ZZ[mi].x;
-                // (y, z) gaps to the faces of the own box, for the corner-run test
-                const float gyl = pyr - (float)ly * Lf, gyh = (float)(ly + 1) * Lf - pyr;
-                const float gzl = pzr - (float)lz * Lf, gzh = (float)(lz + 1) * Lf - pzr;
+        int sides = 0;
+        if (S.edge_only) {
+            const int tc[3] = {tx, ty, tz};
 #pragma unroll
-                for (int r = 0; r < 9; ++r) {
-                    const int dzi = r / 3, dyi = r % 3;
-                    const int lb0 = lbi - 43 + dzi * 36 + dyi * 6;
-                    const uint32_t rs = S.off[lb0], re = S.off[lb0 + 3];
-                    ca += (int)(re - rs);
-                    bool walk = re > rs;
-                    if (dzi != 1 && dyi != 1) {
-                        const float gy = dyi == 0 ? gyl : gyh, gz = dzi == 0 ? gzl : gzh;
-                        walk = walk && fmaf(gz, gz, gy * gy) <= R2f;
-                    }
-                    if (walk) {
-                        Wp.run[nr][lane] = rs | (re << 16);
-                        ++nr;
-                        npair += (int)((re - rs + 1) >> 1);
-                    }
-                }
-                Wp.mi[lane] = (uint16_t)mi;
-                Wp.chg[lane] = 0;
+            for (int a = 0; a < 3; ++a) {
+                sides |= (4 * tc[a] <= S.lo_box[a]) ? (1 << a) : 0;
+                sides |= (4 * tc[a] + 3 >= S.hi_box[a]) ? (8 << a) : 0;
             }
-            const int cmax = __reduce_max_sync(0xffffffffu, npair);
-            __syncwarp();
-            // ---- phase 1: packed pair walk over the runs
-            int cnt = 0;
-            {
-                const unsigned long long pxx = pk2(pxr, pxr), pyy = pk2(pyr, pyr), pzz = pk2(pzr, pzr);
-                const uint32_t v0 = nr > 0 ? Wp.run[0][lane] : 0u;
-                int m = nr > 0 ? (int)(v0 & 0xFFFFu) : M, e = nr > 0 ? (int)(v0 >> 16) : M + 2;
-                int j = 1;
-                uint32_t nxt = Wp.run[1][lane];
-#pragma unroll 2
-                for (int it = 0; it < cmax; ++it) {
-                    const float4 q = S.XY[m];
-                    const float2 qz = S.ZZ[m];
-                    float d0, d1;
-                    dist2_pair(pxx, pyy, pzz, q, qz, d0, d1);
-                    const bool p0 = d0 <= R2f;
-                    const bool p1 = (d1 <= R2f) && (m + 1 < e);
-                    Wp.lst[cnt < kK2Max ? cnt : kK2Max][lane] = (uint16_t)m;
-                    cnt += p0 ? 1 : 0;
-                    Wp.lst[cnt < kK2Max ? cnt : kK2Max][lane] = (uint16_t)(m + 1);
-                    cnt += p1 ? 1 : 0;
-                    m += 2;
-                    const bool at_end = m >= e, more = j < nr;
-                    const int mn = more ? (int)(nxt & 0xFFFFu) : M;
-                    const int en = more ? (int)(nxt >> 16) : M + 2;
-                    m = at_end ? mn : m;
-                    e = at_end ? en : e;
-                    j += at_end ? 1 : 0;
-                    nxt = Wp.run[j < 9 ? j : 8][lane];
-                }
-            }
-            // ---- concatenate the lane lists (lane order = agent-major canonical order)
-            int cincl = cnt;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int y = __shfl_up_sync(0xffffffffu, cincl, o);
-                if (lane >= o) cincl += y;
-            }
-            const int my_off = cincl - cnt;
-            const int total = __shfl_sync(0xffffffffu, cincl, 31);
-            if (__any_sync(0xffffffffu, cnt > kK2Max) || total > kQ2Cap) {
-                if (active) mech_agent_global(A, g, g0 + k, c);
-                __syncwarp();
-                continue;
-            }
-            for (int jj = 0; jj < cnt; ++jj)
-                Wp.pr[my_off + jj] = (uint32_t)Wp.lst[jj][lane] | ((uint32_t)lane << 16);
-            __syncwarp();
-            const bool any_cs = __any_sync(0xffffffffu, cand_static);
-            if (any_cs) {  // static pull test: exact test + neighbour flags
-                for (int p = lane; p < total; p += 32) {
-                    const uint32_t e = Wp.pr[p];
-                    const int m = (int)(e & 0xFFFFu), owner = (int)((e >> 16) & 0xFFu);
-                    const int mo = Wp.mi[owner];
-                    if (m == mo) continue;
-                    const double ex = S.X[mo] - S.X[m], ey = S.Y[mo] - S.Y[m], ez = S.Z[mo] - S.Z[m];
-                    const double D = fma(ez, ez, fma(ey, ey, ex * ex));
-                    if (D <= g.R2 && (S.F[m] & kChanged)) Wp.chg[owner] = 1;
-                }
-                __syncwarp();
-            }
-            const bool is_static = active && cand_static && !Wp.chg[lane];
-            const unsigned stat_mask = __ballot_sync(0xffffffffu, is_static);
-            // ---- phase 2a: exact test, dist, delta; contacts compacted in order
-            int cbase = 0;
-            for (int p0 = 0; p0 < total; p0 += 32) {  // warp-uniform
-                const int p = p0 + lane;
-                bool contact = false;
-                double dist = 0.0, delta = 0.0;
-                uint32_t e = 0;
-                if (p < total) {
-                    e = Wp.pr[p];
-                    const int m = (int)(e & 0xFFFFu), owner = (int)((e >> 16) & 0xFFu);
-                    const int mo = Wp.mi[owner];
-                    const double ex = S.X[mo] - S.X[m], ey = S.Y[mo] - S.Y[m], ez = S.Z[mo] - S.Z[m];
-                    const double D = fma(ez, ez, fma(ey, ey, ex * ex));
-                    if (D <= g.R2 && m != mo) {
-                        e |= kCodeNbr;
-                        if (!((stat_mask >> owner) & 1u)) {
-                            dist = sqrt(D);
-                            delta = (S.Rr[mo] + S.Rr[m]) - dist;
-                            contact = delta > 0.0 && dist > 0.0;
-                        }
-                    }
-                }
-                const unsigned cb = __ballot_sync(0xffffffffu, contact);
-                const int cidx = cbase + __popc(cb & lt_mask);
-                if (p < total) {
-                    Wp.cpre[p] = (uint16_t)cidx;
-                    Wp.pr[p] = e | (contact ? kCodeContact : 0u);
-                    if (contact && cidx < kC2Cap) {
-                        Wp.cp[cidx] = (uint16_t)p;
-                        Wp.cdist[cidx] = dist;
-                        Wp.cdelta[cidx] = delta;
-                    }
-                }
-                cbase += __popc(cb);
-            }
-            if (cbase > kC2Cap) {  // contact queue overflow: reference path for this batch
-                __syncwarp();
-                if (active) mech_agent_global(A, g, g0 + k, c);
-                __syncwarp();
-                continue;
-            }
-            if (lane == 0) Wp.cpre[total] = (uint16_t)cbase;
-            __syncwarp();
-            // ---- phase 2b: Eq. 4.1/4.2 over the compacted contacts
-            for (int q = lane; q < cbase; q += 32) {
-                const uint32_t e = Wp.pr[Wp.cp[q]];
-                const int m = (int)(e & 0xFFFFu), owner = (int)((e >> 16) & 0xFFu);
-                const int mo = Wp.mi[owner];
-                const double ri = S.Rr[mo], rj = S.Rr[m];
-                const double delta = Wp.cdelta[q], dist = Wp.cdist[q];
-                const double rbar = (ri * rj) / (ri + rj);
-                const double Fn = A.k * delta - A.gamma * sqrt(rbar * delta);
-                Wp.cs[q] = Fn / dist;
-                Wp.cnz[q] = Fn != 0.0 ? 1 : 0;
-            }
-            __syncwarp();
-            // ---- phase 3: ordered accumulation of the own contacts
-            if (active) {
-                double Fx = 0.0, Fy = 0.0, Fz = 0.0;
-                int nnz = 0;
-                const int q0 = Wp.cpre[my_off], q1 = Wp.cpre[my_off + cnt];
-                for (int q = q0; q < q1; ++q) {
-                    const int m = (int)(Wp.pr[Wp.cp[q]] & 0xFFFFu);
-                    const double s_ = Wp.cs[q];
-                    const double ex = xi - S.X[m], ey = yi - S.Y[m], ez = zi - S.Z[m];
-                    Fx = fma(s_, ex, Fx);
-                    Fy = fma(s_, ey, Fy);
-                    Fz = fma(s_, ez, Fz);
-                    nnz += Wp.cnz[q];
-                }
-                nnz = nnz < 2 ? nnz : 2;
-                if (!is_static) {
-                    if (kStats) {
-                        uint32_t my_nbr = 0;
-                        for (int jj = my_off; jj < my_off + cnt; ++jj)
-                            my_nbr += (Wp.pr[jj] & kCodeNbr) ? 1u : 0u;
-                        c.cand += (uint32_t)(ca - 1);
-                        c.nbr += my_nbr;
-                        c.cont += (uint32_t)(q1 - q0);
-                    }
-                } else {
-                    nnz = (int)((fi >> BDM_FLAG_NNZ_SHIFT) & 3u);
-                }
-                finish_agent(A, g0 + k, xi, yi, zi, Fx, Fy, Fz, is_static, nnz, c);
-            }
-            __syncwarp();
+        } else if (A.fuse) {
+            sides = 0x7F;
         }
-        __syncthreads();
+        const int B = max(min(kT6Warps, nc), (nc + 31) >> 5);
+        for (int bb = w; bb < B; bb += kT6Warps) {  // warp-uniform
+            const int klo = (bb * nc) / B, khi = ((bb + 1) * nc) / B;
+            tile6_batch<kStats>(A, S, S.W[w], lane, g0, klo, khi - klo, M, sides);
+        }
+        __syncthreads();  // before the next tile overwrites the staged region
     }
-    flush_counts<kStats>(c, sc, A.fuse);
+    // per-warp accumulators -> device scalars
+    const Warp6 &Wp = S.W[w];
+    if (A.fuse && lane == 0) {
+        for (int q = 0; q < 3; ++q) atomicMin(&sc->enc_lo[q], enc_double(Wp.ext[q]));
+        for (int q = 0; q < 3; ++q) atomicMax(&sc->enc_hi[q], enc_double(Wp.ext[3 + q]));
+        atomicMax(&sc->enc_dmax, enc_double(Wp.ext[6]));
+    }
+    if (kStats && lane < 5) atomicAdd(&sc->stats[lane], Wp.cnt[lane]);
 }
 
-template <bool kStats>
-static bdm_status launch_tile2(Ctx *c, const MechArgs &A, cudaStream_t st) {
+template <bool kStats, int kMinBlocks>
+static bdm_status launch_tile6(Ctx *c, const MechArgs &A, cudaStream_t st) {
     static bool attr_set = false;
     static int per_sm = 0;
-    const int smem = (int)sizeof(Tile2Smem);
+    const int smem = (int)sizeof(Tile6Smem);
     if (!attr_set) {
-        BDM_CUDA_TRY(cudaFuncSetAttribute(k_mech_tile2<kStats>,
+        BDM_CUDA_TRY(cudaFuncSetAttribute(k_mech_tile6<kStats, kMinBlocks>,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        BDM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mech_tile2<kStats>,
-                                                                   kT2Threads, smem));
+        BDM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+            &per_sm, k_mech_tile6<kStats, kMinBlocks>, kT6Threads, smem));
         if (per_sm < 1) per_sm = 1;
         attr_set = true;
     }
-    k_mech_tile2<kStats><<<(unsigned)(c->sm_count * per_sm), kT2Threads, smem, st>>>(
+    k_mech_tile6<kStats, kMinBlocks><<<(unsigned)(c->sm_count * per_sm), kT6Threads, smem, st>>>(
         A, c->sc, c->prefilter);
     return BDM_OK;
 }
@@ -986,7 +1066,7 @@ bdm_status launch_mech(Ctx *c, bdm_agents *a, const bdm_params *p, cudaStream_t 
     MechArgs A;
     A.n = a->n;
     A.sx = c->sx; A.sy = c->sy; A.sz = c->sz; A.sd = c->sd;
-    A.sid = c->sidf; A.sflags = c->sflags; A.box_start = c->box_start;
+    A.sid = c->sidf; A.skey = c->skey; A.sflags = c->sflags; A.box_start = c->box_start;
     A.ox = a->x; A.oy = a->y; A.oz = a->z; A.od = a->diameter; A.oid = a->id; A.oflags = a->flags;
     A.svol = a->volume ? c->svol : nullptr;
     A.lrank = c->grid_ng > 0 ? c->lrank : nullptr;
@@ -1000,8 +1080,12 @@ bdm_status launch_mech(Ctx *c, bdm_agents *a, const bdm_params *p, cudaStream_t 
     if (p->collect_stats)
         BDM_CUDA_TRY(cudaMemsetAsync(c->sc->stats, 0, sizeof(c->sc->stats), st));
     if (c->mech_kernel == 0) {
-        const bdm_status s = p->collect_stats ? launch_tile2<true>(c, A, st)
-                                              : launch_tile2<false>(c, A, st);
+        const bdm_status s = p->collect_stats ? launch_tile6<true, 5>(c, A, st)
+                                              : launch_tile6<false, 5>(c, A, st);
+        if (s != BDM_OK) return s;
+    } else if (c->mech_kernel == 3) {  // same kernel at 4 CTAs/SM (128 registers)
+        const bdm_status s = p->collect_stats ? launch_tile6<true, 4>(c, A, st)
+                                              : launch_tile6<false, 4>(c, A, st);
         if (s != BDM_OK) return s;
     } else if (c->mech_kernel == 2) {
         const bdm_status s = p->collect_stats ? launch_tile<true>(c, A, st)

@@ -16,7 +16,7 @@ pytestmark = pytest.mark.gpu
 REL_TOL = 1e-9  # north_star tolerance for fp64 positions
 
 
-@pytest.fixture(scope="module", params=[0, 1], ids=["tile", "reference"])
+@pytest.fixture(scope="module", params=[0, 1, 2, 3], ids=["tile", "reference", "tile_v1", "tile_4cta"])
 def eng(request):
     """Both mechanics kernels: the tile kernel (default) and the per-agent reference."""
     import torch
@@ -25,7 +25,7 @@ def eng(request):
     from paper_2503_10796_b200 import Engine
     e = Engine(0, 1 << 16)
     e.set_option("mech_kernel", request.param)
-    e.set_option("fuse_reduce", 1 if request.param == 0 else 0)  # tile kernel: fused a1
+    e.set_option("fuse_reduce", 0 if request.param == 1 else 1)  # tile kernels: fused a1
     yield e
     e.close()
 
