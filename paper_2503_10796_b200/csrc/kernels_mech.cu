@@ -627,7 +627,8 @@ struct Tile6Smem {
     float4 P[kM6Max + 1];                   // fp32 region-relative x, y, z (+ sentinel)
     double X[kM6Max], Y[kM6Max], Z[kM6Max], Rr[kM6Max];
     uint32_t F[kM6Max];
-    uint32_t kmi[kM6Max];                   // tile agent k -> staged index | region box << 9
+    uint16_t kmi[kM6Max];                   // tile agent k -> staged index
+    uint16_t lbxyz[216];                    // region box -> x | y << 3 | z << 6 | inner << 9
     uint8_t mbox[kM6Max];                   // staged index -> region box
     Warp6 W[kT6Warps];
 };
@@ -702,15 +703,15 @@ __device__ __forceinline__ void tile6_batch(const MechArgs &A, const Tile6Smem &
     // squared fp32 distance overflows to +inf and never passes
     float4 pi = make_float4(-kSentinel, -kSentinel, -kSentinel, 0.f);
     if (lane < na) {
-        const uint32_t km = S.kmi[k];
-        mi = (int)(km & 511u);
-        const int lbi = (int)(km >> 9);
+        mi = (int)S.kmi[k];
+        const int lbi = (int)S.mbox[mi];
         fi = S.F[mi];
         active = !(fi & kGhost);
         if (active) {
             cand_static = A.detect_static && !(fi & kChanged) && ((fi >> BDM_FLAG_NNZ_SHIFT) & 3u) <= 1u;
             pi = S.P[mi];
-            const int lx = lbi % 6, ly = (lbi / 6) % 6, lz = lbi / 36;
+            const uint32_t v = S.lbxyz[lbi];
+            const int lx = (int)(v & 7u), ly = (int)((v >> 3) & 7u), lz = (int)((v >> 6) & 7u);
             // squared gaps to the faces of the own box (fp32, conservative, see above)
             const float glx = pi.x - (float)lx * Lf, ghx = (float)(lx + 1) * Lf - pi.x;
             const float gly = pi.y - (float)ly * Lf, ghy = (float)(ly + 1) * Lf - pi.y;
@@ -728,8 +729,8 @@ __device__ __forceinline__ void tile6_batch(const MechArgs &A, const Tile6Smem &
                     const int xs = (b2 + gx2l <= R2f) ? 0 : 1;
                     const int xe = (b2 + gx2h <= R2f) ? 3 : 2;
                     const uint32_t rs = S.off[row + xs], re = S.off[row + xe];
-                    if (re > rs) {
-                        Wp.u.a.run[nr][lane] = rs | (re << 16);
+                    if (re > rs) {  // stored as byte offsets into P (16 B per agent)
+                        Wp.u.a.run[nr][lane] = (rs << 4) | (re << 20);
                         ++nr;
                         walk += (int)(re - rs);
                     }
@@ -737,37 +738,42 @@ __device__ __forceinline__ void tile6_batch(const MechArgs &A, const Tile6Smem &
             }
         }
     }
-    // sentinel run [M, 0xFFFF): after its last real run a lane walks on past M, its
-    // loads clamped to the sentinel agent P[M] (at 1e30, never passes), and never
-    // advances again
-    Wp.u.a.run[nr][lane] = (uint32_t)M | (0xFFFFu << 16);
+    // sentinel run [16 M, 0xFFFF) (byte offsets into P): after its last real run a lane
+    // walks on past M, its loads clamped to the sentinel agent P[M] (at 1e30, never
+    // passes), and never advances again (0xFFFF is not a multiple of 16)
+    Wp.u.a.run[nr][lane] = ((uint32_t)M << 4) | (0xFFFFu << 16);
     Wp.chg[lane] = 0;
     const int cmax = __reduce_max_sync(0xffffffffu, walk);
     const bool any_cs = __any_sync(0xffffffffu, cand_static);
     __syncwarp();
-    // ---- phase 1: flattened, branch-free walk over the trimmed runs
+    // ---- phase 1: flattened, branch-free walk over the trimmed runs; the walk variable
+    // is the byte offset of the candidate in P
     int cnt = 0;
     {
-        uint16_t *lrow = &Wp.u.a.lst[0][lane];
-        const uint32_t *rrow = &Wp.u.a.run[0][lane];
+        const char *pb = reinterpret_cast<const char *>(&S.P[0]);
+        const uint32_t mlast = (uint32_t)M << 4;
+        uint16_t *const lrow = &Wp.u.a.lst[0][lane];
+        const uint32_t *const rrow = &Wp.u.a.run[0][lane];
         uint32_t cur = rrow[0];
-        int m = (int)(cur & 0xFFFFu), e = (int)(cur >> 16);
-        const uint32_t *rp = rrow + 32;   // next run (row nr + 1 <= 10 is never consumed)
-        uint32_t nxt = *rp;
+        uint32_t mo = cur & 0xFFFFu, eo = cur >> 16;
+        int j = 32;  // next run (row nr + 1 <= 10 is never consumed)
+        uint32_t nxt = rrow[j];
 #pragma unroll 2
         for (int it = 0; it < cmax; ++it) {
-            const float4 q = S.P[min(m, M)];
+            const float4 q = *reinterpret_cast<const float4 *>(pb + min(mo, mlast));
             const float ex = pi.x - q.x, ey = pi.y - q.y, ez = pi.z - q.z;
             const bool pass = fmaf(ez, ez, fmaf(ey, ey, ex * ex)) <= R2f;
-            lrow[32 * cnt] = (uint16_t)m;
-            cnt = min(cnt + (pass ? 1 : 0), kK6Max);
-            ++m;
-            const bool adv = (m == e);
-            m = adv ? (int)(nxt & 0xFFFFu) : m;
-            e = adv ? (int)(nxt >> 16) : e;
-            rp += adv ? 32 : 0;
-            nxt = *rp;
+            lrow[cnt] = (uint16_t)mo;
+            cnt = min(cnt + (pass ? 32 : 0), 32 * kK6Max);
+            mo += 16;
+            if (mo == eo) {
+                mo = nxt & 0xFFFFu;
+                eo = nxt >> 16;
+                j += 32;
+            }
+            nxt = rrow[j];
         }
+        cnt >>= 5;
     }
     // a full list (cnt == kK6Max) may have lost survivors: the batch takes the
     // reference path (kK6Max - 1 survivors + self is far above the mean 7.6)
@@ -787,7 +793,7 @@ __device__ __forceinline__ void tile6_batch(const MechArgs &A, const Tile6Smem &
     }
     if (!done) {
         const uint32_t tag = ((uint32_t)mi << 9) | ((uint32_t)lane << 18);
-        for (int jj = 0; jj < cnt; ++jj) Wp.pr[my_off + jj] = (uint32_t)Wp.u.a.lst[jj][lane] | tag;
+        for (int jj = 0; jj < cnt; ++jj) Wp.pr[my_off + jj] = ((uint32_t)Wp.u.a.lst[jj][lane] >> 4) | tag;
         __syncwarp();
         // ---- phase 2a: exact test, static flags, contact pre-test, compaction
         const double R2 = S.g.R2;
@@ -908,21 +914,38 @@ __global__ void __launch_bounds__(kT6Threads, kMinBlocks) k_mech_tile6(MechArgs 
             if (blockIdx.x == 0) atomicMax(&sc->enc_dmax, enc_double(sc->dmax_prev));
         }
     }
+    for (int lb = tid; lb < 216; lb += kT6Threads) {
+        const uint32_t lx = lb % 6, ly = (lb / 6) % 6, lz = lb / 36;
+        const uint32_t inner = lx >= 1 && lx <= 4 && ly >= 1 && ly <= 4 && lz >= 1 && lz <= 4;
+        S.lbxyz[lb] = (uint16_t)(lx | (ly << 3) | (lz << 6) | (inner << 9));
+    }
     if (lane < 7) S.W[w].ext[lane] = lane < 3 ? INFINITY : -INFINITY;
     if (lane < 5) S.W[w].cnt[lane] = 0ull;
     __syncthreads();
-    const int ntiles = S.g.T0 * S.g.T1 * S.g.T2;  // < 2^26 (nslots < 2^32)
+    const int T0 = S.g.T0, T1 = S.g.T1;
+    const int ntiles = T0 * T1 * S.g.T2;  // < 2^26 (nslots < 2^32)
+    // tile coordinates advance incrementally by gridDim.x (no divisions per tile)
+    const int gsx = (int)gridDim.x % T0, gsy = ((int)gridDim.x / T0) % T1,
+              gsz = (int)gridDim.x / (T0 * T1);
+    int tx = (int)blockIdx.x % T0, ty = ((int)blockIdx.x / T0) % T1, tz = (int)blockIdx.x / (T0 * T1);
 
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        if (t != (int)blockIdx.x) {
+            tx += gsx;
+            ty += gsy;
+            tz += gsz;
+            if (tx >= T0) { tx -= T0; ++ty; }
+            if (ty >= T1) { ty -= T1; ++tz; }
+        }
         const uint32_t g0 = A.box_start[(uint32_t)t * 64u];
         const int nc = (int)(A.box_start[(uint32_t)t * 64u + 64u] - g0);
         if (nc == 0) continue;  // uniform across the CTA
-        const int T0 = S.g.T0, T1 = S.g.T1;
-        const int tx = t % T0, ty = (t / T0) % T1, tz = t / (T0 * T1);
         const int bx0 = 4 * tx - 1, by0 = 4 * ty - 1, bz0 = 4 * tz - 1;
         // ---- box table of the 6^3 region (out-of-grid boxes are empty)
         for (int lb = tid; lb < 216; lb += kT6Threads) {
-            const int gx = bx0 + lb % 6, gy = by0 + (lb / 6) % 6, gz = bz0 + lb / 36;
+            const uint32_t v = S.lbxyz[lb];
+            const int gx = bx0 + (int)(v & 7u), gy = by0 + (int)((v >> 3) & 7u),
+                      gz = bz0 + (int)((v >> 6) & 7u);
             uint32_t st = 0, cn = 0;
             if (gx >= 0 && gy >= 0 && gz >= 0 && gx < S.g.D0 && gy < S.g.D1 && gz < S.g.D2) {
                 const uint32_t key = box_key(gx, gy, gz, T0, T1);
@@ -970,12 +993,11 @@ __global__ void __launch_bounds__(kT6Threads, kMinBlocks) k_mech_tile6(MechArgs 
         // ---- staged index -> box, tile agent -> staged index
         for (int lb = tid; lb < 216; lb += kT6Threads) {
             const uint32_t o = S.off[lb], n = S.off[lb + 1] - o;
-            const int lx = lb % 6, ly = (lb / 6) % 6, lz = lb / 36;
-            const bool inner = lx >= 1 && lx <= 4 && ly >= 1 && ly <= 4 && lz >= 1 && lz <= 4;
+            const bool inner = (S.lbxyz[lb] >> 9) != 0u;
             const uint32_t kb = S.start[lb] - g0;
             for (uint32_t u = 0; u < n; ++u) {
                 S.mbox[o + u] = (uint8_t)lb;
-                if (inner) S.kmi[kb + u] = (o + u) | ((uint32_t)lb << 9);
+                if (inner) S.kmi[kb + u] = (uint16_t)(o + u);
             }
         }
         __syncthreads();
@@ -1011,7 +1033,10 @@ __global__ void __launch_bounds__(kT6Threads, kMinBlocks) k_mech_tile6(MechArgs 
         }
         const int B = max(min(kT6Warps, nc), (nc + 31) >> 5);
         for (int bb = w; bb < B; bb += kT6Warps) {  // warp-uniform
-            const int klo = (bb * nc) / B, khi = ((bb + 1) * nc) / B;
+            // floor(bb nc / B): B <= 14, so the quotient is >= 1/14 from the next integer
+            // and the fp32 quotient (bb nc < 2^24) floors exactly
+            const int klo = (int)__fdividef((float)(bb * nc), (float)B);
+            const int khi = (int)__fdividef((float)((bb + 1) * nc), (float)B);
             tile6_batch<kStats>(A, S, S.W[w], lane, g0, klo, khi - klo, M, sides);
         }
         __syncthreads();  // before the next tile overwrites the staged region
