@@ -617,14 +617,27 @@ struct Warp6 {
     unsigned long long cnt[5];              // cand, nbr, cont, static, moved
     uint8_t chg[32];                        // agent saw a changed neighbour (a5)
 };
-struct Tile6Smem {
+// fp32 region-relative copy of the staged agents for the candidate test: one float4 per
+// agent, or (kPair) the packed pair layout (x_m, x_m+1, y_m, y_m+1), (z_m, z_m+1) that the
+// f32x2 walk loads with one LDS.128 + one LDS.64 per two candidates
+template <bool kPair>
+struct Fp32Stage {
+    float4 P[kM6Max + 1];                   // x, y, z (+ sentinel at M)
+};
+template <>
+struct Fp32Stage<true> {
+    float4 XY[kM6Max + 2];
+    float2 ZZ[kM6Max + 2];
+};
+template <bool kPair>
+struct Tile6SmemT {
     GridView g;
     float R2f, Lf;
     int use_pf, edge_only;                  // edge_only: fused extent from boundary tiles only
     int lo_box[3], hi_box[3];               // boxes that can hold a new extremum (see below)
     uint32_t start[216];
     uint32_t off[220];
-    float4 P[kM6Max + 1];                   // fp32 region-relative x, y, z (+ sentinel)
+    Fp32Stage<kPair> f;
     double X[kM6Max], Y[kM6Max], Z[kM6Max], Rr[kM6Max];
     uint32_t F[kM6Max];
     uint16_t kmi[kM6Max];                   // tile agent k -> staged index
@@ -632,6 +645,28 @@ struct Tile6Smem {
     uint8_t mbox[kM6Max];                   // staged index -> region box
     Warp6 W[kT6Warps];
 };
+using Tile6Smem = Tile6SmemT<false>;
+
+__device__ __forceinline__ unsigned long long pk2(float a, float b) {
+    unsigned long long r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+// squared fp32 distances of (px,py,pz) to the staged pair (m, m+1), per element exactly
+// the scalar test's fl(fma(dz,dz, fma(dy,dy, dx*dx))) (packed FADD2/FMUL2/FFMA2)
+__device__ __forceinline__ void dist2_pair(unsigned long long pxx, unsigned long long pyy,
+                                           unsigned long long pzz, float4 q, float2 qz,
+                                           float &d0, float &d1) {
+    unsigned long long ex, ey, ez, d;
+    const unsigned long long qx = pk2(q.x, q.y), qy = pk2(q.z, q.w), qzz = pk2(qz.x, qz.y);
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(ex) : "l"(pxx), "l"(qx));
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(ey) : "l"(pyy), "l"(qy));
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(ez) : "l"(pzz), "l"(qzz));
+    asm("mul.rn.f32x2 %0, %1, %1;" : "=l"(d) : "l"(ex));
+    asm("fma.rn.f32x2 %0, %1, %1, %2;" : "=l"(d) : "l"(ey), "l"(d));
+    asm("fma.rn.f32x2 %0, %1, %1, %2;" : "=l"(d) : "l"(ez), "l"(d));
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(d0), "=f"(d1) : "l"(d));
+}
 
 // Merges one batch's counters into the warp's shared accumulators (lane 0 writes).
 // `sides` selects which of the 7 extent values (lo x,y,z, hi x,y,z, max d) this batch
@@ -668,7 +703,8 @@ __device__ __forceinline__ void merge_counts(const Counts &c, Warp6 &Wp, int sid
 }
 
 // Eq. 4.1/4.2 for one contact candidate: s = F_N / dist and its flags
-__device__ __forceinline__ void contact_force6(const MechArgs &A, const Tile6Smem &S, double D,
+template <class SmemT>
+__device__ __forceinline__ void contact_force6(const MechArgs &A, const SmemT &S, double D,
                                                uint32_t e, unsigned stat_mask, double &s_,
                                                uint8_t &fl) {
     const int m = (int)(e & 511u), mo = (int)((e >> 9) & 511u);
@@ -688,8 +724,8 @@ __device__ __forceinline__ void contact_force6(const MechArgs &A, const Tile6Sme
 }
 
 // One batch of <= 32 agents of the staged tile (lane = tile agent klo + lane).
-template <bool kStats>
-__device__ __forceinline__ void tile6_batch(const MechArgs &A, const Tile6Smem &S, Warp6 &Wp,
+template <bool kStats, bool kPair>
+__device__ __forceinline__ void tile6_batch(const MechArgs &A, const Tile6SmemT<kPair> &S, Warp6 &Wp,
                                             int lane, uint32_t g0, int klo, int na, int M,
                                             int sides) {
     const unsigned lt_mask = (1u << lane) - 1u;
@@ -709,7 +745,12 @@ __device__ __forceinline__ void tile6_batch(const MechArgs &A, const Tile6Smem &
         active = !(fi & kGhost);
         if (active) {
             cand_static = A.detect_static && !(fi & kChanged) && ((fi >> BDM_FLAG_NNZ_SHIFT) & 3u) <= 1u;
-            pi = S.P[mi];
+            if constexpr (kPair) {
+                const float4 q = S.f.XY[mi];
+                pi = make_float4(q.x, q.z, S.f.ZZ[mi].x, 0.f);
+            } else {
+                pi = S.f.P[mi];
+            }
             const uint32_t v = S.lbxyz[lbi];
             const int lx = (int)(v & 7u), ly = (int)((v >> 3) & 7u), lz = (int)((v >> 6) & 7u);
             // squared gaps to the faces of the own box (fp32, conservative, see above)
@@ -729,10 +770,15 @@ __device__ __forceinline__ void tile6_batch(const MechArgs &A, const Tile6Smem &
                     const int xs = (b2 + gx2l <= R2f) ? 0 : 1;
                     const int xe = (b2 + gx2h <= R2f) ? 3 : 2;
                     const uint32_t rs = S.off[row + xs], re = S.off[row + xe];
-                    if (re > rs) {  // stored as byte offsets into P (16 B per agent)
-                        Wp.u.a.run[nr][lane] = (rs << 4) | (re << 20);
+                    if (re > rs) {
+                        if constexpr (kPair) {  // indices; the walk takes two candidates per step
+                            Wp.u.a.run[nr][lane] = rs | (re << 16);
+                            walk += (int)((re - rs + 1) >> 1);
+                        } else {      // byte offsets into P (16 B per agent)
+                            Wp.u.a.run[nr][lane] = (rs << 4) | (re << 20);
+                            walk += (int)(re - rs);
+                        }
                         ++nr;
-                        walk += (int)(re - rs);
                     }
                 }
             }
@@ -741,7 +787,7 @@ __device__ __forceinline__ void tile6_batch(const MechArgs &A, const Tile6Smem &
     // sentinel run [16 M, 0xFFFF) (byte offsets into P): after its last real run a lane
     // walks on past M, its loads clamped to the sentinel agent P[M] (at 1e30, never
     // passes), and never advances again (0xFFFF is not a multiple of 16)
-    Wp.u.a.run[nr][lane] = ((uint32_t)M << 4) | (0xFFFFu << 16);
+    Wp.u.a.run[nr][lane] = ((uint32_t)M << (kPair ? 0 : 4)) | (0xFFFFu << 16);
     Wp.chg[lane] = 0;
     const int cmax = __reduce_max_sync(0xffffffffu, walk);
     const bool any_cs = __any_sync(0xffffffffu, cand_static);
@@ -749,8 +795,40 @@ __device__ __forceinline__ void tile6_batch(const MechArgs &A, const Tile6Smem &
     // ---- phase 1: flattened, branch-free walk over the trimmed runs; the walk variable
     // is the byte offset of the candidate in P
     int cnt = 0;
-    {
-        const char *pb = reinterpret_cast<const char *>(&S.P[0]);
+    if constexpr (kPair) {
+        // packed pair walk: candidates m and m + 1 per step (m + 1 masked past the run end);
+        // the sentinel run [M, 0xFFFF) parks the lane on the sentinel pair at M
+        uint16_t *const lrow = &Wp.u.a.lst[0][lane];
+        const uint32_t *const rrow = &Wp.u.a.run[0][lane];
+        const uint32_t cur = rrow[0];
+        int m = (int)(cur & 0xFFFFu), e = (int)(cur >> 16);
+        int j = 32;
+        uint32_t nxt = rrow[j];
+        const unsigned long long pxx = pk2(pi.x, pi.x), pyy = pk2(pi.y, pi.y), pzz = pk2(pi.z, pi.z);
+#pragma unroll 2
+        for (int it = 0; it < cmax; ++it) {
+            const int mc = min(m, M);
+            const float4 q = reinterpret_cast<const float4 *>(&S.f.XY[0])[mc];
+            const float2 qz = reinterpret_cast<const float2 *>(&S.f.ZZ[0])[mc];
+            float d0, d1;
+            dist2_pair(pxx, pyy, pzz, q, qz, d0, d1);
+            const bool p0 = d0 <= R2f;
+            const bool p1 = (d1 <= R2f) && (m + 1 < e);
+            lrow[cnt] = (uint16_t)m;
+            cnt = min(cnt + (p0 ? 32 : 0), 32 * kK6Max);
+            lrow[cnt] = (uint16_t)(m + 1);
+            cnt = min(cnt + (p1 ? 32 : 0), 32 * kK6Max);
+            m += 2;
+            if (m >= e) {
+                m = (int)(nxt & 0xFFFFu);
+                e = (int)(nxt >> 16);
+                j += 32;
+            }
+            nxt = rrow[j];
+        }
+        cnt >>= 5;
+    } else {
+        const char *pb = reinterpret_cast<const char *>(&S.f.P[0]);
         const uint32_t mlast = (uint32_t)M << 4;
         uint16_t *const lrow = &Wp.u.a.lst[0][lane];
         const uint32_t *const rrow = &Wp.u.a.run[0][lane];
@@ -793,7 +871,8 @@ __device__ __forceinline__ void tile6_batch(const MechArgs &A, const Tile6Smem &
     }
     if (!done) {
         const uint32_t tag = ((uint32_t)mi << 9) | ((uint32_t)lane << 18);
-        for (int jj = 0; jj < cnt; ++jj) Wp.pr[my_off + jj] = ((uint32_t)Wp.u.a.lst[jj][lane] >> 4) | tag;
+        for (int jj = 0; jj < cnt; ++jj)
+            Wp.pr[my_off + jj] = ((uint32_t)Wp.u.a.lst[jj][lane] >> (kPair ? 0 : 4)) | tag;
         __syncwarp();
         // ---- phase 2a: exact test, static flags, contact pre-test, compaction
         const double R2 = S.g.R2;
@@ -883,12 +962,12 @@ __device__ __forceinline__ void tile6_batch(const MechArgs &A, const Tile6Smem &
     merge_counts<kStats>(c, Wp, sides, lane);
 }
 
-template <bool kStats, int kMinBlocks>
+template <bool kStats, int kMinBlocks, bool kPair>
 __global__ void __launch_bounds__(kT6Threads, kMinBlocks) k_mech_tile6(MechArgs A, DevScalars *__restrict__ sc,
                                                                       int allow_prefilter) {
     if (sc->overflow) return;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    Tile6Smem &S = *reinterpret_cast<Tile6Smem *>(smem_raw);
+    Tile6SmemT<kPair> &S = *reinterpret_cast<Tile6SmemT<kPair> *>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     if (tid == 0) {
         const GridView g = load_grid(sc);
@@ -1015,10 +1094,38 @@ __global__ void __launch_bounds__(kT6Threads, kMinBlocks) k_mech_tile6(MechArgs 
                 S.Z[m] = z;
                 S.Rr[m] = d * 0.5;
                 S.F[m] = A.sflags[gi];
-                S.P[m] = make_float4((float)(x - X0), (float)(y - Y0), (float)(z - Z0), 0.f);
+                const float xr = (float)(x - X0), yr = (float)(y - Y0), zr = (float)(z - Z0);
+                if constexpr (kPair) {
+                    float *xy = reinterpret_cast<float *>(&S.f.XY[0]);
+                    float *zz = reinterpret_cast<float *>(&S.f.ZZ[0]);
+                    xy[4 * m + 0] = xr;
+                    xy[4 * m + 2] = yr;
+                    zz[2 * m + 0] = zr;
+                    if (m > 0) {
+                        xy[4 * (m - 1) + 1] = xr;
+                        xy[4 * (m - 1) + 3] = yr;
+                        zz[2 * (m - 1) + 1] = zr;
+                    }
+                } else {
+                    S.f.P[m] = make_float4(xr, yr, zr, 0.f);
+                }
             }
         }
-        if (tid == 0) S.P[M] = make_float4(kSentinel, kSentinel, kSentinel, 0.f);
+        if (tid == 0) {  // sentinel agent at M (both halves of its pair, and M's half of M-1)
+            if constexpr (kPair) {
+                float *xy = reinterpret_cast<float *>(&S.f.XY[0]);
+                float *zz = reinterpret_cast<float *>(&S.f.ZZ[0]);
+                S.f.XY[M] = make_float4(kSentinel, kSentinel, kSentinel, kSentinel);
+                S.f.ZZ[M] = make_float2(kSentinel, kSentinel);
+                if (M > 0) {
+                    xy[4 * (M - 1) + 1] = kSentinel;
+                    xy[4 * (M - 1) + 3] = kSentinel;
+                    zz[2 * (M - 1) + 1] = kSentinel;
+                }
+            } else {
+                S.f.P[M] = make_float4(kSentinel, kSentinel, kSentinel, 0.f);
+            }
+        }
         __syncthreads();
         int sides = 0;
         if (S.edge_only) {
@@ -1037,7 +1144,7 @@ __global__ void __launch_bounds__(kT6Threads, kMinBlocks) k_mech_tile6(MechArgs 
             // and the fp32 quotient (bb nc < 2^24) floors exactly
             const int klo = (int)__fdividef((float)(bb * nc), (float)B);
             const int khi = (int)__fdividef((float)((bb + 1) * nc), (float)B);
-            tile6_batch<kStats>(A, S, S.W[w], lane, g0, klo, khi - klo, M, sides);
+            tile6_batch<kStats, kPair>(A, S, S.W[w], lane, g0, klo, khi - klo, M, sides);
         }
         __syncthreads();  // before the next tile overwrites the staged region
     }
@@ -1051,20 +1158,20 @@ __global__ void __launch_bounds__(kT6Threads, kMinBlocks) k_mech_tile6(MechArgs 
     if (kStats && lane < 5) atomicAdd(&sc->stats[lane], Wp.cnt[lane]);
 }
 
-template <bool kStats, int kMinBlocks>
+template <bool kStats, int kMinBlocks, bool kPair>
 static bdm_status launch_tile6(Ctx *c, const MechArgs &A, cudaStream_t st) {
     static bool attr_set = false;
     static int per_sm = 0;
-    const int smem = (int)sizeof(Tile6Smem);
+    const int smem = (int)sizeof(Tile6SmemT<kPair>);
     if (!attr_set) {
-        BDM_CUDA_TRY(cudaFuncSetAttribute(k_mech_tile6<kStats, kMinBlocks>,
+        BDM_CUDA_TRY(cudaFuncSetAttribute(k_mech_tile6<kStats, kMinBlocks, kPair>,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         BDM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-            &per_sm, k_mech_tile6<kStats, kMinBlocks>, kT6Threads, smem));
+            &per_sm, k_mech_tile6<kStats, kMinBlocks, kPair>, kT6Threads, smem));
         if (per_sm < 1) per_sm = 1;
         attr_set = true;
     }
-    k_mech_tile6<kStats, kMinBlocks><<<(unsigned)(c->sm_count * per_sm), kT6Threads, smem, st>>>(
+    k_mech_tile6<kStats, kMinBlocks, kPair><<<(unsigned)(c->sm_count * per_sm), kT6Threads, smem, st>>>(
         A, c->sc, c->prefilter);
     return BDM_OK;
 }
@@ -1105,12 +1212,12 @@ bdm_status launch_mech(Ctx *c, bdm_agents *a, const bdm_params *p, cudaStream_t 
     if (p->collect_stats)
         BDM_CUDA_TRY(cudaMemsetAsync(c->sc->stats, 0, sizeof(c->sc->stats), st));
     if (c->mech_kernel == 0) {
-        const bdm_status s = p->collect_stats ? launch_tile6<true, 5>(c, A, st)
-                                              : launch_tile6<false, 5>(c, A, st);
+        const bdm_status s = p->collect_stats ? launch_tile6<true, 5, false>(c, A, st)
+                                              : launch_tile6<false, 5, false>(c, A, st);
         if (s != BDM_OK) return s;
-    } else if (c->mech_kernel == 3) {  // same kernel at 4 CTAs/SM (128 registers)
-        const bdm_status s = p->collect_stats ? launch_tile6<true, 4>(c, A, st)
-                                              : launch_tile6<false, 4>(c, A, st);
+    } else if (c->mech_kernel == 3) {  // packed f32x2 pair walk, 4 CTAs/SM
+        const bdm_status s = p->collect_stats ? launch_tile6<true, 4, true>(c, A, st)
+                                              : launch_tile6<false, 4, true>(c, A, st);
         if (s != BDM_OK) return s;
     } else if (c->mech_kernel == 2) {
         const bdm_status s = p->collect_stats ? launch_tile<true>(c, A, st)
