@@ -277,6 +277,9 @@ bdm_status bdm_neighbor_pairs(bdm_handle h, const bdm_agents *a, double radius,
  *                  2 the first tile kernel (per-lane pair lists, no run trimming);
  *                  3 the kernel of 0 compiled for 4 CTAs per SM (no register spills).
  *   "sir_index_capacity"  infected agents the SIR index holds (0 = max(65536, n/16)).
+ *   "dense"        1 (default) / 0: regions too crowded for the tile kernel's shared-memory
+ *                  staging (> 416 agents in a 6^3-box region) go to the dense-box kernel
+ *                  (warp per box, broadcast candidate stream); 0: reference formulation.
  *   "prefilter"    1 (default) / 0: conservative fp32 candidate test in the tile kernel
  *                  (never rejects a neighbour; the exact fp64 test decides).
  *   "fuse_reduce"  0 (default) / 1: bdm_mech_step also reduces the extent of the new

@@ -74,7 +74,10 @@ static bdm_status grow_slots(Ctx *c, int64_t nslots) {
     if (nslots <= c->slot_cap) return BDM_OK;
     BDM_CUDA_TRY(cudaDeviceSynchronize());
     bdm_status s;
-    if ((s = dalloc(&c->box_start, nslots + 1))) { c->slot_cap = 0; return s; }
+    if ((s = dalloc(&c->box_start, nslots + 1)) || (s = dalloc(&c->dense_list, nslots / 64 + 1))) {
+        c->slot_cap = 0;
+        return s;
+    }
     const int64_t nb = scan_block_count(nslots > c->agent_cap ? nslots : c->agent_cap) + 1;
     if (nb > c->block_sums_cap) {
         if ((s = dalloc(&c->block_sums, nb))) { c->slot_cap = 0; return s; }
@@ -171,7 +174,7 @@ bdm_status bdm_destroy(bdm_handle h) {
     cudaSetDevice(c->device);
     cudaDeviceSynchronize();
     void *bufs[] = {c->key, c->rank, c->perm_tmp, c->skey, c->sid, c->perm, c->sx, c->sy,
-                    c->sz, c->sd, c->sidf, c->sflags, c->svol, c->div_rank, c->box_start,
+                    c->sz, c->sd, c->sidf, c->sflags, c->svol, c->div_rank, c->box_start, c->dense_list,
                     c->block_sums, c->pair_count, c->n_new, c->lrank, c->cls, c->cls2,
                     c->pack_counts, c->sc};
     for (void *p : bufs)
@@ -471,6 +474,11 @@ bdm_status bdm_set_option(bdm_handle h, const char *name, int64_t value) {
         if (value < 0 || value > 1) return fail(BDM_EINVAL, "fuse_reduce must be 0 or 1");
         c->fuse_reduce = (int)value;
         c->fused_valid = false;
+        return BDM_OK;
+    }
+    if (strcmp(name, "dense") == 0) {
+        if (value < 0 || value > 1) return fail(BDM_EINVAL, "dense must be 0 or 1");
+        c->dense = (int)value;
         return BDM_OK;
     }
     if (strcmp(name, "prefilter") == 0) {

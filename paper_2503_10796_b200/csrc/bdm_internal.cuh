@@ -45,6 +45,8 @@ struct DevScalars {
     unsigned long long stats[5];  // cand, nbr, cont, n_static, n_moved
     int32_t boff[3];       // lattice offset: box index = floor((x - o)/L) - boff (R12, 8(e))
     int32_t has_frame;     // the origin came from a global frame (multi-GPU)
+    unsigned int n_dense;  // dense tiles handed from the tile kernel to the dense kernel
+    unsigned int dense_next;  // dense kernel work counter (box tasks taken)
     double dmax_prev;      // max diameter of the grid build's input (the step keeps it)
 };
 
@@ -77,6 +79,7 @@ struct Ctx {
     long long *n_new = nullptr;                        // growth/division: new agent count
     // grid
     uint32_t *box_start = nullptr;  // slot_cap + 1
+    uint32_t *dense_list = nullptr; // slot_cap / 64 + 1 tile ids (dense regions)
     uint32_t *block_sums = nullptr;
     int64_t block_sums_cap = 0;
     // misc
@@ -97,6 +100,7 @@ struct Ctx {
     int mech_kernel = 0;   // option "mech_kernel": 0 tile kernel, 1 per-agent reference kernel
     int prefilter = 1;     // option "prefilter": fp32 conservative candidate test in the tile kernel
     int fuse_reduce = 0;   // option "fuse_reduce": next step's a1 extent from the mech epilogue
+    int dense = 1;         // option "dense": dense regions go to the dense-box kernel
     bool fused_valid = false;          // the scalars hold the extent of (fused_x, fused_n)
     const double *fused_x = nullptr;
     int64_t fused_n = 0;

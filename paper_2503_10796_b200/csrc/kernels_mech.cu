@@ -37,6 +37,7 @@ struct MechArgs {
     const uint32_t *__restrict__ lrank;  // nullable: output index of sorted local slots (ghosts)
     const double *__restrict__ svol;  // nullable: volume travels with the agents
     double *__restrict__ ovol;
+    uint32_t *__restrict__ dense_list;   // nullable: dense tiles go to k_mech_dense
     double k, gamma, dt, max_disp, tau;
     int detect_static, boundary, fuse;
     double lo0, lo1, lo2, hi0, hi1, hi2;
@@ -1059,6 +1060,11 @@ __global__ void __launch_bounds__(kT6Threads, kMinBlocks) k_mech_tile6(MechArgs 
         }
         __syncthreads();
         const int M = (int)S.off[216];
+        if (M > kM6Max && S.use_pf && A.dense_list) {  // dense region: the dense-box kernel
+            if (tid == 0) A.dense_list[atomicAdd(&sc->n_dense, 1u)] = (uint32_t)t;
+            __syncthreads();
+            continue;
+        }
         if (M > kM6Max || !S.use_pf) {
             // over-full region or |coordinates| / L >= 2^30: reference formulation
             for (int k0 = 32 * w; k0 < nc; k0 += kT6Threads) {
@@ -1194,6 +1200,303 @@ static bdm_status launch_tile(Ctx *c, const MechArgs &A, cudaStream_t st) {
     return BDM_OK;
 }
 
+// ============================================================== dense-box kernel
+// Regions too crowded for the tile kernel's staging (cfg3 late steps: 100-300 agents per
+// box) are handed over as tiles.  Warp-independent tasks: a warp takes one box (dynamic
+// scheduling through a device counter) and processes its agents in groups of <= 32, one
+// per lane.  All lanes of a group share the same candidate stream: the 27 neighbour
+// boxes in canonical order (dz, dy, dx), ascending id inside a box (R9), which the warp
+// stages in batches of 32 candidates in its own shared memory (a 5-step search maps a
+// stream position to its box).  Per batch:
+//   phase 1  broadcast fp32 test of every candidate against every lane's agent (the
+//            same conservative prefilter as the tile kernel; coordinates relative to the
+//            corner of the agent's box, |x - C| <= 2L), survivors as one bitmask per lane
+//   queue    the lanes' survivors are concatenated (warp scan of the popcounts) into a
+//            queue in owner-major, candidate-ascending (= canonical) order
+//   phase 2a lane-parallel over the queue (chunks of 192): exact fp64 test D <= R^2, self
+//            excluded, static pull flags, contact pre-test and compaction (as k_mech_tile6);
+//            a queued contact keeps its exact differences x_i - x_j
+//   phase 2b lane-parallel Eq. 4.1/4.2 over the compacted contacts, s = F_N / dist
+//   phase 3  each lane adds its own contacts of the chunk in order with fma (the
+//            contacts of one word concentrate on few lanes, so this loop is kept to
+//            loads and three fma)
+// The static decision needs every neighbour's flags, so forces of a candidate static
+// agent are computed and dropped when it turns out static (a5 result unchanged).
+constexpr int kDWarps = 4;
+constexpr int kDB = 32;     // staged candidates per warp batch (one word)
+constexpr int kDQ = 192;    // survivors per processed chunk
+
+struct DenseWarp {
+    float4 P[kDB];                          // fp32 x, y, z relative to the box corner
+    double X[kDB], Y[kDB], Z[kDB], Rr[kDB];
+    uint32_t F[kDB], G[kDB];                // flags, sorted index
+    uint32_t bs[32], bp[32];                // neighbour boxes: first agent, stream offset
+    double ox[32], oy[32], oz[32], orr[32]; // the group's own agents
+    uint32_t os[32];                        // their sorted index
+    uint32_t nbrc[32];                      // neighbours per owner (stats)
+    uint16_t Q[32 * 32];                    // survivor queue: j | owner << 8
+    uint16_t cpre[kDQ + 1];                 // contacts before survivor p (chunk-relative)
+    double cq[kDQ];                         // D, then s
+    double cx[kDQ], cy[kDQ], cz[kDQ];       // x_i - x_j of the contact
+    uint16_t ce[kDQ];                       // contact -> survivor entry (j | owner << 8)
+    uint8_t cf[kDQ];                        // bit1 contact, bit0 F_N != 0
+    uint8_t chg[32];
+};
+
+template <bool kStats>
+__global__ void __launch_bounds__(32 * kDWarps, 4) k_mech_dense(MechArgs A, DevScalars *__restrict__ sc) {
+    if (sc->overflow) return;
+    extern __shared__ __align__(16) unsigned char dsm_raw[];
+    DenseWarp *Sd = reinterpret_cast<DenseWarp *>(dsm_raw);
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const unsigned lt_mask = (1u << lane) - 1u;
+    DenseWarp &Wd = Sd[w];
+    const unsigned ntask = sc->n_dense * 64u;
+    if (ntask == 0) return;
+    const GridView g = load_grid(sc);
+    const float R2f = (float)(g.R2 * (1.0 + 0x1p-12));
+    Counts c;
+    for (;;) {
+        unsigned item = 0;
+        if (lane == 0) item = atomicAdd(&sc->dense_next, 1u);
+        item = __shfl_sync(0xffffffffu, item, 0);
+        if (item >= ntask) break;
+        const int t = (int)A.dense_list[item >> 6];
+        const uint32_t mort = item & 63u;
+        const int tx = t % g.T0, ty = (t / g.T0) % g.T1, tz = t / (g.T0 * g.T1);
+        const int bx = 4 * tx + (int)((mort & 1u) | ((mort >> 2) & 2u));
+        const int by = 4 * ty + (int)(((mort >> 1) & 1u) | ((mort >> 3) & 2u));
+        const int bz = 4 * tz + (int)(((mort >> 2) & 1u) | ((mort >> 4) & 2u));
+        if (bx >= g.D0 || by >= g.D1 || bz >= g.D2) continue;
+        const uint32_t key = (uint32_t)t * 64u + mort;
+        const uint32_t b0 = A.box_start[key];
+        const int nb = (int)(A.box_start[key + 1] - b0);
+        if (nb == 0) continue;
+        // ---- the 27 neighbour boxes (lanes 0..26) in canonical order, stream offsets
+        uint32_t T;
+        {
+            uint32_t st = 0, cn = 0;
+            if (lane < 27) {
+                const int dz = lane / 9 - 1, dy = (lane / 3) % 3 - 1, dx = lane % 3 - 1;
+                const int cx = bx + dx, cy = by + dy, cz = bz + dz;
+                if (cx >= 0 && cy >= 0 && cz >= 0 && cx < g.D0 && cy < g.D1 && cz < g.D2) {
+                    const uint32_t k2 = box_key(cx, cy, cz, g.T0, g.T1);
+                    st = A.box_start[k2];
+                    cn = A.box_start[k2 + 1] - st;
+                }
+            }
+            uint32_t inc = cn;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+                if (lane >= o) inc += y;
+            }
+            Wd.bs[lane] = st;
+            Wd.bp[lane] = inc - cn;  // lanes 27..31: = T, keeps the table monotone
+            T = __shfl_sync(0xffffffffu, inc, 31);
+        }
+        const double C0 = g.o0 + (double)(bx + g.b0) * g.L, C1 = g.o1 + (double)(by + g.b1) * g.L,
+                     C2 = g.o2 + (double)(bz + g.b2) * g.L;
+        const int ngrp = (nb + 31) >> 5;
+        for (int gq = 0; gq < ngrp; ++gq) {
+            const int a0 = (gq * nb) / ngrp, a1 = ((gq + 1) * nb) / ngrp;
+            const uint32_t s = b0 + (uint32_t)(a0 + lane);
+            uint32_t fi = 0;
+            bool active = false;
+            if (lane < a1 - a0) {
+                fi = A.sflags[s];
+                active = !(fi & kGhost);
+            }
+            double xi = 0.0, yi = 0.0, zi = 0.0;
+            float px = -kSentinel, py = -kSentinel, pz = -kSentinel;
+            if (active) {
+                xi = A.sx[s];
+                yi = A.sy[s];
+                zi = A.sz[s];
+                px = (float)(xi - C0);
+                py = (float)(yi - C1);
+                pz = (float)(zi - C2);
+                Wd.orr[lane] = A.sd[s] * 0.5;
+            }
+            Wd.ox[lane] = xi;
+            Wd.oy[lane] = yi;
+            Wd.oz[lane] = zi;
+            Wd.os[lane] = s;
+            Wd.chg[lane] = 0;
+            Wd.nbrc[lane] = 0;
+            const int nnz_in = (int)((fi >> BDM_FLAG_NNZ_SHIFT) & 3u);
+            const bool cand_static = active && A.detect_static && !(fi & kChanged) && nnz_in <= 1;
+            double Fx = 0.0, Fy = 0.0, Fz = 0.0;
+            int nnz = 0;
+            uint32_t my_cont = 0;
+            for (uint32_t base = 0; base < T; base += kDB) {
+                const int nbt = (int)min((uint32_t)kDB, T - base);
+                __syncwarp();  // the previous batch is fully consumed
+                // ---- stage the batch (coalesced: a box's agents are contiguous)
+#pragma unroll
+                for (int u = 0; u < kDB / 32; ++u) {
+                    const int q = 32 * u + lane;
+                    if (q < nbt) {
+                        const uint32_t pos = base + (uint32_t)q;
+                        int r = 0;
+#pragma unroll
+                        for (int st = 16; st >= 1; st >>= 1)
+                            if (Wd.bp[r + st] <= pos) r += st;
+                        const uint32_t gj = Wd.bs[r] + (pos - Wd.bp[r]);
+                        const double x = A.sx[gj], y = A.sy[gj], z = A.sz[gj];
+                        Wd.X[q] = x;
+                        Wd.Y[q] = y;
+                        Wd.Z[q] = z;
+                        Wd.Rr[q] = A.sd[gj] * 0.5;
+                        Wd.F[q] = A.sflags[gj];
+                        Wd.G[q] = gj;
+                        Wd.P[q] = make_float4((float)(x - C0), (float)(y - C1), (float)(z - C2), 0.f);
+                    }
+                }
+                __syncwarp();
+                for (int u = 0; u < kDB / 32 && 32 * u < nbt; ++u) {  // warp-uniform
+                    // ---- phase 1: broadcast fp32 prefilter -> survivor bitmask
+                    uint32_t m = 0;
+                    const int jn = min(32, nbt - 32 * u);
+#pragma unroll 4
+                    for (int j = 0; j < jn; ++j) {
+                        const float4 q = Wd.P[32 * u + j];
+                        const float ex = px - q.x, ey = py - q.y, ez = pz - q.z;
+                        if (fmaf(ez, ez, fmaf(ey, ey, ex * ex)) <= R2f) m |= 1u << j;
+                    }
+                    // ---- survivor queue, owner-major, candidate-ascending
+                    const int cnt = __popc(m);
+                    int cincl = cnt;
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const int y = __shfl_up_sync(0xffffffffu, cincl, o);
+                        if (lane >= o) cincl += y;
+                    }
+                    const int my_off = cincl - cnt;
+                    const int total = __shfl_sync(0xffffffffu, cincl, 31);
+                    {
+                        int o = my_off;
+                        uint32_t mm = m;
+                        while (mm) {
+                            const int j = __ffs(mm) - 1;
+                            mm &= mm - 1;
+                            Wd.Q[o++] = (uint16_t)((32 * u + j) | (lane << 8));
+                        }
+                    }
+                    __syncwarp();
+                    for (int c0 = 0; c0 < total; c0 += kDQ) {  // warp-uniform
+                        const int c1 = min(total, c0 + kDQ);
+                        // ---- phase 2a: exact test, static flags, contact pre-test, compaction
+                        int cbase = 0;
+                        for (int p0 = c0; p0 < c1; p0 += 32) {
+                            const int p = p0 + lane;
+                            bool cc = false;
+                            double D = 0.0, ex = 0.0, ey = 0.0, ez = 0.0;
+                            uint32_t e = 0;
+                            if (p < c1) {
+                                e = Wd.Q[p];
+                                const int j = (int)(e & 255u), ow = (int)(e >> 8);
+                                if (Wd.G[j] != Wd.os[ow]) {
+                                    ex = Wd.ox[ow] - Wd.X[j];
+                                    ey = Wd.oy[ow] - Wd.Y[j];
+                                    ez = Wd.oz[ow] - Wd.Z[j];
+                                    D = fma(ez, ez, fma(ey, ey, ex * ex));
+                                    if (D <= g.R2) {
+                                        if (kStats) atomicAdd(&Wd.nbrc[ow], 1u);
+                                        if (Wd.F[j] & kChanged) Wd.chg[ow] = 1;
+                                        const double s2 = Wd.orr[ow] + Wd.Rr[j];
+                                        cc = D > 0.0 && D < (s2 * s2) * (1.0 + 0x1p-30);
+                                    }
+                                }
+                            }
+                            const unsigned cb = __ballot_sync(0xffffffffu, cc);
+                            const int cidx = cbase + __popc(cb & lt_mask);
+                            if (p < c1) Wd.cpre[p - c0] = (uint16_t)cidx;
+                            if (cc) {
+                                Wd.cq[cidx] = D;
+                                Wd.cx[cidx] = ex;
+                                Wd.cy[cidx] = ey;
+                                Wd.cz[cidx] = ez;
+                                Wd.ce[cidx] = (uint16_t)e;
+                            }
+                            cbase += __popc(cb);
+                        }
+                        if (lane == 0) Wd.cpre[c1 - c0] = (uint16_t)cbase;
+                        __syncwarp();
+                        // ---- phase 2b: Eq. 4.1/4.2 over the compacted contact candidates
+                        for (int q = lane; q < cbase; q += 32) {
+                            const uint32_t e = Wd.ce[q];
+                            const int j = (int)(e & 255u), ow = (int)(e >> 8);
+                            double s_ = 0.0;
+                            uint8_t fl = 0;
+                            const double dist = sqrt(Wd.cq[q]);
+                            const double ri = Wd.orr[ow], rj = Wd.Rr[j];
+                            const double delta = (ri + rj) - dist;
+                            if (delta > 0.0) {
+                                const double rbar = (ri * rj) / (ri + rj);
+                                const double Fn = A.k * delta - A.gamma * sqrt(rbar * delta);
+                                s_ = Fn / dist;
+                                fl = (uint8_t)(2u | (Fn != 0.0 ? 1u : 0u));
+                            }
+                            Wd.cq[q] = s_;
+                            Wd.cf[q] = fl;
+                        }
+                        __syncwarp();
+                        // ---- phase 3: own contacts of the chunk, in order
+                        const int lo = max(my_off, c0) - c0, hi = min(my_off + cnt, c1) - c0;
+                        if (hi > lo) {
+                            const int q0 = Wd.cpre[lo], q1 = Wd.cpre[hi];
+                            for (int q = q0; q < q1; ++q) {
+                                const uint32_t fl = Wd.cf[q];
+                                if (fl & 2u) {
+                                    const double s_ = Wd.cq[q];
+                                    Fx = fma(s_, Wd.cx[q], Fx);
+                                    Fy = fma(s_, Wd.cy[q], Fy);
+                                    Fz = fma(s_, Wd.cz[q], Fz);
+                                    nnz += (int)(fl & 1u);
+                                    ++my_cont;
+                                }
+                            }
+                        }
+                        __syncwarp();
+                    }
+                }
+            }
+            __syncwarp();
+            if (active) {
+                const bool is_static = cand_static && !Wd.chg[lane];
+                if (is_static) {
+                    nnz = nnz_in;
+                } else {
+                    nnz = nnz < 2 ? nnz : 2;
+                    if (kStats) {
+                        c.cand += T - 1u;
+                        c.nbr += Wd.nbrc[lane];
+                        c.cont += my_cont;
+                    }
+                }
+                finish_agent(A, s, xi, yi, zi, Fx, Fy, Fz, is_static, nnz, c);
+            }
+        }
+    }
+    flush_counts<kStats>(c, sc, A.fuse);
+}
+
+template <bool kStats>
+static bdm_status launch_dense(Ctx *c, const MechArgs &A, cudaStream_t st) {
+    static int per_sm = 0;
+    const int smem = (int)(sizeof(DenseWarp) * kDWarps);
+    if (!per_sm) {
+        BDM_CUDA_TRY(cudaFuncSetAttribute(k_mech_dense<kStats>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        BDM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mech_dense<kStats>,
+                                                                   32 * kDWarps, smem));
+        if (per_sm < 1) per_sm = 1;
+    }
+    k_mech_dense<kStats><<<(unsigned)(c->sm_count * per_sm), 32 * kDWarps, smem, st>>>(A, c->sc);
+    return BDM_OK;
+}
+
 bdm_status launch_mech(Ctx *c, bdm_agents *a, const bdm_params *p, cudaStream_t st) {
     MechArgs A;
     A.n = a->n;
@@ -1211,6 +1514,9 @@ bdm_status launch_mech(Ctx *c, bdm_agents *a, const bdm_params *p, cudaStream_t 
     A.hi0 = p->hi[0]; A.hi1 = p->hi[1]; A.hi2 = p->hi[2];
     if (p->collect_stats)
         BDM_CUDA_TRY(cudaMemsetAsync(c->sc->stats, 0, sizeof(c->sc->stats), st));
+    const bool dense = c->dense && (c->mech_kernel == 0 || c->mech_kernel == 3);
+    A.dense_list = dense ? c->dense_list : nullptr;
+    if (dense) BDM_CUDA_TRY(cudaMemsetAsync(&c->sc->n_dense, 0, 2 * sizeof(unsigned int), st));
     if (c->mech_kernel == 0) {
         const bdm_status s = p->collect_stats ? launch_tile6<true, 5, false>(c, A, st)
                                               : launch_tile6<false, 5, false>(c, A, st);
@@ -1230,6 +1536,12 @@ bdm_status launch_mech(Ctx *c, bdm_agents *a, const bdm_params *p, cudaStream_t 
     }
     c->launches += 1;
     BDM_LAUNCH_CHECK("k_mech");
+    if (dense) {
+        const bdm_status s = p->collect_stats ? launch_dense<true>(c, A, st) : launch_dense<false>(c, A, st);
+        if (s != BDM_OK) return s;
+        c->launches += 1;
+        BDM_LAUNCH_CHECK("k_mech_dense");
+    }
     return BDM_OK;
 }
 

@@ -211,6 +211,43 @@ def test_crowded_neighbourhoods(eng, orc, k):
         assert_state_equal(a.numpy(), s, f"k={k} step {t}")
 
 
+def _dense_population(orc, n_bg, side_bg, n_cl, side_cl, seed):
+    """A uniform background (n_bg agents, cfg2 diameter mix, cube side_bg) plus a dense
+    cluster of n_cl agents in a cube of side side_cl at its centre (ids follow on)."""
+    bg = orc.init_spheres(n_bg, seed, side_bg, 8.0, 4.0, True)
+    cl = orc.init_spheres(n_cl, seed + 1, side_cl, 8.0, 4.0, True)
+    off = 0.5 * (side_bg - side_cl)
+    s = {}
+    for k in ("x", "y", "z"):
+        s[k] = np.concatenate([bg[k], cl[k] + off])
+    s["d"] = np.concatenate([bg["d"], cl["d"]])
+    s["id"] = np.arange(n_bg + n_cl, dtype=np.uint32)
+    s["flags"] = np.full(n_bg + n_cl, 4, np.uint32)
+    return s
+
+
+@pytest.mark.parametrize("n_bg,side_bg,n_cl,side_cl,static,tau", [
+    (0, 1.0, 6000, 40.0, False, 0.0),        # every region dense, ~100 agents per box
+    (20000, 220.0, 3000, 24.0, True, 1e-3),  # dense cluster inside sparse tiles, static on
+    (4000, 120.0, 1500, 14.0, True, 0.0),    # > 32 agents per box (several lane groups)
+])
+def test_dense_regions(eng, orc, n_bg, side_bg, n_cl, side_cl, static, tau):
+    """Regions too crowded for the tile kernel's staging (cfg3 late-step densities) go to
+    the dense-box kernel: candidate streams longer than one staged batch, boxes with
+    more agents than lanes, mixed with sparse tiles; bit-exact state and counters."""
+    from paper_2503_10796_b200 import Agents
+    s = _dense_population(orc, n_bg, side_bg, n_cl, side_cl, 5)
+    gp, op = params_pair(orc, W.CFG1, detect_static=static, force_threshold=tau)
+    a = Agents.from_numpy(s)
+    for t in range(3):
+        eng.step(a, gp)
+        st = eng.stats()
+        s, cnt = orc.step_full(s, op)
+        assert_state_equal(a.numpy(), s, f"dense step {t}")
+        assert (st["cand"], st["nbr"], st["cont"], st["n_static"]) == (
+            cnt["cand"], cnt["nbr"], cnt["cont"], cnt["n_static"]), t
+
+
 def test_capacity_overflow_is_recovered(eng, orc):
     """An agent far outside the first grid's extent exceeds the slot capacity; the
     overflowed step is a no-op and the binding grows the slots and re-issues it."""
