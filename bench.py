@@ -339,7 +339,7 @@ def run_cfg3(args, ws, rank, local):
                     "l2": "inputs larger than L2 from step 1 (48 B/agent x >= 1M)"},
                    clk.summary(), eng.stats()["launches"] - launches0)
     line["roofline"] = None
-    line["note"] = "proliferation: per-step rate in config.per_step; dense late steps use the global-memory kernel"
+    line["note"] = "proliferation: per-step rate in config.per_step; dense late steps run the dense-box kernel"
     print(json.dumps(line), flush=True)
 
 
