@@ -14,7 +14,9 @@
 // neighbourhood; only if one is set does it probe the 27 fine boxes.
 //   k_sir_collect  snapshot of the infected agents: positions, hash insert, bitmap
 //   k_sir_update   per agent, in place: infection query, recovery, movement, wrap,
-//                  S/I/R counts
+//                  S/I/R counts.  A warp handles two 32-agent slices per iteration
+//                  (loads first); infection queries are compacted into a per-warp queue
+//                  and resolved one per lane
 #include <cuda_runtime.h>
 #include <math.h>
 
@@ -218,50 +220,137 @@ __device__ __forceinline__ double wrap_alg9(double el, double max_bound) {
     return r;
 }
 
-__global__ void __launch_bounds__(256, 3) k_sir_update(SirArgs A, DevScalars *__restrict__ sc) {
-    if (sc->overflow) return;
-    unsigned long long cs = 0, ci = 0, cr = 0, cn = 0;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < A.n;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const uint32_t me = A.id ? A.id[i] : (uint32_t)i;
-        const double px = A.x[i], py = A.y[i], pz = A.z[i];
-        uint8_t st = A.state[i];
-        const U4 w = philox10(me, 0u, A.step, 0u, A.k0, A.k1);
-        // Alg. 7: infection (R17: strict '<', u = w * 2^-32)
-        if (st == 0 && uniform32(w.d) < A.p_inf && infected_within(A, px, py, pz)) {
-            st = 1;
-            ++cn;
-        }
-        // Alg. 8: recovery (own state updated in sequence, R18)
+// Infection queries (S agents whose draw passed, ~p_inf of them) are compacted into a
+// per-warp queue with their start-of-step position and resolved 32 at a time, one per
+// lane, so the index search does not run with a few lanes of each warp; movement and
+// the other state updates do not depend on the query and proceed at once.
+constexpr int kSirThreads = 256;
+constexpr int kSirQ = 64;  // queue entries per warp (<= 31 left over + <= 32 new)
+
+struct SirQueue {
+    uint32_t idx[kSirQ];
+    double px[kSirQ], py[kSirQ], pz[kSirQ];
+};
+
+// The final state of a queried S agent and its counters.
+__device__ __forceinline__ void sir_resolve(const SirArgs &A, uint32_t i, double px, double py,
+                                            double pz, unsigned long long &cs,
+                                            unsigned long long &ci, unsigned long long &cr,
+                                            unsigned long long &cn) {
+    uint8_t st = 0;
+    if (infected_within(A, px, py, pz)) {
+        st = 1;
+        ++cn;
+        const uint32_t me = A.id ? A.id[i] : i;
+        const U4 r = philox10(me, 0u, A.step, 1u, A.k0, A.k1);
+        if (uniform32(r.a) < A.p_rec) st = 2;  // Alg. 8 in sequence (R18)
+    }
+    A.state[i] = st;
+    cs += st == 0;
+    ci += st == 1;
+    cr += st == 2;
+}
+
+// One agent of the update (its start-of-step x, y, z, state already loaded): Philox
+// draws, the queue entry for an infection query, recovery, movement and wrap.
+__device__ __forceinline__ void sir_agent(const SirArgs &A, SirQueue &Q, int lane, unsigned lt_mask,
+                                          int64_t i, bool valid, double px, double py, double pz,
+                                          uint8_t st, int &qn, unsigned long long &cs,
+                                          unsigned long long &ci, unsigned long long &cr,
+                                          unsigned long long &cn) {
+    const uint32_t me = valid ? (A.id ? A.id[i] : (uint32_t)i) : 0u;
+    const U4 w = philox10(me, 0u, A.step, 0u, A.k0, A.k1);
+    // Alg. 7: an S agent whose draw passed (R17: strict '<', u = w * 2^-32) is queued
+    const bool query = valid && st == 0 && uniform32(w.d) < A.p_inf;
+    if (valid && !query) {
+        // Alg. 8: recovery (own state in sequence, R18)
         if (st == 1) {
             const U4 r = philox10(me, 0u, A.step, 1u, A.k0, A.k1);
-            if (uniform32(r.a) < A.p_rec) st = 2;
+            if (uniform32(r.a) < A.p_rec) {
+                st = 2;
+                A.state[i] = st;
+            }
         }
-        A.state[i] = st;
         cs += st == 0;
         ci += st == 1;
         cr += st == 2;
-        // Alg. 9: movement capped at unit length (R16), toroidal wrap (R20)
+    }
+    // Alg. 9: movement capped at unit length (R16), toroidal wrap (R20)
+    if (valid) {
         double vx = 2.0 * uniform32(w.a) - 1.0;
         double vy = 2.0 * uniform32(w.b) - 1.0;
         double vz = 2.0 * uniform32(w.c) - 1.0;
         const double v2 = vx * vx + vy * vy + vz * vz;
-        {   // computed by every lane (no divergence), selected where v.v > 1
+        if (v2 > 1.0) {
             const double nv = sqrt(v2);
-            const bool cap = v2 > 1.0;
-            const double qx = vx / nv, qy = vy / nv, qz = vz / nv;
-            vx = cap ? qx : vx;
-            vy = cap ? qy : vy;
-            vz = cap ? qz : vz;
+            vx = vx / nv;
+            vy = vy / nv;
+            vz = vz / nv;
         }
         A.x[i] = wrap_alg9(px + vx, A.side);
         A.y[i] = wrap_alg9(py + vy, A.side);
         A.z[i] = wrap_alg9(pz + vz, A.side);
     }
-    // block reduction of the counters, one atomic each per block
-    __shared__ unsigned long long red[4][8];
-    unsigned long long v[4] = {cs, ci, cr, cn};
+    // queue the infection queries (start-of-step positions)
+    const unsigned qb = __ballot_sync(0xffffffffu, query);
+    if (query) {
+        const int p = qn + __popc(qb & lt_mask);
+        Q.idx[p] = (uint32_t)i;
+        Q.px[p] = px;
+        Q.py[p] = py;
+        Q.pz[p] = pz;
+    }
+    qn += __popc(qb);
+    if (qn >= 32) {  // warp-uniform: resolve 32 queries, one per lane
+        __syncwarp();
+        sir_resolve(A, Q.idx[lane], Q.px[lane], Q.py[lane], Q.pz[lane], cs, ci, cr, cn);
+        __syncwarp();
+        qn -= 32;
+        if (lane < qn) {
+            Q.idx[lane] = Q.idx[32 + lane];
+            Q.px[lane] = Q.px[32 + lane];
+            Q.py[lane] = Q.py[32 + lane];
+            Q.pz[lane] = Q.pz[32 + lane];
+        }
+        __syncwarp();
+    }
+}
+
+__global__ void __launch_bounds__(kSirThreads, 3) k_sir_update(SirArgs A, DevScalars *__restrict__ sc) {
+    if (sc->overflow) return;
+    __shared__ SirQueue Qs[kSirThreads / 32];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    SirQueue &Q = Qs[wid];
+    const unsigned lt_mask = (1u << lane) - 1u;
+    unsigned long long cs = 0, ci = 0, cr = 0, cn = 0;
+    int qn = 0;  // warp-uniform queue fill
+    const int64_t nwarps = (int64_t)gridDim.x * (kSirThreads / 32);
+    // two 32-agent slices per warp iteration, all their loads issued first
+    for (int64_t i0 = ((int64_t)blockIdx.x * (kSirThreads / 32) + wid) * 64; i0 < A.n; i0 += nwarps * 64) {
+        const int64_t ia = i0 + lane, ib = i0 + 32 + lane;
+        const bool va = ia < A.n, vb = ib < A.n;
+        double xa = 0.0, ya = 0.0, za = 0.0, xb = 0.0, yb = 0.0, zb = 0.0;
+        uint8_t sa = 0, sb = 0;
+        if (va) {
+            xa = A.x[ia];
+            ya = A.y[ia];
+            za = A.z[ia];
+            sa = A.state[ia];
+        }
+        if (vb) {
+            xb = A.x[ib];
+            yb = A.y[ib];
+            zb = A.z[ib];
+            sb = A.state[ib];
+        }
+        sir_agent(A, Q, lane, lt_mask, ia, va, xa, ya, za, sa, qn, cs, ci, cr, cn);
+        sir_agent(A, Q, lane, lt_mask, ib, vb, xb, yb, zb, sb, qn, cs, ci, cr, cn);
+    }
+    __syncwarp();
+    if (lane < qn) sir_resolve(A, Q.idx[lane], Q.px[lane], Q.py[lane], Q.pz[lane], cs, ci, cr, cn);
+    // block reduction of the counters, one atomic each per block
+    __shared__ unsigned long long red[4][kSirThreads / 32];
+    unsigned long long v[4] = {cs, ci, cr, cn};
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
         unsigned long long t = v[q];
@@ -272,7 +361,7 @@ __global__ void __launch_bounds__(256, 3) k_sir_update(SirArgs A, DevScalars *__
     __syncthreads();
     if (threadIdx.x < 4) {
         unsigned long long t = 0;
-        for (int k = 0; k < (int)(blockDim.x >> 5); ++k) t += red[threadIdx.x][k];
+        for (int k = 0; k < kSirThreads / 32; ++k) t += red[threadIdx.x][k];
         if (t) atomicAdd(&A.counts[threadIdx.x], t);
     }
 }
@@ -369,7 +458,7 @@ bdm_status launch_sir_step(Ctx *c, bdm_agents *a, const bdm_params *p, double si
         int64_t ub = (a->n + 255) / 256;
         const int64_t maxb = (int64_t)c->sm_count * 16;
         if (ub > maxb) ub = maxb;
-        k_sir_update<<<(unsigned)ub, 256, 0, st>>>(A, c->sc);
+        k_sir_update<<<(unsigned)ub, kSirThreads, 0, st>>>(A, c->sc);
         c->launches += 2;
         BDM_LAUNCH_CHECK("SIR kernels");
     }
