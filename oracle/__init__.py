@@ -16,6 +16,9 @@ Parity status per function (DESIGN.md section 4 lists the pins):
   neighbor_pairs_*     pinned (brute force on tiny inputs, pure-Python recount)
   mech_step            pinned (Eq. 4.1 closed forms, antisymmetry, cap, static transparency)
   sorted_order         pinned (Morton worked example P:4762-4766, sortedness invariants)
+  diffuse_step         pinned (discrete sine eigenmodes, decay-only, mass conservation,
+                       convergence to the heat kernel at sqrt(1000) um)
+  secrete, chemotaxis  pinned (closed forms: k agents per cell, linear fields)
 """
 from __future__ import annotations
 
@@ -90,6 +93,9 @@ def lib() -> ctypes.CDLL:
         L.orc_sir_step_sample.argtypes = [i64, P, P, P, P, P, dbl, dbl, dbl, dbl, u64,
                                           ctypes.c_uint32, i64, P, P, P, P, P, P]
         L.orc_sir_step_sample.restype = i64
+        L.orc_diffuse_step.argtypes = [i64, i64, i64, P, P, dbl, dbl, dbl, dbl, dbl, dbl]
+        L.orc_secrete.argtypes = [i64, P, P, P, P, i32, dbl, P, i64, i64, i64, P, dbl, dbl, dbl]
+        L.orc_chemotaxis.argtypes = [i64, P, P, P, P, i32, dbl, P, i64, i64, i64, P, dbl, dbl, dbl]
         _lib = L
     return _lib
 
@@ -374,3 +380,61 @@ def sir_step_sample(s, side, radius, p_inf, p_rec, seed, step, sample):
                                    p_inf, p_rec, seed, step, m, _p(idx), _p(out["x"]),
                                    _p(out["y"]), _p(out["z"]), _p(out["state"]), _p(counts))
     return out, counts, ni
+
+
+# ------------------------------------------------------------------ diffusion (row f4)
+class Grid3:
+    """Diffusion grid (reading R34): shape (nz, ny, nx) of cell-centred points, the cell
+    (i, j, k) being [lo + i d, lo + (i+1) d) per axis; values outside are 0."""
+
+    def __init__(self, nx, ny, nz, lo=(0.0, 0.0, 0.0), dx=1.0, dy=None, dz=None):
+        self.nx, self.ny, self.nz = int(nx), int(ny), int(nz)
+        self.lo = np.ascontiguousarray(lo, np.float64)
+        self.dx = float(dx)
+        self.dy = float(dx if dy is None else dy)
+        self.dz = float(dx if dz is None else dz)
+
+
+def diffuse(u, g, nu, mu, dt, steps=1):
+    """Eq. 4.3, `steps` explicit steps of the (nz, ny, nx) array u (R35)."""
+    a = np.ascontiguousarray(u, np.float64).copy()
+    b = np.empty_like(a)
+    for _ in range(steps):
+        lib().orc_diffuse_step(g.nx, g.ny, g.nz, _p(a), _p(b), nu, mu, dt, g.dx, g.dy, g.dz)
+        a, b = b, a
+    return a
+
+
+def secrete(s, type_, type_sel, q, u, g):
+    """Alg. secretion_module into a copy of u (R36)."""
+    out = np.ascontiguousarray(u, np.float64).copy()
+    x, y, z = _f64(s["x"]), _f64(s["y"]), _f64(s["z"])
+    t = np.ascontiguousarray(type_, np.uint8)
+    lib().orc_secrete(len(x), _p(x), _p(y), _p(z), _p(t), int(type_sel), q, _p(out), g.nx, g.ny,
+                      g.nz, _p(g.lo), g.dx, g.dy, g.dz)
+    return out
+
+
+def chemotaxis(s, type_, type_sel, weight, u, g):
+    """Alg. chemotaxis_module on a copy of the positions (R37, R38)."""
+    out = {k: np.array(v, copy=True) for k, v in s.items()}
+    for k in ("x", "y", "z"):
+        out[k] = np.ascontiguousarray(out[k], np.float64)
+    t = np.ascontiguousarray(type_, np.uint8)
+    uu = np.ascontiguousarray(u, np.float64)
+    lib().orc_chemotaxis(len(out["x"]), _p(out["x"]), _p(out["y"]), _p(out["z"]), _p(t),
+                         int(type_sel), weight, _p(uu), g.nx, g.ny, g.nz, _p(g.lo), g.dx, g.dy,
+                         g.dz)
+    return out
+
+
+def soma_step(s, type_, grids, g, nu, mu, dt, q, weight):
+    """One soma-clustering step (reading R39): secretion of every type into
+    its own substance, chemotaxis of every type up its substance's gradient, then one
+    diffusion step (Eq. 4.3) of every substance.  Returns (new positions, new grids)."""
+    gs = [secrete(s, type_, t, q, grids[t], g) for t in range(len(grids))]
+    out = dict(s)
+    for t in range(len(grids)):
+        out = chemotaxis(out, type_, t, weight, gs[t], g)
+    gs = [diffuse(u, g, nu, mu, dt, 1) for u in gs]
+    return out, gs

@@ -842,3 +842,96 @@ void orc_init_sir(int64_t n, uint64_t seed, double side, int64_t n_infected, dou
         state[k] = (k < n_infected) ? ORC_I : ORC_S;
     }
 }
+
+/* ------------------------------------------------------------------------------ */
+/* Extracellular diffusion, secretion and chemotaxis.         */
+/* Grid (reading R34): nx*ny*nz points, point (i,j,k) stored at i + nx*(j + ny*k); */
+/* point (i,j,k) is the centre of the cell [lo + i*dx, lo + (i+1)*dx) x ... and    */
+/* values outside the grid are 0: "substances diffuse out of the simulation        */
+/* space".                                                           */
+/* ------------------------------------------------------------------------------ */
+static double grid_at(const double *u, int64_t nx, int64_t ny, int64_t nz, int64_t i, int64_t j,
+                      int64_t k)
+{
+    if (i < 0 || j < 0 || k < 0 || i >= nx || j >= ny || k >= nz) return 0.0;
+    return u[i + nx * (j + ny * k)];
+}
+
+/* Eq. 4.3 (eq:centraldiff), one explicit step from u to out (distinct
+ * arrays).  Reading R35 fixes the operation order: the decay factor 1 - mu*dt and the
+ * coefficients nu*dt / (dx*dx) are computed once; per point
+ *   v = u*(1 - mu dt);  v = v + cx*((u_{i+1} - 2u) + u_{i-1});  then the y and z terms,
+ * each second difference left to right, no fused multiply-add. */
+void orc_diffuse_step(int64_t nx, int64_t ny, int64_t nz, const double *u, double *out, double nu,
+                      double mu, double dt, double dx, double dy, double dz)
+{
+    const double decay = 1.0 - mu * dt;
+    const double cx = (nu * dt) / (dx * dx);
+    const double cy = (nu * dt) / (dy * dy);
+    const double cz = (nu * dt) / (dz * dz);
+    for (int64_t k = 0; k < nz; ++k)
+        for (int64_t j = 0; j < ny; ++j)
+            for (int64_t i = 0; i < nx; ++i) {
+                const double c = u[i + nx * (j + ny * k)];
+                double v = c * decay;
+                v = v + cx * ((grid_at(u, nx, ny, nz, i + 1, j, k) - 2.0 * c) +
+                              grid_at(u, nx, ny, nz, i - 1, j, k));
+                v = v + cy * ((grid_at(u, nx, ny, nz, i, j + 1, k) - 2.0 * c) +
+                              grid_at(u, nx, ny, nz, i, j - 1, k));
+                v = v + cz * ((grid_at(u, nx, ny, nz, i, j, k + 1) - 2.0 * c) +
+                              grid_at(u, nx, ny, nz, i, j, k - 1));
+                out[i + nx * (j + ny * k)] = v;
+            }
+}
+
+/* The cell containing a position (reading R36): floor((p - lo)/d), clamped to the grid. */
+static int64_t grid_cell(double p, double lo, double d, int64_t n)
+{
+    double b = floor((p - lo) / d);
+    if (b < 0.0) b = 0.0;
+    if (b > (double)(n - 1)) b = (double)(n - 1);
+    return (int64_t)b;
+}
+
+/* Alg. secretion_module: every agent of the selected type adds q to the
+ * cell containing its position, agents in index order (R36).  For a constant q the
+ * result does not depend on the order (every partial sum adds the same q). */
+void orc_secrete(int64_t n, const double *x, const double *y, const double *z, const uint8_t *type,
+                 int type_sel, double q, double *u, int64_t nx, int64_t ny, int64_t nz,
+                 const double lo[3], double dx, double dy, double dz)
+{
+    for (int64_t a = 0; a < n; ++a) {
+        if ((int)type[a] != type_sel) continue;
+        const int64_t i = grid_cell(x[a], lo[0], dx, nx), j = grid_cell(y[a], lo[1], dy, ny),
+                      k = grid_cell(z[a], lo[2], dz, nz);
+        u[i + nx * (j + ny * k)] = u[i + nx * (j + ny * k)] + q;
+    }
+}
+
+/* Alg. chemotaxis_module: agents of the selected type move by
+ * weight * GetNormalizedGradient(pos).  Reading R37: the gradient is the central
+ * difference at the cell of pos, g_a = (u_{+1} - u_{-1}) / (2 d_a) (outside = 0),
+ * normalized as g / sqrt((gx*gx + gy*gy) + gz*gz) (zero gradient -> no move); R38:
+ * p_a = p_a + weight * g_a. */
+void orc_chemotaxis(int64_t n, double *x, double *y, double *z, const uint8_t *type, int type_sel,
+                    double weight, const double *u, int64_t nx, int64_t ny, int64_t nz,
+                    const double lo[3], double dx, double dy, double dz)
+{
+    for (int64_t a = 0; a < n; ++a) {
+        if ((int)type[a] != type_sel) continue;
+        const int64_t i = grid_cell(x[a], lo[0], dx, nx), j = grid_cell(y[a], lo[1], dy, ny),
+                      k = grid_cell(z[a], lo[2], dz, nz);
+        const double gx = (grid_at(u, nx, ny, nz, i + 1, j, k) - grid_at(u, nx, ny, nz, i - 1, j, k)) /
+                          (2.0 * dx);
+        const double gy = (grid_at(u, nx, ny, nz, i, j + 1, k) - grid_at(u, nx, ny, nz, i, j - 1, k)) /
+                          (2.0 * dy);
+        const double gz = (grid_at(u, nx, ny, nz, i, j, k + 1) - grid_at(u, nx, ny, nz, i, j, k - 1)) /
+                          (2.0 * dz);
+        const double n2 = gx * gx + gy * gy + gz * gz;
+        if (!(n2 > 0.0)) continue;
+        const double nrm = sqrt(n2);
+        x[a] = x[a] + weight * (gx / nrm);
+        y[a] = y[a] + weight * (gy / nrm);
+        z[a] = z[a] + weight * (gz / nrm);
+    }
+}
