@@ -181,6 +181,8 @@ def run_ours(args, ws, rank, local):
         return run_cfg3(args, ws, rank, local)
     if args.config == "cfg4":
         return run_cfg4(args, ws, rank, local)
+    if args.config == "soma":
+        return run_soma(args, ws, rank, local)
     torch.cuda.set_device(local)
     cfg = W.PRESETS[args.config]
     eng = Engine(local, cfg.n)
@@ -393,6 +395,74 @@ def run_cfg4(args, ws, rank, local):
                         "achieved": ach / 1e9, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                         "frac": ach / (peaks["hbm_gbs"] * 1e9), "traffic": None,
                         "peak_source": src, "alg_bytes_per_agent": 50}
+    print(json.dumps(line), flush=True)
+
+
+def run_soma(args, ws, rank, local):
+    """soma clustering steps (secretion, chemotaxis, Eq. 4.3 diffusion
+    of two substances on res^3 fp64 grids).  The stencil kernel is HBM-bound: 8 B read +
+    8 B written per grid point and step."""
+    import torch
+    from paper_2503_10796_b200 import Agents, CGrid3, Engine
+    torch.cuda.set_device(local)
+    cfg = W.SOMA
+    eng = Engine(local, cfg.n)
+    a = Agents.empty(cfg.n)
+    stream = torch.cuda.Stream()
+    eng.init_spheres(a, cfg.n, seed=cfg.seed, side=cfg.side, d_lo=cfg.d, stream=stream)
+    ttype = (torch.arange(cfg.n, device="cuda") % 2).to(torch.uint8)
+    r = cfg.res
+    dx = cfg.side / r
+    grid = CGrid3.make(r, r, r, (0.0, 0.0, 0.0), dx)
+    grids = [torch.zeros((r, r, r), dtype=torch.float64, device="cuda") for _ in range(2)]
+    spares = [torch.zeros_like(grids[0]) for _ in range(2)]
+    torch.cuda.synchronize()
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            grids, spares = eng.soma_step(a, ttype, grids, spares, grid, cfg.nu, cfg.mu, cfg.dt,
+                                          cfg.q, cfg.weight, stream=stream)
+    K = args.steps
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+           torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    launches0 = eng.stats()["launches"]
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for k in range(K):
+            e0, e1, e2 = ev[k]
+            e0.record(stream)
+            for t, u in enumerate(grids):
+                eng.secrete(a, ttype, t, cfg.q, u, grid, stream)
+            for t, u in enumerate(grids):
+                eng.chemotaxis(a, ttype, t, cfg.weight, u, grid, stream)
+            e1.record(stream)
+            for u, v in zip(grids, spares):
+                eng.diffuse(u, v, grid, cfg.nu, cfg.mu, cfg.dt, stream)
+            e2.record(stream)
+            grids, spares = spares, grids
+        torch.cuda.synchronize()
+    ms = [ev[k][0].elapsed_time(ev[k][2]) for k in range(K)]
+    dms = [ev[k][1].elapsed_time(ev[k][2]) for k in range(K)]
+    ms_step = statistics.mean(ms)
+    points = 2 * r ** 3
+    peaks, src = _peaks()
+    d_s = statistics.mean(dms) * 1e-3 / 2          # one substance's k_diffuse launch
+    ach = 16.0 * r ** 3 / d_s
+    line = {
+        "metric": "grid-point updates/s (Eq. 4.3 diffusion, soma clustering; SURVEY 8(f) f4)",
+        "value": points / (ms_step * 1e-3), "unit": "point-updates/s", "n_gpus": ws,
+        "steps": K, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "soma clustering (SURVEY 8(f) row f4)", **cfg.to_dict(),
+                   "substances": 2, "grid_points": points,
+                   "agent_updates_per_s": cfg.n / (ms_step * 1e-3),
+                   "l2": "grids (1 GiB each) larger than L2; no flush"},
+        "roofline": {"bound": "hbm", "kernel": "k_diffuse (one substance, one step)",
+                     "achieved": ach / 1e9, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                     "frac": ach / (peaks["hbm_gbs"] * 1e9), "traffic": None,
+                     "peak_source": src, "alg_bytes_per_point": 16,
+                     "diffuse_ms": statistics.mean(dms) / 2},
+        "clocks": clk.summary(), "gpu_launches": eng.stats()["launches"] - launches0,
+    }
     print(json.dumps(line), flush=True)
 
 

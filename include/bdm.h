@@ -101,6 +101,16 @@ typedef struct {
     int64_t slot_capacity;   /* allocated slots                                       */
 } bdm_grid_info;
 
+/* Diffusion grid (reading R34): nx*ny*nz points of a substance,
+ * fp64, point (i,j,k) stored at index i + nx*(j + ny*k) (x fastest), the centre of the
+ * cell [lo + i*dx, lo + (i+1)*dx) x [..dy..) x [..dz..).  Values outside the grid are 0
+ * ("substances diffuse out of the simulation space"). */
+typedef struct {
+    int64_t nx, ny, nz;      /* points per axis (nx*ny < 2^31, nz < 2^31)             */
+    double lo[3];            /* lower corner of cell (0,0,0)                          */
+    double dx, dy, dz;       /* cell edge per axis (> 0)                              */
+} bdm_grid3;
+
 typedef struct bdm_ctx *bdm_handle;
 
 /* Create a library context on CUDA device `device` with workspace for up to
@@ -212,6 +222,35 @@ bdm_status bdm_sir_step(bdm_handle h, bdm_agents *a, const bdm_params *p, double
                         double radius, double p_inf, double p_rec, int64_t *counts_host,
                         void *stream);
 
+/* ---- extracellular diffusion, secretion, chemotaxis -------- */
+
+/* Eq. 4.3 (eq:centraldiff): one explicit step from the device grid u_in to
+ * u_out (layout bdm_grid3; distinct buffers, the caller alternates them over steps).
+ * Per point, in this order and without fused multiply-add (R35):
+ *   v = u*(1 - mu*dt)
+ *   v = v + cx*((u[i+1] - 2u) + u[i-1]),  cx = (nu*dt)/(dx*dx); then the y and z terms,
+ * with 0 for neighbours outside the grid (R34).  The explicit scheme is stable for
+ * 2(cx + cy + cz) <= 1 - mu*dt; the call does not check it.  Asynchronous on stream.
+ * Errors: BDM_EINVAL (NULL pointers, u_in == u_out, non-positive spacing). */
+bdm_status bdm_diffuse(bdm_handle h, const double *u_in, double *u_out, const bdm_grid3 *g,
+                       double nu, double mu, double dt, void *stream);
+
+/* Alg. secretion_module: every agent i < a->n with type[i] == type_sel adds
+ * q to the grid point of the cell containing (x, y, z)_i; cells are floor((p - lo)/d),
+ * clamped to the grid (R36).  type is a device u8 array of a->n entries.  The result is
+ * independent of the order of the additions because every addend is the same q.
+ * Errors: BDM_EINVAL. */
+bdm_status bdm_secrete(bdm_handle h, const bdm_agents *a, const uint8_t *type, int32_t type_sel,
+                       double q, double *u, const bdm_grid3 *g, void *stream);
+
+/* Alg. chemotaxis_module: every agent with type[i] == type_sel moves, in
+ * place, by weight * GetNormalizedGradient: the central difference at its cell,
+ * g_a = (u[+1] - u[-1]) / (2 d_a) with 0 outside the grid (R37), divided by
+ * sqrt((gx*gx + gy*gy) + gz*gz) (no move for a zero gradient); p_a = p_a + weight*g_a
+ * (R38).  Only x, y, z are read and written.  Errors: BDM_EINVAL. */
+bdm_status bdm_chemotaxis(bdm_handle h, bdm_agents *a, const uint8_t *type, int32_t type_sel,
+                          double weight, const double *u, const bdm_grid3 *g, void *stream);
+
 /* ---- multi-GPU x-slabs (TeraAgent partitioning P:6058-6081, aura
  * P:6083-6106, migration P:6116-6126).  The transport between ranks is the
  * caller's (torch.distributed over NCCL in paper_2503_10796_b200/slabs.py); these
@@ -280,6 +319,8 @@ bdm_status bdm_neighbor_pairs(bdm_handle h, const bdm_agents *a, double radius,
  *   "dense"        1 (default) / 0: regions too crowded for the tile kernel's shared-memory
  *                  staging (> 416 agents in a 6^3-box region) go to the dense-box kernel
  *                  (warp per box, broadcast candidate stream); 0: reference formulation.
+ *   "diffuse_tma"  1 (default) / 0: bdm_diffuse streams the grid planes with TMA box loads
+ *                  (nx even); 0, or nx odd: the register/shared-memory stencil kernel.
  *   "prefilter"    1 (default) / 0: conservative fp32 candidate test in the tile kernel
  *                  (never rejects a neighbour; the exact fp64 test decides).
  *   "fuse_reduce"  0 (default) / 1: bdm_mech_step also reduces the extent of the new

@@ -25,7 +25,7 @@ EXPORTS = [
     "bdm_grid_build", "bdm_mech_step", "bdm_step", "bdm_step_host", "bdm_sync", "bdm_reserve",
     "bdm_get_stats", "bdm_get_grid_info", "bdm_neighbor_pairs", "bdm_peak_dfma",
     "bdm_set_option", "bdm_grow_divide", "bdm_sir_step", "bdm_local_frame", "bdm_set_frame",
-    "bdm_pack_slab", "bdm_append",
+    "bdm_pack_slab", "bdm_append", "bdm_diffuse", "bdm_secrete", "bdm_chemotaxis",
 ]
 PACK_MIGRATE, PACK_AURA = 1, 2
 
@@ -58,6 +58,23 @@ class CParams(ctypes.Structure):
 class CStats(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int64) for n in ("cand", "nbr", "cont", "n_static", "n_moved",
                                               "launches")]
+
+
+class CGrid3(ctypes.Structure):
+    """bdm_grid3: the diffusion grid (R34); u is a (nz, ny, nx) float64 device tensor."""
+    _fields_ = [("nx", ctypes.c_int64), ("ny", ctypes.c_int64), ("nz", ctypes.c_int64),
+                ("lo", ctypes.c_double * 3), ("dx", ctypes.c_double), ("dy", ctypes.c_double),
+                ("dz", ctypes.c_double)]
+
+    @staticmethod
+    def make(nx, ny, nz, lo=(0.0, 0.0, 0.0), dx=1.0, dy=None, dz=None) -> "CGrid3":
+        g = CGrid3()
+        g.nx, g.ny, g.nz = int(nx), int(ny), int(nz)
+        g.lo = (ctypes.c_double * 3)(*[float(v) for v in lo])
+        g.dx = float(dx)
+        g.dy = float(dx if dy is None else dy)
+        g.dz = float(dx if dz is None else dz)
+        return g
 
 
 class CGridInfo(ctypes.Structure):
@@ -104,6 +121,9 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "bdm_set_frame": [P, P],
         "bdm_pack_slab": [P, AG, dbl, dbl, dbl, i32, AG, AG, P, P],
         "bdm_append": [P, AG, AG, P],
+        "bdm_diffuse": [P, P, P, ctypes.POINTER(CGrid3), dbl, dbl, dbl, P],
+        "bdm_secrete": [P, AG, P, i32, dbl, P, ctypes.POINTER(CGrid3), P],
+        "bdm_chemotaxis": [P, AG, P, i32, dbl, P, ctypes.POINTER(CGrid3), P],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -378,6 +398,43 @@ class Engine:
             _check(st)
             return [int(v) for v in self._sir_counts]
         return None
+
+    # ---------------------------------------------------------------- row f4
+    def diffuse(self, u_in, u_out, grid: CGrid3, nu: float, mu: float, dt: float, stream=None):
+        """bdm_diffuse: one Eq. 4.3 step from the (nz, ny, nx) float64 tensor u_in to
+        u_out (distinct)."""
+        _check(self.lib.bdm_diffuse(self.h, _ptr(u_in), _ptr(u_out), ctypes.byref(grid),
+                                    float(nu), float(mu), float(dt), _stream_ptr(stream)))
+
+    def secrete(self, agents: Agents, type_, type_sel: int, q: float, u, grid: CGrid3,
+                stream=None):
+        """bdm_secrete: agents of type type_sel add q to the cell of their position."""
+        ca = agents.c()
+        _check(self.lib.bdm_secrete(self.h, ctypes.byref(ca), _ptr(type_), int(type_sel),
+                                    float(q), _ptr(u), ctypes.byref(grid), _stream_ptr(stream)))
+
+    def chemotaxis(self, agents: Agents, type_, type_sel: int, weight: float, u, grid: CGrid3,
+                   stream=None):
+        """bdm_chemotaxis: agents of type type_sel move by weight x the normalized
+        gradient of u at their cell."""
+        ca = agents.c()
+        _check(self.lib.bdm_chemotaxis(self.h, ctypes.byref(ca), _ptr(type_), int(type_sel),
+                                       float(weight), _ptr(u), ctypes.byref(grid),
+                                       _stream_ptr(stream)))
+
+    def soma_step(self, agents: Agents, type_, grids, spares, grid: CGrid3, nu: float,
+                  mu: float, dt: float, q: float, weight: float, stream=None):
+        """One soma-clustering step (reading R39): secretion of every type
+        into its own substance, chemotaxis of every type, one diffusion step of every
+        substance from grids[t] into spares[t].  Returns (grids, spares) swapped: the new
+        concentrations and the buffers free for the next step."""
+        for t, u in enumerate(grids):
+            self.secrete(agents, type_, t, q, u, grid, stream)
+        for t, u in enumerate(grids):
+            self.chemotaxis(agents, type_, t, weight, u, grid, stream)
+        for u, v in zip(grids, spares):
+            self.diffuse(u, v, grid, nu, mu, dt, stream)
+        return list(spares), list(grids)
 
     def cfg3_step(self, agents: Agents, params: Params, growth: float, v_max: float,
                   stream=None) -> int:

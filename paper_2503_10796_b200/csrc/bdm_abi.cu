@@ -338,6 +338,52 @@ bdm_status bdm_sir_step(bdm_handle h, bdm_agents *a, const bdm_params *p, double
                            (cudaStream_t)stream);
 }
 
+static bdm_status check_grid3(const bdm_grid3 *g) {
+    if (!g) return fail(BDM_EINVAL, "grid is NULL");
+    if (g->nx < 0 || g->ny < 0 || g->nz < 0) return fail(BDM_EINVAL, "negative grid size");
+    if (g->nx * g->ny >= (1ll << 31) || g->nz >= (1ll << 31))
+        return fail(BDM_EINVAL, "grid too large (nx*ny and nz must be < 2^31)");
+    if (!(g->dx > 0.0) || !(g->dy > 0.0) || !(g->dz > 0.0))
+        return fail(BDM_EINVAL, "grid spacing must be > 0");
+    return BDM_OK;
+}
+
+bdm_status bdm_diffuse(bdm_handle h, const double *u_in, double *u_out, const bdm_grid3 *g,
+                       double nu, double mu, double dt, void *stream) {
+    if (!h) return fail(BDM_EINVAL, "handle is NULL");
+    bdm_status s = check_grid3(g);
+    if (s != BDM_OK) return s;
+    if (g->nx * g->ny * g->nz > 0 && (!u_in || !u_out || u_in == u_out))
+        return fail(BDM_EINVAL, "u_in and u_out must be distinct device buffers");
+    return launch_diffuse((Ctx *)h, u_in, u_out, g, nu, mu, dt, (cudaStream_t)stream);
+}
+
+bdm_status bdm_secrete(bdm_handle h, const bdm_agents *a, const uint8_t *type, int32_t type_sel,
+                       double q, double *u, const bdm_grid3 *g, void *stream) {
+    if (!h || !a) return fail(BDM_EINVAL, "NULL argument");
+    bdm_status s = check_grid3(g);
+    if (s != BDM_OK) return s;
+    if (a->n < 0 || a->n > a->capacity) return fail(BDM_EINVAL, "n < 0 or n > capacity");
+    if (a->n > 0 && (!a->x || !a->y || !a->z || !type || !u))
+        return fail(BDM_EINVAL, "secretion needs x, y, z, type and the grid");
+    if (g->nx * g->ny * g->nz == 0 && a->n > 0) return fail(BDM_EINVAL, "empty grid");
+    return launch_secrete((Ctx *)h, a, type, type_sel, q, u, g, (cudaStream_t)stream);
+}
+
+bdm_status bdm_chemotaxis(bdm_handle h, bdm_agents *a, const uint8_t *type, int32_t type_sel,
+                          double weight, const double *u, const bdm_grid3 *g, void *stream) {
+    if (h) ((Ctx *)h)->fused_valid = false;
+    if (!h || !a) return fail(BDM_EINVAL, "NULL argument");
+    bdm_status s = check_grid3(g);
+    if (s != BDM_OK) return s;
+    if (a->n < 0 || a->n > a->capacity) return fail(BDM_EINVAL, "n < 0 or n > capacity");
+    if (a->n > 0 && (!a->x || !a->y || !a->z || !type || !u))
+        return fail(BDM_EINVAL, "chemotaxis needs x, y, z, type and the grid");
+    if (g->nx * g->ny * g->nz == 0 && a->n > 0) return fail(BDM_EINVAL, "empty grid");
+    ((Ctx *)h)->grid_valid = false;
+    return launch_chemotaxis((Ctx *)h, a, type, type_sel, weight, u, g, (cudaStream_t)stream);
+}
+
 bdm_status bdm_local_frame(bdm_handle h, const bdm_agents *a, double *frame_dev, void *stream) {
     if (!h || !a || !frame_dev) return fail(BDM_EINVAL, "NULL argument");
     bdm_status s = check_agents(a, true);
@@ -474,6 +520,11 @@ bdm_status bdm_set_option(bdm_handle h, const char *name, int64_t value) {
         if (value < 0 || value > 1) return fail(BDM_EINVAL, "fuse_reduce must be 0 or 1");
         c->fuse_reduce = (int)value;
         c->fused_valid = false;
+        return BDM_OK;
+    }
+    if (strcmp(name, "diffuse_tma") == 0) {
+        if (value < 0 || value > 1) return fail(BDM_EINVAL, "diffuse_tma must be 0 or 1");
+        c->diffuse_tma = (int)value;
         return BDM_OK;
     }
     if (strcmp(name, "dense") == 0) {

@@ -101,6 +101,7 @@ struct Ctx {
     int prefilter = 1;     // option "prefilter": fp32 conservative candidate test in the tile kernel
     int fuse_reduce = 0;   // option "fuse_reduce": next step's a1 extent from the mech epilogue
     int dense = 1;         // option "dense": dense regions go to the dense-box kernel
+    int diffuse_tma = 1;   // option "diffuse_tma": TMA-pipelined stencil when nx is even
     bool fused_valid = false;          // the scalars hold the extent of (fused_x, fused_n)
     const double *fused_x = nullptr;
     int64_t fused_n = 0;
@@ -180,6 +181,13 @@ bdm_status launch_scan_u32(Ctx *c, uint32_t *data, long long m, cudaStream_t st)
 // SIR (kernels_sir.cu)
 bdm_status launch_sir_step(Ctx *c, bdm_agents *a, const bdm_params *p, double side, double radius,
                            double p_inf, double p_rec, long long *counts_host, cudaStream_t st);
+// diffusion, secretion, chemotaxis (kernels_diffusion.cu)
+bdm_status launch_diffuse(Ctx *c, const double *u_in, double *u_out, const bdm_grid3 *g,
+                          double nu, double mu, double dt, cudaStream_t st);
+bdm_status launch_secrete(Ctx *c, const bdm_agents *a, const uint8_t *type, int type_sel, double q,
+                          double *u, const bdm_grid3 *g, cudaStream_t st);
+bdm_status launch_chemotaxis(Ctx *c, bdm_agents *a, const uint8_t *type, int type_sel,
+                             double weight, const double *u, const bdm_grid3 *g, cudaStream_t st);
 // growth + division (kernels_divide.cu)
 bdm_status launch_grow_divide(Ctx *c, bdm_agents *a, double growth, double v_max, double vol_to_r3,
                               uint64_t seed, uint32_t step, long long *n_new_host, cudaStream_t st);

@@ -94,4 +94,28 @@ def cfg4_scaled(n: int, side: float = None) -> SirConfig:
     return SirConfig(f"cfg4@{n}", n, side, 2.0, 0.1, 0.01, max(1, n // 1000), 200)
 
 
-PRESETS = {"cfg1": CFG1, "cfg2": CFG2, "cfg3": CFG3, "cfg4": CFG4, "cfg5": CFG5}
+@dataclass(frozen=True)
+class SomaConfig:
+    """SURVEY 8(f) row f4 (not one of BASELINE.json's configs): soma clustering
+    (Algs. secretion_module / chemotaxis_module) with Eq. 4.3 diffusion.
+    The paper's benchmark has 32k agents; its grid resolution, nu, mu and
+    dt are not given, so the grid is chosen to make the stencil the measured kernel."""
+    name: str
+    n: int            # agents, type = id % 2
+    side: float       # agents and grid cover [0, side)^3 um
+    res: int          # grid points per axis (per substance)
+    nu: float         # diffusion coefficient, um^2/s
+    mu: float         # decay constant, 1/s
+    dt: float         # s; 2 (cx+cy+cz) = 6 nu dt / dx^2 <= 1 - mu dt (explicit stability)
+    q: float          # secretion_quantity (P:3517-3518)
+    weight: float     # gradient_weight (P:3517-3518)
+    d: float          # diameter (mechanics is not part of this step)
+    seed: int = 1
+
+    def to_dict(self):
+        return asdict(self)
+
+
+SOMA = SomaConfig("soma", 32_768, 1000.0, 512, 1.0, 0.01, 0.5, 1.0, 0.75, 10.0)
+
+PRESETS = {"cfg1": CFG1, "cfg2": CFG2, "cfg3": CFG3, "cfg4": CFG4, "cfg5": CFG5, "soma": SOMA}
