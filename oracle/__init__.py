@@ -19,6 +19,9 @@ Parity status per function (DESIGN.md section 4 lists the pins):
   diffuse_step         pinned (discrete sine eigenmodes, decay-only, mass conservation,
                        convergence to the heat kernel at sqrt(1000) um)
   secrete, chemotaxis  pinned (closed forms: k agents per cell, linear fields)
+  onco_step            pinned (unit Brownian steps, exact age/volume bookkeeping, the
+                       age gate, death / division frequencies within 5 sigma, removal
+                       invariants, id uniqueness, population accounting)
 """
 from __future__ import annotations
 
@@ -94,6 +97,9 @@ def lib() -> ctypes.CDLL:
                                           ctypes.c_uint32, i64, P, P, P, P, P, P]
         L.orc_sir_step_sample.restype = i64
         L.orc_diffuse_step.argtypes = [i64, i64, i64, P, P, dbl, dbl, dbl, dbl, dbl, dbl]
+        L.orc_onco_step.argtypes = [i64, P, P, P, P, P, P, P, P, i64, P, P]
+        L.orc_onco_step.restype = i64
+        L.orc_init_ages.argtypes = [i64, P, u64, ctypes.c_uint32, P]
         L.orc_secrete.argtypes = [i64, P, P, P, P, i32, dbl, P, i64, i64, i64, P, dbl, dbl, dbl]
         L.orc_chemotaxis.argtypes = [i64, P, P, P, P, i32, dbl, P, i64, i64, i64, P, dbl, dbl, dbl]
         _lib = L
@@ -438,3 +444,63 @@ def soma_step(s, type_, grids, g, nu, mu, dt, q, weight):
         out = chemotaxis(out, type_, t, weight, gs[t], g)
     gs = [diffuse(u, g, nu, mu, dt, 1) for u in gs]
     return out, gs
+
+
+# ------------------------------------------------------------------ oncology (row f2)
+class OncoParams(ctypes.Structure):
+    """Mirror of orc_onco_params (oracle.c): Alg. 4 with Table 4.2's parameters."""
+    _fields_ = [("displacement_rate", ctypes.c_double), ("growth", ctypes.c_double),
+                ("max_diameter", ctypes.c_double), ("p_death", ctypes.c_double),
+                ("p_div", ctypes.c_double), ("min_age", ctypes.c_uint32),
+                ("seed", ctypes.c_uint64), ("step", ctypes.c_uint32)]
+
+
+def onco_params(displacement_rate=0.005, growth=42.0, max_diameter=14.0, p_death=0.033,
+                p_div=0.0215, min_age=87, seed=1, step=0) -> OncoParams:
+    return OncoParams(displacement_rate, growth, max_diameter, p_death, p_div, min_age, seed,
+                      step)
+
+
+def init_ages(ids, seed, max_age):
+    """Initial ages (reading R44): floor(u32 * max_age) from Philox (id, 0xFFFFFFFC, 2)."""
+    ids = _u32(ids)
+    out = np.zeros(len(ids), np.uint32)
+    lib().orc_init_ages(len(ids), _p(ids), seed, max_age, _p(out))
+    return out
+
+
+def onco_step(s, p: OncoParams, id_next: int):
+    """Alg. 4 + removal (R41-R45) on a copy of s (x, y, z, d, vol, id, flags, age, all
+    post-mechanics); returns (new state, new id_next)."""
+    n = len(s["x"])
+    cap = 2 * n + 1
+    out = {}
+    for k in ("x", "y", "z", "d", "vol"):
+        a = np.zeros(cap, np.float64)
+        a[:n] = s[k]
+        out[k] = a
+    for k in ("id", "flags", "age"):
+        a = np.zeros(cap, np.uint32)
+        a[:n] = s[k]
+        out[k] = a
+    nxt = ctypes.c_int64(int(id_next))
+    r = lib().orc_onco_step(n, _p(out["x"]), _p(out["y"]), _p(out["z"]), _p(out["d"]),
+                            _p(out["vol"]), _p(out["id"]), _p(out["flags"]), _p(out["age"]),
+                            cap, ctypes.byref(p), ctypes.byref(nxt))
+    assert r >= 0, r
+    return {k: v[:r] for k, v in out.items()}, int(nxt.value)
+
+
+def onco_full_step(s, mp: MechParams, p: OncoParams, id_next: int):
+    """One oncology step (R40): mechanics on the snapshot, then Alg. 4 + removal at the
+    post-mechanics state.  s carries x, y, z, d, vol, id, flags, age in any order; the
+    mechanics leaves the grid's (box, id) order, then removal keeps it and daughters
+    follow.  Returns (new state, mechanics counters, new id_next)."""
+    out, cnt = mech_step(s, mp)
+    perm, _ = sorted_order(s, mp.radius)
+    post = {"x": out["x"][perm], "y": out["y"][perm], "z": out["z"][perm],
+            "d": np.asarray(s["d"], np.float64)[perm], "id": np.asarray(s["id"], np.uint32)[perm],
+            "flags": out["flags"][perm], "vol": np.asarray(s["vol"], np.float64)[perm],
+            "age": np.asarray(s["age"], np.uint32)[perm]}
+    new, nxt = onco_step(post, p, id_next)
+    return new, cnt, nxt

@@ -935,3 +935,141 @@ void orc_chemotaxis(int64_t n, double *x, double *y, double *z, const uint8_t *t
         z[a] = z[a] + weight * (gz / nrm);
     }
 }
+
+/* ------------------------------------------------------------------------------ */
+/* Oncology behaviour + agent removal.                          */
+/* Alg. 4 (algo:tumor_growth_module) with the Table 4.2 parameters     */
+/* and the parallel removal of sec. "Agent addition and removal"     */
+/* (P:4545-4603).  Readings:                                             */
+/*   R41  brownian = v / |v| with v = 2 u32(w0..w2) - 1 (a unit vector, not a cap);   */
+/*        v = 0 -> no move; pos += brownian * displacement_rate                      */
+/*   R42  Philox counter (id, step, 5): w0..w2 movement, w3 death;                    */
+/*        (id, step, 6): w0 division; division axis as R13 (streams 3 + 4k)          */
+/*   R43  growth as R28 (V += growth, d = 2 cbrt_det(V 0.75/pi)), division as R13      */
+/*        (V/2 each, touching daughters, mother MOVED, daughter ADDED with age 0)     */
+/*   R45  removal keeps the survivors' order; daughters follow the survivors in       */
+/*        mother-id order with ids id_next + rank; ids are never reused               */
+/* One pass in ascending id over agents carrying their post-mechanics state.         */
+/* ------------------------------------------------------------------------------ */
+typedef struct {
+    double displacement_rate, growth, max_diameter, p_death, p_div;
+    uint32_t min_age;
+    uint64_t seed;
+    uint32_t step;
+} orc_onco_params;
+
+
+
+/* Returns the new agent count (or -(required capacity) and leaves everything unchanged);
+ * *id_next is advanced by the number of daughters. */
+int64_t orc_onco_step(int64_t n, double *x, double *y, double *z, double *d, double *vol,
+                      uint32_t *id, uint32_t *flags, uint32_t *age, int64_t capacity,
+                      const orc_onco_params *p, int64_t *id_next)
+{
+    const double C = 0.75 / M_PI;
+    /* ascending id order (ids are unique but not dense after removals) */
+    orc_kv *kv = (orc_kv *)malloc(sizeof(orc_kv) * (size_t)(n > 0 ? n : 1));
+    for (int64_t i = 0; i < n; ++i) { kv[i].key = (int64_t)id[i]; kv[i].idx = i; }
+    qsort(kv, (size_t)n, sizeof(orc_kv), cmp_kv);
+    int64_t *ord = (int64_t *)malloc(sizeof(int64_t) * (size_t)(n > 0 ? n : 1));
+    for (int64_t i = 0; i < n; ++i) ord[i] = kv[i].idx;
+    free(kv);
+    uint8_t *dead = (uint8_t *)calloc((size_t)(n > 0 ? n : 1), 1);
+    uint8_t *div = (uint8_t *)calloc((size_t)(n > 0 ? n : 1), 1);
+    int64_t ndiv = 0, ndead = 0;
+    /* first decide (draws only; nothing is modified before the capacity check) */
+    for (int64_t k = 0; k < n; ++k) {
+        int64_t i = ord[k];
+        uint32_t w[4];
+        philox_draw(p->seed, id[i], p->step, 5u, w);
+        if (age[i] >= p->min_age && orc_u32(w[3]) < p->p_death) { dead[i] = 1; ++ndead; continue; }
+        if (!(d[i] < p->max_diameter)) {
+            uint32_t v[4];
+            philox_draw(p->seed, id[i], p->step, 6u, v);
+            if (orc_u32(v[0]) < p->p_div) { div[i] = 1; ++ndiv; }
+        }
+    }
+    const int64_t nsurv = n - ndead, nnew = nsurv + ndiv;
+    if (nnew > capacity || n > capacity) {
+        free(ord); free(dead); free(div);
+        return -(nnew > n ? nnew : n);
+    }
+    /* apply, in ascending id: Brownian move, age, growth or division */
+    int64_t rank = 0;
+    double *dx = (double *)malloc(sizeof(double) * (size_t)(ndiv > 0 ? ndiv : 1) * 3);
+    double *dd = (double *)malloc(sizeof(double) * (size_t)(ndiv > 0 ? ndiv : 1) * 2);
+    for (int64_t k = 0; k < n; ++k) {
+        int64_t i = ord[k];
+        if (dead[i]) continue;
+        uint32_t w[4];
+        philox_draw(p->seed, id[i], p->step, 5u, w);
+        double vx = 2.0 * orc_u32(w[0]) - 1.0;
+        double vy = 2.0 * orc_u32(w[1]) - 1.0;
+        double vz = 2.0 * orc_u32(w[2]) - 1.0;
+        double n2 = vx * vx + vy * vy + vz * vz;
+        if (n2 > 0.0) {
+            double nv = sqrt(n2);
+            x[i] = x[i] + (vx / nv) * p->displacement_rate;
+            y[i] = y[i] + (vy / nv) * p->displacement_rate;
+            z[i] = z[i] + (vz / nv) * p->displacement_rate;
+            if (p->displacement_rate != 0.0) flags[i] |= ORC_MOVED;
+        }
+        age[i] += 1u;
+        if (d[i] < p->max_diameter) {
+            double Vn = vol[i] + p->growth;
+            double dn = 2.0 * orc_cbrt_det(Vn * C);
+            if (dn > d[i]) flags[i] |= ORC_GREW;
+            vol[i] = Vn;
+            d[i] = dn;
+        } else if (div[i]) {
+            double Vh = vol[i] * 0.5;
+            double r = orc_cbrt_det(Vh * C);
+            double u[3];
+            orc_division_axis(p->seed, id[i], p->step, u);
+            double px = x[i], py = y[i], pz = z[i];
+            x[i] = px - r * u[0];
+            y[i] = py - r * u[1];
+            z[i] = pz - r * u[2];
+            dx[3 * rank + 0] = px + r * u[0];
+            dx[3 * rank + 1] = py + r * u[1];
+            dx[3 * rank + 2] = pz + r * u[2];
+            dd[2 * rank + 0] = 2.0 * r;
+            dd[2 * rank + 1] = Vh;
+            vol[i] = Vh;
+            d[i] = 2.0 * r;
+            flags[i] |= ORC_MOVED;
+            ++rank;
+        }
+    }
+    /* removal: survivors keep their order */
+    int64_t m = 0;
+    for (int64_t i = 0; i < n; ++i) {
+        if (dead[i]) continue;
+        x[m] = x[i]; y[m] = y[i]; z[m] = z[i]; d[m] = d[i]; vol[m] = vol[i];
+        id[m] = id[i]; flags[m] = flags[i]; age[m] = age[i];
+        ++m;
+    }
+    /* daughters in mother-id order */
+    for (int64_t r = 0; r < ndiv; ++r) {
+        int64_t j = nsurv + r;
+        x[j] = dx[3 * r + 0]; y[j] = dx[3 * r + 1]; z[j] = dx[3 * r + 2];
+        d[j] = dd[2 * r + 0]; vol[j] = dd[2 * r + 1];
+        id[j] = (uint32_t)(*id_next + r);
+        flags[j] = ORC_ADDED;
+        age[j] = 0u;
+    }
+    *id_next += ndiv;
+    free(ord); free(dead); free(div); free(dx); free(dd);
+    return nnew;
+}
+
+/* Initial ages for the oncology workload (reading R44): floor(u32(w0) * max_age) with
+ * Philox (id, 0xFFFFFFFC, 2). */
+void orc_init_ages(int64_t n, const uint32_t *id, uint64_t seed, uint32_t max_age, uint32_t *age)
+{
+    for (int64_t k = 0; k < n; ++k) {
+        uint32_t w[4];
+        philox_draw(seed, id[k], 0xFFFFFFFCu, 2u, w);
+        age[k] = (uint32_t)floor(orc_u32(w[0]) * (double)max_age);
+    }
+}
