@@ -183,6 +183,8 @@ def run_ours(args, ws, rank, local):
         return run_cfg4(args, ws, rank, local)
     if args.config == "soma":
         return run_soma(args, ws, rank, local)
+    if args.config == "onco":
+        return run_onco(args, ws, rank, local)
     torch.cuda.set_device(local)
     cfg = W.PRESETS[args.config]
     eng = Engine(local, cfg.n)
@@ -464,6 +466,88 @@ def run_soma(args, ws, rank, local):
         "clocks": clk.summary(), "gpu_launches": eng.stats()["launches"] - launches0,
     }
     print(json.dumps(line), flush=True)
+
+
+def run_onco(args, ws, rank, local):
+    """tumor-spheroid steps (grid + mechanics, then Alg. 4 with
+    removal and division).  Every step has a different N; value = sum(N_t) / sum(t)."""
+    import torch
+    from paper_2503_10796_b200 import Agents, COncoParams, Engine, Params
+    torch.cuda.set_device(local)
+    cfg = W.ONCO
+    steps = min(args.steps, cfg.steps)
+    cap = int(cfg.n * 1.6) + 1024
+    eng = Engine(local, cap)
+    a = Agents.empty(cap, volume=True)
+    stream = torch.cuda.Stream()
+    eng.init_spheres(a, cfg.n, seed=cfg.seed, side=cfg.side, d_lo=cfg.d_lo, d_width=cfg.d_width,
+                     d_random=True, stream=stream)
+    torch.cuda.synchronize()
+    d = a.diameter[:cfg.n]
+    a.volume[:cfg.n].copy_((math.pi / 6.0) * (d * d * d))
+    # ages (R44): floor(u32(Philox(seed, (id, 0xFFFFFFFC, 2)).w0) * 120), drawn on the host
+    # by the same counter-based generator the init uses (ids 0..n-1)
+    age = torch.zeros(2 * cap, dtype=torch.int32, device="cuda")
+    age[:cfg.n].copy_(_onco_ages(cfg.n, cfg.seed, cfg.max_age0))
+    mp = Params(k=2.0, gamma=1.0, dt=1.0, max_displacement=1.0, force_threshold=1.8)
+    tiles = int(math.ceil((cfg.side + 2 * steps) / 10.0 / 4.0)) + 8
+    eng.reserve(cap, tiles ** 3 * 64)
+    id_next = cfg.n
+    per_step = []
+    launches0 = eng.stats()["launches"]
+    with ClockSampler(local) as clk:
+        for t in range(steps):
+            n0 = a.n
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            e0.record(stream)
+            eng.step(a, mp, stream=stream)
+            e1.record(stream)
+            id_next = eng.onco_step(a, age, COncoParams.make(step=t, seed=cfg.seed), id_next,
+                                    stream=stream)
+            e2 = torch.cuda.Event(enable_timing=True)
+            e2.record(stream)
+            torch.cuda.synchronize()
+            per_step.append((n0, e0.elapsed_time(e2), e0.elapsed_time(e1)))
+    total_agents = sum(n for n, _, _ in per_step)
+    total_ms = sum(ms for _, ms, _ in per_step)
+    line = _common(total_agents / (total_ms * 1e-3), total_ms / steps, ws, args,
+                   {"workload": "tumor spheroid cells (SURVEY 8(f) row f2)", **asdict_safe(cfg),
+                    "final_agents": a.n, "id_next": id_next,
+                    "per_step": [{"n": n, "ms": round(ms, 4), "mech_ms": round(m, 4)}
+                                 for n, ms, m in per_step],
+                    "l2": "inputs larger than L2 (>= 48 B/agent x 1M); no flush"},
+                   clk.summary(), eng.stats()["launches"] - launches0)
+    line["roofline"] = None
+    line["note"] = "the step is the cfg2-type mechanics + the behaviour/removal pass (HBM-bound)"
+    print(json.dumps(line), flush=True)
+
+
+def asdict_safe(cfg):
+    from dataclasses import asdict
+    return asdict(cfg)
+
+
+def _onco_ages(n, seed, max_age):
+    """Reading R44 ages on the host: the product's own Philox4x32-10 in numpy (the oracle
+    is test infrastructure and is not called here)."""
+    import numpy as np
+    import torch
+    ids = np.arange(n, dtype=np.uint64)
+    c0, c1 = (ids & 0xFFFFFFFF).astype(np.uint32), (ids >> 32).astype(np.uint32)
+    c2 = np.full(n, 0xFFFFFFFC, np.uint32)
+    c3 = np.full(n, 2, np.uint32)
+    k0, k1 = np.uint32(seed & 0xFFFFFFFF), np.uint32(seed >> 32)
+    for _ in range(10):
+        p0 = np.uint64(0xD2511F53) * c0.astype(np.uint64)
+        p1 = np.uint64(0xCD9E8D57) * c2.astype(np.uint64)
+        hi0, lo0 = (p0 >> np.uint64(32)).astype(np.uint32), p0.astype(np.uint32)
+        hi1, lo1 = (p1 >> np.uint64(32)).astype(np.uint32), p1.astype(np.uint32)
+        c0, c1, c2, c3 = hi1 ^ c1 ^ k0, lo1, hi0 ^ c3 ^ k1, lo0
+        k0 = np.uint32((int(k0) + 0x9E3779B9) & 0xFFFFFFFF)
+        k1 = np.uint32((int(k1) + 0xBB67AE85) & 0xFFFFFFFF)
+    age = np.floor(c0.astype(np.float64) * 2.0 ** -32 * max_age).astype(np.int32)
+    return torch.from_numpy(age)
 
 
 def run_slabs(args, ws, rank, local):

@@ -251,6 +251,42 @@ bdm_status bdm_secrete(bdm_handle h, const bdm_agents *a, const uint8_t *type, i
 bdm_status bdm_chemotaxis(bdm_handle h, bdm_agents *a, const uint8_t *type, int32_t type_sel,
                           double weight, const double *u, const bdm_grid3 *g, void *stream);
 
+/* ---- oncology behaviour with agent removal ------------------ */
+
+/* Alg. 4 (algo:tumor_growth_module); values of Table 4.2 per
+ * step of 1 h: displacement_rate 0.005 um, growth 42 um^3, p_div 0.0215, p_death 0.033,
+ * min_age 87.  max_diameter is not given by the paper (reading R43: 14 um). */
+typedef struct {
+    double displacement_rate;  /* Brownian step length per step                       */
+    double growth;             /* volume added per step while d < max_diameter        */
+    double max_diameter;       /* growth below it, else division with p_div            */
+    double p_death;            /* per step, for agents with age >= min_age             */
+    double p_div;              /* per step, for agents with d >= max_diameter          */
+    uint32_t min_age;          /* steps                                                */
+    uint64_t seed;
+    uint32_t step;
+} bdm_onco_params;
+
+/* One oncology behaviour pass with removal over agents carrying their post-mechanics
+ * state (call after bdm_step; reading R40).  For every agent, in any memory order, with
+ * Philox(seed, (id, step, 5)) = w and (id, step, 6) = v (R42):
+ *   b = 2 u32(w0..w2) - 1, x += (b / |b|) * displacement_rate (R41; b = 0: no move);
+ *   if age >= min_age and u32(w3) < p_death: removed;
+ *   else age += 1 and, if d < max_diameter, V += growth, d = 2 cbrt_det(V 0.75/pi) (R28),
+ *   else if u32(v0) < p_div: Cell::Divide as bdm_grow_divide (R13).
+ * Removal keeps the survivors' relative order; daughters follow them in mother-id order
+ * with ids id_next + rank (R45); ids are never reused.  Requires x, y, z, diameter,
+ * volume, id (all < id_next, unique) and flags.  age is a device u32 property table
+ * indexed by id (age_cap entries; the mechanics step reorders the SoA, ids travel with
+ * it): read and incremented for every survivor, 0 for a daughter.  out_host (pinned, 2
+ * int64) receives the new n and the new id_next, asynchronously; a->n is NOT updated.
+ * If the new population exceeds a->capacity or the new id_next exceeds age_cap nothing
+ * is modified, out_host[0] = -(required capacity) and bdm_sync reports BDM_ECAPACITY.
+ * Errors: BDM_EINVAL. */
+bdm_status bdm_onco_step(bdm_handle h, bdm_agents *a, uint32_t *age, int64_t age_cap,
+                         const bdm_onco_params *p, int64_t id_next, int64_t *out_host,
+                         void *stream);
+
 /* ---- multi-GPU x-slabs (TeraAgent partitioning P:6058-6081, aura
  * P:6083-6106, migration P:6116-6126).  The transport between ranks is the
  * caller's (torch.distributed over NCCL in paper_2503_10796_b200/slabs.py); these

@@ -26,6 +26,7 @@ EXPORTS = [
     "bdm_get_stats", "bdm_get_grid_info", "bdm_neighbor_pairs", "bdm_peak_dfma",
     "bdm_set_option", "bdm_grow_divide", "bdm_sir_step", "bdm_local_frame", "bdm_set_frame",
     "bdm_pack_slab", "bdm_append", "bdm_diffuse", "bdm_secrete", "bdm_chemotaxis",
+    "bdm_onco_step",
 ]
 PACK_MIGRATE, PACK_AURA = 1, 2
 
@@ -77,6 +78,20 @@ class CGrid3(ctypes.Structure):
         return g
 
 
+class COncoParams(ctypes.Structure):
+    """bdm_onco_params: Alg. 4 with Table 4.2's values per 1 h step (R43: d_max 14 um)."""
+    _fields_ = [("displacement_rate", ctypes.c_double), ("growth", ctypes.c_double),
+                ("max_diameter", ctypes.c_double), ("p_death", ctypes.c_double),
+                ("p_div", ctypes.c_double), ("min_age", ctypes.c_uint32),
+                ("seed", ctypes.c_uint64), ("step", ctypes.c_uint32)]
+
+    @staticmethod
+    def make(displacement_rate=0.005, growth=42.0, max_diameter=14.0, p_death=0.033,
+             p_div=0.0215, min_age=87, seed=1, step=0) -> "COncoParams":
+        return COncoParams(displacement_rate, growth, max_diameter, p_death, p_div, min_age,
+                           seed, step)
+
+
 class CGridInfo(ctypes.Structure):
     _fields_ = [
         ("R", ctypes.c_double), ("L", ctypes.c_double), ("origin", ctypes.c_double * 3),
@@ -124,6 +139,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "bdm_diffuse": [P, P, P, ctypes.POINTER(CGrid3), dbl, dbl, dbl, P],
         "bdm_secrete": [P, AG, P, i32, dbl, P, ctypes.POINTER(CGrid3), P],
         "bdm_chemotaxis": [P, AG, P, i32, dbl, P, ctypes.POINTER(CGrid3), P],
+        "bdm_onco_step": [P, AG, P, i64, ctypes.POINTER(COncoParams), i64, P, P],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -435,6 +451,26 @@ class Engine:
         for u, v in zip(grids, spares):
             self.diffuse(u, v, grid, nu, mu, dt, stream)
         return list(spares), list(grids)
+
+    def onco_step(self, agents: Agents, age, p: "COncoParams", id_next: int, stream=None):
+        """bdm_onco_step (Alg. 4 + removal, row f2); age is an int32/uint32 device tensor
+        indexed by id.  Synchronizes, sets agents.n and returns the new id_next.  Raises
+        BdmError(BDM_ECAPACITY) with nothing modified if the population would exceed the
+        capacity of agents or of age."""
+        import torch
+        if not hasattr(self, "_onco_out"):
+            self._onco_out = torch.zeros(2, dtype=torch.int64, pin_memory=True)
+        ca = agents.c()
+        _check(self.lib.bdm_onco_step(self.h, ctypes.byref(ca), _ptr(age), int(age.numel()),
+                                      ctypes.byref(p),
+                                      int(id_next), ctypes.c_void_p(self._onco_out.data_ptr()),
+                                      _stream_ptr(stream)))
+        st = self.lib.bdm_sync(self.h, _stream_ptr(stream))
+        if st != BDM_OK:
+            _check(st)
+        n, nxt = (int(v) for v in self._onco_out)
+        agents.n = n
+        return nxt
 
     def cfg3_step(self, agents: Agents, params: Params, growth: float, v_max: float,
                   stream=None) -> int:

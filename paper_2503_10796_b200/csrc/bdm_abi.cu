@@ -175,6 +175,7 @@ bdm_status bdm_destroy(bdm_handle h) {
     cudaDeviceSynchronize();
     void *bufs[] = {c->key, c->rank, c->perm_tmp, c->skey, c->sid, c->perm, c->sx, c->sy,
                     c->sz, c->sd, c->sidf, c->sflags, c->svol, c->div_rank, c->box_start, c->dense_list,
+                    c->onco_id, c->onco_out,
                     c->block_sums, c->pair_count, c->n_new, c->lrank, c->cls, c->cls2,
                     c->pack_counts, c->sc};
     for (void *p : bufs)
@@ -319,6 +320,33 @@ bdm_status bdm_grow_divide(bdm_handle h, bdm_agents *a, const bdm_params *p, dou
     const double vol_to_r3 = 0.75 / M_PI;  // r^3 = V * 0.75/pi, computed once (R28)
     return launch_grow_divide(c, a, growth, v_max, vol_to_r3, p->seed, p->step,
                               (long long *)n_out_host, (cudaStream_t)stream);
+}
+
+bdm_status bdm_onco_step(bdm_handle h, bdm_agents *a, uint32_t *age, int64_t age_cap,
+                         const bdm_onco_params *p, int64_t id_next, int64_t *out_host,
+                         void *stream) {
+    if (h) ((Ctx *)h)->fused_valid = false;
+    if (!h || !p || !out_host) return fail(BDM_EINVAL, "NULL argument");
+    Ctx *c = (Ctx *)h;
+    bdm_status s = check_agents(a, true);
+    if (s != BDM_OK) return s;
+    if (a->n > 0 && (!a->volume || !age)) return fail(BDM_EINVAL, "oncology needs volume and age");
+    if (id_next < a->n || id_next > 0xFFFFFFFFll)
+        return fail(BDM_EINVAL, "id_next must be >= n (ids < id_next) and < 2^32");
+    if (age_cap < id_next) return fail(BDM_EINVAL, "age_cap < id_next");
+    if (!(p->growth >= 0.0) || !(p->max_diameter >= 0.0) || !(p->p_death >= 0.0) ||
+        !(p->p_div >= 0.0))
+        return fail(BDM_EINVAL, "negative oncology parameter");
+    if ((s = grow_agents(c, a->capacity)) != BDM_OK) return s;
+    const int64_t nb = scan_block_count(id_next + 1) + 1;
+    if (nb > c->block_sums_cap) {
+        BDM_CUDA_TRY(cudaDeviceSynchronize());
+        if ((s = dalloc(&c->block_sums, nb)) != BDM_OK) return s;
+        c->block_sums_cap = nb;
+    }
+    c->grid_valid = false;
+    return launch_onco_step(c, a, age, age_cap, p, id_next, (long long *)out_host,
+                            (cudaStream_t)stream);
 }
 
 bdm_status bdm_sir_step(bdm_handle h, bdm_agents *a, const bdm_params *p, double side,

@@ -80,6 +80,9 @@ struct Ctx {
     // grid
     uint32_t *box_start = nullptr;  // slot_cap + 1
     uint32_t *dense_list = nullptr; // slot_cap / 64 + 1 tile ids (dense regions)
+    uint32_t *onco_id = nullptr;    // row f2: divider flags by id, then their ranks
+    int64_t onco_id_cap = 0;
+    long long *onco_out = nullptr;  // row f2: new n, new id_next
     uint32_t *block_sums = nullptr;
     int64_t block_sums_cap = 0;
     // misc
@@ -156,6 +159,50 @@ __device__ __forceinline__ uint32_t box_key(int bx, int by, int bz, int T0, int 
     return tile * 64u + m;
 }
 
+// R28: deterministic cube root.  v = m 2^e (frexp, m in [0.5, 1)); y0 = 2^k with
+// k = floor((e+1)/3); exactly 8 Newton steps y <- (2y + v/(y*y))/3 without fma
+// (the library is compiled with -fmad=false).
+__device__ __forceinline__ double cbrt_det(double v) {
+    if (!(v > 0.0)) return 0.0;
+    int e;
+    (void)frexp(v, &e);
+    const int num = e + 1;
+    const int k = num >= 0 ? num / 3 : -((-num + 2) / 3);
+    double y = ldexp(1.0, k);
+#pragma unroll
+    for (int it = 0; it < 8; ++it) {
+        const double yy = y * y;
+        const double q = v / yy;
+        const double t = 2.0 * y + q;
+        y = t / 3.0;
+    }
+    return y;
+}
+
+// R13: axis uniform on the sphere by rejection in the unit ball; try k uses Philox
+// counter (id_lo, id_hi, step, 3 + 4k); after 16 rejections the axis is +x.
+__device__ __forceinline__ void division_axis(uint32_t k0, uint32_t k1, uint32_t id,
+                                              uint32_t step, double &ux, double &uy,
+                                              double &uz) {
+    for (uint32_t k = 0; k < 16; ++k) {
+        const U4 w = philox10(id, 0u, step, 3u + 4u * k, k0, k1);
+        const double vx = 2.0 * uniform32(w.a) - 1.0;
+        const double vy = 2.0 * uniform32(w.b) - 1.0;
+        const double vz = 2.0 * uniform32(w.c) - 1.0;
+        const double n2 = vx * vx + vy * vy + vz * vz;
+        if (n2 > 0.0 && n2 <= 1.0) {
+            const double nn = sqrt(n2);
+            ux = vx / nn;
+            uy = vy / nn;
+            uz = vz / nn;
+            return;
+        }
+    }
+    ux = 1.0;
+    uy = 0.0;
+    uz = 0.0;
+}
+
 constexpr uint32_t kChanged = BDM_FLAG_MOVED | BDM_FLAG_GREW | BDM_FLAG_ADDED;
 constexpr uint32_t kGhost = 1u << 31;  // internal sorted-workspace flag: aura (ghost) agent
 
@@ -178,6 +225,11 @@ bdm_status launch_pairs(Ctx *c, int64_t n, uint64_t *pairs, int64_t cap, cudaStr
 bdm_status launch_peak_dfma(int sm_count, double *dfma_per_s);
 // generic exclusive scan of m u32 values in place (kernels_grid.cu)
 bdm_status launch_scan_u32(Ctx *c, uint32_t *data, long long m, cudaStream_t st);
+int64_t scan_block_count(int64_t m);
+// oncology behaviour + removal (kernels_onco.cu)
+bdm_status launch_onco_step(Ctx *c, bdm_agents *a, uint32_t *age, int64_t age_cap,
+                            const bdm_onco_params *p, int64_t id_next, long long *out_host,
+                            cudaStream_t st);
 // SIR (kernels_sir.cu)
 bdm_status launch_sir_step(Ctx *c, bdm_agents *a, const bdm_params *p, double side, double radius,
                            double p_inf, double p_rec, long long *counts_host, cudaStream_t st);

@@ -18,49 +18,7 @@
 
 namespace bdm {
 
-// R28: deterministic cube root.  v = m 2^e (frexp, m in [0.5, 1)); y0 = 2^k with
-// k = floor((e+1)/3); exactly 8 Newton steps y <- (2y + v/(y*y))/3 without fma
-// (the library is compiled with -fmad=false).
-__device__ __forceinline__ double cbrt_det(double v) {
-    if (!(v > 0.0)) return 0.0;
-    int e;
-    (void)frexp(v, &e);
-    const int num = e + 1;
-    const int k = num >= 0 ? num / 3 : -((-num + 2) / 3);
-    double y = ldexp(1.0, k);
-#pragma unroll
-    for (int it = 0; it < 8; ++it) {
-        const double yy = y * y;
-        const double q = v / yy;
-        const double t = 2.0 * y + q;
-        y = t / 3.0;
-    }
-    return y;
-}
-
-// R13: axis uniform on the sphere by rejection in the unit ball; try k uses Philox
-// counter (id_lo, id_hi, step, 3 + 4k); after 16 rejections the axis is +x.
-__device__ __forceinline__ void division_axis(uint32_t k0, uint32_t k1, uint32_t id,
-                                              uint32_t step, double &ux, double &uy,
-                                              double &uz) {
-    for (uint32_t k = 0; k < 16; ++k) {
-        const U4 w = philox10(id, 0u, step, 3u + 4u * k, k0, k1);
-        const double vx = 2.0 * uniform32(w.a) - 1.0;
-        const double vy = 2.0 * uniform32(w.b) - 1.0;
-        const double vz = 2.0 * uniform32(w.c) - 1.0;
-        const double n2 = vx * vx + vy * vy + vz * vz;
-        if (n2 > 0.0 && n2 <= 1.0) {
-            const double nn = sqrt(n2);
-            ux = vx / nn;
-            uy = vy / nn;
-            uz = vz / nn;
-            return;
-        }
-    }
-    ux = 1.0;
-    uy = 0.0;
-    uz = 0.0;
-}
+// cbrt_det (R28) and division_axis (R13) live in bdm_internal.cuh (shared with row f2).
 
 __global__ void __launch_bounds__(256) k_div_mark(int64_t n, const double *__restrict__ vol,
                                                   const uint32_t *__restrict__ id, double v_max,

@@ -118,4 +118,25 @@ class SomaConfig:
 
 SOMA = SomaConfig("soma", 32_768, 1000.0, 512, 1.0, 0.01, 0.5, 1.0, 0.75, 10.0)
 
-PRESETS = {"cfg1": CFG1, "cfg2": CFG2, "cfg3": CFG3, "cfg4": CFG4, "cfg5": CFG5, "soma": SOMA}
+@dataclass(frozen=True)
+class OncoConfig:
+    """SURVEY 8(f) row f2 (not one of BASELINE.json's configs): tumor-spheroid cells
+    (Alg. 4, Table 4.2 per 1 h step) at GPU scale.  Mechanics: adherence 1.8 as the force
+    threshold, maximum speed 1.0 um/h as the cap, dt = 1 h.  Ages start uniform in
+    [0, 120) h so apoptosis (age >= 87 h) runs from the first step (R44); diameters
+    start uniform in [10, 14) um so divisions begin early (d_max = 14 um, R43)."""
+    name: str
+    n: int
+    side: float
+    d_lo: float
+    d_width: float
+    steps: int
+    max_age0: int = 120
+    seed: int = 1
+
+
+ONCO = OncoConfig("onco", 1_000_000, side_for_fraction(1_000_000, (14.0**4 - 10.0**4) / 16.0, 0.3),
+                  10.0, 4.0, 20)
+
+PRESETS = {"cfg1": CFG1, "cfg2": CFG2, "cfg3": CFG3, "cfg4": CFG4, "cfg5": CFG5, "soma": SOMA,
+           "onco": ONCO}
