@@ -39,6 +39,9 @@ UNIT = "agent-updates/s"
 # and fp64 pipe instructions the method must issue.
 B_ALG_PER_AGENT = 72.0           # x,y,z,d read (32) + x,y,z write (24) + key/perm (16)
 B_ALG_STATIC_EXTRA = 8.0         # flags read + write with detect_static
+# the mechanics kernel alone: sorted x,y,z,d + id + flags read (40), x,y,z,d + id + flags
+# written to the caller's arrays (40)
+MECH_ALG_BYTES_PER_AGENT = 80.0
 FP64_PER_CAND, FP64_PER_NBR, FP64_PER_CONT, FP64_PER_AGENT = 7.0, 3.0, 60.0, 40.0
 
 
@@ -270,7 +273,8 @@ def run_ours(args, ws, rank, local):
                    "parallelism": f"{ws} GPU"},
         "roofline": {"bound": "alu", "kernel": "k_mech (a5-a9)",
                      "achieved": achieved / 1e12, "peak": fp64_peak / 1e12,
-                     "unit": "T fp64-inst/s", "frac": achieved / fp64_peak, "traffic": None,
+                     "unit": "T fp64-inst/s", "frac": achieved / fp64_peak,
+                     "traffic": _traffic("k_mech_tile6", MECH_ALG_BYTES_PER_AGENT * cfg.n),
                      "peak_source": f"{sm_count} SMs x 64 fp64 lanes x {max_mhz:.0f} MHz "
                                     f"(guide unit counts, max clock); measured DFMA "
                                     f"{dfma_meas / 1e12:.2f} T/s",
@@ -395,9 +399,26 @@ def run_cfg4(args, ws, rank, local):
                    clk.summary(), eng.stats()["launches"] - launches0)
     line["roofline"] = {"bound": "hbm", "kernel": "k_sir_update + k_sir_collect (whole step)",
                         "achieved": ach / 1e9, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                        "frac": ach / (peaks["hbm_gbs"] * 1e9), "traffic": None,
+                        "frac": ach / (peaks["hbm_gbs"] * 1e9),
+                        "traffic": _traffic("k_sir_update", b_alg),
                         "peak_source": src, "alg_bytes_per_agent": 50}
     print(json.dumps(line), flush=True)
+
+
+def _traffic(kernel, alg_bytes):
+    """DRAM bytes per launch of `kernel` from the committed ncu --set full capture
+    (profiles/r01/traffic.json, written from the .ncu-rep summaries), next to the
+    algorithmic bytes of the same launch; None if there is no capture."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01", "traffic.json")
+    try:
+        with open(path) as f:
+            t = json.load(f)[kernel]
+    except (OSError, KeyError, ValueError):
+        return None
+    return {"dram_bytes_per_launch": t["dram_bytes_per_launch"],
+            "alg_bytes_per_launch": alg_bytes,
+            "ratio": t["dram_bytes_per_launch"] / alg_bytes if alg_bytes else None,
+            "source": t["source"], "capture_workload": t["workload"]}
 
 
 def run_soma(args, ws, rank, local):
@@ -460,7 +481,8 @@ def run_soma(args, ws, rank, local):
                    "l2": "grids (1 GiB each) larger than L2; no flush"},
         "roofline": {"bound": "hbm", "kernel": "k_diffuse (one substance, one step)",
                      "achieved": ach / 1e9, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                     "frac": ach / (peaks["hbm_gbs"] * 1e9), "traffic": None,
+                     "frac": ach / (peaks["hbm_gbs"] * 1e9),
+                     "traffic": _traffic("k_diffuse_tma", 16.0 * r ** 3),
                      "peak_source": src, "alg_bytes_per_point": 16,
                      "diffuse_ms": statistics.mean(dms) / 2},
         "clocks": clk.summary(), "gpu_launches": eng.stats()["launches"] - launches0,

@@ -234,9 +234,8 @@ struct SirQueue {
 
 // The final state of a queried S agent and its counters.
 __device__ __forceinline__ void sir_resolve(const SirArgs &A, uint32_t i, double px, double py,
-                                            double pz, unsigned long long &cs,
-                                            unsigned long long &ci, unsigned long long &cr,
-                                            unsigned long long &cn) {
+                                            double pz, uint32_t &cs, uint32_t &ci, uint32_t &cr,
+                                            uint32_t &cn) {
     uint8_t st = 0;
     if (infected_within(A, px, py, pz)) {
         st = 1;
@@ -255,9 +254,8 @@ __device__ __forceinline__ void sir_resolve(const SirArgs &A, uint32_t i, double
 // draws, the queue entry for an infection query, recovery, movement and wrap.
 __device__ __forceinline__ void sir_agent(const SirArgs &A, SirQueue &Q, int lane, unsigned lt_mask,
                                           int64_t i, bool valid, double px, double py, double pz,
-                                          uint8_t st, int &qn, unsigned long long &cs,
-                                          unsigned long long &ci, unsigned long long &cr,
-                                          unsigned long long &cn) {
+                                          uint8_t st, int &qn, uint32_t &cs, uint32_t &ci,
+                                          uint32_t &cr, uint32_t &cn) {
     const uint32_t me = valid ? (A.id ? A.id[i] : (uint32_t)i) : 0u;
     const U4 w = philox10(me, 0u, A.step, 0u, A.k0, A.k1);
     // Alg. 7: an S agent whose draw passed (R17: strict '<', u = w * 2^-32) is queued
@@ -316,13 +314,14 @@ __device__ __forceinline__ void sir_agent(const SirArgs &A, SirQueue &Q, int lan
     }
 }
 
-__global__ void __launch_bounds__(kSirThreads, 3) k_sir_update(SirArgs A, DevScalars *__restrict__ sc) {
+__global__ void __launch_bounds__(kSirThreads, 4) k_sir_update(SirArgs A, DevScalars *__restrict__ sc) {
     if (sc->overflow) return;
     __shared__ SirQueue Qs[kSirThreads / 32];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     SirQueue &Q = Qs[wid];
     const unsigned lt_mask = (1u << lane) - 1u;
-    unsigned long long cs = 0, ci = 0, cr = 0, cn = 0;
+    // per-thread counters: a thread sees at most n / (grid threads) agents (< 2^32)
+    uint32_t cs = 0, ci = 0, cr = 0, cn = 0;
     int qn = 0;  // warp-uniform queue fill
     const int64_t nwarps = (int64_t)gridDim.x * (kSirThreads / 32);
     // two 32-agent slices per warp iteration, all their loads issued first
@@ -350,7 +349,7 @@ __global__ void __launch_bounds__(kSirThreads, 3) k_sir_update(SirArgs A, DevSca
     if (lane < qn) sir_resolve(A, Q.idx[lane], Q.px[lane], Q.py[lane], Q.pz[lane], cs, ci, cr, cn);
     // block reduction of the counters, one atomic each per block
     __shared__ unsigned long long red[4][kSirThreads / 32];
-    unsigned long long v[4] = {cs, ci, cr, cn};
+    unsigned long long v[4] = {cs, ci, cr, cn};  // warp sums in 64 bits
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
         unsigned long long t = v[q];
