@@ -46,16 +46,20 @@ static bdm_status dalloc(T **p, int64_t count) {
 static bdm_status grow_agents(Ctx *c, int64_t n) {
     if (n <= c->agent_cap) return BDM_OK;
     BDM_CUDA_TRY(cudaDeviceSynchronize());
-    const int64_t cap = n + n / 8 + 1024;
+    // exact on the first sizing (the caller's stated maximum), with slack on regrowth
+    const int64_t cap = c->agent_cap == 0 ? n : n + n / 8 + 1024;
+    // optional buffers are re-allocated at the new size on their next use
+    void *opt[] = {c->svol, c->div_rank, c->lrank, c->cls, c->cls2};
+    for (void *p : opt)
+        if (p) cudaFree(p);
+    c->svol = nullptr;
+    c->div_rank = c->lrank = c->cls = c->cls2 = nullptr;
     bdm_status s;
     if ((s = dalloc(&c->key, cap)) || (s = dalloc(&c->rank, cap)) ||
         (s = dalloc(&c->perm_tmp, cap)) || (s = dalloc(&c->skey, cap)) ||
-        (s = dalloc(&c->sid, cap)) || (s = dalloc(&c->perm, cap)) || (s = dalloc(&c->sx, cap)) ||
+        (s = dalloc(&c->sid, cap)) || (s = dalloc(&c->sx, cap)) ||
         (s = dalloc(&c->sy, cap)) || (s = dalloc(&c->sz, cap)) || (s = dalloc(&c->sd, cap)) ||
-        (s = dalloc(&c->sidf, cap)) || (s = dalloc(&c->sflags, cap)) ||
-        (s = dalloc(&c->svol, cap)) || (s = dalloc(&c->div_rank, cap + 1)) ||
-        (s = dalloc(&c->lrank, cap + 1)) || (s = dalloc(&c->cls, cap + 1)) ||
-        (s = dalloc(&c->cls2, cap + 1))) {
+        (s = dalloc(&c->sidf, cap)) || (s = dalloc(&c->sflags, cap))) {
         c->agent_cap = 0;
         return s;
     }
@@ -173,7 +177,7 @@ bdm_status bdm_destroy(bdm_handle h) {
     Ctx *c = (Ctx *)h;
     cudaSetDevice(c->device);
     cudaDeviceSynchronize();
-    void *bufs[] = {c->key, c->rank, c->perm_tmp, c->skey, c->sid, c->perm, c->sx, c->sy,
+    void *bufs[] = {c->key, c->rank, c->perm_tmp, c->skey, c->sid, c->sx, c->sy,
                     c->sz, c->sd, c->sidf, c->sflags, c->svol, c->div_rank, c->box_start, c->dense_list,
                     c->onco_id, c->onco_out,
                     c->block_sums, c->pair_count, c->n_new, c->lrank, c->cls, c->cls2,

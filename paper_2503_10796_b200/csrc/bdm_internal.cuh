@@ -71,9 +71,10 @@ struct Ctx {
     // per-agent workspace
     uint32_t *key = nullptr, *rank = nullptr;          // unsorted order
     uint32_t *perm_tmp = nullptr, *skey = nullptr, *sid = nullptr;  // after scatter
-    uint32_t *perm = nullptr;                          // sorted slot -> input index
     double *sx = nullptr, *sy = nullptr, *sz = nullptr, *sd = nullptr;  // sorted SoA
     uint32_t *sidf = nullptr, *sflags = nullptr;
+    // allocated on first use (need_agent_buf), so the mechanics path alone holds
+    // 60 B/agent of workspace (cfg5 on one GPU)
     double *svol = nullptr;                            // sorted volume (when present)
     uint32_t *div_rank = nullptr;                      // growth/division: flag -> rank by id
     long long *n_new = nullptr;                        // growth/division: new agent count
@@ -110,6 +111,19 @@ struct Ctx {
     int64_t fused_n = 0;
     SirWs sir;
 };
+
+// An optional per-agent buffer (agent_cap + 1 entries), allocated on first use.
+template <class T>
+inline bdm_status need_agent_buf(Ctx *c, T **p) {
+    if (*p) return BDM_OK;
+    const cudaError_t e = cudaMalloc((void **)p, (size_t)(c->agent_cap + 1) * sizeof(T));
+    if (e != cudaSuccess) {
+        *p = nullptr;
+        cudaGetLastError();
+        return cuda_fail(e, "cudaMalloc of an optional per-agent buffer");
+    }
+    return BDM_OK;
+}
 
 // ------------------------------------------------------------------ device helpers
 __device__ inline unsigned long long enc_double(double v) {

@@ -82,6 +82,10 @@ bdm_status launch_grow_divide(Ctx *c, bdm_agents *a, double growth, double v_max
                               cudaStream_t st) {
     const int64_t n = a->n;
     const unsigned nb = (unsigned)((n + 256) / 256);
+    {
+        const bdm_status s0 = need_agent_buf(c, &c->div_rank);
+        if (s0 != BDM_OK) return s0;
+    }
     k_div_mark<<<nb, 256, 0, st>>>(n, a->volume, a->id, v_max, c->div_rank);
     BDM_LAUNCH_CHECK("k_div_mark");
     bdm_status s = launch_scan_u32(c, c->div_rank, n + 1, st);

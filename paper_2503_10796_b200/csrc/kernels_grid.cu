@@ -352,7 +352,7 @@ __global__ void __launch_bounds__(256) k_fix_gather(
     const uint32_t *__restrict__ perm_tmp, const uint32_t *__restrict__ box_start,
     double *__restrict__ sx, double *__restrict__ sy, double *__restrict__ sz,
     double *__restrict__ sd, uint32_t *__restrict__ sidf, uint32_t *__restrict__ sflags,
-    uint32_t *__restrict__ perm, double *__restrict__ svol, uint32_t *__restrict__ lflag,
+    double *__restrict__ svol, uint32_t *__restrict__ lflag,
     const DevScalars *__restrict__ sc) {
     if (sc->overflow) return;
     const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -387,7 +387,6 @@ __global__ void __launch_bounds__(256) k_fix_gather(
         lflag[dst] = 0u;
     }
     sidf[dst] = me;
-    perm[dst] = src;
 }
 
 bdm_status launch_grid_sort(Ctx *c, const bdm_agents *a, const bdm_agents *g, cudaStream_t st) {
@@ -408,6 +407,9 @@ bdm_status launch_grid_sort(Ctx *c, const bdm_agents *a, const bdm_agents *g, cu
         if (zb > maxb) zb = maxb;
         k_zero_counts<<<(unsigned)zb, 1024, 0, st>>>(c->box_start, c->sc);
     }
+    bdm_status s;
+    if (S.vol && (s = need_agent_buf(c, &c->svol)) != BDM_OK) return s;
+    if (S.ng > 0 && (s = need_agent_buf(c, &c->lrank)) != BDM_OK) return s;
     k_key<<<nb, threads, 0, st>>>(S, c->sc, c->key, c->rank, c->box_start);
     const unsigned sb = (unsigned)((c->slot_cap + 1 + kScanTile - 1) / kScanTile);
     k_scan_reduce<<<sb, kScanThreads, 0, st>>>(c->box_start, c->block_sums, c->sc, 0);
@@ -418,7 +420,7 @@ bdm_status launch_grid_sort(Ctx *c, const bdm_agents *a, const bdm_agents *g, cu
     uint32_t *lflag = S.ng > 0 ? c->lrank : nullptr;
     k_fix_gather<<<(unsigned)((n + 1 + threads - 1) / threads), threads, 0, st>>>(
         S, c->skey, c->sid, c->perm_tmp, c->box_start, c->sx, c->sy, c->sz, c->sd, c->sidf,
-        c->sflags, c->perm, c->svol, lflag, c->sc);
+        c->sflags, c->svol, lflag, c->sc);
     c->launches += 7;
     BDM_LAUNCH_CHECK("grid sort");
     if (S.ng > 0) return launch_scan_u32(c, c->lrank, n + 1, st);  // output index of locals

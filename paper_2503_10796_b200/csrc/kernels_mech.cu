@@ -1498,6 +1498,10 @@ static bdm_status launch_dense(Ctx *c, const MechArgs &A, cudaStream_t st) {
 }
 
 bdm_status launch_mech(Ctx *c, bdm_agents *a, const bdm_params *p, cudaStream_t st) {
+    if (a->volume && !c->svol) {
+        set_error("agents carry a volume array but the grid was built without it");
+        return BDM_EINVAL;
+    }
     MechArgs A;
     A.n = a->n;
     A.sx = c->sx; A.sy = c->sy; A.sz = c->sz; A.sd = c->sd;

@@ -167,6 +167,11 @@ bdm_status launch_onco_step(Ctx *c, bdm_agents *a, uint32_t *age, int64_t age_ca
         BDM_CUDA_TRY(cudaMalloc(&c->onco_id, (size_t)cap * sizeof(uint32_t)));
         c->onco_id_cap = cap;
     }
+    {
+        bdm_status s0;
+        if ((s0 = need_agent_buf(c, &c->svol)) != BDM_OK) return s0;
+        if ((s0 = need_agent_buf(c, &c->lrank)) != BDM_OK) return s0;
+    }
     if (!c->onco_out) BDM_CUDA_TRY(cudaMalloc(&c->onco_out, 2 * sizeof(long long)));
     OncoArgs A;
     A.n = n;

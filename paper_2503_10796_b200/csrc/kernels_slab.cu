@@ -169,6 +169,14 @@ bdm_status launch_pack_slab(Ctx *c, bdm_agents *a, double lo, double hi, double 
                             bdm_agents *to_left, bdm_agents *to_right, long long *counts_host,
                             cudaStream_t st) {
     const int64_t n = a->n;
+    {
+        bdm_status s0;
+        if ((s0 = need_agent_buf(c, &c->cls)) != BDM_OK) return s0;
+        if ((s0 = need_agent_buf(c, &c->cls2)) != BDM_OK) return s0;
+        if (what == BDM_PACK_MIGRATE && (s0 = need_agent_buf(c, &c->div_rank)) != BDM_OK)
+            return s0;
+        if (a->volume && (s0 = need_agent_buf(c, &c->svol)) != BDM_OK) return s0;
+    }
     uint32_t *fl = c->cls, *fr = c->cls2, *fs = what == BDM_PACK_MIGRATE ? c->div_rank : nullptr;
     const unsigned nb = (unsigned)((n + 1 + 255) / 256);
     k_classify<<<nb, 256, 0, st>>>(n, a->x, lo, hi, margin, what, fl, fr, fs);
