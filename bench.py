@@ -193,6 +193,7 @@ def run_ours(args, ws, rank, local):
     eng = Engine(local, cfg.n)
     eng.set_option("mech_kernel", args.mech_kernel)
     eng.set_option("fuse_reduce", 1)   # a1 of the next step fused into the mechanics epilogue
+    eng.set_option("tile_order", args.tile_order)
     a = Agents.empty(cfg.n)
     stream = torch.cuda.Stream()
     with torch.cuda.stream(stream):
@@ -205,7 +206,19 @@ def run_ours(args, ws, rank, local):
     eng.step(a, params, stream=stream)
     gi = eng.grid_info()
     T = [(d + 3) // 4 + 8 for d in gi["dims"]]
+    if args.tile_order:
+        T = [(t + 7) // 8 * 8 for t in T]
     eng.reserve(0, T[0] * T[1] * T[2] * 64)
+    if args.shuffle:  # row f1: a random memory order (the sorted order is undone)
+        torch.cuda.synchronize()
+        g = torch.Generator(device="cuda")
+        g.manual_seed(11)
+        p = torch.randperm(cfg.n, device="cuda", generator=g)
+        for f in ("x", "y", "z", "diameter", "id", "flags"):
+            t = getattr(a, f)
+            t[:cfg.n] = t[:cfg.n][p]
+        torch.cuda.synchronize()
+    eng.set_option("sort_every", args.sort_every)
     for _ in range(max(args.warmup - 1, 0)):
         eng.step(a, params, stream=stream)
     # work counters of a representative step (the last warm-up step)
@@ -272,6 +285,9 @@ def run_ours(args, ws, rank, local):
                    "dt": cfg.dt, "max_displacement_um": cfg.max_disp,
                    "l2": "inputs (44 B/agent SoA) larger than L2; no flush",
                    "parallelism": f"{ws} GPU"},
+        **({"f1": {"tile_order": args.tile_order, "sort_every": args.sort_every,
+                   "shuffled_start": args.shuffle}}
+           if (args.tile_order, args.sort_every, args.shuffle) != (0, 1, False) else {}),
         "roofline": {"bound": "alu", "kernel": "k_mech (a5-a9)",
                      "achieved": achieved / 1e12, "peak": fp64_peak / 1e12,
                      "unit": "T fp64-inst/s", "frac": achieved / fp64_peak,
@@ -720,6 +736,12 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--mech-kernel", type=int, default=0, help="0 tile kernel, 1 reference")
+    ap.add_argument("--tile-order", type=int, default=0,
+                    help="row f1: 0 row-major tiles, 1 blocked Hilbert")
+    ap.add_argument("--sort-every", type=int, default=1,
+                    help="row f1: reorder the agents every K-th step (0 = never)")
+    ap.add_argument("--shuffle", action="store_true",
+                    help="start from a random memory order of the agents (row f1 sweeps)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     ws, rank, local = dist_env()

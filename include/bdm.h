@@ -357,6 +357,16 @@ bdm_status bdm_neighbor_pairs(bdm_handle h, const bdm_agents *a, double radius,
  *                  (warp per box, broadcast candidate stream); 0: reference formulation.
  *   "diffuse_tma"  1 (default) / 0: bdm_diffuse streams the grid planes with TMA box loads
  *                  (nx even); 0, or nx odd: the register/shared-memory stencil kernel.
+ *   "tile_order"   0 (default) row-major 4x4x4-box tiles; 1 blocked Hilbert: super-tiles
+ *                  of 8^3 tiles row-major, the tiles inside one along a 3-D Hilbert
+ *                  curve (the paper's Hilbert variant of agent
+ *                  sorting).  Changes only the memory order of the sorted
+ *                  agents; the slot array is re-sized at the next build.
+ *   "sort_every"   K >= 0 (default 1): the mechanics step leaves the caller's arrays in
+ *                  the grid's sorted order only on every K-th bdm_grid_build (counted
+ *                  from this call; 0 = never) and otherwise writes every agent back
+ *                  to its input index (the paper's sorting
+ *                  frequency).  The state per id is identical for every K.
  *   "prefilter"    1 (default) / 0: conservative fp32 candidate test in the tile kernel
  *                  (never rejects a neighbour; the exact fp64 test decides).
  *   "fuse_reduce"  0 (default) / 1: bdm_mech_step also reduces the extent of the new
@@ -364,8 +374,17 @@ bdm_status bdm_neighbor_pairs(bdm_handle h, const bdm_agents *a, double radius,
  *                  same arrays (same x pointer and n) skips its own reduction.  The
  *                  caller must not modify positions or diameters in between (every
  *                  other bdm_* call that changes agents clears the fused extent).
- * All settings produce bit-identical results.  Errors: BDM_EINVAL for an unknown name/value. */
+ * All settings produce bit-identical results (per agent id; "tile_order" and
+ * "sort_every" change only the memory order).  Errors: BDM_EINVAL for an unknown
+ * name/value. */
 bdm_status bdm_set_option(bdm_handle h, const char *name, int64_t value);
+
+/* Host-only query of the tile numbering inside an 8^3 super-tile (option "tile_order"):
+ * rank_out[x | y<<3 | z<<6] = position of local tile (x, y, z) along the curve, for
+ * order 0 (row-major, the identity) or 1 (3-D Hilbert curve, Skilling's transform).
+ * rank_out: caller-owned host array of 512 entries.  No GPU needed.
+ * Errors: BDM_EINVAL for NULL or a bad order. */
+bdm_status bdm_tile_curve(int32_t order, uint16_t *rank_out);
 
 /* Diagnostic: measured fp64 FMA throughput of this GPU (DFMA lane-operations per
  * second, i.e. half the fp64 FLOP/s) and the SM count.  Synchronizing. */

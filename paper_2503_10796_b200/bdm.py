@@ -26,7 +26,7 @@ EXPORTS = [
     "bdm_get_stats", "bdm_get_grid_info", "bdm_neighbor_pairs", "bdm_peak_dfma",
     "bdm_set_option", "bdm_grow_divide", "bdm_sir_step", "bdm_local_frame", "bdm_set_frame",
     "bdm_pack_slab", "bdm_append", "bdm_diffuse", "bdm_secrete", "bdm_chemotaxis",
-    "bdm_onco_step",
+    "bdm_onco_step", "bdm_tile_curve",
 ]
 PACK_MIGRATE, PACK_AURA = 1, 2
 
@@ -140,6 +140,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "bdm_secrete": [P, AG, P, i32, dbl, P, ctypes.POINTER(CGrid3), P],
         "bdm_chemotaxis": [P, AG, P, i32, dbl, P, ctypes.POINTER(CGrid3), P],
         "bdm_onco_step": [P, AG, P, i64, ctypes.POINTER(COncoParams), i64, P, P],
+        "bdm_tile_curve": [i32, P],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -154,6 +155,14 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
 def _check(status: int):
     if status != BDM_OK:
         raise BdmError(status, load_library().bdm_last_error().decode())
+
+
+def tile_curve(order: int):
+    """Host-only (bdm_tile_curve): curve position of each tile x | y<<3 | z<<6 of an
+    8^3 super-tile for tile_order `order` (0 row-major, 1 Hilbert), as a list."""
+    buf = (ctypes.c_uint16 * 512)()
+    _check(load_library().bdm_tile_curve(int(order), ctypes.cast(buf, ctypes.c_void_p)))
+    return list(buf)
 
 
 def _ptr(t):

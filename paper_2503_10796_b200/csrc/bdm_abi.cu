@@ -49,11 +49,11 @@ static bdm_status grow_agents(Ctx *c, int64_t n) {
     // exact on the first sizing (the caller's stated maximum), with slack on regrowth
     const int64_t cap = c->agent_cap == 0 ? n : n + n / 8 + 1024;
     // optional buffers are re-allocated at the new size on their next use
-    void *opt[] = {c->svol, c->div_rank, c->lrank, c->cls, c->cls2};
+    void *opt[] = {c->svol, c->div_rank, c->lrank, c->cls, c->cls2, c->perm};
     for (void *p : opt)
         if (p) cudaFree(p);
     c->svol = nullptr;
-    c->div_rank = c->lrank = c->cls = c->cls2 = nullptr;
+    c->div_rank = c->lrank = c->cls = c->cls2 = c->perm = nullptr;
     bdm_status s;
     if ((s = dalloc(&c->key, cap)) || (s = dalloc(&c->rank, cap)) ||
         (s = dalloc(&c->perm_tmp, cap)) || (s = dalloc(&c->skey, cap)) ||
@@ -131,6 +131,45 @@ static bdm_status read_latches(Ctx *c, bool clear) {
     return st;
 }
 
+// Skilling's transform (AxesToTranspose, "Programming the Hilbert curve", 2004) of
+// the b-bit coordinates X[0..n) into the transposed Hilbert index.
+static void axes_to_transpose(uint32_t *X, int b, int n) {
+    const uint32_t M = 1u << (b - 1);
+    for (uint32_t Q = M; Q > 1; Q >>= 1) {  // inverse undo
+        const uint32_t P = Q - 1;
+        for (int i = 0; i < n; ++i) {
+            if (X[i] & Q) {
+                X[0] ^= P;
+            } else {
+                const uint32_t t = (X[0] ^ X[i]) & P;
+                X[0] ^= t;
+                X[i] ^= t;
+            }
+        }
+    }
+    for (int i = 1; i < n; ++i) X[i] ^= X[i - 1];  // Gray encode
+    uint32_t t = 0;
+    for (uint32_t Q = M; Q > 1; Q >>= 1)
+        if (X[n - 1] & Q) t ^= Q - 1;
+    for (int i = 0; i < n; ++i) X[i] ^= t;
+}
+
+// Curve position of each tile (x | y<<3 | z<<6) of an 8^3 super-tile.
+static void tile_curve(int order, uint16_t *rank, uint16_t *inv) {
+    for (uint32_t l = 0; l < 512; ++l) {
+        uint32_t r = l;
+        if (order == 1) {
+            uint32_t X[3] = {l & 7u, (l >> 3) & 7u, l >> 6};
+            axes_to_transpose(X, 3, 3);
+            r = 0;
+            for (int b = 2; b >= 0; --b)
+                for (int i = 0; i < 3; ++i) r = (r << 1) | ((X[i] >> b) & 1u);
+        }
+        rank[l] = (uint16_t)r;
+        if (inv) inv[r] = (uint16_t)l;
+    }
+}
+
 }  // namespace bdm
 
 using namespace bdm;
@@ -177,7 +216,7 @@ bdm_status bdm_destroy(bdm_handle h) {
     Ctx *c = (Ctx *)h;
     cudaSetDevice(c->device);
     cudaDeviceSynchronize();
-    void *bufs[] = {c->key, c->rank, c->perm_tmp, c->skey, c->sid, c->sx, c->sy,
+    void *bufs[] = {c->key, c->rank, c->perm_tmp, c->skey, c->sid, c->perm, c->sx, c->sy,
                     c->sz, c->sd, c->sidf, c->sflags, c->svol, c->div_rank, c->box_start, c->dense_list,
                     c->onco_id, c->onco_out,
                     c->block_sums, c->pair_count, c->n_new, c->lrank, c->cls, c->cls2,
@@ -239,8 +278,10 @@ bdm_status bdm_grid_build(bdm_handle h, const bdm_agents *a, const bdm_agents *g
             cudaMemcpy(&c->sc->overflow, z, sizeof(z), cudaMemcpyHostToDevice);
             return fail(BDM_ENOTFINITE, "a position or diameter is NaN/Inf");
         }
-        const int64_t t0 = c->sc_host->T[0] + 4, t1 = c->sc_host->T[1] + 4,
-                      t2 = c->sc_host->T[2] + 4;
+        // (+8 in blocked Hilbert order: T is padded to whole super-tiles)
+        const int64_t pad = c->tile_order ? 8 : 4;
+        const int64_t t0 = c->sc_host->T[0] + pad, t1 = c->sc_host->T[1] + pad,
+                      t2 = c->sc_host->T[2] + pad;
         if ((s = grow_slots(c, t0 * t1 * t2 * 64)) != BDM_OK) return s;
         int32_t z[2] = {0, 0};
         BDM_CUDA_TRY(cudaMemcpy(&c->sc->overflow, z, sizeof(z), cudaMemcpyHostToDevice));
@@ -564,12 +605,44 @@ bdm_status bdm_set_option(bdm_handle h, const char *name, int64_t value) {
         c->dense = (int)value;
         return BDM_OK;
     }
+    if (strcmp(name, "tile_order") == 0) {
+        if (value < 0 || value > 1) return fail(BDM_EINVAL, "tile_order must be 0 or 1");
+        if (value == c->tile_order) return BDM_OK;
+        BDM_CUDA_TRY(cudaDeviceSynchronize());
+        uint16_t tab[1024];
+        tile_curve((int)value, tab, tab + 512);
+        const int32_t v = (int32_t)value;
+        BDM_CUDA_TRY(cudaMemcpy(c->sc->hilb, tab, sizeof(tab), cudaMemcpyHostToDevice));
+        BDM_CUDA_TRY(cudaMemcpy(&c->sc->tile_order, &v, sizeof(v), cudaMemcpyHostToDevice));
+        c->tile_order = (int)value;
+        // the slot layout changes: the next build re-sizes the slot array from its geometry
+        if (c->box_start) cudaFree(c->box_start);
+        if (c->dense_list) cudaFree(c->dense_list);
+        c->box_start = nullptr;
+        c->dense_list = nullptr;
+        c->slot_cap = 0;
+        c->grid_valid = false;
+        return BDM_OK;
+    }
+    if (strcmp(name, "sort_every") == 0) {
+        if (value < 0) return fail(BDM_EINVAL, "sort_every must be >= 0");
+        c->sort_every = value;
+        c->grid_builds = 0;
+        return BDM_OK;
+    }
     if (strcmp(name, "prefilter") == 0) {
         if (value < 0 || value > 1) return fail(BDM_EINVAL, "prefilter must be 0 or 1");
         c->prefilter = (int)value;
         return BDM_OK;
     }
     return fail(BDM_EINVAL, std::string("unknown option ") + name);
+}
+
+bdm_status bdm_tile_curve(int32_t order, uint16_t *rank_out) {
+    if (!rank_out) return fail(BDM_EINVAL, "rank_out is NULL");
+    if (order < 0 || order > 1) return fail(BDM_EINVAL, "order must be 0 or 1");
+    tile_curve((int)order, rank_out, nullptr);
+    return BDM_OK;
 }
 
 bdm_status bdm_peak_dfma(bdm_handle h, double *dfma_per_s, int32_t *sm_count) {

@@ -37,7 +37,7 @@ struct DevScalars {
     double R, R2, L;
     double o[3], hi[3];
     int32_t dims[3];
-    int32_t T[3];          // tiles per axis = ceil(dims / 4)
+    int32_t T[3];          // tiles per axis = ceil(dims / 4) (a multiple of 8 in Hilbert order)
     long long nslots;      // T0*T1*T2*64
     long long slot_cap;    // allocated slots (host-written)
     int32_t overflow;      // latched: nslots > slot_cap
@@ -48,6 +48,9 @@ struct DevScalars {
     unsigned int n_dense;  // dense tiles handed from the tile kernel to the dense kernel
     unsigned int dense_next;  // dense kernel work counter (box tasks taken)
     double dmax_prev;      // max diameter of the grid build's input (the step keeps it)
+    int32_t tile_order;    // option "tile_order" (row f1): 0 row-major tiles, 1 blocked Hilbert
+    uint16_t hilb[512];    // blocked Hilbert: local tile (x | y<<3 | z<<6) -> curve position
+    uint16_t hilb_inv[512];  // curve position -> local tile
 };
 
 // SIR workspace (kernels_sir.cu), allocated on first use
@@ -106,6 +109,11 @@ struct Ctx {
     int fuse_reduce = 0;   // option "fuse_reduce": next step's a1 extent from the mech epilogue
     int dense = 1;         // option "dense": dense regions go to the dense-box kernel
     int diffuse_tma = 1;   // option "diffuse_tma": TMA-pipelined stencil when nx is even
+    int tile_order = 0;    // option "tile_order" (row f1): 0 row-major, 1 blocked Hilbert
+    int64_t sort_every = 1;  // option "sort_every" (row f1): reorder the caller's SoA every K-th build
+    int64_t grid_builds = 0;
+    bool keep_order = false;  // this grid's mechanics writes back in the input order (via perm)
+    uint32_t *perm = nullptr; // sorted slot -> input index (optional, sort_every != 1)
     bool fused_valid = false;          // the scalars hold the extent of (fused_x, fused_n)
     const double *fused_x = nullptr;
     int64_t fused_n = 0;
@@ -164,13 +172,45 @@ __device__ inline double uniform53(uint32_t a, uint32_t b) {
 }
 __device__ inline double uniform32(uint32_t w) { return (double)w * 0x1p-32; }
 
-// Blocked-Morton slot of box (bx, by, bz) (R32): 4x4x4 tiles numbered row-major,
-// 6-bit Morton code inside the tile with x in the lowest bit.
-__device__ __forceinline__ uint32_t box_key(int bx, int by, int bz, int T0, int T1) {
-    const uint32_t tile = (uint32_t)(((bz >> 2) * T1 + (by >> 2)) * T0 + (bx >> 2));
+// Tile numbering (R32, row f1).  Row-major: (tz*T1 + ty)*T0 + tx.  Blocked Hilbert
+// (hilb != NULL, T0 and T1 multiples of 8): super-tiles of 8^3 tiles numbered row-major,
+// the 512 tiles inside a super-tile along a 3-D Hilbert curve (table in DevScalars).
+__device__ __forceinline__ uint32_t tile_rank(int tx, int ty, int tz, int T0, int T1,
+                                              const uint16_t *hilb) {
+    if (!hilb) return (uint32_t)((tz * T1 + ty) * T0 + tx);
+    const uint32_t sup = (uint32_t)(((tz >> 3) * (T1 >> 3) + (ty >> 3)) * (T0 >> 3) + (tx >> 3));
+    return sup * 512u + hilb[((tz & 7) << 6) | ((ty & 7) << 3) | (tx & 7)];
+}
+// inverse of tile_rank
+__device__ __forceinline__ void tile_xyz(uint32_t t, int T0, int T1, const uint16_t *hilb_inv,
+                                         int &tx, int &ty, int &tz) {
+    if (!hilb_inv) {
+        tx = (int)(t % (uint32_t)T0);
+        ty = (int)((t / (uint32_t)T0) % (uint32_t)T1);
+        tz = (int)(t / ((uint32_t)T0 * (uint32_t)T1));
+        return;
+    }
+    const uint32_t sup = t >> 9, h = hilb_inv[t & 511u];
+    const uint32_t S0 = (uint32_t)T0 >> 3, S1 = (uint32_t)T1 >> 3;
+    tx = (int)((sup % S0) * 8u + (h & 7u));
+    ty = (int)(((sup / S0) % S1) * 8u + ((h >> 3) & 7u));
+    tz = (int)((sup / (S0 * S1)) * 8u + (h >> 6));
+}
+
+// Slot of box (bx, by, bz): tile number * 64 + the 6-bit Morton code inside the 4x4x4
+// tile, x in the lowest bit.
+__device__ __forceinline__ uint32_t box_key(int bx, int by, int bz, int T0, int T1,
+                                            const uint16_t *hilb = nullptr) {
+    const uint32_t tile = tile_rank(bx >> 2, by >> 2, bz >> 2, T0, T1, hilb);
     const uint32_t m = (uint32_t)((bx & 1) | ((by & 1) << 1) | ((bz & 1) << 2) |
                                   ((bx & 2) << 2) | ((by & 2) << 3) | ((bz & 2) << 4));
     return tile * 64u + m;
+}
+__device__ __forceinline__ const uint16_t *sc_hilb(const DevScalars *sc) {
+    return sc->tile_order ? sc->hilb : nullptr;
+}
+__device__ __forceinline__ const uint16_t *sc_hilb_inv(const DevScalars *sc) {
+    return sc->tile_order ? sc->hilb_inv : nullptr;
 }
 
 // R28: deterministic cube root.  v = m 2^e (frexp, m in [0.5, 1)); y0 = 2^k with

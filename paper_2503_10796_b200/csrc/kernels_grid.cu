@@ -143,6 +143,7 @@ __global__ void k_setup(DevScalars *sc, double radius, const double *__restrict_
         const int dim = bad ? 1 : (int)ext + 1;
         sc->dims[a] = dim;
         sc->T[a] = (dim + 3) >> 2;
+        if (sc->tile_order) sc->T[a] = (sc->T[a] + 7) & ~7;  // whole 8^3 super-tiles
         ns *= (long long)sc->T[a];
         if (ns > (1ll << 40)) bad = true;
     }
@@ -213,7 +214,7 @@ __global__ void __launch_bounds__(256) k_key(Src S, const DevScalars *__restrict
     const int bx = (int)floor((px - sc->o[0]) / L) - sc->boff[0];
     const int by = (int)floor((py - sc->o[1]) / L) - sc->boff[1];
     const int bz = (int)floor((pz - sc->o[2]) / L) - sc->boff[2];
-    const uint32_t k = box_key(bx, by, bz, sc->T[0], sc->T[1]);
+    const uint32_t k = box_key(bx, by, bz, sc->T[0], sc->T[1], sc_hilb(sc));
     key[i] = k;
     rank[i] = atomicAdd(&counts[k], 1u);
 }
@@ -352,7 +353,7 @@ __global__ void __launch_bounds__(256) k_fix_gather(
     const uint32_t *__restrict__ perm_tmp, const uint32_t *__restrict__ box_start,
     double *__restrict__ sx, double *__restrict__ sy, double *__restrict__ sz,
     double *__restrict__ sd, uint32_t *__restrict__ sidf, uint32_t *__restrict__ sflags,
-    double *__restrict__ svol, uint32_t *__restrict__ lflag,
+    double *__restrict__ svol, uint32_t *__restrict__ lflag, uint32_t *__restrict__ perm,
     const DevScalars *__restrict__ sc) {
     if (sc->overflow) return;
     const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -368,6 +369,7 @@ __global__ void __launch_bounds__(256) k_fix_gather(
     for (uint32_t t = lo; t < hi; ++t) r += (sid[t] < me);
     const uint32_t dst = lo + r;
     const uint32_t src = perm_tmp[s];
+    if (perm) perm[dst] = src;  // sort_every != 1: the mechanics writes back to src
     if ((int64_t)src < S.nl) {
         sx[dst] = S.x[src];
         sy[dst] = S.y[src];
@@ -410,6 +412,12 @@ bdm_status launch_grid_sort(Ctx *c, const bdm_agents *a, const bdm_agents *g, cu
     bdm_status s;
     if (S.vol && (s = need_agent_buf(c, &c->svol)) != BDM_OK) return s;
     if (S.ng > 0 && (s = need_agent_buf(c, &c->lrank)) != BDM_OK) return s;
+    // row f1: physically reorder the caller's SoA only on every sort_every-th build
+    // (0: never); otherwise the mechanics writes each agent back to its input index
+    c->keep_order = c->sort_every != 1 &&
+                    (c->sort_every == 0 || c->grid_builds % c->sort_every != 0);
+    ++c->grid_builds;
+    if (c->keep_order && (s = need_agent_buf(c, &c->perm)) != BDM_OK) return s;
     k_key<<<nb, threads, 0, st>>>(S, c->sc, c->key, c->rank, c->box_start);
     const unsigned sb = (unsigned)((c->slot_cap + 1 + kScanTile - 1) / kScanTile);
     k_scan_reduce<<<sb, kScanThreads, 0, st>>>(c->box_start, c->block_sums, c->sc, 0);
@@ -420,7 +428,7 @@ bdm_status launch_grid_sort(Ctx *c, const bdm_agents *a, const bdm_agents *g, cu
     uint32_t *lflag = S.ng > 0 ? c->lrank : nullptr;
     k_fix_gather<<<(unsigned)((n + 1 + threads - 1) / threads), threads, 0, st>>>(
         S, c->skey, c->sid, c->perm_tmp, c->box_start, c->sx, c->sy, c->sz, c->sd, c->sidf,
-        c->sflags, c->svol, lflag, c->sc);
+        c->sflags, c->svol, lflag, c->keep_order ? c->perm : nullptr, c->sc);
     c->launches += 7;
     BDM_LAUNCH_CHECK("grid sort");
     if (S.ng > 0) return launch_scan_u32(c, c->lrank, n + 1, st);  // output index of locals

@@ -54,6 +54,7 @@ struct GridView {
     double L, R2, o0, o1, o2;
     int D0, D1, D2, T0, T1, T2;
     int b0, b1, b2;  // lattice offset (global frame, 8(e))
+    const uint16_t *hilb, *hilb_inv;  // tile numbering (NULL: row-major)
 };
 __device__ __forceinline__ GridView load_grid(const DevScalars *__restrict__ sc) {
     GridView g;
@@ -61,6 +62,8 @@ __device__ __forceinline__ GridView load_grid(const DevScalars *__restrict__ sc)
     g.b0 = sc->boff[0]; g.b1 = sc->boff[1]; g.b2 = sc->boff[2];
     g.D0 = sc->dims[0]; g.D1 = sc->dims[1]; g.D2 = sc->dims[2];
     g.T0 = sc->T[0]; g.T1 = sc->T[1]; g.T2 = sc->T[2];
+    g.hilb = sc_hilb(sc);
+    g.hilb_inv = sc_hilb_inv(sc);
     return g;
 }
 
@@ -143,7 +146,7 @@ __device__ __forceinline__ void mech_agent_global(const MechArgs &A, const GridV
                 for (int dx = -1; dx <= 1 && is_static; ++dx) {
                     const int cx = bx + dx;
                     if (cx < 0 || cx >= g.D0) continue;
-                    const uint32_t key = box_key(cx, cy, cz, g.T0, g.T1);
+                    const uint32_t key = box_key(cx, cy, cz, g.T0, g.T1, g.hilb);
                     const uint32_t b0 = A.box_start[key], b1 = A.box_start[key + 1];
                     for (uint32_t t = b0; t < b1; ++t) {
                         if (t == (uint32_t)s) continue;
@@ -172,7 +175,7 @@ __device__ __forceinline__ void mech_agent_global(const MechArgs &A, const GridV
                 for (int dx = -1; dx <= 1; ++dx) {
                     const int cx = bx + dx;
                     if (cx < 0 || cx >= g.D0) continue;
-                    const uint32_t key = box_key(cx, cy, cz, g.T0, g.T1);
+                    const uint32_t key = box_key(cx, cy, cz, g.T0, g.T1, g.hilb);
                     const uint32_t b0 = A.box_start[key], b1 = A.box_start[key + 1];
                     for (uint32_t t = b0; t < b1; ++t) {
                         if (t == (uint32_t)s) continue;
@@ -347,8 +350,8 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_mech_tile(MechArgs A, DevSc
     Counts c;
 
     for (long long t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        const int tx = (int)(t % g.T0), ty = (int)((t / g.T0) % g.T1);
-        const int tz = (int)(t / ((long long)g.T0 * g.T1));
+        int tx, ty, tz;
+        tile_xyz((uint32_t)t, g.T0, g.T1, g.hilb_inv, tx, ty, tz);
         const int bx0 = 4 * tx - 1, by0 = 4 * ty - 1, bz0 = 4 * tz - 1;
         const uint32_t g0 = A.box_start[(uint32_t)t * 64u];
         const uint32_t g1 = A.box_start[(uint32_t)t * 64u + 64u];
@@ -359,7 +362,7 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_mech_tile(MechArgs A, DevSc
             const int gx = bx0 + lb % 6, gy = by0 + (lb / 6) % 6, gz = bz0 + lb / 36;
             uint32_t st = 0, cnt = 0;
             if (gx >= 0 && gy >= 0 && gz >= 0 && gx < g.D0 && gy < g.D1 && gz < g.D2) {
-                const uint32_t key = box_key(gx, gy, gz, g.T0, g.T1);
+                const uint32_t key = box_key(gx, gy, gz, g.T0, g.T1, g.hilb);
                 st = A.box_start[key];
                 cnt = A.box_start[key + 1] - st;
             }
@@ -1009,8 +1012,11 @@ __global__ void __launch_bounds__(kT6Threads, kMinBlocks) k_mech_tile6(MechArgs 
               gsz = (int)gridDim.x / (T0 * T1);
     int tx = (int)blockIdx.x % T0, ty = ((int)blockIdx.x / T0) % T1, tz = (int)blockIdx.x / (T0 * T1);
 
+    const uint16_t *const hilb = S.g.hilb, *const hilb_inv = S.g.hilb_inv;
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        if (t != (int)blockIdx.x) {
+        if (hilb_inv) {
+            tile_xyz((uint32_t)t, T0, T1, hilb_inv, tx, ty, tz);
+        } else if (t != (int)blockIdx.x) {
             tx += gsx;
             ty += gsy;
             tz += gsz;
@@ -1028,7 +1034,7 @@ __global__ void __launch_bounds__(kT6Threads, kMinBlocks) k_mech_tile6(MechArgs 
                       gz = bz0 + (int)((v >> 6) & 7u);
             uint32_t st = 0, cn = 0;
             if (gx >= 0 && gy >= 0 && gz >= 0 && gx < S.g.D0 && gy < S.g.D1 && gz < S.g.D2) {
-                const uint32_t key = box_key(gx, gy, gz, T0, T1);
+                const uint32_t key = box_key(gx, gy, gz, T0, T1, hilb);
                 st = A.box_start[key];
                 cn = A.box_start[key + 1] - st;
             }
@@ -1263,7 +1269,8 @@ __global__ void __launch_bounds__(32 * kDWarps, 4) k_mech_dense(MechArgs A, DevS
         if (item >= ntask) break;
         const int t = (int)A.dense_list[item >> 6];
         const uint32_t mort = item & 63u;
-        const int tx = t % g.T0, ty = (t / g.T0) % g.T1, tz = t / (g.T0 * g.T1);
+        int tx, ty, tz;
+        tile_xyz((uint32_t)t, g.T0, g.T1, g.hilb_inv, tx, ty, tz);
         const int bx = 4 * tx + (int)((mort & 1u) | ((mort >> 2) & 2u));
         const int by = 4 * ty + (int)(((mort >> 1) & 1u) | ((mort >> 3) & 2u));
         const int bz = 4 * tz + (int)(((mort >> 2) & 1u) | ((mort >> 4) & 2u));
@@ -1280,7 +1287,7 @@ __global__ void __launch_bounds__(32 * kDWarps, 4) k_mech_dense(MechArgs A, DevS
                 const int dz = lane / 9 - 1, dy = (lane / 3) % 3 - 1, dx = lane % 3 - 1;
                 const int cx = bx + dx, cy = by + dy, cz = bz + dz;
                 if (cx >= 0 && cy >= 0 && cz >= 0 && cx < g.D0 && cy < g.D1 && cz < g.D2) {
-                    const uint32_t k2 = box_key(cx, cy, cz, g.T0, g.T1);
+                    const uint32_t k2 = box_key(cx, cy, cz, g.T0, g.T1, g.hilb);
                     st = A.box_start[k2];
                     cn = A.box_start[k2 + 1] - st;
                 }
@@ -1508,7 +1515,7 @@ bdm_status launch_mech(Ctx *c, bdm_agents *a, const bdm_params *p, cudaStream_t 
     A.sid = c->sidf; A.skey = c->skey; A.sflags = c->sflags; A.box_start = c->box_start;
     A.ox = a->x; A.oy = a->y; A.oz = a->z; A.od = a->diameter; A.oid = a->id; A.oflags = a->flags;
     A.svol = a->volume ? c->svol : nullptr;
-    A.lrank = c->grid_ng > 0 ? c->lrank : nullptr;
+    A.lrank = c->keep_order ? c->perm : (c->grid_ng > 0 ? c->lrank : nullptr);
     A.ovol = a->volume;
     A.k = p->k; A.gamma = p->gamma; A.dt = p->dt; A.max_disp = p->max_displacement;
     A.tau = p->force_threshold;
@@ -1574,7 +1581,7 @@ __global__ void __launch_bounds__(256) k_pairs(int64_t n, const double *__restri
                 if (cx < 0 || cy < 0 || cz < 0 || cx >= sc->dims[0] || cy >= sc->dims[1] ||
                     cz >= sc->dims[2])
                     continue;
-                const uint32_t key = box_key(cx, cy, cz, sc->T[0], sc->T[1]);
+                const uint32_t key = box_key(cx, cy, cz, sc->T[0], sc->T[1], sc_hilb(sc));
                 for (uint32_t t = box_start[key]; t < box_start[key + 1]; ++t) {
                     if (t == (uint32_t)s) continue;
                     const double ex = xi - sx[t], ey = yi - sy[t], ez = zi - sz[t];
