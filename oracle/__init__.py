@@ -19,6 +19,10 @@ Parity status per function (DESIGN.md section 4 lists the pins):
   diffuse_step         pinned (discrete sine eigenmodes, decay-only, mass conservation,
                        convergence to the heat kernel at sqrt(1000) um)
   secrete, chemotaxis  pinned (closed forms: k agents per cell, linear fields)
+  lz4_*, aura_*        pinned (LZ4 block-format streams built by hand from the format
+                       definition, round trips, worst-case expansion bound, zero runs;
+                       delta encoding: XOR identities, placeholders, new agents, the
+                       reference-order defragmentation of P:6350-6352)
   onco_step            pinned (unit Brownian steps, exact age/volume bookkeeping, the
                        age gate, death / division frequencies within 5 sigma, removal
                        invariants, id uniqueness, population accounting)
@@ -102,6 +106,21 @@ def lib() -> ctypes.CDLL:
         L.orc_init_ages.argtypes = [i64, P, u64, ctypes.c_uint32, P]
         L.orc_secrete.argtypes = [i64, P, P, P, P, i32, dbl, P, i64, i64, i64, P, dbl, dbl, dbl]
         L.orc_chemotaxis.argtypes = [i64, P, P, P, P, i32, dbl, P, i64, i64, i64, P, dbl, dbl, dbl]
+        u8p = P
+        L.orc_lz4_compress_block.argtypes = [u8p, i64, u8p, i64]
+        L.orc_lz4_compress_block.restype = i64
+        L.orc_lz4_decompress_block.argtypes = [u8p, i64, u8p, i64]
+        L.orc_lz4_decompress_block.restype = i64
+        L.orc_aura_payload_size.argtypes = [i64, i64]
+        L.orc_aura_payload_size.restype = i64
+        L.orc_aura_payload.argtypes = [i64, P, P, P, P, P, P, i64, P, P, P, P, P, P, P, P]
+        L.orc_aura_payload.restype = i64
+        L.orc_aura_unpayload.argtypes = [P, i64, i64, P, P, P, P, P, P, P, P, P, P, P, P]
+        L.orc_aura_unpayload.restype = i64
+        L.orc_aura_compress.argtypes = [P, i64, i64, i64, P, i64]
+        L.orc_aura_compress.restype = i64
+        L.orc_aura_decompress.argtypes = [P, i64, P, i64, P, P]
+        L.orc_aura_decompress.restype = i64
         _lib = L
     return _lib
 
@@ -504,3 +523,87 @@ def onco_full_step(s, mp: MechParams, p: OncoParams, id_next: int):
             "age": np.asarray(s["age"], np.uint32)[perm]}
     new, nxt = onco_step(post, p, id_next)
     return new, cnt, nxt
+
+
+# ---------------------------------------------------------------- row f3 (R46-R51)
+AURA_FIELDS = ("x", "y", "z", "d", "id", "flags")
+
+
+def lz4_compress_block(data: bytes) -> bytes:
+    """R50 greedy LZ4 block of data (<= 65535 bytes)."""
+    src = np.frombuffer(bytes(data), np.uint8).copy()
+    cap = len(src) + len(src) // 255 + 16
+    dst = np.zeros(cap, np.uint8)
+    k = lib().orc_lz4_compress_block(_p(src), len(src), _p(dst), cap)
+    assert k >= 0
+    return dst[:k].tobytes()
+
+
+def lz4_decompress_block(data: bytes, cap: int) -> bytes:
+    """LZ4 block decoder; raises ValueError on a malformed block."""
+    src = np.frombuffer(bytes(data), np.uint8).copy()
+    dst = np.zeros(max(cap, 1), np.uint8)
+    k = lib().orc_lz4_decompress_block(_p(src), len(src), _p(dst), cap)
+    if k < 0:
+        raise ValueError("malformed LZ4 block")
+    return dst[:k].tobytes()
+
+
+def _soa(s):
+    return [_f64(s[k]) for k in ("x", "y", "z", "d")] + [_u32(s["id"]), _u32(s["flags"])]
+
+
+def aura_reference(msg):
+    """R46: a reference is a message in ascending id order."""
+    o = np.argsort(np.asarray(msg["id"], np.uint32), kind="stable")
+    return {k: np.ascontiguousarray(np.asarray(msg[k])[o]) for k in AURA_FIELDS}
+
+
+def aura_payload(msg, ref):
+    """R47-R49: (payload bytes, nnew)."""
+    m, r = _soa(msg), _soa(ref)
+    n, nref = len(m[0]), len(r[0])
+    out = np.zeros(max(lib().orc_aura_payload_size(nref, n), 1), np.uint8)
+    nnew = ctypes.c_int64()
+    size = lib().orc_aura_payload(n, *[_p(a) for a in m], nref, *[_p(a) for a in r], _p(out),
+                                  ctypes.byref(nnew))
+    return out[:size].tobytes(), int(nnew.value)
+
+
+def aura_unpayload(payload: bytes, ref, nnew: int):
+    """R51: the message (reference order, then new agents)."""
+    r = _soa(ref)
+    nref = len(r[0])
+    buf = np.frombuffer(bytes(payload), np.uint8).copy()
+    cap = nref + nnew
+    out = {k: np.zeros(max(cap, 1), np.float64) for k in ("x", "y", "z", "d")}
+    out.update({k: np.zeros(max(cap, 1), np.uint32) for k in ("id", "flags")})
+    m = lib().orc_aura_unpayload(_p(buf), nref, nnew, *[_p(a) for a in r],
+                                 *[_p(out[k]) for k in AURA_FIELDS])
+    return {k: v[:m] for k, v in out.items()}
+
+
+def aura_encode(msg, ref) -> bytes:
+    """R46-R50: the compressed stream of msg against ref."""
+    payload, nnew = aura_payload(msg, ref)
+    src = np.frombuffer(payload, np.uint8).copy() if payload else np.zeros(1, np.uint8)
+    size = len(payload)
+    cap = 40 + 4 * (size // 4096 + 1) + size + size // 255 + 16 * (size // 4096 + 1) + 16
+    out = np.zeros(cap, np.uint8)
+    k = lib().orc_aura_compress(_p(src), size, len(ref["id"]), nnew, _p(out), cap)
+    assert k >= 0
+    return out[:k].tobytes()
+
+
+def aura_decode(stream: bytes, ref):
+    """Inverse of aura_encode (R51)."""
+    src = np.frombuffer(bytes(stream), np.uint8).copy()
+    cap = max(int(np.frombuffer(src[24:32].tobytes(), np.uint64)[0]) if len(src) >= 32 else 0, 1)
+    pay = np.zeros(cap, np.uint8)
+    nref, nnew = ctypes.c_int64(), ctypes.c_int64()
+    size = lib().orc_aura_decompress(_p(src), len(src), _p(pay), cap, ctypes.byref(nref),
+                                     ctypes.byref(nnew))
+    if size < 0:
+        raise ValueError("malformed aura stream")
+    assert nref.value == len(ref["id"])
+    return aura_unpayload(pay[:size].tobytes(), ref, int(nnew.value))

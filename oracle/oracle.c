@@ -1073,3 +1073,306 @@ void orc_init_ages(int64_t n, const uint32_t *id, uint64_t seed, uint32_t max_ag
         age[k] = (uint32_t)floor(orc_u32(w[0]) * (double)max_age);
     }
 }
+
+/* ===================================================================== row f3
+ * Delta-encoded + LZ4-compressed aura messages (sec. "Data Transfer Minimization",
+ * P:6291-6356; evaluation P:6911-6937 with LZ4 [lz4]).  Readings R46-R51:
+ *
+ *   R46 the reference is a previous aura message held by sender and receiver, kept in
+ *       ascending id order;
+ *   R47 matching: slot r < nref carries the message agent whose id is
+ *       ref.id[r], or a placeholder (presence bit 0); agents not in the reference
+ *       follow at slots nref.. in message order;
+ *   R48 "the difference" of a matched agent is the XOR of the IEEE bit patterns of
+ *       x, y, z, d and of flags (lossless; id is implied by the slot); placeholders
+ *       carry zeros; new agents carry their raw bits and their id;
+ *   R49 payload layout: presence words, then the x, y, z, d columns over all
+ *       nref + nnew slots each split into 8 byte planes, flags into 4 byte planes,
+ *       then the ids of the new agents (little-endian);
+ *   R50 LZ4 block format, payload cut into independent 4096-byte chunks, greedy
+ *       parse with an 11-bit hash of the next 4 bytes (h = (v * 2654435761) >> 21,
+ *       one candidate per bucket, updated at every position the parse visits), match
+ *       >= 4 bytes, a match starts before n - 12 and ends by n - 5;
+ *   R51 decoding restores the message in reference order (placeholders removed,
+ *       P:6350-6352), then the new agents.
+ * Stream: u32 magic 'BDA1', u32 chunk size, u64 nref, u64 nnew, u64 payload bytes,
+ * u32 nchunks, u32 0, u32 compressed size per chunk, the chunks. */
+
+#define ORC_LZ4_CHUNK 4096
+#define ORC_LZ4_HBITS 11
+
+static uint32_t rd32(const uint8_t *p)
+{
+    return (uint32_t)p[0] | ((uint32_t)p[1] << 8) | ((uint32_t)p[2] << 16) | ((uint32_t)p[3] << 24);
+}
+
+static int64_t lz4_put_len(uint8_t *dst, int64_t o, int64_t cap, int64_t L)
+{
+    while (L >= 255) {
+        if (o >= cap) return -1;
+        dst[o++] = 255;
+        L -= 255;
+    }
+    if (o >= cap) return -1;
+    dst[o++] = (uint8_t)L;
+    return o;
+}
+
+/* One sequence: literals src[a, a+nlit), then (if mlen > 0) a match of mlen bytes at
+ * distance off.  Returns the new output position or -1 (no room). */
+static int64_t lz4_sequence(const uint8_t *src, int64_t a, int64_t nlit, int64_t off, int64_t mlen,
+                            uint8_t *dst, int64_t o, int64_t cap)
+{
+    if (o >= cap) return -1;
+    int64_t tok = o++;
+    uint8_t t = (uint8_t)((nlit < 15 ? nlit : 15) << 4);
+    if (nlit >= 15 && (o = lz4_put_len(dst, o, cap, nlit - 15)) < 0) return -1;
+    if (o + nlit > cap) return -1;
+    memcpy(dst + o, src + a, (size_t)nlit);
+    o += nlit;
+    if (mlen > 0) {
+        if (o + 2 > cap) return -1;
+        dst[o++] = (uint8_t)(off & 255);
+        dst[o++] = (uint8_t)(off >> 8);
+        int64_t m = mlen - 4;
+        t |= (uint8_t)(m < 15 ? m : 15);
+        if (m >= 15 && (o = lz4_put_len(dst, o, cap, m - 15)) < 0) return -1;
+    }
+    dst[tok] = t;
+    return o;
+}
+
+/* R50: compress one block of n <= 65535 bytes.  Returns the compressed size or -1. */
+int64_t orc_lz4_compress_block(const uint8_t *src, int64_t n, uint8_t *dst, int64_t cap)
+{
+    int32_t table[1 << ORC_LZ4_HBITS];
+    for (int k = 0; k < (1 << ORC_LZ4_HBITS); ++k) table[k] = -1;
+    int64_t ip = 0, anchor = 0, o = 0;
+    if (n >= 13) {
+        while (ip < n - 12) {
+            uint32_t v = rd32(src + ip);
+            uint32_t h = (uint32_t)(v * 2654435761u) >> (32 - ORC_LZ4_HBITS);
+            int32_t ref = table[h];
+            table[h] = (int32_t)ip;
+            if (ref >= 0 && rd32(src + ref) == v) {
+                int64_t len = 4;
+                while (ip + len < n - 5 && src[ref + len] == src[ip + len]) ++len;
+                o = lz4_sequence(src, anchor, ip - anchor, ip - ref, len, dst, o, cap);
+                if (o < 0) return -1;
+                ip += len;
+                anchor = ip;
+            } else {
+                ++ip;
+            }
+        }
+    }
+    o = lz4_sequence(src, anchor, n - anchor, 0, 0, dst, o, cap);
+    return o;
+}
+
+/* LZ4 block decoder (format definition).  Returns the decoded size or -1 (malformed or
+ * more than cap bytes). */
+int64_t orc_lz4_decompress_block(const uint8_t *src, int64_t n, uint8_t *dst, int64_t cap)
+{
+    int64_t i = 0, o = 0;
+    while (i < n) {
+        uint8_t t = src[i++];
+        int64_t nlit = t >> 4;
+        if (nlit == 15) {
+            uint8_t b;
+            do {
+                if (i >= n) return -1;
+                b = src[i++];
+                nlit += b;
+            } while (b == 255);
+        }
+        if (i + nlit > n || o + nlit > cap) return -1;
+        memcpy(dst + o, src + i, (size_t)nlit);
+        i += nlit;
+        o += nlit;
+        if (i == n) break;  /* the last sequence has literals only */
+        if (i + 2 > n) return -1;
+        int64_t off = (int64_t)src[i] | ((int64_t)src[i + 1] << 8);
+        i += 2;
+        int64_t mlen = (t & 15) + 4;
+        if ((t & 15) == 15) {
+            uint8_t b;
+            do {
+                if (i >= n) return -1;
+                b = src[i++];
+                mlen += b;
+            } while (b == 255);
+        }
+        if (off == 0 || off > o || o + mlen > cap) return -1;
+        for (int64_t k = 0; k < mlen; ++k, ++o) dst[o] = dst[o - off]; /* may overlap */
+    }
+    return o;
+}
+
+static uint64_t bits64(double v)
+{
+    uint64_t b;
+    memcpy(&b, &v, 8);
+    return b;
+}
+
+static double from_bits64(uint64_t b)
+{
+    double v;
+    memcpy(&v, &b, 8);
+    return v;
+}
+
+static int64_t find_id(const uint32_t *ids, int64_t n, uint32_t id)
+{
+    int64_t lo = 0, hi = n;
+    while (lo < hi) {
+        int64_t mid = lo + (hi - lo) / 2;
+        if (ids[mid] < id) lo = mid + 1; else hi = mid;
+    }
+    return (lo < n && ids[lo] == id) ? lo : -1;
+}
+
+/* Payload size for nref reference slots and nnew new agents (R49). */
+int64_t orc_aura_payload_size(int64_t nref, int64_t nnew)
+{
+    int64_t ns = nref + nnew;
+    return 4 * ((nref + 31) / 32) + 4 * 8 * ns + 4 * ns + 4 * nnew;
+}
+
+/* R46-R49: the uncompressed payload of message (n agents) against the reference
+ * (nref agents, ascending ids).  *nnew_out = agents not in the reference.  The payload
+ * buffer must hold orc_aura_payload_size(nref, n) bytes.  Returns the payload size. */
+int64_t orc_aura_payload(int64_t n, const double *x, const double *y, const double *z,
+                         const double *d, const uint32_t *id, const uint32_t *flags,
+                         int64_t nref, const double *rx, const double *ry, const double *rz,
+                         const double *rd, const uint32_t *rid, const uint32_t *rflags,
+                         uint8_t *out, int64_t *nnew_out)
+{
+    int64_t *slot_of = (int64_t *)malloc((size_t)(n > 0 ? n : 1) * sizeof(int64_t));
+    int64_t nnew = 0;
+    for (int64_t i = 0; i < n; ++i) {
+        int64_t r = find_id(rid, nref, id[i]);
+        slot_of[i] = r >= 0 ? r : nref + nnew++;
+    }
+    int64_t ns = nref + nnew, nw = (nref + 31) / 32;
+    int64_t size = orc_aura_payload_size(nref, nnew);
+    memset(out, 0, (size_t)size);
+    uint8_t *pres = out;
+    uint8_t *col = out + 4 * nw;             /* x, y, z, d: 8 planes of ns bytes each */
+    uint8_t *fcol = col + 4 * 8 * ns;        /* flags: 4 planes */
+    uint8_t *nid = fcol + 4 * ns;            /* ids of the new agents */
+    for (int64_t i = 0; i < n; ++i) {
+        int64_t s = slot_of[i];
+        const double mv[4] = {x[i], y[i], z[i], d[i]};
+        uint64_t v[4];
+        uint32_t f = flags[i];
+        if (s < nref) {
+            const double rv[4] = {rx[s], ry[s], rz[s], rd[s]};
+            for (int c = 0; c < 4; ++c) v[c] = bits64(mv[c]) ^ bits64(rv[c]);
+            f ^= rflags[s];
+            pres[4 * (s / 32) + (s % 32) / 8] |= (uint8_t)(1u << (s % 8));
+        } else {
+            for (int c = 0; c < 4; ++c) v[c] = bits64(mv[c]);
+            int64_t j = s - nref;
+            for (int b = 0; b < 4; ++b) nid[4 * j + b] = (uint8_t)(id[i] >> (8 * b));
+        }
+        for (int c = 0; c < 4; ++c)
+            for (int b = 0; b < 8; ++b) col[(int64_t)(8 * c + b) * ns + s] = (uint8_t)(v[c] >> (8 * b));
+        for (int b = 0; b < 4; ++b) fcol[(int64_t)b * ns + s] = (uint8_t)(f >> (8 * b));
+    }
+    free(slot_of);
+    *nnew_out = nnew;
+    return size;
+}
+
+/* R51: the message back from a payload and the reference; returns its size n
+ * (reference-order survivors, then the new agents). */
+int64_t orc_aura_unpayload(const uint8_t *in, int64_t nref, int64_t nnew, const double *rx,
+                           const double *ry, const double *rz, const double *rd,
+                           const uint32_t *rid, const uint32_t *rflags, double *x, double *y,
+                           double *z, double *d, uint32_t *id, uint32_t *flags)
+{
+    int64_t ns = nref + nnew, nw = (nref + 31) / 32;
+    const uint8_t *pres = in, *col = in + 4 * nw, *fcol = col + 4 * 8 * ns, *nid = fcol + 4 * ns;
+    int64_t m = 0;
+    for (int64_t s = 0; s < ns; ++s) {
+        int present = s >= nref || ((pres[4 * (s / 32) + (s % 32) / 8] >> (s % 8)) & 1);
+        if (!present) continue;
+        uint64_t v[4] = {0, 0, 0, 0};
+        uint32_t f = 0;
+        for (int c = 0; c < 4; ++c)
+            for (int b = 0; b < 8; ++b) v[c] |= (uint64_t)col[(int64_t)(8 * c + b) * ns + s] << (8 * b);
+        for (int b = 0; b < 4; ++b) f |= (uint32_t)fcol[(int64_t)b * ns + s] << (8 * b);
+        if (s < nref) {
+            const double rv[4] = {rx[s], ry[s], rz[s], rd[s]};
+            for (int c = 0; c < 4; ++c) v[c] ^= bits64(rv[c]);
+            f ^= rflags[s];
+            id[m] = rid[s];
+        } else {
+            int64_t j = s - nref;
+            id[m] = (uint32_t)nid[4 * j] | ((uint32_t)nid[4 * j + 1] << 8) |
+                    ((uint32_t)nid[4 * j + 2] << 16) | ((uint32_t)nid[4 * j + 3] << 24);
+        }
+        x[m] = from_bits64(v[0]);
+        y[m] = from_bits64(v[1]);
+        z[m] = from_bits64(v[2]);
+        d[m] = from_bits64(v[3]);
+        flags[m] = f;
+        ++m;
+    }
+    return m;
+}
+
+/* R50: the stream of a payload (header, sizes, LZ4 chunks).  Returns its size or -1. */
+int64_t orc_aura_compress(const uint8_t *payload, int64_t size, int64_t nref, int64_t nnew,
+                          uint8_t *out, int64_t cap)
+{
+    int64_t nch = (size + ORC_LZ4_CHUNK - 1) / ORC_LZ4_CHUNK;
+    int64_t hdr = 40 + 4 * nch;
+    if (cap < hdr) return -1;
+    uint32_t h32[2] = {0x31414442u, ORC_LZ4_CHUNK};
+    uint64_t h64[3] = {(uint64_t)nref, (uint64_t)nnew, (uint64_t)size};
+    uint32_t t32[2] = {(uint32_t)nch, 0u};
+    memcpy(out, h32, 8);
+    memcpy(out + 8, h64, 24);
+    memcpy(out + 32, t32, 8);
+    int64_t o = hdr;
+    for (int64_t c = 0; c < nch; ++c) {
+        int64_t a = c * ORC_LZ4_CHUNK, len = size - a < ORC_LZ4_CHUNK ? size - a : ORC_LZ4_CHUNK;
+        int64_t k = orc_lz4_compress_block(payload + a, len, out + o, cap - o);
+        if (k < 0) return -1;
+        uint32_t k32 = (uint32_t)k;
+        memcpy(out + 40 + 4 * c, &k32, 4);
+        o += k;
+    }
+    return o;
+}
+
+/* Inverse of orc_aura_compress: writes the payload, returns its size (or -1) and the
+ * header's nref / nnew. */
+int64_t orc_aura_decompress(const uint8_t *in, int64_t n, uint8_t *payload, int64_t cap,
+                            int64_t *nref, int64_t *nnew)
+{
+    if (n < 40) return -1;
+    uint32_t h32[2], t32[2];
+    uint64_t h64[3];
+    memcpy(h32, in, 8);
+    memcpy(h64, in + 8, 24);
+    memcpy(t32, in + 32, 8);
+    if (h32[0] != 0x31414442u || h32[1] != ORC_LZ4_CHUNK) return -1;
+    int64_t size = (int64_t)h64[2], nch = t32[0];
+    if (size > cap || nch != (size + ORC_LZ4_CHUNK - 1) / ORC_LZ4_CHUNK || n < 40 + 4 * nch) return -1;
+    int64_t o = 40 + 4 * nch;
+    for (int64_t c = 0; c < nch; ++c) {
+        uint32_t k;
+        memcpy(&k, in + 40 + 4 * c, 4);
+        int64_t a = c * ORC_LZ4_CHUNK, len = size - a < ORC_LZ4_CHUNK ? size - a : ORC_LZ4_CHUNK;
+        if (o + k > n) return -1;
+        if (orc_lz4_decompress_block(in + o, k, payload + a, len) != len) return -1;
+        o += k;
+    }
+    *nref = (int64_t)h64[0];
+    *nnew = (int64_t)h64[1];
+    return size;
+}
