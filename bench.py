@@ -188,6 +188,8 @@ def run_ours(args, ws, rank, local):
         return run_soma(args, ws, rank, local)
     if args.config == "onco":
         return run_onco(args, ws, rank, local)
+    if args.config == "aura":
+        return run_aura(args, ws, rank, local)
     torch.cuda.set_device(local)
     cfg = W.PRESETS[args.config]
     eng = Engine(local, cfg.n)
@@ -568,6 +570,92 @@ def run_onco(args, ws, rank, local):
     print(json.dumps(line), flush=True)
 
 
+def run_aura(args, ws, rank, local):
+    """the aura a cfg2 x-slab sends its neighbour (agents within the
+    interaction radius of the slab plane x = side/2), encoded against a reference taken
+    at the first timed step (delta + LZ4, bdm_aura_encode) and decoded back, once per
+    mechanics step.  value = aura agents encoded per second; the sizes compare the
+    stream with the raw 40 B/agent message and with LZ4 alone (empty reference)."""
+    import torch
+    from paper_2503_10796_b200 import Agents, Engine, Params
+    torch.cuda.set_device(local)
+    cfg = W.CFG2
+    eng = Engine(local, cfg.n)
+    eng.set_option("fuse_reduce", 1)
+    a = Agents.empty(cfg.n)
+    stream = torch.cuda.Stream()
+    eng.init_spheres(a, cfg.n, seed=cfg.seed, side=cfg.side, d_lo=cfg.d_lo, d_width=cfg.d_width,
+                     d_random=cfg.d_random, stream=stream)
+    params = Params(k=cfg.k, gamma=cfg.gamma, dt=cfg.dt, max_displacement=cfg.max_disp,
+                    force_threshold=cfg.force_threshold, detect_static=cfg.detect_static)
+    for _ in range(args.warmup):
+        eng.step(a, params, stream=stream)
+    torch.cuda.synchronize()
+    mid, margin = 0.5 * cfg.side, cfg.d_lo + cfg.d_width      # R = max diameter
+    fields = (("x", "x"), ("y", "y"), ("z", "z"), ("diameter", "diameter"), ("id", "id"),
+              ("flags", "flags"))
+
+    def aura():
+        sel = torch.nonzero((a.x[:a.n] - mid).abs() < margin).squeeze(1)
+        m = Agents.empty(int(sel.numel()) + 1)
+        for f, _ in fields:
+            getattr(m, f)[:sel.numel()].copy_(getattr(a, f)[:a.n][sel])
+        m.n = int(sel.numel())
+        return m
+
+    msg0 = aura()
+    ref = Agents.empty(msg0.n + 1)
+    eng.aura_reference(msg0, ref, stream=stream)
+    empty = Agents.empty(1)
+    empty.n = 0
+    # warm-up of the codec (workspace allocation, kernel attributes)
+    wbuf = torch.empty(eng.aura_max_size(ref.n, msg0.n), dtype=torch.uint8, device="cuda")
+    wout = Agents.empty(2 * msg0.n + 1)
+    eng.aura_decode(wbuf, eng.aura_encode(msg0, ref, wbuf, stream=stream), ref, wout, stream=stream)
+    rows = []
+    launches0 = eng.stats()["launches"]
+    with ClockSampler(local) as clk:
+        for t in range(args.steps):
+            eng.step(a, params, stream=stream)
+            torch.cuda.synchronize()
+            m = aura()
+            cap = eng.aura_max_size(ref.n, m.n)
+            buf = torch.empty(cap, dtype=torch.uint8, device="cuda")
+            out = Agents.empty(m.n + ref.n + 1)
+            e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+            torch.cuda.synchronize()
+            e0.record(stream)
+            nb = eng.aura_encode(m, ref, buf, stream=stream)
+            e1.record(stream)
+            eng.aura_decode(buf, nb, ref, out, stream=stream)
+            e2.record(stream)
+            torch.cuda.synchronize()
+            plain = eng.aura_encode(m, empty, torch.empty(eng.aura_max_size(0, m.n),
+                                                          dtype=torch.uint8, device="cuda"),
+                                    stream=stream)
+            assert out.n == m.n
+            rows.append({"step": t + 1, "aura_agents": m.n, "raw_bytes": 40 * m.n,
+                         "stream_bytes": nb, "lz4_only_bytes": plain,
+                         "encode_ms": round(e0.elapsed_time(e1), 4),
+                         "decode_ms": round(e1.elapsed_time(e2), 4)})
+    enc_ms = sum(r["encode_ms"] for r in rows)
+    n_tot = sum(r["aura_agents"] for r in rows)
+    line = _common(n_tot / (enc_ms * 1e-3), enc_ms / len(rows), ws, args,
+                   {"workload": "cfg2 slab aura (R = 12 um each side of x = side/2), row f3",
+                    "reference": "aura at the last warm-up step, kept for all timed steps",
+                    "per_step": rows,
+                    "ratio_raw_over_stream": round(sum(r["raw_bytes"] for r in rows) /
+                                                   sum(r["stream_bytes"] for r in rows), 3),
+                    "ratio_raw_over_lz4_only": round(sum(r["raw_bytes"] for r in rows) /
+                                                     sum(r["lz4_only_bytes"] for r in rows), 3)},
+                   clk.summary(), eng.stats()["launches"] - launches0, dtype="u8")
+    line["metric"] = "aura agents encoded/s (delta + LZ4, device timed)"
+    line["unit"] = "agents/s"
+    line["roofline"] = None
+    line["note"] = "timed region: bdm_aura_encode per step (decode timed alongside); one warp per 4 KB LZ4 chunk"
+    print(json.dumps(line), flush=True)
+
+
 def asdict_safe(cfg):
     from dataclasses import asdict
     return asdict(cfg)
@@ -732,7 +820,7 @@ def main():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="cfg2", choices=sorted(W.PRESETS))
+    ap.add_argument("--config", default="cfg2", choices=sorted(W.PRESETS) + ["aura"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--mech-kernel", type=int, default=0, help="0 tile kernel, 1 reference")

@@ -379,6 +379,44 @@ bdm_status bdm_neighbor_pairs(bdm_handle h, const bdm_agents *a, double radius,
  * name/value. */
 bdm_status bdm_set_option(bdm_handle h, const char *name, int64_t value);
 
+/* ---- Row f3: delta-encoded + LZ4-compressed aura messages ------------------------
+ * Sec. "Data Transfer Minimization" (LZ4 evaluation P:6911-6937): sender
+ * and receiver keep the same reference (a previous aura message); the sender reorders
+ * the message to the reference, writes its difference against the reference and
+ * compresses it; the receiver inverts both.  Readings R46-R51: the
+ * reference is kept in ascending id order; slot r of the reference carries the message
+ * agent with the same id (XOR of the IEEE bit patterns of x, y, z, d and of flags) or a
+ * placeholder (presence bit 0); agents not in the reference follow in message order
+ * (raw values + id); the payload is stored as byte planes and compressed as independent
+ * 4096-byte LZ4 blocks (greedy parse, 11-bit hash).  Stream: 40-byte header (u32 magic
+ * "BDA1", u32 4096, u64 nref, u64 nnew, u64 payload bytes, u32 chunks, u32 0), u32
+ * compressed size per chunk, the chunks.  All arrays are device memory.  Ids must be
+ * unique within a message.  Messages of up to 2^31 - 1 agents. */
+
+/* Upper bound of the stream size for a reference of nref agents and a message of n
+ * agents (host-only; -1 for negative sizes). */
+int64_t bdm_aura_max_size(int64_t nref, int64_t n);
+
+/* ref := msg sorted by ascending id (R46; CUB radix sort + gather).  ref->capacity >=
+ * msg->n; sets ref->n.  Asynchronous on `stream`.  Errors: BDM_EINVAL (NULL arrays),
+ * BDM_ECAPACITY. */
+bdm_status bdm_aura_reference(bdm_handle h, const bdm_agents *msg, bdm_agents *ref, void *stream);
+
+/* Encodes msg against ref (R47-R50) into the device buffer out (out_cap bytes).
+ * Synchronizing; *out_size_host = stream bytes.  msg is not modified.  Errors:
+ * BDM_ECAPACITY if out_cap is too small (nothing meaningful is written; *out_size_host
+ * holds the size needed), BDM_EINVAL for NULL arguments. */
+bdm_status bdm_aura_encode(bdm_handle h, const bdm_agents *msg, const bdm_agents *ref,
+                           uint8_t *out, int64_t out_cap, int64_t *out_size_host, void *stream);
+
+/* Decodes the device stream in[0, in_size) against ref (the receiver's copy of the
+ * sender's reference) into msg (R51: the reference-order survivors, then the new
+ * agents); sets msg->n.  Synchronizing.  Errors: BDM_EINVAL for a malformed stream or
+ * one encoded against a reference of another size, BDM_ECAPACITY if msg->capacity is
+ * too small (msg unchanged). */
+bdm_status bdm_aura_decode(bdm_handle h, const uint8_t *in, int64_t in_size, const bdm_agents *ref,
+                           bdm_agents *msg, void *stream);
+
 /* Host-only query of the tile numbering inside an 8^3 super-tile (option "tile_order"):
  * rank_out[x | y<<3 | z<<6] = position of local tile (x, y, z) along the curve, for
  * order 0 (row-major, the identity) or 1 (3-D Hilbert curve, Skilling's transform).

@@ -1089,10 +1089,11 @@ void orc_init_ages(int64_t n, const uint32_t *id, uint64_t seed, uint32_t max_ag
  *   R49 payload layout: presence words, then the x, y, z, d columns over all
  *       nref + nnew slots each split into 8 byte planes, flags into 4 byte planes,
  *       then the ids of the new agents (little-endian);
- *   R50 LZ4 block format, payload cut into independent 4096-byte chunks, greedy
- *       parse with an 11-bit hash of the next 4 bytes (h = (v * 2654435761) >> 21,
- *       one candidate per bucket, updated at every position the parse visits), match
- *       >= 4 bytes, a match starts before n - 12 and ends by n - 5;
+ *   R50 LZ4 block format, payload cut into independent 4096-byte chunks; the match
+ *       candidate of a position is the last earlier position with the same 11-bit
+ *       hash of its next 4 bytes (h = (v * 2654435761) >> 21, every position enters
+ *       the table); greedy parse, match >= 4 bytes, a match starts before n - 12 and
+ *       ends by n - 5;
  *   R51 decoding restores the message in reference order (placeholders removed,
  *       P:6350-6352), then the new agents.
  * Stream: u32 magic 'BDA1', u32 chunk size, u64 nref, u64 nnew, u64 payload bytes,
@@ -1142,30 +1143,40 @@ static int64_t lz4_sequence(const uint8_t *src, int64_t a, int64_t nlit, int64_t
     return o;
 }
 
-/* R50: compress one block of n <= 65535 bytes.  Returns the compressed size or -1. */
+/* R50: compress one block of n <= 65535 bytes.  Two passes, in this order:
+ *   1. candidates: cand[p] = the last position q < p whose next 4 bytes hash to the
+ *      same 11-bit bucket (every position of the block enters the table), or none;
+ *   2. greedy parse from ip = 0: if ip < n - 12 and cand[ip] holds the same 4 bytes as
+ *      ip, emit the literals since the last match and a match extended forward while
+ *      the bytes agree and ip + len < n - 5, then continue after it; otherwise ip + 1.
+ * Returns the compressed size or -1. */
 int64_t orc_lz4_compress_block(const uint8_t *src, int64_t n, uint8_t *dst, int64_t cap)
 {
     int32_t table[1 << ORC_LZ4_HBITS];
     for (int k = 0; k < (1 << ORC_LZ4_HBITS); ++k) table[k] = -1;
+    int32_t *cand = (int32_t *)malloc((size_t)(n > 0 ? n : 1) * sizeof(int32_t));
+    for (int64_t p = 0; p < n; ++p) {
+        cand[p] = -1;
+        if (p + 4 > n) continue;
+        uint32_t h = (uint32_t)(rd32(src + p) * 2654435761u) >> (32 - ORC_LZ4_HBITS);
+        cand[p] = table[h];
+        table[h] = (int32_t)p;
+    }
     int64_t ip = 0, anchor = 0, o = 0;
-    if (n >= 13) {
-        while (ip < n - 12) {
-            uint32_t v = rd32(src + ip);
-            uint32_t h = (uint32_t)(v * 2654435761u) >> (32 - ORC_LZ4_HBITS);
-            int32_t ref = table[h];
-            table[h] = (int32_t)ip;
-            if (ref >= 0 && rd32(src + ref) == v) {
-                int64_t len = 4;
-                while (ip + len < n - 5 && src[ref + len] == src[ip + len]) ++len;
-                o = lz4_sequence(src, anchor, ip - anchor, ip - ref, len, dst, o, cap);
-                if (o < 0) return -1;
-                ip += len;
-                anchor = ip;
-            } else {
-                ++ip;
-            }
+    while (ip < n - 12) {
+        int32_t ref = cand[ip];
+        if (ref >= 0 && rd32(src + ref) == rd32(src + ip)) {
+            int64_t len = 4;
+            while (ip + len < n - 5 && src[ref + len] == src[ip + len]) ++len;
+            o = lz4_sequence(src, anchor, ip - anchor, ip - ref, len, dst, o, cap);
+            if (o < 0) { free(cand); return -1; }
+            ip += len;
+            anchor = ip;
+        } else {
+            ++ip;
         }
     }
+    free(cand);
     o = lz4_sequence(src, anchor, n - anchor, 0, 0, dst, o, cap);
     return o;
 }

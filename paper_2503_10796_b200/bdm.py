@@ -26,7 +26,8 @@ EXPORTS = [
     "bdm_get_stats", "bdm_get_grid_info", "bdm_neighbor_pairs", "bdm_peak_dfma",
     "bdm_set_option", "bdm_grow_divide", "bdm_sir_step", "bdm_local_frame", "bdm_set_frame",
     "bdm_pack_slab", "bdm_append", "bdm_diffuse", "bdm_secrete", "bdm_chemotaxis",
-    "bdm_onco_step", "bdm_tile_curve",
+    "bdm_onco_step", "bdm_tile_curve", "bdm_aura_max_size", "bdm_aura_reference",
+    "bdm_aura_encode", "bdm_aura_decode",
 ]
 PACK_MIGRATE, PACK_AURA = 1, 2
 
@@ -141,11 +142,16 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "bdm_chemotaxis": [P, AG, P, i32, dbl, P, ctypes.POINTER(CGrid3), P],
         "bdm_onco_step": [P, AG, P, i64, ctypes.POINTER(COncoParams), i64, P, P],
         "bdm_tile_curve": [i32, P],
+        "bdm_aura_reference": [P, AG, AG, P],
+        "bdm_aura_encode": [P, AG, AG, P, i64, ctypes.POINTER(i64), P],
+        "bdm_aura_decode": [P, P, i64, AG, AG, P],
     }
     for name, args in sig.items():
         f = getattr(L, name)
         f.argtypes = args
         f.restype = ctypes.c_int
+    L.bdm_aura_max_size.argtypes = [i64, i64]
+    L.bdm_aura_max_size.restype = i64
     L.bdm_last_error.restype = ctypes.c_char_p
     L.bdm_version.restype = ctypes.c_char_p
     _lib = L
@@ -480,6 +486,32 @@ class Engine:
         n, nxt = (int(v) for v in self._onco_out)
         agents.n = n
         return nxt
+
+    # ---- row f3: delta + LZ4 aura codec (bdm_aura_*)
+    def aura_reference(self, msg: Agents, ref: Agents, stream=None):
+        """ref := msg in ascending id order (the reference both sides keep, R46)."""
+        cm, cr = msg.c(), ref.c()
+        _check(self.lib.bdm_aura_reference(self.h, ctypes.byref(cm), ctypes.byref(cr),
+                                           _stream_ptr(stream)))
+        ref.n = cr.n
+
+    def aura_encode(self, msg: Agents, ref: Agents, out, stream=None) -> int:
+        """Stream of msg against ref into the uint8 device tensor out; returns its bytes."""
+        cm, cr = msg.c(), ref.c()
+        size = ctypes.c_int64()
+        _check(self.lib.bdm_aura_encode(self.h, ctypes.byref(cm), ctypes.byref(cr), _ptr(out),
+                                        int(out.numel()), ctypes.byref(size), _stream_ptr(stream)))
+        return int(size.value)
+
+    def aura_decode(self, stream_buf, nbytes: int, ref: Agents, msg: Agents, stream=None):
+        """msg := the message of stream_buf[:nbytes] decoded against ref (sets msg.n)."""
+        cr, cm = ref.c(), msg.c()
+        _check(self.lib.bdm_aura_decode(self.h, _ptr(stream_buf), int(nbytes), ctypes.byref(cr),
+                                        ctypes.byref(cm), _stream_ptr(stream)))
+        msg.n = cm.n
+
+    def aura_max_size(self, nref: int, n: int) -> int:
+        return int(self.lib.bdm_aura_max_size(int(nref), int(n)))
 
     def cfg3_step(self, agents: Agents, params: Params, growth: float, v_max: float,
                   stream=None) -> int:

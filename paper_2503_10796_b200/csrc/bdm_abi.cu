@@ -216,6 +216,7 @@ bdm_status bdm_destroy(bdm_handle h) {
     Ctx *c = (Ctx *)h;
     cudaSetDevice(c->device);
     cudaDeviceSynchronize();
+    free_aura(c);
     void *bufs[] = {c->key, c->rank, c->perm_tmp, c->skey, c->sid, c->perm, c->sx, c->sy,
                     c->sz, c->sd, c->sidf, c->sflags, c->svol, c->div_rank, c->box_start, c->dense_list,
                     c->onco_id, c->onco_out,
@@ -636,6 +637,52 @@ bdm_status bdm_set_option(bdm_handle h, const char *name, int64_t value) {
         return BDM_OK;
     }
     return fail(BDM_EINVAL, std::string("unknown option ") + name);
+}
+
+int64_t bdm_aura_max_size(int64_t nref, int64_t n) {
+    if (nref < 0 || n < 0) return -1;
+    return aura_max_size(nref, n);
+}
+
+static bdm_status check_aura_agents(const bdm_agents *a, const char *what) {
+    if (!a) return fail(BDM_EINVAL, std::string(what) + " is NULL");
+    if (a->n < 0 || a->n > a->capacity) return fail(BDM_EINVAL, std::string(what) + ": bad n");
+    if (a->n > 0 && (!a->x || !a->y || !a->z || !a->diameter || !a->id || !a->flags))
+        return fail(BDM_EINVAL, std::string(what) + ": an array is NULL");
+    if (a->n > 0x7FFFFFFFll) return fail(BDM_EINVAL, std::string(what) + ": more than 2^31 - 1 agents");
+    return BDM_OK;
+}
+
+bdm_status bdm_aura_reference(bdm_handle h, const bdm_agents *msg, bdm_agents *ref, void *stream) {
+    if (!h) return fail(BDM_EINVAL, "handle is NULL");
+    bdm_status s;
+    if ((s = check_aura_agents(msg, "msg")) != BDM_OK) return s;
+    if (!ref || (msg->n > 0 && (!ref->x || !ref->y || !ref->z || !ref->diameter || !ref->id ||
+                                !ref->flags)))
+        return fail(BDM_EINVAL, "ref is NULL or an array is NULL");
+    if (ref->capacity < msg->n) return fail(BDM_ECAPACITY, "ref capacity < msg->n");
+    return launch_aura_reference((Ctx *)h, msg, ref, (cudaStream_t)stream);
+}
+
+bdm_status bdm_aura_encode(bdm_handle h, const bdm_agents *msg, const bdm_agents *ref,
+                           uint8_t *out, int64_t out_cap, int64_t *out_size_host, void *stream) {
+    if (!h || !out_size_host) return fail(BDM_EINVAL, "handle or out_size_host is NULL");
+    bdm_status s;
+    if ((s = check_aura_agents(msg, "msg")) != BDM_OK) return s;
+    if ((s = check_aura_agents(ref, "ref")) != BDM_OK) return s;
+    if (!out && out_cap > 0) return fail(BDM_EINVAL, "out is NULL");
+    return launch_aura_encode((Ctx *)h, msg, ref, out, out_cap, out_size_host, (cudaStream_t)stream);
+}
+
+bdm_status bdm_aura_decode(bdm_handle h, const uint8_t *in, int64_t in_size, const bdm_agents *ref,
+                           bdm_agents *msg, void *stream) {
+    if (!h || !in) return fail(BDM_EINVAL, "handle or in is NULL");
+    bdm_status s;
+    if ((s = check_aura_agents(ref, "ref")) != BDM_OK) return s;
+    if (!msg || (msg->capacity > 0 && (!msg->x || !msg->y || !msg->z || !msg->diameter ||
+                                       !msg->id || !msg->flags)))
+        return fail(BDM_EINVAL, "msg is NULL or an array is NULL");
+    return launch_aura_decode((Ctx *)h, in, in_size, ref, msg, (cudaStream_t)stream);
 }
 
 bdm_status bdm_tile_curve(int32_t order, uint16_t *rank_out) {

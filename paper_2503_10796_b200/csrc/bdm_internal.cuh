@@ -65,6 +65,17 @@ struct SirWs {
     int64_t icap_override = 0;
 };
 
+// Aura codec workspace (kernels_aura.cu, row f3), allocated on first use
+struct AuraWs {
+    uint32_t *u32a = nullptr, *u32b = nullptr;
+    int64_t u32a_cap = 0, u32b_cap = 0;
+    uint8_t *pay = nullptr, *tmp = nullptr;
+    int64_t pay_cap = 0, tmp_cap = 0;
+    uint32_t *sizes = nullptr;
+    int64_t sizes_cap = 0;
+    int *err = nullptr;
+};
+
 // ------------------------------------------------------------------ library context
 struct Ctx {
     int device = 0;
@@ -118,6 +129,7 @@ struct Ctx {
     const double *fused_x = nullptr;
     int64_t fused_n = 0;
     SirWs sir;
+    AuraWs aura;
 };
 
 // An optional per-agent buffer (agent_cap + 1 entries), allocated on first use.
@@ -284,6 +296,14 @@ int64_t scan_block_count(int64_t m);
 bdm_status launch_onco_step(Ctx *c, bdm_agents *a, uint32_t *age, int64_t age_cap,
                             const bdm_onco_params *p, int64_t id_next, long long *out_host,
                             cudaStream_t st);
+// delta + LZ4 aura codec (kernels_aura.cu)
+int64_t aura_max_size(int64_t nref, int64_t n);
+bdm_status launch_aura_reference(Ctx *c, const bdm_agents *m, bdm_agents *r, cudaStream_t st);
+bdm_status launch_aura_encode(Ctx *c, const bdm_agents *m, const bdm_agents *r, uint8_t *out,
+                              int64_t out_cap, int64_t *out_size, cudaStream_t st);
+bdm_status launch_aura_decode(Ctx *c, const uint8_t *in, int64_t in_size, const bdm_agents *r,
+                              bdm_agents *m, cudaStream_t st);
+void free_aura(Ctx *c);
 // SIR (kernels_sir.cu)
 bdm_status launch_sir_step(Ctx *c, bdm_agents *a, const bdm_params *p, double side, double radius,
                            double p_inf, double p_rec, long long *counts_host, cudaStream_t st);
