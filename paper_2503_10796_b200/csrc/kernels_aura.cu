@@ -257,13 +257,23 @@ __global__ void __launch_bounds__(32 * kLzWarps) k_lz4_decompress(const uint8_t 
                                                                  uint8_t *__restrict__ pay,
                                                                  int *__restrict__ err) {
     __shared__ __align__(16) uint8_t outb[kLzWarps][kChunk];
+    __shared__ __align__(16) uint8_t inb[kLzWarps][kChunkCap + 16];
     const int lane = threadIdx.x & 31;
     const int64_t c = blockIdx.x * (int64_t)kLzWarps + (threadIdx.x >> 5);
     if (c >= nch) return;
     uint8_t *dst = outb[threadIdx.x >> 5];
-    const uint8_t *src = in + off[c];
     const int n = (int)len[c];
     const int cap = (int)(size - c * kChunk < kChunk ? size - c * kChunk : kChunk);
+    // the parse is a chain of dependent byte reads: stage the block in shared memory
+    // (a block longer than any this encoder writes is parsed from global memory)
+    const uint8_t *gsrc = in + off[c];
+    const uint8_t *src = gsrc;
+    if (n <= kChunkCap + 16) {
+        uint8_t *st = inb[threadIdx.x >> 5];
+        for (int k = lane; k < n; k += 32) st[k] = gsrc[k];
+        __syncwarp();
+        src = st;
+    }
     int i = 0, o = 0;
     bool bad = false;
     while (i < n) {  // warp-uniform parse; copies are lane-parallel

@@ -1,0 +1,78 @@
+"""configs[4] at full size on one GPU (1.7e9 agents, the bench's `--config cfg5` launch
+configuration): after one step, every agent of two sampled cubes (one interior, one at
+the domain corner) must match the oracle bit-exactly.  The oracle steps only the
+agents within R of the cubes, in the GPU's global grid frame (origin and R from
+bdm_get_grid_info, oracle `frame`), which fixes the same box lattice and therefore the
+same canonical summation order (R9, R12) for the cube agents."""
+import numpy as np
+import pytest
+
+import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+FIELDS = ("x", "y", "z", "diameter", "id", "flags")
+
+
+def _box(a, n, lo, hi):
+    """Agents of the device SoA with lo <= (x, y, z) < hi (numpy dict on the host)."""
+    import torch
+    m = torch.ones(n, dtype=torch.bool, device="cuda")
+    for f, l, h in zip(("x", "y", "z"), lo, hi):
+        t = getattr(a, f)[:n]
+        m &= (t >= l) & (t < h)
+    idx = torch.nonzero(m).squeeze(1)
+    del m
+    out = {("d" if f == "diameter" else f): getattr(a, f)[:n][idx].cpu().numpy() for f in FIELDS}
+    out["id"] = out["id"].view(np.uint32)
+    out["flags"] = out["flags"].view(np.uint32)
+    return out
+
+
+def test_cfg5_full_size_sampled_cubes(orc):
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    torch.cuda.empty_cache()
+    free, _ = torch.cuda.mem_get_info()
+    cfg = W.CFG5
+    if free < 182e9:
+        pytest.skip(f"needs ~182 GB free, {free / 1e9:.0f} GB")
+    from paper_2503_10796_b200 import Agents, Engine, Params
+    e = Engine(0, cfg.n)
+    try:
+        e.set_option("fuse_reduce", 1)
+        a = Agents.empty(cfg.n)
+        e.init_spheres(a, cfg.n, seed=cfg.seed, side=cfg.side, d_lo=cfg.d_lo, d_width=cfg.d_width,
+                       d_random=cfg.d_random)
+        gp = Params(k=cfg.k, gamma=cfg.gamma, dt=cfg.dt, max_displacement=cfg.max_disp,
+                    force_threshold=cfg.force_threshold, detect_static=cfg.detect_static)
+        e.step(a, gp)                       # step 0 (sizes the grid), then the checked step
+        torch.cuda.synchronize()
+        S, R = 100.0, cfg.d_lo + cfg.d_width    # cube side, interaction radius (max d)
+        gmin = [float(getattr(a, f)[:cfg.n].min()) for f in ("x", "y", "z")]
+        cubes = [[0.5 * cfg.side] * 3, gmin]     # interior, and the domain's low corner
+        befores = []
+        for c in cubes:
+            befores.append(_box(a, cfg.n, [v - R - 1.0 for v in c], [v + S + R + 1.0 for v in c]))
+        e.step(a, gp)
+        gi = e.grid_info()
+        torch.cuda.synchronize()
+        op = orc.mech_params(k=cfg.k, gamma=cfg.gamma, dt=cfg.dt, max_disp=cfg.max_disp,
+                             force_threshold=cfg.force_threshold, detect_static=cfg.detect_static,
+                             frame=(*gi["origin"], gi["R"]))
+        for c, sub in zip(cubes, befores):
+            inside = np.all([(sub[k] >= c[j]) & (sub[k] < c[j] + S)
+                             for j, k in enumerate(("x", "y", "z"))], axis=0)
+            sample = np.flatnonzero(inside)
+            assert len(sample) > 500
+            want, _ = orc.mech_step(sub, op, sample=sample)
+            m = cfg.max_disp + 0.5
+            after = _box(a, cfg.n, [v - m for v in c], [v + S + m for v in c])
+            pos = {int(i): k for k, i in enumerate(after["id"])}
+            idx = np.array([pos[int(i)] for i in sub["id"][sample]])
+            for k in ("x", "y", "z", "flags"):
+                assert np.array_equal(after[k][idx], want[k]), (c, k)
+    finally:
+        e.close()
+        torch.cuda.empty_cache()
