@@ -388,8 +388,8 @@ bdm_status bdm_set_option(bdm_handle h, const char *name, int64_t value);
  * agent with the same id (XOR of the IEEE bit patterns of x, y, z, d and of flags) or a
  * placeholder (presence bit 0); agents not in the reference follow in message order
  * (raw values + id); the payload is stored as byte planes and compressed as independent
- * 4096-byte LZ4 blocks (greedy parse, 11-bit hash).  Stream: 40-byte header (u32 magic
- * "BDA1", u32 4096, u64 nref, u64 nnew, u64 payload bytes, u32 chunks, u32 0), u32
+ * 1024-byte LZ4 blocks (greedy parse, 11-bit hash).  Stream: 40-byte header (u32 magic
+ * "BDA1", u32 1024, u64 nref, u64 nnew, u64 payload bytes, u32 chunks, u32 0), u32
  * compressed size per chunk, the chunks.  All arrays are device memory.  Ids must be
  * unique within a message.  Messages of up to 2^31 - 1 agents. */
 

@@ -527,6 +527,7 @@ def onco_full_step(s, mp: MechParams, p: OncoParams, id_next: int):
 
 # ---------------------------------------------------------------- row f3 (R46-R51)
 AURA_FIELDS = ("x", "y", "z", "d", "id", "flags")
+LZ4_CHUNK = 1024  # payload bytes per LZ4 block (R50; ORC_LZ4_CHUNK in oracle.c)
 
 
 def lz4_compress_block(data: bytes) -> bytes:
@@ -588,7 +589,7 @@ def aura_encode(msg, ref) -> bytes:
     payload, nnew = aura_payload(msg, ref)
     src = np.frombuffer(payload, np.uint8).copy() if payload else np.zeros(1, np.uint8)
     size = len(payload)
-    cap = 40 + 4 * (size // 4096 + 1) + size + size // 255 + 16 * (size // 4096 + 1) + 16
+    cap = 40 + 4 * (size // LZ4_CHUNK + 1) + size + size // 255 + 16 * (size // LZ4_CHUNK + 1) + 16
     out = np.zeros(cap, np.uint8)
     k = lib().orc_aura_compress(_p(src), size, len(ref["id"]), nnew, _p(out), cap)
     assert k >= 0

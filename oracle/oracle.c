@@ -1089,7 +1089,7 @@ void orc_init_ages(int64_t n, const uint32_t *id, uint64_t seed, uint32_t max_ag
  *   R49 payload layout: presence words, then the x, y, z, d columns over all
  *       nref + nnew slots each split into 8 byte planes, flags into 4 byte planes,
  *       then the ids of the new agents (little-endian);
- *   R50 LZ4 block format, payload cut into independent 4096-byte chunks; the match
+ *   R50 LZ4 block format, payload cut into independent 1024-byte chunks; the match
  *       candidate of a position is the last earlier position with the same 11-bit
  *       hash of its next 4 bytes (h = (v * 2654435761) >> 21, every position enters
  *       the table); greedy parse, match >= 4 bytes, a match starts before n - 12 and
@@ -1099,7 +1099,7 @@ void orc_init_ages(int64_t n, const uint32_t *id, uint64_t seed, uint32_t max_ag
  * Stream: u32 magic 'BDA1', u32 chunk size, u64 nref, u64 nnew, u64 payload bytes,
  * u32 nchunks, u32 0, u32 compressed size per chunk, the chunks. */
 
-#define ORC_LZ4_CHUNK 4096
+#define ORC_LZ4_CHUNK 1024
 #define ORC_LZ4_HBITS 11
 
 static uint32_t rd32(const uint8_t *p)

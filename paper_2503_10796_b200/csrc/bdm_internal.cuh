@@ -74,6 +74,7 @@ struct AuraWs {
     uint32_t *sizes = nullptr;
     int64_t sizes_cap = 0;
     int *err = nullptr;
+    long long *res = nullptr;
 };
 
 // ------------------------------------------------------------------ library context

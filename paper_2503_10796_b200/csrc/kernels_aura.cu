@@ -10,14 +10,14 @@
 //   R48 difference = XOR of the IEEE bit patterns of x, y, z, d and of flags;
 //   R49 payload = presence words | x, y, z, d columns as 8 byte planes each | flags as
 //       4 byte planes | ids of the new agents;
-//   R50 LZ4 block format over independent 4096-byte chunks, greedy parse with an
+//   R50 LZ4 block format over independent 1024-byte chunks, greedy parse with an
 //       11-bit hash bucket per 4-byte sequence;
 //   R51 decoding returns the reference-order survivors, then the new agents.
 //
 //   k_aura_match     binary search of every message id in the reference; presence bits
 //   scan             rank of the new agents
 //   k_aura_fill      XOR / raw values into the byte planes
-//   k_lz4_compress   one warp per 4 KB chunk in shared memory: bucket candidates of all
+//   k_lz4_compress   one warp per 1 KB chunk in shared memory: bucket candidates of all
 //                    positions (match_any), then the greedy parse 32 positions per probe
 //   scan + k_aura_pack   header, chunk sizes, chunks concatenated
 //   k_lz4_decompress / k_aura_unfill   the inverse
@@ -35,7 +35,7 @@
 
 namespace bdm {
 
-constexpr int kChunk = 4096;                       // payload bytes per LZ4 block
+constexpr int kChunk = 1024;                       // payload bytes per LZ4 block
 constexpr int kChunkCap = kChunk + kChunk / 255 + 16;  // worst-case block size
 constexpr int kHBits = 11;
 constexpr uint32_t kMagic = 0x31414442u;           // "BDA1"
@@ -57,7 +57,7 @@ static int64_t payload_size(int64_t nref, int64_t nnew) {
 __global__ void k_aura_match(int64_t n, const uint32_t *__restrict__ id,
                              const uint32_t *__restrict__ rid, int64_t nref,
                              uint32_t *__restrict__ slot, uint32_t *__restrict__ isnew,
-                             uint32_t *__restrict__ pres) {
+                             uint32_t *__restrict__ pres, uint32_t *__restrict__ inv) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i == 0) isnew[n] = 0u;
     if (i >= n) return;
@@ -70,7 +70,17 @@ __global__ void k_aura_match(int64_t n, const uint32_t *__restrict__ id,
     const bool found = lo < nref && rid[lo] == me;
     slot[i] = found ? (uint32_t)lo : 0xFFFFFFFFu;
     isnew[i] = found ? 0u : 1u;
-    if (found) atomicOr(&pres[lo >> 5], 1u << (lo & 31));
+    if (found) {
+        atomicOr(&pres[lo >> 5], 1u << (lo & 31));
+        inv[lo] = (uint32_t)i;  // reference slot -> message index
+    }
+}
+
+// message index of each new agent, by its rank
+__global__ void k_aura_newlist(int64_t n, const uint32_t *__restrict__ slot,
+                               const uint32_t *__restrict__ newrank, uint32_t *__restrict__ newlist) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n && slot[i] == 0xFFFFFFFFu) newlist[newrank[i]] = (uint32_t)i;
 }
 
 struct AuraView {
@@ -78,26 +88,27 @@ struct AuraView {
     const uint32_t *id, *flags;
 };
 
+// One thread per payload slot (coalesced byte-plane writes); nnew is read on the device.
 __global__ void k_aura_fill(int64_t n, AuraView m, AuraView r, int64_t nref,
-                            const uint32_t *__restrict__ slot, const uint32_t *__restrict__ newrank,
-                            uint8_t *__restrict__ pay) {
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= n) return;
+                            const uint32_t *__restrict__ inv, const uint32_t *__restrict__ newlist,
+                            const uint32_t *__restrict__ newrank, uint8_t *__restrict__ pay) {
+    const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int64_t nnew = (int64_t)newrank[n];
     const int64_t ns = nref + nnew, nw = (nref + 31) / 32;
-    const uint32_t sl = slot[i];
-    const bool matched = sl != 0xFFFFFFFFu;
-    const int64_t s = matched ? (int64_t)sl : nref + (int64_t)newrank[i];
+    if (s >= ns) return;
+    const bool matched = s < nref;
+    const uint32_t i = matched ? inv[s] : newlist[s - nref];
+    if (i == 0xFFFFFFFFu) return;  // placeholder: zeros
     unsigned long long v[4] = {
         (unsigned long long)__double_as_longlong(m.x[i]), (unsigned long long)__double_as_longlong(m.y[i]),
         (unsigned long long)__double_as_longlong(m.z[i]), (unsigned long long)__double_as_longlong(m.d[i])};
     uint32_t f = m.flags[i];
     if (matched) {
-        v[0] ^= (unsigned long long)__double_as_longlong(r.x[sl]);
-        v[1] ^= (unsigned long long)__double_as_longlong(r.y[sl]);
-        v[2] ^= (unsigned long long)__double_as_longlong(r.z[sl]);
-        v[3] ^= (unsigned long long)__double_as_longlong(r.d[sl]);
-        f ^= r.flags[sl];
+        v[0] ^= (unsigned long long)__double_as_longlong(r.x[s]);
+        v[1] ^= (unsigned long long)__double_as_longlong(r.y[s]);
+        v[2] ^= (unsigned long long)__double_as_longlong(r.z[s]);
+        v[3] ^= (unsigned long long)__double_as_longlong(r.d[s]);
+        f ^= r.flags[s];
     } else {
         uint8_t *nid = pay + 4 * nw + 36 * ns + 4 * (s - nref);
         const uint32_t me = m.id[i];
@@ -114,13 +125,13 @@ __global__ void k_aura_fill(int64_t n, AuraView m, AuraView r, int64_t nref,
     for (int b = 0; b < 4; ++b) fcol[(int64_t)b * ns + s] = (uint8_t)(f >> (8 * b));
 }
 
-// ---- LZ4 (R50), one warp per 4 KB chunk staged in shared memory
+// ---- LZ4 (R50), one warp per 1 KB chunk staged in shared memory
 struct LzWarp {
     uint8_t src[kChunk + 16];
     uint16_t cand[kChunk];
     uint16_t table[1 << kHBits];
 };
-constexpr int kLzWarps = 4;
+constexpr int kLzWarps = 8;
 
 __device__ __forceinline__ uint32_t rd32s(const uint8_t *p) {
     return (uint32_t)p[0] | ((uint32_t)p[1] << 8) | ((uint32_t)p[2] << 16) | ((uint32_t)p[3] << 24);
@@ -162,15 +173,30 @@ __device__ __forceinline__ int warp_sequence(const uint8_t *src, int a, int nlit
     return e;
 }
 
+__device__ __forceinline__ int64_t dev_payload_size(int64_t nref, int64_t nnew) {
+    const int64_t ns = nref + nnew;
+    return 4 * ((nref + 31) / 32) + 32 * ns + 4 * ns + 4 * nnew;
+}
+
+// The payload size follows from nnew = newrank[n] on the device; chunks past it
+// report size 0 (the grid covers the bound for nnew = n).
 __global__ void __launch_bounds__(32 * kLzWarps) k_lz4_compress(const uint8_t *__restrict__ pay,
-                                                               int64_t size, int64_t nch,
+                                                               const uint32_t *__restrict__ newrank,
+                                                               int64_t nmsg, int64_t nref,
+                                                               int64_t nch_max,
                                                                uint8_t *__restrict__ tmp,
                                                                uint32_t *__restrict__ csize) {
     extern __shared__ __align__(16) unsigned char lz_smem[];
     LzWarp &S = reinterpret_cast<LzWarp *>(lz_smem)[threadIdx.x >> 5];
     const int lane = threadIdx.x & 31;
     const int64_t c = blockIdx.x * (int64_t)kLzWarps + (threadIdx.x >> 5);
-    if (c >= nch) return;
+    if (c >= nch_max) return;
+    const int64_t size = dev_payload_size(nref, (int64_t)newrank[nmsg]);
+    const int64_t nch = (size + kChunk - 1) / kChunk;
+    if (c >= nch) {
+        if (lane == 0) csize[c] = 0u;
+        return;
+    }
     const int n = (int)(size - c * kChunk < kChunk ? size - c * kChunk : kChunk);
     const uint8_t *g = pay + c * kChunk;
     if (n == kChunk) {
@@ -234,14 +260,29 @@ __global__ void __launch_bounds__(32 * kLzWarps) k_lz4_compress(const uint8_t *_
     if (lane == 0) csize[c] = (uint32_t)o;
 }
 
-// Header, chunk sizes, chunks (a warp per chunk).  csize holds the exclusive scan of
-// the sizes with the total at [nch]; sizes are recovered as differences.
+// Header, chunk sizes, chunks (a warp per chunk).  off holds the exclusive scan of the
+// chunk sizes over nch_max + 1 entries (chunks past nch have size 0).  Writes nothing
+// if the stream does not fit in out_cap; res = {stream bytes, fits}.
 __global__ void k_aura_pack(const uint8_t *__restrict__ tmp, const uint32_t *__restrict__ off,
-                            int64_t nch, AuraHeader h, uint8_t *__restrict__ out) {
+                            const uint32_t *__restrict__ newrank, int64_t n, int64_t nref,
+                            int64_t nch_max, int64_t out_cap, uint8_t *__restrict__ out,
+                            long long *__restrict__ res) {
     const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
-    if (w == 0 && lane == 0) memcpy(out, &h, sizeof(h));
-    if (w >= nch) return;
+    const int64_t nnew = (int64_t)newrank[n], size = dev_payload_size(nref, nnew);
+    const int64_t nch = (size + kChunk - 1) / kChunk;
+    const int64_t bytes = kHdr + 4 * nch + (int64_t)off[nch_max];
+    const bool fits = bytes <= out_cap;
+    if (w == 0 && lane == 0) {
+        res[0] = bytes;
+        res[1] = fits ? 1 : 0;
+        if (fits) {
+            AuraHeader h{kMagic, (uint32_t)kChunk, (uint64_t)nref, (uint64_t)nnew, (uint64_t)size,
+                         (uint32_t)nch, 0u};
+            memcpy(out, &h, sizeof(h));
+        }
+    }
+    if (!fits || w >= nch) return;
     const uint32_t a = off[w], k = off[w + 1] - a;
     if (lane == 0) memcpy(out + kHdr + 4 * w, &k, 4);
     const uint8_t *s = tmp + w * kChunkCap;
@@ -476,41 +517,45 @@ bdm_status launch_aura_reference(Ctx *c, const bdm_agents *m, bdm_agents *r, cud
 
 bdm_status launch_aura_encode(Ctx *c, const bdm_agents *m, const bdm_agents *r, uint8_t *out,
                               int64_t out_cap, int64_t *out_size, cudaStream_t st) {
-    const int64_t n = m->n, nref = r->n, nw = (nref + 31) / 32;
+    // one synchronization: every size past the match is read on the device, the grids
+    // cover the bound nnew = n
+    const int64_t n = m->n, nref = r->n;
     AuraWs &W = c->aura;
     bdm_status s;
-    if ((s = ensure(&W.u32a, W.u32a_cap, n + 1)) != BDM_OK) return s;   // slot
-    if ((s = ensure(&W.u32b, W.u32b_cap, n + 1)) != BDM_OK) return s;   // new rank
+    if ((s = ensure(&W.u32a, W.u32a_cap, (n + 1) + nref + n + 1)) != BDM_OK) return s;
+    if ((s = ensure(&W.u32b, W.u32b_cap, n + 1)) != BDM_OK) return s;
+    uint32_t *slot = W.u32a, *inv = W.u32a + n + 1, *newlist = inv + nref, *newrank = W.u32b;
     const int64_t pmax = payload_size(nref, n);
+    const int64_t nch_max = (pmax + kChunk - 1) / kChunk;
     if ((s = ensure(&W.pay, W.pay_cap, pmax)) != BDM_OK) return s;
-    if ((s = ensure_scan(c, n + 1)) != BDM_OK) return s;
+    if ((s = ensure(&W.tmp, W.tmp_cap, nch_max * (int64_t)kChunkCap)) != BDM_OK) return s;
+    if ((s = ensure(&W.sizes, W.sizes_cap, nch_max + 1)) != BDM_OK) return s;
+    if ((s = ensure_scan(c, (n > nch_max ? n : nch_max) + 1)) != BDM_OK) return s;
+    if (!W.res) BDM_CUDA_TRY(cudaMalloc(&W.res, 2 * sizeof(long long)));
     BDM_CUDA_TRY(cudaMemsetAsync(W.pay, 0, (size_t)pmax, st));
+    if (nref > 0) BDM_CUDA_TRY(cudaMemsetAsync(inv, 0xFF, (size_t)nref * 4, st));
+    BDM_CUDA_TRY(cudaMemsetAsync(W.sizes + nch_max, 0, sizeof(uint32_t), st));
     if (n > 0) {
-        k_aura_match<<<nblk(n, 256), 256, 0, st>>>(n, m->id, r->id, nref, W.u32a, W.u32b,
-                                                    (uint32_t *)W.pay);
-        BDM_LAUNCH_CHECK("k_aura_match");
+        k_aura_match<<<nblk(n, 256), 256, 0, st>>>(n, m->id, r->id, nref, slot, newrank,
+                                                    (uint32_t *)W.pay, inv);
         c->launches += 1;
     } else {
-        BDM_CUDA_TRY(cudaMemsetAsync(W.u32b, 0, sizeof(uint32_t), st));
+        BDM_CUDA_TRY(cudaMemsetAsync(newrank, 0, sizeof(uint32_t), st));
     }
-    if ((s = launch_scan_u32(c, W.u32b, n + 1, st)) != BDM_OK) return s;
-    uint32_t nnew32 = 0;
-    BDM_CUDA_TRY(cudaMemcpyAsync(&nnew32, W.u32b + n, 4, cudaMemcpyDeviceToHost, st));
-    BDM_CUDA_TRY(cudaStreamSynchronize(st));
-    const int64_t nnew = nnew32, size = payload_size(nref, nnew);
-    const int64_t nch = (size + kChunk - 1) / kChunk;
+    BDM_LAUNCH_CHECK("k_aura_match");
+    if ((s = launch_scan_u32(c, newrank, n + 1, st)) != BDM_OK) return s;
     if (n > 0) {
-        // the presence words were written in place; the planes start after them
-        k_aura_fill<<<nblk(n, 256), 256, 0, st>>>(n, view(m), view(r), nref, W.u32a, W.u32b, W.pay);
-        BDM_LAUNCH_CHECK("k_aura_fill");
+        k_aura_newlist<<<nblk(n, 256), 256, 0, st>>>(n, slot, newrank, newlist);
         c->launches += 1;
     }
-    (void)nw;
-    if ((s = ensure(&W.tmp, W.tmp_cap, nch * (int64_t)kChunkCap)) != BDM_OK) return s;
-    if ((s = ensure(&W.sizes, W.sizes_cap, nch + 1)) != BDM_OK) return s;
-    if ((s = ensure_scan(c, nch + 1)) != BDM_OK) return s;
-    BDM_CUDA_TRY(cudaMemsetAsync(W.sizes + nch, 0, sizeof(uint32_t), st));
-    if (nch > 0) {
+    if (nref + n > 0) {
+        // the presence words were written in place; the planes start after them
+        k_aura_fill<<<nblk(nref + n, 256), 256, 0, st>>>(n, view(m), view(r), nref, inv, newlist,
+                                                         newrank, W.pay);
+        c->launches += 1;
+    }
+    BDM_LAUNCH_CHECK("k_aura_fill");
+    if (nch_max > 0) {
         static bool attr = false;
         const int smem = (int)(sizeof(LzWarp) * kLzWarps);
         if (!attr) {
@@ -518,28 +563,25 @@ bdm_status launch_aura_encode(Ctx *c, const bdm_agents *m, const bdm_agents *r, 
                                               cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
             attr = true;
         }
-        k_lz4_compress<<<nblk(nch, kLzWarps), 32 * kLzWarps, smem, st>>>(W.pay, size, nch, W.tmp,
-                                                                         W.sizes);
+        k_lz4_compress<<<nblk(nch_max, kLzWarps), 32 * kLzWarps, smem, st>>>(
+            W.pay, newrank, n, nref, nch_max, W.tmp, W.sizes);
         BDM_LAUNCH_CHECK("k_lz4_compress");
         c->launches += 1;
     }
-    if ((s = launch_scan_u32(c, W.sizes, nch + 1, st)) != BDM_OK) return s;
-    uint32_t total = 0;
-    BDM_CUDA_TRY(cudaMemcpyAsync(&total, W.sizes + nch, 4, cudaMemcpyDeviceToHost, st));
-    BDM_CUDA_TRY(cudaStreamSynchronize(st));
-    const int64_t bytes = kHdr + 4 * nch + (int64_t)total;
-    *out_size = bytes;
-    if (bytes > out_cap) {
-        set_error("aura stream needs " + std::to_string((long long)bytes) + " bytes");
-        return BDM_ECAPACITY;
-    }
-    AuraHeader h{kMagic, (uint32_t)kChunk, (uint64_t)nref, (uint64_t)nnew, (uint64_t)size,
-                 (uint32_t)nch, 0u};
-    const int64_t thr = 32 * (nch > 0 ? nch : 1);
-    k_aura_pack<<<nblk(thr, 256), 256, 0, st>>>(W.tmp, W.sizes, nch, h, out);
+    if ((s = launch_scan_u32(c, W.sizes, nch_max + 1, st)) != BDM_OK) return s;
+    const int64_t thr = 32 * (nch_max > 0 ? nch_max : 1);
+    k_aura_pack<<<nblk(thr, 256), 256, 0, st>>>(W.tmp, W.sizes, newrank, n, nref, nch_max, out_cap,
+                                                out, W.res);
     BDM_LAUNCH_CHECK("k_aura_pack");
     c->launches += 1;
+    long long res[2] = {0, 0};
+    BDM_CUDA_TRY(cudaMemcpyAsync(res, W.res, sizeof(res), cudaMemcpyDeviceToHost, st));
     BDM_CUDA_TRY(cudaStreamSynchronize(st));
+    *out_size = res[0];
+    if (!res[1]) {
+        set_error("aura stream needs " + std::to_string(res[0]) + " bytes");
+        return BDM_ECAPACITY;
+    }
     return BDM_OK;
 }
 
@@ -622,7 +664,7 @@ bdm_status launch_aura_decode(Ctx *c, const uint8_t *in, int64_t in_size, const 
 
 void free_aura(Ctx *c) {
     AuraWs &W = c->aura;
-    void *p[] = {W.u32a, W.u32b, W.pay, W.tmp, W.sizes, W.err};
+    void *p[] = {W.u32a, W.u32b, W.pay, W.tmp, W.sizes, W.err, W.res};
     for (void *q : p)
         if (q) cudaFree(q);
     W = AuraWs();

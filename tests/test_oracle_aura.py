@@ -211,8 +211,8 @@ def test_stream_header_and_delta_gain():
     msg["x"] = ref["x"] + np.random.default_rng(9).uniform(-1e-3, 1e-3, 20000)
     st = orc.aura_encode(msg, ref)
     magic, chunk, nref, nnew, size, nch, _ = struct.unpack_from("<IIQQQII", st)
-    assert (magic, chunk, nref, nnew) == (0x31414442, 4096, 20000, 0)
-    assert nch == (size + 4095) // 4096
+    assert (magic, chunk, nref, nnew) == (0x31414442, orc.LZ4_CHUNK, 20000, 0)
+    assert nch == (size + orc.LZ4_CHUNK - 1) // orc.LZ4_CHUNK
     empty = {k: v[:0] for k, v in ref.items()}
     plain = orc.aura_encode(msg, empty)
     assert len(st) * 1.1 < len(plain) < 40 * 20000
