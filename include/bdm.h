@@ -171,7 +171,8 @@ bdm_status bdm_grid_build(bdm_handle h, const bdm_agents *a, const bdm_agents *g
  *   max_displacement; x_i += displacement; boundary (open: no-op; closed: clamp).
  * Static agents (R8) skip the force: displacement 0, nnz carried.
  * On return (stream order) the caller's arrays x,y,z,diameter,id,flags hold the
- * new state in the grid's sorted order (key, then id): a permutation of the input.
+ * new state in the grid's sorted order (key, then id): a permutation of the input
+ * (or, on builds that option "sort_every" leaves in place, in the input order).
  * Errors: BDM_EINVAL (no matching grid build, bad params), BDM_ENOTIMPL
  * (toroidal boundary), BDM_ECUDA. */
 bdm_status bdm_mech_step(bdm_handle h, bdm_agents *a, const bdm_params *p, void *stream);
@@ -182,7 +183,10 @@ bdm_status bdm_step(bdm_handle h, bdm_agents *a, const bdm_params *p, void *stre
 /* End-to-end step on HOST arrays (the e2e entry point): copies the n agents of
  * `host_in` to the device arrays `dev` (host->device), runs bdm_step, copies the
  * new state back into `host_out` (device->host) and synchronizes `stream`.
- * host_in may equal host_out.  Host arrays should be pinned for full bandwidth.
+ * host_in may equal host_out.  In place (the same diameter and id arrays) on a step
+ * that keeps the input order (option "sort_every"), only x, y, z and flags are copied
+ * back: a mechanics step does not change d or id.  Host arrays should be pinned for
+ * full bandwidth.
  * Errors: as bdm_step, plus deferred device conditions (as bdm_sync). */
 bdm_status bdm_step_host(bdm_handle h, const bdm_agents *host_in, bdm_agents *host_out,
                          bdm_agents *dev, const bdm_params *p, void *stream);

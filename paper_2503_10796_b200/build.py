@@ -26,7 +26,7 @@ NVCC_FLAGS = [
     "-O3", "-lineinfo", "-fmad=false", "-std=c++17",
     "-Xcompiler", "-fPIC", "-Xptxas", "-v",
     "--expt-relaxed-constexpr",
-]
+] + os.environ.get("BDM_NVCC_EXTRA", "").split()  # experiments only (A/B variants)
 
 
 def _newest_input() -> float:

@@ -346,9 +346,14 @@ bdm_status bdm_step_host(bdm_handle h, const bdm_agents *hin, bdm_agents *hout, 
     BDM_CUDA_TRY(cudaMemcpyAsync(hout->x, dev->x, n * 8, cudaMemcpyDeviceToHost, st));
     BDM_CUDA_TRY(cudaMemcpyAsync(hout->y, dev->y, n * 8, cudaMemcpyDeviceToHost, st));
     BDM_CUDA_TRY(cudaMemcpyAsync(hout->z, dev->z, n * 8, cudaMemcpyDeviceToHost, st));
-    BDM_CUDA_TRY(cudaMemcpyAsync(hout->diameter, dev->diameter, n * 8, cudaMemcpyDeviceToHost, st));
-    BDM_CUDA_TRY(cudaMemcpyAsync(hout->id, dev->id, n * 4, cudaMemcpyDeviceToHost, st));
     BDM_CUDA_TRY(cudaMemcpyAsync(hout->flags, dev->flags, n * 4, cudaMemcpyDeviceToHost, st));
+    // a step that kept the input order (option sort_every) leaves d and id where they
+    // were: in place they are already on the host
+    const bool inplace = hout->diameter == hin->diameter && hout->id == hin->id;
+    if (!(inplace && ((Ctx *)h)->keep_order)) {
+        BDM_CUDA_TRY(cudaMemcpyAsync(hout->diameter, dev->diameter, n * 8, cudaMemcpyDeviceToHost, st));
+        BDM_CUDA_TRY(cudaMemcpyAsync(hout->id, dev->id, n * 4, cudaMemcpyDeviceToHost, st));
+    }
     return bdm_sync(h, stream);
 }
 

@@ -122,3 +122,42 @@ def test_hilbert_sorted_order_follows_the_curve(torch_cuda, orc):
     key = rank * 64 + m
     order = np.lexsort((out["id"], key))
     assert np.array_equal(order, np.arange(cfg.n))
+
+
+@pytest.mark.parametrize("inplace", [True, False])
+def test_step_host_keep_order(torch_cuda, orc, inplace):
+    """bdm_step_host with sort_every = 0: the host arrays keep their order; in place only
+    x, y, z, flags travel back (d, id unchanged by a mechanics step), otherwise all six.
+    The state per id equals the oracle's after every step."""
+    import torch
+    from paper_2503_10796_b200 import Agents, Engine
+    cfg = W.cfg2_scaled(40_000)
+    s = orc.init_spheres(cfg.n, cfg.seed, cfg.side, cfg.d_lo, cfg.d_width, cfg.d_random)
+    gp, op = _params(orc, cfg)
+    e = Engine(0, cfg.n)
+    try:
+        e.set_option("sort_every", 0)
+        hin = Agents.empty(cfg.n, pin=True)
+        hout = Agents.empty(cfg.n, pin=True)
+        for k, src in (("x", "x"), ("y", "y"), ("z", "z"), ("diameter", "d")):
+            getattr(hin, k).copy_(torch.from_numpy(np.ascontiguousarray(s[src])))
+        hin.id.copy_(torch.from_numpy(s["id"].view(np.int32)))
+        hin.flags.copy_(torch.from_numpy(s["flags"].view(np.int32)))
+        hin.n = cfg.n
+        dev = Agents.empty(cfg.n)
+        o = s
+        src_buf = hin
+        for t in range(3):
+            dst = src_buf if inplace else (hout if src_buf is hin else hin)
+            e.step_host(src_buf, dst, dev, gp)
+            o, _ = orc.step_full(o, op)
+            got = {"x": dst.x.numpy().copy(), "y": dst.y.numpy().copy(), "z": dst.z.numpy().copy(),
+                   "d": dst.diameter.numpy().copy(), "id": dst.id.numpy().view(np.uint32).copy(),
+                   "flags": dst.flags.numpy().view(np.uint32).copy()}
+            assert np.array_equal(got["id"], s["id"]), t          # input order kept
+            gi, oi = _by_id(got), _by_id(o)
+            for k in ("id", "flags", "d", "x", "y", "z"):
+                assert np.array_equal(gi[k], oi[k]), (t, k)
+            src_buf = dst
+    finally:
+        e.close()
