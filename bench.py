@@ -738,7 +738,7 @@ def run_slabs(args, ws, rank, local):
         tr = LocalTransport()
     params = Params(k=cfg.k, gamma=cfg.gamma, dt=cfg.dt, max_displacement=cfg.max_disp,
                     detect_static=cfg.detect_static)
-    dom = SlabDomain([Slab(rank, lo, hi, ops, a)], tr, params)
+    dom = SlabDomain([Slab(rank, lo, hi, ops, a)], tr, params, aura_codec=args.aura_codec)
     for _ in range(args.warmup):
         dom.step()
     n_loc = a.n
@@ -838,6 +838,8 @@ def main():
                     help="row f1: 0 row-major tiles, 1 blocked Hilbert")
     ap.add_argument("--sort-every", type=int, default=1,
                     help="row f1: reorder the agents every K-th step (0 = never)")
+    ap.add_argument("--aura-codec", action="store_true",
+                    help="row f3: x-slab aura as delta + LZ4 streams (links slower than NVLink)")
     ap.add_argument("--shuffle", action="store_true",
                     help="start from a random memory order of the agents (row f1 sweeps)")
     args = ap.parse_args()

@@ -12,7 +12,10 @@ slabs unbounded ("partitioning grid").  Every iteration:
                 summation order (R9) -- and therefore every bit of the result -- is the
                 same as on one GPU (R12, R24);
   3. aura       agents within R(1+2^-20) of a slab border are copied to the neighbour
-                (P:6083-6106; rebuilt every iteration, P:6280-6281);
+                (rebuilt every iteration); optionally as a
+                delta-encoded + LZ4 stream against a reference both sides keep and
+                refresh every `ref_every` iterations (row f3, P:6291-6356,
+                bdm_aura_*), for links slower than NVLink;
   4. compute    bdm_grid_build(locals, ghosts) + bdm_mech_step (locals only).
 
 The device side (packing, appending, frames, the step) is libbdm.so; the transport is
@@ -87,6 +90,31 @@ class LibOps:
             return
         raise RuntimeError("grid capacity could not be satisfied")
 
+    # row f3: aura codec (device byte streams)
+    def empty_ref(self) -> Agents:
+        a = self.buffer(1)
+        a.n = 0
+        return a
+
+    def aura_reference(self, msg: Agents) -> Agents:
+        ref = self.buffer(max(msg.n, 1))
+        self.eng.aura_reference(msg, ref, stream=self.stream)
+        return ref
+
+    def aura_encode(self, msg: Agents, ref: Agents):
+        import torch
+        buf = torch.empty(self.eng.aura_max_size(ref.n, msg.n), dtype=torch.uint8,
+                          device=self.device)
+        nb = self.eng.aura_encode(msg, ref, buf, stream=self.stream)
+        return buf[:nb]
+
+    def aura_decode(self, stream_bytes, ref: Agents) -> Agents:
+        hdr = stream_bytes[:40].cpu().numpy().tobytes() if stream_bytes.numel() >= 40 else b""
+        nnew = int.from_bytes(hdr[16:24], "little") if hdr else 0
+        out = self.buffer(max(ref.n + nnew, 1))
+        self.eng.aura_decode(stream_bytes, int(stream_bytes.numel()), ref, out, stream=self.stream)
+        return out
+
     # payload <-> tensors (views, no copy)
     def to_payload(self, a: Agents):
         fields = {k: getattr(a, k)[:a.n] for k in F64_FIELDS + I32_FIELDS}
@@ -125,6 +153,9 @@ class LocalTransport:
             from_right = sends[g + 1][0] if (g + 1) in sends else None
             recv[g] = (from_left, from_right)
         return recv
+
+    def exchange_bytes(self, sends: dict) -> dict:
+        return self.exchange(sends)
 
     def allreduce_min(self, frames: dict) -> dict:
         import torch
@@ -194,6 +225,40 @@ class DistTransport:
         from_r = self.ops.from_payload(recv_r, n_from_r) if has_r else None
         return {g: (from_l, from_r)}
 
+    def exchange_bytes(self, sends: dict) -> dict:
+        """Byte streams (uint8 tensors) with the two neighbours: sizes, then bytes."""
+        import torch
+        dist = self.dist
+        (g, (to_left, to_right)), = sends.items()
+        left, right = g - 1, g + 1
+        has_l, has_r = left >= 0, right < self.world
+        size = lambda t: int(t.numel()) if t is not None else 0  # noqa: E731
+        cnt_out = torch.tensor([size(to_left), size(to_right)], dtype=torch.int64,
+                               device=self.device)
+        cnt_in = torch.zeros(2, dtype=torch.int64, device=self.device)
+        ops = []
+        if has_l:
+            ops += [dist.P2POp(dist.isend, cnt_out[0:1], left, self.group),
+                    dist.P2POp(dist.irecv, cnt_in[0:1], left, self.group)]
+        if has_r:
+            ops += [dist.P2POp(dist.isend, cnt_out[1:2], right, self.group),
+                    dist.P2POp(dist.irecv, cnt_in[1:2], right, self.group)]
+        self._p2p(ops)
+        n_l, n_r = (int(v) for v in cnt_in.cpu())
+        recv_l = torch.empty(max(n_l, 1), dtype=torch.uint8, device=self.device)
+        recv_r = torch.empty(max(n_r, 1), dtype=torch.uint8, device=self.device)
+        ops = []
+        if has_l and size(to_left) > 0:
+            ops.append(dist.P2POp(dist.isend, to_left.contiguous(), left, self.group))
+        if has_l and n_l > 0:
+            ops.append(dist.P2POp(dist.irecv, recv_l[:n_l], left, self.group))
+        if has_r and size(to_right) > 0:
+            ops.append(dist.P2POp(dist.isend, to_right.contiguous(), right, self.group))
+        if has_r and n_r > 0:
+            ops.append(dist.P2POp(dist.irecv, recv_r[:n_r], right, self.group))
+        self._p2p(ops)
+        return {g: (recv_l[:n_l] if has_l else None, recv_r[:n_r] if has_r else None)}
+
     def allreduce_min(self, frames: dict) -> dict:
         (g, f), = frames.items()
         t = f.clone()
@@ -216,11 +281,18 @@ class SlabDomain:
     """The per-iteration protocol over the slabs this process owns (one per process with
     DistTransport, several with LocalTransport)."""
 
-    def __init__(self, slabs: list, transport, params: Params):
+    def __init__(self, slabs: list, transport, params: Params, aura_codec: bool = False,
+                 ref_every: int = 10):
         self.slabs = {s.g: s for s in slabs}
         self.tr = transport
         self.params = params
         self.last = {}
+        self.aura_codec = aura_codec
+        self.ref_every = max(int(ref_every), 1)
+        self.iteration = 0
+        # row f3 references: (slab, "L"/"R") -> the last message sent that way, and
+        # (slab, "L"/"R") -> the receiver's copy of what arrives from that side
+        self.ref_send, self.ref_recv = {}, {}
 
     def migrate(self):
         sends = {g: s.ops.pack(s.agents, s.lo, s.hi, 0.0, PACK_MIGRATE) for g, s in self.slabs.items()}
@@ -245,7 +317,11 @@ class SlabDomain:
     def aura(self, R: float):
         margin = R * GHOST_MARGIN
         sends = {g: s.ops.pack(s.agents, s.lo, s.hi, margin, PACK_AURA) for g, s in self.slabs.items()}
-        recvs = self.tr.exchange(sends)
+        self.aura_bytes = [0, 0]  # (stream bytes, raw 40 B/agent bytes) sent
+        if self.aura_codec:
+            recvs = self._aura_codec(sends)
+        else:
+            recvs = self.tr.exchange(sends)
         n_ghosts = 0
         for g, s in self.slabs.items():
             fl, fr = recvs[g]
@@ -259,6 +335,46 @@ class SlabDomain:
             n_ghosts += total
         return n_ghosts
 
+    def _aura_codec(self, sends: dict) -> dict:
+        """Row f3: each direction encodes against the reference both ends hold; every
+        ref_every iterations both ends replace it with the message just exchanged (the
+        receiver's decoded copy has the same agents, so the id-ordered references stay
+        identical).  Ghost order does not enter a result (R9)."""
+        refresh = self.iteration % self.ref_every == 0
+        streams = {}
+        for g, (left, right) in sends.items():
+            ops = self.slabs[g].ops
+            enc = []
+            for side, msg in (("L", left), ("R", right)):
+                ref = self.ref_send.get((g, side))
+                if ref is None:
+                    ref = ops.empty_ref()
+                st = ops.aura_encode(msg, ref)
+                self.aura_bytes[0] += int(st.numel())
+                self.aura_bytes[1] += 40 * msg.n
+                enc.append(st)
+                if refresh:
+                    self.ref_send[(g, side)] = ops.aura_reference(msg)
+            streams[g] = tuple(enc)
+        got = self.tr.exchange_bytes(streams)
+        recvs = {}
+        for g, (bl, br) in got.items():
+            ops = self.slabs[g].ops
+            parts = []
+            for side, st in (("L", bl), ("R", br)):  # from the left / right neighbour
+                if st is None:
+                    parts.append(None)
+                    continue
+                ref = self.ref_recv.get((g, side))
+                if ref is None:
+                    ref = ops.empty_ref()
+                msg = ops.aura_decode(st, ref)
+                if refresh:
+                    self.ref_recv[(g, side)] = ops.aura_reference(msg)
+                parts.append(msg)
+            recvs[g] = tuple(parts)
+        return recvs
+
     def step(self):
         moved = self.migrate()
         f = self.frame()
@@ -267,4 +383,7 @@ class SlabDomain:
         for g, s in self.slabs.items():
             s.ops.compute(s.agents, s.ghosts, self.params)
         self.last = {"migrated": moved, "ghosts": ng, "frame": f}
+        if self.aura_codec:
+            self.last["aura_stream_bytes"], self.last["aura_raw_bytes"] = self.aura_bytes
+        self.iteration += 1
         return self.last

@@ -96,6 +96,20 @@ class OracleOps:
         agents.arrays["z"][:agents.n] = out["z"]
         agents.arrays["flags"][:agents.n] = out["flags"]
 
+    # row f3 codec (byte streams as torch uint8 CPU tensors)
+    def empty_ref(self):
+        return NpAgents(0)
+
+    def aura_reference(self, msg):
+        return NpAgents.from_state(oracle.aura_reference(msg.state()))
+
+    def aura_encode(self, msg, ref):
+        st = oracle.aura_encode(msg.state(), ref.state())
+        return torch.frombuffer(bytearray(st), dtype=torch.uint8)
+
+    def aura_decode(self, stream_bytes, ref):
+        return NpAgents.from_state(oracle.aura_decode(stream_bytes.numpy().tobytes(), ref.state()))
+
     # payloads for DistTransport (torch CPU tensors)
     def to_payload(self, a):
         p = {k: torch.from_numpy(np.ascontiguousarray(a.arrays[k][:a.n], np.float64)) for k in F64}

@@ -16,7 +16,7 @@ def _by_id(s):
     return {k: np.asarray(v)[o] for k, v in s.items()}
 
 
-def _slab_run(G, cfg, steps, params):
+def _slab_run(G, cfg, steps, params, codec=False):
     import torch
     from paper_2503_10796_b200 import Agents, Engine
     from paper_2503_10796_b200.slabs import LibOps, LocalTransport, Slab, SlabDomain, slab_bounds
@@ -35,7 +35,7 @@ def _slab_run(G, cfg, steps, params):
             getattr(a, k)[:n].copy_(getattr(full, k)[:cfg.n][m])
         a.n = n
         slabs.append(Slab(g, lo, hi, LibOps(Engine(0, a.capacity)), a))
-    dom = SlabDomain(slabs, LocalTransport(), params)
+    dom = SlabDomain(slabs, LocalTransport(), params, aura_codec=codec, ref_every=2)
     stats = [dom.step() for _ in range(steps)]
     torch.cuda.synchronize()
     parts = [s.agents.numpy() for s in slabs]
@@ -43,12 +43,15 @@ def _slab_run(G, cfg, steps, params):
     return _by_id(got), stats
 
 
-@pytest.mark.parametrize("G,n", [(2, 20_000), (4, 60_000), (8, 100_003)])
-def test_virtual_slabs_bit_identical(orc, G, n):
+@pytest.mark.parametrize("G,n,codec", [(2, 20_000, False), (4, 60_000, False), (8, 100_003, False),
+                                       (4, 60_000, True)])
+def test_virtual_slabs_bit_identical(orc, G, n, codec):
+    """codec: the aura travels as delta + LZ4 streams (row f3, bdm_aura_*), references
+    refreshed every 2 iterations."""
     from paper_2503_10796_b200 import Agents, Engine, Params
     cfg = W.cfg2_scaled(n)
     params = Params(detect_static=True)
-    got, stats = _slab_run(G, cfg, 4, params)
+    got, stats = _slab_run(G, cfg, 4, params, codec)
     # undivided GPU run
     a = Agents.empty(cfg.n)
     e = Engine(0, cfg.n)
@@ -70,6 +73,9 @@ def test_virtual_slabs_bit_identical(orc, G, n):
     for k in ("x", "y", "z", "flags"):
         assert np.array_equal(got[k], o[k]), k
     assert sum(s["ghosts"] for s in stats) > 0
+    if codec:
+        assert sum(s["aura_stream_bytes"] for s in stats[1:]) < sum(
+            s["aura_raw_bytes"] for s in stats[1:])
 
 
 def test_pack_slab_and_append(eng=None):

@@ -34,7 +34,7 @@ def _by_id(s):
     return {k: np.asarray(v)[o] for k, v in s.items()}
 
 
-def _run_slabs(G, slabs_owned, transport_factory, detect_static=False, tau=0.0):
+def _run_slabs(G, slabs_owned, transport_factory, detect_static=False, tau=0.0, codec=False):
     import oracle
     from paper_2503_10796_b200 import Params
     from paper_2503_10796_b200.slabs import Slab, SlabDomain, slab_bounds
@@ -49,18 +49,21 @@ def _run_slabs(G, slabs_owned, transport_factory, detect_static=False, tau=0.0):
         agents = NpAgents.from_state(s, (s["x"] >= lo) & (s["x"] < hi))
         slabs.append(Slab(g, lo, hi, ops, agents))
     tr = transport_factory(slabs)
-    dom = SlabDomain(slabs, tr, Params(detect_static=detect_static, force_threshold=tau))
+    dom = SlabDomain(slabs, tr, Params(detect_static=detect_static, force_threshold=tau),
+                     aura_codec=codec, ref_every=3)
     stats = []
     for _ in range(STEPS):
         stats.append(dom.step())
     return {sl.g: sl.agents.state() for sl in slabs}, stats
 
 
-@pytest.mark.parametrize("G", [2, 3, 5])
-def test_virtual_slabs_match_undivided_run(orc, G):
+@pytest.mark.parametrize("G,codec", [(2, False), (3, False), (5, False), (3, True)])
+def test_virtual_slabs_match_undivided_run(orc, G, codec):
+    """codec: the aura travels as delta + LZ4 streams (row f3), references refreshed
+    every 3 iterations."""
     from paper_2503_10796_b200.slabs import LocalTransport
     ref = _by_id(_reference(orc, STEPS))
-    parts, stats = _run_slabs(G, range(G), lambda slabs: LocalTransport())
+    parts, stats = _run_slabs(G, range(G), lambda slabs: LocalTransport(), codec=codec)
     got = {k: np.concatenate([parts[g][k] for g in range(G)]) for k in ref}
     got = _by_id(got)
     assert np.array_equal(got["id"], ref["id"])          # every agent exactly once
@@ -68,6 +71,9 @@ def test_virtual_slabs_match_undivided_run(orc, G):
         assert np.array_equal(got[k], ref[k]), k
     assert sum(st["ghosts"] for st in stats) > 0
     assert sum(st["migrated"] for st in stats) > 0       # migration actually exercised
+    if codec:  # steps after the first reference travel as deltas
+        assert sum(st["aura_stream_bytes"] for st in stats[1:]) < sum(
+            st["aura_raw_bytes"] for st in stats[1:])
 
 
 def test_virtual_slabs_static_skip(orc):
@@ -87,7 +93,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, outdir):
+def _worker(rank, world, port, outdir, codec=False):
     import sys
     sys.path.insert(0, ROOT)
     sys.path.insert(0, os.path.join(ROOT, "tests"))
@@ -97,7 +103,7 @@ def _worker(rank, world, port, outdir):
     from paper_2503_10796_b200.slabs import DistTransport
     try:
         parts, stats = _run_slabs(world, [rank],
-                                  lambda slabs: DistTransport(slabs[0].ops, "cpu"))
+                                  lambda slabs: DistTransport(slabs[0].ops, "cpu"), codec=codec)
         np.savez(os.path.join(outdir, f"rank{rank}.npz"), **parts[rank],
                  migrated=np.array([st["migrated"] for st in stats]),
                  ghosts=np.array([st["ghosts"] for st in stats]))
@@ -105,13 +111,15 @@ def _worker(rank, world, port, outdir):
         dist.destroy_process_group()
 
 
-def test_gloo_world_size_2_matches_undivided_run(orc, tmp_path):
+@pytest.mark.parametrize("codec", [False, True], ids=["raw_aura", "delta_lz4_aura"])
+def test_gloo_world_size_2_matches_undivided_run(orc, tmp_path, codec):
     """world_size-2 gloo run of the protocol with the DistTransport (the transport used
-    over NCCL on GPUs) is bit-identical to the undivided run."""
+    over NCCL on GPUs) is bit-identical to the undivided run, with the aura sent as
+    SoA fields or as delta + LZ4 byte streams (row f3)."""
     world = 2
     port = _free_port()
-    mp.start_processes(_worker, args=(world, port, str(tmp_path)), nprocs=world, join=True,
-                       start_method="spawn")
+    mp.start_processes(_worker, args=(world, port, str(tmp_path), codec), nprocs=world,
+                       join=True, start_method="spawn")
     ref = _by_id(_reference(orc, STEPS))
     parts = [dict(np.load(tmp_path / f"rank{r}.npz")) for r in range(world)]
     got = _by_id({k: np.concatenate([p[k] for p in parts]) for k in ref})
