@@ -170,6 +170,25 @@ static void tile_curve(int order, uint16_t *rank, uint16_t *inv) {
     }
 }
 
+// Makes the context's device current for one entry point and restores the caller's
+// (contexts on several devices may share a thread).
+struct DeviceScope {
+    int prev = -1;
+    explicit DeviceScope(bdm_handle h) {
+        if (!h) return;
+        const int want = ((Ctx *)h)->device;
+        if (cudaGetDevice(&prev) != cudaSuccess) {
+            cudaGetLastError();
+            prev = -1;
+        }
+        if (prev != want) cudaSetDevice(want);
+        else prev = -1;
+    }
+    ~DeviceScope() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
 }  // namespace bdm
 
 using namespace bdm;
@@ -186,7 +205,8 @@ bdm_status bdm_create(bdm_handle *out, int device, int64_t max_agents) {
     if (max_agents < 0) return fail(BDM_EINVAL, "max_agents < 0");
     int ndev = 0;
     BDM_CUDA_TRY(cudaGetDeviceCount(&ndev));
-    if (device < 0 || device >= ndev) return fail(BDM_EINVAL, "bad device index");
+    if (device < 0 || device >= ndev || device >= kMaxDevices)
+        return fail(BDM_EINVAL, "bad device index");
     BDM_CUDA_TRY(cudaSetDevice(device));
     Ctx *c = new Ctx();
     c->device = device;
@@ -236,6 +256,7 @@ bdm_status bdm_destroy(bdm_handle h) {
 bdm_status bdm_init_spheres(bdm_handle h, bdm_agents *a, int64_t id0, int64_t n, uint64_t seed,
                             double side, double d_lo, double d_width, int32_t d_random,
                             void *stream) {
+    DeviceScope ds__(h);
     if (h) ((Ctx *)h)->fused_valid = false;
     if (!h) return fail(BDM_EINVAL, "handle is NULL");
     if (!a || n < 0 || n > a->capacity || id0 < 0)
@@ -250,6 +271,7 @@ bdm_status bdm_init_spheres(bdm_handle h, bdm_agents *a, int64_t id0, int64_t n,
 
 bdm_status bdm_grid_build(bdm_handle h, const bdm_agents *a, const bdm_agents *ghosts,
                           double radius, void *stream) {
+    DeviceScope ds__(h);
     if (!h) return fail(BDM_EINVAL, "handle is NULL");
     Ctx *c = (Ctx *)h;
     bdm_status s = check_agents(a, true);
@@ -297,6 +319,7 @@ bdm_status bdm_grid_build(bdm_handle h, const bdm_agents *a, const bdm_agents *g
 }
 
 bdm_status bdm_mech_step(bdm_handle h, bdm_agents *a, const bdm_params *p, void *stream) {
+    DeviceScope ds__(h);
     if (!h || !p) return fail(BDM_EINVAL, "handle or params is NULL");
     Ctx *c = (Ctx *)h;
     bdm_status s = check_agents(a, true);
@@ -320,6 +343,7 @@ bdm_status bdm_mech_step(bdm_handle h, bdm_agents *a, const bdm_params *p, void 
 }
 
 bdm_status bdm_step(bdm_handle h, bdm_agents *a, const bdm_params *p, void *stream) {
+    DeviceScope ds__(h);
     if (!p) return fail(BDM_EINVAL, "params is NULL");
     bdm_status s = bdm_grid_build(h, a, nullptr, p->radius, stream);
     if (s != BDM_OK) return s;
@@ -328,6 +352,7 @@ bdm_status bdm_step(bdm_handle h, bdm_agents *a, const bdm_params *p, void *stre
 
 bdm_status bdm_step_host(bdm_handle h, const bdm_agents *hin, bdm_agents *hout, bdm_agents *dev,
                          const bdm_params *p, void *stream) {
+    DeviceScope ds__(h);
     if (!h || !hin || !hout || !dev || !p) return fail(BDM_EINVAL, "NULL argument");
     if (hin->n > dev->capacity || hin->n > hout->capacity)
         return fail(BDM_EINVAL, "n exceeds a capacity");
@@ -359,6 +384,7 @@ bdm_status bdm_step_host(bdm_handle h, const bdm_agents *hin, bdm_agents *hout, 
 
 bdm_status bdm_grow_divide(bdm_handle h, bdm_agents *a, const bdm_params *p, double growth,
                            double v_max, int64_t *n_out_host, void *stream) {
+    DeviceScope ds__(h);
     if (h) ((Ctx *)h)->fused_valid = false;
     if (!h || !p || !n_out_host) return fail(BDM_EINVAL, "NULL argument");
     Ctx *c = (Ctx *)h;
@@ -376,6 +402,7 @@ bdm_status bdm_grow_divide(bdm_handle h, bdm_agents *a, const bdm_params *p, dou
 bdm_status bdm_onco_step(bdm_handle h, bdm_agents *a, uint32_t *age, int64_t age_cap,
                          const bdm_onco_params *p, int64_t id_next, int64_t *out_host,
                          void *stream) {
+    DeviceScope ds__(h);
     if (h) ((Ctx *)h)->fused_valid = false;
     if (!h || !p || !out_host) return fail(BDM_EINVAL, "NULL argument");
     Ctx *c = (Ctx *)h;
@@ -403,6 +430,7 @@ bdm_status bdm_onco_step(bdm_handle h, bdm_agents *a, uint32_t *age, int64_t age
 bdm_status bdm_sir_step(bdm_handle h, bdm_agents *a, const bdm_params *p, double side,
                         double radius, double p_inf, double p_rec, int64_t *counts_host,
                         void *stream) {
+    DeviceScope ds__(h);
     if (h) ((Ctx *)h)->fused_valid = false;
     if (!h || !p || !a) return fail(BDM_EINVAL, "NULL argument");
     Ctx *c = (Ctx *)h;
@@ -429,6 +457,7 @@ static bdm_status check_grid3(const bdm_grid3 *g) {
 
 bdm_status bdm_diffuse(bdm_handle h, const double *u_in, double *u_out, const bdm_grid3 *g,
                        double nu, double mu, double dt, void *stream) {
+    DeviceScope ds__(h);
     if (!h) return fail(BDM_EINVAL, "handle is NULL");
     bdm_status s = check_grid3(g);
     if (s != BDM_OK) return s;
@@ -439,6 +468,7 @@ bdm_status bdm_diffuse(bdm_handle h, const double *u_in, double *u_out, const bd
 
 bdm_status bdm_secrete(bdm_handle h, const bdm_agents *a, const uint8_t *type, int32_t type_sel,
                        double q, double *u, const bdm_grid3 *g, void *stream) {
+    DeviceScope ds__(h);
     if (!h || !a) return fail(BDM_EINVAL, "NULL argument");
     bdm_status s = check_grid3(g);
     if (s != BDM_OK) return s;
@@ -451,6 +481,7 @@ bdm_status bdm_secrete(bdm_handle h, const bdm_agents *a, const uint8_t *type, i
 
 bdm_status bdm_chemotaxis(bdm_handle h, bdm_agents *a, const uint8_t *type, int32_t type_sel,
                           double weight, const double *u, const bdm_grid3 *g, void *stream) {
+    DeviceScope ds__(h);
     if (h) ((Ctx *)h)->fused_valid = false;
     if (!h || !a) return fail(BDM_EINVAL, "NULL argument");
     bdm_status s = check_grid3(g);
@@ -464,6 +495,7 @@ bdm_status bdm_chemotaxis(bdm_handle h, bdm_agents *a, const uint8_t *type, int3
 }
 
 bdm_status bdm_local_frame(bdm_handle h, const bdm_agents *a, double *frame_dev, void *stream) {
+    DeviceScope ds__(h);
     if (!h || !a || !frame_dev) return fail(BDM_EINVAL, "NULL argument");
     bdm_status s = check_agents(a, true);
     if (s != BDM_OK) return s;
@@ -471,6 +503,7 @@ bdm_status bdm_local_frame(bdm_handle h, const bdm_agents *a, double *frame_dev,
 }
 
 bdm_status bdm_set_frame(bdm_handle h, const double *frame_dev) {
+    DeviceScope ds__(h);
     if (h) ((Ctx *)h)->fused_valid = false;
     if (!h) return fail(BDM_EINVAL, "handle is NULL");
     Ctx *c = (Ctx *)h;
@@ -482,6 +515,7 @@ bdm_status bdm_set_frame(bdm_handle h, const double *frame_dev) {
 bdm_status bdm_pack_slab(bdm_handle h, bdm_agents *a, double lo, double hi, double margin,
                          int32_t what, bdm_agents *to_left, bdm_agents *to_right,
                          int64_t *counts_host, void *stream) {
+    DeviceScope ds__(h);
     if (h) ((Ctx *)h)->fused_valid = false;
     if (!h || !a || !to_left || !to_right || !counts_host) return fail(BDM_EINVAL, "NULL argument");
     if (what != BDM_PACK_MIGRATE && what != BDM_PACK_AURA) return fail(BDM_EINVAL, "bad what");
@@ -496,6 +530,7 @@ bdm_status bdm_pack_slab(bdm_handle h, bdm_agents *a, double lo, double hi, doub
 }
 
 bdm_status bdm_append(bdm_handle h, bdm_agents *dst, const bdm_agents *src, void *stream) {
+    DeviceScope ds__(h);
     if (h) ((Ctx *)h)->fused_valid = false;
     if (!h || !dst || !src) return fail(BDM_EINVAL, "NULL argument");
     if (src->n < 0 || dst->n < 0) return fail(BDM_EINVAL, "negative n");
@@ -516,6 +551,7 @@ bdm_status bdm_append(bdm_handle h, bdm_agents *dst, const bdm_agents *src, void
 }
 
 bdm_status bdm_sync(bdm_handle h, void *stream) {
+    DeviceScope ds__(h);
     if (!h) return fail(BDM_EINVAL, "handle is NULL");
     Ctx *c = (Ctx *)h;
     BDM_CUDA_TRY(cudaStreamSynchronize((cudaStream_t)stream));
@@ -524,6 +560,7 @@ bdm_status bdm_sync(bdm_handle h, void *stream) {
 }
 
 bdm_status bdm_reserve(bdm_handle h, int64_t max_agents, int64_t nslots) {
+    DeviceScope ds__(h);
     if (!h) return fail(BDM_EINVAL, "handle is NULL");
     Ctx *c = (Ctx *)h;
     bdm_status s = grow_agents(c, max_agents);
@@ -532,6 +569,7 @@ bdm_status bdm_reserve(bdm_handle h, int64_t max_agents, int64_t nslots) {
 }
 
 bdm_status bdm_get_stats(bdm_handle h, bdm_stats *out) {
+    DeviceScope ds__(h);
     if (!h || !out) return fail(BDM_EINVAL, "NULL argument");
     Ctx *c = (Ctx *)h;
     BDM_CUDA_TRY(cudaDeviceSynchronize());
@@ -546,6 +584,7 @@ bdm_status bdm_get_stats(bdm_handle h, bdm_stats *out) {
 }
 
 bdm_status bdm_get_grid_info(bdm_handle h, bdm_grid_info *out) {
+    DeviceScope ds__(h);
     if (!h || !out) return fail(BDM_EINVAL, "NULL argument");
     Ctx *c = (Ctx *)h;
     BDM_CUDA_TRY(cudaDeviceSynchronize());
@@ -565,6 +604,7 @@ bdm_status bdm_get_grid_info(bdm_handle h, bdm_grid_info *out) {
 
 bdm_status bdm_neighbor_pairs(bdm_handle h, const bdm_agents *a, double radius, uint64_t *pairs,
                               int64_t cap, int64_t *count_host, void *stream) {
+    DeviceScope ds__(h);
     if (!h || !count_host) return fail(BDM_EINVAL, "NULL argument");
     if (cap > 0 && !pairs) return fail(BDM_EINVAL, "pairs is NULL");
     Ctx *c = (Ctx *)h;
@@ -583,6 +623,7 @@ bdm_status bdm_neighbor_pairs(bdm_handle h, const bdm_agents *a, double radius, 
 }
 
 bdm_status bdm_set_option(bdm_handle h, const char *name, int64_t value) {
+    DeviceScope ds__(h);
     if (!h || !name) return fail(BDM_EINVAL, "NULL argument");
     Ctx *c = (Ctx *)h;
     if (strcmp(name, "mech_kernel") == 0) {
@@ -659,6 +700,7 @@ static bdm_status check_aura_agents(const bdm_agents *a, const char *what) {
 }
 
 bdm_status bdm_aura_reference(bdm_handle h, const bdm_agents *msg, bdm_agents *ref, void *stream) {
+    DeviceScope ds__(h);
     if (!h) return fail(BDM_EINVAL, "handle is NULL");
     bdm_status s;
     if ((s = check_aura_agents(msg, "msg")) != BDM_OK) return s;
@@ -671,6 +713,7 @@ bdm_status bdm_aura_reference(bdm_handle h, const bdm_agents *msg, bdm_agents *r
 
 bdm_status bdm_aura_encode(bdm_handle h, const bdm_agents *msg, const bdm_agents *ref,
                            uint8_t *out, int64_t out_cap, int64_t *out_size_host, void *stream) {
+    DeviceScope ds__(h);
     if (!h || !out_size_host) return fail(BDM_EINVAL, "handle or out_size_host is NULL");
     bdm_status s;
     if ((s = check_aura_agents(msg, "msg")) != BDM_OK) return s;
@@ -681,6 +724,7 @@ bdm_status bdm_aura_encode(bdm_handle h, const bdm_agents *msg, const bdm_agents
 
 bdm_status bdm_aura_decode(bdm_handle h, const uint8_t *in, int64_t in_size, const bdm_agents *ref,
                            bdm_agents *msg, void *stream) {
+    DeviceScope ds__(h);
     if (!h || !in) return fail(BDM_EINVAL, "handle or in is NULL");
     bdm_status s;
     if ((s = check_aura_agents(ref, "ref")) != BDM_OK) return s;
@@ -698,6 +742,7 @@ bdm_status bdm_tile_curve(int32_t order, uint16_t *rank_out) {
 }
 
 bdm_status bdm_peak_dfma(bdm_handle h, double *dfma_per_s, int32_t *sm_count) {
+    DeviceScope ds__(h);
     if (!h || !dfma_per_s || !sm_count) return fail(BDM_EINVAL, "NULL argument");
     Ctx *c = (Ctx *)h;
     *sm_count = c->sm_count;

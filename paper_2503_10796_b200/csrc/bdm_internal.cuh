@@ -77,6 +77,9 @@ struct AuraWs {
     long long *res = nullptr;
 };
 
+// Kernel attributes and occupancy are set once per device (arrays indexed by device).
+constexpr int kMaxDevices = 64;
+
 // ------------------------------------------------------------------ library context
 struct Ctx {
     int device = 0;

@@ -556,12 +556,12 @@ bdm_status launch_aura_encode(Ctx *c, const bdm_agents *m, const bdm_agents *r, 
     }
     BDM_LAUNCH_CHECK("k_aura_fill");
     if (nch_max > 0) {
-        static bool attr = false;
+        static bool attr_dev[kMaxDevices] = {};
         const int smem = (int)(sizeof(LzWarp) * kLzWarps);
-        if (!attr) {
+        if (!attr_dev[c->device]) {
             BDM_CUDA_TRY(cudaFuncSetAttribute(k_lz4_compress,
                                               cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-            attr = true;
+            attr_dev[c->device] = true;
         }
         k_lz4_compress<<<nblk(nch_max, kLzWarps), 32 * kLzWarps, smem, st>>>(
             W.pay, newrank, n, nref, nch_max, W.tmp, W.sizes);

@@ -264,10 +264,12 @@ static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
 bdm_status launch_diffuse(Ctx *c, const double *u_in, double *u_out, const bdm_grid3 *g,
                           double nu, double mu, double dt, cudaStream_t st) {
     if (g->nx <= 0 || g->ny <= 0 || g->nz <= 0) return BDM_OK;
-    static int per_sm = 0;
+    static int per_sm_dev[kMaxDevices] = {};
+    int &per_sm = per_sm_dev[c->device];
     if (!per_sm) {
-        BDM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_diffuse, kFThreads, 0));
-        if (per_sm < 1) per_sm = 1;
+        int v = 0;
+        BDM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k_diffuse, kFThreads, 0));
+        per_sm = v < 1 ? 1 : v;
     }
     DiffArgs A;
     A.u = u_in;
@@ -287,13 +289,15 @@ bdm_status launch_diffuse(Ctx *c, const double *u_in, double *u_out, const bdm_g
     // grids narrower than one box take the other kernel
     PFN_cuTensorMapEncodeTiled_v12000 enc = c->diffuse_tma ? tensor_map_encoder() : nullptr;
     if (enc && (A.nx % 2) == 0 && A.nx >= kTBx && A.ny >= kTBy) {
-        static int per_sm_t = 0;
+        static int per_sm_t_dev[kMaxDevices] = {};
+        int &per_sm_t = per_sm_t_dev[c->device];
         if (!per_sm_t) {
             BDM_CUDA_TRY(cudaFuncSetAttribute(k_diffuse_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                               kTSmem));
-            BDM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_t, k_diffuse_tma,
+            int v = 0;
+            BDM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k_diffuse_tma,
                                                                        kFThreads, kTSmem));
-            if (per_sm_t < 1) per_sm_t = 1;
+            per_sm_t = v < 1 ? 1 : v;
         }
         CUtensorMap tm;
         const cuuint64_t gdim[3] = {(cuuint64_t)A.nx, (cuuint64_t)A.ny, (cuuint64_t)A.nz};

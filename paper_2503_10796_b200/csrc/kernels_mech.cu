@@ -1172,16 +1172,16 @@ __global__ void __launch_bounds__(kT6Threads, kMinBlocks) k_mech_tile6(MechArgs 
 
 template <bool kStats, int kMinBlocks, bool kPair>
 static bdm_status launch_tile6(Ctx *c, const MechArgs &A, cudaStream_t st) {
-    static bool attr_set = false;
-    static int per_sm = 0;
+    static int per_sm_dev[kMaxDevices] = {};
+    int &per_sm = per_sm_dev[c->device];
     const int smem = (int)sizeof(Tile6SmemT<kPair>);
-    if (!attr_set) {
+    if (!per_sm) {
         BDM_CUDA_TRY(cudaFuncSetAttribute(k_mech_tile6<kStats, kMinBlocks, kPair>,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        int v = 0;
         BDM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-            &per_sm, k_mech_tile6<kStats, kMinBlocks, kPair>, kT6Threads, smem));
-        if (per_sm < 1) per_sm = 1;
-        attr_set = true;
+            &v, k_mech_tile6<kStats, kMinBlocks, kPair>, kT6Threads, smem));
+        per_sm = v < 1 ? 1 : v;
     }
     k_mech_tile6<kStats, kMinBlocks, kPair><<<(unsigned)(c->sm_count * per_sm), kT6Threads, smem, st>>>(
         A, c->sc, c->prefilter);
@@ -1190,16 +1190,16 @@ static bdm_status launch_tile6(Ctx *c, const MechArgs &A, cudaStream_t st) {
 
 template <bool kStats>
 static bdm_status launch_tile(Ctx *c, const MechArgs &A, cudaStream_t st) {
-    static bool attr_set = false;
-    static int per_sm = 0;
+    static int per_sm_dev[kMaxDevices] = {};
+    int &per_sm = per_sm_dev[c->device];
     const int smem = (int)sizeof(TileSmem);
-    if (!attr_set) {
+    if (!per_sm) {
         BDM_CUDA_TRY(cudaFuncSetAttribute(k_mech_tile<kStats>,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        BDM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mech_tile<kStats>,
+        int v = 0;
+        BDM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k_mech_tile<kStats>,
                                                                    kTileThreads, smem));
-        if (per_sm < 1) per_sm = 1;
-        attr_set = true;
+        per_sm = v < 1 ? 1 : v;
     }
     k_mech_tile<kStats><<<(unsigned)(c->sm_count * per_sm), kTileThreads, smem, st>>>(
         A, c->sc, c->prefilter);
@@ -1491,14 +1491,16 @@ __global__ void __launch_bounds__(32 * kDWarps, 4) k_mech_dense(MechArgs A, DevS
 
 template <bool kStats>
 static bdm_status launch_dense(Ctx *c, const MechArgs &A, cudaStream_t st) {
-    static int per_sm = 0;
+    static int per_sm_dev[kMaxDevices] = {};
+    int &per_sm = per_sm_dev[c->device];
     const int smem = (int)(sizeof(DenseWarp) * kDWarps);
     if (!per_sm) {
         BDM_CUDA_TRY(cudaFuncSetAttribute(k_mech_dense<kStats>,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        BDM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mech_dense<kStats>,
+        int v = 0;
+        BDM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k_mech_dense<kStats>,
                                                                    32 * kDWarps, smem));
-        if (per_sm < 1) per_sm = 1;
+        per_sm = v < 1 ? 1 : v;
     }
     k_mech_dense<kStats><<<(unsigned)(c->sm_count * per_sm), 32 * kDWarps, smem, st>>>(A, c->sc);
     return BDM_OK;
