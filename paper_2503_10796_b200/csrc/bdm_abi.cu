@@ -359,6 +359,7 @@ bdm_status bdm_step_host(bdm_handle h, const bdm_agents *hin, bdm_agents *hout, 
     cudaStream_t st = (cudaStream_t)stream;
     const size_t n = (size_t)hin->n;
     dev->n = hin->n;
+    ((Ctx *)h)->fused_valid = false;  // the device arrays are overwritten from the host
     BDM_CUDA_TRY(cudaMemcpyAsync(dev->x, hin->x, n * 8, cudaMemcpyHostToDevice, st));
     BDM_CUDA_TRY(cudaMemcpyAsync(dev->y, hin->y, n * 8, cudaMemcpyHostToDevice, st));
     BDM_CUDA_TRY(cudaMemcpyAsync(dev->z, hin->z, n * 8, cudaMemcpyHostToDevice, st));

@@ -290,6 +290,34 @@ def test_step_host_equals_device_step(eng, orc):
     assert_state_equal(got, want, "step_host")
 
 
+def test_step_host_new_input_ignores_fused_extent(eng, orc):
+    """bdm_step_host overwrites the device arrays from the host, so a fused extent left
+    by the previous step (option fuse_reduce) must not be reused: a second call with
+    different host data (shifted by 40 um) still matches the oracle."""
+    import torch
+    from paper_2503_10796_b200 import Agents
+    cfg = W.cfg2_scaled(30_000)
+    gp, op = params_pair(orc, cfg)
+    dev = Agents.empty(cfg.n)
+    hin = Agents.empty(cfg.n, pin=True)
+    hout = Agents.empty(cfg.n, pin=True)
+    for shift in (0.0, 40.0):
+        o = orc_init(orc, cfg)
+        for k in ("x", "y", "z"):
+            o[k] = o[k] + shift
+        for k, src in (("x", "x"), ("y", "y"), ("z", "z"), ("diameter", "d")):
+            getattr(hin, k).copy_(torch.from_numpy(o[src]))
+        hin.id.copy_(torch.from_numpy(o["id"].view(np.int32)))
+        hin.flags.copy_(torch.from_numpy(o["flags"].view(np.int32)))
+        hin.n = cfg.n
+        eng.step_host(hin, hout, dev, gp)
+        want, _ = orc.step_full(o, op)
+        got = {"x": hout.x.numpy(), "y": hout.y.numpy(), "z": hout.z.numpy(),
+               "d": hout.diameter.numpy(), "id": hout.id.numpy().view(np.uint32),
+               "flags": hout.flags.numpy().view(np.uint32)}
+        assert_state_equal(got, want, f"step_host shift {shift}")
+
+
 @pytest.mark.slow
 def test_cfg2_full_size_teacher_forced(eng, orc):
     """configs[1] at full size (10M agents), the bench's launch configuration: after
