@@ -540,6 +540,16 @@ def run_onco(args, ws, rank, local):
     tiles = int(math.ceil((cfg.side + 2 * steps) / 10.0 / 4.0)) + 8
     eng.reserve(cap, tiles ** 3 * 64)
     id_next = cfg.n
+    if args.warmup:  # one untimed step on a scratch copy: lazy buffers, first launches
+        w = Agents.empty(cap, volume=True)
+        for f in ("x", "y", "z", "diameter", "id", "flags", "volume"):
+            getattr(w, f)[:a.n].copy_(getattr(a, f)[:a.n])
+        w.n = a.n
+        eng.step(w, mp, stream=stream)
+        eng.onco_step(w, age.clone(), COncoParams.make(step=0, seed=cfg.seed), id_next,
+                      stream=stream)
+        torch.cuda.synchronize()
+        del w
     per_step = []
     launches0 = eng.stats()["launches"]
     with ClockSampler(local) as clk:
