@@ -817,8 +817,22 @@ def measure_e2e(eng, cfg, params, stream, steps: int = 7):
     eng.set_option("sort_every", 1)
     bi = n * (4 * 8 + 2 * 4)
     bo = n * (3 * 8 + 4)
+    # the PCIe floor: the same bytes copied alone (pinned host <-> device, same stream)
+    tr = []
+    for _ in range(3):
+        t0 = time.perf_counter()
+        for f in ("x", "y", "z", "diameter", "id", "flags"):
+            getattr(dev, f)[:n].copy_(getattr(hout, f)[:n], non_blocking=True)
+        for f in ("x", "y", "z", "flags"):
+            getattr(hout, f)[:n].copy_(getattr(dev, f)[:n], non_blocking=True)
+        torch.cuda.synchronize()
+        tr.append(time.perf_counter() - t0)
+    t_copy = statistics.median(tr)
     return {"value": n / dt, "unit": UNIT, "h2d_bytes_per_step": bi, "d2h_bytes_per_step": bo,
             "ms_per_step": dt * 1e3, "ms_per_step_all": [round(t * 1e3, 3) for t in times],
+            "copy_only_ms": t_copy * 1e3,
+            "copy_gbs": (bi + bo) / t_copy / 1e9,
+            "note": "floor = copy_only_ms + the device step; the copies are PCIe-bound",
             "timing": "host clock around each synchronizing call, median of the steps",
             "api": "bdm_step_host (C ABI, pinned host buffers, in place, sort_every 0)"}
 
