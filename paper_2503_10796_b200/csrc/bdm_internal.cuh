@@ -47,6 +47,7 @@ struct DevScalars {
     int32_t has_frame;     // the origin came from a global frame (multi-GPU)
     unsigned int n_dense;  // dense tiles handed from the tile kernel to the dense kernel
     unsigned int dense_next;  // dense kernel work counter (box tasks taken)
+    unsigned int tile_next;   // tile kernel work counter (tiles taken)
     double dmax_prev;      // max diameter of the grid build's input (the step keeps it)
     int32_t tile_order;    // option "tile_order" (row f1): 0 row-major tiles, 1 blocked Hilbert
     uint16_t hilb[512];    // blocked Hilbert: local tile (x | y<<3 | z<<6) -> curve position

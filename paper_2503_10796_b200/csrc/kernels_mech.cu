@@ -638,6 +638,7 @@ struct Tile6SmemT {
     GridView g;
     float R2f, Lf;
     int use_pf, edge_only;                  // edge_only: fused extent from boundary tiles only
+    int next_tile[2];                       // dynamic tile scheduling (ping-pong)
     int lo_box[3], hi_box[3];               // boxes that can hold a new extremum (see below)
     uint32_t start[216];
     uint32_t off[220];
@@ -1007,22 +1008,18 @@ __global__ void __launch_bounds__(kT6Threads, kMinBlocks) k_mech_tile6(MechArgs 
     __syncthreads();
     const int T0 = S.g.T0, T1 = S.g.T1;
     const int ntiles = T0 * T1 * S.g.T2;  // < 2^26 (nslots < 2^32)
-    // tile coordinates advance incrementally by gridDim.x (no divisions per tile)
-    const int gsx = (int)gridDim.x % T0, gsy = ((int)gridDim.x / T0) % T1,
-              gsz = (int)gridDim.x / (T0 * T1);
-    int tx = (int)blockIdx.x % T0, ty = ((int)blockIdx.x / T0) % T1, tz = (int)blockIdx.x / (T0 * T1);
+    int tx, ty, tz;
 
     const uint16_t *const hilb = S.g.hilb, *const hilb_inv = S.g.hilb_inv;
-    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        if (hilb_inv) {
-            tile_xyz((uint32_t)t, T0, T1, hilb_inv, tx, ty, tz);
-        } else if (t != (int)blockIdx.x) {
-            tx += gsx;
-            ty += gsy;
-            tz += gsz;
-            if (tx >= T0) { tx -= T0; ++ty; }
-            if (ty >= T1) { ty -= T1; ++tz; }
-        }
+    // tiles are taken from a device counter: no tail imbalance between the persistent
+    // CTAs (a static stride left 8 % on the table at cfg2); the broadcast slot
+    // alternates so a slow warp still reads this tile's number while the next is drawn
+    for (int it = 0;; ++it) {
+        if (tid == 0) S.next_tile[it & 1] = (int)atomicAdd(&sc->tile_next, 1u);
+        __syncthreads();
+        const int t = S.next_tile[it & 1];
+        if (t >= ntiles) break;
+        tile_xyz((uint32_t)t, T0, T1, hilb_inv, tx, ty, tz);
         const uint32_t g0 = A.box_start[(uint32_t)t * 64u];
         const int nc = (int)(A.box_start[(uint32_t)t * 64u + 64u] - g0);
         if (nc == 0) continue;  // uniform across the CTA
@@ -1529,7 +1526,7 @@ bdm_status launch_mech(Ctx *c, bdm_agents *a, const bdm_params *p, cudaStream_t 
         BDM_CUDA_TRY(cudaMemsetAsync(c->sc->stats, 0, sizeof(c->sc->stats), st));
     const bool dense = c->dense && (c->mech_kernel == 0 || c->mech_kernel == 3);
     A.dense_list = dense ? c->dense_list : nullptr;
-    if (dense) BDM_CUDA_TRY(cudaMemsetAsync(&c->sc->n_dense, 0, 2 * sizeof(unsigned int), st));
+    BDM_CUDA_TRY(cudaMemsetAsync(&c->sc->n_dense, 0, 3 * sizeof(unsigned int), st));
     if (c->mech_kernel == 0) {
         const bdm_status s = p->collect_stats ? launch_tile6<true, 5, false>(c, A, st)
                                               : launch_tile6<false, 5, false>(c, A, st);
