@@ -707,27 +707,6 @@ __device__ __forceinline__ void merge_counts(const Counts &c, Warp6 &Wp, int sid
     __syncwarp();
 }
 
-// Eq. 4.1/4.2 for one contact candidate: s = F_N / dist and its flags
-template <class SmemT>
-__device__ __forceinline__ void contact_force6(const MechArgs &A, const SmemT &S, double D,
-                                               uint32_t e, unsigned stat_mask, double &s_,
-                                               uint8_t &fl) {
-    const int m = (int)(e & 511u), mo = (int)((e >> 9) & 511u);
-    s_ = 0.0;
-    fl = 0;
-    if (!((stat_mask >> ((e >> 18) & 31u)) & 1u)) {
-        const double dist = sqrt(D);
-        const double ri = S.Rr[mo], rj = S.Rr[m];
-        const double delta = (ri + rj) - dist;
-        if (delta > 0.0) {
-            const double rbar = (ri * rj) / (ri + rj);
-            const double Fn = A.k * delta - A.gamma * sqrt(rbar * delta);
-            s_ = Fn / dist;
-            fl = (uint8_t)(2u | (Fn != 0.0 ? 1u : 0u));
-        }
-    }
-}
-
 // One batch of <= 32 agents of the staged tile (lane = tile agent klo + lane).
 template <bool kStats, bool kPair>
 __device__ __forceinline__ void tile6_batch(const MechArgs &A, const Tile6SmemT<kPair> &S, Warp6 &Wp,
@@ -920,12 +899,28 @@ __device__ __forceinline__ void tile6_batch(const MechArgs &A, const Tile6SmemT<
             const bool is_static = cand_static && !Wp.chg[lane];
             const unsigned stat_mask = __ballot_sync(0xffffffffu, is_static);
             // ---- phase 2b: Eq. 4.1/4.2 over the compacted contact candidates
-            for (int q = lane; q < cbase; q += 32) {
-                double s_;
-                uint8_t fl;
-                contact_force6(A, S, Wp.u.b.cq[q], Wp.u.b.ce[q], stat_mask, s_, fl);
-                Wp.u.b.cq[q] = s_;
-                Wp.u.b.cf[q] = fl;
+            for (int q = lane; q < cbase; q += 64) {  // two contacts per lane, straight-line
+                const int q2 = q + 32;
+                const bool h2 = q2 < cbase;
+                const uint32_t e1 = Wp.u.b.ce[q], e2 = h2 ? Wp.u.b.ce[q2] : e1;
+                const double D1 = Wp.u.b.cq[q], D2 = h2 ? Wp.u.b.cq[q2] : D1;
+                const double ri1 = S.Rr[(e1 >> 9) & 511u], rj1 = S.Rr[e1 & 511u];
+                const double ri2 = S.Rr[(e2 >> 9) & 511u], rj2 = S.Rr[e2 & 511u];
+                const double dist1 = sqrt(D1), dist2 = sqrt(D2);
+                const double del1 = (ri1 + rj1) - dist1, del2 = (ri2 + rj2) - dist2;
+                const double rb1 = (ri1 * rj1) / (ri1 + rj1);
+                const double rb2 = (ri2 * rj2) / (ri2 + rj2);
+                const double Fn1 = A.k * del1 - A.gamma * sqrt(rb1 * del1);
+                const double Fn2 = A.k * del2 - A.gamma * sqrt(rb2 * del2);
+                const double s1 = Fn1 / dist1, s2 = Fn2 / dist2;
+                const bool c1 = del1 > 0.0 && !((stat_mask >> ((e1 >> 18) & 31u)) & 1u);
+                const bool c2 = del2 > 0.0 && !((stat_mask >> ((e2 >> 18) & 31u)) & 1u);
+                Wp.u.b.cq[q] = c1 ? s1 : 0.0;
+                Wp.u.b.cf[q] = c1 ? (uint8_t)(2u | (Fn1 != 0.0 ? 1u : 0u)) : (uint8_t)0;
+                if (h2) {
+                    Wp.u.b.cq[q2] = c2 ? s2 : 0.0;
+                    Wp.u.b.cf[q2] = c2 ? (uint8_t)(2u | (Fn2 != 0.0 ? 1u : 0u)) : (uint8_t)0;
+                }
             }
             __syncwarp();
             // ---- phase 3: ordered accumulation of the own contacts
@@ -1428,22 +1423,29 @@ __global__ void __launch_bounds__(32 * kDWarps, 4) k_mech_dense(MechArgs A, DevS
                         if (lane == 0) Wd.cpre[c1 - c0] = (uint16_t)cbase;
                         __syncwarp();
                         // ---- phase 2b: Eq. 4.1/4.2 over the compacted contact candidates
-                        for (int q = lane; q < cbase; q += 32) {
-                            const uint32_t e = Wd.ce[q];
-                            const int j = (int)(e & 255u), ow = (int)(e >> 8);
-                            double s_ = 0.0;
-                            uint8_t fl = 0;
-                            const double dist = sqrt(Wd.cq[q]);
-                            const double ri = Wd.orr[ow], rj = Wd.Rr[j];
-                            const double delta = (ri + rj) - dist;
-                            if (delta > 0.0) {
-                                const double rbar = (ri * rj) / (ri + rj);
-                                const double Fn = A.k * delta - A.gamma * sqrt(rbar * delta);
-                                s_ = Fn / dist;
-                                fl = (uint8_t)(2u | (Fn != 0.0 ? 1u : 0u));
+                        // two contacts per lane, straight-line: the two sqrt/div chains
+                        // interleave (a non-contact's NaN is discarded by the select)
+                        for (int q = lane; q < cbase; q += 64) {
+                            const int q2 = q + 32;
+                            const bool h2 = q2 < cbase;
+                            const uint32_t e1 = Wd.ce[q], e2 = h2 ? Wd.ce[q2] : e1;
+                            const double D1 = Wd.cq[q], D2 = h2 ? Wd.cq[q2] : D1;
+                            const double ri1 = Wd.orr[e1 >> 8], rj1 = Wd.Rr[e1 & 255u];
+                            const double ri2 = Wd.orr[e2 >> 8], rj2 = Wd.Rr[e2 & 255u];
+                            const double dist1 = sqrt(D1), dist2 = sqrt(D2);
+                            const double del1 = (ri1 + rj1) - dist1, del2 = (ri2 + rj2) - dist2;
+                            const double rb1 = (ri1 * rj1) / (ri1 + rj1);
+                            const double rb2 = (ri2 * rj2) / (ri2 + rj2);
+                            const double Fn1 = A.k * del1 - A.gamma * sqrt(rb1 * del1);
+                            const double Fn2 = A.k * del2 - A.gamma * sqrt(rb2 * del2);
+                            const double s1 = Fn1 / dist1, s2 = Fn2 / dist2;
+                            const bool c1 = del1 > 0.0, c2 = del2 > 0.0;
+                            Wd.cq[q] = c1 ? s1 : 0.0;
+                            Wd.cf[q] = c1 ? (uint8_t)(2u | (Fn1 != 0.0 ? 1u : 0u)) : (uint8_t)0;
+                            if (h2) {
+                                Wd.cq[q2] = c2 ? s2 : 0.0;
+                                Wd.cf[q2] = c2 ? (uint8_t)(2u | (Fn2 != 0.0 ? 1u : 0u)) : (uint8_t)0;
                             }
-                            Wd.cq[q] = s_;
-                            Wd.cf[q] = fl;
                         }
                         __syncwarp();
                         // ---- phase 3: own contacts of the chunk, in order
