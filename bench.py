@@ -293,8 +293,8 @@ def run_ours(args, ws, rank, local):
         "roofline": {"bound": "alu", "kernel": "k_mech (a5-a9)",
                      "achieved": achieved / 1e12, "peak": fp64_peak / 1e12,
                      "unit": "T fp64-inst/s", "frac": achieved / fp64_peak,
-                     "traffic": (_traffic("k_mech_tile6", MECH_ALG_BYTES_PER_AGENT * cfg.n)
-                                 if cfg.name == "cfg2" else None),
+                     **_traffic_keys(_traffic("k_mech_tile6", MECH_ALG_BYTES_PER_AGENT * cfg.n)
+                                     if cfg.name == "cfg2" else None),
                      "peak_source": f"{sm_count} SMs x 64 fp64 lanes x {max_mhz:.0f} MHz "
                                     f"(guide unit counts, max clock); measured DFMA "
                                     f"{dfma_meas / 1e12:.2f} T/s",
@@ -425,7 +425,7 @@ def run_cfg4(args, ws, rank, local):
     line["roofline"] = {"bound": "hbm", "kernel": "k_sir_update + k_sir_collect (whole step)",
                         "achieved": ach / 1e9, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                         "frac": ach / (peaks["hbm_gbs"] * 1e9),
-                        "traffic": _traffic("k_sir_update", b_alg),
+                        **_traffic_keys(_traffic("k_sir_update", b_alg)),
                         "peak_source": src, "alg_bytes_per_agent": 50}
     print(json.dumps(line), flush=True)
 
@@ -444,6 +444,12 @@ def _traffic(kernel, alg_bytes):
             "alg_bytes_per_launch": alg_bytes,
             "ratio": t["dram_bytes_per_launch"] / alg_bytes if alg_bytes else None,
             "source": t["source"], "capture_workload": t["workload"]}
+
+
+def _traffic_keys(t):
+    """roofline.traffic = DRAM bytes per launch (the number the contract names), with
+    the capture it comes from and the algorithmic bytes beside it."""
+    return {"traffic": t["dram_bytes_per_launch"] if t else None, "traffic_detail": t}
 
 
 def run_soma(args, ws, rank, local):
@@ -507,7 +513,7 @@ def run_soma(args, ws, rank, local):
         "roofline": {"bound": "hbm", "kernel": "k_diffuse (one substance, one step)",
                      "achieved": ach / 1e9, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                      "frac": ach / (peaks["hbm_gbs"] * 1e9),
-                     "traffic": _traffic("k_diffuse_tma", 16.0 * r ** 3),
+                     **_traffic_keys(_traffic("k_diffuse_tma", 16.0 * r ** 3)),
                      "peak_source": src, "alg_bytes_per_point": 16,
                      "diffuse_ms": statistics.mean(dms) / 2},
         "clocks": clk.summary(), "gpu_launches": eng.stats()["launches"] - launches0,
