@@ -1,6 +1,6 @@
 #!/bin/bash
 # One GPU iteration: parity tests, a short bench, and an ncu capture of the tile kernel.
-# usage (under gpurun): bash tools_gpu_cycle.sh TAG [extra bench args]
+# usage (under gpurun): bash tools/gpu_cycle.sh TAG [extra bench args]
 TAG=$1; shift
 timeout 900 python -m pytest tests -m gpu -x -q -p no:cacheprovider > gpurun_out/pytest_$TAG.log 2>&1; echo pytest=$?; tail -3 gpurun_out/pytest_$TAG.log
 python bench.py --steps 20 --warmup 3 --no-cpu-baseline --no-e2e "$@" > gpurun_out/bench_$TAG.log 2>&1; echo bench=$?

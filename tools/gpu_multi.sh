@@ -1,6 +1,6 @@
 #!/bin/bash
 # Parity tests, then a short bench per mechanics kernel, then ncu of the first one.
-# usage (under gpurun): bash tools_gpu_multi.sh TAG "k1 k2 ..." [pytest-args]
+# usage (under gpurun): bash tools/gpu_multi.sh TAG "k1 k2 ..." [pytest-args]
 TAG=$1; KS=$2; shift 2
 timeout 900 python -m pytest tests -m gpu -x -q -p no:cacheprovider "$@" > gpurun_out/pytest_$TAG.log 2>&1; echo pytest=$?; tail -3 gpurun_out/pytest_$TAG.log
 for k in $KS; do

@@ -1,5 +1,5 @@
 """Per-CUDA-source-line breakdown of an ncu report (needs -lineinfo):
-python tools_ncu_lines.py rep [file-substring] [min-pct]
+python tools/ncu_lines.py rep [file-substring] [min-pct]
 
 Prints, for each source line of the matching file with >= min-pct of the kernel's warp
 instructions or stall samples: warp instructions, avg active threads, stall share, text.

@@ -1,4 +1,4 @@
-"""Per-region SASS breakdown of an ncu report: python tools_ncu_regions.py rep [chunk]"""
+"""Per-region SASS breakdown of an ncu report: python tools/ncu_regions.py rep [chunk]"""
 import csv, subprocess, sys
 rep = sys.argv[1]; chunk = int(sys.argv[2]) if len(sys.argv) > 2 else 40
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"], capture_output=True, text=True).stdout

@@ -1,6 +1,6 @@
 """Summary of an ncu --set full report (one kernel launch): duration, DRAM bytes,
 occupancy, issue, fp64 pipe, shared-memory wavefronts and the top warp stalls.
-python tools_ncu_summary.py report.ncu-rep > summary.txt"""
+python tools/ncu_summary.py report.ncu-rep > summary.txt"""
 import csv
 import io
 import subprocess
