@@ -861,11 +861,11 @@ __device__ __forceinline__ void tile6_batch(const MechArgs &A, const Tile6SmemT<
         // ---- phase 2a: exact test, static flags, contact pre-test, compaction
         const double R2 = S.g.R2;
         int cbase = 0;
-        for (int p0 = 0; p0 < total; p0 += 32) {  // warp-uniform
-            const int p = p0 + lane;
+        // two survivors per lane per round (their loads overlap), compacted in order
+        auto p2a_test = [&](int p, uint32_t &e, double &D) -> bool {
             bool cc = false;
-            double D = 0.0;
-            uint32_t e = 0;
+            D = 0.0;
+            e = 0;
             if (p < total) {
                 e = Wp.pr[p];
                 const int m = (int)(e & 511u), mo = (int)((e >> 9) & 511u);
@@ -879,14 +879,28 @@ __device__ __forceinline__ void tile6_batch(const MechArgs &A, const Tile6SmemT<
                     cc = D > 0.0 && D < (s2 * s2) * (1.0 + 0x1p-30);
                 }
             }
-            const unsigned cb = __ballot_sync(0xffffffffu, cc);
-            const int cidx = cbase + __popc(cb & lt_mask);
-            if (p < total) Wp.cpre[p] = (uint16_t)cidx;
-            if (cc && cidx < kC6Cap) {
-                Wp.u.b.cq[cidx] = D;
-                Wp.u.b.ce[cidx] = e;
+            return cc;
+        };
+        for (int p0 = 0; p0 < total; p0 += 64) {  // warp-uniform
+            uint32_t e1, e2;
+            double D1, D2;
+            const bool cc1 = p2a_test(p0 + lane, e1, D1);
+            const bool cc2 = p2a_test(p0 + 32 + lane, e2, D2);
+            const unsigned cb1 = __ballot_sync(0xffffffffu, cc1);
+            const unsigned cb2 = __ballot_sync(0xffffffffu, cc2);
+            const int ci1 = cbase + __popc(cb1 & lt_mask);
+            const int ci2 = cbase + __popc(cb1) + __popc(cb2 & lt_mask);
+            if (p0 + lane < total) Wp.cpre[p0 + lane] = (uint16_t)ci1;
+            if (p0 + 32 + lane < total) Wp.cpre[p0 + 32 + lane] = (uint16_t)ci2;
+            if (cc1 && ci1 < kC6Cap) {
+                Wp.u.b.cq[ci1] = D1;
+                Wp.u.b.ce[ci1] = e1;
             }
-            cbase += __popc(cb);
+            if (cc2 && ci2 < kC6Cap) {
+                Wp.u.b.cq[ci2] = D2;
+                Wp.u.b.ce[ci2] = e2;
+            }
+            cbase += __popc(cb1) + __popc(cb2);
         }
         if (cbase > kC6Cap) {  // contact queue overflow: reference path for this batch
             __syncwarp();
