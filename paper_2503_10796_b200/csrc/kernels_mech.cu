@@ -820,7 +820,7 @@ __device__ __forceinline__ void tile6_batch(const MechArgs &A, const Tile6SmemT<
         uint32_t mo = cur & 0xFFFFu, eo = cur >> 16;
         int j = 32;  // next run (row nr + 1 <= 10 is never consumed)
         uint32_t nxt = rrow[j];
-#pragma unroll 2
+#pragma unroll 4
         for (int it = 0; it < cmax; ++it) {
             const float4 q = *reinterpret_cast<const float4 *>(pb + min(mo, mlast));
             const float ex = pi.x - q.x, ey = pi.y - q.y, ez = pi.z - q.z;
@@ -944,17 +944,16 @@ __device__ __forceinline__ void tile6_batch(const MechArgs &A, const Tile6SmemT<
                 int nnz = 0;
                 uint32_t my_cont = 0;
                 const int q0 = Wp.cpre[my_off], q1 = Wp.cpre[my_off + cnt];
+                // a non-contact carries s = 0: fma(0, d, F) == F exactly (F never is -0)
                 for (int q = q0; q < q1; ++q) {
                     const uint32_t fl = Wp.u.b.cf[q];
-                    if (fl & 2u) {
-                        const int m = (int)(Wp.u.b.ce[q] & 511u);
-                        const double s_ = Wp.u.b.cq[q];
-                        Fx = fma(s_, xi - S.X[m], Fx);
-                        Fy = fma(s_, yi - S.Y[m], Fy);
-                        Fz = fma(s_, zi - S.Z[m], Fz);
-                        nnz += (int)(fl & 1u);
-                        ++my_cont;
-                    }
+                    const int m = (int)(Wp.u.b.ce[q] & 511u);
+                    const double s_ = Wp.u.b.cq[q];
+                    Fx = fma(s_, xi - S.X[m], Fx);
+                    Fy = fma(s_, yi - S.Y[m], Fy);
+                    Fz = fma(s_, zi - S.Z[m], Fz);
+                    nnz += (int)(fl & 1u);
+                    my_cont += (fl >> 1) & 1u;
                 }
                 nnz = nnz < 2 ? nnz : 2;
                 if (!is_static) {
@@ -1466,16 +1465,15 @@ __global__ void __launch_bounds__(32 * kDWarps, 4) k_mech_dense(MechArgs A, DevS
                         const int lo = max(my_off, c0) - c0, hi = min(my_off + cnt, c1) - c0;
                         if (hi > lo) {
                             const int q0 = Wd.cpre[lo], q1 = Wd.cpre[hi];
+                            // a non-contact carries s = 0: fma(0, d, F) == F exactly
                             for (int q = q0; q < q1; ++q) {
                                 const uint32_t fl = Wd.cf[q];
-                                if (fl & 2u) {
-                                    const double s_ = Wd.cq[q];
-                                    Fx = fma(s_, Wd.cx[q], Fx);
-                                    Fy = fma(s_, Wd.cy[q], Fy);
-                                    Fz = fma(s_, Wd.cz[q], Fz);
-                                    nnz += (int)(fl & 1u);
-                                    ++my_cont;
-                                }
+                                const double s_ = Wd.cq[q];
+                                Fx = fma(s_, Wd.cx[q], Fx);
+                                Fy = fma(s_, Wd.cy[q], Fy);
+                                Fz = fma(s_, Wd.cz[q], Fz);
+                                nnz += (int)(fl & 1u);
+                                my_cont += (fl >> 1) & 1u;
                             }
                         }
                         __syncwarp();
