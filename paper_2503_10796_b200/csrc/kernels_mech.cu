@@ -613,8 +613,8 @@ struct Warp6 {
         } a;
         struct {
             double cq[kC6Cap];              // D, then s = F_N / dist
-            uint32_t ce[kC6Cap];            // the survivor entry of the queue slot
-            uint8_t cf[kC6Cap];             // bit1 contact, bit0 F_N != 0
+            uint32_t ce[kC6Cap];            // the survivor entry; after 2b bits 24-25 = flags
+                                            // (bit1 contact, bit0 F_N != 0)
         } b;
     } u;
     double ext[7];                          // fused extent: lo x,y,z, hi x,y,z, max d
@@ -929,11 +929,14 @@ __device__ __forceinline__ void tile6_batch(const MechArgs &A, const Tile6SmemT<
                 const double s1 = Fn1 / dist1, s2 = Fn2 / dist2;
                 const bool c1 = del1 > 0.0 && !((stat_mask >> ((e1 >> 18) & 31u)) & 1u);
                 const bool c2 = del2 > 0.0 && !((stat_mask >> ((e2 >> 18) & 31u)) & 1u);
+                // the flags (bit1 contact, bit0 F_N != 0) ride in bits 24-25 of the entry
+                const uint32_t f1 = c1 ? (2u | (Fn1 != 0.0 ? 1u : 0u)) : 0u;
+                const uint32_t f2 = c2 ? (2u | (Fn2 != 0.0 ? 1u : 0u)) : 0u;
                 Wp.u.b.cq[q] = c1 ? s1 : 0.0;
-                Wp.u.b.cf[q] = c1 ? (uint8_t)(2u | (Fn1 != 0.0 ? 1u : 0u)) : (uint8_t)0;
+                Wp.u.b.ce[q] = (e1 & 0x00FFFFFFu) | (f1 << 24);
                 if (h2) {
                     Wp.u.b.cq[q2] = c2 ? s2 : 0.0;
-                    Wp.u.b.cf[q2] = c2 ? (uint8_t)(2u | (Fn2 != 0.0 ? 1u : 0u)) : (uint8_t)0;
+                    Wp.u.b.ce[q2] = (e2 & 0x00FFFFFFu) | (f2 << 24);
                 }
             }
             __syncwarp();
@@ -946,8 +949,9 @@ __device__ __forceinline__ void tile6_batch(const MechArgs &A, const Tile6SmemT<
                 const int q0 = Wp.cpre[my_off], q1 = Wp.cpre[my_off + cnt];
                 // a non-contact carries s = 0: fma(0, d, F) == F exactly (F never is -0)
                 for (int q = q0; q < q1; ++q) {
-                    const uint32_t fl = Wp.u.b.cf[q];
-                    const int m = (int)(Wp.u.b.ce[q] & 511u);
+                    const uint32_t ev = Wp.u.b.ce[q];
+                    const uint32_t fl = ev >> 24;
+                    const int m = (int)(ev & 511u);
                     const double s_ = Wp.u.b.cq[q];
                     Fx = fma(s_, xi - S.X[m], Fx);
                     Fy = fma(s_, yi - S.Y[m], Fy);
