@@ -1242,7 +1242,9 @@ constexpr int kDB = 32;     // staged candidates per warp batch (one word)
 constexpr int kDQ = 192;    // survivors per processed chunk
 
 struct DenseWarp {
-    float4 P[kDB];                          // fp32 x, y, z relative to the box corner
+    float4 PXY[kDB / 2];                    // fp32 relative to the box corner, f32x2 layout:
+                                            // (x_2k, x_2k+1, y_2k, y_2k+1)
+    float2 PZ[kDB / 2];                     //               (z_2k, z_2k+1)
     double X[kDB], Y[kDB], Z[kDB], Rr[kDB];
     uint32_t F[kDB], G[kDB];                // flags, sorted index
     uint32_t bs[32], bp[32];                // neighbour boxes: first agent, stream offset
@@ -1366,7 +1368,12 @@ __global__ void __launch_bounds__(32 * kDWarps, 4) k_mech_dense(MechArgs A, DevS
                         Wd.Rr[q] = A.sd[gj] * 0.5;
                         Wd.F[q] = A.sflags[gj];
                         Wd.G[q] = gj;
-                        Wd.P[q] = make_float4((float)(x - C0), (float)(y - C1), (float)(z - C2), 0.f);
+                        {
+                            float *xy = reinterpret_cast<float *>(&Wd.PXY[q >> 1]);
+                            xy[q & 1] = (float)(x - C0);
+                            xy[2 + (q & 1)] = (float)(y - C1);
+                            reinterpret_cast<float *>(&Wd.PZ[q >> 1])[q & 1] = (float)(z - C2);
+                        }
                     }
                 }
                 __syncwarp();
@@ -1374,11 +1381,19 @@ __global__ void __launch_bounds__(32 * kDWarps, 4) k_mech_dense(MechArgs A, DevS
                     // ---- phase 1: broadcast fp32 prefilter -> survivor bitmask
                     uint32_t m = 0;
                     const int jn = min(32, nbt - 32 * u);
+                    // two candidates per packed f32x2 step (the same IEEE fp32 operations as
+                    // the scalar test, so the same bits); an odd tail's partner is masked
+                    {
+                        const unsigned long long pxx = pk2(px, px), pyy = pk2(py, py),
+                                                 pzz = pk2(pz, pz);
 #pragma unroll 4
-                    for (int j = 0; j < jn; ++j) {
-                        const float4 q = Wd.P[32 * u + j];
-                        const float ex = px - q.x, ey = py - q.y, ez = pz - q.z;
-                        if (fmaf(ez, ez, fmaf(ey, ey, ex * ex)) <= R2f) m |= 1u << j;
+                        for (int k = 0; k < (jn + 1) >> 1; ++k) {
+                            float d0, d1;
+                            dist2_pair(pxx, pyy, pzz, Wd.PXY[16 * u + k], Wd.PZ[16 * u + k], d0, d1);
+                            m |= (d0 <= R2f ? 1u : 0u) << (2 * k);
+                            m |= (d1 <= R2f ? 1u : 0u) << (2 * k + 1);
+                        }
+                        if (jn < 32) m &= (1u << jn) - 1u;
                     }
                     // ---- survivor queue, owner-major, candidate-ascending
                     const int cnt = __popc(m);
