@@ -855,8 +855,12 @@ __device__ __forceinline__ void tile6_batch(const MechArgs &A, const Tile6SmemT<
     }
     if (!done) {
         const uint32_t tag = ((uint32_t)mi << 9) | ((uint32_t)lane << 18);
-        for (int jj = 0; jj < cnt; ++jj)
-            Wp.pr[my_off + jj] = ((uint32_t)Wp.u.a.lst[jj][lane] >> (kPair ? 0 : 4)) | tag;
+        {  // warp-uniform trip count, predicated body
+            const int cmx = __reduce_max_sync(0xffffffffu, cnt);
+            for (int jj = 0; jj < cmx; ++jj)
+                if (jj < cnt)
+                    Wp.pr[my_off + jj] = ((uint32_t)Wp.u.a.lst[jj][lane] >> (kPair ? 0 : 4)) | tag;
+        }
         __syncwarp();
         // ---- phase 2a: exact test, static flags, contact pre-test, compaction
         const double R2 = S.g.R2;
@@ -1408,10 +1412,14 @@ __global__ void __launch_bounds__(32 * kDWarps, 4) k_mech_dense(MechArgs A, DevS
                     {
                         int o = my_off;
                         uint32_t mm = m;
-                        while (mm) {
-                            const int j = __ffs(mm) - 1;
+                        while (mm) {  // two survivors per iteration
+                            const int j1 = __ffs(mm) - 1;
                             mm &= mm - 1;
-                            Wd.Q[o++] = (uint16_t)((32 * u + j) | (lane << 8));
+                            const int j2 = __ffs(mm) - 1;  // -1 when none is left
+                            mm &= mm - 1;
+                            Wd.Q[o] = (uint16_t)((32 * u + j1) | (lane << 8));
+                            if (j2 >= 0) Wd.Q[o + 1] = (uint16_t)((32 * u + j2) | (lane << 8));
+                            o += 2;
                         }
                     }
                     __syncwarp();
