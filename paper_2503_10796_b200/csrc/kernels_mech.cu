@@ -952,6 +952,9 @@ __device__ __forceinline__ void tile6_batch(const MechArgs &A, const Tile6SmemT<
                 uint32_t my_cont = 0;
                 const int q0 = Wp.cpre[my_off], q1 = Wp.cpre[my_off + cnt];
                 // a non-contact carries s = 0: fma(0, d, F) == F exactly (F never is -0)
+#ifdef BDM_TILE_P3U
+#pragma unroll BDM_TILE_P3U
+#endif
                 for (int q = q0; q < q1; ++q) {
                     const uint32_t ev = Wp.u.b.ce[q];
                     const uint32_t fl = ev >> 24;
@@ -1493,6 +1496,7 @@ __global__ void __launch_bounds__(32 * kDWarps, 4) k_mech_dense(MechArgs A, DevS
                         if (hi > lo) {
                             const int q0 = Wd.cpre[lo], q1 = Wd.cpre[hi];
                             // a non-contact carries s = 0: fma(0, d, F) == F exactly
+#pragma unroll 2
                             for (int q = q0; q < q1; ++q) {
                                 const uint32_t fl = Wd.cf[q];
                                 const double s_ = Wd.cq[q];
