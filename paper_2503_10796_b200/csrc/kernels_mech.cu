@@ -952,9 +952,7 @@ __device__ __forceinline__ void tile6_batch(const MechArgs &A, const Tile6SmemT<
                 uint32_t my_cont = 0;
                 const int q0 = Wp.cpre[my_off], q1 = Wp.cpre[my_off + cnt];
                 // a non-contact carries s = 0: fma(0, d, F) == F exactly (F never is -0)
-#ifdef BDM_TILE_P3U
-#pragma unroll BDM_TILE_P3U
-#endif
+#pragma unroll 2
                 for (int q = q0; q < q1; ++q) {
                     const uint32_t ev = Wp.u.b.ce[q];
                     const uint32_t fl = ev >> 24;
