@@ -750,20 +750,19 @@ __device__ __forceinline__ void tile6_batch(const MechArgs &A, const Tile6SmemT<
                 const int row = lbi - 43 + dzi * 36 + dyi * 6;  // box (lx-1, ly-1+dyi, lz-1+dzi)
                 if (kStats) ca += (int)(S.off[row + 3] - S.off[row]);
                 const float b2 = gz2[dzi] + gy2[dyi];
-                if (b2 <= R2f) {
+                {  // straight-line: the run is stored at nr and kept only if non-empty
                     const int xs = (b2 + gx2l <= R2f) ? 0 : 1;
                     const int xe = (b2 + gx2h <= R2f) ? 3 : 2;
                     const uint32_t rs = S.off[row + xs], re = S.off[row + xe];
-                    if (re > rs) {
-                        if constexpr (kPair) {  // indices; the walk takes two candidates per step
-                            Wp.u.a.run[nr][lane] = rs | (re << 16);
-                            walk += (int)((re - rs + 1) >> 1);
-                        } else {      // byte offsets into P (16 B per agent)
-                            Wp.u.a.run[nr][lane] = (rs << 4) | (re << 20);
-                            walk += (int)(re - rs);
-                        }
-                        ++nr;
+                    const bool keep = b2 <= R2f && re > rs;
+                    if constexpr (kPair) {
+                        Wp.u.a.run[nr][lane] = rs | (re << 16);
+                        walk += keep ? (int)((re - rs + 1) >> 1) : 0;
+                    } else {
+                        Wp.u.a.run[nr][lane] = (rs << 4) | (re << 20);
+                        walk += keep ? (int)(re - rs) : 0;
                     }
+                    nr += keep ? 1 : 0;
                 }
             }
         }
