@@ -874,12 +874,13 @@ __device__ __forceinline__ void tile6_batch(const MechArgs &A, const Tile6SmemT<
                 const int m = (int)(e & 511u), mo = (int)((e >> 9) & 511u);
                 const double ex = S.X[mo] - S.X[m], ey = S.Y[mo] - S.Y[m], ez = S.Z[mo] - S.Z[m];
                 D = fma(ez, ez, fma(ey, ey, ex * ex));
-                if (D <= R2 && m != mo) {
-                    e |= kNbrBit;
-                    if (kStats) Wp.pr[p] = e;
-                    if (any_cs && (S.F[m] & kChanged)) Wp.chg[(e >> 18) & 31u] = 1;
+                {  // survivors are almost all neighbours: no inner branch
+                    const bool nbr = D <= R2 && m != mo;
                     const double s2 = S.Rr[mo] + S.Rr[m];
-                    cc = D > 0.0 && D < (s2 * s2) * (1.0 + 0x1p-30);
+                    e |= nbr ? kNbrBit : 0u;
+                    if (kStats && nbr) Wp.pr[p] = e;
+                    if (nbr && any_cs && (S.F[m] & kChanged)) Wp.chg[(e >> 18) & 31u] = 1;
+                    cc = nbr && D > 0.0 && D < (s2 * s2) * (1.0 + 0x1p-30);
                 }
             }
             return cc;
@@ -1435,17 +1436,16 @@ __global__ void __launch_bounds__(32 * kDWarps, 4) k_mech_dense(MechArgs A, DevS
                             if (p < c1) {
                                 e = Wd.Q[p];
                                 const int j = (int)(e & 255u), ow = (int)(e >> 8);
-                                if (Wd.G[j] != Wd.os[ow]) {
+                                {
                                     ex = Wd.ox[ow] - Wd.X[j];
                                     ey = Wd.oy[ow] - Wd.Y[j];
                                     ez = Wd.oz[ow] - Wd.Z[j];
                                     D = fma(ez, ez, fma(ey, ey, ex * ex));
-                                    if (D <= g.R2) {
-                                        if (kStats) atomicAdd(&Wd.nbrc[ow], 1u);
-                                        if (Wd.F[j] & kChanged) Wd.chg[ow] = 1;
-                                        const double s2 = Wd.orr[ow] + Wd.Rr[j];
-                                        cc = D > 0.0 && D < (s2 * s2) * (1.0 + 0x1p-30);
-                                    }
+                                    const bool nbr = Wd.G[j] != Wd.os[ow] && D <= g.R2;
+                                    const double s2 = Wd.orr[ow] + Wd.Rr[j];
+                                    if (kStats && nbr) atomicAdd(&Wd.nbrc[ow], 1u);
+                                    if (nbr && (Wd.F[j] & kChanged)) Wd.chg[ow] = 1;
+                                    cc = nbr && D > 0.0 && D < (s2 * s2) * (1.0 + 0x1p-30);
                                 }
                             }
                             const unsigned cb = __ballot_sync(0xffffffffu, cc);
