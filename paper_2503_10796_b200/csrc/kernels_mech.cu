@@ -38,6 +38,7 @@ struct MechArgs {
     const double *__restrict__ svol;  // nullable: volume travels with the agents
     double *__restrict__ ovol;
     uint32_t *__restrict__ dense_list;   // nullable: dense tiles go to k_mech_dense
+    uint32_t *__restrict__ dense_perm;   // dense kernel scratch: octant order of a box's agents
     double k, gamma, dt, max_disp, tau;
     int detect_static, boundary, fuse;
     double lo0, lo1, lo2, hi0, hi1, hi2;
@@ -1320,13 +1321,58 @@ __global__ void __launch_bounds__(32 * kDWarps, 4) k_mech_dense(MechArgs A, DevS
         }
         const double C0 = g.o0 + (double)(bx + g.b0) * g.L, C1 = g.o1 + (double)(by + g.b1) * g.L,
                      C2 = g.o2 + (double)(bz + g.b2) * g.L;
+        // a box with more agents than lanes is grouped in octant order (a counting sort
+        // into dense_perm[b0 ..)): the lanes of a group then sit close together, and a
+        // word's contacts spread more evenly over them (phase 3 is per-lane sequential)
+        const bool oct = nb > 32;
+        if (oct) {
+            const double h = 0.5 * g.L, M0 = C0 + h, M1 = C1 + h, M2 = C2 + h;
+            unsigned cntv = 0;  // lanes 0..7: agents of octant `lane`
+            for (int a = 0; a < nb; a += 32) {
+                const int ai = a + lane;
+                int oc = -1;
+                if (ai < nb) {
+                    const uint32_t sa = b0 + (uint32_t)ai;
+                    oc = (A.sx[sa] >= M0 ? 1 : 0) | (A.sy[sa] >= M1 ? 2 : 0) | (A.sz[sa] >= M2 ? 4 : 0);
+                }
+#pragma unroll
+                for (int o = 0; o < 8; ++o) {
+                    const unsigned bo = __ballot_sync(0xffffffffu, oc == o);
+                    if (lane == o) cntv += (unsigned)__popc(bo);
+                }
+            }
+            int inc = (int)cntv;
+#pragma unroll
+            for (int o = 1; o < 8; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, inc, o);
+                if (lane >= o) inc += y;
+            }
+            int run = inc - (int)cntv;  // lanes 0..7: next slot of octant `lane`
+            for (int a = 0; a < nb; a += 32) {
+                const int ai = a + lane;
+                int oc = -1;
+                if (ai < nb) {
+                    const uint32_t sa = b0 + (uint32_t)ai;
+                    oc = (A.sx[sa] >= M0 ? 1 : 0) | (A.sy[sa] >= M1 ? 2 : 0) | (A.sz[sa] >= M2 ? 4 : 0);
+                }
+#pragma unroll
+                for (int o = 0; o < 8; ++o) {
+                    const unsigned bo = __ballot_sync(0xffffffffu, oc == o);
+                    const int r0 = __shfl_sync(0xffffffffu, run, o);
+                    if (oc == o) A.dense_perm[b0 + (uint32_t)(r0 + __popc(bo & lt_mask))] = b0 + (uint32_t)ai;
+                    if (lane == o) run += __popc(bo);
+                }
+            }
+            __syncwarp();
+        }
         const int ngrp = (nb + 31) >> 5;
         for (int gq = 0; gq < ngrp; ++gq) {
             const int a0 = (gq * nb) / ngrp, a1 = ((gq + 1) * nb) / ngrp;
-            const uint32_t s = b0 + (uint32_t)(a0 + lane);
+            uint32_t s = b0 + (uint32_t)(a0 + lane);
             uint32_t fi = 0;
             bool active = false;
             if (lane < a1 - a0) {
+                if (oct) s = A.dense_perm[s];
                 fi = A.sflags[s];
                 active = !(fi & kGhost);
             }
@@ -1568,6 +1614,12 @@ bdm_status launch_mech(Ctx *c, bdm_agents *a, const bdm_params *p, cudaStream_t 
         BDM_CUDA_TRY(cudaMemsetAsync(c->sc->stats, 0, sizeof(c->sc->stats), st));
     const bool dense = c->dense && (c->mech_kernel == 0 || c->mech_kernel == 3);
     A.dense_list = dense ? c->dense_list : nullptr;
+    A.dense_perm = nullptr;
+    if (dense) {
+        const bdm_status s0 = need_agent_buf(c, &c->cls);  // dense-kernel octant order
+        if (s0 != BDM_OK) return s0;
+        A.dense_perm = c->cls;
+    }
     BDM_CUDA_TRY(cudaMemsetAsync(&c->sc->n_dense, 0, 3 * sizeof(unsigned int), st));
     if (c->mech_kernel == 0) {
         const bdm_status s = p->collect_stats ? launch_tile6<true, 5, false>(c, A, st)
