@@ -1395,36 +1395,71 @@ __global__ void __launch_bounds__(32 * kDWarps, 4) k_mech_dense(MechArgs A, DevS
             Wd.nbrc[lane] = 0;
             const int nnz_in = (int)((fi >> BDM_FLAG_NNZ_SHIFT) & 3u);
             const bool cand_static = active && A.detect_static && !(fi & kChanged) && nnz_in <= 1;
+            // bounding box of the group's fp32 points: a candidate farther than R from it
+            // cannot pass any lane's test (each operation of the box distance is bounded by
+            // the same operation of a lane's distance, and rounding is monotone)
+            float blx = INFINITY, bly = INFINITY, blz = INFINITY;
+            float bhx = -INFINITY, bhy = -INFINITY, bhz = -INFINITY;
+            if (active) {
+                blx = bhx = px;
+                bly = bhy = py;
+                blz = bhz = pz;
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                blx = fminf(blx, __shfl_xor_sync(0xffffffffu, blx, o));
+                bly = fminf(bly, __shfl_xor_sync(0xffffffffu, bly, o));
+                blz = fminf(blz, __shfl_xor_sync(0xffffffffu, blz, o));
+                bhx = fmaxf(bhx, __shfl_xor_sync(0xffffffffu, bhx, o));
+                bhy = fmaxf(bhy, __shfl_xor_sync(0xffffffffu, bhy, o));
+                bhz = fmaxf(bhz, __shfl_xor_sync(0xffffffffu, bhz, o));
+            }
             double Fx = 0.0, Fy = 0.0, Fz = 0.0;
             int nnz = 0;
             uint32_t my_cont = 0;
             for (uint32_t base = 0; base < T; base += kDB) {
-                const int nbt = (int)min((uint32_t)kDB, T - base);
+                int nbt = (int)min((uint32_t)kDB, T - base);
                 __syncwarp();  // the previous batch is fully consumed
                 // ---- stage the batch (coalesced: a box's agents are contiguous)
 #pragma unroll
                 for (int u = 0; u < kDB / 32; ++u) {
-                    const int q = 32 * u + lane;
-                    if (q < nbt) {
-                        const uint32_t pos = base + (uint32_t)q;
+                    const int qs = 32 * u + lane;
+                    bool keep = qs < nbt;
+                    uint32_t gj = 0;
+                    double x = 0.0, y = 0.0, z = 0.0;
+                    float xr = 0.f, yr = 0.f, zr = 0.f;
+                    if (keep) {
+                        const uint32_t pos = base + (uint32_t)qs;
                         int r = 0;
 #pragma unroll
                         for (int st = 16; st >= 1; st >>= 1)
                             if (Wd.bp[r + st] <= pos) r += st;
-                        const uint32_t gj = Wd.bs[r] + (pos - Wd.bp[r]);
-                        const double x = A.sx[gj], y = A.sy[gj], z = A.sz[gj];
+                        gj = Wd.bs[r] + (pos - Wd.bp[r]);
+                        x = A.sx[gj];
+                        y = A.sy[gj];
+                        z = A.sz[gj];
+                        xr = (float)(x - C0);
+                        yr = (float)(y - C1);
+                        zr = (float)(z - C2);
+                        const float ux = fmaxf(fmaxf(blx - xr, xr - bhx), 0.f);
+                        const float uy = fmaxf(fmaxf(bly - yr, yr - bhy), 0.f);
+                        const float uz = fmaxf(fmaxf(blz - zr, zr - bhz), 0.f);
+                        keep = fmaf(uz, uz, fmaf(uy, uy, ux * ux)) <= R2f;
+                    }
+                    const unsigned kb = __ballot_sync(0xffffffffu, keep);
+                    const int q = __popc(kb & lt_mask);   // kept candidates, stream order
+                    nbt = __popc(kb);                     // kDB == 32: one staging round
+                    if (keep) {
                         Wd.X[q] = x;
                         Wd.Y[q] = y;
                         Wd.Z[q] = z;
                         Wd.Rr[q] = A.sd[gj] * 0.5;
                         Wd.F[q] = A.sflags[gj];
                         Wd.G[q] = gj;
-                        {
-                            float *xy = reinterpret_cast<float *>(&Wd.PXY[q >> 1]);
-                            xy[q & 1] = (float)(x - C0);
-                            xy[2 + (q & 1)] = (float)(y - C1);
-                            reinterpret_cast<float *>(&Wd.PZ[q >> 1])[q & 1] = (float)(z - C2);
-                        }
+                        float *xy = reinterpret_cast<float *>(&Wd.PXY[q >> 1]);
+                        xy[q & 1] = xr;
+                        xy[2 + (q & 1)] = yr;
+                        reinterpret_cast<float *>(&Wd.PZ[q >> 1])[q & 1] = zr;
                     }
                 }
                 __syncwarp();
