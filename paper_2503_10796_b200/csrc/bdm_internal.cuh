@@ -100,6 +100,8 @@ struct Ctx {
     // grid
     uint32_t *box_start = nullptr;  // slot_cap + 1
     uint32_t *dense_list = nullptr; // slot_cap / 64 + 1 tile ids (dense regions)
+    uint32_t *dense_scr = nullptr;  // dense kernel: per-warp octant-order scratch
+    int64_t dense_scr_cap = 0;
     uint32_t *onco_id = nullptr;    // row f2: divider flags by id, then their ranks
     int64_t onco_id_cap = 0;
     long long *onco_out = nullptr;  // row f2: new n, new id_next

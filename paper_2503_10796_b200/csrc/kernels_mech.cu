@@ -38,7 +38,7 @@ struct MechArgs {
     const double *__restrict__ svol;  // nullable: volume travels with the agents
     double *__restrict__ ovol;
     uint32_t *__restrict__ dense_list;   // nullable: dense tiles go to k_mech_dense
-    uint32_t *__restrict__ dense_perm;   // dense kernel scratch: octant order of a box's agents
+    uint32_t *__restrict__ dense_perm;   // dense kernel: kDScr entries of scratch per warp
     double k, gamma, dt, max_disp, tau;
     int detect_static, boundary, fuse;
     double lo0, lo1, lo2, hi0, hi1, hi2;
@@ -1244,6 +1244,7 @@ static bdm_status launch_tile(Ctx *c, const MechArgs &A, cudaStream_t st) {
 // The static decision needs every neighbour's flags, so forces of a candidate static
 // agent are computed and dropped when it turns out static (a5 result unchanged).
 constexpr int kDWarps = 4;
+constexpr int kDScr = 4096;  // per-warp octant-order scratch (boxes above it stay unsorted)
 constexpr int kDB = 32;     // staged candidates per warp batch (one word)
 constexpr int kDQ = 192;    // survivors per processed chunk
 
@@ -1322,9 +1323,10 @@ __global__ void __launch_bounds__(32 * kDWarps, 4) k_mech_dense(MechArgs A, DevS
         const double C0 = g.o0 + (double)(bx + g.b0) * g.L, C1 = g.o1 + (double)(by + g.b1) * g.L,
                      C2 = g.o2 + (double)(bz + g.b2) * g.L;
         // a box with more agents than lanes is grouped in octant order (a counting sort
-        // into dense_perm[b0 ..)): the lanes of a group then sit close together, and a
+        // into the warp's scratch): the lanes of a group then sit close together, and a
         // word's contacts spread more evenly over them (phase 3 is per-lane sequential)
-        const bool oct = nb > 32;
+        uint32_t *const scr = A.dense_perm + ((size_t)blockIdx.x * kDWarps + w) * kDScr;
+        const bool oct = nb > 32 && nb <= kDScr;
         if (oct) {
             const double h = 0.5 * g.L, M0 = C0 + h, M1 = C1 + h, M2 = C2 + h;
             unsigned cntv = 0;  // lanes 0..7: agents of octant `lane`
@@ -1359,7 +1361,7 @@ __global__ void __launch_bounds__(32 * kDWarps, 4) k_mech_dense(MechArgs A, DevS
                 for (int o = 0; o < 8; ++o) {
                     const unsigned bo = __ballot_sync(0xffffffffu, oc == o);
                     const int r0 = __shfl_sync(0xffffffffu, run, o);
-                    if (oc == o) A.dense_perm[b0 + (uint32_t)(r0 + __popc(bo & lt_mask))] = b0 + (uint32_t)ai;
+                    if (oc == o) scr[r0 + __popc(bo & lt_mask)] = b0 + (uint32_t)ai;
                     if (lane == o) run += __popc(bo);
                 }
             }
@@ -1372,7 +1374,7 @@ __global__ void __launch_bounds__(32 * kDWarps, 4) k_mech_dense(MechArgs A, DevS
             uint32_t fi = 0;
             bool active = false;
             if (lane < a1 - a0) {
-                if (oct) s = A.dense_perm[s];
+                if (oct) s = scr[a0 + lane];
                 fi = A.sflags[s];
                 active = !(fi & kGhost);
             }
@@ -1622,7 +1624,18 @@ static bdm_status launch_dense(Ctx *c, const MechArgs &A, cudaStream_t st) {
                                                                    32 * kDWarps, smem));
         per_sm = v < 1 ? 1 : v;
     }
-    k_mech_dense<kStats><<<(unsigned)(c->sm_count * per_sm), 32 * kDWarps, smem, st>>>(A, c->sc);
+    const int64_t nblk = (int64_t)c->sm_count * per_sm;
+    const int64_t need = nblk * kDWarps * kDScr;  // per-warp scratch (32 MB on a B200)
+    if (c->dense_scr_cap < need) {
+        if (c->dense_scr) cudaFree(c->dense_scr);
+        c->dense_scr = nullptr;
+        c->dense_scr_cap = 0;
+        BDM_CUDA_TRY(cudaMalloc(&c->dense_scr, (size_t)need * sizeof(uint32_t)));
+        c->dense_scr_cap = need;
+    }
+    MechArgs B = A;
+    B.dense_perm = c->dense_scr;
+    k_mech_dense<kStats><<<(unsigned)nblk, 32 * kDWarps, smem, st>>>(B, c->sc);
     return BDM_OK;
 }
 
@@ -1650,11 +1663,6 @@ bdm_status launch_mech(Ctx *c, bdm_agents *a, const bdm_params *p, cudaStream_t 
     const bool dense = c->dense && (c->mech_kernel == 0 || c->mech_kernel == 3);
     A.dense_list = dense ? c->dense_list : nullptr;
     A.dense_perm = nullptr;
-    if (dense) {
-        const bdm_status s0 = need_agent_buf(c, &c->cls);  // dense-kernel octant order
-        if (s0 != BDM_OK) return s0;
-        A.dense_perm = c->cls;
-    }
     BDM_CUDA_TRY(cudaMemsetAsync(&c->sc->n_dense, 0, 3 * sizeof(unsigned int), st));
     if (c->mech_kernel == 0) {
         const bdm_status s = p->collect_stats ? launch_tile6<true, 5, false>(c, A, st)
