@@ -1,0 +1,99 @@
+"""Randomized parity (hypothesis, derandomized): small populations drawn over the
+corners of the input space -- box-aligned coordinates, coincident and touching agents,
+tiny and mixed diameters, clustered and sparse layouts, static detection, thresholds,
+caps and the closed boundary -- stepped through the C ABI by the tile and the reference
+kernels and by the oracle; the state must agree bit for bit after two steps."""
+import numpy as np
+import pytest
+
+hyp = pytest.importorskip("hypothesis")
+from hypothesis import HealthCheck, given, settings, strategies as st  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+FIELDS = ("x", "y", "z", "d", "id", "flags")
+
+
+@pytest.fixture(scope="module")
+def engines():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_2503_10796_b200 import Engine
+    es = {}
+    for k in (0, 1):
+        e = Engine(0, 1 << 13)
+        e.set_option("mech_kernel", k)
+        es[k] = e
+    yield es
+    for e in es.values():
+        e.close()
+
+
+@st.composite
+def populations(draw):
+    n = draw(st.integers(1, 1500))
+    seed = draw(st.integers(0, 2**31 - 1))
+    rng = np.random.default_rng(seed)
+    layout = draw(st.sampled_from(["uniform", "lattice", "cluster", "pairs"]))
+    dmode = draw(st.sampled_from(["fixed", "mixed", "tiny", "wide"]))
+    if dmode == "fixed":
+        d = np.full(n, 10.0)
+    elif dmode == "mixed":
+        d = rng.uniform(8.0, 12.0, n)
+    elif dmode == "tiny":
+        d = rng.uniform(0.5, 2.0, n)
+    else:
+        d = rng.choice([2.0, 30.0], n)
+    R = d.max()
+    side = max(R, (n * np.mean(d) ** 3 / draw(st.floats(0.05, 1.2))) ** (1 / 3))
+    if layout == "uniform":
+        p = rng.uniform(0.0, side, (n, 3))
+    elif layout == "lattice":  # coordinates on multiples of the box edge (boundary cases)
+        L = R * (1.0 + 2.0 ** -20)
+        k = max(int(side / L), 1)
+        p = rng.integers(0, k + 1, (n, 3)) * L + rng.choice([0.0, 1e-12, -1e-12], (n, 3))
+    elif layout == "cluster":
+        p = rng.normal(0.0, side / 6.0, (n, 3))
+    else:  # pairs at exact contact distance and coincident centres
+        base = rng.uniform(0.0, side, (n, 3))
+        p = base.copy()
+        p[1::2] = base[0::2][: len(p[1::2])]
+        p[1::4, 0] += d[1::4]
+    s = {"x": np.ascontiguousarray(p[:, 0]), "y": np.ascontiguousarray(p[:, 1]),
+         "z": np.ascontiguousarray(p[:, 2]), "d": d.astype(np.float64),
+         "id": rng.permutation(4 * n)[:n].astype(np.uint32),
+         "flags": rng.choice(np.array([0, 4, 1 << 4, 2 << 4, 5], np.uint32), n)}
+    prm = {"k": draw(st.sampled_from([2.0, 0.5])), "gamma": draw(st.sampled_from([1.0, 0.0])),
+           "dt": draw(st.sampled_from([0.01, 1.0])), "max_disp": draw(st.sampled_from([3.0, 0.1])),
+           "tau": draw(st.sampled_from([0.0, 1e-3, 0.5])),
+           "static": draw(st.booleans()), "boundary": draw(st.sampled_from([0, 1]))}
+    return s, prm
+
+
+@settings(max_examples=150, deadline=None, derandomize=True,
+          suppress_health_check=[HealthCheck.too_slow, HealthCheck.data_too_large,
+                                 HealthCheck.function_scoped_fixture])
+@given(case=populations())
+def test_random_populations_bit_exact(engines, orc, case):
+    from paper_2503_10796_b200 import Agents, Params
+    s, q = case
+    lo = tuple(float(min(s[c].min(), 0.0)) for c in ("x", "y", "z"))
+    hi = tuple(float(max(s[c].max(), 1.0)) for c in ("x", "y", "z"))
+    gp = Params(k=q["k"], gamma=q["gamma"], dt=q["dt"], max_displacement=q["max_disp"],
+                force_threshold=q["tau"], detect_static=q["static"], boundary=q["boundary"],
+                lo=lo, hi=hi)
+    op = orc.mech_params(k=q["k"], gamma=q["gamma"], dt=q["dt"], max_disp=q["max_disp"],
+                         force_threshold=q["tau"], detect_static=q["static"],
+                         boundary=q["boundary"], lo=lo, hi=hi)
+    o = s
+    for _ in range(2):
+        o, _ = orc.step_full(o, op)
+    for k, e in engines.items():
+        a = Agents.from_numpy(s)
+        for _ in range(2):
+            e.step(a, gp)
+        g = a.numpy()
+        for f in FIELDS:
+            assert np.array_equal(np.asarray(g[f]).view(np.uint8),
+                                  np.asarray(o[f]).view(np.uint8)), (k, f)
