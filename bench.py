@@ -441,6 +441,7 @@ def _traffic(kernel, alg_bytes):
     except (OSError, KeyError, ValueError):
         return None
     return {"dram_bytes_per_launch": t["dram_bytes_per_launch"],
+            **{k: t[k] for k in ("issue_active_pct", "fp64_pipe_active_pct") if k in t},
             "alg_bytes_per_launch": alg_bytes,
             "ratio": t["dram_bytes_per_launch"] / alg_bytes if alg_bytes else None,
             "source": t["source"], "capture_workload": t["workload"]}
