@@ -196,6 +196,7 @@ def run_ours(args, ws, rank, local):
     eng.set_option("mech_kernel", args.mech_kernel)
     eng.set_option("fuse_reduce", 1)   # a1 of the next step fused into the mechanics epilogue
     eng.set_option("tile_order", args.tile_order)
+    eng.set_option("tile_depth", args.tile_depth)
     a = Agents.empty(cfg.n)
     stream = torch.cuda.Stream()
     with torch.cuda.stream(stream):
@@ -865,6 +866,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--mech-kernel", type=int, default=0, help="0 tile kernel, 1 reference")
+    ap.add_argument("--tile-depth", type=int, default=0,
+                    help="tile work unit: 0 auto (by agents per box), 1 or 2 tiles deep")
     ap.add_argument("--tile-order", type=int, default=0,
                     help="row f1: 0 row-major tiles, 1 blocked Hilbert")
     ap.add_argument("--sort-every", type=int, default=1,

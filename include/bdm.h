@@ -361,6 +361,10 @@ bdm_status bdm_neighbor_pairs(bdm_handle h, const bdm_agents *a, double radius,
  *                  (warp per box, broadcast candidate stream); 0: reference formulation.
  *   "diffuse_tma"  1 (default) / 0: bdm_diffuse streams the grid planes with TMA box loads
  *                  (nx even); 0, or nx odd: the register/shared-memory stencil kernel.
+ *   "tile_depth"   0 (default) auto: two-tile work units when the first grid build of the
+ *                  context had at most one agent per box, else one; 1 or 2 force it.
+ *                  Two tiles stacked in z share one staged 6x6x10-box region, so sparse
+ *                  populations fill the 32-lane batches (cfg5: -18 % k_mech).
  *   "tile_order"   0 (default) row-major 4x4x4-box tiles; 1 blocked Hilbert: super-tiles
  *                  of 8^3 tiles row-major, the tiles inside one along a 3-D Hilbert
  *                  curve (the paper's Hilbert variant of agent

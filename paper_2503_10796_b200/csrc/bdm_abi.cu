@@ -213,6 +213,7 @@ bdm_status bdm_create(bdm_handle *out, int device, int64_t max_agents) {
     cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device);
     if (cudaMalloc(&c->sc, sizeof(DevScalars)) != cudaSuccess ||
         cudaMallocHost(&c->sc_host, sizeof(DevScalars)) != cudaSuccess ||
+        cudaMallocHost(&c->dims_hint, 4 * sizeof(int32_t)) != cudaSuccess ||
         cudaMalloc(&c->pair_count, sizeof(unsigned long long)) != cudaSuccess ||
         cudaMalloc(&c->n_new, sizeof(long long)) != cudaSuccess ||
         cudaMalloc(&c->pack_counts, 16 * sizeof(long long)) != cudaSuccess) {
@@ -221,6 +222,7 @@ bdm_status bdm_create(bdm_handle *out, int device, int64_t max_agents) {
         return fail(BDM_ECUDA, "allocation of the context scalars failed");
     }
     cudaMemset(c->sc, 0, sizeof(DevScalars));
+    c->dims_hint[0] = c->dims_hint[1] = c->dims_hint[2] = 0;
     bdm_status s = grow_agents(c, max_agents > 0 ? max_agents : 1);
     if (s != BDM_OK) {
         bdm_destroy((bdm_handle)c);
@@ -249,6 +251,7 @@ bdm_status bdm_destroy(bdm_handle h) {
     for (void *q : sbufs)
         if (q) cudaFree(q);
     if (c->sc_host) cudaFreeHost(c->sc_host);
+    if (c->dims_hint) cudaFreeHost(c->dims_hint);
     delete c;
     return BDM_OK;
 }
@@ -302,6 +305,8 @@ bdm_status bdm_grid_build(bdm_handle h, const bdm_agents *a, const bdm_agents *g
             return fail(BDM_ENOTFINITE, "a position or diameter is NaN/Inf");
         }
         // (+8 in blocked Hilbert order: T is padded to whole super-tiles)
+        c->density_hint = (double)ntot / ((double)c->sc_host->dims[0] * (double)c->sc_host->dims[1] *
+                                          (double)c->sc_host->dims[2]);
         const int64_t pad = c->tile_order ? 8 : 4;
         const int64_t t0 = c->sc_host->T[0] + pad, t1 = c->sc_host->T[1] + pad,
                       t2 = c->sc_host->T[2] + pad;
@@ -311,6 +316,14 @@ bdm_status bdm_grid_build(bdm_handle h, const bdm_agents *a, const bdm_agents *g
         if ((s = launch_grid_geometry(c, a, g, radius, st)) != BDM_OK) return s;
     }
     if ((s = launch_grid_sort(c, a, g, st)) != BDM_OK) return s;
+    // every 8th build the box counts travel to a pinned mirror in stream order; later
+    // mechanics launches read whatever has arrived as their auto tile-depth hint (no
+    // synchronization; the hint only picks the faster of two exact kernels)
+    if (c->tile_depth == 0 && (c->grid_builds & 7) == 1) {
+        BDM_CUDA_TRY(cudaMemcpyAsync(c->dims_hint, c->sc->dims, sizeof(c->sc->dims),
+                                     cudaMemcpyDeviceToHost, st));
+        c->hint_n = ntot;
+    }
     c->grid_valid = true;
     c->grid_x = a->x;
     c->grid_n = a->n;
@@ -670,6 +683,11 @@ bdm_status bdm_set_option(bdm_handle h, const char *name, int64_t value) {
         c->dense_list = nullptr;
         c->slot_cap = 0;
         c->grid_valid = false;
+        return BDM_OK;
+    }
+    if (strcmp(name, "tile_depth") == 0) {
+        if (value < 0 || value > 2) return fail(BDM_EINVAL, "tile_depth must be 0, 1 or 2");
+        c->tile_depth = (int)value;
         return BDM_OK;
     }
     if (strcmp(name, "sort_every") == 0) {

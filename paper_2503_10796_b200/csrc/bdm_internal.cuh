@@ -78,6 +78,11 @@ struct AuraWs {
     long long *res = nullptr;
 };
 
+// Agents per box at or below which two-tile units (tile_depth 2) are used in auto mode: a
+// unit's region then holds 360 boxes x 1.0 = 360 agents on average, 3 sd under the
+// 416-agent staging limit.
+constexpr double kSparseDensity = 1.0;
+
 // Kernel attributes and occupancy are set once per device (arrays indexed by device).
 constexpr int kMaxDevices = 64;
 
@@ -126,6 +131,10 @@ struct Ctx {
     int prefilter = 1;     // option "prefilter": fp32 conservative candidate test in the tile kernel
     int fuse_reduce = 0;   // option "fuse_reduce": next step's a1 extent from the mech epilogue
     int dense = 1;         // option "dense": dense regions go to the dense-box kernel
+    int tile_depth = 0;    // option "tile_depth": 0 auto (by agents per box), 1, 2 (two-tile units)
+    double density_hint = 0.0;  // agents per box of the first grid build (auto depth)
+    int32_t *dims_hint = nullptr;  // pinned: box counts of a recent grid build (auto depth)
+    int64_t hint_n = 0;
     int diffuse_tma = 1;   // option "diffuse_tma": TMA-pipelined stencil when nx is even
     int tile_order = 0;    // option "tile_order" (row f1): 0 row-major, 1 blocked Hilbert
     int64_t sort_every = 1;  // option "sort_every" (row f1): reorder the caller's SoA every K-th build

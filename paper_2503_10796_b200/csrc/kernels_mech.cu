@@ -12,6 +12,7 @@
 // Compiled with -fmad=false: the only fused multiply-adds are the explicit fma()
 // calls at the two canonical sites (squared distance, force accumulation; R9).
 #include <cuda_runtime.h>
+#include <type_traits>
 #include <math.h>
 
 #include "bdm_internal.cuh"
@@ -634,21 +635,30 @@ struct Fp32Stage<true> {
     float4 XY[kM6Max + 2];
     float2 ZZ[kM6Max + 2];
 };
-template <bool kPair>
+// kTZ = 1: a work unit is one 4x4x4-box tile, staged with a one-box halo (6x6x6
+// boxes); kTZ = 2 (option "tile_depth" 2, sparse populations): two tiles stacked in z,
+// 6x6x10 boxes, so a unit holds twice the agents for the same staging budget.
+template <int kTZ>
+struct TileGeo {
+    static constexpr int kNB = 36 * (4 * kTZ + 2);   // region boxes
+    static constexpr int kSQ = (kNB + 31) / 32;      // scan items per lane
+    using MBox = typename std::conditional<(kNB > 255), uint16_t, uint8_t>::type;
+};
+template <bool kPair, int kTZ = 1>
 struct Tile6SmemT {
     GridView g;
     float R2f, Lf;
     int use_pf, edge_only;                  // edge_only: fused extent from boundary tiles only
     int next_tile[2];                       // dynamic tile scheduling (ping-pong)
     int lo_box[3], hi_box[3];               // boxes that can hold a new extremum (see below)
-    uint32_t start[216];
-    uint32_t off[220];
+    uint32_t start[TileGeo<kTZ>::kNB];
+    uint32_t off[TileGeo<kTZ>::kNB + 4];
     Fp32Stage<kPair> f;
     double X[kM6Max], Y[kM6Max], Z[kM6Max], Rr[kM6Max];
     uint32_t F[kM6Max];
     uint16_t kmi[kM6Max];                   // tile agent k -> staged index
-    uint16_t lbxyz[216];                    // region box -> x | y << 3 | z << 6 | inner << 9
-    uint8_t mbox[kM6Max];                   // staged index -> region box
+    uint16_t lbxyz[TileGeo<kTZ>::kNB];      // region box -> x | y << 3 | z << 6 | inner << 10
+    typename TileGeo<kTZ>::MBox mbox[kM6Max];  // staged index -> region box
     Warp6 W[kT6Warps];
 };
 using Tile6Smem = Tile6SmemT<false>;
@@ -709,14 +719,15 @@ __device__ __forceinline__ void merge_counts(const Counts &c, Warp6 &Wp, int sid
 }
 
 // One batch of <= 32 agents of the staged tile (lane = tile agent klo + lane).
-template <bool kStats, bool kPair>
-__device__ __forceinline__ void tile6_batch(const MechArgs &A, const Tile6SmemT<kPair> &S, Warp6 &Wp,
-                                            int lane, uint32_t g0, int klo, int na, int M,
-                                            int sides) {
+template <bool kStats, bool kPair, int kTZ>
+__device__ __forceinline__ void tile6_batch(const MechArgs &A, const Tile6SmemT<kPair, kTZ> &S,
+                                            Warp6 &Wp, int lane, uint32_t g0, int n0, uint32_t g1,
+                                            int klo, int na, int M, int sides) {
     const unsigned lt_mask = (1u << lane) - 1u;
     const float R2f = S.R2f, Lf = S.Lf;
     const int k = klo + lane;
-    const uint32_t gk = g0 + (uint32_t)k;
+    // own agent k: [0, n0) in the first tile of the unit, then the second (kTZ = 2)
+    const uint32_t gk = k < n0 ? g0 + (uint32_t)k : g1 + (uint32_t)(k - n0);
     int mi = M, nr = 0, walk = 0, ca = 0;
     uint32_t fi = 0;
     bool active = false, cand_static = false;
@@ -737,7 +748,7 @@ __device__ __forceinline__ void tile6_batch(const MechArgs &A, const Tile6SmemT<
                 pi = S.f.P[mi];
             }
             const uint32_t v = S.lbxyz[lbi];
-            const int lx = (int)(v & 7u), ly = (int)((v >> 3) & 7u), lz = (int)((v >> 6) & 7u);
+            const int lx = (int)(v & 7u), ly = (int)((v >> 3) & 7u), lz = (int)((v >> 6) & 15u);
             // squared gaps to the faces of the own box (fp32, conservative, see above)
             const float glx = pi.x - (float)lx * Lf, ghx = (float)(lx + 1) * Lf - pi.x;
             const float gly = pi.y - (float)ly * Lf, ghy = (float)(ly + 1) * Lf - pi.y;
@@ -985,12 +996,14 @@ __device__ __forceinline__ void tile6_batch(const MechArgs &A, const Tile6SmemT<
     merge_counts<kStats>(c, Wp, sides, lane);
 }
 
-template <bool kStats, int kMinBlocks, bool kPair>
+
+template <bool kStats, int kMinBlocks, bool kPair, int kTZ = 1>
 __global__ void __launch_bounds__(kT6Threads, kMinBlocks) k_mech_tile6(MechArgs A, DevScalars *__restrict__ sc,
                                                                       int allow_prefilter) {
     if (sc->overflow) return;
+    constexpr int kNB = TileGeo<kTZ>::kNB, kSQ = TileGeo<kTZ>::kSQ;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    Tile6SmemT<kPair> &S = *reinterpret_cast<Tile6SmemT<kPair> *>(smem_raw);
+    Tile6SmemT<kPair, kTZ> &S = *reinterpret_cast<Tile6SmemT<kPair, kTZ> *>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     if (tid == 0) {
         const GridView g = load_grid(sc);
@@ -1016,16 +1029,18 @@ __global__ void __launch_bounds__(kT6Threads, kMinBlocks) k_mech_tile6(MechArgs 
             if (blockIdx.x == 0) atomicMax(&sc->enc_dmax, enc_double(sc->dmax_prev));
         }
     }
-    for (int lb = tid; lb < 216; lb += kT6Threads) {
+    for (int lb = tid; lb < kNB; lb += kT6Threads) {
         const uint32_t lx = lb % 6, ly = (lb / 6) % 6, lz = lb / 36;
-        const uint32_t inner = lx >= 1 && lx <= 4 && ly >= 1 && ly <= 4 && lz >= 1 && lz <= 4;
-        S.lbxyz[lb] = (uint16_t)(lx | (ly << 3) | (lz << 6) | (inner << 9));
+        const uint32_t inner =
+            lx >= 1 && lx <= 4 && ly >= 1 && ly <= 4 && lz >= 1 && lz <= (uint32_t)(4 * kTZ);
+        S.lbxyz[lb] = (uint16_t)(lx | (ly << 3) | (lz << 6) | (inner << 10));
     }
     if (lane < 7) S.W[w].ext[lane] = lane < 3 ? INFINITY : -INFINITY;
     if (lane < 5) S.W[w].cnt[lane] = 0ull;
     __syncthreads();
     const int T0 = S.g.T0, T1 = S.g.T1;
-    const int ntiles = T0 * T1 * S.g.T2;  // < 2^26 (nslots < 2^32)
+    const int TU = (S.g.T2 + kTZ - 1) / kTZ;  // units along z
+    const int ntiles = T0 * T1 * TU;          // work units (< 2^26: nslots < 2^32)
     int tx, ty, tz;
 
     const uint16_t *const hilb = S.g.hilb, *const hilb_inv = S.g.hilb_inv;
@@ -1037,16 +1052,32 @@ __global__ void __launch_bounds__(kT6Threads, kMinBlocks) k_mech_tile6(MechArgs 
         __syncthreads();
         const int t = S.next_tile[it & 1];
         if (t >= ntiles) break;
-        tile_xyz((uint32_t)t, T0, T1, hilb_inv, tx, ty, tz);
-        const uint32_t g0 = A.box_start[(uint32_t)t * 64u];
-        const int nc = (int)(A.box_start[(uint32_t)t * 64u + 64u] - g0);
+        uint32_t ta = (uint32_t)t, tb = 0xFFFFFFFFu;  // the unit's tiles (slot numbers)
+        if constexpr (kTZ == 1) {
+            tile_xyz((uint32_t)t, T0, T1, hilb_inv, tx, ty, tz);
+        } else {
+            tx = t % T0;
+            ty = (t / T0) % T1;
+            tz = kTZ * (t / (T0 * T1));
+            ta = tile_rank(tx, ty, tz, T0, T1, hilb);
+            if (tz + 1 < S.g.T2) tb = tile_rank(tx, ty, tz + 1, T0, T1, hilb);
+        }
+        const uint32_t g0 = A.box_start[ta * 64u];
+        const int n0 = (int)(A.box_start[ta * 64u + 64u] - g0);
+        uint32_t g1 = 0;
+        int n1 = 0;
+        if (kTZ == 2 && tb != 0xFFFFFFFFu) {
+            g1 = A.box_start[tb * 64u];
+            n1 = (int)(A.box_start[tb * 64u + 64u] - g1);
+        }
+        const int nc = n0 + n1;
         if (nc == 0) continue;  // uniform across the CTA
         const int bx0 = 4 * tx - 1, by0 = 4 * ty - 1, bz0 = 4 * tz - 1;
-        // ---- box table of the 6^3 region (out-of-grid boxes are empty)
-        for (int lb = tid; lb < 216; lb += kT6Threads) {
+        // ---- box table of the region (out-of-grid boxes are empty)
+        for (int lb = tid; lb < kNB; lb += kT6Threads) {
             const uint32_t v = S.lbxyz[lb];
             const int gx = bx0 + (int)(v & 7u), gy = by0 + (int)((v >> 3) & 7u),
-                      gz = bz0 + (int)((v >> 6) & 7u);
+                      gz = bz0 + (int)((v >> 6) & 15u);
             uint32_t st = 0, cn = 0;
             if (gx >= 0 && gy >= 0 && gz >= 0 && gx < S.g.D0 && gy < S.g.D1 && gz < S.g.D2) {
                 const uint32_t key = box_key(gx, gy, gz, T0, T1, hilb);
@@ -1057,12 +1088,12 @@ __global__ void __launch_bounds__(kT6Threads, kMinBlocks) k_mech_tile6(MechArgs 
             S.off[lb] = cn;
         }
         __syncthreads();
-        if (w == 0) {  // exclusive scan of the 216 counts (7 per lane)
-            uint32_t v[7], sum = 0;
+        if (w == 0) {  // exclusive scan of the kNB counts (kSQ per lane)
+            uint32_t v[kSQ], sum = 0;
 #pragma unroll
-            for (int q = 0; q < 7; ++q) {
-                const int lb = lane * 7 + q;
-                v[q] = lb < 216 ? S.off[lb] : 0u;
+            for (int q = 0; q < kSQ; ++q) {
+                const int lb = lane * kSQ + q;
+                v[q] = lb < kNB ? S.off[lb] : 0u;
                 sum += v[q];
             }
             uint32_t inc = sum;
@@ -1073,16 +1104,19 @@ __global__ void __launch_bounds__(kT6Threads, kMinBlocks) k_mech_tile6(MechArgs 
             }
             uint32_t run = inc - sum;
 #pragma unroll
-            for (int q = 0; q < 7; ++q) {
-                const int lb = lane * 7 + q;
-                if (lb <= 216) S.off[lb] = run;
+            for (int q = 0; q < kSQ; ++q) {
+                const int lb = lane * kSQ + q;
+                if (lb <= kNB) S.off[lb] = run;
                 run += v[q];
             }
         }
         __syncthreads();
-        const int M = (int)S.off[216];
+        const int M = (int)S.off[kNB];
         if (M > kM6Max && S.use_pf && A.dense_list) {  // dense region: the dense-box kernel
-            if (tid == 0) A.dense_list[atomicAdd(&sc->n_dense, 1u)] = (uint32_t)t;
+            if (tid == 0) {
+                A.dense_list[atomicAdd(&sc->n_dense, 1u)] = ta;
+                if (kTZ == 2 && tb != 0xFFFFFFFFu) A.dense_list[atomicAdd(&sc->n_dense, 1u)] = tb;
+            }
             __syncthreads();
             continue;
         }
@@ -1090,19 +1124,24 @@ __global__ void __launch_bounds__(kT6Threads, kMinBlocks) k_mech_tile6(MechArgs 
             // over-full region or |coordinates| / L >= 2^30: reference formulation
             for (int k0 = 32 * w; k0 < nc; k0 += kT6Threads) {
                 Counts c;
-                if (k0 + lane < nc) mech_agent_global(A, S.g, g0 + k0 + lane, c);
+                const int k = k0 + lane;
+                if (k < nc)
+                    mech_agent_global(A, S.g, k < n0 ? g0 + k : g1 + (k - n0), c);
                 merge_counts<kStats>(c, S.W[w], A.fuse ? 0x7F : 0, lane);
             }
             __syncthreads();
             continue;
         }
         // ---- staged index -> box, tile agent -> staged index
-        for (int lb = tid; lb < 216; lb += kT6Threads) {
+        for (int lb = tid; lb < kNB; lb += kT6Threads) {
             const uint32_t o = S.off[lb], n = S.off[lb + 1] - o;
-            const bool inner = (S.lbxyz[lb] >> 9) != 0u;
-            const uint32_t kb = S.start[lb] - g0;
+            const uint32_t v = S.lbxyz[lb];
+            const bool inner = (v >> 10) != 0u;
+            // own agents: the first tile's in box order, then the second's (lz 5..8)
+            const uint32_t kb = (kTZ == 2 && ((v >> 6) & 15u) > 4u) ? (uint32_t)n0 + (S.start[lb] - g1)
+                                                                   : S.start[lb] - g0;
             for (uint32_t u = 0; u < n; ++u) {
-                S.mbox[o + u] = (uint8_t)lb;
+                S.mbox[o + u] = (typename TileGeo<kTZ>::MBox)lb;
                 if (inner) S.kmi[kb + u] = (uint16_t)(o + u);
             }
         }
@@ -1160,7 +1199,7 @@ __global__ void __launch_bounds__(kT6Threads, kMinBlocks) k_mech_tile6(MechArgs 
 #pragma unroll
             for (int a = 0; a < 3; ++a) {
                 sides |= (4 * tc[a] <= S.lo_box[a]) ? (1 << a) : 0;
-                sides |= (4 * tc[a] + 3 >= S.hi_box[a]) ? (8 << a) : 0;
+                sides |= (4 * tc[a] + (a == 2 ? 4 * kTZ : 4) - 1 >= S.hi_box[a]) ? (8 << a) : 0;
             }
         } else if (A.fuse) {
             sides = 0x7F;
@@ -1173,7 +1212,7 @@ __global__ void __launch_bounds__(kT6Threads, kMinBlocks) k_mech_tile6(MechArgs 
             // and the fp32 quotient (bb nc < 2^24) floors exactly
             const int klo = (int)__fdividef((float)(bb * nc), (float)B);
             const int khi = (int)__fdividef((float)((bb + 1) * nc), (float)B);
-            tile6_batch<kStats, kPair>(A, S, S.W[w], lane, g0, klo, khi - klo, M, sides);
+            tile6_batch<kStats, kPair, kTZ>(A, S, S.W[w], lane, g0, n0, g1, klo, khi - klo, M, sides);
         }
         __syncthreads();  // before the next tile overwrites the staged region
     }
@@ -1187,21 +1226,21 @@ __global__ void __launch_bounds__(kT6Threads, kMinBlocks) k_mech_tile6(MechArgs 
     if (kStats && lane < 5) atomicAdd(&sc->stats[lane], Wp.cnt[lane]);
 }
 
-template <bool kStats, int kMinBlocks, bool kPair>
+template <bool kStats, int kMinBlocks, bool kPair, int kTZ = 1>
 static bdm_status launch_tile6(Ctx *c, const MechArgs &A, cudaStream_t st) {
     static int per_sm_dev[kMaxDevices] = {};
     int &per_sm = per_sm_dev[c->device];
-    const int smem = (int)sizeof(Tile6SmemT<kPair>);
+    const int smem = (int)sizeof(Tile6SmemT<kPair, kTZ>);
     if (!per_sm) {
-        BDM_CUDA_TRY(cudaFuncSetAttribute(k_mech_tile6<kStats, kMinBlocks, kPair>,
+        BDM_CUDA_TRY(cudaFuncSetAttribute(k_mech_tile6<kStats, kMinBlocks, kPair, kTZ>,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         int v = 0;
         BDM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-            &v, k_mech_tile6<kStats, kMinBlocks, kPair>, kT6Threads, smem));
+            &v, k_mech_tile6<kStats, kMinBlocks, kPair, kTZ>, kT6Threads, smem));
         per_sm = v < 1 ? 1 : v;
     }
-    k_mech_tile6<kStats, kMinBlocks, kPair><<<(unsigned)(c->sm_count * per_sm), kT6Threads, smem, st>>>(
-        A, c->sc, c->prefilter);
+    k_mech_tile6<kStats, kMinBlocks, kPair, kTZ>
+        <<<(unsigned)(c->sm_count * per_sm), kT6Threads, smem, st>>>(A, c->sc, c->prefilter);
     return BDM_OK;
 }
 
@@ -1666,7 +1705,20 @@ bdm_status launch_mech(Ctx *c, bdm_agents *a, const bdm_params *p, cudaStream_t 
     A.dense_list = dense ? c->dense_list : nullptr;
     A.dense_perm = nullptr;
     BDM_CUDA_TRY(cudaMemsetAsync(&c->sc->n_dense, 0, 3 * sizeof(unsigned int), st));
-    if (c->mech_kernel == 0) {
+    // auto depth: agents per box of the first grid build (the host saw its geometry when
+    // it sized the slot array); either depth is exact, this only picks the faster one
+    double dens = c->density_hint;
+    if (c->dims_hint) {
+        const double boxes = (double)c->dims_hint[0] * (double)c->dims_hint[1] * (double)c->dims_hint[2];
+        if (boxes > 0.0) dens = (double)c->hint_n / boxes;
+    }
+    const int depth = c->tile_depth != 0 ? c->tile_depth
+                      : (dens > 0.0 && dens <= kSparseDensity ? 2 : 1);
+    if (c->mech_kernel == 0 && depth == 2) {  // sparse: two-tile units, 4 CTAs/SM
+        const bdm_status s = p->collect_stats ? launch_tile6<true, 4, false, 2>(c, A, st)
+                                              : launch_tile6<false, 4, false, 2>(c, A, st);
+        if (s != BDM_OK) return s;
+    } else if (c->mech_kernel == 0) {
         const bdm_status s = p->collect_stats ? launch_tile6<true, 5, false>(c, A, st)
                                               : launch_tile6<false, 5, false>(c, A, st);
         if (s != BDM_OK) return s;

@@ -16,16 +16,20 @@ pytestmark = pytest.mark.gpu
 REL_TOL = 1e-9  # north_star tolerance for fp64 positions
 
 
-@pytest.fixture(scope="module", params=[0, 1, 2, 3], ids=["tile", "reference", "tile_v1", "tile_4cta"])
+@pytest.fixture(scope="module", params=[(0, 1), (1, 1), (2, 1), (3, 1), (0, 2), (0, 0)],
+                ids=["tile", "reference", "tile_v1", "tile_4cta", "tile_depth2", "tile_auto"])
 def eng(request):
-    """Both mechanics kernels: the tile kernel (default) and the per-agent reference."""
+    """Every mechanics kernel: the tile kernel (default; also with two-tile work units,
+    option tile_depth 2), the per-agent reference and the other tile variants."""
     import torch
     if not torch.cuda.is_available():
         pytest.skip("no GPU")
     from paper_2503_10796_b200 import Engine
+    kernel, depth = request.param
     e = Engine(0, 1 << 16)
-    e.set_option("mech_kernel", request.param)
-    e.set_option("fuse_reduce", 0 if request.param == 1 else 1)  # tile kernels: fused a1
+    e.set_option("mech_kernel", kernel)
+    e.set_option("tile_depth", depth)
+    e.set_option("fuse_reduce", 0 if kernel == 1 else 1)  # tile kernels: fused a1
     yield e
     e.close()
 
