@@ -1226,19 +1226,35 @@ __global__ void __launch_bounds__(kT6Threads, kMinBlocks) k_mech_tile6(MechArgs 
     if (kStats && lane < 5) atomicAdd(&sc->stats[lane], Wp.cnt[lane]);
 }
 
-template <bool kStats, int kMinBlocks, bool kPair, int kTZ = 1>
-static bdm_status launch_tile6(Ctx *c, const MechArgs &A, cudaStream_t st) {
+// One-time per-device setup of a tile-kernel instance (shared-memory attribute, CTAs
+// per SM); returns the CTAs per SM.
+template <bool kStats, int kMinBlocks, bool kPair, int kTZ>
+static int tile6_per_sm(Ctx *c) {
     static int per_sm_dev[kMaxDevices] = {};
     int &per_sm = per_sm_dev[c->device];
-    const int smem = (int)sizeof(Tile6SmemT<kPair, kTZ>);
     if (!per_sm) {
-        BDM_CUDA_TRY(cudaFuncSetAttribute(k_mech_tile6<kStats, kMinBlocks, kPair, kTZ>,
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        const int smem = (int)sizeof(Tile6SmemT<kPair, kTZ>);
         int v = 0;
-        BDM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-            &v, k_mech_tile6<kStats, kMinBlocks, kPair, kTZ>, kT6Threads, smem));
+        if (cudaFuncSetAttribute(k_mech_tile6<kStats, kMinBlocks, kPair, kTZ>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess ||
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                &v, k_mech_tile6<kStats, kMinBlocks, kPair, kTZ>, kT6Threads, smem) != cudaSuccess) {
+            cudaGetLastError();
+            return 0;
+        }
         per_sm = v < 1 ? 1 : v;
     }
+    return per_sm;
+}
+
+template <bool kStats, int kMinBlocks, bool kPair, int kTZ = 1>
+static bdm_status launch_tile6(Ctx *c, const MechArgs &A, cudaStream_t st) {
+    const int per_sm = tile6_per_sm<kStats, kMinBlocks, kPair, kTZ>(c);
+    if (!per_sm) {
+        set_error("tile kernel setup failed");
+        return BDM_ECUDA;
+    }
+    const int smem = (int)sizeof(Tile6SmemT<kPair, kTZ>);
     k_mech_tile6<kStats, kMinBlocks, kPair, kTZ>
         <<<(unsigned)(c->sm_count * per_sm), kT6Threads, smem, st>>>(A, c->sc, c->prefilter);
     return BDM_OK;
@@ -1714,6 +1730,12 @@ bdm_status launch_mech(Ctx *c, bdm_agents *a, const bdm_params *p, cudaStream_t 
     }
     const int depth = c->tile_depth != 0 ? c->tile_depth
                       : (dens > 0.0 && dens <= kSparseDensity ? 2 : 1);
+    if (c->tile_depth == 0 && c->mech_kernel == 0) {  // auto may switch: set both up now
+        tile6_per_sm<false, 5, false, 1>(c);
+        tile6_per_sm<true, 5, false, 1>(c);
+        tile6_per_sm<false, 4, false, 2>(c);
+        tile6_per_sm<true, 4, false, 2>(c);
+    }
     if (c->mech_kernel == 0 && depth == 2) {  // sparse: two-tile units, 4 CTAs/SM
         const bdm_status s = p->collect_stats ? launch_tile6<true, 4, false, 2>(c, A, st)
                                               : launch_tile6<false, 4, false, 2>(c, A, st);
