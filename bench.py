@@ -725,7 +725,9 @@ def run_slabs(args, ws, rank, local):
     cap = int(n_local_est * 1.15) + 4096
     eng = Engine(local, cap)
     a = Agents.empty(cap)
-    stream = torch.cuda.Stream()
+    # the library runs on torch's current stream, the one NCCL and the payload copies
+    # of DistTransport are ordered with (a side stream would race with them)
+    stream = torch.cuda.current_stream(local)
     if strong:
         # every rank draws the same per-id population and keeps its slab (A48)
         chunk = 50_000_000

@@ -44,7 +44,9 @@ def slab_bounds(g: int, G: int, side: float):
 
 # ---------------------------------------------------------------------------- device ops
 class LibOps:
-    """Device side of one slab, backed by a libbdm context (one GPU)."""
+    """Device side of one slab, backed by a libbdm context (one GPU).  With DistTransport
+    the stream must be torch's current stream: the transport's NCCL calls and payload
+    copies are ordered on it, and the library's packing and appending must be too."""
 
     def __init__(self, engine: Engine, device="cuda", stream=None):
         self.eng = engine
