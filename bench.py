@@ -178,7 +178,7 @@ def run_ours(args, ws, rank, local):
     import torch
     from paper_2503_10796_b200 import Agents, Engine, Params
 
-    if ws > 1:
+    if ws > 1 or args.force_slabs:
         return run_slabs(args, ws, rank, local)
     if args.config == "cfg3":
         return run_cfg3(args, ws, rank, local)
@@ -874,6 +874,8 @@ def main():
                     help="row f1: 0 row-major tiles, 1 blocked Hilbert")
     ap.add_argument("--sort-every", type=int, default=1,
                     help="row f1: reorder the agents every K-th step (0 = never)")
+    ap.add_argument("--force-slabs", action="store_true",
+                    help="run the x-slab protocol path even on one GPU (a check of that path)")
     ap.add_argument("--aura-codec", action="store_true",
                     help="row f3: x-slab aura as delta + LZ4 streams (links slower than NVLink)")
     ap.add_argument("--shuffle", action="store_true",
