@@ -308,21 +308,39 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_apply(uint32_t *__restric
     const long long m = scan_len(sc, m_host);
     const long long base = (long long)blockIdx.x * kScanTile;
     if (base >= m) return;
-    // thread t owns items base + t*8 .. +7 (contiguous)
+    // thread t owns items base + t*8 .. +7 (contiguous, 32 B: two 16-byte accesses when
+    // the whole run is in range)
+    static_assert(kScanItems == 8, "vector path assumes 8 items per thread");
     uint32_t v[kScanItems];
     const long long i0 = base + (long long)threadIdx.x * kScanItems;
+    const bool full = i0 + kScanItems <= m;
+    if (full) {
+        const uint4 a = *reinterpret_cast<const uint4 *>(cnt + i0);
+        const uint4 b = *reinterpret_cast<const uint4 *>(cnt + i0 + 4);
+        v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+        v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+    } else {
+#pragma unroll
+        for (int k = 0; k < kScanItems; ++k) v[k] = (i0 + k < m) ? cnt[i0 + k] : 0u;
+    }
     uint32_t s = 0;
 #pragma unroll
-    for (int k = 0; k < kScanItems; ++k) {
-        v[k] = (i0 + k < m) ? cnt[i0 + k] : 0u;
-        s += v[k];
-    }
+    for (int k = 0; k < kScanItems; ++k) s += v[k];
     uint32_t tot;
     uint32_t run = block_excl_scan(s, &tot) + bsum[blockIdx.x];
+    uint32_t o[kScanItems];
 #pragma unroll
     for (int k = 0; k < kScanItems; ++k) {
-        if (i0 + k < m) cnt[i0 + k] = run;
+        o[k] = run;
         run += v[k];
+    }
+    if (full) {
+        *reinterpret_cast<uint4 *>(cnt + i0) = make_uint4(o[0], o[1], o[2], o[3]);
+        *reinterpret_cast<uint4 *>(cnt + i0 + 4) = make_uint4(o[4], o[5], o[6], o[7]);
+    } else {
+#pragma unroll
+        for (int k = 0; k < kScanItems; ++k)
+            if (i0 + k < m) cnt[i0 + k] = o[k];
     }
 }
 
