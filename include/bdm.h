@@ -311,7 +311,9 @@ bdm_status bdm_set_frame(bdm_handle h, const double *frame_dev);
 /* Pack agents of `a` for the slab [lo, hi) into the caller's send buffers
  * to_left / to_right (device SoA; x, y, z, diameter, id, flags, volume if both have
  * it), order preserving.  BDM_PACK_MIGRATE: x < lo -> left, x >= hi -> right, and the
- * leavers are removed from `a` by an order-preserving compaction.  BDM_PACK_AURA:
+ * leavers are removed from `a`: the remaining agents above the new count move into the
+ * leavers' slots (the paper's parallel removal; the order of the agents in
+ * `a` changes, which no result depends on).  BDM_PACK_AURA:
  * x < lo + margin -> left, x >= hi - margin -> right (copies; `a` unchanged).
  * counts_host (pinned, 3 int64, asynchronous) receives #left, #right, #remaining;
  * to_left->n, to_right->n and a->n are NOT updated.  If a send buffer is too small

@@ -9,10 +9,11 @@
 //                  (all-reduced by the caller into the global grid frame, R12)
 //   k_classify     per agent: 1 = to the left neighbour, 2 = to the right (a bit
 //                  mask for the aura: an agent near both borders goes both ways)
-//   scans          order-preserving positions in the left / right / remaining lists
-//   k_pack         copies the selected agents into the caller's send buffers and, for
-//                  a migration, compacts the remaining agents (the GPU counterpart of
-//                  the paper's parallel removal)
+//   scans          order-preserving positions in the left / right lists
+//   k_pack         copies the selected agents into the caller's send buffers; for a
+//                  migration it also lists the leavers' slots below the new count
+//   k_fill_holes   the remaining agents above the new count move into those slots:
+//                  the paper's parallel removal (Fig. 5.1), O(leavers)
 #include <cuda_runtime.h>
 #include <math.h>
 
@@ -101,10 +102,9 @@ __global__ void __launch_bounds__(256) k_classify(int64_t n, const double *__res
 struct PackArgs {
     int64_t n;
     bdm_agents a, L, R;
-    const uint32_t *pl, *pr, *ps;  // exclusive scans (n + 1 entries)
+    const uint32_t *pl, *pr;  // exclusive scans (n + 1 entries)
     int what;
-    double *tx, *ty, *tz, *td, *tv;  // compaction scratch (migration)
-    uint32_t *tid, *tfl;
+    uint32_t *holes;          // migration: slot of the h-th leaver below the new count
 };
 
 __device__ __forceinline__ void copy_agent(const bdm_agents &s, int64_t i, const bdm_agents &d,
@@ -131,38 +131,36 @@ __global__ void __launch_bounds__(256) k_pack(PackArgs P, long long *__restrict_
         }
         return;
     }
+    const bool mig = P.holes != nullptr;
+    const int64_t m = mig ? P.n - nl - nr : P.n;  // remaining agents
     if (i == 0) {
         counts[0] = nl;
         counts[1] = nr;
-        counts[2] = P.ps ? (long long)P.ps[P.n] : P.n;
+        counts[2] = m;
     }
     if (i >= P.n) return;
-    if (P.pl[i + 1] != P.pl[i]) copy_agent(P.a, i, P.L, P.pl[i]);
-    if (P.pr[i + 1] != P.pr[i]) copy_agent(P.a, i, P.R, P.pr[i]);
-    if (P.ps && P.ps[i + 1] != P.ps[i]) {  // remaining agent -> compaction scratch
-        const int64_t j = P.ps[i];
-        P.tx[j] = P.a.x[i];
-        P.ty[j] = P.a.y[i];
-        P.tz[j] = P.a.z[i];
-        P.td[j] = P.a.diameter[i];
-        P.tid[j] = P.a.id[i];
-        P.tfl[j] = P.a.flags[i];
-        if (P.a.volume) P.tv[j] = P.a.volume[i];
-    }
+    const uint32_t l0 = P.pl[i], r0 = P.pr[i];
+    const bool to_l = P.pl[i + 1] != l0, to_r = P.pr[i + 1] != r0;
+    if (to_l) copy_agent(P.a, i, P.L, l0);
+    if (to_r) copy_agent(P.a, i, P.R, r0);
+    // a leaver below m leaves a hole; the leavers before i number l0 + r0
+    if (mig && (to_l || to_r) && i < m) P.holes[l0 + r0] = (uint32_t)i;
 }
 
-__global__ void __launch_bounds__(256) k_unpack_remaining(PackArgs P) {
-    if (P.pl[P.n] > P.L.capacity || P.pr[P.n] > P.R.capacity) return;
-    const int64_t m = P.ps[P.n];
-    const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (j >= m) return;
-    P.a.x[j] = P.tx[j];
-    P.a.y[j] = P.ty[j];
-    P.a.z[j] = P.tz[j];
-    P.a.diameter[j] = P.td[j];
-    P.a.id[j] = P.tid[j];
-    P.a.flags[j] = P.tfl[j];
-    if (P.a.volume) P.a.volume[j] = P.tv[j];
+// Remaining agents at or above m fill the holes below m in rank order (the order of
+// agents in a slab never enters a result: the grid sorts them, R32).
+__global__ void __launch_bounds__(256) k_fill_holes(PackArgs P) {
+    const int64_t nl = P.pl[P.n], nr = P.pr[P.n];
+    if (nl > P.L.capacity || nr > P.R.capacity) return;
+    const int64_t m = P.n - nl - nr;
+    const int64_t i = m + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= P.n) return;
+    const int64_t out_i = (int64_t)(P.pl[i] + P.pr[i]);       // leavers before i
+    const int64_t out_m = (int64_t)(P.pl[m] + P.pr[m]);       // leavers before m
+    const bool stays = P.pl[i + 1] == P.pl[i] && P.pr[i + 1] == P.pr[i];
+    if (!stays) return;
+    const int64_t rank = (i - m) - (out_i - out_m);            // stayers in [m, i)
+    copy_agent(P.a, i, P.a, P.holes[rank]);
 }
 
 bdm_status launch_pack_slab(Ctx *c, bdm_agents *a, double lo, double hi, double margin, int what,
@@ -175,16 +173,15 @@ bdm_status launch_pack_slab(Ctx *c, bdm_agents *a, double lo, double hi, double 
         if ((s0 = need_agent_buf(c, &c->cls2)) != BDM_OK) return s0;
         if (what == BDM_PACK_MIGRATE && (s0 = need_agent_buf(c, &c->div_rank)) != BDM_OK)
             return s0;
-        if (a->volume && (s0 = need_agent_buf(c, &c->svol)) != BDM_OK) return s0;
     }
-    uint32_t *fl = c->cls, *fr = c->cls2, *fs = what == BDM_PACK_MIGRATE ? c->div_rank : nullptr;
+    uint32_t *fl = c->cls, *fr = c->cls2;
+    const bool mig = what == BDM_PACK_MIGRATE;
     const unsigned nb = (unsigned)((n + 1 + 255) / 256);
-    k_classify<<<nb, 256, 0, st>>>(n, a->x, lo, hi, margin, what, fl, fr, fs);
+    k_classify<<<nb, 256, 0, st>>>(n, a->x, lo, hi, margin, what, fl, fr, nullptr);
     BDM_LAUNCH_CHECK("k_classify");
     bdm_status s;
     if ((s = launch_scan_u32(c, fl, n + 1, st)) != BDM_OK) return s;
     if ((s = launch_scan_u32(c, fr, n + 1, st)) != BDM_OK) return s;
-    if (fs && (s = launch_scan_u32(c, fs, n + 1, st)) != BDM_OK) return s;
     PackArgs P;
     P.n = n;
     P.a = *a;
@@ -192,13 +189,13 @@ bdm_status launch_pack_slab(Ctx *c, bdm_agents *a, double lo, double hi, double 
     P.R = *to_right;
     P.pl = fl;
     P.pr = fr;
-    P.ps = fs;
     P.what = what;
-    P.tx = c->sx; P.ty = c->sy; P.tz = c->sz; P.td = c->sd; P.tv = c->svol;
-    P.tid = c->sidf; P.tfl = c->sflags;
+    P.holes = mig ? c->div_rank : nullptr;
     k_pack<<<nb, 256, 0, st>>>(P, c->pack_counts, c->sc);
-    if (fs) k_unpack_remaining<<<nb, 256, 0, st>>>(P);
-    c->launches += fs ? 3 : 2;
+    // the fill pass covers at most the n - m agents above m; launched for all n (the
+    // host does not know m), its blocks past the end exit at once
+    if (mig) k_fill_holes<<<nb, 256, 0, st>>>(P);
+    c->launches += mig ? 3 : 2;
     BDM_LAUNCH_CHECK("k_pack");
     BDM_CUDA_TRY(cudaMemcpyAsync(counts_host, c->pack_counts, 3 * sizeof(long long),
                                  cudaMemcpyDeviceToHost, st));
