@@ -52,11 +52,16 @@ def _cluster(orc, n_bg, side_bg, n_cl, side_cl, seed):
 
 @pytest.mark.parametrize("mech_kernel", [0, 1], ids=["tile", "reference"])
 @pytest.mark.parametrize("tile_order,sort_every", [(1, 1), (0, 3), (1, 0), (1, 2)])
-@pytest.mark.parametrize("pop", ["cfg2", "dense"])
+@pytest.mark.parametrize("pop", ["cfg2", "dense", "sparse"])
 def test_state_per_id_bit_exact(torch_cuda, orc, mech_kernel, tile_order, sort_every, pop):
+    """sparse: about one agent per box, where the tile kernel takes two-tile units
+    (auto tile depth) -- also under the Hilbert numbering."""
     from paper_2503_10796_b200 import Agents, Engine
     cfg = W.cfg2_scaled(60_000)
-    if pop == "cfg2":
+    if pop == "sparse":
+        side = (60_000 * 1000.0 / 0.5 * 1.05) ** (1.0 / 3.0)   # d = 10, ~0.95 agents per box
+        s = orc.init_spheres(60_000, 4, side, 10.0, 0.0, False)
+    elif pop == "cfg2":
         s = orc.init_spheres(cfg.n, cfg.seed, cfg.side, cfg.d_lo, cfg.d_width, cfg.d_random)
         # start from an unsorted memory order (a permutation of the ids)
         perm = np.random.default_rng(3).permutation(cfg.n)
