@@ -1322,6 +1322,10 @@ struct DenseWarp {
     uint16_t ce[kDQ];                       // contact -> survivor entry (j | owner << 8)
     uint8_t cf[kDQ];                        // bit1 contact, bit0 F_N != 0
     uint8_t chg[32];
+    // carry: kept candidates of a staging round past the word's 32 slots
+    double kX[32], kY[32], kZ[32], kR[32];
+    uint32_t kF[32], kG[32];
+    float kP[3][32];
 };
 
 template <bool kStats>
@@ -1476,14 +1480,17 @@ __global__ void __launch_bounds__(32 * kDWarps, 4) k_mech_dense(MechArgs A, DevS
             double Fx = 0.0, Fy = 0.0, Fz = 0.0;
             int nnz = 0;
             uint32_t my_cont = 0;
-            for (uint32_t base = 0; base < T; base += kDB) {
-                int nbt = (int)min((uint32_t)kDB, T - base);
-                __syncwarp();  // the previous batch is fully consumed
-                // ---- stage the batch (coalesced: a box's agents are contiguous)
-#pragma unroll
-                for (int u = 0; u < kDB / 32; ++u) {
-                    const int qs = 32 * u + lane;
-                    bool keep = qs < nbt;
+            // Kept candidates fill 32-slot words across staging rounds: a round's kept
+            // candidates past slot 31 wait in the carry and open the next word, so a
+            // word is processed full (its fixed costs are paid once per 32 candidates).
+            int fill = 0;
+            for (uint32_t base = 0; base < T || fill > 0; base += kDB) {
+                const bool more = base < T;
+                __syncwarp();  // the previous word is fully consumed
+                int fnew = fill;
+                if (more) {
+                    const int qs = lane;
+                    bool keep = (uint32_t)qs < T - base;
                     uint32_t gj = 0;
                     double x = 0.0, y = 0.0, z = 0.0;
                     float xr = 0.f, yr = 0.f, zr = 0.f;
@@ -1506,23 +1513,45 @@ __global__ void __launch_bounds__(32 * kDWarps, 4) k_mech_dense(MechArgs A, DevS
                         keep = fmaf(uz, uz, fmaf(uy, uy, ux * ux)) <= R2f;
                     }
                     const unsigned kb = __ballot_sync(0xffffffffu, keep);
-                    const int q = __popc(kb & lt_mask);   // kept candidates, stream order
-                    nbt = __popc(kb);                     // kDB == 32: one staging round
+                    const int q = fill + __popc(kb & lt_mask);  // stream order
+                    fnew = fill + __popc(kb);
                     if (keep) {
-                        Wd.X[q] = x;
-                        Wd.Y[q] = y;
-                        Wd.Z[q] = z;
-                        Wd.Rr[q] = A.sd[gj] * 0.5;
-                        Wd.F[q] = A.sflags[gj];
-                        Wd.G[q] = gj;
-                        float *xy = reinterpret_cast<float *>(&Wd.PXY[q >> 1]);
-                        xy[q & 1] = xr;
-                        xy[2 + (q & 1)] = yr;
-                        reinterpret_cast<float *>(&Wd.PZ[q >> 1])[q & 1] = zr;
+                        const double rr = A.sd[gj] * 0.5;
+                        const uint32_t ff = A.sflags[gj];
+                        if (q < 32) {
+                            Wd.X[q] = x;
+                            Wd.Y[q] = y;
+                            Wd.Z[q] = z;
+                            Wd.Rr[q] = rr;
+                            Wd.F[q] = ff;
+                            Wd.G[q] = gj;
+                            float *xy = reinterpret_cast<float *>(&Wd.PXY[q >> 1]);
+                            xy[q & 1] = xr;
+                            xy[2 + (q & 1)] = yr;
+                            reinterpret_cast<float *>(&Wd.PZ[q >> 1])[q & 1] = zr;
+                        } else {
+                            const int k = q - 32;
+                            Wd.kX[k] = x;
+                            Wd.kY[k] = y;
+                            Wd.kZ[k] = z;
+                            Wd.kR[k] = rr;
+                            Wd.kF[k] = ff;
+                            Wd.kG[k] = gj;
+                            Wd.kP[0][k] = xr;
+                            Wd.kP[1][k] = yr;
+                            Wd.kP[2][k] = zr;
+                        }
                     }
                 }
+                const bool last = base + kDB >= T;  // no staging round after this one
+                const int nbt = fnew >= 32 ? 32 : ((last || !more) ? fnew : 0);
+                if (nbt == 0) {
+                    fill = fnew;
+                    continue;
+                }
                 __syncwarp();
-                for (int u = 0; u < kDB / 32 && 32 * u < nbt; ++u) {  // warp-uniform
+                {  // warp-uniform: one word of nbt candidates
+                    const int u = 0;
                     // ---- phase 1: broadcast fp32 prefilter -> survivor bitmask
                     uint32_t m = 0;
                     const int jn = min(32, nbt - 32 * u);
@@ -1647,6 +1676,22 @@ __global__ void __launch_bounds__(32 * kDWarps, 4) k_mech_dense(MechArgs A, DevS
                         __syncwarp();
                     }
                 }
+                // ---- the carry opens the next word
+                const int rest = fnew - nbt;
+                __syncwarp();
+                if (lane < rest) {
+                    Wd.X[lane] = Wd.kX[lane];
+                    Wd.Y[lane] = Wd.kY[lane];
+                    Wd.Z[lane] = Wd.kZ[lane];
+                    Wd.Rr[lane] = Wd.kR[lane];
+                    Wd.F[lane] = Wd.kF[lane];
+                    Wd.G[lane] = Wd.kG[lane];
+                    float *xy = reinterpret_cast<float *>(&Wd.PXY[lane >> 1]);
+                    xy[lane & 1] = Wd.kP[0][lane];
+                    xy[2 + (lane & 1)] = Wd.kP[1][lane];
+                    reinterpret_cast<float *>(&Wd.PZ[lane >> 1])[lane & 1] = Wd.kP[2][lane];
+                }
+                fill = rest;
             }
             __syncwarp();
             if (active) {
