@@ -310,7 +310,8 @@ bdm_status bdm_set_frame(bdm_handle h, const double *frame_dev);
 
 /* Pack agents of `a` for the slab [lo, hi) into the caller's send buffers
  * to_left / to_right (device SoA; x, y, z, diameter, id, flags, volume if both have
- * it), order preserving.  BDM_PACK_MIGRATE: x < lo -> left, x >= hi -> right, and the
+ * it), in no particular order (no result depends on the order of agents, R32).
+ * BDM_PACK_MIGRATE: x < lo -> left, x >= hi -> right, and the
  * leavers are removed from `a`: the remaining agents above the new count move into the
  * leavers' slots (the paper's parallel removal; the order of the agents in
  * `a` changes, which no result depends on).  BDM_PACK_AURA:

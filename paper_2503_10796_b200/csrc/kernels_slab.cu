@@ -7,13 +7,14 @@
 // volumes are x-slabs [lo, hi) (outer slabs unbounded), one per GPU.
 //   k_local_frame  exact per-axis minimum and largest diameter of this rank's agents
 //                  (all-reduced by the caller into the global grid frame, R12)
-//   k_classify     per agent: 1 = to the left neighbour, 2 = to the right (a bit
-//                  mask for the aura: an agent near both borders goes both ways)
-//   scans          order-preserving positions in the left / right lists
-//   k_pack         copies the selected agents into the caller's send buffers; for a
-//                  migration it also lists the leavers' slots below the new count
-//   k_fill_holes   the remaining agents above the new count move into those slots:
-//                  the paper's parallel removal (Fig. 5.1), O(leavers)
+//   k_pack_count   counts the agents for the left / right neighbour (an aura agent near
+//                  both borders goes both ways)
+//   k_pack_copy    appends them to the caller's send buffers (warp-aggregated atomics:
+//                  the order of agents never enters a result, R32) and, for a
+//                  migration, lists the leavers' slots below the new count m and the
+//                  stayers at or above it
+//   k_pack_fill    the stayers above m move into the leavers' slots: the paper's
+//                  parallel removal (Fig. 5.1), O(leavers)
 #include <cuda_runtime.h>
 #include <math.h>
 
@@ -71,42 +72,6 @@ bdm_status launch_local_frame(Ctx *c, const bdm_agents *a, double *frame_dev, cu
     return BDM_OK;
 }
 
-// what: BDM_PACK_MIGRATE (x < lo -> left, x >= hi -> right, moved out) or BDM_PACK_AURA
-// (x < lo + margin -> left, x >= hi - margin -> right, copied).
-__global__ void __launch_bounds__(256) k_classify(int64_t n, const double *__restrict__ x, double lo,
-                                                  double hi, double margin, int what,
-                                                  uint32_t *__restrict__ fl,
-                                                  uint32_t *__restrict__ fr,
-                                                  uint32_t *__restrict__ fs) {
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i > n) return;
-    if (i == n) {  // the scans run over n + 1 entries (the last gives the totals)
-        fl[n] = fr[n] = 0u;
-        if (fs) fs[n] = 0u;
-        return;
-    }
-    const double px = x[i];
-    uint32_t l, r;
-    if (what == BDM_PACK_MIGRATE) {
-        l = px < lo ? 1u : 0u;
-        r = px >= hi ? 1u : 0u;
-    } else {
-        l = px < lo + margin ? 1u : 0u;
-        r = px >= hi - margin ? 1u : 0u;
-    }
-    fl[i] = l;
-    fr[i] = r;
-    if (fs) fs[i] = (l | r) ? 0u : 1u;
-}
-
-struct PackArgs {
-    int64_t n;
-    bdm_agents a, L, R;
-    const uint32_t *pl, *pr;  // exclusive scans (n + 1 entries)
-    int what;
-    uint32_t *holes;          // migration: slot of the h-th leaver below the new count
-};
-
 __device__ __forceinline__ void copy_agent(const bdm_agents &s, int64_t i, const bdm_agents &d,
                                            int64_t j) {
     d.x[j] = s.x[i];
@@ -118,9 +83,54 @@ __device__ __forceinline__ void copy_agent(const bdm_agents &s, int64_t i, const
     if (s.volume && d.volume) d.volume[j] = s.volume[i];
 }
 
-__global__ void __launch_bounds__(256) k_pack(PackArgs P, long long *__restrict__ counts,
-                                              DevScalars *__restrict__ sc) {
-    const int64_t nl = P.pl[P.n], nr = P.pr[P.n];
+// ---- atomic-append packing (the order of a slab's agents and of its ghosts never
+// enters a result: the grid sorts them, R32)
+__device__ __forceinline__ void side_flags(double px, double lo, double hi, double margin, int what,
+                                           bool &l, bool &r) {
+    if (what == BDM_PACK_MIGRATE) {
+        l = px < lo;
+        r = px >= hi;
+    } else {
+        l = px < lo + margin;
+        r = px >= hi - margin;
+    }
+}
+
+// Warp-aggregated slot in a list: one atomic per warp and list.
+__device__ __forceinline__ unsigned long long warp_slot(bool take, unsigned long long *ctr) {
+    const unsigned b = __ballot_sync(0xffffffffu, take);
+    const int lane = threadIdx.x & 31;
+    unsigned long long base = 0;
+    if (b && lane == __ffs(b) - 1) base = atomicAdd(ctr, (unsigned long long)__popc(b));
+    base = __shfl_sync(0xffffffffu, base, b ? __ffs(b) - 1 : 0);
+    return base + (unsigned long long)__popc(b & ((1u << lane) - 1u));
+}
+
+__global__ void __launch_bounds__(256) k_pack_count(int64_t n, const double *__restrict__ x,
+                                                    double lo, double hi, double margin, int what,
+                                                    unsigned long long *__restrict__ cnt) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    bool l = false, r = false;
+    if (i < n) side_flags(x[i], lo, hi, margin, what, l, r);
+    const unsigned bl = __ballot_sync(0xffffffffu, l), br = __ballot_sync(0xffffffffu, r);
+    if ((threadIdx.x & 31) == 0) {
+        if (bl) atomicAdd(&cnt[0], (unsigned long long)__popc(bl));
+        if (br) atomicAdd(&cnt[1], (unsigned long long)__popc(br));
+    }
+}
+
+struct PackArgs2 {
+    int64_t n;
+    bdm_agents a, L, R;
+    double lo, hi, margin;
+    int what;
+    uint32_t *holes, *fillers;  // migration: leavers below m, stayers at or above m
+};
+
+__global__ void __launch_bounds__(256) k_pack_copy(PackArgs2 P, unsigned long long *__restrict__ cnt,
+                                                   long long *__restrict__ counts,
+                                                   DevScalars *__restrict__ sc) {
+    const int64_t nl = (int64_t)cnt[0], nr = (int64_t)cnt[1];
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (nl > P.L.capacity || nr > P.R.capacity) {  // all-or-nothing on send capacity
         if (i == 0) {
@@ -132,69 +142,62 @@ __global__ void __launch_bounds__(256) k_pack(PackArgs P, long long *__restrict_
         return;
     }
     const bool mig = P.holes != nullptr;
-    const int64_t m = mig ? P.n - nl - nr : P.n;  // remaining agents
+    const int64_t m = mig ? P.n - nl - nr : P.n;
     if (i == 0) {
         counts[0] = nl;
         counts[1] = nr;
         counts[2] = m;
     }
-    if (i >= P.n) return;
-    const uint32_t l0 = P.pl[i], r0 = P.pr[i];
-    const bool to_l = P.pl[i + 1] != l0, to_r = P.pr[i + 1] != r0;
-    if (to_l) copy_agent(P.a, i, P.L, l0);
-    if (to_r) copy_agent(P.a, i, P.R, r0);
-    // a leaver below m leaves a hole; the leavers before i number l0 + r0
-    if (mig && (to_l || to_r) && i < m) P.holes[l0 + r0] = (uint32_t)i;
+    bool l = false, r = false;
+    if (i < P.n) side_flags(P.a.x[i], P.lo, P.hi, P.margin, P.what, l, r);
+    const unsigned long long jl = warp_slot(l, &cnt[2]);
+    const unsigned long long jr = warp_slot(r, &cnt[3]);
+    if (l) copy_agent(P.a, i, P.L, (int64_t)jl);
+    if (r) copy_agent(P.a, i, P.R, (int64_t)jr);
+    if (mig) {
+        const bool hole = (l || r) && i < m;
+        const bool filler = i < P.n && !(l || r) && i >= m;
+        const unsigned long long h = warp_slot(hole, &cnt[4]);
+        const unsigned long long f = warp_slot(filler, &cnt[5]);
+        if (hole) P.holes[h] = (uint32_t)i;
+        if (filler) P.fillers[f] = (uint32_t)i;
+    }
 }
 
-// Remaining agents at or above m fill the holes below m in rank order (the order of
-// agents in a slab never enters a result: the grid sorts them, R32).
-__global__ void __launch_bounds__(256) k_fill_holes(PackArgs P) {
-    const int64_t nl = P.pl[P.n], nr = P.pr[P.n];
-    if (nl > P.L.capacity || nr > P.R.capacity) return;
-    const int64_t m = P.n - nl - nr;
-    const int64_t i = m + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= P.n) return;
-    const int64_t out_i = (int64_t)(P.pl[i] + P.pr[i]);       // leavers before i
-    const int64_t out_m = (int64_t)(P.pl[m] + P.pr[m]);       // leavers before m
-    const bool stays = P.pl[i + 1] == P.pl[i] && P.pr[i + 1] == P.pr[i];
-    if (!stays) return;
-    const int64_t rank = (i - m) - (out_i - out_m);            // stayers in [m, i)
-    copy_agent(P.a, i, P.a, P.holes[rank]);
+__global__ void __launch_bounds__(256) k_pack_fill(PackArgs2 P, const unsigned long long *__restrict__ cnt) {
+    if ((int64_t)cnt[0] > P.L.capacity || (int64_t)cnt[1] > P.R.capacity) return;
+    const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k >= (int64_t)cnt[4]) return;  // as many holes as fillers
+    copy_agent(P.a, P.fillers[k], P.a, P.holes[k]);
 }
 
 bdm_status launch_pack_slab(Ctx *c, bdm_agents *a, double lo, double hi, double margin, int what,
                             bdm_agents *to_left, bdm_agents *to_right, long long *counts_host,
                             cudaStream_t st) {
     const int64_t n = a->n;
-    {
+    const bool mig = what == BDM_PACK_MIGRATE;
+    if (mig) {
         bdm_status s0;
         if ((s0 = need_agent_buf(c, &c->cls)) != BDM_OK) return s0;
         if ((s0 = need_agent_buf(c, &c->cls2)) != BDM_OK) return s0;
-        if (what == BDM_PACK_MIGRATE && (s0 = need_agent_buf(c, &c->div_rank)) != BDM_OK)
-            return s0;
     }
-    uint32_t *fl = c->cls, *fr = c->cls2;
-    const bool mig = what == BDM_PACK_MIGRATE;
-    const unsigned nb = (unsigned)((n + 1 + 255) / 256);
-    k_classify<<<nb, 256, 0, st>>>(n, a->x, lo, hi, margin, what, fl, fr, nullptr);
-    BDM_LAUNCH_CHECK("k_classify");
-    bdm_status s;
-    if ((s = launch_scan_u32(c, fl, n + 1, st)) != BDM_OK) return s;
-    if ((s = launch_scan_u32(c, fr, n + 1, st)) != BDM_OK) return s;
-    PackArgs P;
+    unsigned long long *cnt = (unsigned long long *)c->pack_counts + 8;  // 6 counters
+    BDM_CUDA_TRY(cudaMemsetAsync(cnt, 0, 6 * sizeof(unsigned long long), st));
+    const unsigned nb = (unsigned)((n + 255) / 256 > 0 ? (n + 255) / 256 : 1);
+    k_pack_count<<<nb, 256, 0, st>>>(n, a->x, lo, hi, margin, what, cnt);
+    PackArgs2 P;
     P.n = n;
     P.a = *a;
     P.L = *to_left;
     P.R = *to_right;
-    P.pl = fl;
-    P.pr = fr;
+    P.lo = lo;
+    P.hi = hi;
+    P.margin = margin;
     P.what = what;
-    P.holes = mig ? c->div_rank : nullptr;
-    k_pack<<<nb, 256, 0, st>>>(P, c->pack_counts, c->sc);
-    // the fill pass covers at most the n - m agents above m; launched for all n (the
-    // host does not know m), its blocks past the end exit at once
-    if (mig) k_fill_holes<<<nb, 256, 0, st>>>(P);
+    P.holes = mig ? c->cls : nullptr;
+    P.fillers = mig ? c->cls2 : nullptr;
+    k_pack_copy<<<nb, 256, 0, st>>>(P, cnt, c->pack_counts, c->sc);
+    if (mig) k_pack_fill<<<nb, 256, 0, st>>>(P, cnt);
     c->launches += mig ? 3 : 2;
     BDM_LAUNCH_CHECK("k_pack");
     BDM_CUDA_TRY(cudaMemcpyAsync(counts_host, c->pack_counts, 3 * sizeof(long long),
