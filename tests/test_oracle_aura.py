@@ -216,3 +216,51 @@ def test_stream_header_and_delta_gain():
     empty = {k: v[:0] for k, v in ref.items()}
     plain = orc.aura_encode(msg, empty)
     assert len(st) * 1.1 < len(plain) < 40 * 20000
+
+
+# ---- pins against the LZ4 reference implementation (the system's liblz4) -------------
+import lz4_ref  # noqa: E402
+
+needs_liblz4 = pytest.mark.skipif(lz4_ref.lib() is None, reason="liblz4 not installed")
+
+
+@needs_liblz4
+@pytest.mark.parametrize("data", list(_cases()), ids=lambda d: f"n{len(d)}")
+def test_liblz4_decodes_oracle_blocks(data):
+    """Every block the oracle's compressor emits is a valid LZ4 block whose reference
+    decoding (LZ4_decompress_safe) is exactly the input (R50: losslessness under the
+    format's own decoder, independent of the parse convention)."""
+    blk = orc.lz4_compress_block(data)
+    assert lz4_ref.decompress_block(blk, len(data)) == data
+
+
+def _stream_cases():
+    base = _aura(3000, 11)
+    ref = orc.aura_reference(base)
+    moved = dict(ref)
+    moved["x"] = ref["x"] + np.random.default_rng(12).uniform(-1e-2, 1e-2, 3000)
+    rng = np.random.default_rng(13)
+    keep = rng.random(3000) < 0.6
+    new = _aura(700, 14, id0=50_000)
+    churn = {k: np.concatenate([np.asarray(moved[k])[keep], new[k]]) for k in orc.AURA_FIELDS}
+    empty = {k: v[:0] for k, v in ref.items()}
+    yield "identical", ref, ref
+    yield "moved", moved, ref
+    yield "churn", churn, ref
+    yield "no_reference", moved, empty
+    yield "empty_message", empty, ref
+    big = _aura(40000, 15)                                # > 1,000 chunks, ragged tail
+    yield "multi_chunk", big, orc.aura_reference(_aura(39000, 15))
+
+
+@needs_liblz4
+@pytest.mark.parametrize("case", list(_stream_cases()), ids=lambda c: c[0])
+def test_liblz4_decodes_oracle_aura_streams(case):
+    """Each oracle aura stream, decoded block by block with liblz4, gives exactly the
+    oracle's payload (presence words, XOR byte planes, new ids) and the header counts."""
+    _, msg, ref = case
+    st = orc.aura_encode(msg, ref)
+    pay, nnew = orc.aura_payload(msg, ref)
+    got, nref, nnew2 = lz4_ref.decode_stream(st)
+    assert got == bytes(pay)
+    assert (nref, nnew2) == (len(ref["id"]), nnew)
