@@ -206,7 +206,7 @@ def run_ours(args, ws, rank, local):
                     force_threshold=cfg.force_threshold, detect_static=cfg.detect_static)
     # first step sizes the grid; reserve slot headroom (+8 tiles/axis) for the growth of
     # the open-boundary space over the run so no timed step overflows
-    eng.step(a, params, stream=stream)
+    eng.step(a, params, stream=stream, sync=True)
     gi = eng.grid_info()
     T = [(d + 3) // 4 + 8 for d in gi["dims"]]
     if args.tile_order:
@@ -359,7 +359,7 @@ def run_cfg3(args, ws, rank, local):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             torch.cuda.synchronize()
             e0.record(stream)
-            eng.step(a, params, stream=stream)
+            eng.step(a, params, stream=stream, sync=True)
             eng.grow_divide(a, params, W.CFG3_GROWTH, W.CFG3_V_MAX, stream=stream)
             e1.record(stream)
             torch.cuda.synchronize()
@@ -670,7 +670,7 @@ def run_aura(args, ws, rank, local):
     line["metric"] = "aura agents encoded/s (delta + LZ4, device timed)"
     line["unit"] = "agents/s"
     line["roofline"] = None
-    line["note"] = "timed region: bdm_aura_encode per step (decode timed alongside); one warp per 4 KB LZ4 chunk"
+    line["note"] = "timed region: bdm_aura_encode per step (decode timed alongside); one warp per 1 KB LZ4 chunk"
     print(json.dumps(line), flush=True)
 
 

@@ -205,6 +205,8 @@ bdm_status bdm_step_host(bdm_handle h, const bdm_agents *host_in, bdm_agents *ho
  * the new count to *n_out_host (pinned host memory, asynchronously; valid after the
  * stream synchronizes); a->n is NOT updated.  If n + #dividers > capacity nothing is
  * modified, *n_out_host = -(required capacity) and bdm_sync reports BDM_ECAPACITY.
+ * An id >= n (ids not dense) is detected on the device: nothing is modified,
+ * *n_out_host = n and bdm_sync reports BDM_EINVAL.
  * Errors: BDM_EINVAL (no volume array, growth < 0, v_max <= 0). */
 bdm_status bdm_grow_divide(bdm_handle h, bdm_agents *a, const bdm_params *p, double growth,
                            double v_max, int64_t *n_out_host, void *stream);
@@ -217,7 +219,9 @@ bdm_status bdm_grow_divide(bdm_handle h, bdm_agents *a, const bdm_params *p, dou
  *   if I and u32(Philox(seed, (id, p->step, 1)).w0) < p_rec: R;
  *   v = 2 u32(w0..w2) - 1, v /= |v| if |v| > 1; x = wrap(x + v) with Alg. 9's
  *   el = fmod(el, side); if el < 0: el = side + el.
- * No fused multiply-add.  Needs side/radius >= 3.  If counts_host (pinned, 4 int64)
+ * No fused multiply-add.  Needs 3 <= side/radius < 8193 (boxes per axis; the
+ * infected-index hash keys hold the box index in 40 bits), else BDM_EINVAL.  If
+ * counts_host (pinned, 4 int64)
  * is non-NULL it receives S, I, R after the step and the number of new infections
  * (asynchronously).  The infected index holds up to max(65536, n/16) agents (option
  * "sir_index_capacity"); beyond that the step is a no-op and bdm_sync reports

@@ -370,11 +370,12 @@ class Engine:
         _check(self.lib.bdm_mech_step(self.h, ctypes.byref(ca), ctypes.byref(cp),
                                       _stream_ptr(stream)))
 
-    def step(self, agents: Agents, params: Params, stream=None, sync: bool = True,
+    def step(self, agents: Agents, params: Params, stream=None, sync: bool = False,
              retries: int = 3):
-        """grid build + mechanics step.  With sync=True, checks the latched device
-        conditions and, on a grid-slot overflow, grows the slot array and re-issues the
-        step (the caller's arrays are untouched by an overflowed step)."""
+        """grid build + mechanics step, asynchronous on `stream` by default (errors and
+        a grid-slot overflow surface at the next bdm_sync).  With sync=True, checks the
+        latched device conditions and, on a grid-slot overflow, grows the slot array and
+        re-issues the step (the caller's arrays are untouched by an overflowed step)."""
         for _ in range(retries + 1):
             self.grid_build(agents, params.radius, stream)
             self.mech_step(agents, params, stream)
@@ -517,7 +518,7 @@ class Engine:
                   stream=None) -> int:
         """One proliferation step (R15): grid + mechanics on the snapshot, then
         growth/division at the post-mechanics positions."""
-        self.step(agents, params, stream=stream)
+        self.step(agents, params, stream=stream, sync=True)
         return self.grow_divide(agents, params, growth, v_max, stream=stream)
 
     def step_host(self, host_in: Agents, host_out: Agents, dev: Agents, params: Params,

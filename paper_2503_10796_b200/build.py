@@ -35,22 +35,70 @@ def _newest_input() -> float:
     return max(os.path.getmtime(f) for f in files)
 
 
+STAMP = SO + ".cmd"  # the full nvcc command of the built library (variants rebuild)
+
+
+def _command(out: str) -> list:
+    return [NVCC, *NVCC_FLAGS, "-shared", "-I", os.path.join(ROOT, "include"), "-I", CSRC,
+            *[os.path.join(CSRC, f) for f in SOURCES], "-o", out, "-lcudart"]
+
+
+def _stamp_text() -> str:
+    return " ".join(_command(SO))
+
+
+def up_to_date() -> bool:
+    """The library exists, is newer than every source, and was built by this exact
+    command (flags included: an A/B variant built with BDM_NVCC_EXTRA is not reused)."""
+    if not (os.path.exists(SO) and os.path.exists(STAMP)):
+        return False
+    if os.path.getmtime(SO) < _newest_input():
+        return False
+    with open(STAMP) as f:
+        return f.read() == _stamp_text()
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and os.path.exists(SO) and os.path.getmtime(SO) >= _newest_input():
+    """One nvcc -c per source, in parallel, then one nvcc -shared link."""
+    if not force and up_to_date():
         return SO
-    tmp = SO + ".tmp"
-    cmd = [NVCC, *NVCC_FLAGS, "-shared", "-I", os.path.join(ROOT, "include"), "-I", CSRC,
-           *[os.path.join(CSRC, f) for f in SOURCES], "-o", tmp, "-lcudart"]
-    res = subprocess.run(cmd, capture_output=True, text=True)
+    from concurrent.futures import ThreadPoolExecutor
+    objdir = os.path.join(HERE, "build")
+    os.makedirs(objdir, exist_ok=True)
+    inc = ["-I", os.path.join(ROOT, "include"), "-I", CSRC]
+
+    def compile_one(f):
+        obj = os.path.join(objdir, f.replace(".cu", ".o"))
+        cmd = [NVCC, *NVCC_FLAGS, *inc, "-c", os.path.join(CSRC, f), "-o", obj]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        return f, cmd, r, obj
+
+    with ThreadPoolExecutor(max_workers=min(len(SOURCES), os.cpu_count() or 4)) as ex:
+        results = list(ex.map(compile_one, SOURCES))
     log = os.path.join(HERE, "build.log")
+    tmp = SO + ".tmp"
+    link = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared",
+            *[o for _, _, _, o in results], "-o", tmp, "-lcudart"]
     with open(log, "w") as f:
-        f.write(" ".join(cmd) + "\n" + res.stdout + res.stderr)
+        for name, cmd, r, _ in results:
+            f.write(" ".join(cmd) + "\n" + r.stdout + r.stderr)
+    bad = [(n, r) for n, _, r, _ in results if r.returncode != 0]
+    if bad:
+        for n, r in bad:
+            sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError(f"nvcc failed for {[n for n, _ in bad]} (see {log})")
+    res = subprocess.run(link, capture_output=True, text=True)
+    with open(log, "a") as f:
+        f.write(" ".join(link) + "\n" + res.stdout + res.stderr)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
-        raise RuntimeError(f"nvcc failed (see {log})")
+        raise RuntimeError(f"nvcc link failed (see {log})")
     if verbose:
-        sys.stderr.write(res.stderr)
+        with open(log) as f:
+            sys.stderr.write(f.read())
     os.replace(tmp, SO)
+    with open(STAMP, "w") as f:
+        f.write(_stamp_text())
     return SO
 
 

@@ -113,6 +113,8 @@ static bdm_status read_latches(Ctx *c, bool clear) {
     bdm_status st = BDM_OK;
     if (c->sc_host->nonfinite) {
         st = fail(BDM_ENOTFINITE, "a position or diameter is NaN/Inf");
+    } else if (c->sc_host->overflow == 5) {
+        st = fail(BDM_EINVAL, "growth/division needs ids exactly 0..n-1 (an id is >= n)");
     } else if (c->sc_host->overflow == 4) {
         st = fail(BDM_ECAPACITY, "slab send buffer too small");
     } else if (c->sc_host->overflow == 3) {
@@ -252,6 +254,7 @@ bdm_status bdm_destroy(bdm_handle h) {
         if (q) cudaFree(q);
     if (c->sc_host) cudaFreeHost(c->sc_host);
     if (c->dims_hint) cudaFreeHost(c->dims_hint);
+    if (c->hint_ev) cudaEventDestroy(c->hint_ev);
     delete c;
     return BDM_OK;
 }
@@ -319,10 +322,15 @@ bdm_status bdm_grid_build(bdm_handle h, const bdm_agents *a, const bdm_agents *g
     // every 8th build the box counts travel to a pinned mirror in stream order; later
     // mechanics launches read whatever has arrived as their auto tile-depth hint (no
     // synchronization; the hint only picks the faster of two exact kernels)
-    if (c->tile_depth == 0 && (c->grid_builds & 7) == 1) {
+    // (the host reads the mirror only after the event recorded behind the copy has
+    // completed, together with the agent count saved with it)
+    if (c->tile_depth == 0 && (c->grid_builds & 7) == 1 && !c->hint_pending) {
+        if (!c->hint_ev) BDM_CUDA_TRY(cudaEventCreateWithFlags(&c->hint_ev, cudaEventDisableTiming));
         BDM_CUDA_TRY(cudaMemcpyAsync(c->dims_hint, c->sc->dims, sizeof(c->sc->dims),
                                      cudaMemcpyDeviceToHost, st));
+        BDM_CUDA_TRY(cudaEventRecord(c->hint_ev, st));
         c->hint_n = ntot;
+        c->hint_pending = true;
     }
     c->grid_valid = true;
     c->grid_x = a->x;

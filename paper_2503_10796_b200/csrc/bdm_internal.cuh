@@ -134,7 +134,10 @@ struct Ctx {
     int tile_depth = 0;    // option "tile_depth": 0 auto (by agents per box), 1, 2 (two-tile units)
     double density_hint = 0.0;  // agents per box of the first grid build (auto depth)
     int32_t *dims_hint = nullptr;  // pinned: box counts of a recent grid build (auto depth)
-    int64_t hint_n = 0;
+    int64_t hint_n = 0;            // agents of the build whose counts are in flight
+    cudaEvent_t hint_ev = nullptr; // recorded after the dims_hint copy
+    bool hint_pending = false;     // a copy is in flight: dims_hint is not to be read yet
+    double hint_density = 0.0;     // agents per box of the last completed copy
     int diffuse_tma = 1;   // option "diffuse_tma": TMA-pipelined stencil when nx is even
     int tile_order = 0;    // option "tile_order" (row f1): 0 row-major, 1 blocked Hilbert
     int64_t sort_every = 1;  // option "sort_every" (row f1): reorder the caller's SoA every K-th build

@@ -22,9 +22,14 @@ namespace bdm {
 
 __global__ void __launch_bounds__(256) k_div_mark(int64_t n, const double *__restrict__ vol,
                                                   const uint32_t *__restrict__ id, double v_max,
-                                                  uint32_t *__restrict__ flag_by_id) {
+                                                  uint32_t *__restrict__ flag_by_id,
+                                                  DevScalars *__restrict__ sc) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i < n) flag_by_id[id[i]] = (vol[i] < v_max) ? 0u : 1u;
+    if (i < n) {
+        const uint32_t me = id[i];
+        if ((int64_t)me < n) flag_by_id[me] = (vol[i] < v_max) ? 0u : 1u;
+        else sc->overflow = 5;  // ids must be exactly 0..n-1: nothing is modified
+    }
     if (i == 0) flag_by_id[n] = 0u;
 }
 
@@ -35,8 +40,12 @@ __global__ void __launch_bounds__(256) k_div_apply(
     const uint32_t *__restrict__ rank_by_id, double growth, double v_max, double vol_to_r3,
     uint32_t k0, uint32_t k1, uint32_t step, DevScalars *__restrict__ sc,
     long long *__restrict__ n_new) {
-    const int64_t total = (int64_t)rank_by_id[n];
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (sc->overflow == 5) {  // an id outside 0..n-1 (k_div_mark): no change
+        if (i == 0) *n_new = (long long)n;
+        return;
+    }
+    const int64_t total = (int64_t)rank_by_id[n];
     if (n + total > capacity) {  // all-or-nothing: nothing is modified
         if (i == 0) {
             sc->overflow = 2;
@@ -86,7 +95,7 @@ bdm_status launch_grow_divide(Ctx *c, bdm_agents *a, double growth, double v_max
         const bdm_status s0 = need_agent_buf(c, &c->div_rank);
         if (s0 != BDM_OK) return s0;
     }
-    k_div_mark<<<nb, 256, 0, st>>>(n, a->volume, a->id, v_max, c->div_rank);
+    k_div_mark<<<nb, 256, 0, st>>>(n, a->volume, a->id, v_max, c->div_rank, c->sc);
     BDM_LAUNCH_CHECK("k_div_mark");
     bdm_status s = launch_scan_u32(c, c->div_rank, n + 1, st);
     if (s != BDM_OK) return s;

@@ -1768,11 +1768,17 @@ bdm_status launch_mech(Ctx *c, bdm_agents *a, const bdm_params *p, cudaStream_t 
     BDM_CUDA_TRY(cudaMemsetAsync(&c->sc->n_dense, 0, 3 * sizeof(unsigned int), st));
     // auto depth: agents per box of the first grid build (the host saw its geometry when
     // it sized the slot array); either depth is exact, this only picks the faster one
-    double dens = c->density_hint;
-    if (c->dims_hint) {
-        const double boxes = (double)c->dims_hint[0] * (double)c->dims_hint[1] * (double)c->dims_hint[2];
-        if (boxes > 0.0) dens = (double)c->hint_n / boxes;
+    if (c->hint_pending) {
+        const cudaError_t q = cudaEventQuery(c->hint_ev);
+        if (q == cudaSuccess) {
+            const double boxes = (double)c->dims_hint[0] * (double)c->dims_hint[1] * (double)c->dims_hint[2];
+            if (boxes > 0.0) c->hint_density = (double)c->hint_n / boxes;
+            c->hint_pending = false;
+        } else if (q == cudaErrorNotReady && cudaPeekAtLastError() == cudaErrorNotReady) {
+            cudaGetLastError();  // "not ready" is not a failure; leave real errors alone
+        }
     }
+    const double dens = c->hint_density > 0.0 ? c->hint_density : c->density_hint;
     const int depth = c->tile_depth != 0 ? c->tile_depth
                       : (dens > 0.0 && dens <= kSparseDensity ? 2 : 1);
     if (c->tile_depth == 0 && c->mech_kernel == 0) {  // auto may switch: set both up now

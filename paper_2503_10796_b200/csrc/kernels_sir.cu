@@ -379,7 +379,15 @@ static int next_pow2_bits(int64_t v) {
 bdm_status launch_sir_step(Ctx *c, bdm_agents *a, const bdm_params *p, double side, double radius,
                            double p_inf, double p_rec, long long *counts_host, cudaStream_t st) {
     SirWs &W = c->sir;
-    const int D0 = (int)floor(side / radius);
+    // the hash key packs the box index below the step stamp (kStampShift = 40 bits), so
+    // D^3 must stay below 2^40: D <= 8192 boxes per axis (checked before the int cast)
+    const double ratio = side / radius;
+    if (!(ratio >= 3.0) || !(ratio < 8193.0)) {
+        set_error("SIR needs 3 <= side / radius < 8193 (boxes per axis; the infected-index "
+                  "hash keys hold D^3 < 2^40)");
+        return BDM_EINVAL;
+    }
+    const int D0 = (int)floor(ratio);
     // the GPU's fine lattice: L = side/D >= R, D a multiple of kCoarse when large (the
     // box size does not enter any result: the infection test is exact for any L >= R)
     const int D = D0 >= 2 * kCoarse ? D0 - D0 % kCoarse : D0;
@@ -388,8 +396,8 @@ bdm_status launch_sir_step(Ctx *c, bdm_agents *a, const bdm_params *p, double si
         set_error("SIR needs side / radius >= 3 boxes per axis");
         return BDM_EINVAL;
     }
-    if ((long long)D * D * D >= (1ll << 62)) {
-        set_error("SIR grid too large");
+    if ((long long)D * D * D >= (1ll << kStampShift)) {
+        set_error("SIR grid too large (D^3 >= 2^40)");
         return BDM_EINVAL;
     }
     const int B = D / cf;

@@ -47,7 +47,7 @@ def test_cfg5_full_size_sampled_cubes(orc):
                        d_random=cfg.d_random)
         gp = Params(k=cfg.k, gamma=cfg.gamma, dt=cfg.dt, max_displacement=cfg.max_disp,
                     force_threshold=cfg.force_threshold, detect_static=cfg.detect_static)
-        e.step(a, gp)                       # step 0 (sizes the grid), then the checked step
+        e.step(a, gp, sync=True)                       # step 0 (sizes the grid), then the checked step
         torch.cuda.synchronize()
         S, R = 100.0, cfg.d_lo + cfg.d_width    # cube side, interaction radius (max d)
         gmin = [float(getattr(a, f)[:cfg.n].min()) for f in ("x", "y", "z")]
@@ -55,7 +55,7 @@ def test_cfg5_full_size_sampled_cubes(orc):
         befores = []
         for c in cubes:
             befores.append(_box(a, cfg.n, [v - R - 1.0 for v in c], [v + S + R + 1.0 for v in c]))
-        e.step(a, gp)
+        e.step(a, gp, sync=True)
         gi = e.grid_info()
         torch.cuda.synchronize()
         op = orc.mech_params(k=cfg.k, gamma=cfg.gamma, dt=cfg.dt, max_disp=cfg.max_disp,

@@ -140,8 +140,8 @@ def test_soma_steps_bit_exact(eng):
 
 
 def test_diffuse_full_size_sampled(eng):
-    """The bench grid (256^3 here, the bench's size per substance), one step, compared on
-    every point (the oracle finishes a 16.8M-point step in about a second)."""
+    """A 256^3 grid (the bench uses 512^3 per substance; 256^3 keeps the oracle at about
+    a second for its 16.8M-point step), one step, compared on every point."""
     import torch
     n = 256
     cg, og = _grids(n, n, n, (0.0, 0.0, 0.0), 2.0, 2.0, 2.0)

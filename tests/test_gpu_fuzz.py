@@ -92,7 +92,7 @@ def test_random_populations_bit_exact(engines, orc, case):
     for k, e in engines.items():
         a = Agents.from_numpy(s)
         for _ in range(2):
-            e.step(a, gp)
+            e.step(a, gp, sync=True)
         g = a.numpy()
         for f in FIELDS:
             assert np.array_equal(np.asarray(g[f]).view(np.uint8),

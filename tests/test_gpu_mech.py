@@ -92,7 +92,7 @@ def test_cfg1_trajectory_bit_exact(eng, orc):
     o = orc_init(orc, cfg)
     gp, op = params_pair(orc, cfg)
     for t in range(cfg.steps):
-        eng.step(a, gp)
+        eng.step(a, gp, sync=True)
         st = eng.stats()
         o, cnt = orc.step_full(o, op)
         assert_state_equal(a.numpy(), o, f"cfg1 step {t}")
@@ -127,7 +127,7 @@ def test_cfg2_mix_reduced_n_static_on(eng, orc, n):
     o = orc_init(orc, cfg)
     gp, op = params_pair(orc, cfg)
     for t in range(4):
-        eng.step(a, gp)
+        eng.step(a, gp, sync=True)
         st = eng.stats()
         o, cnt = orc.step_full(o, op)
         assert_state_equal(a.numpy(), o, f"n={n} step {t}")
@@ -148,9 +148,9 @@ def test_static_skip_fires_and_matches_oracle(eng, orc, side, tau):
     gp_off, _ = params_pair(orc, cfg, detect_static=False, force_threshold=tau)
     n_static = 0
     for t in range(8):
-        eng.step(a_on, gp_on)
+        eng.step(a_on, gp_on, sync=True)
         n_static += eng.stats()["n_static"]
-        eng.step(a_off, gp_off)
+        eng.step(a_off, gp_off, sync=True)
         o, _ = orc.step_full(o, op_on)
         g_on = a_on.numpy()
         assert_state_equal(g_on, o, f"static on step {t}")
@@ -166,28 +166,28 @@ def test_edge_cases(eng, orc):
     # n = 0: valid no-op
     a = Agents.empty(4)
     a.n = 0
-    eng.step(a, Params())
+    eng.step(a, Params(), sync=True)
     # all agents in one box; coincident centres (dist = 0 contributes nothing, R10)
     s = {"x": np.array([1.0, 1.0, 1.5, 2.0]), "y": np.array([0.0, 0.0, 0.5, 0.25]),
          "z": np.zeros(4), "d": np.full(4, 10.0), "id": np.arange(4, dtype=np.uint32),
          "flags": np.full(4, 4, np.uint32)}
     a = Agents.from_numpy(s)
     gp, op = params_pair(orc, W.CFG1)
-    eng.step(a, gp)
+    eng.step(a, gp, sync=True)
     o, _ = orc.step_full(s, op)
     assert_state_equal(a.numpy(), o, "one box")
     # heavy overlap with a large dt: the 3 um cap binds (R6)
     s = orc.init_spheres(3000, 2, 40.0, 10.0)
     a = Agents.from_numpy(s)
     gp, op = params_pair(orc, W.CFG1, dt=1.0)
-    eng.step(a, gp)
+    eng.step(a, gp, sync=True)
     o, _ = orc.step_full(s, op)
     assert_state_equal(a.numpy(), o, "cap")
     # closed boundary (clamp into [lo, hi])
     s = orc.init_spheres(2000, 4, 50.0, 10.0)
     a = Agents.from_numpy(s)
     gp, op = params_pair(orc, W.CFG1, dt=1.0, boundary=1, lo=(5, 5, 5), hi=(45, 45, 45))
-    eng.step(a, gp)
+    eng.step(a, gp, sync=True)
     o, _ = orc.step_full(s, op)
     assert_state_equal(a.numpy(), o, "closed")
 
@@ -210,7 +210,7 @@ def test_crowded_neighbourhoods(eng, orc, k):
     gp, op = params_pair(orc, W.CFG1)
     a = Agents.from_numpy(s)
     for t in range(2):
-        eng.step(a, gp)
+        eng.step(a, gp, sync=True)
         s, _ = orc.step_full(s, op)
         assert_state_equal(a.numpy(), s, f"k={k} step {t}")
 
@@ -244,7 +244,7 @@ def test_dense_regions(eng, orc, n_bg, side_bg, n_cl, side_cl, static, tau):
     gp, op = params_pair(orc, W.CFG1, detect_static=static, force_threshold=tau)
     a = Agents.from_numpy(s)
     for t in range(3):
-        eng.step(a, gp)
+        eng.step(a, gp, sync=True)
         st = eng.stats()
         s, cnt = orc.step_full(s, op)
         assert_state_equal(a.numpy(), s, f"dense step {t}")
@@ -261,12 +261,12 @@ def test_capacity_overflow_is_recovered(eng, orc):
     s = orc.init_spheres(500, 5, 50.0, 10.0)
     a = Agents.from_numpy(s)
     gp, op = params_pair(orc, W.CFG1)
-    e.step(a, gp)
+    e.step(a, gp, sync=True)
     s1, _ = orc.step_full(s, op)
     s1 = {k: v.copy() for k, v in s1.items()}
     s1["x"][0] += 5000.0
     a = Agents.from_numpy(s1)
-    e.step(a, gp)
+    e.step(a, gp, sync=True)
     o, _ = orc.step_full(s1, op)
     assert_state_equal(a.numpy(), o, "after regrow")
     e.close()
@@ -334,7 +334,7 @@ def test_cfg2_full_size_teacher_forced(eng, orc):
     rng = np.random.default_rng(0)
     for t in range(2):
         before = a.numpy()
-        eng.step(a, gp)
+        eng.step(a, gp, sync=True)
         after = a.numpy()
         sample = rng.choice(cfg.n, 100_000, replace=False)
         out, cnt = orc.mech_step(before, op, sample=sample)

@@ -59,7 +59,7 @@ def test_onco_steps_bit_exact(eng, orc, n, side, p_death, p_div, steps):
     for t in range(steps):
         po = orc.onco_params(p_death=p_death, p_div=p_div, step=t, seed=7)
         pg = COncoParams.make(p_death=p_death, p_div=p_div, step=t, seed=7)
-        eng.step(a, gp)
+        eng.step(a, gp, sync=True)
         id_next_g = eng.onco_step(a, age, pg, id_next_g)
         s, _, id_next_o = orc.onco_full_step(s, op, po, id_next_o)
         assert id_next_g == id_next_o and a.n == len(s["x"]), t

@@ -79,7 +79,7 @@ def test_state_per_id_bit_exact(torch_cuda, orc, mech_kernel, tile_order, sort_e
         o = s
         for t in range(5):
             ids_before = a.numpy()["id"]
-            e.step(a, gp)
+            e.step(a, gp, sync=True)
             st = e.stats()
             o, cnt = orc.step_full(o, op)
             g = a.numpy()

@@ -58,7 +58,7 @@ def test_virtual_slabs_bit_identical(orc, G, n, codec):
     e.init_spheres(a, cfg.n, seed=cfg.seed, side=cfg.side, d_lo=cfg.d_lo, d_width=cfg.d_width,
                    d_random=cfg.d_random)
     for _ in range(4):
-        e.step(a, params)
+        e.step(a, params, sync=True)
     ref = _by_id(a.numpy())
     assert np.array_equal(got["id"], ref["id"])
     for k in ("x", "y", "z", "d", "flags"):
