@@ -123,50 +123,165 @@ def dist_env():
 
 
 # ------------------------------------------------------------------ CPU oracle legs
-def oracle_step_rate(cfg_n: int, repeats: int = 1):
-    """Times the oracle (single-threaded C, as it stands) on one full mechanics step of
-    the cfg2 workload at cfg_n agents (same density and diameter mix)."""
+_ORC = {}  # state read by the forked oracle workers (shared copy-on-write)
+
+
+def host_cpu():
+    """(cpu model, cores available to this process, logical cpus)."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    return model, cores, os.cpu_count()
+
+
+def _mem_available_gb():
+    try:
+        with open("/proc/meminfo") as f:
+            for line in f:
+                if line.startswith("MemAvailable"):
+                    return int(line.split()[1]) / 2**20
+    except OSError:
+        pass
+    return 16.0
+
+
+def _orc_mech_slice(bounds):
+    import numpy as np
     import oracle
-    cfg = W.cfg2_scaled(cfg_n)
-    s = oracle.init_spheres(cfg.n, cfg.seed, cfg.side, cfg.d_lo, cfg.d_width, cfg.d_random)
-    p = oracle.mech_params(detect_static=True)
-    times = []
-    for _ in range(repeats):
+    lo, hi, _ = bounds
+    oracle.mech_step(_ORC["s"], _ORC["p"], sample=np.arange(lo, hi, dtype=np.int64))
+    return hi - lo
+
+
+def _orc_sir_slice(bounds):
+    import numpy as np
+    import oracle
+    lo, hi, t = bounds
+    c = _ORC["cfg"]
+    oracle.sir_step_sample(_ORC["s"], c.side, c.radius, c.p_inf, c.p_rec, c.seed, t,
+                           np.arange(lo, hi, dtype=np.int64))
+    return hi - lo
+
+
+class OracleAllCores:
+    """The oracle (oracle/, single-threaded C, unchanged) on all host cores.  One worker
+    process per core (fork), each running the oracle's step in its sample mode on a
+    disjoint contiguous slice of the agents, all on the same full start-of-step state;
+    every worker builds the step's grid index itself, as the oracle's step does.  The
+    per-agent results are the oracle's, so the slices together are one whole step."""
+
+    def __init__(self, state, params=None, kind="mech", sir_cfg=None, bytes_per_agent=24.0):
+        import multiprocessing as mp
+
+        import numpy as np
+        _ORC.clear()
+        _ORC.update(s=state, p=params, cfg=sir_cfg)
+        self.kind = kind
+        self.n = len(state["x"])
+        self.model, cores, self.ncpu = host_cpu()
+        per_worker_gb = bytes_per_agent * 1.5 * self.n / 2**30 + 0.2
+        self.workers = max(1, min(cores, int(0.6 * _mem_available_gb() / per_worker_gb)))
+        edges = np.linspace(0, self.n, self.workers + 1).astype(np.int64)
+        self.bounds = [(int(edges[k]), int(edges[k + 1])) for k in range(self.workers)
+                       if edges[k + 1] > edges[k]]
+        self.pool = mp.get_context("fork").Pool(self.workers)
+
+    def step(self, t=0):
+        fn = _orc_mech_slice if self.kind == "mech" else _orc_sir_slice
         t0 = time.perf_counter()
-        out, _ = oracle.mech_step(s, p)
-        times.append(time.perf_counter() - t0)
-        s = dict(s, x=out["x"], y=out["y"], z=out["z"], flags=out["flags"])
-    return cfg.n / statistics.median(times), times
+        done = sum(self.pool.map(fn, [(lo, hi, t) for lo, hi in self.bounds], chunksize=1))
+        dt = time.perf_counter() - t0
+        assert done == self.n
+        return dt
+
+    def close(self):
+        self.pool.close()
+        self.pool.join()
+
+    def describe(self):
+        return {"cores": self.workers, "threads": self.workers, "nproc": self.ncpu,
+                "cpu_model": self.model}
+
+
+def _mech_state(cfg):
+    """A mid-run state of a mechanics config: the seeded population with every agent
+    flagged MOVED (at tau = 0 nearly every agent moves each step, so no agent is a
+    static candidate, as in the GPU's timed steps)."""
+    import oracle
+    s = oracle.init_spheres(cfg.n, cfg.seed, cfg.side, cfg.d_lo, cfg.d_width, cfg.d_random)
+    s["flags"][:] = 1
+    return s
+
+
+def cpu_baseline_mech(cfg, steps=1, note=""):
+    """The oracle on all host cores, `steps` whole steps of `cfg` (rank 0, N = 1)."""
+    import oracle
+    oracle.build()
+    s = _mech_state(cfg)
+    p = oracle.mech_params(k=cfg.k, gamma=cfg.gamma, dt=cfg.dt, max_disp=cfg.max_disp,
+                           force_threshold=cfg.force_threshold, detect_static=cfg.detect_static)
+    orc = OracleAllCores(s, p)
+    try:
+        times = [orc.step() for _ in range(steps)]
+    finally:
+        orc.close()
+    t = statistics.median(times)
+    return {"value": cfg.n / t, "unit": UNIT, "kind": "oracle", **orc.describe(),
+            "sample": f"{steps} whole oracle step(s) of {cfg.name} ({cfg.n} agents, mid-run "
+                      f"flags), agents split over {orc.workers} worker processes (the oracle's "
+                      f"sample mode, disjoint slices; each worker builds the step's grid index); "
+                      f"median {t:.2f} s{note}"}
 
 
 def run_reference(args, ws, rank):
-    """--impl reference: the CPU oracle on the host cores (rank 0 only)."""
+    """--impl reference: the CPU oracle (as it stands) on all host cores (rank 0 only),
+    on cfg2, the metric's workload.  Each step is one whole oracle step of a cube of the
+    cfg2 population (same density, diameter mix, static skip) whose size is chosen so the
+    --steps K --warmup W run ends in about two and a half minutes."""
     if rank != 0:
         return
     import oracle
     oracle.build()
-    n_sample = 200_000
-    cfg = W.cfg2_scaled(n_sample)
-    s = oracle.init_spheres(cfg.n, cfg.seed, cfg.side, cfg.d_lo, cfg.d_width, cfg.d_random)
-    p = oracle.mech_params(detect_static=True)
-    for _ in range(args.warmup):
-        out, _ = oracle.mech_step(s, p)
-        s = dict(s, x=out["x"], y=out["y"], z=out["z"], flags=out["flags"])
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        out, _ = oracle.mech_step(s, p)
-        s = dict(s, x=out["x"], y=out["y"], z=out["z"], flags=out["flags"])
-    dt = time.perf_counter() - t0
-    value = cfg.n * args.steps / dt
-    sample = (f"each step = one full oracle mechanics step of the cfg2 workload at {n_sample} "
-              f"agents (same density, diameter mix, static skip on)")
+    steps, warm = args.steps, min(args.warmup, 3)
+    cal_n = 500_000
+    cal = W.cfg2_scaled(cal_n)
+    orc = OracleAllCores(_mech_state(cal), oracle.mech_params(detect_static=True))
+    try:
+        t_cal = orc.step()
+    finally:
+        orc.close()
+    per_agent = t_cal / cal_n
+    n = int(min(W.CFG2.n, max(200_000, 150.0 / ((steps + warm) * per_agent))))
+    cfg = W.cfg2_scaled(n) if n < W.CFG2.n else W.CFG2
+    orc = OracleAllCores(_mech_state(cfg), oracle.mech_params(detect_static=True))
+    try:
+        for _ in range(warm):
+            orc.step()
+        times = [orc.step() for _ in range(steps)]
+    finally:
+        orc.close()
+    dt = sum(times)
+    value = cfg.n * steps / dt
+    sample = (f"each step = one whole oracle mechanics step of a {cfg.n}-agent cube of the cfg2 "
+              f"population (same density, diameter mix, static skip; mid-run flags), the "
+              f"agents split over {orc.workers} worker processes (oracle sample mode)")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
+        "steps": steps, "warmup": args.warmup, "ms_per_step": dt / steps * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": "cfg2 (configs[1]) sample", "agents_per_step": n_sample},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+        "config": {"workload": "cfg2 (configs[1]), spatial sample", "agents_per_step": cfg.n,
+                   "full_workload_agents": W.CFG2.n},
+        "step_ms": {"median": statistics.median(times) * 1e3,
+                    "p90": sorted(times)[int(0.9 * (len(times) - 1))] * 1e3},
+        "cpu_baseline": {"value": value, "unit": UNIT, "kind": "oracle", **orc.describe(),
                          "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -848,14 +963,9 @@ def measure_e2e(eng, cfg, params, stream, steps: int = 7):
 
 
 def cpu_baseline():
-    import oracle
-    oracle.build()
-    n = 1_000_000
-    value, times = oracle_step_rate(n, repeats=2)
-    return {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"one full oracle step (single-threaded C) of the cfg2 workload at {n} "
-                      f"agents, same density/diameter mix, static skip on; median of "
-                      f"{len(times)} steps ({', '.join(f'{t:.2f}' for t in times)} s)"}
+    """cpu_baseline of the default line: one whole cfg2 step (10M agents) of the oracle
+    on all host cores."""
+    return cpu_baseline_mech(W.CFG2, steps=1)
 
 
 def main():

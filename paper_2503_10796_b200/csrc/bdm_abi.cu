@@ -78,7 +78,7 @@ static bdm_status grow_slots(Ctx *c, int64_t nslots) {
     if (nslots <= c->slot_cap) return BDM_OK;
     BDM_CUDA_TRY(cudaDeviceSynchronize());
     bdm_status s;
-    if ((s = dalloc(&c->box_start, nslots + 1)) || (s = dalloc(&c->dense_list, nslots / 64 + 1))) {
+    if ((s = dalloc(&c->box_start, nslots + 1)) || (s = dalloc(&c->dense_list, 2 * (nslots / 64) + 2))) {
         c->slot_cap = 0;
         return s;
     }
@@ -649,7 +649,7 @@ bdm_status bdm_set_option(bdm_handle h, const char *name, int64_t value) {
     if (!h || !name) return fail(BDM_EINVAL, "NULL argument");
     Ctx *c = (Ctx *)h;
     if (strcmp(name, "mech_kernel") == 0) {
-        if (value < 0 || value > 3) return fail(BDM_EINVAL, "mech_kernel must be 0, 1, 2 or 3");
+        if (value < 0 || value > 4) return fail(BDM_EINVAL, "mech_kernel must be 0..4");
         c->mech_kernel = (int)value;
         return BDM_OK;
     }
@@ -705,7 +705,7 @@ bdm_status bdm_set_option(bdm_handle h, const char *name, int64_t value) {
         return BDM_OK;
     }
     if (strcmp(name, "prefilter") == 0) {
-        if (value < 0 || value > 1) return fail(BDM_EINVAL, "prefilter must be 0 or 1");
+        if (value < 0 || value > 15) return fail(BDM_EINVAL, "prefilter must be 0..15 (bit 0: on; bits 1-2: row-kernel debug paths)");
         c->prefilter = (int)value;
         return BDM_OK;
     }

@@ -104,7 +104,7 @@ struct Ctx {
     long long *n_new = nullptr;                        // growth/division: new agent count
     // grid
     uint32_t *box_start = nullptr;  // slot_cap + 1
-    uint32_t *dense_list = nullptr; // slot_cap / 64 + 1 tile ids (dense regions)
+    uint32_t *dense_list = nullptr; // 2 (slot_cap / 64) + 2 half-tile entries (dense regions)
     uint32_t *dense_scr = nullptr;  // dense kernel: per-warp octant-order scratch
     int64_t dense_scr_cap = 0;
     uint32_t *onco_id = nullptr;    // row f2: divider flags by id, then their ranks

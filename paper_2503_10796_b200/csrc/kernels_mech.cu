@@ -16,225 +16,9 @@
 #include <math.h>
 
 #include "bdm_internal.cuh"
+#include "mech_common.cuh"
 
 namespace bdm {
-
-struct MechArgs {
-    int64_t n;
-    const double *__restrict__ sx;
-    const double *__restrict__ sy;
-    const double *__restrict__ sz;
-    const double *__restrict__ sd;
-    const uint32_t *__restrict__ sid;
-    const uint32_t *__restrict__ skey;  // sorted blocked-Morton key (box of each sorted slot)
-    const uint32_t *__restrict__ sflags;
-    const uint32_t *__restrict__ box_start;
-    double *__restrict__ ox;
-    double *__restrict__ oy;
-    double *__restrict__ oz;
-    double *__restrict__ od;
-    uint32_t *__restrict__ oid;
-    uint32_t *__restrict__ oflags;
-    const uint32_t *__restrict__ lrank;  // nullable: output index of sorted local slots (ghosts)
-    const double *__restrict__ svol;  // nullable: volume travels with the agents
-    double *__restrict__ ovol;
-    uint32_t *__restrict__ dense_list;   // nullable: dense tiles go to k_mech_dense
-    uint32_t *__restrict__ dense_perm;   // dense kernel: kDScr entries of scratch per warp
-    double k, gamma, dt, max_disp, tau;
-    int detect_static, boundary, fuse;
-    double lo0, lo1, lo2, hi0, hi1, hi2;
-};
-
-__device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    return v;
-}
-
-// Grid scalars of the current step, read once per thread/CTA.
-struct GridView {
-    double L, R2, o0, o1, o2;
-    int D0, D1, D2, T0, T1, T2;
-    int b0, b1, b2;  // lattice offset (global frame, 8(e))
-    const uint16_t *hilb, *hilb_inv;  // tile numbering (NULL: row-major)
-};
-__device__ __forceinline__ GridView load_grid(const DevScalars *__restrict__ sc) {
-    GridView g;
-    g.L = sc->L; g.R2 = sc->R2; g.o0 = sc->o[0]; g.o1 = sc->o[1]; g.o2 = sc->o[2];
-    g.b0 = sc->boff[0]; g.b1 = sc->boff[1]; g.b2 = sc->boff[2];
-    g.D0 = sc->dims[0]; g.D1 = sc->dims[1]; g.D2 = sc->dims[2];
-    g.T0 = sc->T[0]; g.T1 = sc->T[1]; g.T2 = sc->T[2];
-    g.hilb = sc_hilb(sc);
-    g.hilb_inv = sc_hilb_inv(sc);
-    return g;
-}
-
-struct Counts {
-    uint32_t cand = 0, nbr = 0, cont = 0, stat = 0, moved = 0;
-    // extent of the new state (a1 of the next step, fused: option "fuse_reduce")
-    double lo0 = INFINITY, lo1 = INFINITY, lo2 = INFINITY;
-    double hi0 = -INFINITY, hi1 = -INFINITY, hi2 = -INFINITY, dmax = -INFINITY;
-};
-
-// a8 + a9 + write-back for one agent (shared by both kernels); s is the sorted slot,
-// the output goes to lrank[s] when ghosts are present.
-__device__ __forceinline__ void finish_agent(const MechArgs &A, int64_t s, double xi, double yi,
-                                             double zi, double Fx, double Fy, double Fz,
-                                             bool is_static, int nnz, Counts &c) {
-    const int64_t o = A.lrank ? (int64_t)A.lrank[s] : s;
-    double Dx = 0.0, Dy = 0.0, Dz = 0.0;
-    if (!is_static) {
-        const double F2 = Fx * Fx + Fy * Fy + Fz * Fz;
-        if (F2 > A.tau * A.tau) {
-            Dx = A.dt * Fx;
-            Dy = A.dt * Fy;
-            Dz = A.dt * Fz;
-            const double n2 = Dx * Dx + Dy * Dy + Dz * Dz;
-            if (n2 > A.max_disp * A.max_disp) {
-                const double scale = A.max_disp / sqrt(n2);
-                Dx = Dx * scale;
-                Dy = Dy * scale;
-                Dz = Dz * scale;
-            }
-        }
-    }
-    double nx = xi + Dx, ny = yi + Dy, nz = zi + Dz;
-    if (A.boundary == 1) {
-        nx = nx < A.lo0 ? A.lo0 : (nx > A.hi0 ? A.hi0 : nx);
-        ny = ny < A.lo1 ? A.lo1 : (ny > A.hi1 ? A.hi1 : ny);
-        nz = nz < A.lo2 ? A.lo2 : (nz > A.hi2 ? A.hi2 : nz);
-    }
-    const bool moved = (Dx != 0.0 || Dy != 0.0 || Dz != 0.0);
-    c.moved += moved ? 1u : 0u;
-    c.lo0 = fmin(c.lo0, nx); c.hi0 = fmax(c.hi0, nx);
-    c.lo1 = fmin(c.lo1, ny); c.hi1 = fmax(c.hi1, ny);
-    c.lo2 = fmin(c.lo2, nz); c.hi2 = fmax(c.hi2, nz);
-    c.dmax = fmax(c.dmax, A.sd[s]);
-    c.stat += is_static ? 1u : 0u;
-    A.ox[o] = nx;
-    A.oy[o] = ny;
-    A.oz[o] = nz;
-    A.od[o] = A.sd[s];
-    A.oid[o] = A.sid[s];
-    if (A.ovol) A.ovol[o] = A.svol[s];
-    A.oflags[o] = (moved ? BDM_FLAG_MOVED : 0u) | (is_static ? BDM_FLAG_STATIC : 0u) |
-                  ((uint32_t)nnz << BDM_FLAG_NNZ_SHIFT);
-}
-
-// The whole step for agent s of the sorted order, reading neighbours from global
-// memory (the reference formulation; used by k_mech and as the tile kernel's
-// fallback for over-full tiles).
-__device__ __forceinline__ void mech_agent_global(const MechArgs &A, const GridView &g, int64_t s,
-                                                  Counts &c) {
-    const uint32_t fi = A.sflags[s];
-    if (fi & kGhost) return;  // aura agents are read-only
-    const double xi = A.sx[s], yi = A.sy[s], zi = A.sz[s], di = A.sd[s];
-    const double ri = di * 0.5;
-    const int bx = (int)floor((xi - g.o0) / g.L) - g.b0;
-    const int by = (int)floor((yi - g.o1) / g.L) - g.b1;
-    const int bz = (int)floor((zi - g.o2) / g.L) - g.b2;
-    const int nnz_in = (int)((fi >> BDM_FLAG_NNZ_SHIFT) & 3u);
-
-    // ---- a5: static classification (pull test over the neighbours' flags)
-    bool is_static = false;
-    if (A.detect_static && !(fi & kChanged) && nnz_in <= 1) {
-        is_static = true;
-        for (int dz = -1; dz <= 1 && is_static; ++dz) {
-            const int cz = bz + dz;
-            if (cz < 0 || cz >= g.D2) continue;
-            for (int dy = -1; dy <= 1 && is_static; ++dy) {
-                const int cy = by + dy;
-                if (cy < 0 || cy >= g.D1) continue;
-                for (int dx = -1; dx <= 1 && is_static; ++dx) {
-                    const int cx = bx + dx;
-                    if (cx < 0 || cx >= g.D0) continue;
-                    const uint32_t key = box_key(cx, cy, cz, g.T0, g.T1, g.hilb);
-                    const uint32_t b0 = A.box_start[key], b1 = A.box_start[key + 1];
-                    for (uint32_t t = b0; t < b1; ++t) {
-                        if (t == (uint32_t)s) continue;
-                        const double ex = xi - A.sx[t], ey = yi - A.sy[t], ez = zi - A.sz[t];
-                        const double D = fma(ez, ez, fma(ey, ey, ex * ex));
-                        if (D <= g.R2 && (A.sflags[t] & kChanged)) {
-                            is_static = false;
-                            break;
-                        }
-                    }
-                }
-            }
-        }
-    }
-    double Fx = 0.0, Fy = 0.0, Fz = 0.0;
-    int nnz = nnz_in;
-    if (!is_static) {
-        // ---- a6 + a7: canonical order (dz, dy, dx), ascending id in a box
-        nnz = 0;
-        for (int dz = -1; dz <= 1; ++dz) {
-            const int cz = bz + dz;
-            if (cz < 0 || cz >= g.D2) continue;
-            for (int dy = -1; dy <= 1; ++dy) {
-                const int cy = by + dy;
-                if (cy < 0 || cy >= g.D1) continue;
-                for (int dx = -1; dx <= 1; ++dx) {
-                    const int cx = bx + dx;
-                    if (cx < 0 || cx >= g.D0) continue;
-                    const uint32_t key = box_key(cx, cy, cz, g.T0, g.T1, g.hilb);
-                    const uint32_t b0 = A.box_start[key], b1 = A.box_start[key + 1];
-                    for (uint32_t t = b0; t < b1; ++t) {
-                        if (t == (uint32_t)s) continue;
-                        ++c.cand;
-                        const double ex = xi - A.sx[t], ey = yi - A.sy[t], ez = zi - A.sz[t];
-                        const double D = fma(ez, ez, fma(ey, ey, ex * ex));
-                        if (!(D <= g.R2)) continue;
-                        ++c.nbr;
-                        const double dist = sqrt(D);
-                        const double rj = A.sd[t] * 0.5;
-                        const double delta = (ri + rj) - dist;
-                        if (!(delta > 0.0 && dist > 0.0)) continue;
-                        ++c.cont;
-                        const double rbar = (ri * rj) / (ri + rj);
-                        const double Fn = A.k * delta - A.gamma * sqrt(rbar * delta);
-                        const double sc_ = Fn / dist;
-                        Fx = fma(sc_, ex, Fx);
-                        Fy = fma(sc_, ey, Fy);
-                        Fz = fma(sc_, ez, Fz);
-                        if (Fn != 0.0 && nnz < 2) ++nnz;
-                    }
-                }
-            }
-        }
-    }
-    finish_agent(A, s, xi, yi, zi, Fx, Fy, Fz, is_static, nnz, c);
-}
-
-template <bool kStats>
-__device__ __forceinline__ void flush_counts(const Counts &c, DevScalars *sc, int fuse) {
-    if (fuse) {  // exact min/max of the new positions -> the next grid build's a1
-        double v[7] = {c.lo0, c.lo1, c.lo2, c.hi0, c.hi1, c.hi2, c.dmax};
-#pragma unroll
-        for (int q = 0; q < 7; ++q)
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                const double t = __shfl_xor_sync(0xffffffffu, v[q], o);
-                v[q] = q < 3 ? fmin(v[q], t) : fmax(v[q], t);
-            }
-        if ((threadIdx.x & 31) == 0) {
-            for (int q = 0; q < 3; ++q) atomicMin(&sc->enc_lo[q], enc_double(v[q]));
-            for (int q = 0; q < 3; ++q) atomicMax(&sc->enc_hi[q], enc_double(v[3 + q]));
-            atomicMax(&sc->enc_dmax, enc_double(v[6]));
-        }
-    }
-    if (!kStats) return;
-    const unsigned long long a = warp_sum_u64(c.cand), b = warp_sum_u64(c.nbr),
-                             d = warp_sum_u64(c.cont), e = warp_sum_u64(c.stat),
-                             f = warp_sum_u64(c.moved);
-    if ((threadIdx.x & 31) == 0) {
-        atomicAdd(&sc->stats[0], a);
-        atomicAdd(&sc->stats[1], b);
-        atomicAdd(&sc->stats[2], d);
-        atomicAdd(&sc->stats[3], e);
-        atomicAdd(&sc->stats[4], f);
-    }
-}
 
 // Thread per agent over global memory (reference formulation).
 template <bool kStats>
@@ -1113,9 +897,14 @@ __global__ void __launch_bounds__(kT6Threads, kMinBlocks) k_mech_tile6(MechArgs 
         __syncthreads();
         const int M = (int)S.off[kNB];
         if (M > kM6Max && S.use_pf && A.dense_list) {  // dense region: the dense-box kernel
-            if (tid == 0) {
-                A.dense_list[atomicAdd(&sc->n_dense, 1u)] = ta;
-                if (kTZ == 2 && tb != 0xFFFFFFFFu) A.dense_list[atomicAdd(&sc->n_dense, 1u)] = tb;
+            if (tid == 0) {  // entries are half tiles (tile << 1 | x-half), see k_mech_dense
+                const unsigned q = atomicAdd(&sc->n_dense, (kTZ == 2 && tb != 0xFFFFFFFFu) ? 4u : 2u);
+                A.dense_list[q] = ta << 1;
+                A.dense_list[q + 1] = (ta << 1) | 1u;
+                if (kTZ == 2 && tb != 0xFFFFFFFFu) {
+                    A.dense_list[q + 2] = tb << 1;
+                    A.dense_list[q + 3] = (tb << 1) | 1u;
+                }
             }
             __syncthreads();
             continue;
@@ -1336,7 +1125,9 @@ __global__ void __launch_bounds__(32 * kDWarps, 4) k_mech_dense(MechArgs A, DevS
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const unsigned lt_mask = (1u << lane) - 1u;
     DenseWarp &Wd = Sd[w];
-    const unsigned ntask = sc->n_dense * 64u;
+    // dense_list entries are half tiles: 4x4x4-box tile number << 1 | x-half (the 32
+    // boxes whose Morton bit 3, i.e. bx & 2, equals the half), one task per box
+    const unsigned ntask = sc->n_dense * 32u;
     if (ntask == 0) return;
     const GridView g = load_grid(sc);
     const float R2f = (float)(g.R2 * (1.0 + 0x1p-12));
@@ -1346,8 +1137,9 @@ __global__ void __launch_bounds__(32 * kDWarps, 4) k_mech_dense(MechArgs A, DevS
         if (lane == 0) item = atomicAdd(&sc->dense_next, 1u);
         item = __shfl_sync(0xffffffffu, item, 0);
         if (item >= ntask) break;
-        const int t = (int)A.dense_list[item >> 6];
-        const uint32_t mort = item & 63u;
+        const uint32_t ent = A.dense_list[item >> 5];
+        const int t = (int)(ent >> 1);
+        const uint32_t mort = (item & 7u) | ((ent & 1u) << 3) | (((item >> 3) & 3u) << 4);
         int tx, ty, tz;
         tile_xyz((uint32_t)t, g.T0, g.T1, g.hilb_inv, tx, ty, tz);
         const int bx = 4 * tx + (int)((mort & 1u) | ((mort >> 2) & 2u));
@@ -1762,7 +1554,7 @@ bdm_status launch_mech(Ctx *c, bdm_agents *a, const bdm_params *p, cudaStream_t 
     A.hi0 = p->hi[0]; A.hi1 = p->hi[1]; A.hi2 = p->hi[2];
     if (p->collect_stats)
         BDM_CUDA_TRY(cudaMemsetAsync(c->sc->stats, 0, sizeof(c->sc->stats), st));
-    const bool dense = c->dense && (c->mech_kernel == 0 || c->mech_kernel == 3);
+    const bool dense = c->dense && (c->mech_kernel == 0 || c->mech_kernel == 3 || c->mech_kernel == 4);
     A.dense_list = dense ? c->dense_list : nullptr;
     A.dense_perm = nullptr;
     BDM_CUDA_TRY(cudaMemsetAsync(&c->sc->n_dense, 0, 3 * sizeof(unsigned int), st));
@@ -1787,7 +1579,10 @@ bdm_status launch_mech(Ctx *c, bdm_agents *a, const bdm_params *p, cudaStream_t 
         tile6_per_sm<false, 4, false, 2>(c);
         tile6_per_sm<true, 4, false, 2>(c);
     }
-    if (c->mech_kernel == 0 && depth == 2) {  // sparse: two-tile units, 4 CTAs/SM
+    if (c->mech_kernel == 4) {  // row-broadcast tile kernel (kernels_row.cu)
+        const bdm_status s = launch_mech_row(c, A, p->collect_stats != 0, st);
+        if (s != BDM_OK) return s;
+    } else if (c->mech_kernel == 0 && depth == 2) {  // sparse: two-tile units, 4 CTAs/SM
         const bdm_status s = p->collect_stats ? launch_tile6<true, 4, false, 2>(c, A, st)
                                               : launch_tile6<false, 4, false, 2>(c, A, st);
         if (s != BDM_OK) return s;

@@ -50,7 +50,7 @@ def _cluster(orc, n_bg, side_bg, n_cl, side_cl, seed):
     return s
 
 
-@pytest.mark.parametrize("mech_kernel", [0, 1], ids=["tile", "reference"])
+@pytest.mark.parametrize("mech_kernel", [0, 1, 4], ids=["tile", "reference", "row"])
 @pytest.mark.parametrize("tile_order,sort_every", [(1, 1), (0, 3), (1, 0), (1, 2)])
 @pytest.mark.parametrize("pop", ["cfg2", "dense", "sparse"])
 def test_state_per_id_bit_exact(torch_cuda, orc, mech_kernel, tile_order, sort_every, pop):
@@ -72,7 +72,7 @@ def test_state_per_id_bit_exact(torch_cuda, orc, mech_kernel, tile_order, sort_e
     e = Engine(0, len(s["x"]))
     try:
         e.set_option("mech_kernel", mech_kernel)
-        e.set_option("fuse_reduce", 1 if mech_kernel == 0 else 0)
+        e.set_option("fuse_reduce", 0 if mech_kernel == 1 else 1)
         e.set_option("tile_order", tile_order)
         e.set_option("sort_every", sort_every)
         a = Agents.from_numpy(s)
