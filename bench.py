@@ -369,6 +369,7 @@ def run_ours(args, ws, rank, local):
     total_ms = start.elapsed_time(stop)
     grid_ms = [ev[k][0].elapsed_time(ev[k][1]) for k in range(K)]
     mech_ms = [ev[k][1].elapsed_time(ev[k][2]) for k in range(K)]
+    step_ms = [ev[k][0].elapsed_time(ev[k][2]) for k in range(K)]
     eng.step(a, pst, stream=stream)
     st_after = eng.stats()
     clocks = clk.summary()
@@ -421,6 +422,7 @@ def run_ours(args, ws, rank, local):
                           "hbm_term_ms": b_alg / hbm_peak * 1e3,
                           "fp64_term_ms": fp64_per_launch / fp64_peak * 1e3,
                           "hbm_peak_gbs": peaks["hbm_gbs"], "hbm_peak_source": peak_src},
+        "step_ms": _dist(step_ms),
         "clocks": clocks,
         "gpu_launches": launches,
     }
@@ -433,8 +435,16 @@ def run_ours(args, ws, rank, local):
     elif not args.no_e2e:
         line["e2e"] = measure_e2e(eng, cfg, params, stream)
     if not args.no_cpu_baseline and rank == 0 and ws == 1:
-        line["cpu_baseline"] = cpu_baseline()
+        line["cpu_baseline"] = cpu_baseline(cfg)
     print(json.dumps(line), flush=True)
+
+
+def _dist(ms):
+    """Per-step device times (CUDA events): mean, median, p90, min, max (ms)."""
+    v = sorted(ms)
+    return {"mean": statistics.mean(v), "median": statistics.median(v),
+            "p90": v[min(len(v) - 1, int(math.ceil(0.9 * len(v))) - 1)], "min": v[0], "max": v[-1],
+            "n": len(v)}
 
 
 def _common(metric_value, ms_step, ws, args, config, clocks, launches, dtype="f64"):
@@ -481,15 +491,76 @@ def run_cfg3(args, ws, rank, local):
             per_step.append((n0, e0.elapsed_time(e1)))
     total_agents = sum(n for n, _ in per_step)
     total_ms = sum(ms for _, ms in per_step)
+    launches = eng.stats()["launches"] - launches0
+    clocks = clk.summary()
+    # the same 20 steps again (deterministic: the same populations) with the work counters
+    # on, untimed, for each step's roofline; and the oracle on the host cores on the
+    # populations of the steps it finishes in seconds (N <= 4M)
+    peaks, src = _peaks()
+    sm_count = torch.cuda.get_device_properties(local).multi_processor_count
+    max_mhz = clocks["sm_max_mhz"] or peaks.get("sm_max_mhz", 1965.0)
+    fp64_peak = sm_count * 64 * max_mhz * 1e6
+    hbm_peak = peaks["hbm_gbs"] * 1e9
+    eng.init_spheres(a, cfg.n, seed=cfg.seed, side=cfg.side, d_lo=cfg.d_lo, stream=stream)
+    a.volume[:cfg.n].copy_((torch.pi / 6.0) * (a.diameter[:cfg.n] ** 3))
+    torch.cuda.synchronize()
+    pst = Params(seed=cfg.seed, dt=cfg.dt, max_displacement=cfg.max_disp, collect_stats=True)
+    rows, orc_rows = [], []
+    do_orc = not args.no_cpu_baseline and rank == 0
+    for t, (n_t, ms) in enumerate(per_step):
+        pst.step = t
+        if do_orc and a.n <= 4_000_000:
+            h = a.numpy()
+            orc_rows.append((a.n, _oracle_mech_time({k: h[k] for k in ("x", "y", "z", "d", "id", "flags")},
+                                                    cfg)))
+        eng.step(a, pst, stream=stream, sync=True)
+        st = eng.stats()
+        eng.grow_divide(a, pst, W.CFG3_GROWTH, W.CFG3_V_MAX, stream=stream)
+        fp64 = (FP64_PER_CAND * st["cand"] + FP64_PER_NBR * st["nbr"] + FP64_PER_CONT * st["cont"] +
+                FP64_PER_AGENT * n_t)
+        b_alg = (B_ALG_PER_AGENT + 16.0) * n_t    # + volume read and write (cfg3)
+        t_roof = max(b_alg / hbm_peak, fp64 / fp64_peak)
+        rows.append({"n": n_t, "ms": round(ms, 4), "t_roof_ms": round(t_roof * 1e3, 4),
+                     "frac": round(t_roof * 1e3 / ms, 4), "cand_per_agent": st["cand"] / n_t,
+                     "cont_per_agent": st["cont"] / n_t,
+                     "bound": "fp64" if fp64 / fp64_peak > b_alg / hbm_peak else "hbm"})
+    t_roof_total = sum(r["t_roof_ms"] for r in rows)
     line = _common(total_agents / (total_ms * 1e-3), total_ms / steps, ws, args,
                    {"workload": "cfg3 (configs[2])", "initial_agents": cfg.n,
-                    "final_agents": a.n, "steps": steps,
-                    "per_step": [{"n": n, "ms": round(ms, 4)} for n, ms in per_step],
+                    "final_agents": a.n, "steps": steps, "per_step": rows,
                     "l2": "inputs larger than L2 from step 1 (48 B/agent x >= 1M)"},
-                   clk.summary(), eng.stats()["launches"] - launches0)
-    line["roofline"] = None
-    line["note"] = "proliferation: per-step rate in config.per_step; dense late steps run the dense-box kernel"
+                   clocks, launches)
+    line["roofline"] = {"bound": "alu", "kernel": "whole step (grid + mechanics + division), per step",
+                        "t_roof_total_ms": t_roof_total, "t_total_ms": total_ms,
+                        "frac": t_roof_total / total_ms,
+                        "peak_source": f"fp64: {sm_count} SMs x 64 lanes x {max_mhz:.0f} MHz; "
+                                       f"HBM {peaks['hbm_gbs']} GB/s ({src})",
+                        "work": "fp64 term 7 cand + 3 nbr + 60 cont + 40 per agent; 88 B/agent"}
+    if orc_rows:
+        on = sum(n for n, _ in orc_rows)
+        ot = sum(t for _, (t, _) in orc_rows)
+        line["cpu_baseline"] = {"value": on / ot, "unit": UNIT, "kind": "oracle", **orc_rows[0][1][1],
+                                "sample": f"the oracle on all host cores, one whole step on each of "
+                                          f"the populations of steps 0-{len(orc_rows) - 1} "
+                                          f"(N = {orc_rows[0][0]} .. {orc_rows[-1][0]}; taken from the "
+                                          f"GPU run, which is bit-identical to the oracle's); the "
+                                          f"later, denser steps (up to {a.n} agents) are not run"}
+    line["note"] = "proliferation: per-step rate and roofline in config.per_step; dense late steps run the dense-box kernel"
     print(json.dumps(line), flush=True)
+
+
+def _oracle_mech_time(state, cfg):
+    """One whole oracle mechanics step of `state` on all host cores -> (s, describe)."""
+    import oracle
+    oracle.build()
+    p = oracle.mech_params(k=cfg.k, gamma=cfg.gamma, dt=cfg.dt, max_disp=cfg.max_disp,
+                           force_threshold=cfg.force_threshold, detect_static=cfg.detect_static)
+    orc = OracleAllCores(state, p)
+    try:
+        dt = orc.step()
+    finally:
+        orc.close()
+    return dt, orc.describe()
 
 
 def run_cfg4(args, ws, rank, local):
@@ -543,7 +614,31 @@ def run_cfg4(args, ws, rank, local):
                         "frac": ach / (peaks["hbm_gbs"] * 1e9),
                         **_traffic_keys(_traffic("k_sir_update", b_alg)),
                         "peak_source": src, "alg_bytes_per_agent": 50}
+    line["step_ms"] = _dist([evs[k].elapsed_time(evs[k + 1]) for k in range(K)])
+    if not args.no_cpu_baseline and rank == 0:
+        line["cpu_baseline"] = cpu_baseline_sir(a, cfg)
     print(json.dumps(line), flush=True)
+
+
+def cpu_baseline_sir(a, cfg, steps=3):
+    """The SIR oracle on all host cores, `steps` whole steps of the cfg4 population (the
+    GPU's current state copied to the host; each worker process updates a disjoint slice
+    of the agents with orc_sir_step_sample, which builds the infected index itself)."""
+    import numpy as np
+    import oracle
+    oracle.build()
+    n = a.n
+    s = {"x": a.x[:n].cpu().numpy(), "y": a.y[:n].cpu().numpy(), "z": a.z[:n].cpu().numpy(),
+         "state": a.state[:n].cpu().numpy(), "id": np.arange(n, dtype=np.uint32)}
+    orc = OracleAllCores(s, kind="sir", sir_cfg=cfg, bytes_per_agent=8.0)
+    try:
+        times = [orc.step(t) for t in range(steps)]
+    finally:
+        orc.close()
+    t = statistics.median(times)
+    return {"value": n / t, "unit": UNIT, "kind": "oracle", **orc.describe(),
+            "sample": f"{steps} whole oracle SIR steps of the cfg4 population ({n} agents), "
+                      f"agents split over {orc.workers} worker processes; median {t:.2f} s"}
 
 
 def _traffic(kernel, alg_bytes):
@@ -962,10 +1057,19 @@ def measure_e2e(eng, cfg, params, stream, steps: int = 7):
             "api": "bdm_step_host (C ABI, pinned host buffers, in place, sort_every 0)"}
 
 
-def cpu_baseline():
-    """cpu_baseline of the default line: one whole cfg2 step (10M agents) of the oracle
-    on all host cores."""
-    return cpu_baseline_mech(W.CFG2, steps=1)
+def cpu_baseline(cfg=W.CFG2):
+    """cpu_baseline of a mechanics line: whole oracle steps of the config on all host
+    cores (cfg1: 10 steps; cfg2: one 10M-agent step; cfg5: one step of a 10M-agent cube
+    of the cfg5 population, the 1.7B agents do not fit the host)."""
+    if cfg.name == "cfg5":
+        sub = W.MechConfig("cfg5 (10M-agent cube)", 10_000_000,
+                           W.side_for_fraction(10_000_000, 1000.0, 0.5), cfg.d_lo, 0.0, False,
+                           cfg.steps, cfg.detect_static)
+        return cpu_baseline_mech(sub, steps=1, note="; a 10M-agent cube of the cfg5 population "
+                                 "(same density and diameter) stands in for the 1.7B agents")
+    if cfg.name == "cfg1":
+        return cpu_baseline_mech(cfg, steps=10)
+    return cpu_baseline_mech(cfg, steps=1)
 
 
 def main():

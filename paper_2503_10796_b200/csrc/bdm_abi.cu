@@ -649,7 +649,7 @@ bdm_status bdm_set_option(bdm_handle h, const char *name, int64_t value) {
     if (!h || !name) return fail(BDM_EINVAL, "NULL argument");
     Ctx *c = (Ctx *)h;
     if (strcmp(name, "mech_kernel") == 0) {
-        if (value < 0 || value > 4) return fail(BDM_EINVAL, "mech_kernel must be 0..4");
+        if (value < 0 || value > 5) return fail(BDM_EINVAL, "mech_kernel must be 0..5");
         c->mech_kernel = (int)value;
         return BDM_OK;
     }

@@ -402,6 +402,9 @@ struct Warp6 {
             uint32_t ce[kC6Cap];            // the survivor entry; after 2b bits 24-25 = flags
                                             // (bit1 contact, bit0 F_N != 0)
         } b;
+        struct {
+            double sq[kQ6Cap];              // (tile7) s = F_N / dist per survivor
+        } c;
     } u;
     double ext[7];                          // fused extent: lo x,y,z, hi x,y,z, max d
     unsigned long long cnt[5];              // cand, nbr, cont, static, moved
@@ -781,7 +784,220 @@ __device__ __forceinline__ void tile6_batch(const MechArgs &A, const Tile6SmemT<
 }
 
 
-template <bool kStats, int kMinBlocks, bool kPair, int kTZ = 1>
+// Version 7 of the batch (option mech_kernel 5; the staging and tiles of k_mech_tile6):
+// the walk's conservative fp32 test is the contact test
+//       D32 <= min((r'_i + r'_j)^2, R2f),   r' = fl32(r + 2^-16 L)   (P.w)
+// for every lane that only needs its contacts (the force sum and nnz involve contacts
+// only), and the neighbour test D32 <= R2f for lanes that need the whole neighbour set
+// (static candidates: r'_i = inf; the counters: kStats).  Survivors are then (almost)
+// only contacts, and one lane-parallel pass does the exact fp64 test and Eq. 4.1/4.2 for
+// all of them (no separate compaction); phase 3 accumulates each lane's survivors in
+// order.  Conservative: each staged coordinate carries <= 2^-24 8 L = 2^-21 L of
+// rounding (|x - X0| <= 6L; 10L for two-tile units: 2^-20 L), so D32 <= (rho + sqrt(3)
+// 2^-19 L)^2 (1 + 2^-22); a counted contact has rho < (r_i + r_j)(1 + 2^-49) and rho <=
+// R(1 + 2^-50), while the threshold is >= (r_i + r_j + 2^-15 L)^2 (1 - 2^-21.4): at
+// least 8x margin whenever r_i + r_j <= L, and beyond that rho <= R bounds it.
+template <bool kStats, int kTZ>
+__device__ __forceinline__ void tile7_batch(const MechArgs &A, const Tile6SmemT<false, kTZ> &S,
+                                            Warp6 &Wp, int lane, uint32_t g0, int n0, uint32_t g1,
+                                            int klo, int na, int M, int sides) {
+    const float R2f = S.R2f, Lf = S.Lf;
+    const int k = klo + lane;
+    const uint32_t gk = k < n0 ? g0 + (uint32_t)k : g1 + (uint32_t)(k - n0);
+    int mi = M, nr = 0, walk = 0, ca = 0;
+    uint32_t fi = 0;
+    bool active = false, cand_static = false;
+    float4 pi = make_float4(-kSentinel, -kSentinel, -kSentinel, 0.f);
+    if (lane < na) {
+        mi = (int)S.kmi[k];
+        const int lbi = (int)S.mbox[mi];
+        fi = S.F[mi];
+        active = !(fi & kGhost);
+        if (active) {
+            cand_static = A.detect_static && !(fi & kChanged) && ((fi >> BDM_FLAG_NNZ_SHIFT) & 3u) <= 1u;
+            pi = S.f.P[mi];
+            if (cand_static) pi.w = INFINITY;  // whole neighbour set (a5 pull test)
+            const uint32_t v = S.lbxyz[lbi];
+            const int lx = (int)(v & 7u), ly = (int)((v >> 3) & 7u), lz = (int)((v >> 6) & 15u);
+            const float glx = pi.x - (float)lx * Lf, ghx = (float)(lx + 1) * Lf - pi.x;
+            const float gly = pi.y - (float)ly * Lf, ghy = (float)(ly + 1) * Lf - pi.y;
+            const float glz = pi.z - (float)lz * Lf, ghz = (float)(lz + 1) * Lf - pi.z;
+            const float gx2l = glx * glx, gx2h = ghx * ghx;
+            const float gy2[3] = {gly * gly, 0.f, ghy * ghy};
+            const float gz2[3] = {glz * glz, 0.f, ghz * ghz};
+#pragma unroll
+            for (int r = 0; r < 9; ++r) {
+                const int dzi = r / 3, dyi = r % 3;
+                const int row = lbi - 43 + dzi * 36 + dyi * 6;  // box (lx-1, ly-1+dyi, lz-1+dzi)
+                if (kStats) ca += (int)(S.off[row + 3] - S.off[row]);
+                const float b2 = gz2[dzi] + gy2[dyi];
+                const int xs = (b2 + gx2l <= R2f) ? 0 : 1;
+                const int xe = (b2 + gx2h <= R2f) ? 3 : 2;
+                const uint32_t rs = S.off[row + xs], re = S.off[row + xe];
+                const bool keep = b2 <= R2f && re > rs;
+                Wp.u.a.run[nr][lane] = (rs << 4) | (re << 20);
+                walk += keep ? (int)(re - rs) : 0;
+                nr += keep ? 1 : 0;
+            }
+        }
+    }
+    Wp.u.a.run[nr][lane] = ((uint32_t)M << 4) | (0xFFFFu << 16);  // sentinel run (see tile6)
+    Wp.chg[lane] = 0;
+    const int cmax = __reduce_max_sync(0xffffffffu, walk);
+    const unsigned cs_mask = __ballot_sync(0xffffffffu, cand_static);
+    __syncwarp();
+    // ---- phase 1: the flattened walk with the contact (or neighbour) test
+    int cnt = 0;
+    {
+        const char *pb = reinterpret_cast<const char *>(&S.f.P[0]);
+        const uint32_t mlast = (uint32_t)M << 4;
+        uint16_t *const lrow = &Wp.u.a.lst[0][lane];
+        const uint32_t *const rrow = &Wp.u.a.run[0][lane];
+        uint32_t cur = rrow[0];
+        uint32_t mo = cur & 0xFFFFu, eo = cur >> 16;
+        int j = 32;
+        uint32_t nxt = rrow[j];
+#pragma unroll 4
+        for (int it = 0; it < cmax; ++it) {
+            const float4 q = *reinterpret_cast<const float4 *>(pb + min(mo, mlast));
+            const float ex = pi.x - q.x, ey = pi.y - q.y, ez = pi.z - q.z;
+            const float d = fmaf(ez, ez, fmaf(ey, ey, ex * ex));
+            bool pass;
+            if (kStats) {
+                pass = d <= R2f;
+            } else {
+                const float sr = pi.w + q.w;
+                pass = d <= fminf(sr * sr, R2f);
+            }
+            lrow[cnt] = (uint16_t)mo;
+            cnt = min(cnt + (pass ? 32 : 0), 32 * kK6Max);
+            mo += 16;
+            if (mo == eo) {
+                mo = nxt & 0xFFFFu;
+                eo = nxt >> 16;
+                j += 32;
+            }
+            nxt = rrow[j];
+        }
+        cnt >>= 5;
+    }
+    int cincl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, cincl, o);
+        if (lane >= o) cincl += y;
+    }
+    const int my_off = cincl - cnt;
+    const int total = __shfl_sync(0xffffffffu, cincl, 31);
+    Counts c;
+    if (__any_sync(0xffffffffu, cnt >= kK6Max) || total > kQ6Cap) {
+        // a full list may have lost survivors: the reference formulation for the batch
+        if (active) mech_agent_global(A, S.g, gk, c);
+        merge_counts<kStats>(c, Wp, sides, lane);
+        return;
+    }
+    {
+        const uint32_t tag = ((uint32_t)mi << 9) | ((uint32_t)lane << 18);
+        const int cmx = __reduce_max_sync(0xffffffffu, cnt);
+        for (int jj = 0; jj < cmx; ++jj)
+            if (jj < cnt) Wp.pr[my_off + jj] = ((uint32_t)Wp.u.a.lst[jj][lane] >> 4) | tag;
+    }
+    __syncwarp();
+    const double R2 = S.g.R2;
+    // ---- a5 pull test, only for static candidates: exact neighbours with a changed flag
+    bool is_static = false;
+    if (cs_mask) {
+        for (int p = lane; p < total; p += 32) {
+            const uint32_t e = Wp.pr[p];
+            const int ow = (int)((e >> 18) & 31u);
+            if (!((cs_mask >> ow) & 1u)) continue;
+            const int m = (int)(e & 511u), mo = (int)((e >> 9) & 511u);
+            const double ex = S.X[mo] - S.X[m], ey = S.Y[mo] - S.Y[m], ez = S.Z[mo] - S.Z[m];
+            const double D = fma(ez, ez, fma(ey, ey, ex * ex));
+            if (D <= R2 && m != mo && (S.F[m] & kChanged)) Wp.chg[ow] = 1;
+        }
+        __syncwarp();
+        is_static = cand_static && !Wp.chg[lane];
+    }
+    const unsigned stat_mask = __ballot_sync(0xffffffffu, is_static);
+    // ---- phase 2: exact test + Eq. 4.1/4.2 for every survivor of a non-static owner,
+    // two per lane in straight-line code; s goes to u.b.sq, the flags (bit0 F_N != 0,
+    // bit1 contact, bit2 neighbour) to bits 24-26 of the entry
+    double *const sq = Wp.u.c.sq;
+    for (int p = lane; p < total; p += 64) {  // (u.a is no longer needed)
+        const int p2 = p + 32;
+        const bool h2 = p2 < total;
+        const uint32_t e1 = Wp.pr[p], e2 = h2 ? Wp.pr[p2] : e1;
+        const int m1 = (int)(e1 & 511u), mo1 = (int)((e1 >> 9) & 511u);
+        const int m2 = (int)(e2 & 511u), mo2 = (int)((e2 >> 9) & 511u);
+        const double ex1 = S.X[mo1] - S.X[m1], ey1 = S.Y[mo1] - S.Y[m1], ez1 = S.Z[mo1] - S.Z[m1];
+        const double ex2 = S.X[mo2] - S.X[m2], ey2 = S.Y[mo2] - S.Y[m2], ez2 = S.Z[mo2] - S.Z[m2];
+        const double D1 = fma(ez1, ez1, fma(ey1, ey1, ex1 * ex1));
+        const double D2 = fma(ez2, ez2, fma(ey2, ey2, ex2 * ex2));
+        const double ri1 = S.Rr[mo1], rj1 = S.Rr[m1], ri2 = S.Rr[mo2], rj2 = S.Rr[m2];
+        const bool w1 = !((stat_mask >> ((e1 >> 18) & 31u)) & 1u);
+        const bool w2 = !((stat_mask >> ((e2 >> 18) & 31u)) & 1u);
+        const bool nb1 = D1 <= R2 && m1 != mo1, nb2 = D2 <= R2 && m2 != mo2;
+        // non-contacts (the agent itself, D = 0, overlap <= 0) run on harmless stand-in
+        // operands: no NaN or zero reaches the IEEE sqrt/div, so they stay on their fast
+        // paths; every contact sees exactly its own operands (the results are discarded
+        // otherwise)
+        const double dist1 = sqrt(nb1 && D1 > 0.0 ? D1 : 1.0), dist2 = sqrt(nb2 && D2 > 0.0 ? D2 : 1.0);
+        const double del1 = (ri1 + rj1) - dist1, del2 = (ri2 + rj2) - dist2;
+        const bool c1 = w1 && nb1 && D1 > 0.0 && del1 > 0.0;
+        const bool c2 = w2 && nb2 && D2 > 0.0 && del2 > 0.0;
+        const double dl1 = c1 ? del1 : 1.0, dl2 = c2 ? del2 : 1.0;
+        const double rs1 = ri1 + rj1, rs2 = ri2 + rj2;  // > 0 for a contact
+        const double rb1 = (ri1 * rj1) / (rs1 > 0.0 ? rs1 : 1.0), rb2 = (ri2 * rj2) / (rs2 > 0.0 ? rs2 : 1.0);
+        const double q1 = rb1 * dl1, q2 = rb2 * dl2;
+        const double Fn1 = A.k * dl1 - A.gamma * (q1 > 0.0 ? sqrt(q1) : 0.0);
+        const double Fn2 = A.k * dl2 - A.gamma * (q2 > 0.0 ? sqrt(q2) : 0.0);
+        const double s1 = Fn1 / dist1, s2 = Fn2 / dist2;
+        const uint32_t f1 = (nb1 ? 4u : 0u) | (c1 ? (2u | (Fn1 != 0.0 ? 1u : 0u)) : 0u);
+        const uint32_t f2 = (nb2 ? 4u : 0u) | (c2 ? (2u | (Fn2 != 0.0 ? 1u : 0u)) : 0u);
+        sq[p] = c1 ? s1 : 0.0;
+        Wp.pr[p] = (e1 & 0x00FFFFFFu) | (f1 << 24);
+        if (h2) {
+            sq[p2] = c2 ? s2 : 0.0;
+            Wp.pr[p2] = (e2 & 0x00FFFFFFu) | (f2 << 24);
+        }
+    }
+    __syncwarp();
+    // ---- phase 3: ordered accumulation of the own survivors (a non-contact has s = 0:
+    // fma(0, d, F) == F exactly, F never is -0)
+    if (active) {
+        const double xi = S.X[mi], yi = S.Y[mi], zi = S.Z[mi];
+        double Fx = 0.0, Fy = 0.0, Fz = 0.0;
+        int nnz = 0;
+        uint32_t my_cont = 0, my_nbr = 0;
+#pragma unroll 2
+        for (int q = my_off; q < my_off + cnt; ++q) {
+            const uint32_t ev = Wp.pr[q];
+            const int m = (int)(ev & 511u);
+            const double s_ = sq[q];
+            Fx = fma(s_, xi - S.X[m], Fx);
+            Fy = fma(s_, yi - S.Y[m], Fy);
+            Fz = fma(s_, zi - S.Z[m], Fz);
+            nnz += (int)((ev >> 24) & 1u);
+            my_cont += (ev >> 25) & 1u;
+            my_nbr += (ev >> 26) & 1u;
+        }
+        nnz = nnz < 2 ? nnz : 2;
+        if (!is_static) {
+            if (kStats) {
+                c.cand += (uint32_t)(ca - 1);
+                c.nbr += my_nbr;
+                c.cont += my_cont;
+            }
+        } else {
+            nnz = (int)((fi >> BDM_FLAG_NNZ_SHIFT) & 3u);
+        }
+        finish_agent(A, gk, xi, yi, zi, Fx, Fy, Fz, is_static, nnz, c);
+    }
+    merge_counts<kStats>(c, Wp, sides, lane);
+}
+
+template <bool kStats, int kMinBlocks, bool kPair, int kTZ = 1, bool kV7 = false>
 __global__ void __launch_bounds__(kT6Threads, kMinBlocks) k_mech_tile6(MechArgs A, DevScalars *__restrict__ sc,
                                                                       int allow_prefilter) {
     if (sc->overflow) return;
@@ -940,6 +1156,7 @@ __global__ void __launch_bounds__(kT6Threads, kMinBlocks) k_mech_tile6(MechArgs 
             const double L = S.g.L;
             const double X0 = S.g.o0 + (double)(bx0 + S.g.b0) * L, Y0 = S.g.o1 + (double)(by0 + S.g.b1) * L,
                          Z0 = S.g.o2 + (double)(bz0 + S.g.b2) * L;
+            const double hpad = 0x1p-16 * L;  // r' pad of the tile7 contact prefilter
             for (int m = tid; m < M; m += kT6Threads) {
                 const int lb = S.mbox[m];
                 const uint32_t gi = S.start[lb] + ((uint32_t)m - S.off[lb]);
@@ -962,7 +1179,7 @@ __global__ void __launch_bounds__(kT6Threads, kMinBlocks) k_mech_tile6(MechArgs 
                         zz[2 * (m - 1) + 1] = zr;
                     }
                 } else {
-                    S.f.P[m] = make_float4(xr, yr, zr, 0.f);
+                    S.f.P[m] = make_float4(xr, yr, zr, (float)(d * 0.5 + hpad));
                 }
             }
         }
@@ -1001,7 +1218,10 @@ __global__ void __launch_bounds__(kT6Threads, kMinBlocks) k_mech_tile6(MechArgs 
             // and the fp32 quotient (bb nc < 2^24) floors exactly
             const int klo = (int)__fdividef((float)(bb * nc), (float)B);
             const int khi = (int)__fdividef((float)((bb + 1) * nc), (float)B);
-            tile6_batch<kStats, kPair, kTZ>(A, S, S.W[w], lane, g0, n0, g1, klo, khi - klo, M, sides);
+            if constexpr (kV7 && !kPair)
+                tile7_batch<kStats, kTZ>(A, S, S.W[w], lane, g0, n0, g1, klo, khi - klo, M, sides);
+            else
+                tile6_batch<kStats, kPair, kTZ>(A, S, S.W[w], lane, g0, n0, g1, klo, khi - klo, M, sides);
         }
         __syncthreads();  // before the next tile overwrites the staged region
     }
@@ -1017,17 +1237,17 @@ __global__ void __launch_bounds__(kT6Threads, kMinBlocks) k_mech_tile6(MechArgs 
 
 // One-time per-device setup of a tile-kernel instance (shared-memory attribute, CTAs
 // per SM); returns the CTAs per SM.
-template <bool kStats, int kMinBlocks, bool kPair, int kTZ>
+template <bool kStats, int kMinBlocks, bool kPair, int kTZ, bool kV7 = false>
 static int tile6_per_sm(Ctx *c) {
     static int per_sm_dev[kMaxDevices] = {};
     int &per_sm = per_sm_dev[c->device];
     if (!per_sm) {
         const int smem = (int)sizeof(Tile6SmemT<kPair, kTZ>);
         int v = 0;
-        if (cudaFuncSetAttribute(k_mech_tile6<kStats, kMinBlocks, kPair, kTZ>,
+        if (cudaFuncSetAttribute(k_mech_tile6<kStats, kMinBlocks, kPair, kTZ, kV7>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess ||
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-                &v, k_mech_tile6<kStats, kMinBlocks, kPair, kTZ>, kT6Threads, smem) != cudaSuccess) {
+                &v, k_mech_tile6<kStats, kMinBlocks, kPair, kTZ, kV7>, kT6Threads, smem) != cudaSuccess) {
             cudaGetLastError();
             return 0;
         }
@@ -1036,15 +1256,15 @@ static int tile6_per_sm(Ctx *c) {
     return per_sm;
 }
 
-template <bool kStats, int kMinBlocks, bool kPair, int kTZ = 1>
+template <bool kStats, int kMinBlocks, bool kPair, int kTZ = 1, bool kV7 = false>
 static bdm_status launch_tile6(Ctx *c, const MechArgs &A, cudaStream_t st) {
-    const int per_sm = tile6_per_sm<kStats, kMinBlocks, kPair, kTZ>(c);
+    const int per_sm = tile6_per_sm<kStats, kMinBlocks, kPair, kTZ, kV7>(c);
     if (!per_sm) {
         set_error("tile kernel setup failed");
         return BDM_ECUDA;
     }
     const int smem = (int)sizeof(Tile6SmemT<kPair, kTZ>);
-    k_mech_tile6<kStats, kMinBlocks, kPair, kTZ>
+    k_mech_tile6<kStats, kMinBlocks, kPair, kTZ, kV7>
         <<<(unsigned)(c->sm_count * per_sm), kT6Threads, smem, st>>>(A, c->sc, c->prefilter);
     return BDM_OK;
 }
@@ -1554,7 +1774,7 @@ bdm_status launch_mech(Ctx *c, bdm_agents *a, const bdm_params *p, cudaStream_t 
     A.hi0 = p->hi[0]; A.hi1 = p->hi[1]; A.hi2 = p->hi[2];
     if (p->collect_stats)
         BDM_CUDA_TRY(cudaMemsetAsync(c->sc->stats, 0, sizeof(c->sc->stats), st));
-    const bool dense = c->dense && (c->mech_kernel == 0 || c->mech_kernel == 3 || c->mech_kernel == 4);
+    const bool dense = c->dense && (c->mech_kernel == 0 || c->mech_kernel >= 3);
     A.dense_list = dense ? c->dense_list : nullptr;
     A.dense_perm = nullptr;
     BDM_CUDA_TRY(cudaMemsetAsync(&c->sc->n_dense, 0, 3 * sizeof(unsigned int), st));
@@ -1573,13 +1793,27 @@ bdm_status launch_mech(Ctx *c, bdm_agents *a, const bdm_params *p, cudaStream_t 
     const double dens = c->hint_density > 0.0 ? c->hint_density : c->density_hint;
     const int depth = c->tile_depth != 0 ? c->tile_depth
                       : (dens > 0.0 && dens <= kSparseDensity ? 2 : 1);
+    if (c->tile_depth == 0 && c->mech_kernel == 5) {  // auto may switch: set both up now
+        tile6_per_sm<false, 5, false, 1, true>(c);
+        tile6_per_sm<true, 5, false, 1, true>(c);
+        tile6_per_sm<false, 4, false, 2, true>(c);
+        tile6_per_sm<true, 4, false, 2, true>(c);
+    }
     if (c->tile_depth == 0 && c->mech_kernel == 0) {  // auto may switch: set both up now
         tile6_per_sm<false, 5, false, 1>(c);
         tile6_per_sm<true, 5, false, 1>(c);
         tile6_per_sm<false, 4, false, 2>(c);
         tile6_per_sm<true, 4, false, 2>(c);
     }
-    if (c->mech_kernel == 4) {  // row-broadcast tile kernel (kernels_row.cu)
+    if (c->mech_kernel == 5 && depth == 2) {  // tile7 batches (contact prefilter), two-tile units
+        const bdm_status s = p->collect_stats ? launch_tile6<true, 4, false, 2, true>(c, A, st)
+                                              : launch_tile6<false, 4, false, 2, true>(c, A, st);
+        if (s != BDM_OK) return s;
+    } else if (c->mech_kernel == 5) {  // tile7 batches (contact prefilter)
+        const bdm_status s = p->collect_stats ? launch_tile6<true, 5, false, 1, true>(c, A, st)
+                                              : launch_tile6<false, 5, false, 1, true>(c, A, st);
+        if (s != BDM_OK) return s;
+    } else if (c->mech_kernel == 4) {  // row-broadcast tile kernel (kernels_row.cu)
         const bdm_status s = launch_mech_row(c, A, p->collect_stats != 0, st);
         if (s != BDM_OK) return s;
     } else if (c->mech_kernel == 0 && depth == 2) {  // sparse: two-tile units, 4 CTAs/SM

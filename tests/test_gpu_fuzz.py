@@ -21,7 +21,7 @@ def engines():
         pytest.skip("no GPU")
     from paper_2503_10796_b200 import Engine
     es = {}
-    for k in (0, 1, 4):
+    for k in (0, 1, 4, 5):
         e = Engine(0, 1 << 13)
         e.set_option("mech_kernel", k)
         es[k] = e

@@ -16,8 +16,10 @@ pytestmark = pytest.mark.gpu
 REL_TOL = 1e-9  # north_star tolerance for fp64 positions
 
 
-@pytest.fixture(scope="module", params=[(0, 1), (1, 1), (2, 1), (3, 1), (0, 2), (0, 0), (4, 0)],
-                ids=["tile", "reference", "tile_v1", "tile_4cta", "tile_depth2", "tile_auto", "row"])
+@pytest.fixture(scope="module", params=[(0, 1), (1, 1), (2, 1), (3, 1), (0, 2), (0, 0), (4, 0),
+                                        (5, 1), (5, 2)],
+                ids=["tile", "reference", "tile_v1", "tile_4cta", "tile_depth2", "tile_auto", "row",
+                     "tile7", "tile7_depth2"])
 def eng(request):
     """Every mechanics kernel: the tile kernel (default; also with two-tile work units,
     option tile_depth 2), the per-agent reference and the other tile variants."""

@@ -50,7 +50,7 @@ def _cluster(orc, n_bg, side_bg, n_cl, side_cl, seed):
     return s
 
 
-@pytest.mark.parametrize("mech_kernel", [0, 1, 4], ids=["tile", "reference", "row"])
+@pytest.mark.parametrize("mech_kernel", [0, 1, 4, 5], ids=["tile", "reference", "row", "tile7"])
 @pytest.mark.parametrize("tile_order,sort_every", [(1, 1), (0, 3), (1, 0), (1, 2)])
 @pytest.mark.parametrize("pop", ["cfg2", "dense", "sparse"])
 def test_state_per_id_bit_exact(torch_cuda, orc, mech_kernel, tile_order, sort_every, pop):
