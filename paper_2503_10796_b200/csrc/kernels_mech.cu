@@ -784,6 +784,45 @@ __device__ __forceinline__ void tile6_batch(const MechArgs &A, const Tile6SmemT<
 }
 
 
+// The flattened walk of one lane over its trimmed runs (see tile7_batch); returns the
+// number of survivors, listed (byte offsets m << 4) in Wp.u.a.lst[.][lane].
+template <bool kStats, bool kMin, int kTZ>
+__device__ __forceinline__ int tile7_walk(const Tile6SmemT<false, kTZ> &S, Warp6 &Wp, int lane,
+                                          float4 pi, int cmax, int M, float R2f) {
+    int cnt = 0;
+    const char *pb = reinterpret_cast<const char *>(&S.f.P[0]);
+    const uint32_t mlast = (uint32_t)M << 4;
+    uint16_t *const lrow = &Wp.u.a.lst[0][lane];
+    const uint32_t *const rrow = &Wp.u.a.run[0][lane];
+    uint32_t cur = rrow[0];
+    uint32_t mo = cur & 0xFFFFu, eo = cur >> 16;
+    int j = 32;
+    uint32_t nxt = rrow[j];
+#pragma unroll 4
+    for (int it = 0; it < cmax; ++it) {
+        const float4 q = *reinterpret_cast<const float4 *>(pb + min(mo, mlast));
+        const float ex = pi.x - q.x, ey = pi.y - q.y, ez = pi.z - q.z;
+        const float d = fmaf(ez, ez, fmaf(ey, ey, ex * ex));
+        bool pass;
+        if (kStats) {
+            pass = d <= R2f;
+        } else {
+            const float sr = pi.w + q.w;
+            pass = kMin ? d <= fminf(sr * sr, R2f) : d <= sr * sr;
+        }
+        lrow[cnt] = (uint16_t)mo;
+        cnt = min(cnt + (pass ? 32 : 0), 32 * kK6Max);
+        mo += 16;
+        if (mo == eo) {
+            mo = nxt & 0xFFFFu;
+            eo = nxt >> 16;
+            j += 32;
+        }
+        nxt = rrow[j];
+    }
+    return cnt >> 5;
+}
+
 // Version 7 of the batch (option mech_kernel 5; the staging and tiles of k_mech_tile6):
 // the walk's conservative fp32 test is the contact test
 //       D32 <= min((r'_i + r'_j)^2, R2f),   r' = fl32(r + 2^-16 L)   (P.w)
@@ -846,41 +885,11 @@ __device__ __forceinline__ void tile7_batch(const MechArgs &A, const Tile6SmemT<
     const int cmax = __reduce_max_sync(0xffffffffu, walk);
     const unsigned cs_mask = __ballot_sync(0xffffffffu, cand_static);
     __syncwarp();
-    // ---- phase 1: the flattened walk with the contact (or neighbour) test
-    int cnt = 0;
-    {
-        const char *pb = reinterpret_cast<const char *>(&S.f.P[0]);
-        const uint32_t mlast = (uint32_t)M << 4;
-        uint16_t *const lrow = &Wp.u.a.lst[0][lane];
-        const uint32_t *const rrow = &Wp.u.a.run[0][lane];
-        uint32_t cur = rrow[0];
-        uint32_t mo = cur & 0xFFFFu, eo = cur >> 16;
-        int j = 32;
-        uint32_t nxt = rrow[j];
-#pragma unroll 4
-        for (int it = 0; it < cmax; ++it) {
-            const float4 q = *reinterpret_cast<const float4 *>(pb + min(mo, mlast));
-            const float ex = pi.x - q.x, ey = pi.y - q.y, ez = pi.z - q.z;
-            const float d = fmaf(ez, ez, fmaf(ey, ey, ex * ex));
-            bool pass;
-            if (kStats) {
-                pass = d <= R2f;
-            } else {
-                const float sr = pi.w + q.w;
-                pass = d <= fminf(sr * sr, R2f);
-            }
-            lrow[cnt] = (uint16_t)mo;
-            cnt = min(cnt + (pass ? 32 : 0), 32 * kK6Max);
-            mo += 16;
-            if (mo == eo) {
-                mo = nxt & 0xFFFFu;
-                eo = nxt >> 16;
-                j += 32;
-            }
-            nxt = rrow[j];
-        }
-        cnt >>= 5;
-    }
+    // ---- phase 1: the flattened walk with the contact (or neighbour) test; the min with
+    // R2f only matters for static candidates (r'_i = inf), so warps without one skip it
+    int cnt = cs_mask ? tile7_walk<kStats, true, kTZ>(S, Wp, lane, pi, cmax, M, R2f)
+                      : tile7_walk<kStats, false, kTZ>(S, Wp, lane, pi, cmax, M, R2f);
+    if (active) --cnt;  // the agent itself (D32 = 0) is always among the survivors
     int cincl = cnt;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -890,7 +899,7 @@ __device__ __forceinline__ void tile7_batch(const MechArgs &A, const Tile6SmemT<
     const int my_off = cincl - cnt;
     const int total = __shfl_sync(0xffffffffu, cincl, 31);
     Counts c;
-    if (__any_sync(0xffffffffu, cnt >= kK6Max) || total > kQ6Cap) {
+    if (__any_sync(0xffffffffu, cnt >= kK6Max - 1) || total > kQ6Cap) {
         // a full list may have lost survivors: the reference formulation for the batch
         if (active) mech_agent_global(A, S.g, gk, c);
         merge_counts<kStats>(c, Wp, sides, lane);
@@ -898,9 +907,13 @@ __device__ __forceinline__ void tile7_batch(const MechArgs &A, const Tile6SmemT<
     }
     {
         const uint32_t tag = ((uint32_t)mi << 9) | ((uint32_t)lane << 18);
-        const int cmx = __reduce_max_sync(0xffffffffu, cnt);
-        for (int jj = 0; jj < cmx; ++jj)
-            if (jj < cnt) Wp.pr[my_off + jj] = ((uint32_t)Wp.u.a.lst[jj][lane] >> 4) | tag;
+        const uint32_t self = (uint32_t)mi << 4;
+        const int cmx = __reduce_max_sync(0xffffffffu, active ? cnt + 1 : cnt);
+        int wo = my_off;
+        for (int jj = 0; jj < cmx; ++jj) {
+            const uint32_t v = Wp.u.a.lst[jj][lane];
+            if (jj < (active ? cnt + 1 : cnt) && v != self) Wp.pr[wo++] = (v >> 4) | tag;
+        }
     }
     __syncwarp();
     const double R2 = S.g.R2;
