@@ -244,7 +244,7 @@ def run_reference(args, ws, rank):
     """--impl reference: the CPU oracle (as it stands) on all host cores (rank 0 only),
     on cfg2, the metric's workload.  Each step is one whole oracle step of a cube of the
     cfg2 population (same density, diameter mix, static skip) whose size is chosen so the
-    --steps K --warmup W run ends in about two and a half minutes."""
+    --steps K --warmup W run ends in about --ref-budget seconds (150 by default)."""
     if rank != 0:
         return
     import oracle
@@ -258,7 +258,7 @@ def run_reference(args, ws, rank):
     finally:
         orc.close()
     per_agent = t_cal / cal_n
-    n = int(min(W.CFG2.n, max(200_000, 150.0 / ((steps + warm) * per_agent))))
+    n = int(min(W.CFG2.n, max(200_000, args.ref_budget / ((steps + warm) * per_agent))))
     cfg = W.cfg2_scaled(n) if n < W.CFG2.n else W.CFG2
     orc = OracleAllCores(_mech_state(cfg), oracle.mech_params(detect_static=True))
     try:
@@ -436,6 +436,16 @@ def run_ours(args, ws, rank, local):
         line["e2e"] = measure_e2e(eng, cfg, params, stream)
     if not args.no_cpu_baseline and rank == 0 and ws == 1:
         line["cpu_baseline"] = cpu_baseline(cfg)
+    if cfg.name == "cfg2" and args.strong_steps > 0:
+        # T_1 of the strong-scaled cfg5 (1.7B agents on this one GPU), for S_N = T_1 / T_N
+        eng.close()
+        del a, eng
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
+        try:
+            line["strong_cfg5"] = _slab_phase(args, 1, 0, local, True, args.strong_steps, 2)
+        except Exception as e:  # noqa: BLE001 (reported in the line)
+            line["strong_cfg5"] = {"error": f"{type(e).__name__}: {e}"[:300]}
     print(json.dumps(line), flush=True)
 
 
@@ -911,35 +921,15 @@ def _onco_ages(n, seed, max_age):
     return torch.from_numpy(age)
 
 
-def run_slabs(args, ws, rank, local):
-    """x-slab decomposition over N GPUs.  Default: weak scaling with the
-    cfg2 workload per GPU (10M agents in one cfg2 cube per slab, slabs side by side in
-    x); --config cfg5: the 1.7B-agent cube split into N slabs (strong scaling)."""
+def _slab_population(eng, a, cfg, strong, ws, rank, lo, hi, stream):
+    """This rank's agents: (strong) the slab's share of the one cfg5 cube, every rank
+    drawing the same per-id population (A48); (weak) one cfg2 cube per rank, shifted
+    to the rank's x-slab."""
     import torch
-    import torch.distributed as dist
-    from paper_2503_10796_b200 import Agents, Engine, Params
-    from paper_2503_10796_b200.slabs import DistTransport, LibOps, Slab, SlabDomain
-    torch.cuda.set_device(local)
-    if ws > 1 and not dist.is_initialized():
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    strong = args.config == "cfg5"
-    cfg = W.CFG5 if strong else W.CFG2
-    if strong:
-        n_local_est = cfg.n // ws
-        side_x = cfg.side
-    else:
-        n_local_est = cfg.n
-        side_x = cfg.side * ws
-    lo = -math.inf if rank == 0 else rank * side_x / ws
-    hi = math.inf if rank == ws - 1 else (rank + 1) * side_x / ws
-    cap = int(n_local_est * 1.15) + 4096
-    eng = Engine(local, cap)
-    a = Agents.empty(cap)
-    # the library runs on torch's current stream, the one NCCL and the payload copies
-    # of DistTransport are ordered with (a side stream would race with them)
-    stream = torch.cuda.current_stream(local)
-    if strong:
-        # every rank draws the same per-id population and keeps its slab (A48)
+    from paper_2503_10796_b200 import Agents
+    if strong and ws == 1:  # the whole cube on one GPU (178 GB: no staging buffer)
+        eng.init_spheres(a, cfg.n, seed=cfg.seed, side=cfg.side, d_lo=cfg.d_lo, stream=stream)
+    elif strong:
         chunk = 50_000_000
         tmp = Agents.empty(chunk)
         a.n = 0
@@ -948,12 +938,18 @@ def run_slabs(args, ws, rank, local):
             eng.init_spheres(tmp, m, id0=id0, seed=cfg.seed, side=cfg.side, d_lo=cfg.d_lo,
                              stream=stream)
             torch.cuda.synchronize()
-            sel = (tmp.x[:m] >= lo) & (tmp.x[:m] < hi)
-            k = int(sel.sum())
+            if ws == 1:
+                sel = None
+                k = m
+            else:
+                sel = (tmp.x[:m] >= lo) & (tmp.x[:m] < hi)
+                k = int(sel.sum())
             for f in ("x", "y", "z", "diameter", "id", "flags"):
-                getattr(a, f)[a.n:a.n + k].copy_(getattr(tmp, f)[:m][sel])
+                src = getattr(tmp, f)[:m] if sel is None else getattr(tmp, f)[:m][sel]
+                getattr(a, f)[a.n:a.n + k].copy_(src)
             a.n += k
         del tmp
+        torch.cuda.empty_cache()
     else:
         eng.init_spheres(a, cfg.n, id0=rank * cfg.n, seed=cfg.seed, side=cfg.side,
                          d_lo=cfg.d_lo, d_width=cfg.d_width, d_random=cfg.d_random,
@@ -961,6 +957,181 @@ def run_slabs(args, ws, rank, local):
         torch.cuda.synchronize()
         a.x[:cfg.n] += rank * cfg.side
     torch.cuda.synchronize()
+
+
+def _slab_phase(args, ws, rank, local, strong, steps, warmup):
+    """One x-slab measurement through the C-ABI exchange (bdm_aura_exchange over NCCL,
+    or the plain step on one GPU): device time per step (max over ranks), the exchange
+    share, and the work counters of one step for the roofline."""
+    import torch
+    import torch.distributed as dist
+    from paper_2503_10796_b200 import Agents, Engine, Params
+    from paper_2503_10796_b200.slabs import NativeSlabDomain
+    cfg = W.CFG5 if strong else W.CFG2
+    side_x = cfg.side if strong else cfg.side * ws
+    lo = -math.inf if rank == 0 else rank * side_x / ws
+    hi = math.inf if rank == ws - 1 else (rank + 1) * side_x / ws
+    n_est = cfg.n // ws if strong else cfg.n
+    cap = n_est + 4096 if strong and ws == 1 else int(n_est * 1.15) + 4096
+    eng = Engine(local, cap)
+    eng.set_option("mech_kernel", args.mech_kernel)
+    a = Agents.empty(cap)
+    stream = torch.cuda.current_stream(local)
+    _slab_population(eng, a, cfg, strong, ws, rank, lo, hi, stream)
+    params = Params(k=cfg.k, gamma=cfg.gamma, dt=cfg.dt, max_displacement=cfg.max_disp,
+                    detect_static=cfg.detect_static)
+    uid = None
+    if ws > 1:
+        obj = [eng.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        uid = obj[0]
+        dom = NativeSlabDomain([eng], [a], [(lo, hi)], params, stream=stream, uid=uid, rank=rank,
+                               nranks=ws, ghost_capacity=int(0.02 * n_est) + 65536)
+    else:
+        dom = None
+    eng.step(a, params, stream=stream, sync=True)  # sizes the grid
+    gi = eng.grid_info()
+    T = [(d + 3) // 4 + 8 for d in gi["dims"]]
+    eng.reserve(0, T[0] * T[1] * T[2] * 64)
+    for _ in range(warmup):
+        if dom:
+            dom.step()
+        else:
+            eng.step(a, params, stream=stream)
+    pst = Params(**{**params.__dict__, "collect_stats": True})
+    if dom:
+        dom.exchange()
+        eng.grid_build(a, params.radius, stream=stream, ghosts=dom.ghosts[0] if dom.ghosts[0].n else None)
+        eng.mech_step(a, pst, stream=stream)
+    else:
+        eng.step(a, pst, stream=stream)
+    eng.sync(stream)
+    st = eng.stats()
+    n_loc = a.n
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(steps)]
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = eng.stats()["launches"]
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for k in range(steps):
+            ev[k][0].record(stream)
+            if dom:
+                dom.exchange()
+            ev[k][1].record(stream)
+            g = dom.ghosts[0] if dom and dom.ghosts[0].n else None
+            eng.grid_build(a, params.radius, stream=stream, ghosts=g)
+            eng.mech_step(a, params, stream=stream)
+            ev[k][2].record(stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    eng.sync(stream)
+    x_ms = sum(ev[k][0].elapsed_time(ev[k][1]) for k in range(steps)) / steps
+    c_ms = sum(ev[k][1].elapsed_time(ev[k][2]) for k in range(steps)) / steps
+    vals = torch.tensor([e0.elapsed_time(e1) / steps, x_ms, c_ms, float(n_loc)],
+                        dtype=torch.float64, device="cuda")
+    if ws > 1:
+        mx = vals.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        tot = vals[3:4].clone()
+        dist.all_reduce(tot, op=dist.ReduceOp.SUM)
+    else:
+        mx, tot = vals, vals[3:4]
+    ms_step = float(mx[0])
+    peaks, src = _peaks()
+    sm_count = torch.cuda.get_device_properties(local).multi_processor_count
+    clocks = clk.summary()
+    max_mhz = clocks["sm_max_mhz"] or peaks.get("sm_max_mhz", 1965.0)
+    fp64 = (FP64_PER_CAND * st["cand"] + FP64_PER_NBR * st["nbr"] + FP64_PER_CONT * st["cont"] +
+            FP64_PER_AGENT * n_loc)
+    fp64_peak = sm_count * 64 * max_mhz * 1e6
+    b_alg = (B_ALG_PER_AGENT + (B_ALG_STATIC_EXTRA if cfg.detect_static else 0.0)) * n_loc
+    t_roof = max(b_alg / (peaks["hbm_gbs"] * 1e9), fp64 / fp64_peak)
+    res = {"ms_per_step": ms_step, "value": float(tot[0]) / (ms_step * 1e-3),
+           "agents_total": int(tot[0]), "agents_rank0": n_loc,
+           "exchange_ms": float(mx[1]), "compute_ms": float(mx[2]),
+           "exchange_share": float(mx[1]) / ms_step if ms_step > 0 else None,
+           "ghosts_rank0": dom.ghosts[0].n if dom else 0,
+           "roofline_rank0": {"bound": "alu", "t_roof_ms": t_roof * 1e3,
+                              "frac_of_step": t_roof * 1e3 / ms_step,
+                              "fp64_term_ms": fp64 / fp64_peak * 1e3,
+                              "hbm_term_ms": b_alg / (peaks["hbm_gbs"] * 1e9) * 1e3},
+           "clocks": clocks, "gpu_launches": eng.stats()["launches"] - launches0}
+    del dom, a, eng
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    return res
+
+
+def run_slabs(args, ws, rank, local):
+    """x-slab decomposition over N GPUs through the C-ABI exchange
+    (bdm_dist_init / bdm_aura_exchange over NCCL, one rank per GPU).  The line is the
+    weak-scaled cfg2 workload (one 10M-agent cfg2 cube per GPU, slabs side by side in
+    x); strong_cfg5 is the 1.7B-agent cfg5 cube split into N slabs (the north_star's
+    scaling target: S_N = T_1 / T_N with T_1 from the N = 1 line's strong_cfg5).
+    --python-protocol (or --aura-codec) runs the reference protocol of slabs.py."""
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    if ws > 1 and not dist.is_initialized():
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if args.python_protocol or args.aura_codec:
+        return run_slabs_python(args, ws, rank, local)
+    strong_only = args.config == "cfg5"
+    weak = None if strong_only else _slab_phase(args, ws, rank, local, False, args.steps, args.warmup)
+    strong = None
+    if strong_only or args.strong_steps > 0:
+        try:
+            strong = _slab_phase(args, ws, rank, local, True,
+                                 args.steps if strong_only else args.strong_steps,
+                                 args.warmup if strong_only else 2)
+        except Exception as e:  # noqa: BLE001 (reported in the line)
+            strong = {"error": f"{type(e).__name__}: {e}"[:300]}
+    if rank == 0:
+        main = weak if weak is not None else strong
+        line = _common(main["value"], main["ms_per_step"], ws, args,
+                       {"workload": ("cfg5 (configs[4]) x-slabs" if weak is None
+                                     else "cfg2 (configs[1]) per GPU, x-slabs side by side"),
+                        "agents_total": main["agents_total"], "slabs": ws,
+                        "transport": "bdm_aura_exchange (C ABI, NCCL p2p + all-reduce)"
+                        if ws > 1 else "none (one slab)",
+                        "l2": "inputs larger than L2; no flush", "parallelism": f"x-slab {ws}"},
+                       main["clocks"], main["gpu_launches"])
+        line["scaling"] = "strong" if weak is None else "weak"
+        line["roofline"] = {"bound": "alu", "kernel": "rank 0's step (grid + mechanics)",
+                            **main["roofline_rank0"]}
+        line["exchange"] = {k: main[k] for k in ("exchange_ms", "compute_ms", "exchange_share",
+                                                 "ghosts_rank0", "agents_rank0")}
+        line["e2e"] = None
+        line["e2e_note"] = "multi-GPU: no host round trip in the step; see the N = 1 line's e2e"
+        if weak is not None and strong is not None:
+            line["strong_cfg5"] = strong
+        line["note"] = "device-timed, max over ranks, of the whole step (exchange + grid + mechanics)"
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+def run_slabs_python(args, ws, rank, local):
+    """The reference protocol (slabs.py SlabDomain over torch.distributed), kept for the
+    row-f3 aura codec and as a cross-check of the C path."""
+    import torch
+    import torch.distributed as dist
+    from paper_2503_10796_b200 import Agents, Engine, Params
+    from paper_2503_10796_b200.slabs import DistTransport, LibOps, Slab, SlabDomain
+    strong = args.config == "cfg5"
+    cfg = W.CFG5 if strong else W.CFG2
+    n_local_est = cfg.n // ws if strong else cfg.n
+    side_x = cfg.side if strong else cfg.side * ws
+    lo = -math.inf if rank == 0 else rank * side_x / ws
+    hi = math.inf if rank == ws - 1 else (rank + 1) * side_x / ws
+    cap = int(n_local_est * 1.15) + 4096
+    eng = Engine(local, cap)
+    a = Agents.empty(cap)
+    stream = torch.cuda.current_stream(local)
+    _slab_population(eng, a, cfg, strong, ws, rank, lo, hi, stream)
     ops = LibOps(eng, stream=stream)
     tr = DistTransport(ops, torch.device("cuda", local)) if ws > 1 else None
     if tr is None:
@@ -995,13 +1166,14 @@ def run_slabs(args, ws, rank, local):
                        {"workload": ("cfg5 (configs[4]) x-slabs" if strong
                                      else "cfg2 (configs[1]) per GPU, x-slabs side by side"),
                         "agents_total": int(tot[0]), "slabs": ws,
-                        "transport": "torch.distributed NCCL p2p + all-reduce" if ws > 1 else "local",
+                        "transport": "torch.distributed NCCL p2p + all-reduce (slabs.py)" if ws > 1
+                        else "local", "aura_codec": bool(args.aura_codec),
                         "l2": "inputs larger than L2; no flush", "parallelism": f"x-slab {ws}"},
                        clk.summary(), eng.stats()["launches"] - launches0)
         line["scaling"] = "strong" if strong else "weak"
         line["roofline"] = None
         line["e2e"] = None
-        line["note"] = "multi-GPU: device-timed max over ranks of the whole protocol step"
+        line["note"] = "reference protocol (slabs.py); device-timed max over ranks"
         print(json.dumps(line), flush=True)
     if ws > 1:
         dist.destroy_process_group()
@@ -1090,6 +1262,13 @@ def main():
                     help="row f1: reorder the agents every K-th step (0 = never)")
     ap.add_argument("--force-slabs", action="store_true",
                     help="run the x-slab protocol path even on one GPU (a check of that path)")
+    ap.add_argument("--ref-budget", type=float, default=150.0,
+                    help="--impl reference: seconds the oracle's --steps K --warmup W should take")
+    ap.add_argument("--python-protocol", action="store_true",
+                    help="x-slabs through the reference protocol of slabs.py (not the C ABI)")
+    ap.add_argument("--strong-steps", type=int, default=3,
+                    help="steps of the strong-scaled cfg5 x-slab measurement added to the "
+                         "N-GPU line (and T_1 to the N = 1 line); 0 skips it")
     ap.add_argument("--aura-codec", action="store_true",
                     help="row f3: x-slab aura as delta + LZ4 streams (links slower than NVLink)")
     ap.add_argument("--shuffle", action="store_true",

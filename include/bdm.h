@@ -36,7 +36,7 @@ typedef enum {
     BDM_EINVAL = -1,      /* bad argument (null pointer, n > capacity, radius < 0, ...) */
     BDM_ECAPACITY = -2,   /* a library or caller capacity is too small; see bdm_last_error */
     BDM_ECUDA = -3,       /* CUDA runtime error (possibly from an earlier async launch) */
-    BDM_ENCCL = -4,       /* reserved for collective errors */
+    BDM_ENCCL = -4,       /* NCCL missing or a collective failed (bdm_last_error)     */
     BDM_ENOTFINITE = -5,  /* a position was NaN/Inf */
     BDM_ENOTIMPL = -6     /* feature not implemented in this build */
 } bdm_status;
@@ -295,10 +295,66 @@ bdm_status bdm_onco_step(bdm_handle h, bdm_agents *a, uint32_t *age, int64_t age
                          const bdm_onco_params *p, int64_t id_next, int64_t *out_host,
                          void *stream);
 
-/* ---- multi-GPU x-slabs (TeraAgent partitioning P:6058-6081, aura
- * P:6083-6106, migration P:6116-6126).  The transport between ranks is the
- * caller's (torch.distributed over NCCL in paper_2503_10796_b200/slabs.py); these
- * calls are the device side: the global frame, packing and appending. */
+/* ---- multi-GPU x-slabs (TeraAgent partitioning P:6058-6081,
+ * aura update P:6083-6106, agent migration P:6116-6126).
+ *
+ * Rank r of N owns the static x-slab [slab_lo, slab_hi) (rank 0 unbounded below,
+ * rank N-1 above: every agent has exactly one owner, R24).  One bdm_aura_exchange per
+ * step, before bdm_grid_build(local, ghosts), does on `stream`, with ONE host
+ * synchronization (for the received counts):
+ *   - the global grid frame: element-wise MIN all-reduce of (min x, min y, min z,
+ *     -max d) of the local agents; the following grid builds use it (R12), so every
+ *     rank's box lattice and canonical order are those of the undivided run;
+ *   - migration: agents with x < slab_lo go to rank r-1, x >= slab_hi to rank r+1
+ *     and leave `local` (removal by refilling their slots from the end, Fig. 5.1);
+ *   - aura: staying agents with x < slab_lo + R' go to rank r-1 and x >= slab_hi - R'
+ *     to rank r+1, R' = R (1 + 2^-20) (R24), R = `radius` of bdm_dist_init or, if
+ *     that is <= 0, the global largest diameter -- computed on the device;
+ *   - local <- kept agents + arrivals; ghosts <- the neighbours' aura + this rank's own
+ *     leavers (they belong to the neighbour now and lie at the shared border).
+ * local->n and ghosts->n are updated.  The agent order in `local` changes (no result
+ * depends on it, R32).  Buffers for sending and receiving are the library's
+ * (persistent, grown geometrically; nothing is allocated in a step of steady size).
+ * Precondition: agents move less than (slab width - R') per step.
+ * Errors: BDM_EINVAL (arguments, no bdm_dist_init), BDM_ENCCL (NCCL missing or a
+ * collective failed), BDM_ECUDA, BDM_ECAPACITY (local or ghosts too small for the
+ * arrivals: the received agents are kept by the library, local->n = the kept
+ * count; bdm_aura_pending gives the sizes needed, then grow the arrays (keeping
+ * their contents) and call bdm_aura_finish). */
+#define BDM_PACK_MIGRATE 1  /* x < lo -> left, x >= hi -> right; leavers removed        */
+#define BDM_PACK_AURA 2     /* x < lo + margin -> left, x >= hi - margin -> right; copy */
+
+/* A new NCCL unique id (128 bytes) for bdm_dist_init; rank 0 makes it, the caller
+ * broadcasts it (e.g. torch.distributed).  Errors: BDM_ENCCL (no libnccl.so.2). */
+bdm_status bdm_nccl_unique_id(uint8_t id[128]);
+
+/* Join the N-rank x-slab group (NCCL communicator from the 128-byte unique id; N = 1
+ * needs no NCCL).  radius > 0 fixes R for the aura margin, else R = max diameter.
+ * Collective over the N ranks (blocks until all joined).  One rank per GPU. */
+bdm_status bdm_dist_init(bdm_handle h, const uint8_t nccl_unique_id[128], int32_t rank,
+                         int32_t nranks, double slab_lo, double slab_hi, double radius);
+
+/* One step's frame + migration + aura exchange (see above). */
+bdm_status bdm_aura_exchange(bdm_handle h, bdm_agents *local, bdm_agents *ghosts, void *stream);
+
+/* Virtual slabs (tests on one GPU): N contexts of one process on one device form a
+ * group; bdm_aura_exchange_virtual does the exchange for all of them at once (device
+ * copies instead of NCCL), with the same semantics and one synchronization.
+ * slab_lo/slab_hi: N bounds each (outer bounds ignored, unbounded). */
+bdm_status bdm_dist_init_virtual(bdm_handle *hs, int32_t nranks, const double *slab_lo,
+                                 const double *slab_hi, double radius);
+bdm_status bdm_aura_exchange_virtual(bdm_handle *hs, int32_t nranks, bdm_agents *locals,
+                                     bdm_agents *ghosts, void *stream);
+
+/* After BDM_ECAPACITY from an exchange: need[0] = local capacity needed, need[1] =
+ * ghost capacity needed (0, 0 when nothing is pending). */
+bdm_status bdm_aura_pending(bdm_handle h, int64_t need[2]);
+/* Completes a pending exchange into the (grown) arrays; local->n must be the kept
+ * count the exchange left. */
+bdm_status bdm_aura_finish(bdm_handle h, bdm_agents *local, bdm_agents *ghosts, void *stream);
+
+/* The device halves used by the Python reference protocol (slabs.py, CPU tests):
+ * the local frame, packing and appending. */
 #define BDM_PACK_MIGRATE 1  /* x < lo -> left, x >= hi -> right; leavers removed        */
 #define BDM_PACK_AURA 2     /* x < lo + margin -> left, x >= hi - margin -> right; copy */
 

@@ -145,6 +145,13 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "bdm_aura_reference": [P, AG, AG, P],
         "bdm_aura_encode": [P, AG, AG, P, i64, ctypes.POINTER(i64), P],
         "bdm_aura_decode": [P, P, i64, AG, AG, P],
+        "bdm_nccl_unique_id": [P],
+        "bdm_dist_init": [P, P, i32, i32, dbl, dbl, dbl],
+        "bdm_aura_exchange": [P, AG, AG, P],
+        "bdm_dist_init_virtual": [P, i32, P, P, dbl],
+        "bdm_aura_exchange_virtual": [P, i32, P, P, P],
+        "bdm_aura_pending": [P, P],
+        "bdm_aura_finish": [P, AG, AG, P],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -236,6 +243,17 @@ class Agents:
     @property
     def capacity(self) -> int:
         return int(self.x.numel())
+
+    def grow(self, capacity: int):
+        """Reallocate to `capacity` (same device), keeping the first n agents."""
+        import torch
+        for f in ("x", "y", "z", "diameter", "id", "flags", "volume", "state"):
+            t = getattr(self, f)
+            if t is None:
+                continue
+            nt = torch.empty(int(capacity), dtype=t.dtype, device=t.device)
+            nt[:self.n].copy_(t[:self.n])
+            setattr(self, f, nt)
 
     def c(self) -> CAgents:
         a = CAgents()
@@ -356,6 +374,74 @@ class Engine:
         if what == PACK_MIGRATE:
             agents.n = rem
         return nl, nr
+
+    # ---- x-slab exchange behind the C ABI (bdm_dist_init / bdm_aura_exchange)
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        buf = ctypes.create_string_buffer(128)
+        _check(load_library().bdm_nccl_unique_id(ctypes.cast(buf, ctypes.c_void_p)))
+        return buf.raw
+
+    def dist_init(self, uid: bytes, rank: int, nranks: int, lo: float, hi: float,
+                  radius: float = 0.0):
+        """Join the NCCL x-slab group (collective over the ranks)."""
+        buf = ctypes.create_string_buffer(bytes(uid), 128)
+        _check(self.lib.bdm_dist_init(self.h, ctypes.cast(buf, ctypes.c_void_p), int(rank),
+                                      int(nranks), float(lo), float(hi), float(radius)))
+
+    def aura_exchange(self, local: Agents, ghosts: Agents, stream=None):
+        """Frame + migration + aura for this step (one host synchronization).  Grows
+        `local` / `ghosts` when the arrivals do not fit and completes the exchange."""
+        cl, cg = local.c(), ghosts.c()
+        st = self.lib.bdm_aura_exchange(self.h, ctypes.byref(cl), ctypes.byref(cg),
+                                        _stream_ptr(stream))
+        local.n, ghosts.n = cl.n, cg.n
+        if st == BDM_ECAPACITY:
+            self._finish_pending(local, ghosts, stream)
+        else:
+            _check(st)
+
+    def _finish_pending(self, local: Agents, ghosts: Agents, stream=None):
+        need = (ctypes.c_int64 * 2)()
+        _check(self.lib.bdm_aura_pending(self.h, ctypes.cast(need, ctypes.c_void_p)))
+        if need[0] > local.capacity:
+            local.grow(int(need[0] * 5 // 4 + 1024))
+        if need[1] > ghosts.capacity:
+            ghosts.grow(int(need[1] * 5 // 4 + 1024))
+        cl, cg = local.c(), ghosts.c()
+        _check(self.lib.bdm_aura_finish(self.h, ctypes.byref(cl), ctypes.byref(cg),
+                                        _stream_ptr(stream)))
+        local.n, ghosts.n = cl.n, cg.n
+
+    @staticmethod
+    def dist_init_virtual(engines, lo, hi, radius: float = 0.0):
+        """G contexts of this process (one device) as G virtual x-slabs."""
+        G = len(engines)
+        hs = (ctypes.c_void_p * G)(*[e.h for e in engines])
+        los = (ctypes.c_double * G)(*[float(v) for v in lo])
+        his = (ctypes.c_double * G)(*[float(v) for v in hi])
+        _check(load_library().bdm_dist_init_virtual(ctypes.cast(hs, ctypes.c_void_p), G,
+                                                     ctypes.cast(los, ctypes.c_void_p),
+                                                     ctypes.cast(his, ctypes.c_void_p),
+                                                     float(radius)))
+
+    @staticmethod
+    def aura_exchange_virtual(engines, locals_, ghosts, stream=None):
+        G = len(engines)
+        hs = (ctypes.c_void_p * G)(*[e.h for e in engines])
+        cl = (CAgents * G)(*[a.c() for a in locals_])
+        cg = (CAgents * G)(*[g.c() for g in ghosts])
+        st = load_library().bdm_aura_exchange_virtual(ctypes.cast(hs, ctypes.c_void_p), G,
+                                                      ctypes.cast(cl, ctypes.c_void_p),
+                                                      ctypes.cast(cg, ctypes.c_void_p),
+                                                      _stream_ptr(stream))
+        for k in range(G):
+            locals_[k].n, ghosts[k].n = cl[k].n, cg[k].n
+        if st == BDM_ECAPACITY:
+            for k in range(G):
+                engines[k]._finish_pending(locals_[k], ghosts[k], stream)
+        else:
+            _check(st)
 
     def append(self, dst: Agents, src: Agents, stream=None):
         cd, cs = dst.c(), src.c()

@@ -17,7 +17,7 @@ CSRC = os.path.join(HERE, "csrc")
 SO = os.path.join(HERE, "libbdm.so")
 SOURCES = ["bdm_abi.cu", "kernels_grid.cu", "kernels_mech.cu", "kernels_divide.cu",
            "kernels_sir.cu", "kernels_slab.cu", "kernels_diffusion.cu", "kernels_onco.cu",
-           "kernels_aura.cu", "kernels_row.cu"]
+           "kernels_aura.cu", "kernels_row.cu", "dist_abi.cu"]
 HEADERS = ["bdm_internal.cuh", "mech_common.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 

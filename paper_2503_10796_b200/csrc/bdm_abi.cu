@@ -241,6 +241,7 @@ bdm_status bdm_destroy(bdm_handle h) {
     cudaSetDevice(c->device);
     cudaDeviceSynchronize();
     free_aura(c);
+    free_dist(c);
     void *bufs[] = {c->key, c->rank, c->perm_tmp, c->skey, c->sid, c->perm, c->sx, c->sy,
                     c->sz, c->sd, c->sidf, c->sflags, c->svol, c->div_rank, c->box_start, c->dense_list, c->dense_scr,
                     c->onco_id, c->onco_out,

@@ -54,6 +54,8 @@ struct DevScalars {
     uint16_t hilb_inv[512];  // curve position -> local tile
 };
 
+struct Dist;  // x-slab exchange state (dist_abi.cu)
+
 // SIR workspace (kernels_sir.cu), allocated on first use
 struct SirWs {
     unsigned long long *keys = nullptr;
@@ -149,6 +151,7 @@ struct Ctx {
     int64_t fused_n = 0;
     SirWs sir;
     AuraWs aura;
+    Dist *dist = nullptr;  // bdm_dist_init / bdm_dist_init_virtual
 };
 
 // An optional per-agent buffer (agent_cap + 1 entries), allocated on first use.
@@ -323,6 +326,8 @@ bdm_status launch_aura_encode(Ctx *c, const bdm_agents *m, const bdm_agents *r, 
 bdm_status launch_aura_decode(Ctx *c, const uint8_t *in, int64_t in_size, const bdm_agents *r,
                               bdm_agents *m, cudaStream_t st);
 void free_aura(Ctx *c);
+// x-slab exchange (dist_abi.cu)
+void free_dist(Ctx *c);
 // SIR (kernels_sir.cu)
 bdm_status launch_sir_step(Ctx *c, bdm_agents *a, const bdm_params *p, double side, double radius,
                            double p_inf, double p_rec, long long *counts_host, cudaStream_t st);

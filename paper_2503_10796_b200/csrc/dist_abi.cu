@@ -1,0 +1,820 @@
+// dist_abi.cu -- the x-slab exchange behind the C ABI (SURVEY 8(b) bdm_dist_init /
+// bdm_aura_exchange, 8(e)): TeraAgent's aura update and agent migration
+// between the static x-slabs [lo, hi) of the ranks, one rank
+// per GPU over NCCL, or G virtual slabs of one process on one device (tests).
+//
+// One exchange, all on the caller's stream with ONE host synchronization:
+//   1. frame     per-axis minimum and largest diameter of the local agents, all-reduced
+//                (MIN of x, y, z, -d) into the global grid frame (R12), which the next
+//                bdm_grid_build uses; the aura margin R' = R (1 + 2^-20) is computed on
+//                the device from it (R24)
+//   2. pack      one classification pass: x < lo or x >= hi leave (migrants to the
+//                left / right), the others stay and are aura for the left / right when
+//                x < lo + R' / x >= hi - R'; leavers and aura are copied to library send
+//                buffers (warp-aggregated appends; order never enters a result, R32) and
+//                the leavers' slots are refilled from the end of the array (the paper's
+//                parallel removal, Fig. 5.1)
+//   3. counts    the four counts go to the neighbours (NCCL send/recv of int64), and the
+//                host reads all counts once (the synchronization)
+//   4. payload   leavers and aura travel in one NCCL group (per field arrays, exact
+//                counts) into library receive buffers
+//   5. append    one gather kernel appends the arrivals to the local agents, and writes
+//                the ghosts: the neighbours' aura plus this rank's own leavers, which now
+//                belong to the neighbour and lie within max_disp of the shared border
+// Precondition: an agent moves less than (slab width - R') in one step, so an agent
+// that migrates out of a neighbour's far side cannot be within R' of this rank.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+#include <string.h>
+
+#include <string>
+#include <vector>
+
+#include "bdm_internal.cuh"
+
+namespace bdm {
+
+// ------------------------------------------------------------------ NCCL (dlopen)
+// The library links no NCCL: it uses the process's libnccl.so.2 (torch's, when torch
+// loaded it), found with dlopen, so that the library loads and runs on machines
+// without NCCL (single GPU, CPU test hosts).
+struct NcclApi {
+    ncclResult_t (*GetUniqueId)(ncclUniqueId *);
+    ncclResult_t (*CommInitRank)(ncclComm_t *, int, ncclUniqueId, int);
+    ncclResult_t (*CommDestroy)(ncclComm_t);
+    ncclResult_t (*Send)(const void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
+    ncclResult_t (*Recv)(void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
+    ncclResult_t (*GroupStart)();
+    ncclResult_t (*GroupEnd)();
+    ncclResult_t (*AllReduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                              cudaStream_t);
+    const char *(*GetErrorString)(ncclResult_t);
+};
+
+static const NcclApi *nccl_api(std::string &why) {
+    static NcclApi api;
+    static int state = 0;  // 0 untried, 1 ok, -1 failed
+    static std::string err;
+    if (state == 0) {
+        void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+        if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        state = -1;
+        if (!h) {
+            err = std::string("libnccl.so.2 not found: ") + dlerror();
+        } else {
+            bool ok = true;
+            auto sym = [&](const char *name) {
+                void *p = dlsym(h, name);
+                if (!p) ok = false;
+                return p;
+            };
+            api.GetUniqueId = (decltype(api.GetUniqueId))sym("ncclGetUniqueId");
+            api.CommInitRank = (decltype(api.CommInitRank))sym("ncclCommInitRank");
+            api.CommDestroy = (decltype(api.CommDestroy))sym("ncclCommDestroy");
+            api.Send = (decltype(api.Send))sym("ncclSend");
+            api.Recv = (decltype(api.Recv))sym("ncclRecv");
+            api.GroupStart = (decltype(api.GroupStart))sym("ncclGroupStart");
+            api.GroupEnd = (decltype(api.GroupEnd))sym("ncclGroupEnd");
+            api.AllReduce = (decltype(api.AllReduce))sym("ncclAllReduce");
+            api.GetErrorString = (decltype(api.GetErrorString))sym("ncclGetErrorString");
+            if (ok) state = 1;
+            else err = "libnccl.so.2 lacks a needed symbol";
+        }
+    }
+    why = err;
+    return state == 1 ? &api : nullptr;
+}
+
+// ------------------------------------------------------------------ buffers
+struct XBuf {  // library-owned SoA agent buffer
+    double *x = nullptr, *y = nullptr, *z = nullptr, *d = nullptr, *v = nullptr;
+    uint32_t *id = nullptr, *f = nullptr;
+    int64_t cap = 0;
+};
+
+static void xbuf_free(XBuf &b) {
+    void *p[] = {b.x, b.y, b.z, b.d, b.v, b.id, b.f};
+    for (void *q : p)
+        if (q) cudaFree(q);
+    b = XBuf();
+}
+
+static bdm_status xbuf_reserve(XBuf &b, int64_t n, bool vol) {
+    if (n <= b.cap && (!vol || b.v)) return BDM_OK;
+    const int64_t cap = n > b.cap ? n + n / 4 + 1024 : b.cap;
+    xbuf_free(b);
+    cudaError_t e = cudaSuccess;
+    auto al = [&](void **p, size_t sz) {
+        if (e == cudaSuccess) e = cudaMalloc(p, (size_t)cap * sz);
+    };
+    al((void **)&b.x, 8);
+    al((void **)&b.y, 8);
+    al((void **)&b.z, 8);
+    al((void **)&b.d, 8);
+    al((void **)&b.id, 4);
+    al((void **)&b.f, 4);
+    if (vol) al((void **)&b.v, 8);
+    if (e != cudaSuccess) {
+        xbuf_free(b);
+        cudaGetLastError();
+        return cuda_fail(e, "allocation of an exchange buffer");
+    }
+    b.cap = cap;
+    return BDM_OK;
+}
+
+static bdm_agents xbuf_view(const XBuf &b, int64_t n) {
+    bdm_agents a;
+    memset(&a, 0, sizeof(a));
+    a.n = n;
+    a.capacity = b.cap;
+    a.x = b.x; a.y = b.y; a.z = b.z; a.diameter = b.d; a.volume = b.v;
+    a.id = b.id; a.flags = b.f;
+    return a;
+}
+
+// Send/receive slots: 0 migrants to/from the left, 1 migrants right, 2 aura left, 3 aura right.
+struct Dist {
+    int rank = 0, nranks = 1;
+    double lo = 0.0, hi = 0.0;   // owned x-interval (outer slabs unbounded)
+    ncclComm_t comm = nullptr;
+    bool virt = false;
+    std::vector<Ctx *> group;    // virtual mode: the slabs in rank order
+    XBuf send[4], recv[4];
+    long long *cnt = nullptr;    // device: [0..3] sent, [4..7] received (slot order), [8] n kept
+    long long *cnt_h = nullptr;  // pinned mirror
+    unsigned long long *ctr = nullptr;  // device: 12 pack counters
+    double **vframes = nullptr;  // virtual mode (rank 0): device array of the slabs' frames
+    unsigned long long *enc = nullptr;  // device: 4 encoded frame values
+    double *frame = nullptr;     // device: global (o_x, o_y, o_z, -max d)
+    uint32_t *holes = nullptr, *fillers = nullptr;
+    int64_t hf_cap = 0;
+    double radius = 0.0;         // > 0: fixed interaction radius; else max diameter
+    // the agents received but not yet appended (a capacity shortfall)
+    bool pending = false;
+    int64_t kept = 0, in_mig[2] = {0, 0}, in_aura[2] = {0, 0}, out_mig[2] = {0, 0};
+};
+
+void free_dist(Ctx *c) {
+    Dist *D = c->dist;
+    if (!D) return;
+    for (int k = 0; k < 4; ++k) {
+        xbuf_free(D->send[k]);
+        xbuf_free(D->recv[k]);
+    }
+    void *p[] = {D->cnt, D->ctr, D->enc, D->frame, D->holes, D->fillers, D->vframes};
+    for (void *q : p)
+        if (q) cudaFree(q);
+    if (D->cnt_h) cudaFreeHost(D->cnt_h);
+    if (D->comm) {
+        std::string why;
+        const NcclApi *api = nccl_api(why);
+        if (api) api->CommDestroy(D->comm);
+    }
+    delete D;
+    c->dist = nullptr;
+}
+
+static bdm_status dist_alloc(Ctx *c, Dist *D) {
+    cudaError_t e = cudaSuccess;
+    if (e == cudaSuccess) e = cudaMalloc(&D->cnt, 16 * sizeof(long long));
+    if (e == cudaSuccess) e = cudaMalloc(&D->ctr, 12 * sizeof(unsigned long long));
+    if (e == cudaSuccess) e = cudaMalloc(&D->enc, 4 * sizeof(unsigned long long));
+    if (e == cudaSuccess) e = cudaMalloc(&D->frame, 4 * sizeof(double));
+    if (e == cudaSuccess) e = cudaMallocHost(&D->cnt_h, 16 * sizeof(long long));
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return cuda_fail(e, "allocation of the exchange scalars");
+    }
+    (void)c;
+    return BDM_OK;
+}
+
+// ------------------------------------------------------------------ kernels
+__global__ void k_xfr_init(unsigned long long *enc) {
+    if (threadIdx.x < 4) enc[threadIdx.x] = enc_double(INFINITY);
+}
+
+__global__ void __launch_bounds__(256) k_xfr_local(int64_t n, const double *__restrict__ x,
+                                                   const double *__restrict__ y,
+                                                   const double *__restrict__ z,
+                                                   const double *__restrict__ d,
+                                                   unsigned long long *__restrict__ enc) {
+    double a0 = INFINITY, a1 = INFINITY, a2 = INFINITY, a3 = INFINITY;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        a0 = fmin(a0, x[i]);
+        a1 = fmin(a1, y[i]);
+        a2 = fmin(a2, z[i]);
+        a3 = fmin(a3, -d[i]);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        a0 = fmin(a0, __shfl_xor_sync(0xffffffffu, a0, o));
+        a1 = fmin(a1, __shfl_xor_sync(0xffffffffu, a1, o));
+        a2 = fmin(a2, __shfl_xor_sync(0xffffffffu, a2, o));
+        a3 = fmin(a3, __shfl_xor_sync(0xffffffffu, a3, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMin(&enc[0], enc_double(a0));
+        atomicMin(&enc[1], enc_double(a1));
+        atomicMin(&enc[2], enc_double(a2));
+        atomicMin(&enc[3], enc_double(a3));
+    }
+}
+
+__global__ void k_xfr_decode(const unsigned long long *enc, double *out) {
+    if (threadIdx.x < 4) out[threadIdx.x] = dec_double(enc[threadIdx.x]);
+}
+
+// virtual mode: elementwise minimum of G frames, written back to all of them
+__global__ void k_xfr_min(double *const *frames, int G) {
+    const int q = threadIdx.x;
+    if (q >= 4) return;
+    double v = INFINITY;
+    for (int g = 0; g < G; ++g) v = fmin(v, frames[g][q]);
+    for (int g = 0; g < G; ++g) frames[g][q] = v;
+}
+
+struct XPack {
+    int64_t n;
+    bdm_agents a;
+    bdm_agents s[4];     // send buffers (capacity = their size)
+    double lo, hi, radius;
+    const double *frame;
+    uint32_t *holes, *fillers;
+};
+
+__device__ __forceinline__ double xmargin(const XPack &P) {
+    const double R = P.radius > 0.0 ? P.radius : -P.frame[3];
+    return R * (1.0 + 0x1p-20);  // R24: a superset is harmless (the exact test filters)
+}
+
+__device__ __forceinline__ void xclass(double px, const XPack &P, double mg, bool f[4]) {
+    f[0] = px < P.lo;                    // migrant to the left
+    f[1] = px >= P.hi;                   // migrant to the right
+    const bool stay = !(f[0] || f[1]);
+    f[2] = stay && px < P.lo + mg;       // aura for the left
+    f[3] = stay && px >= P.hi - mg;      // aura for the right
+}
+
+__device__ __forceinline__ unsigned long long xslot(bool take, unsigned long long *ctr) {
+    const unsigned b = __ballot_sync(0xffffffffu, take);
+    const int lane = threadIdx.x & 31;
+    unsigned long long base = 0;
+    if (b && lane == __ffs(b) - 1) base = atomicAdd(ctr, (unsigned long long)__popc(b));
+    base = __shfl_sync(0xffffffffu, base, b ? __ffs(b) - 1 : 0);
+    return base + (unsigned long long)__popc(b & ((1u << lane) - 1u));
+}
+
+__device__ __forceinline__ void xcopy(const bdm_agents &s, int64_t i, const bdm_agents &d, int64_t j) {
+    d.x[j] = s.x[i];
+    d.y[j] = s.y[i];
+    d.z[j] = s.z[i];
+    d.diameter[j] = s.diameter[i];
+    d.id[j] = s.id[i];
+    d.flags[j] = s.flags[i];
+    if (s.volume && d.volume) d.volume[j] = s.volume[i];
+}
+
+// ctr: [0..3] class counts, [4..7] append slots, [8] holes, [9] fillers
+__global__ void __launch_bounds__(256) k_xpack_count(XPack P, unsigned long long *__restrict__ ctr) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const double mg = xmargin(P);
+    bool f[4] = {false, false, false, false};
+    if (i < P.n) xclass(P.a.x[i], P, mg, f);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const unsigned b = __ballot_sync(0xffffffffu, f[k]);
+        if ((threadIdx.x & 31) == 0 && b) atomicAdd(&ctr[k], (unsigned long long)__popc(b));
+    }
+}
+
+// Copies leavers and aura to the send buffers (all-or-nothing on their capacities:
+// nothing is modified when one is too small, cnt[9] = 1) and lists the leavers' slots
+// below the kept count m and the stayers at or above it.  cnt: [0..3] the class counts,
+// [8] kept, [9] capacity shortfall.
+__global__ void __launch_bounds__(256) k_xpack_copy(XPack P, unsigned long long *__restrict__ ctr,
+                                                    long long *__restrict__ cnt) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    long long c[4];
+    bool fits = true;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        c[k] = (long long)ctr[k];
+        fits = fits && c[k] <= P.s[k].capacity;
+    }
+    const int64_t m = P.n - c[0] - c[1];
+    if (i == 0) {
+        for (int k = 0; k < 4; ++k) cnt[k] = c[k];
+        cnt[8] = fits ? m : P.n;
+        cnt[9] = fits ? 0 : 1;
+    }
+    if (!fits) return;
+    const double mg = xmargin(P);
+    bool f[4] = {false, false, false, false};
+    if (i < P.n) xclass(P.a.x[i], P, mg, f);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const unsigned long long j = xslot(f[k], &ctr[4 + k]);
+        if (f[k]) xcopy(P.a, i, P.s[k], (int64_t)j);
+    }
+    const bool leave = f[0] || f[1];
+    const bool hole = leave && i < m;
+    const bool filler = i < P.n && !leave && i >= m;
+    const unsigned long long h = xslot(hole, &ctr[8]);
+    const unsigned long long g = xslot(filler, &ctr[9]);
+    if (hole) P.holes[h] = (uint32_t)i;
+    if (filler) P.fillers[g] = (uint32_t)i;
+}
+
+// The stayers above m move into the leavers' slots below it (as many of each).
+__global__ void __launch_bounds__(256) k_xpack_fill(XPack P, const unsigned long long *__restrict__ ctr,
+                                                    const long long *__restrict__ cnt) {
+    if (cnt[9]) return;
+    const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k >= (int64_t)ctr[8]) return;
+    xcopy(P.a, P.fillers[k], P.a, P.holes[k]);
+}
+
+// Gathers up to 6 sources into dst at base + (prefix of the source counts) (one launch).
+struct XGather {
+    bdm_agents dst;
+    bdm_agents src[6];
+    int64_t off[7];
+    int64_t base;
+    int nsrc;
+};
+
+__global__ void __launch_bounds__(256) k_xgather(XGather G) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= G.off[G.nsrc]) return;
+    int k = 0;
+    while (k + 1 < G.nsrc && t >= G.off[k + 1]) ++k;
+    xcopy(G.src[k], t - G.off[k], G.dst, G.base + t);
+}
+
+// ------------------------------------------------------------------ host steps
+static bdm_status x_frame(Ctx *c, Dist *D, const bdm_agents *a, cudaStream_t st) {
+    k_xfr_init<<<1, 32, 0, st>>>(D->enc);
+    if (a->n > 0) {
+        int64_t blocks = (a->n + 255) / 256;
+        if (blocks > c->sm_count * 8) blocks = c->sm_count * 8;
+        k_xfr_local<<<(unsigned)blocks, 256, 0, st>>>(a->n, a->x, a->y, a->z, a->diameter, D->enc);
+    }
+    k_xfr_decode<<<1, 32, 0, st>>>(D->enc, D->frame);
+    c->launches += 3;
+    BDM_LAUNCH_CHECK("exchange frame");
+    return BDM_OK;
+}
+
+static bdm_status x_pack(Ctx *c, Dist *D, bdm_agents *a, cudaStream_t st) {
+    if (D->hf_cap < a->n + 1) {
+        if (D->holes) cudaFree(D->holes);
+        if (D->fillers) cudaFree(D->fillers);
+        D->holes = D->fillers = nullptr;
+        D->hf_cap = 0;
+        const int64_t cap = a->capacity + 1;
+        BDM_CUDA_TRY(cudaMalloc(&D->holes, (size_t)cap * 4));
+        BDM_CUDA_TRY(cudaMalloc(&D->fillers, (size_t)cap * 4));
+        D->hf_cap = cap;
+    }
+    const bool vol = a->volume != nullptr;
+    for (int k = 0; k < 4; ++k) {
+        bdm_status s = xbuf_reserve(D->send[k], 1, vol);
+        if (s != BDM_OK) return s;
+    }
+    BDM_CUDA_TRY(cudaMemsetAsync(D->ctr, 0, 10 * sizeof(unsigned long long), st));
+    XPack P;
+    P.n = a->n;
+    P.a = *a;
+    for (int k = 0; k < 4; ++k) P.s[k] = xbuf_view(D->send[k], D->send[k].cap);
+    P.lo = D->lo;
+    P.hi = D->hi;
+    P.radius = D->radius;
+    P.frame = D->frame;
+    P.holes = D->holes;
+    P.fillers = D->fillers;
+    const unsigned nb = (unsigned)(a->n > 0 ? (a->n + 255) / 256 : 1);
+    k_xpack_count<<<nb, 256, 0, st>>>(P, D->ctr);
+    k_xpack_copy<<<nb, 256, 0, st>>>(P, D->ctr, D->cnt);
+    k_xpack_fill<<<nb, 256, 0, st>>>(P, D->ctr, D->cnt);
+    c->launches += 3;
+    BDM_LAUNCH_CHECK("exchange pack");
+    return BDM_OK;
+}
+
+// Arrivals -> local (after the kept agents); neighbours' aura + own leavers -> ghosts.
+static bdm_status x_append(Ctx *c, Dist *D, bdm_agents *a, bdm_agents *g, cudaStream_t st) {
+    const int64_t in = D->in_mig[0] + D->in_mig[1];
+    const int64_t ng = D->in_aura[0] + D->in_aura[1] + D->out_mig[0] + D->out_mig[1];
+    if (D->kept + in > a->capacity || ng > g->capacity) {
+        D->pending = true;
+        a->n = D->kept;
+        return BDM_ECAPACITY;
+    }
+    XGather G;
+    memset(&G, 0, sizeof(G));
+    G.dst = *a;
+    G.base = D->kept;
+    G.nsrc = 2;
+    G.src[0] = xbuf_view(D->recv[0], D->in_mig[0]);
+    G.src[1] = xbuf_view(D->recv[1], D->in_mig[1]);
+    G.off[0] = 0;
+    G.off[1] = D->in_mig[0];
+    G.off[2] = in;
+    if (in > 0) k_xgather<<<(unsigned)((in + 255) / 256), 256, 0, st>>>(G);
+    XGather H;
+    memset(&H, 0, sizeof(H));
+    H.dst = *g;
+    H.base = 0;
+    H.nsrc = 4;
+    const int64_t cn[4] = {D->in_aura[0], D->in_aura[1], D->out_mig[0], D->out_mig[1]};
+    H.src[0] = xbuf_view(D->recv[2], cn[0]);
+    H.src[1] = xbuf_view(D->recv[3], cn[1]);
+    H.src[2] = xbuf_view(D->send[0], cn[2]);
+    H.src[3] = xbuf_view(D->send[1], cn[3]);
+    H.off[0] = 0;
+    for (int k = 0; k < 4; ++k) H.off[k + 1] = H.off[k] + cn[k];
+    if (ng > 0) k_xgather<<<(unsigned)((ng + 255) / 256), 256, 0, st>>>(H);
+    c->launches += 2;
+    BDM_LAUNCH_CHECK("exchange append");
+    a->n = D->kept + in;
+    g->n = ng;
+    D->pending = false;
+    return BDM_OK;
+}
+
+// Reads the counts after the one synchronization; repacks if a send buffer was short.
+static bdm_status x_after_counts(Ctx *c, Dist *D, bdm_agents *a, cudaStream_t st) {
+    const long long *h = D->cnt_h;
+    if (h[9]) {  // a send buffer was too small: grow and pack again (stream order)
+        const bool vol = a->volume != nullptr;
+        for (int k = 0; k < 4; ++k) {
+            bdm_status s = xbuf_reserve(D->send[k], h[k], vol);
+            if (s != BDM_OK) return s;
+        }
+        bdm_status s = x_pack(c, D, a, st);
+        if (s != BDM_OK) return s;
+    }
+    D->kept = a->n - h[0] - h[1];
+    D->out_mig[0] = h[0];
+    D->out_mig[1] = h[1];
+    D->in_mig[0] = h[4];
+    D->in_mig[1] = h[5];
+    D->in_aura[0] = h[6];
+    D->in_aura[1] = h[7];
+    const bool vol = a->volume != nullptr;
+    for (int k = 0; k < 4; ++k) {
+        bdm_status s = xbuf_reserve(D->recv[k], h[4 + k] > 0 ? h[4 + k] : 1, vol);
+        if (s != BDM_OK) return s;
+    }
+    return BDM_OK;
+}
+
+static bdm_status nccl_fail(ncclResult_t r, const NcclApi *api, const char *what) {
+    set_error(std::string(what) + ": " + (api ? api->GetErrorString(r) : "nccl"));
+    return BDM_ENCCL;
+}
+#define BDM_NCCL_TRY(api, expr)                                          \
+    do {                                                                 \
+        ncclResult_t r__ = (expr);                                       \
+        if (r__ != ncclSuccess) return nccl_fail(r__, api, #expr);       \
+    } while (0)
+
+// per-field arrays of an XBuf for the payload group (same order on both sides)
+static int xfields(const XBuf &b, void *ptr[7], size_t bytes[7], bool vol) {
+    int k = 0;
+    ptr[k] = b.x; bytes[k++] = 8;
+    ptr[k] = b.y; bytes[k++] = 8;
+    ptr[k] = b.z; bytes[k++] = 8;
+    ptr[k] = b.d; bytes[k++] = 8;
+    ptr[k] = b.id; bytes[k++] = 4;
+    ptr[k] = b.f; bytes[k++] = 4;
+    if (vol) {
+        ptr[k] = b.v;
+        bytes[k++] = 8;
+    }
+    return k;
+}
+
+static bdm_status x_nccl(Ctx *c, Dist *D, bdm_agents *a, bdm_agents *g, cudaStream_t st) {
+    std::string why;
+    const NcclApi *api = nccl_api(why);
+    if (!api) {
+        set_error(why);
+        return BDM_ENCCL;
+    }
+    const int left = D->rank - 1, right = D->rank + 1 < D->nranks ? D->rank + 1 : -1;
+    bdm_status s = x_frame(c, D, a, st);
+    if (s != BDM_OK) return s;
+    BDM_NCCL_TRY(api, api->AllReduce(D->frame, D->frame, 4, ncclFloat64, ncclMin, D->comm, st));
+    if ((s = x_pack(c, D, a, st)) != BDM_OK) return s;
+    BDM_CUDA_TRY(cudaMemsetAsync(D->cnt + 4, 0, 4 * sizeof(long long), st));
+    BDM_NCCL_TRY(api, api->GroupStart());
+    if (left >= 0) {
+        BDM_NCCL_TRY(api, api->Send(D->cnt + 0, 1, ncclInt64, left, D->comm, st));
+        BDM_NCCL_TRY(api, api->Send(D->cnt + 2, 1, ncclInt64, left, D->comm, st));
+        BDM_NCCL_TRY(api, api->Recv(D->cnt + 4, 1, ncclInt64, left, D->comm, st));
+        BDM_NCCL_TRY(api, api->Recv(D->cnt + 6, 1, ncclInt64, left, D->comm, st));
+    }
+    if (right >= 0) {
+        BDM_NCCL_TRY(api, api->Send(D->cnt + 1, 1, ncclInt64, right, D->comm, st));
+        BDM_NCCL_TRY(api, api->Send(D->cnt + 3, 1, ncclInt64, right, D->comm, st));
+        BDM_NCCL_TRY(api, api->Recv(D->cnt + 5, 1, ncclInt64, right, D->comm, st));
+        BDM_NCCL_TRY(api, api->Recv(D->cnt + 7, 1, ncclInt64, right, D->comm, st));
+    }
+    BDM_NCCL_TRY(api, api->GroupEnd());
+    BDM_CUDA_TRY(cudaMemcpyAsync(D->cnt_h, D->cnt, 10 * sizeof(long long), cudaMemcpyDeviceToHost, st));
+    BDM_CUDA_TRY(cudaStreamSynchronize(st));  // the exchange's one synchronization
+    if ((s = x_after_counts(c, D, a, st)) != BDM_OK) return s;
+    const bool vol = a->volume != nullptr;
+    BDM_NCCL_TRY(api, api->GroupStart());
+    for (int side = 0; side < 2; ++side) {
+        const int peer = side == 0 ? left : right;
+        if (peer < 0) continue;
+        // to the peer: migrants (slot side) then aura (slot 2 + side); from the peer: its
+        // migrants (recv slot side) then its aura (recv slot 2 + side)
+        const int64_t nsend[2] = {D->cnt_h[side], D->cnt_h[2 + side]};
+        const int64_t nrecv[2] = {D->cnt_h[4 + side], D->cnt_h[6 + side]};
+        for (int q = 0; q < 2; ++q) {
+            void *sp[7], *rp[7];
+            size_t sb[7], rb[7];
+            const int nf = xfields(D->send[q == 0 ? side : 2 + side], sp, sb, vol);
+            xfields(D->recv[q == 0 ? side : 2 + side], rp, rb, vol);
+            for (int f = 0; f < nf; ++f) {
+                if (nsend[q] > 0)
+                    BDM_NCCL_TRY(api, api->Send(sp[f], (size_t)nsend[q] * sb[f], ncclUint8, peer, D->comm, st));
+                if (nrecv[q] > 0)
+                    BDM_NCCL_TRY(api, api->Recv(rp[f], (size_t)nrecv[q] * rb[f], ncclUint8, peer, D->comm, st));
+            }
+        }
+    }
+    BDM_NCCL_TRY(api, api->GroupEnd());
+    c->frame = D->frame;
+    c->grid_valid = false;
+    c->fused_valid = false;
+    return x_append(c, D, a, g, st);
+}
+
+// Virtual slabs: G contexts of one process on one device exchange by device copies.
+static bdm_status x_virtual(Ctx **cs, int G, bdm_agents *as, bdm_agents *gs, cudaStream_t st) {
+    Dist *D0 = cs[0]->dist;
+    for (int r = 0; r < G; ++r) {
+        bdm_status s = x_frame(cs[r], cs[r]->dist, &as[r], st);
+        if (s != BDM_OK) return s;
+    }
+    k_xfr_min<<<1, 32, 0, st>>>(D0->vframes, G);  // global frame: minimum over the slabs
+    BDM_LAUNCH_CHECK("exchange frame min");
+    for (int r = 0; r < G; ++r) {
+        bdm_status s = x_pack(cs[r], cs[r]->dist, &as[r], st);
+        if (s != BDM_OK) return s;
+    }
+    for (int r = 0; r < G; ++r) {
+        Dist *D = cs[r]->dist;
+        BDM_CUDA_TRY(cudaMemsetAsync(D->cnt + 4, 0, 4 * sizeof(long long), st));
+        if (r > 0) {  // from the left slab: its right-going migrants and aura
+            Dist *L = cs[r - 1]->dist;
+            BDM_CUDA_TRY(cudaMemcpyAsync(D->cnt + 4, L->cnt + 1, 8, cudaMemcpyDeviceToDevice, st));
+            BDM_CUDA_TRY(cudaMemcpyAsync(D->cnt + 6, L->cnt + 3, 8, cudaMemcpyDeviceToDevice, st));
+        }
+        if (r + 1 < G) {
+            Dist *R = cs[r + 1]->dist;
+            BDM_CUDA_TRY(cudaMemcpyAsync(D->cnt + 5, R->cnt + 0, 8, cudaMemcpyDeviceToDevice, st));
+            BDM_CUDA_TRY(cudaMemcpyAsync(D->cnt + 7, R->cnt + 2, 8, cudaMemcpyDeviceToDevice, st));
+        }
+    }
+    for (int r = 0; r < G; ++r)
+        BDM_CUDA_TRY(cudaMemcpyAsync(cs[r]->dist->cnt_h, cs[r]->dist->cnt, 10 * sizeof(long long),
+                                     cudaMemcpyDeviceToHost, st));
+    BDM_CUDA_TRY(cudaStreamSynchronize(st));  // one synchronization for all slabs
+    for (int r = 0; r < G; ++r) {
+        bdm_status s = x_after_counts(cs[r], cs[r]->dist, &as[r], st);
+        if (s != BDM_OK) return s;
+    }
+    for (int r = 0; r < G; ++r) {
+        Dist *D = cs[r]->dist;
+        const bool vol = as[r].volume != nullptr;
+        for (int side = 0; side < 2; ++side) {
+            const int peer = side == 0 ? r - 1 : r + 1;
+            if (peer < 0 || peer >= G) continue;
+            Dist *P = cs[peer]->dist;
+            // my recv slot `side` <- the peer's migrants towards me (its send slot 1 - side),
+            // my recv slot 2 + side <- its aura towards me (its send slot 3 - side)
+            for (int q = 0; q < 2; ++q) {
+                const int mine = q == 0 ? side : 2 + side, theirs = q == 0 ? 1 - side : 3 - side;
+                const int64_t n = D->cnt_h[4 + mine];
+                if (n <= 0) continue;
+                void *sp[7], *rp[7];
+                size_t sb[7], rb[7];
+                const int nf = xfields(P->send[theirs], sp, sb, vol);
+                xfields(D->recv[mine], rp, rb, vol);
+                for (int f = 0; f < nf; ++f)
+                    BDM_CUDA_TRY(cudaMemcpyAsync(rp[f], sp[f], (size_t)n * sb[f], cudaMemcpyDeviceToDevice, st));
+            }
+        }
+    }
+    bdm_status worst = BDM_OK;
+    for (int r = 0; r < G; ++r) {
+        Ctx *c = cs[r];
+        c->frame = c->dist->frame;
+        c->grid_valid = false;
+        c->fused_valid = false;
+        bdm_status s = x_append(c, c->dist, &as[r], &gs[r], st);
+        if (s != BDM_OK && worst == BDM_OK) worst = s;
+    }
+    return worst;
+}
+
+}  // namespace bdm
+
+// ------------------------------------------------------------------ C ABI
+using namespace bdm;
+
+namespace {
+struct DevScope {
+    int prev = -1;
+    explicit DevScope(int want) {
+        if (cudaGetDevice(&prev) != cudaSuccess) {
+            cudaGetLastError();
+            prev = -1;
+        }
+        if (prev != want) cudaSetDevice(want);
+        else prev = -1;
+    }
+    ~DevScope() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+bdm_status xfail(bdm_status s, const char *msg) {
+    set_error(msg);
+    return s;
+}
+bdm_status xcheck(const bdm_agents *a) {
+    if (!a) return xfail(BDM_EINVAL, "agents is NULL");
+    if (a->n < 0 || a->n > a->capacity) return xfail(BDM_EINVAL, "n < 0 or n > capacity");
+    if (a->n > 0 && (!a->x || !a->y || !a->z || !a->diameter || !a->id || !a->flags))
+        return xfail(BDM_EINVAL, "a required agent array is NULL");
+    return BDM_OK;
+}
+}  // namespace
+
+extern "C" {
+
+bdm_status bdm_nccl_unique_id(uint8_t id[128]) {
+    if (!id) return xfail(BDM_EINVAL, "id is NULL");
+    std::string why;
+    const NcclApi *api = nccl_api(why);
+    if (!api) return xfail(BDM_ENCCL, why.c_str());
+    ncclUniqueId u;
+    const ncclResult_t r = api->GetUniqueId(&u);
+    if (r != ncclSuccess) return xfail(BDM_ENCCL, api->GetErrorString(r));
+    static_assert(sizeof(u) == 128, "ncclUniqueId is 128 bytes");
+    memcpy(id, &u, 128);
+    return BDM_OK;
+}
+
+bdm_status bdm_dist_init(bdm_handle h, const uint8_t nccl_unique_id[128], int32_t rank,
+                         int32_t nranks, double slab_lo, double slab_hi, double radius) {
+    if (!h || !nccl_unique_id) return xfail(BDM_EINVAL, "handle or id is NULL");
+    if (nranks < 1 || rank < 0 || rank >= nranks) return xfail(BDM_EINVAL, "bad rank / nranks");
+    if (!(slab_lo <= slab_hi)) return xfail(BDM_EINVAL, "need slab_lo <= slab_hi");
+    Ctx *c = (Ctx *)h;
+    DevScope ds(c->device);
+    free_dist(c);
+    Dist *D = new Dist();
+    D->rank = rank;
+    D->nranks = nranks;
+    D->lo = rank == 0 ? -INFINITY : slab_lo;
+    D->hi = rank == nranks - 1 ? INFINITY : slab_hi;
+    D->radius = radius;
+    bdm_status s = dist_alloc(c, D);
+    if (s != BDM_OK) {
+        delete D;
+        return s;
+    }
+    c->dist = D;
+    if (nranks > 1) {
+        std::string why;
+        const NcclApi *api = nccl_api(why);
+        if (!api) {
+            free_dist(c);
+            return xfail(BDM_ENCCL, why.c_str());
+        }
+        ncclUniqueId u;
+        memcpy(&u, nccl_unique_id, 128);
+        const ncclResult_t r = api->CommInitRank(&D->comm, nranks, u, rank);
+        if (r != ncclSuccess) {
+            D->comm = nullptr;
+            free_dist(c);
+            return xfail(BDM_ENCCL, api->GetErrorString(r));
+        }
+    }
+    return BDM_OK;
+}
+
+bdm_status bdm_dist_init_virtual(bdm_handle *hs, int32_t nranks, const double *slab_lo,
+                                 const double *slab_hi, double radius) {
+    if (!hs || !slab_lo || !slab_hi || nranks < 1) return xfail(BDM_EINVAL, "bad arguments");
+    for (int r = 0; r < nranks; ++r) {
+        if (!hs[r]) return xfail(BDM_EINVAL, "a handle is NULL");
+        if (((Ctx *)hs[r])->device != ((Ctx *)hs[0])->device)
+            return xfail(BDM_EINVAL, "virtual slabs share one device");
+    }
+    for (int r = 0; r < nranks; ++r) {
+        Ctx *c = (Ctx *)hs[r];
+        DevScope ds(c->device);
+        free_dist(c);
+        Dist *D = new Dist();
+        D->rank = r;
+        D->nranks = nranks;
+        D->virt = true;
+        D->lo = r == 0 ? -INFINITY : slab_lo[r];
+        D->hi = r == nranks - 1 ? INFINITY : slab_hi[r];
+        D->radius = radius;
+        bdm_status s = dist_alloc(c, D);
+        if (s != BDM_OK) {
+            delete D;
+            return s;
+        }
+        c->dist = D;
+    }
+    std::vector<double *> fr(nranks);
+    for (int r = 0; r < nranks; ++r) {
+        Dist *D = ((Ctx *)hs[r])->dist;
+        for (int q = 0; q < nranks; ++q) D->group.push_back((Ctx *)hs[q]);
+        fr[r] = D->frame;
+    }
+    Dist *D0 = ((Ctx *)hs[0])->dist;
+    DevScope ds(((Ctx *)hs[0])->device);
+    if (cudaMalloc(&D0->vframes, nranks * sizeof(double *)) != cudaSuccess ||
+        cudaMemcpy(D0->vframes, fr.data(), nranks * sizeof(double *), cudaMemcpyHostToDevice) != cudaSuccess) {
+        cudaGetLastError();
+        return xfail(BDM_ECUDA, "virtual slab setup failed");
+    }
+    return BDM_OK;
+}
+
+bdm_status bdm_aura_exchange(bdm_handle h, bdm_agents *local, bdm_agents *ghosts, void *stream) {
+    if (!h) return xfail(BDM_EINVAL, "handle is NULL");
+    Ctx *c = (Ctx *)h;
+    if (!c->dist || c->dist->virt) return xfail(BDM_EINVAL, "bdm_dist_init first (not a virtual slab)");
+    bdm_status s;
+    if ((s = xcheck(local)) != BDM_OK || (s = xcheck(ghosts)) != BDM_OK) return s;
+    DevScope ds(c->device);
+    cudaStream_t st = (cudaStream_t)stream;
+    if (c->dist->nranks == 1) {  // one slab: only the frame
+        if ((s = x_frame(c, c->dist, local, st)) != BDM_OK) return s;
+        c->frame = c->dist->frame;
+        c->grid_valid = false;
+        c->fused_valid = false;
+        ghosts->n = 0;
+        return BDM_OK;
+    }
+    return x_nccl(c, c->dist, local, ghosts, st);
+}
+
+bdm_status bdm_aura_exchange_virtual(bdm_handle *hs, int32_t nranks, bdm_agents *locals,
+                                     bdm_agents *ghosts, void *stream) {
+    if (!hs || !locals || !ghosts || nranks < 1) return xfail(BDM_EINVAL, "bad arguments");
+    std::vector<Ctx *> cs(nranks);
+    for (int r = 0; r < nranks; ++r) {
+        cs[r] = (Ctx *)hs[r];
+        if (!cs[r] || !cs[r]->dist || !cs[r]->dist->virt || cs[r]->dist->nranks != nranks ||
+            cs[r]->dist->rank != r)
+            return xfail(BDM_EINVAL, "bdm_dist_init_virtual first (same handles, rank order)");
+        bdm_status s;
+        if ((s = xcheck(&locals[r])) != BDM_OK || (s = xcheck(&ghosts[r])) != BDM_OK) return s;
+    }
+    DevScope ds(cs[0]->device);
+    return x_virtual(cs.data(), nranks, locals, ghosts, (cudaStream_t)stream);
+}
+
+bdm_status bdm_aura_pending(bdm_handle h, int64_t need[2]) {
+    if (!h || !need) return xfail(BDM_EINVAL, "NULL argument");
+    Dist *D = ((Ctx *)h)->dist;
+    if (!D || !D->pending) {
+        need[0] = need[1] = 0;
+        return BDM_OK;
+    }
+    need[0] = D->kept + D->in_mig[0] + D->in_mig[1];
+    need[1] = D->in_aura[0] + D->in_aura[1] + D->out_mig[0] + D->out_mig[1];
+    return BDM_OK;
+}
+
+bdm_status bdm_aura_finish(bdm_handle h, bdm_agents *local, bdm_agents *ghosts, void *stream) {
+    if (!h) return xfail(BDM_EINVAL, "handle is NULL");
+    Ctx *c = (Ctx *)h;
+    if (!c->dist || !c->dist->pending) return BDM_OK;
+    bdm_status s;
+    if ((s = xcheck(local)) != BDM_OK || (s = xcheck(ghosts)) != BDM_OK) return s;
+    if (local->n != c->dist->kept) return xfail(BDM_EINVAL, "local->n must be the kept count");
+    DevScope ds(c->device);
+    s = x_append(c, c->dist, local, ghosts, (cudaStream_t)stream);
+    if (s == BDM_ECAPACITY) set_error("exchange: local or ghost capacity still too small");
+    return s;
+}
+
+}  // extern "C"

@@ -389,3 +389,57 @@ class SlabDomain:
             self.last["aura_stream_bytes"], self.last["aura_raw_bytes"] = self.aura_bytes
         self.iteration += 1
         return self.last
+
+
+# ---------------------------------------------------------------------------- native path
+class NativeSlabDomain:
+    """The x-slab step through the C ABI: one bdm_aura_exchange per slab and step (the
+    global frame, migration and aura in one call with one host synchronization, over
+    NCCL between ranks, or bdm_aura_exchange_virtual for several slabs of this process
+    on one device), then bdm_grid_build(local, ghosts) + bdm_mech_step, with no further
+    host synchronization.  The protocol is the one-round variant of SlabDomain: every
+    rank packs its leavers and its aura from the same pre-step state, and keeps its own
+    leavers as ghosts (they now belong to the neighbour and sit at the shared border),
+    so migration and aura travel together.
+
+    engines[k] / agents[k]: the slabs of this process (k = its rank in the group).  With
+    uid (bytes from Engine.nccl_unique_id on rank 0, broadcast by the caller) the single
+    slab joins the NCCL group `rank` of `nranks`; without it the slabs form a virtual
+    group."""
+
+    def __init__(self, engines, agents, bounds, params: Params, stream=None, uid=None,
+                 rank: int = 0, nranks: int = 1, ghost_capacity: int = 1 << 16):
+        self.engines = list(engines)
+        self.agents = list(agents)
+        self.params = params
+        self.stream = stream
+        self.virtual = uid is None
+        vol = self.agents[0].volume is not None
+        self.ghosts = [Agents.empty(ghost_capacity, device=a.x.device, volume=vol) for a in self.agents]
+        if self.virtual:
+            Engine.dist_init_virtual(self.engines, [b[0] for b in bounds], [b[1] for b in bounds],
+                                     params.radius)
+        else:
+            assert len(self.engines) == 1
+            lo, hi = bounds[0]
+            self.engines[0].dist_init(uid, rank, nranks, lo, hi, params.radius)
+        self.last = {}
+
+    def exchange(self):
+        if self.virtual:
+            Engine.aura_exchange_virtual(self.engines, self.agents, self.ghosts, stream=self.stream)
+        else:
+            self.engines[0].aura_exchange(self.agents[0], self.ghosts[0], stream=self.stream)
+
+    def step(self):
+        self.exchange()
+        for e, a, g in zip(self.engines, self.agents, self.ghosts):
+            e.grid_build(a, self.params.radius, stream=self.stream, ghosts=g if g.n > 0 else None)
+            e.mech_step(a, self.params, stream=self.stream)
+        self.last = {"ghosts": sum(g.n for g in self.ghosts), "local": sum(a.n for a in self.agents)}
+        return self.last
+
+    def check(self):
+        """Synchronize and report any latched device condition (grid slots, ...)."""
+        for e in self.engines:
+            e.sync(self.stream)
