@@ -27,7 +27,9 @@ EXPORTS = [
     "bdm_set_option", "bdm_grow_divide", "bdm_sir_step", "bdm_local_frame", "bdm_set_frame",
     "bdm_pack_slab", "bdm_append", "bdm_diffuse", "bdm_secrete", "bdm_chemotaxis",
     "bdm_onco_step", "bdm_tile_curve", "bdm_aura_max_size", "bdm_aura_reference",
-    "bdm_aura_encode", "bdm_aura_decode",
+    "bdm_aura_encode", "bdm_aura_decode", "bdm_nccl_unique_id", "bdm_dist_init",
+    "bdm_aura_exchange", "bdm_dist_init_virtual", "bdm_aura_exchange_virtual", "bdm_aura_pending",
+    "bdm_aura_finish",
 ]
 PACK_MIGRATE, PACK_AURA = 1, 2
 
