@@ -373,6 +373,7 @@ def run_ours(args, ws, rank, local):
     eng.step(a, pst, stream=stream)
     st_after = eng.stats()
     clocks = clk.summary()
+    graph = _graph_steps(eng, a, params, stream, K) if not args.no_graph else None
 
     ms_step = total_ms / K
     value = cfg.n / (ms_step * 1e-3)
@@ -423,6 +424,7 @@ def run_ours(args, ws, rank, local):
                           "fp64_term_ms": fp64_per_launch / fp64_peak * 1e3,
                           "hbm_peak_gbs": peaks["hbm_gbs"], "hbm_peak_source": peak_src},
         "step_ms": _dist(step_ms),
+        "graph": graph,
         "clocks": clocks,
         "gpu_launches": launches,
     }
@@ -447,6 +449,39 @@ def run_ours(args, ws, rank, local):
         except Exception as e:  # noqa: BLE001 (reported in the line)
             line["strong_cfg5"] = {"error": f"{type(e).__name__}: {e}"[:300]}
     print(json.dumps(line), flush=True)
+
+
+def _graph_steps(eng, a, params, stream, K):
+    """The same step (grid build + mechanics, a fixed launch sequence at fixed n) captured
+    once as a CUDA graph and replayed K times: the device time per step without the
+    host's launch path.  (The JSON line's value is the direct-launch number.)"""
+    import torch
+    try:
+        eng.step(a, params, stream=stream)          # leaves the fused extent for the graph
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(stream):
+            g.capture_begin(capture_error_mode="relaxed")
+            eng.grid_build(a, params.radius, stream=stream)
+            eng.mech_step(a, params, stream=stream)
+            g.capture_end()
+        torch.cuda.synchronize()
+        for _ in range(2):
+            g.replay()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(K):
+            g.replay()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        rc = eng.try_sync(stream)
+        if rc != 0:
+            return {"error": f"bdm status {rc} after the graph replays"}
+        return {"ms_per_step": e0.elapsed_time(e1) / K, "replays": K,
+                "kernels_per_step": "grid build + mechanics, one graph"}
+    except Exception as e:  # noqa: BLE001 (reported in the line)
+        return {"error": f"{type(e).__name__}: {e}"[:200]}
 
 
 def _dist(ms):
@@ -1253,7 +1288,8 @@ def main():
     ap.add_argument("--config", default="cfg2", choices=sorted(W.PRESETS) + ["aura"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--mech-kernel", type=int, default=0, help="0 tile kernel, 1 reference")
+    ap.add_argument("--mech-kernel", type=int, default=5,
+                    help="5 tile7 (default), 0 tile6, 1 per-agent reference, 4 row-broadcast")
     ap.add_argument("--tile-depth", type=int, default=0,
                     help="tile work unit: 0 auto (by agents per box), 1 or 2 tiles deep")
     ap.add_argument("--tile-order", type=int, default=0,
@@ -1264,6 +1300,8 @@ def main():
                     help="run the x-slab protocol path even on one GPU (a check of that path)")
     ap.add_argument("--ref-budget", type=float, default=150.0,
                     help="--impl reference: seconds the oracle's --steps K --warmup W should take")
+    ap.add_argument("--no-graph", action="store_true",
+                    help="skip the CUDA-graph replay measurement of the step")
     ap.add_argument("--python-protocol", action="store_true",
                     help="x-slabs through the reference protocol of slabs.py (not the C ABI)")
     ap.add_argument("--strong-steps", type=int, default=3,

@@ -412,12 +412,18 @@ bdm_status bdm_neighbor_pairs(bdm_handle h, const bdm_agents *a, double radius,
                               void *stream);
 
 /* Tuning/diagnostic options (host-side, take effect at the next launch):
- *   "mech_kernel"  0 (default) tile kernel: CTA per 4x4x4-box tile with the halo staged
- *                  in shared memory, trimmed candidate runs and a lane-parallel contact
- *                  queue (5 CTAs per SM);
+ *   "mech_kernel"  5 (default) tile kernel, batch version 7: CTA per 4x4x4-box tile with
+ *                  the halo staged in shared memory, trimmed candidate runs walked with a
+ *                  conservative fp32 contact test (D32 <= min((r'_i+r'_j)^2, R^2(1+2^-12)),
+ *                  the neighbour test for static candidates), one lane-parallel exact +
+ *                  Eq. 4.1/4.2 pass over the survivors, ordered accumulation;
+ *                  0 the same tiles with the version-6 batch (fp32 neighbour prefilter,
+ *                  exact-test compaction, contact queue);
  *                  1 per-agent reference kernel reading neighbours from global memory;
  *                  2 the first tile kernel (per-lane pair lists, no run trimming);
- *                  3 the kernel of 0 compiled for 4 CTAs per SM (no register spills).
+ *                  3 version 6 with the packed f32x2 pair walk (4 CTAs per SM);
+ *                  4 the row-broadcast kernel (2x4x8-box tiles, candidate words in
+ *                  registers, agents broadcast, ballot masks; measured slower).
  *   "sir_index_capacity"  infected agents the SIR index holds (0 = max(65536, n/16)).
  *   "dense"        1 (default) / 0: regions too crowded for the tile kernel's shared-memory
  *                  staging (> 416 agents in a 6^3-box region) go to the dense-box kernel

@@ -129,7 +129,7 @@ struct Ctx {
     uint32_t *cls2 = nullptr;
     long long *pack_counts = nullptr;  // device: left, right, remaining
     int64_t launches = 0;  // kernels launched (host-side count)
-    int mech_kernel = 0;   // option "mech_kernel": 0 tile kernel, 1 per-agent reference kernel
+    int mech_kernel = 5;   // option "mech_kernel": 5 tile7 (default), 0 tile6, 1 per-agent reference, 2-4 variants
     int prefilter = 1;     // option "prefilter": fp32 conservative candidate test in the tile kernel
     int fuse_reduce = 0;   // option "fuse_reduce": next step's a1 extent from the mech epilogue
     int dense = 1;         // option "dense": dense regions go to the dense-box kernel

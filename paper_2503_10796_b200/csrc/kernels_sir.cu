@@ -319,7 +319,10 @@ __device__ __forceinline__ void sir_agent(const SirArgs &A, SirQueue &Q, int lan
     }
 }
 
-__global__ void __launch_bounds__(kSirThreads, 4) k_sir_update(SirArgs A, DevScalars *__restrict__ sc) {
+#ifndef BDM_SIR_MINB
+#define BDM_SIR_MINB 4  // resident blocks per SM the register budget is set for
+#endif
+__global__ void __launch_bounds__(kSirThreads, BDM_SIR_MINB) k_sir_update(SirArgs A, DevScalars *__restrict__ sc) {
     if (sc->overflow) return;
     __shared__ SirQueue Qs[kSirThreads / 32];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;

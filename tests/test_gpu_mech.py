@@ -350,3 +350,39 @@ def test_cfg2_full_size_teacher_forced(eng, orc):
         assert np.array_equal(after["id"], before["id"][perm])
         del before, after
         torch.cuda.empty_cache()
+
+
+@pytest.mark.slow
+def test_cfg2_bench_instance_teacher_forced(orc):
+    """The exact instance bench.py times: cfg2 at full size (10M agents), the default
+    mechanics kernel, counters off (collect_stats = False) and the next step's grid
+    extent fused into the mechanics epilogue (fuse_reduce = 1), three consecutive steps
+    without a synchronizing check in between; after each, 100k sampled agents
+    recomputed by the oracle from the GPU's input state must match bit-exactly."""
+    import torch
+    from paper_2503_10796_b200 import Engine, Params
+    cfg = W.CFG2
+    e = Engine(0, cfg.n)
+    e.set_option("fuse_reduce", 1)
+    a = gpu_init(e, cfg)
+    gp = Params(k=cfg.k, gamma=cfg.gamma, dt=cfg.dt, max_displacement=cfg.max_disp,
+                force_threshold=cfg.force_threshold, detect_static=cfg.detect_static)
+    op = orc.mech_params(k=cfg.k, gamma=cfg.gamma, dt=cfg.dt, max_disp=cfg.max_disp,
+                         force_threshold=cfg.force_threshold, detect_static=cfg.detect_static)
+    rng = np.random.default_rng(1)
+    for t in range(3):
+        before = a.numpy()
+        e.step(a, gp)                       # asynchronous, as in the timed loop
+        after = a.numpy()
+        sample = rng.choice(cfg.n, 100_000, replace=False)
+        out, _ = orc.mech_step(before, op, sample=sample)
+        pos = {int(i): k for k, i in enumerate(after["id"])}
+        idx = np.array([pos[int(before["id"][i])] for i in sample])
+        for k in ("x", "y", "z", "flags"):
+            assert np.array_equal(after[k][idx], out[k]), (t, k)
+        perm, _ = orc.sorted_order(before)
+        assert np.array_equal(after["id"], before["id"][perm])
+        del before, after
+        torch.cuda.empty_cache()
+    e.sync()
+    e.close()
