@@ -466,14 +466,15 @@ def _graph_steps(eng, a, params, stream, K):
             eng.mech_step(a, params, stream=stream)
             g.capture_end()
         torch.cuda.synchronize()
-        for _ in range(2):
-            g.replay()
-        torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(K):
-            g.replay()
-        e1.record(stream)
+        with torch.cuda.stream(stream):  # replays go to the current stream
+            for _ in range(2):
+                g.replay()
+            torch.cuda.synchronize()
+            e0.record(stream)
+            for _ in range(K):
+                g.replay()
+            e1.record(stream)
         torch.cuda.synchronize()
         rc = eng.try_sync(stream)
         if rc != 0:
@@ -688,9 +689,9 @@ def cpu_baseline_sir(a, cfg, steps=3):
 
 def _traffic(kernel, alg_bytes):
     """DRAM bytes per launch of `kernel` from the committed ncu --set full capture
-    (profiles/r01/traffic.json, written from the .ncu-rep summaries), next to the
+    (profiles/r02/traffic.json, written from the .ncu-rep summaries), next to the
     algorithmic bytes of the same launch; None if there is no capture."""
-    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01", "traffic.json")
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r02", "traffic.json")
     try:
         with open(path) as f:
             t = json.load(f)[kernel]
