@@ -1021,6 +1021,9 @@ def _slab_phase(args, ws, rank, local, strong, steps, warmup):
         obj = [eng.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         uid = obj[0]
+    elif args.force_slabs:
+        uid = bytes(128)  # one rank: the exchange runs (frame only), no NCCL
+    if uid is not None:
         dom = NativeSlabDomain([eng], [a], [(lo, hi)], params, stream=stream, uid=uid, rank=rank,
                                nranks=ws, ghost_capacity=int(0.02 * n_est) + 65536)
     else:
