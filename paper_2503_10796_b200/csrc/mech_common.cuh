@@ -71,7 +71,8 @@ struct Counts {
 // the output goes to lrank[s] when ghosts are present.
 __device__ __forceinline__ void finish_agent(const MechArgs &A, int64_t s, double xi, double yi,
                                              double zi, double Fx, double Fy, double Fz,
-                                             bool is_static, int nnz, Counts &c) {
+                                             bool is_static, int nnz, Counts &c,
+                                             bool track = true) {
     const int64_t o = A.lrank ? (int64_t)A.lrank[s] : s;
     double Dx = 0.0, Dy = 0.0, Dz = 0.0;
     if (!is_static) {
@@ -97,10 +98,12 @@ __device__ __forceinline__ void finish_agent(const MechArgs &A, int64_t s, doubl
     }
     const bool moved = (Dx != 0.0 || Dy != 0.0 || Dz != 0.0);
     c.moved += moved ? 1u : 0u;
-    c.lo0 = fmin(c.lo0, nx); c.hi0 = fmax(c.hi0, nx);
-    c.lo1 = fmin(c.lo1, ny); c.hi1 = fmax(c.hi1, ny);
-    c.lo2 = fmin(c.lo2, nz); c.hi2 = fmax(c.hi2, nz);
-    c.dmax = fmax(c.dmax, A.sd[s]);
+    if (track) {  // (the tile kernels skip it where no extremum can move, see k_mech_tile6)
+        c.lo0 = fmin(c.lo0, nx); c.hi0 = fmax(c.hi0, nx);
+        c.lo1 = fmin(c.lo1, ny); c.hi1 = fmax(c.hi1, ny);
+        c.lo2 = fmin(c.lo2, nz); c.hi2 = fmax(c.hi2, nz);
+        c.dmax = fmax(c.dmax, A.sd[s]);
+    }
     c.stat += is_static ? 1u : 0u;
     A.ox[o] = nx;
     A.oy[o] = ny;

@@ -456,7 +456,6 @@ struct Tile6SmemT {
     using WarpT = typename std::conditional<kV7, Warp7, Warp6>::type;
     GridView g;
     float R2f, Lf;
-    float rmaxf;                            // fp32 r' bound of every staged agent (tile7)
     int use_pf, edge_only;                  // edge_only: fused extent from boundary tiles only
     int tinfo[2][6];                        // drawn unit (ping-pong): t, tx, ty, tz, ta, tb
     int lo_box[3], hi_box[3];               // boxes that can hold a new extremum (see below)
@@ -877,14 +876,6 @@ __device__ __forceinline__ void tile7_batch(const MechArgs &A, const Tile6SmemT<
         if (active) {
             cand_static = A.detect_static && !(fi & kChanged) && ((fi >> BDM_FLAG_NNZ_SHIFT) & 3u) <= 1u;
             pi = S.f.P[mi];
-            // boxes are trimmed at the contact reach r'_i + r'_max (every staged r' is at
-            // most rmaxf: same margin as the walk's test) unless the lane needs the
-            // whole neighbour set
-            float T2 = R2f;
-            if (!kStats && !cand_static) {
-                const float t = pi.w + S.rmaxf;
-                T2 = fminf(R2f, t * t);
-            }
             if (cand_static) pi.w = INFINITY;  // whole neighbour set (a5 pull test)
             const uint32_t v = S.lbxyz[lbi];
             const int lx = (int)(v & 7u), ly = (int)((v >> 3) & 7u), lz = (int)((v >> 6) & 15u);
@@ -900,10 +891,10 @@ __device__ __forceinline__ void tile7_batch(const MechArgs &A, const Tile6SmemT<
                 const int row = lbi - 43 + dzi * 36 + dyi * 6;  // box (lx-1, ly-1+dyi, lz-1+dzi)
                 if (kStats) ca += (int)(S.off[row + 3] - S.off[row]);
                 const float b2 = gz2[dzi] + gy2[dyi];
-                const int xs = (b2 + gx2l <= T2) ? 0 : 1;
-                const int xe = (b2 + gx2h <= T2) ? 3 : 2;
+                const int xs = (b2 + gx2l <= R2f) ? 0 : 1;
+                const int xe = (b2 + gx2h <= R2f) ? 3 : 2;
                 const uint32_t rs = S.off[row + xs], re = S.off[row + xe];
-                const bool keep = b2 <= T2 && re > rs;
+                const bool keep = b2 <= R2f && re > rs;
                 Wp.u.a.run[nr][lane] = (rs << 4) | (re << 20);
                 walk += keep ? (int)(re - rs) : 0;
                 nr += keep ? 1 : 0;
@@ -1057,7 +1048,6 @@ __global__ void __launch_bounds__(kT6Threads, kMinBlocks) k_mech_tile6(MechArgs 
         S.g = g;
         S.R2f = (float)(g.R2 * (1.0 + 0x1p-12));
         S.Lf = (float)g.L;
-        S.rmaxf = (float)(sc->dmax_prev * 0.5 + 0x1p-16 * g.L);
         const double amax = fmax(fmax(fmax(fabs(g.o0), fabs(g.o1)), fmax(fabs(g.o2), fabs(sc->hi[0]))),
                                  fmax(fabs(sc->hi[1]), fabs(sc->hi[2])));
         S.use_pf = allow_prefilter && amax < 0x1p30 * g.L;
@@ -1095,14 +1085,10 @@ __global__ void __launch_bounds__(kT6Threads, kMinBlocks) k_mech_tile6(MechArgs 
     // tiles are taken from a device counter: no tail imbalance between the persistent
     // CTAs (a static stride left 8 % on the table at cfg2); the broadcast slot
     // alternates so a slow warp still reads this tile's number while the next is drawn
-    // Thread 0 draws each unit one tile ahead (the atomic's latency hides behind a whole
-    // tile) and decodes it for the CTA at the top of the iteration.
-    int t_next = tid == 0 ? (int)atomicAdd(&sc->tile_next, 1u) : 0;
     for (int it = 0;; ++it) {
-        if (tid == 0) {
+        if (tid == 0) {  // thread 0 draws the unit and decodes it for the CTA
             int *const ti = S.tinfo[it & 1];
-            const int t = t_next;
-            if (t < ntiles) t_next = (int)atomicAdd(&sc->tile_next, 1u);
+            const int t = (int)atomicAdd(&sc->tile_next, 1u);
             int x = 0, y = 0, z = 0;
             uint32_t a = (uint32_t)t, b = 0xFFFFFFFFu;  // the unit's tiles (slot numbers)
             if (t < ntiles) {

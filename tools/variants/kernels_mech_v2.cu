@@ -456,7 +456,6 @@ struct Tile6SmemT {
     using WarpT = typename std::conditional<kV7, Warp7, Warp6>::type;
     GridView g;
     float R2f, Lf;
-    float rmaxf;                            // fp32 r' bound of every staged agent (tile7)
     int use_pf, edge_only;                  // edge_only: fused extent from boundary tiles only
     int tinfo[2][6];                        // drawn unit (ping-pong): t, tx, ty, tz, ta, tb
     int lo_box[3], hi_box[3];               // boxes that can hold a new extremum (see below)
@@ -806,19 +805,17 @@ __device__ __forceinline__ void tile6_batch(const MechArgs &A, const Tile6SmemT<
 }
 
 
-// The flattened walk of one lane over its trimmed runs (see tile7_batch); returns the
-// number of survivors, listed (byte offsets m << 4) in Wp.u.a.lst[.][lane].
+// The flattened walk of one lane over trimmed runs (see tile7_batch), from staged byte
+// offset mo in the run ending at eo, the following runs at rrow[j], rrow[j + 32], ...;
+// returns the number of survivors, listed (byte offsets m << 4) in Wp.u.a.lst[.][lane].
 template <bool kStats, bool kMin, int kTZ>
 __device__ __forceinline__ int tile7_walk(const Tile6SmemT<false, kTZ, true> &S, Warp7 &Wp, int lane,
-                                          float4 pi, int cmax, int M, float R2f) {
+                                          float4 pi, int cmax, int M, float R2f,
+                                          const uint32_t *rrow, uint32_t mo, uint32_t eo, int j) {
     int cnt = 0;
     const char *pb = reinterpret_cast<const char *>(&S.f.P[0]);
     const uint32_t mlast = (uint32_t)M << 4;
     uint16_t *const lrow = &Wp.u.a.lst[0][lane];
-    const uint32_t *const rrow = &Wp.u.a.run[0][lane];
-    uint32_t cur = rrow[0];
-    uint32_t mo = cur & 0xFFFFu, eo = cur >> 16;
-    int j = 32;
     uint32_t nxt = rrow[j];
 #pragma unroll 4
     for (int it = 0; it < cmax; ++it) {
@@ -865,7 +862,7 @@ __device__ __forceinline__ void tile7_batch(const MechArgs &A, const Tile6SmemT<
     const float R2f = S.R2f, Lf = S.Lf;
     const int k = klo + lane;
     const uint32_t gk = k < n0 ? g0 + (uint32_t)k : g1 + (uint32_t)(k - n0);
-    int mi = M, nr = 0, walk = 0, ca = 0;
+    int mi = M, nr = 0, walk = 0, ca = 0, offself = 0;
     uint32_t fi = 0;
     bool active = false, cand_static = false;
     float4 pi = make_float4(-kSentinel, -kSentinel, -kSentinel, 0.f);
@@ -877,14 +874,6 @@ __device__ __forceinline__ void tile7_batch(const MechArgs &A, const Tile6SmemT<
         if (active) {
             cand_static = A.detect_static && !(fi & kChanged) && ((fi >> BDM_FLAG_NNZ_SHIFT) & 3u) <= 1u;
             pi = S.f.P[mi];
-            // boxes are trimmed at the contact reach r'_i + r'_max (every staged r' is at
-            // most rmaxf: same margin as the walk's test) unless the lane needs the
-            // whole neighbour set
-            float T2 = R2f;
-            if (!kStats && !cand_static) {
-                const float t = pi.w + S.rmaxf;
-                T2 = fminf(R2f, t * t);
-            }
             if (cand_static) pi.w = INFINITY;  // whole neighbour set (a5 pull test)
             const uint32_t v = S.lbxyz[lbi];
             const int lx = (int)(v & 7u), ly = (int)((v >> 3) & 7u), lz = (int)((v >> 6) & 15u);
@@ -900,11 +889,12 @@ __device__ __forceinline__ void tile7_batch(const MechArgs &A, const Tile6SmemT<
                 const int row = lbi - 43 + dzi * 36 + dyi * 6;  // box (lx-1, ly-1+dyi, lz-1+dzi)
                 if (kStats) ca += (int)(S.off[row + 3] - S.off[row]);
                 const float b2 = gz2[dzi] + gy2[dyi];
-                const int xs = (b2 + gx2l <= T2) ? 0 : 1;
-                const int xe = (b2 + gx2h <= T2) ? 3 : 2;
+                const int xs = (b2 + gx2l <= R2f) ? 0 : 1;
+                const int xe = (b2 + gx2h <= R2f) ? 3 : 2;
                 const uint32_t rs = S.off[row + xs], re = S.off[row + xe];
-                const bool keep = b2 <= T2 && re > rs;
+                const bool keep = b2 <= R2f && re > rs;
                 Wp.u.a.run[nr][lane] = (rs << 4) | (re << 20);
+                if (r == 4) offself = walk + (mi - (int)rs);  // the own box's row
                 walk += keep ? (int)(re - rs) : 0;
                 nr += keep ? 1 : 0;
             }
@@ -912,14 +902,69 @@ __device__ __forceinline__ void tile7_batch(const MechArgs &A, const Tile6SmemT<
     }
     Wp.u.a.run[nr][lane] = ((uint32_t)M << 4) | (0xFFFFu << 16);  // sentinel run (see tile6)
     Wp.chg[lane] = 0;
-    const int cmax = __reduce_max_sync(0xffffffffu, walk);
     const unsigned cs_mask = __ballot_sync(0xffffffffu, cand_static);
+    // ---- balance: an agent's walk is cut into np <= 4 pieces of T steps, one lane per
+    // piece, pieces in agent order; T is the least length for which the pieces fit in 32
+    // lanes (batches hold nc / ceil(nc / 32) agents, so a few lanes are spare).  A piece
+    // stops after T steps exactly or runs into the agent's sentinel run (its last piece).
+    const int cmax = __reduce_max_sync(0xffffffffu, walk);
+    int T;
+    {
+        const int W = __reduce_add_sync(0xffffffffu, walk);
+        int lo = max((W + 31) >> 5, (cmax + 3) >> 2), hi = cmax;
+        while (lo < hi) {  // warp-uniform
+            const int mid = (lo + hi) >> 1;
+            const int q = (walk > 0) + (walk > mid) + (walk > 2 * mid) + (walk > 3 * mid);
+            if (__reduce_add_sync(0xffffffffu, q) <= 32) hi = mid; else lo = mid + 1;
+        }
+        T = lo;
+    }
+    const int np = (walk > 0) + (walk > T) + (walk > 2 * T) + (walk > 3 * T);
+    int pincl = np;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, pincl, o);
+        if (lane >= o) pincl += y;
+    }
+    const int p0 = pincl - np;  // this agent's first piece lane
+    const int npieces = __shfl_sync(0xffffffffu, pincl, 31);
+    // piece lane -> agent, through the scratch row of the survivor lists (each lane reads
+    // its own entry before its walk can write there)
+    for (int q = 0; q < np; ++q) Wp.u.a.lst[kK6Max][p0 + q] = (uint16_t)lane;
     __syncwarp();
+    const bool has = lane < npieces;
+    const int a = has ? (int)Wp.u.a.lst[kK6Max][lane] : 0;
+    const int jp = lane - __shfl_sync(0xffffffffu, p0, a);  // piece number
+    const int a_mi = __shfl_sync(0xffffffffu, mi, a);
+    const int a_self = __shfl_sync(0xffffffffu, offself, a);
+    float4 pa;
+    pa.x = __shfl_sync(0xffffffffu, pi.x, a);
+    pa.y = __shfl_sync(0xffffffffu, pi.y, a);
+    pa.z = __shfl_sync(0xffffffffu, pi.z, a);
+    pa.w = __shfl_sync(0xffffffffu, pi.w, a);
+    __syncwarp();
+    const uint32_t *const rrow = &Wp.u.a.run[0][a];
+    uint32_t mo = (uint32_t)M << 4, eo = 0xFFFFu;  // no piece: the sentinel agent only
+    int jr = 32;
+    const int s0 = jp * T;
+    if (has) {
+        int s = s0, r = 0;
+        uint32_t cur = rrow[0];
+        while (s >= (int)((cur >> 20) - ((cur & 0xFFFFu) >> 4))) {
+            s -= (int)((cur >> 20) - ((cur & 0xFFFFu) >> 4));
+            cur = rrow[32 * ++r];
+        }
+        mo = (cur & 0xFFFFu) + ((uint32_t)s << 4);
+        eo = cur >> 16;
+        jr = 32 * (r + 1);
+    }
     // ---- phase 1: the flattened walk with the contact (or neighbour) test; the min with
     // R2f only matters for static candidates (r'_i = inf), so warps without one skip it
-    int cnt = cs_mask ? tile7_walk<kStats, true, kTZ>(S, Wp, lane, pi, cmax, M, R2f)
-                      : tile7_walk<kStats, false, kTZ>(S, Wp, lane, pi, cmax, M, R2f);
-    if (active) --cnt;  // the agent itself (D32 = 0) is always among the survivors
+    int cnt = cs_mask ? tile7_walk<kStats, true, kTZ>(S, Wp, lane, pa, T, M, R2f, rrow, mo, eo, jr)
+                      : tile7_walk<kStats, false, kTZ>(S, Wp, lane, pa, T, M, R2f, rrow, mo, eo, jr);
+    // the agent itself (D32 = 0) is always a survivor, in the piece that walks past it
+    const bool has_self = has && a_self >= s0 && a_self < s0 + T;
+    if (has_self) --cnt;
     int cincl = cnt;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -928,6 +973,9 @@ __device__ __forceinline__ void tile7_batch(const MechArgs &A, const Tile6SmemT<
     }
     const int my_off = cincl - cnt;
     const int total = __shfl_sync(0xffffffffu, cincl, 31);
+    // the agent's survivors: from its first piece's offset to its last piece's end
+    const int a_lo = __shfl_sync(0xffffffffu, my_off, p0 & 31);
+    const int a_hi = __shfl_sync(0xffffffffu, cincl, (p0 + np - 1) & 31);
     Counts c;
     if (__any_sync(0xffffffffu, cnt >= kK6Max - 1) || total > kQ7Cap) {
         // a full list may have lost survivors: the reference formulation for the batch
@@ -936,13 +984,14 @@ __device__ __forceinline__ void tile7_batch(const MechArgs &A, const Tile6SmemT<
         return;
     }
     {
-        const uint32_t tag = ((uint32_t)mi << 9) | ((uint32_t)lane << 18);
-        const uint32_t self = (uint32_t)mi << 4;
-        const int cmx = __reduce_max_sync(0xffffffffu, active ? cnt + 1 : cnt);
+        const uint32_t tag = ((uint32_t)a_mi << 9) | ((uint32_t)a << 18);
+        const uint32_t self = (uint32_t)a_mi << 4;
+        const int nl = has_self ? cnt + 1 : cnt;
+        const int cmx = __reduce_max_sync(0xffffffffu, nl);
         int wo = my_off;
         for (int jj = 0; jj < cmx; ++jj) {
             const uint32_t v = Wp.u.a.lst[jj][lane];
-            if (jj < (active ? cnt + 1 : cnt) && v != self) Wp.pr[wo++] = (v >> 4) | tag;
+            if (jj < nl && v != self) Wp.pr[wo++] = (v >> 4) | tag;
         }
     }
     __syncwarp();
@@ -1017,7 +1066,7 @@ __device__ __forceinline__ void tile7_batch(const MechArgs &A, const Tile6SmemT<
         int nnz = 0;
         uint32_t my_cont = 0, my_nbr = 0;
 #pragma unroll 2
-        for (int q = my_off; q < my_off + cnt; ++q) {
+        for (int q = a_lo; q < a_hi; ++q) {
             const uint32_t ev = Wp.pr[q];
             const int m = (int)(ev & 511u);
             const double s_ = sq[q];
@@ -1057,7 +1106,6 @@ __global__ void __launch_bounds__(kT6Threads, kMinBlocks) k_mech_tile6(MechArgs 
         S.g = g;
         S.R2f = (float)(g.R2 * (1.0 + 0x1p-12));
         S.Lf = (float)g.L;
-        S.rmaxf = (float)(sc->dmax_prev * 0.5 + 0x1p-16 * g.L);
         const double amax = fmax(fmax(fmax(fabs(g.o0), fabs(g.o1)), fmax(fabs(g.o2), fabs(sc->hi[0]))),
                                  fmax(fabs(sc->hi[1]), fabs(sc->hi[2])));
         S.use_pf = allow_prefilter && amax < 0x1p30 * g.L;
@@ -1095,14 +1143,10 @@ __global__ void __launch_bounds__(kT6Threads, kMinBlocks) k_mech_tile6(MechArgs 
     // tiles are taken from a device counter: no tail imbalance between the persistent
     // CTAs (a static stride left 8 % on the table at cfg2); the broadcast slot
     // alternates so a slow warp still reads this tile's number while the next is drawn
-    // Thread 0 draws each unit one tile ahead (the atomic's latency hides behind a whole
-    // tile) and decodes it for the CTA at the top of the iteration.
-    int t_next = tid == 0 ? (int)atomicAdd(&sc->tile_next, 1u) : 0;
     for (int it = 0;; ++it) {
-        if (tid == 0) {
+        if (tid == 0) {  // thread 0 draws the unit and decodes it for the CTA
             int *const ti = S.tinfo[it & 1];
-            const int t = t_next;
-            if (t < ntiles) t_next = (int)atomicAdd(&sc->tile_next, 1u);
+            const int t = (int)atomicAdd(&sc->tile_next, 1u);
             int x = 0, y = 0, z = 0;
             uint32_t a = (uint32_t)t, b = 0xFFFFFFFFu;  // the unit's tiles (slot numbers)
             if (t < ntiles) {
