@@ -42,6 +42,7 @@ struct SirArgs {
     double Rq, invC;                  // coarse test: padded radius, 1 / (16 L)
     int D, B, cf;                     // fine boxes / coarse blocks per axis; boxes per block
     uint32_t k0, k1, step;
+    uint32_t rk0[10], rk1[10];        // Philox round keys k + r (0x9E3779B9, 0xBB67AE85)
     // infected index
     unsigned long long *__restrict__ keys;   // stamp << 40 | box key
     unsigned long long *__restrict__ heads;  // stamp << 32 | first infected slot
@@ -66,6 +67,23 @@ __device__ __forceinline__ int sir_box(double v, double L, int D) {
 
 __device__ __forceinline__ unsigned long long box_hash(unsigned long long key, int tbits) {
     return (key * 0x9E3779B97F4A7C15ull) >> (64 - tbits);
+}
+
+// Philox4x32-10 (bdm_internal.cuh) with the round keys precomputed on the host: they
+// enter the XORs as constant-bank operands instead of two adds per round
+__device__ __forceinline__ U4 philox10_rk(const SirArgs &A, uint32_t c0, uint32_t c1, uint32_t c2,
+                                         uint32_t c3) {
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        const uint32_t lo0 = 0xD2511F53u * c0, hi0 = __umulhi(0xD2511F53u, c0);
+        const uint32_t lo1 = 0xCD9E8D57u * c2, hi1 = __umulhi(0xCD9E8D57u, c2);
+        const uint32_t n0 = hi1 ^ c1 ^ A.rk0[r], n2 = hi0 ^ c3 ^ A.rk1[r];
+        c0 = n0;
+        c1 = lo1;
+        c2 = n2;
+        c3 = lo0;
+    }
+    return U4{c0, c1, c2, c3};
 }
 
 __device__ __forceinline__ double min_image(double d, double side, double half) {
@@ -164,7 +182,7 @@ __device__ __forceinline__ bool coarse_hit(const SirArgs &A, double px, double p
     return hit;
 }
 
-__device__ __noinline__ bool infected_fine(const SirArgs &A, double px, double py, double pz);
+__device__ __forceinline__ bool infected_fine(const SirArgs &A, double px, double py, double pz);
 
 __device__ __forceinline__ bool infected_within(const SirArgs &A, double px, double py, double pz) {
     if (!coarse_hit(A, px, py, pz)) return false;
@@ -172,7 +190,7 @@ __device__ __forceinline__ bool infected_within(const SirArgs &A, double px, dou
 }
 
 // Exact search of the 27 fine boxes (same box formula as the index), minimum image.
-__device__ __noinline__ bool infected_fine(const SirArgs &A, double px, double py, double pz) {
+__device__ __forceinline__ bool infected_fine(const SirArgs &A, double px, double py, double pz) {
     const int bx = sir_box(px, A.L, A.D), by = sir_box(py, A.L, A.D), bz = sir_box(pz, A.L, A.D);
     const int D = A.D;
     for (int dz = -1; dz <= 1; ++dz)
@@ -208,19 +226,17 @@ __device__ __noinline__ bool infected_fine(const SirArgs &A, double px, double p
 }
 
 // Alg. 9 wrap: el = fmod(el, max); if el < 0: el = max + el (R20, literal).  For
-// -max < el < 2 max, fmod is exact and equals el or el - max (Sterbenz: el - max is
-// exact for max <= el <= 2 max), so the fast path is bit-identical to fmod.
+// -max < el < 2 max, fmod is exact and equals el (|el| < max, sign kept: -0 stays -0 and
+// is not < 0) or el - max (max <= el < 2 max, exact by Sterbenz), so the fast path is
+// bit-identical to the literal form: el < 0 -> max + el, el >= max -> el - max, else el.
 // fmod out of line: |el| >= max never happens in a unit-step walk, and an inlined fmod
 // costs the whole kernel registers (spills): 1.94 -> 1.79 ms/step at cfg4
 __device__ __noinline__ double fmod_slow(double el, double max_bound) { return fmod(el, max_bound); }
 __device__ __forceinline__ double wrap_alg9(double el, double max_bound) {
-    double r;
-    if (el >= 0.0 && el < max_bound) r = el;
-    else if (el >= max_bound && el <= 2.0 * max_bound) r = el - max_bound;
-    else if (el < 0.0 && el > -max_bound) r = el;
-    else r = fmod_slow(el, max_bound);
-    if (r < 0.0) r = max_bound + r;
-    return r;
+    if (el > -max_bound && el < 2.0 * max_bound)
+        return el < 0.0 ? max_bound + el : (el >= max_bound ? el - max_bound : el);
+    const double r = fmod_slow(el, max_bound);
+    return r < 0.0 ? max_bound + r : r;
 }
 
 // Infection queries (S agents whose draw passed, ~p_inf of them) are compacted into a
@@ -244,7 +260,7 @@ __device__ __forceinline__ void sir_resolve(const SirArgs &A, uint32_t i, double
         st = 1;
         ++cn;
         const uint32_t me = A.id ? A.id[i] : i;
-        const U4 r = philox10(me, 0u, A.step, 1u, A.k0, A.k1);
+        const U4 r = philox10_rk(A, me, 0u, A.step, 1u);
         if (uniform32(r.a) < A.p_rec) st = 2;  // Alg. 8 in sequence (R18)
     }
     A.state[i] = st;
@@ -260,13 +276,13 @@ __device__ __forceinline__ void sir_agent(const SirArgs &A, SirQueue &Q, int lan
                                           uint8_t st, int &qn, uint32_t &cs, uint32_t &ci,
                                           uint32_t &cr, uint32_t &cn) {
     const uint32_t me = valid ? (A.id ? A.id[i] : (uint32_t)i) : 0u;
-    const U4 w = philox10(me, 0u, A.step, 0u, A.k0, A.k1);
+    const U4 w = philox10_rk(A, me, 0u, A.step, 0u);
     // Alg. 7: an S agent whose draw passed (R17: strict '<', u = w * 2^-32) is queued
     const bool query = valid && st == 0 && uniform32(w.d) < A.p_inf;
     if (valid && !query) {
         // Alg. 8: recovery (own state in sequence, R18)
         if (st == 1) {
-            const U4 r = philox10(me, 0u, A.step, 1u, A.k0, A.k1);
+            const U4 r = philox10_rk(A, me, 0u, A.step, 1u);
             if (uniform32(r.a) < A.p_rec) {
                 st = 2;
                 A.state[i] = st;
@@ -455,6 +471,10 @@ bdm_status launch_sir_step(Ctx *c, bdm_agents *a, const bdm_params *p, double si
     A.B = B;
     A.k0 = (uint32_t)p->seed;
     A.k1 = (uint32_t)(p->seed >> 32);
+    for (int r = 0; r < 10; ++r) {
+        A.rk0[r] = A.k0 + 0x9E3779B9u * (uint32_t)r;
+        A.rk1[r] = A.k1 + 0xBB67AE85u * (uint32_t)r;
+    }
     A.step = p->step;
     A.keys = W.keys; A.heads = (unsigned long long *)W.heads; A.next = W.next;
     A.stamp = W.stamp;

@@ -39,14 +39,16 @@ def _start(orc, n, side):
     return s
 
 
+@pytest.mark.parametrize("stats", [True, False], ids=["counters", "timed_instance"])
 @pytest.mark.parametrize("n,steps", [(1, 6), (257, 10), (2000, 12)])
-def test_cfg3_reduced_trajectory(eng, orc, n, steps):
-    """cfg3 density (1M per mm^3) at reduced N; every step bit-exact by id."""
+def test_cfg3_reduced_trajectory(eng, orc, n, steps, stats):
+    """cfg3 density (1M per mm^3) at reduced N; every step bit-exact by id (with the
+    counters on, and off as the bench runs it: contact-only prefilters)."""
     from paper_2503_10796_b200 import Agents, Params
     side = 1000.0 * (n / 1e6) ** (1 / 3)
     o = _start(orc, n, side)
     a = Agents.from_numpy(o, capacity=n * 2 ** (steps // 2 + 2))
-    gp = Params(seed=1, collect_stats=True)
+    gp = Params(seed=1, collect_stats=stats)
     op = orc.mech_params()
     for t in range(steps):
         gp.step = t

@@ -58,7 +58,7 @@ def params_pair(orc, cfg, **over):
     gp = Params(k=kw["k"], gamma=kw["gamma"], dt=kw["dt"], max_displacement=kw["max_disp"],
                 force_threshold=kw["force_threshold"], detect_static=kw["detect_static"],
                 boundary=kw.get("boundary", 0), lo=kw.get("lo", (0, 0, 0)),
-                hi=kw.get("hi", (0, 0, 0)), collect_stats=True)
+                hi=kw.get("hi", (0, 0, 0)), collect_stats=kw.get("stats", True))
     op = orc.mech_params(k=kw["k"], gamma=kw["gamma"], dt=kw["dt"], max_disp=kw["max_disp"],
                          force_threshold=kw["force_threshold"],
                          detect_static=kw["detect_static"], boundary=kw.get("boundary", 0),
@@ -386,3 +386,43 @@ def test_cfg2_bench_instance_teacher_forced(orc):
         torch.cuda.empty_cache()
     e.sync()
     e.close()
+
+
+@pytest.mark.parametrize("case", ["cfg2@20011", "dense_all", "dense_cluster_static", "dense_groups",
+                                  "crowded25", "crowded90", "cap"])
+def test_counters_off_bit_exact(eng, orc, case):
+    """The timed instances run without counters (collect_stats = 0): there the tile7 and
+    dense kernels test contacts only in fp32 (r'_i + r'_j) for every lane that needs no
+    more, and trim boxes at the contact reach.  Same populations as the counting tests,
+    state bit-exact after every step."""
+    from paper_2503_10796_b200 import Agents
+    if case.startswith("cfg2"):
+        cfg = W.cfg2_scaled(20011)
+        s = orc_init(orc, cfg)
+        gp, op = params_pair(orc, cfg, stats=False)
+    elif case.startswith("dense"):
+        n_bg, side_bg, n_cl, side_cl, static, tau = {
+            "dense_all": (0, 1.0, 6000, 40.0, False, 0.0),
+            "dense_cluster_static": (20000, 220.0, 3000, 24.0, True, 1e-3),
+            "dense_groups": (4000, 120.0, 1500, 14.0, True, 0.0)}[case]
+        s = _dense_population(orc, n_bg, side_bg, n_cl, side_cl, 5)
+        gp, op = params_pair(orc, W.CFG1, detect_static=static, force_threshold=tau, stats=False)
+    elif case.startswith("crowded"):
+        k = int(case[7:])
+        rng = np.random.default_rng(k)
+        v = rng.normal(size=(k, 3))
+        v *= (rng.uniform(0.2, 0.9, k) ** (1 / 3) * 9.0 / np.linalg.norm(v, axis=1))[:, None]
+        pts = np.vstack([[0, 0, 0], v, rng.uniform(-60, 60, (300, 3))])
+        n = len(pts)
+        s = {"x": pts[:, 0].copy(), "y": pts[:, 1].copy(), "z": pts[:, 2].copy(),
+             "d": np.full(n, 10.0), "id": np.arange(n, dtype=np.uint32),
+             "flags": np.full(n, 4, np.uint32)}
+        gp, op = params_pair(orc, W.CFG1, stats=False)
+    else:  # heavy overlap, large dt: the cap binds
+        s = orc.init_spheres(3000, 2, 40.0, 10.0)
+        gp, op = params_pair(orc, W.CFG1, dt=1.0, stats=False)
+    a = Agents.from_numpy(s)
+    for t in range(3):
+        eng.step(a, gp, sync=True)
+        s, _ = orc.step_full(s, op)
+        assert_state_equal(a.numpy(), s, f"{case} step {t}")
