@@ -253,7 +253,6 @@ __device__ __forceinline__ void row_merge(const Counts &c, RowWarp &Wp, int side
 template <bool kStats>
 __device__ __forceinline__ void row_group(const MechArgs &A, const RowSmem &S, RowWarp &Wp,
                                           int gn, int sides, int lane, int tile) {
-    const unsigned lt = (1u << lane) - 1u;
     Counts c;
     const int k = lane;
     bool act = false, cs = false;
