@@ -200,23 +200,48 @@ struct Src {
     const uint32_t *__restrict__ gid, *__restrict__ gflags;
 };
 
-__global__ void __launch_bounds__(256) k_key(Src S, const DevScalars *__restrict__ sc,
-                                             uint32_t *__restrict__ key,
-                                             uint32_t *__restrict__ rank,
-                                             uint32_t *__restrict__ counts) {
+// kGridIlp agents per thread (strided by the block size, so every load and store stays
+// coalesced): the per-agent atomics' round trips overlap instead of one per thread
+constexpr int kGridIlp = 4;
+constexpr int kGridThreads = 256;
+
+__global__ void __launch_bounds__(kGridThreads) k_key(Src S, const DevScalars *__restrict__ sc,
+                                                      uint32_t *__restrict__ key,
+                                                      uint32_t *__restrict__ rank,
+                                                      uint32_t *__restrict__ counts) {
     if (sc->overflow) return;
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= S.nl + S.ng) return;
-    const bool gh = i >= S.nl;
-    const int64_t j = gh ? i - S.nl : i;
-    const double px = gh ? S.gx[j] : S.x[j], py = gh ? S.gy[j] : S.y[j], pz = gh ? S.gz[j] : S.z[j];
-    const double L = sc->L;
-    const int bx = (int)floor((px - sc->o[0]) / L) - sc->boff[0];
-    const int by = (int)floor((py - sc->o[1]) / L) - sc->boff[1];
-    const int bz = (int)floor((pz - sc->o[2]) / L) - sc->boff[2];
-    const uint32_t k = box_key(bx, by, bz, sc->T[0], sc->T[1], sc_hilb(sc));
-    key[i] = k;
-    rank[i] = atomicAdd(&counts[k], 1u);
+    const int64_t n = S.nl + S.ng;
+    const int64_t i0 = blockIdx.x * (int64_t)(kGridThreads * kGridIlp) + threadIdx.x;
+    const double L = sc->L, o0 = sc->o[0], o1 = sc->o[1], o2 = sc->o[2];
+    const int f0 = sc->boff[0], f1 = sc->boff[1], f2 = sc->boff[2], T0 = sc->T[0], T1 = sc->T[1];
+    const uint16_t *const hilb = sc_hilb(sc);
+    uint32_t k[kGridIlp], r[kGridIlp];
+#pragma unroll
+    for (int q = 0; q < kGridIlp; ++q) {
+        const int64_t i = i0 + q * kGridThreads;
+        k[q] = 0;
+        if (i < n) {
+            const bool gh = i >= S.nl;
+            const int64_t j = gh ? i - S.nl : i;
+            const double px = gh ? S.gx[j] : S.x[j], py = gh ? S.gy[j] : S.y[j],
+                         pz = gh ? S.gz[j] : S.z[j];
+            const int bx = (int)floor((px - o0) / L) - f0;
+            const int by = (int)floor((py - o1) / L) - f1;
+            const int bz = (int)floor((pz - o2) / L) - f2;
+            k[q] = box_key(bx, by, bz, T0, T1, hilb);
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < kGridIlp; ++q)
+        if (i0 + q * kGridThreads < n) r[q] = atomicAdd(&counts[k[q]], 1u);
+#pragma unroll
+    for (int q = 0; q < kGridIlp; ++q) {
+        const int64_t i = i0 + q * kGridThreads;
+        if (i < n) {
+            key[i] = k[q];
+            rank[i] = r[q];
+        }
+    }
 }
 
 // ============================================================== a3: exclusive scan
@@ -345,21 +370,38 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_apply(uint32_t *__restric
 }
 
 // ============================================================== a4: scatter + order + gather
-__global__ void __launch_bounds__(256) k_scatter(Src S, const uint32_t *__restrict__ key,
-                                                 const uint32_t *__restrict__ rank,
-                                                 const uint32_t *__restrict__ box_start,
-                                                 uint32_t *__restrict__ perm_tmp,
-                                                 uint32_t *__restrict__ skey,
-                                                 uint32_t *__restrict__ sid,
-                                                 const DevScalars *__restrict__ sc) {
+__global__ void __launch_bounds__(kGridThreads) k_scatter(Src S, const uint32_t *__restrict__ key,
+                                                          const uint32_t *__restrict__ rank,
+                                                          const uint32_t *__restrict__ box_start,
+                                                          uint32_t *__restrict__ perm_tmp,
+                                                          uint32_t *__restrict__ skey,
+                                                          uint32_t *__restrict__ sid,
+                                                          const DevScalars *__restrict__ sc) {
     if (sc->overflow) return;
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= S.nl + S.ng) return;
-    const uint32_t k = key[i];
-    const uint32_t slot = box_start[k] + rank[i];
-    perm_tmp[slot] = (uint32_t)i;
-    skey[slot] = k;
-    sid[slot] = i >= S.nl ? S.gid[i - S.nl] : S.id[i];
+    const int64_t n = S.nl + S.ng;
+    const int64_t i0 = blockIdx.x * (int64_t)(kGridThreads * kGridIlp) + threadIdx.x;
+    uint32_t k[kGridIlp], slot[kGridIlp], id[kGridIlp];
+#pragma unroll
+    for (int q = 0; q < kGridIlp; ++q) {
+        const int64_t i = i0 + q * kGridThreads;
+        if (i < n) {
+            k[q] = key[i];
+            slot[q] = rank[i];
+            id[q] = i >= S.nl ? S.gid[i - S.nl] : S.id[i];
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < kGridIlp; ++q)
+        if (i0 + q * kGridThreads < n) slot[q] += box_start[k[q]];
+#pragma unroll
+    for (int q = 0; q < kGridIlp; ++q) {
+        const int64_t i = i0 + q * kGridThreads;
+        if (i < n) {
+            perm_tmp[slot[q]] = (uint32_t)i;
+            skey[slot[q]] = k[q];
+            sid[slot[q]] = id[q];
+        }
+    }
 }
 
 // Slot s of the scatter holds an agent of box k in arbitrary order; its final slot
@@ -420,7 +462,6 @@ bdm_status launch_grid_sort(Ctx *c, const bdm_agents *a, const bdm_agents *g, cu
     S.gflags = g ? g->flags : nullptr;
     const int64_t n = S.nl + S.ng;
     const int threads = 256;
-    const unsigned nb = (unsigned)((n + threads - 1) / threads);
     {
         int64_t zb = (c->slot_cap + 1 + 1023) / 1024;
         const int64_t maxb = (int64_t)c->sm_count * 16;
@@ -436,13 +477,14 @@ bdm_status launch_grid_sort(Ctx *c, const bdm_agents *a, const bdm_agents *g, cu
                     (c->sort_every == 0 || c->grid_builds % c->sort_every != 0);
     ++c->grid_builds;
     if (c->keep_order && (s = need_agent_buf(c, &c->perm)) != BDM_OK) return s;
-    k_key<<<nb, threads, 0, st>>>(S, c->sc, c->key, c->rank, c->box_start);
+    const unsigned nbi = (unsigned)((n + kGridThreads * kGridIlp - 1) / (kGridThreads * kGridIlp));
+    k_key<<<nbi, kGridThreads, 0, st>>>(S, c->sc, c->key, c->rank, c->box_start);
     const unsigned sb = (unsigned)((c->slot_cap + 1 + kScanTile - 1) / kScanTile);
     k_scan_reduce<<<sb, kScanThreads, 0, st>>>(c->box_start, c->block_sums, c->sc, 0);
     k_scan_top<<<1, 1024, 0, st>>>(c->block_sums, c->sc, 0);
     k_scan_apply<<<sb, kScanThreads, 0, st>>>(c->box_start, c->block_sums, c->sc, 0);
-    k_scatter<<<nb, threads, 0, st>>>(S, c->key, c->rank, c->box_start, c->perm_tmp, c->skey,
-                                      c->sid, c->sc);
+    k_scatter<<<nbi, kGridThreads, 0, st>>>(S, c->key, c->rank, c->box_start, c->perm_tmp, c->skey,
+                                            c->sid, c->sc);
     uint32_t *lflag = S.ng > 0 ? c->lrank : nullptr;
     k_fix_gather<<<(unsigned)((n + 1 + threads - 1) / threads), threads, 0, st>>>(
         S, c->skey, c->sid, c->perm_tmp, c->box_start, c->sx, c->sy, c->sz, c->sd, c->sidf,
