@@ -1098,10 +1098,62 @@ def _slab_phase(args, ws, rank, local, strong, steps, warmup):
                               "fp64_term_ms": fp64 / fp64_peak * 1e3,
                               "hbm_term_ms": b_alg / (peaks["hbm_gbs"] * 1e9) * 1e3},
            "clocks": clocks, "gpu_launches": eng.stats()["launches"] - launches0}
+    if dom is not None and not strong and not args.no_e2e:
+        res["e2e"] = _slab_e2e(dom, a, ws, steps)
     del dom, a, eng
     torch.cuda.synchronize()
     torch.cuda.empty_cache()
     return res
+
+
+def _slab_e2e(dom, a, ws, steps):
+    """End to end through the public API at N GPUs: every rank keeps its slab's state in
+    pinned host memory; each step copies it to the device, runs the whole step
+    (bdm_aura_exchange + bdm_grid_build + bdm_mech_step) and copies the new state back.
+    Host clock around each synchronized step, max over ranks."""
+    import torch
+    import torch.distributed as dist
+    fields = ("x", "y", "z", "diameter", "id", "flags")
+    host = {f: torch.empty(getattr(a, f).shape, dtype=getattr(a, f).dtype, pin_memory=True)
+            for f in fields}
+    n = a.n
+    for f in fields:
+        host[f][:n].copy_(getattr(a, f)[:n])
+    torch.cuda.synchronize()
+    times, h2d, d2h = [], 0, 0
+    for _ in range(steps):
+        if ws > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for f in fields:
+            getattr(a, f)[:n].copy_(host[f][:n], non_blocking=True)
+        a.n = n
+        dom.step()
+        n2 = a.n
+        if n2 > host["x"].numel():  # the slab grew past the host copy: stop measuring
+            break
+        for f in fields:
+            host[f][:n2].copy_(getattr(a, f)[:n2], non_blocking=True)
+        torch.cuda.synchronize()
+        times.append(time.perf_counter() - t0)
+        h2d += 40 * n
+        d2h += 40 * n2
+        n = n2
+    k = len(times)
+    t = torch.tensor([statistics.median(times) if k else float("nan"), float(n)],
+                     dtype=torch.float64, device="cuda")
+    tmax = t[0:1].clone()
+    tot = t[1:2].clone()
+    if ws > 1:
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+        dist.all_reduce(tot, op=dist.ReduceOp.SUM)
+    ms = float(tmax[0]) * 1e3
+    return {"value": float(tot[0]) / (ms * 1e-3), "unit": UNIT,
+            "h2d_bytes_per_step": h2d // max(k, 1), "d2h_bytes_per_step": d2h // max(k, 1),
+            "ms_per_step": ms, "steps": k,
+            "timing": "host clock around each synchronized step, median, max over ranks",
+            "api": "per rank: pinned host SoA -> device, bdm_aura_exchange + bdm_grid_build + "
+                   "bdm_mech_step, device -> host (rank 0's bytes)"}
 
 
 def run_slabs(args, ws, rank, local):
@@ -1143,8 +1195,9 @@ def run_slabs(args, ws, rank, local):
                             **main["roofline_rank0"]}
         line["exchange"] = {k: main[k] for k in ("exchange_ms", "compute_ms", "exchange_share",
                                                  "ghosts_rank0", "agents_rank0")}
-        line["e2e"] = None
-        line["e2e_note"] = "multi-GPU: no host round trip in the step; see the N = 1 line's e2e"
+        line["e2e"] = main.get("e2e")
+        if line["e2e"] is None:
+            line["e2e_note"] = "not measured (--no-e2e, or the strong cfg5 line: no host staging)"
         if weak is not None and strong is not None:
             line["strong_cfg5"] = strong
         line["note"] = "device-timed, max over ranks, of the whole step (exchange + grid + mechanics)"

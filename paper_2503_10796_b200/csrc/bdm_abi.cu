@@ -245,7 +245,7 @@ bdm_status bdm_destroy(bdm_handle h) {
     void *bufs[] = {c->key, c->rank, c->perm_tmp, c->skey, c->sid, c->perm, c->sx, c->sy,
                     c->sz, c->sd, c->sidf, c->sflags, c->svol, c->div_rank, c->box_start, c->dense_list, c->dense_scr,
                     c->onco_id, c->onco_out,
-                    c->block_sums, c->pair_count, c->n_new, c->lrank, c->cls, c->cls2,
+                    c->block_sums, c->scan_state, c->pair_count, c->n_new, c->lrank, c->cls, c->cls2,
                     c->pack_counts, c->sc};
     for (void *p : bufs)
         if (p) cudaFree(p);

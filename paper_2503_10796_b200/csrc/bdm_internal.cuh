@@ -48,6 +48,8 @@ struct DevScalars {
     unsigned int n_dense;  // dense tiles handed from the tile kernel to the dense kernel
     unsigned int dense_next;  // dense kernel work counter (box tasks taken)
     unsigned int tile_next;   // tile kernel work counter (tiles taken)
+    uint32_t scan_epoch;      // tag of the slot scan's look-back words (k_zero_counts bumps
+                              // it on the device, so graph replays get fresh tags)
     double dmax_prev;      // max diameter of the grid build's input (the step keeps it)
     int32_t tile_order;    // option "tile_order" (row f1): 0 row-major tiles, 1 blocked Hilbert
     uint16_t hilb[512];    // blocked Hilbert: local tile (x | y<<3 | z<<6) -> curve position
@@ -114,6 +116,8 @@ struct Ctx {
     long long *onco_out = nullptr;  // row f2: new n, new id_next
     uint32_t *block_sums = nullptr;
     int64_t block_sums_cap = 0;
+    unsigned long long *scan_state = nullptr;  // single-pass slot scan: per-tile look-back words
+    int64_t scan_state_cap = 0;
     // misc
     unsigned long long *pair_count = nullptr;
     DevScalars *sc = nullptr;       // device

@@ -183,8 +183,9 @@ bdm_status launch_grid_geometry(Ctx *c, const bdm_agents *a, const bdm_agents *g
 }
 
 // ============================================================== a2: keys + histogram
-__global__ void k_zero_counts(uint32_t *__restrict__ counts, const DevScalars *__restrict__ sc) {
+__global__ void k_zero_counts(uint32_t *__restrict__ counts, DevScalars *__restrict__ sc) {
     if (sc->overflow) return;
+    if (blockIdx.x == 0 && threadIdx.x == 0) sc->scan_epoch = sc->scan_epoch % 0x3FFFFFFFu + 1u;
     const long long m = sc->nslots + 1;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < m;
          i += (long long)gridDim.x * blockDim.x)
@@ -369,6 +370,103 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_apply(uint32_t *__restric
     }
 }
 
+// Single-pass exclusive scan of the slot counts (decoupled look-back): tile b (4096
+// counts, blockIdx order) publishes its aggregate, then its inclusive prefix once the
+// prefixes before it are known; warp 0 looks back over the predecessors 32 at a time.
+// One word per tile: epoch << 34 | status << 32 | value (status 1 = aggregate, 2 =
+// inclusive prefix; a word of another epoch is "not ready"), so the array is never
+// cleared (the epoch is bumped on the device by k_zero_counts, so a replayed CUDA
+// graph tags every scan afresh).  Counts sum to the agent count (< 2^32).  Relies on tiles being dispatched in
+// blockIdx order, so a tile only waits for tiles that are resident or done.
+constexpr unsigned long long kScanAgg = 1ull, kScanInc = 2ull;
+__device__ __forceinline__ unsigned long long scan_word(uint32_t epoch, unsigned long long st,
+                                                        uint32_t v) {
+    return ((unsigned long long)epoch << 34) | (st << 32) | v;
+}
+__global__ void __launch_bounds__(kScanThreads) k_scan_single(uint32_t *__restrict__ cnt,
+                                                              unsigned long long *state,
+                                                              const DevScalars *__restrict__ sc) {
+    if (sc->overflow) return;
+    const uint32_t epoch = sc->scan_epoch;  // 1 .. 2^30 - 1 (0 = never written)
+    const long long m = sc->nslots + 1;
+    const long long base = (long long)blockIdx.x * kScanTile;
+    if (base >= m) return;
+    uint32_t v[kScanItems];
+    const long long i0 = base + (long long)threadIdx.x * kScanItems;
+    const bool full = i0 + kScanItems <= m;
+    if (full) {
+        const uint4 a = *reinterpret_cast<const uint4 *>(cnt + i0);
+        const uint4 b = *reinterpret_cast<const uint4 *>(cnt + i0 + 4);
+        v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+        v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+    } else {
+#pragma unroll
+        for (int k = 0; k < kScanItems; ++k) v[k] = (i0 + k < m) ? cnt[i0 + k] : 0u;
+    }
+    uint32_t s = 0;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) s += v[k];
+    uint32_t tot;
+    const uint32_t before = block_excl_scan(s, &tot);
+    __shared__ uint32_t tile_prefix;
+    if (threadIdx.x < 32) {
+        const int lane = threadIdx.x;
+        volatile unsigned long long *vs = state;
+        const long long b = blockIdx.x;
+        if (b == 0) {
+            if (lane == 0) {
+                vs[0] = scan_word(epoch, kScanInc, tot);
+                tile_prefix = 0u;
+            }
+        } else {
+            if (lane == 0) vs[b] = scan_word(epoch, kScanAgg, tot);
+            uint32_t excl = 0;
+            long long j = b - 1;  // lane l looks at tile j - l
+            for (;;) {
+                const long long t = j - lane;
+                unsigned long long w = t >= 0 ? vs[t] : scan_word(epoch, kScanInc, 0u);
+                uint32_t st = (uint32_t)(w >> 34) == epoch ? (uint32_t)((w >> 32) & 3u) : 0u;
+                while (__any_sync(0xffffffffu, st == 0u)) {  // wait for every predecessor's word
+                    if (st == 0u) {
+                        w = vs[t];
+                        st = (uint32_t)(w >> 34) == epoch ? (uint32_t)((w >> 32) & 3u) : 0u;
+                    }
+                }
+                const unsigned inc = __ballot_sync(0xffffffffu, st == (uint32_t)kScanInc);
+                // the nearest inclusive prefix ends the look-back: sum lanes 0..k
+                const int k = inc ? __ffs(inc) - 1 : 31;
+                uint32_t val = lane <= k ? (uint32_t)w : 0u;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) val += __shfl_xor_sync(0xffffffffu, val, o);
+                excl += val;
+                if (inc) break;
+                j -= 32;
+            }
+            if (lane == 0) {
+                __threadfence();
+                vs[b] = scan_word(epoch, kScanInc, excl + tot);
+                tile_prefix = excl;
+            }
+        }
+    }
+    __syncthreads();
+    uint32_t run = tile_prefix + before;
+    uint32_t o[kScanItems];
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        o[k] = run;
+        run += v[k];
+    }
+    if (full) {
+        *reinterpret_cast<uint4 *>(cnt + i0) = make_uint4(o[0], o[1], o[2], o[3]);
+        *reinterpret_cast<uint4 *>(cnt + i0 + 4) = make_uint4(o[4], o[5], o[6], o[7]);
+    } else {
+#pragma unroll
+        for (int k = 0; k < kScanItems; ++k)
+            if (i0 + k < m) cnt[i0 + k] = o[k];
+    }
+}
+
 // ============================================================== a4: scatter + order + gather
 __global__ void __launch_bounds__(kGridThreads) k_scatter(Src S, const uint32_t *__restrict__ key,
                                                           const uint32_t *__restrict__ rank,
@@ -408,7 +506,10 @@ __global__ void __launch_bounds__(kGridThreads) k_scatter(Src S, const uint32_t 
 // is box_start[k] + #(agents of box k with a smaller id).  Gathers the SoA there.
 // Ghosts are marked with kGhost in the sorted flags; with ghosts, lflag[dst] = 1 for
 // local agents (scanned afterwards into their output index).
-__global__ void __launch_bounds__(256) k_fix_gather(
+// kFixIlp slots per thread (strided by the block size): their dependent chains (key ->
+// box range -> id rank -> source -> SoA) overlap.
+constexpr int kFixIlp = 2;
+__global__ void __launch_bounds__(kGridThreads) k_fix_gather(
     Src S, const uint32_t *__restrict__ skey, const uint32_t *__restrict__ sid,
     const uint32_t *__restrict__ perm_tmp, const uint32_t *__restrict__ box_start,
     double *__restrict__ sx, double *__restrict__ sy, double *__restrict__ sz,
@@ -416,39 +517,55 @@ __global__ void __launch_bounds__(256) k_fix_gather(
     double *__restrict__ svol, uint32_t *__restrict__ lflag, uint32_t *__restrict__ perm,
     const DevScalars *__restrict__ sc) {
     if (sc->overflow) return;
-    const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int64_t n = S.nl + S.ng;
-    if (s >= n) {
+    const int64_t s0 = blockIdx.x * (int64_t)(kGridThreads * kFixIlp) + threadIdx.x;
+    uint32_t lo[kFixIlp], hi[kFixIlp], me[kFixIlp], src[kFixIlp];
+#pragma unroll
+    for (int q = 0; q < kFixIlp; ++q) {
+        const int64_t s = s0 + q * kGridThreads;
         if (s == n && lflag) lflag[n] = 0u;
-        return;
+        if (s < n) {
+            const uint32_t k = skey[s];
+            lo[q] = box_start[k];
+            hi[q] = box_start[k + 1];
+            me[q] = sid[s];
+            src[q] = perm_tmp[s];
+        }
     }
-    const uint32_t k = skey[s];
-    const uint32_t lo = box_start[k], hi = box_start[k + 1];
-    const uint32_t me = sid[s];
-    uint32_t r = 0;
-    for (uint32_t t = lo; t < hi; ++t) r += (sid[t] < me);
-    const uint32_t dst = lo + r;
-    const uint32_t src = perm_tmp[s];
-    if (perm) perm[dst] = src;  // sort_every != 1: the mechanics writes back to src
-    if ((int64_t)src < S.nl) {
-        sx[dst] = S.x[src];
-        sy[dst] = S.y[src];
-        sz[dst] = S.z[src];
-        sd[dst] = S.d[src];
-        sflags[dst] = S.flags[src];
-        if (S.vol) svol[dst] = S.vol[src];
-        if (lflag) lflag[dst] = 1u;
-    } else {
-        const int64_t j = (int64_t)src - S.nl;
-        sx[dst] = S.gx[j];
-        sy[dst] = S.gy[j];
-        sz[dst] = S.gz[j];
-        sd[dst] = S.gd[j];
-        sflags[dst] = S.gflags[j] | kGhost;
-        if (S.vol) svol[dst] = 0.0;
-        lflag[dst] = 0u;
+#pragma unroll
+    for (int q = 0; q < kFixIlp; ++q) {
+        const int64_t s = s0 + q * kGridThreads;
+        if (s >= n) continue;
+        uint32_t r = 0;
+        for (uint32_t t = lo[q]; t < hi[q]; ++t) r += (sid[t] < me[q]);
+        lo[q] += r;  // the destination slot
     }
-    sidf[dst] = me;
+#pragma unroll
+    for (int q = 0; q < kFixIlp; ++q) {
+        const int64_t s = s0 + q * kGridThreads;
+        if (s >= n) continue;
+        const uint32_t dst = lo[q], sr = src[q];
+        if (perm) perm[dst] = sr;  // sort_every != 1: the mechanics writes back to src
+        if ((int64_t)sr < S.nl) {
+            sx[dst] = S.x[sr];
+            sy[dst] = S.y[sr];
+            sz[dst] = S.z[sr];
+            sd[dst] = S.d[sr];
+            sflags[dst] = S.flags[sr];
+            if (S.vol) svol[dst] = S.vol[sr];
+            if (lflag) lflag[dst] = 1u;
+        } else {
+            const int64_t j = (int64_t)sr - S.nl;
+            sx[dst] = S.gx[j];
+            sy[dst] = S.gy[j];
+            sz[dst] = S.gz[j];
+            sd[dst] = S.gd[j];
+            sflags[dst] = S.gflags[j] | kGhost;
+            if (S.vol) svol[dst] = 0.0;
+            lflag[dst] = 0u;
+        }
+        sidf[dst] = me[q];
+    }
 }
 
 bdm_status launch_grid_sort(Ctx *c, const bdm_agents *a, const bdm_agents *g, cudaStream_t st) {
@@ -461,7 +578,6 @@ bdm_status launch_grid_sort(Ctx *c, const bdm_agents *a, const bdm_agents *g, cu
     S.gd = g ? g->diameter : nullptr; S.gid = g ? g->id : nullptr;
     S.gflags = g ? g->flags : nullptr;
     const int64_t n = S.nl + S.ng;
-    const int threads = 256;
     {
         int64_t zb = (c->slot_cap + 1 + 1023) / 1024;
         const int64_t maxb = (int64_t)c->sm_count * 16;
@@ -480,16 +596,23 @@ bdm_status launch_grid_sort(Ctx *c, const bdm_agents *a, const bdm_agents *g, cu
     const unsigned nbi = (unsigned)((n + kGridThreads * kGridIlp - 1) / (kGridThreads * kGridIlp));
     k_key<<<nbi, kGridThreads, 0, st>>>(S, c->sc, c->key, c->rank, c->box_start);
     const unsigned sb = (unsigned)((c->slot_cap + 1 + kScanTile - 1) / kScanTile);
-    k_scan_reduce<<<sb, kScanThreads, 0, st>>>(c->box_start, c->block_sums, c->sc, 0);
-    k_scan_top<<<1, 1024, 0, st>>>(c->block_sums, c->sc, 0);
-    k_scan_apply<<<sb, kScanThreads, 0, st>>>(c->box_start, c->block_sums, c->sc, 0);
+    if (c->scan_state_cap < (int64_t)sb) {
+        if (c->scan_state) cudaFree(c->scan_state);
+        c->scan_state = nullptr;
+        c->scan_state_cap = 0;
+        BDM_CUDA_TRY(cudaMalloc(&c->scan_state, (size_t)sb * sizeof(unsigned long long)));
+        BDM_CUDA_TRY(cudaMemsetAsync(c->scan_state, 0, (size_t)sb * sizeof(unsigned long long), st));
+        c->scan_state_cap = sb;
+    }
+    k_scan_single<<<sb, kScanThreads, 0, st>>>(c->box_start, c->scan_state, c->sc);
     k_scatter<<<nbi, kGridThreads, 0, st>>>(S, c->key, c->rank, c->box_start, c->perm_tmp, c->skey,
                                             c->sid, c->sc);
     uint32_t *lflag = S.ng > 0 ? c->lrank : nullptr;
-    k_fix_gather<<<(unsigned)((n + 1 + threads - 1) / threads), threads, 0, st>>>(
+    k_fix_gather<<<(unsigned)((n + 1 + kGridThreads * kFixIlp - 1) / (kGridThreads * kFixIlp)),
+                   kGridThreads, 0, st>>>(
         S, c->skey, c->sid, c->perm_tmp, c->box_start, c->sx, c->sy, c->sz, c->sd, c->sidf,
         c->sflags, c->svol, lflag, c->keep_order ? c->perm : nullptr, c->sc);
-    c->launches += 7;
+    c->launches += 5;
     BDM_LAUNCH_CHECK("grid sort");
     if (S.ng > 0) return launch_scan_u32(c, c->lrank, n + 1, st);  // output index of locals
     return BDM_OK;

@@ -832,8 +832,8 @@ __device__ __forceinline__ int tile7_walk(const Tile6SmemT<false, kTZ, true> &S,
             const float sr = pi.w + q.w;
             pass = kMin ? d <= fminf(sr * sr, R2f) : d <= sr * sr;
         }
-        lrow[cnt] = (uint16_t)mo;
-        cnt = min(cnt + (pass ? 32 : 0), 32 * kK6Max);
+        lrow[min(cnt, 32 * kK6Max)] = (uint16_t)mo;  // (a full list is caught after the walk)
+        cnt += pass ? 32 : 0;
         mo += 16;
         if (mo == eo) {
             mo = nxt & 0xFFFFu;
