@@ -87,6 +87,7 @@ def lib() -> ctypes.CDLL:
         L.orc_pair_force.restype = dbl
         L.orc_mech_step.argtypes = [i64, P, P, P, P, P, P, P, i64, P, P, P, P, P, P, P]
         L.orc_sorted_order.argtypes = [i64, P, P, P, P, P, dbl, P, P]
+        L.orc_sorted_order_torus.argtypes = [i64, P, P, P, P, P, dbl, dbl, P, P]
         L.orc_cbrt_det.argtypes = [dbl]
         L.orc_cbrt_det.restype = dbl
         L.orc_division_axis.argtypes = [u64, u64, ctypes.c_uint32, P]
@@ -277,18 +278,23 @@ def mech_step(s, params: MechParams, sample=None):
     lib().orc_mech_step(n, _p(x), _p(y), _p(z), _p(d), _p(i), _p(f), ctypes.byref(params), m,
                         None if idx is None else _p(idx), _p(out["x"]), _p(out["y"]),
                         _p(out["z"]), _p(out["flags"]), _p(out["force"]), ctypes.byref(c))
+    if c.n_static < 0:
+        raise ValueError("toroidal boundary needs lo = 0, a cube hi[0] = hi[1] = hi[2] and at "
+                         "least 3 boxes of edge >= R per axis (R52)")
     return out, {k: getattr(c, k) for k in ("cand", "nbr", "cont", "n_static")}
 
 
-def sorted_order(s, radius=0.0):
-    """Input indices in (blocked Morton key, id) order, and the sorted keys."""
+def sorted_order(s, radius=0.0, torus_side=0.0):
+    """Input indices in (blocked Morton key, id) order, and the sorted keys
+    (torus_side > 0: the toroidal lattice of R52)."""
     x, y, z, d, i = (_f64(s["x"]), _f64(s["y"]), _f64(s["z"]), _f64(s["d"]),
                      _u32(s["id"]))
     n = len(x)
     perm = np.zeros(n, np.int64)
     keys = np.zeros(n, np.uint64)
     if n:
-        lib().orc_sorted_order(n, _p(x), _p(y), _p(z), _p(d), _p(i), radius, _p(perm), _p(keys))
+        lib().orc_sorted_order_torus(n, _p(x), _p(y), _p(z), _p(d), _p(i), radius, torus_side,
+                                     _p(perm), _p(keys))
     return perm, keys
 
 
@@ -296,7 +302,7 @@ def step_full(s, params: MechParams):
     """Convenience: one step returning the full new state in the product's output
     order (sorted by the step's grid), as the GPU library leaves it."""
     out, cnt = mech_step(s, params)
-    perm, _ = sorted_order(s, params.radius)
+    perm, _ = sorted_order(s, params.radius, params.hi[0] if params.boundary == 2 else 0.0)
     new = {
         "x": out["x"][perm], "y": out["y"][perm], "z": out["z"][perm],
         "d": np.asarray(s["d"], np.float64)[perm], "id": np.asarray(s["id"], np.uint32)[perm],

@@ -149,6 +149,7 @@ uint64_t orc_blocked_key(int64_t bx, int64_t by, int64_t bz, const int64_t D[3])
 typedef struct {
     double R, L, o[3], hi[3];
     int64_t D[3];
+    double side;   /* > 0: toroidal cube [0, side)^3 (boundary 2, reading R52) */
 } orc_grid;
 
 void orc_grid_geometry(int64_t n, const double *x, const double *y, const double *z,
@@ -179,6 +180,26 @@ static void box_of(const orc_grid *g, double px, double py, double pz, int64_t b
     b[0] = (int64_t)floor((px - g->o[0]) / g->L);
     b[1] = (int64_t)floor((py - g->o[1]) / g->L);
     b[2] = (int64_t)floor((pz - g->o[2]) / g->L);
+    if (g->side > 0.0)  /* toroidal: the last box also takes x == side (R20), R52 */
+        for (int a = 0; a < 3; ++a) b[a] = b[a] < 0 ? 0 : (b[a] > g->D[a] - 1 ? g->D[a] - 1 : b[a]);
+}
+
+/* Toroidal grid (boundary 2, reading R52): the periodic cube [0, side)^3 of the paper's
+ * toroidal boundary ("agents that leave the space on one side, will enter on the
+ * opposite side"), with the lattice of R19: D = floor(side / R) boxes of edge
+ * L = side / D per axis (D >= 3, so the 27 neighbour boxes are distinct). */
+static int torus_geometry(orc_grid *g, double R, double side)
+{
+    int64_t D = (int64_t)floor(side / R);
+    if (!(R > 0.0) || D < 3) return -1;
+    g->R = R;
+    g->L = side / (double)D;
+    g->side = side;
+    for (int a = 0; a < 3; ++a) {
+        g->o[a] = 0.0;
+        g->D[a] = D;
+    }
+    return 0;
 }
 
 /* ---- the grid itself: agents sorted by (row-major box index, id) ---------------- */
@@ -212,10 +233,12 @@ static int64_t lin_box(const orc_grid *g, int64_t bx, int64_t by, int64_t bz)
  * agents' extent measured from that origin. */
 static void index_build(orc_index *ix, int64_t n, const double *x, const double *y,
                         const double *z, const double *d, const uint32_t *id, double radius,
-                        const double *frame)
+                        const double *frame, double torus_side)
 {
     ix->n = n;
     orc_grid_geometry(n, x, y, z, d, radius, &ix->g.R, &ix->g.L, ix->g.o, ix->g.D);
+    ix->g.side = 0.0;
+    if (torus_side > 0.0) torus_geometry(&ix->g, ix->g.R, torus_side);
     if (frame) {
         double R = radius > 0.0 ? radius : frame[3];
         double L = R * (1.0 + 0x1p-20);
@@ -295,7 +318,7 @@ int64_t orc_neighbor_pairs_grid(int64_t n, const double *x, const double *y, con
                                 uint64_t *pairs, int64_t cap)
 {
     orc_index ix;
-    index_build(&ix, n, x, y, z, d, id, radius, NULL);
+    index_build(&ix, n, x, y, z, d, id, radius, NULL, 0.0);
     double R2 = ix.g.R * ix.g.R;
     int64_t cnt = 0;
     for (int64_t i = 0; i < n; ++i) {
@@ -366,6 +389,27 @@ typedef struct {
 
 static int nnz_of(uint32_t f) { return (int)((f >> ORC_NNZ_SHIFT) & 3u); }
 
+double orc_wrap(double el, double max_bound);
+
+/* Toroidal difference (R52): the minimum image of own - other per axis, as Alg. 7's
+ * periodic search (R19): d > side/2 -> d - side, d < -side/2 -> d + side. */
+static double torus_diff(const orc_grid *g, double v)
+{
+    if (!(g->side > 0.0)) return v;
+    double half = g->side * 0.5;
+    if (v > half) return v - g->side;
+    if (v < -half) return v + g->side;
+    return v;
+}
+
+/* Neighbour box c + off along one axis: -1 if outside an open/closed grid; wrapped
+ * periodically on the torus. */
+static int64_t nbr_box(const orc_grid *g, int64_t c, int a)
+{
+    if (g->side > 0.0) return c < 0 ? c + g->D[a] : (c >= g->D[a] ? c - g->D[a] : c);
+    return (c < 0 || c >= g->D[a]) ? -1 : c;
+}
+
 /* Computes the step for agents idx_list[0..m) (all agents when idx_list == NULL;
  * then m must equal n).  Results are written at position k of the out arrays for
  * the k-th listed agent. */
@@ -378,8 +422,21 @@ void orc_mech_step(int64_t n, const double *x, const double *y, const double *z,
 {
     memset(cnt, 0, sizeof(*cnt));
     if (n == 0) return;
+    double torus = 0.0;
+    if (p->boundary == 2) {  /* R52: the cube [0, hi[0])^3, at least 3 boxes per axis */
+        torus = p->hi[0];
+        orc_grid chk;
+        double R = p->radius;
+        if (!(R > 0.0))
+            for (int64_t i = 0; i < n; ++i) R = d[i] > R ? d[i] : R;
+        if (p->lo[0] != 0.0 || p->lo[1] != 0.0 || p->lo[2] != 0.0 || p->hi[1] != torus ||
+            p->hi[2] != torus || torus_geometry(&chk, R, torus) != 0) {
+            cnt->n_static = -1;  /* invalid torus: nothing computed */
+            return;
+        }
+    }
     orc_index ix;
-    index_build(&ix, n, x, y, z, d, id, p->radius, p->use_frame ? p->frame : NULL);
+    index_build(&ix, n, x, y, z, d, id, p->radius, p->use_frame ? p->frame : NULL, torus);
     const orc_grid *g = &ix.g;
     double R2 = g->R * g->R;
     const uint32_t CHANGED = ORC_MOVED | ORC_GREW | ORC_ADDED;
@@ -401,16 +458,16 @@ void orc_mech_step(int64_t n, const double *x, const double *y, const double *z,
             for (int dz = -1; dz <= 1 && is_static; ++dz)
                 for (int dy = -1; dy <= 1 && is_static; ++dy)
                     for (int dx = -1; dx <= 1 && is_static; ++dx) {
-                        int64_t cx = b[0] + dx, cy = b[1] + dy, cz = b[2] + dz;
-                        if (cx < 0 || cy < 0 || cz < 0 || cx >= g->D[0] || cy >= g->D[1] ||
-                            cz >= g->D[2])
-                            continue;
+                        int64_t cx = nbr_box(g, b[0] + dx, 0), cy = nbr_box(g, b[1] + dy, 1),
+                                cz = nbr_box(g, b[2] + dz, 2);
+                        if (cx < 0 || cy < 0 || cz < 0) continue;
                         int64_t f, l;
                         box_range(&ix, lin_box(g, cx, cy, cz), &f, &l);
                         for (int64_t s = f; s < l; ++s) {
                             int64_t j = ix.e[s].idx;
                             if (j == i) continue;
-                            double D = sqdist(x[i] - x[j], y[i] - y[j], z[i] - z[j]);
+                            double D = sqdist(torus_diff(g, x[i] - x[j]), torus_diff(g, y[i] - y[j]),
+                                              torus_diff(g, z[i] - z[j]));
                             if (D <= R2 && (flags[j] & CHANGED)) {
                                 is_static = 0;
                                 break;
@@ -432,17 +489,17 @@ void orc_mech_step(int64_t n, const double *x, const double *y, const double *z,
             for (int dz = -1; dz <= 1; ++dz)
                 for (int dy = -1; dy <= 1; ++dy)
                     for (int dx = -1; dx <= 1; ++dx) {
-                        int64_t cx = b[0] + dx, cy = b[1] + dy, cz = b[2] + dz;
-                        if (cx < 0 || cy < 0 || cz < 0 || cx >= g->D[0] || cy >= g->D[1] ||
-                            cz >= g->D[2])
-                            continue;
+                        int64_t cx = nbr_box(g, b[0] + dx, 0), cy = nbr_box(g, b[1] + dy, 1),
+                                cz = nbr_box(g, b[2] + dz, 2);
+                        if (cx < 0 || cy < 0 || cz < 0) continue;
                         int64_t f, l;
                         box_range(&ix, lin_box(g, cx, cy, cz), &f, &l);
                         for (int64_t s = f; s < l; ++s) {
                             int64_t j = ix.e[s].idx;
                             if (j == i) continue;
                             cnt->cand++;
-                            double ex = x[i] - x[j], ey = y[i] - y[j], ez = z[i] - z[j];
+                            double ex = torus_diff(g, x[i] - x[j]), ey = torus_diff(g, y[i] - y[j]),
+                                   ez = torus_diff(g, z[i] - z[j]);
                             double D = sqdist(ex, ey, ez);
                             if (!(D <= R2)) continue;
                             cnt->nbr++;
@@ -485,6 +542,10 @@ void orc_mech_step(int64_t n, const double *x, const double *y, const double *z,
                 if (*q[a] < p->lo[a]) *q[a] = p->lo[a];
                 if (*q[a] > p->hi[a]) *q[a] = p->hi[a];
             }
+        } else if (p->boundary == 2) {  /* toroidal: Alg. 9's literal wrap (R20, R52) */
+            nx = orc_wrap(nx, torus);
+            ny = orc_wrap(ny, torus);
+            nz = orc_wrap(nz, torus);
         }
         int moved = (Dx != 0.0 || Dy != 0.0 || Dz != 0.0);
         if (force_out) {
@@ -520,13 +581,16 @@ static int cmp_kentry(const void *pa, const void *pb)
     return 0;
 }
 
-void orc_sorted_order(int64_t n, const double *x, const double *y, const double *z,
-                      const double *d, const uint32_t *id, double radius, int64_t *perm,
-                      uint64_t *keys_sorted)
+/* torus_side > 0: the toroidal lattice of R52 (boxes clamped to D - 1, R20) */
+void orc_sorted_order_torus(int64_t n, const double *x, const double *y, const double *z,
+                            const double *d, const uint32_t *id, double radius, double torus_side,
+                            int64_t *perm, uint64_t *keys_sorted)
 {
     if (n == 0) return;
     orc_grid g;
     orc_grid_geometry(n, x, y, z, d, radius, &g.R, &g.L, g.o, g.D);
+    g.side = 0.0;
+    if (torus_side > 0.0 && torus_geometry(&g, g.R, torus_side) != 0) return;
     orc_kentry *e = (orc_kentry *)malloc(sizeof(orc_kentry) * (size_t)n);
     for (int64_t i = 0; i < n; ++i) {
         int64_t b[3];
@@ -541,6 +605,13 @@ void orc_sorted_order(int64_t n, const double *x, const double *y, const double 
         if (keys_sorted) keys_sorted[i] = e[i].key;
     }
     free(e);
+}
+
+void orc_sorted_order(int64_t n, const double *x, const double *y, const double *z,
+                      const double *d, const uint32_t *id, double radius, int64_t *perm,
+                      uint64_t *keys_sorted)
+{
+    orc_sorted_order_torus(n, x, y, z, d, id, radius, 0.0, perm, keys_sorted);
 }
 
 /* ------------------------------------------------------------------------------ */
