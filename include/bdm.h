@@ -73,8 +73,9 @@ typedef struct {
     double force_threshold;    /* move only if |F| > threshold (R7)            */
     double radius;             /* interaction radius; <= 0: largest diameter  */
     int32_t detect_static;     /* 1: skip the force of static agents (sec:static-agents)    */
-    int32_t boundary;          /* 0 open (P:2671 (i)), 1 closed = clamp to [lo, hi]        */
-    double lo[3], hi[3];       /* closed-boundary box                                       */
+    int32_t boundary;          /* 0 open (P:2671 (i)), 1 closed = clamp to [lo, hi],       */
+                               /* 2 toroidal = the periodic cube [0, hi[0])^3 (R52)         */
+    double lo[3], hi[3];       /* closed-boundary box; toroidal: lo = 0, hi = (side,side,side) */
     uint64_t seed;             /* Philox key for steps that draw random numbers            */
     uint32_t step;             /* iteration number (Philox counter word)                    */
     uint32_t collect_stats;    /* 1: count candidates/neighbours/contacts (costs atomics)  */
@@ -168,16 +169,22 @@ bdm_status bdm_grid_build(bdm_handle h, const bdm_agents *a, const bdm_agents *g
  *     rbar = r_i r_j/(r_i + r_j); F_N = k delta - gamma sqrt(rbar delta);
  *     F_i = fma(F_N/dist, x_i - x_j, F_i) per component
  *   displacement = dt F_i if |F_i|^2 > threshold^2 else 0, capped at
- *   max_displacement; x_i += displacement; boundary (open: no-op; closed: clamp).
+ *   max_displacement; x_i += displacement; boundary (open: no-op; closed: clamp;
+ *   toroidal: x = fmod(x, side), + side if negative -- Alg. 9's wrap, R20).
+ * Toroidal (boundary 2, P:2671 (iii), reading R52): the grid is the periodic lattice of
+ * [0, side)^3, D = floor(side / R) >= 3 boxes of edge side / D per axis; the 27 boxes
+ * wrap modulo D (same canonical order) and (dx,dy,dz) is the minimum image (+-side
+ * beyond side/2).  Only bdm_step builds that grid (the reference formulation runs).
  * Static agents (R8) skip the force: displacement 0, nnz carried.
  * On return (stream order) the caller's arrays x,y,z,diameter,id,flags hold the
  * new state in the grid's sorted order (key, then id): a permutation of the input
  * (or, on builds that option "sort_every" leaves in place, in the input order).
- * Errors: BDM_EINVAL (no matching grid build, bad params), BDM_ENOTIMPL
- * (toroidal boundary), BDM_ECUDA. */
+ * Errors: BDM_EINVAL (no matching grid build, bad params, a toroidal step without its
+ * grid; deferred: side < 3 R), BDM_ECUDA. */
 bdm_status bdm_mech_step(bdm_handle h, bdm_agents *a, const bdm_params *p, void *stream);
 
-/* Convenience: bdm_grid_build(a, NULL, p->radius) then bdm_mech_step(a, p). */
+/* Convenience: bdm_grid_build(a, NULL, p->radius) then bdm_mech_step(a, p); with
+ * boundary 2 the build is on the torus (lo must be 0 and hi a cube, else BDM_EINVAL). */
 bdm_status bdm_step(bdm_handle h, bdm_agents *a, const bdm_params *p, void *stream);
 
 /* End-to-end step on HOST arrays (the e2e entry point): copies the n agents of
@@ -190,6 +197,17 @@ bdm_status bdm_step(bdm_handle h, bdm_agents *a, const bdm_params *p, void *stre
  * Errors: as bdm_step, plus deferred device conditions (as bdm_sync). */
 bdm_status bdm_step_host(bdm_handle h, const bdm_agents *host_in, bdm_agents *host_out,
                          bdm_agents *dev, const bdm_params *p, void *stream);
+
+/* K end-to-end steps on the HOST state `host` (in place): every step copies the n
+ * agents host -> device (x, y, z, diameter, id, flags into `dev`), runs bdm_step and
+ * copies the new state device -> host (x, y, z, flags; diameter and id too unless the
+ * step kept the input order, option "sort_every").  Pipelined: the arrays are split
+ * into `chunks` (1..64) index ranges, and chunk c of step k+1 is uploaded as soon as
+ * chunk c of step k has come down, so downloads and uploads overlap on PCIe (two copy
+ * streams next to `stream`).  Host arrays must be pinned for the overlap.  Returns
+ * after the last download (synchronizes).  Errors: as bdm_step_host. */
+bdm_status bdm_run_host(bdm_handle h, bdm_agents *host, bdm_agents *dev, const bdm_params *p,
+                        int32_t steps, int32_t chunks, void *stream);
 
 /* Growth and division with add-compaction (Alg. 4 control flow
  * "grow while below the maximum size, else divide", with division

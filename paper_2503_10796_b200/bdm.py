@@ -22,7 +22,8 @@ NNZ_SHIFT = 4
 # Every symbol include/bdm.h declares (checked by tests/test_abi.py).
 EXPORTS = [
     "bdm_create", "bdm_destroy", "bdm_last_error", "bdm_version", "bdm_init_spheres",
-    "bdm_grid_build", "bdm_mech_step", "bdm_step", "bdm_step_host", "bdm_sync", "bdm_reserve",
+    "bdm_grid_build", "bdm_mech_step", "bdm_step", "bdm_step_host", "bdm_run_host", "bdm_sync",
+    "bdm_reserve",
     "bdm_get_stats", "bdm_get_grid_info", "bdm_neighbor_pairs", "bdm_peak_dfma",
     "bdm_set_option", "bdm_grow_divide", "bdm_sir_step", "bdm_local_frame", "bdm_set_frame",
     "bdm_pack_slab", "bdm_append", "bdm_diffuse", "bdm_secrete", "bdm_chemotaxis",
@@ -126,6 +127,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "bdm_mech_step": [P, AG, PR, P],
         "bdm_step": [P, AG, PR, P],
         "bdm_step_host": [P, AG, AG, AG, PR, P],
+        "bdm_run_host": [P, AG, AG, PR, ctypes.c_int32, ctypes.c_int32, P],
         "bdm_sync": [P, P],
         "bdm_reserve": [P, i64, i64],
         "bdm_get_stats": [P, ctypes.POINTER(CStats)],
@@ -465,8 +467,13 @@ class Engine:
         latched device conditions and, on a grid-slot overflow, grows the slot array and
         re-issues the step (the caller's arrays are untouched by an overflowed step)."""
         for _ in range(retries + 1):
-            self.grid_build(agents, params.radius, stream)
-            self.mech_step(agents, params, stream)
+            if params.boundary == 2:  # toroidal: bdm_step builds the grid on the torus (R52)
+                ca, cp = agents.c(), params.c()
+                _check(self.lib.bdm_step(self.h, ctypes.byref(ca), ctypes.byref(cp),
+                                         _stream_ptr(stream)))
+            else:
+                self.grid_build(agents, params.radius, stream)
+                self.mech_step(agents, params, stream)
             if not sync:
                 return
             st = self.lib.bdm_sync(self.h, _stream_ptr(stream))
@@ -616,6 +623,15 @@ class Engine:
                                       ctypes.byref(cd), ctypes.byref(cp), _stream_ptr(stream)))
         host_out.n = host_in.n
         dev.n = host_in.n
+
+    def run_host(self, host: Agents, dev: Agents, params: Params, steps: int, chunks: int = 8,
+                 stream=None):
+        """`steps` end-to-end steps on the pinned host state `host` (in place), uploads
+        of step k+1 overlapping downloads of step k chunk by chunk (bdm_run_host)."""
+        ch, cd, cp = host.c(), dev.c(), params.c()
+        _check(self.lib.bdm_run_host(self.h, ctypes.byref(ch), ctypes.byref(cd), ctypes.byref(cp),
+                                     int(steps), int(chunks), _stream_ptr(stream)))
+        dev.n = host.n
 
     def sync(self, stream=None):
         _check(self.lib.bdm_sync(self.h, _stream_ptr(stream)))

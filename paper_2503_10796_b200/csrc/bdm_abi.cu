@@ -113,6 +113,9 @@ static bdm_status read_latches(Ctx *c, bool clear) {
     bdm_status st = BDM_OK;
     if (c->sc_host->nonfinite) {
         st = fail(BDM_ENOTFINITE, "a position or diameter is NaN/Inf");
+    } else if (c->sc_host->overflow == 6) {
+        st = fail(BDM_EINVAL, "toroidal boundary needs at least 3 boxes of edge >= R per axis "
+                              "(side >= 3 R)");
     } else if (c->sc_host->overflow == 5) {
         st = fail(BDM_EINVAL, "growth/division needs ids exactly 0..n-1 (an id is >= n)");
     } else if (c->sc_host->overflow == 4) {
@@ -337,6 +340,7 @@ bdm_status bdm_grid_build(bdm_handle h, const bdm_agents *a, const bdm_agents *g
     c->grid_x = a->x;
     c->grid_n = a->n;
     c->grid_ng = g ? g->n : 0;
+    c->grid_torus = c->torus_side;
     return BDM_OK;
 }
 
@@ -348,8 +352,9 @@ bdm_status bdm_mech_step(bdm_handle h, bdm_agents *a, const bdm_params *p, void 
     if (s != BDM_OK) return s;
     if (!c->grid_valid || c->grid_x != a->x || c->grid_n != a->n)
         return fail(BDM_EINVAL, "bdm_mech_step needs a preceding bdm_grid_build on the same agents");
-    if (p->boundary == 2) return fail(BDM_ENOTIMPL, "toroidal mechanics not implemented");
-    if (p->boundary != 0 && p->boundary != 1) return fail(BDM_EINVAL, "bad boundary");
+    if (p->boundary != 0 && p->boundary != 1 && p->boundary != 2) return fail(BDM_EINVAL, "bad boundary");
+    if ((p->boundary == 2) != (c->grid_torus > 0.0) || (p->boundary == 2 && c->grid_torus != p->hi[0]))
+        return fail(BDM_EINVAL, "toroidal mechanics needs the grid built on the same torus (bdm_step)");
     if (!(p->dt >= 0.0) || !(p->max_displacement >= 0.0) || !(p->force_threshold >= 0.0))
         return fail(BDM_EINVAL, "dt, max_displacement and force_threshold must be >= 0");
     c->grid_valid = false;  // positions change: the grid is stale afterwards
@@ -366,8 +371,17 @@ bdm_status bdm_mech_step(bdm_handle h, bdm_agents *a, const bdm_params *p, void 
 
 bdm_status bdm_step(bdm_handle h, bdm_agents *a, const bdm_params *p, void *stream) {
     DeviceScope ds__(h);
-    if (!p) return fail(BDM_EINVAL, "params is NULL");
+    if (!p || !h) return fail(BDM_EINVAL, "handle or params is NULL");
+    Ctx *c = (Ctx *)h;
+    if (p->boundary == 2) {  // toroidal (R52): the cube [0, hi[0])^3
+        const double L = p->hi[0];
+        if (!(L > 0.0) || p->hi[1] != L || p->hi[2] != L || p->lo[0] != 0.0 || p->lo[1] != 0.0 ||
+            p->lo[2] != 0.0)
+            return fail(BDM_EINVAL, "toroidal boundary needs lo = 0 and a cube hi[0] = hi[1] = hi[2] > 0");
+        c->torus_side = L;
+    }
     bdm_status s = bdm_grid_build(h, a, nullptr, p->radius, stream);
+    c->torus_side = 0.0;
     if (s != BDM_OK) return s;
     return bdm_mech_step(h, a, p, stream);
 }
@@ -402,6 +416,101 @@ bdm_status bdm_step_host(bdm_handle h, const bdm_agents *hin, bdm_agents *hout, 
         BDM_CUDA_TRY(cudaMemcpyAsync(hout->diameter, dev->diameter, n * 8, cudaMemcpyDeviceToHost, st));
         BDM_CUDA_TRY(cudaMemcpyAsync(hout->id, dev->id, n * 4, cudaMemcpyDeviceToHost, st));
     }
+    return bdm_sync(h, stream);
+}
+
+// K end-to-end steps on a host state, pipelined: the device -> host copy of step k's
+// result and the host -> device copy of step k+1's input run concurrently, chunk by
+// chunk (chunk c of step k+1 goes up as soon as chunk c of step k has come down), on
+// two copy streams next to the compute stream -- PCIe is full duplex.
+bdm_status bdm_run_host(bdm_handle h, bdm_agents *host, bdm_agents *dev, const bdm_params *p,
+                        int32_t steps, int32_t chunks, void *stream) {
+    DeviceScope ds__(h);
+    if (!h || !host || !dev || !p) return fail(BDM_EINVAL, "NULL argument");
+    if (steps < 0 || chunks < 1 || chunks > 64) return fail(BDM_EINVAL, "steps < 0 or chunks not in 1..64");
+    if (host->n > dev->capacity) return fail(BDM_EINVAL, "n exceeds the device capacity");
+    Ctx *c = (Ctx *)h;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t n = host->n;
+    dev->n = n;
+    if (steps == 0 || n == 0) return BDM_OK;
+    cudaStream_t up = nullptr, down = nullptr;
+    cudaEvent_t ev_up = nullptr, ev_comp = nullptr, ev_down[64] = {};
+    bdm_status res = BDM_OK;
+    auto cleanup = [&]() {
+        if (up) cudaStreamSynchronize(up);
+        if (down) cudaStreamSynchronize(down);
+        for (int k = 0; k < chunks; ++k)
+            if (ev_down[k]) cudaEventDestroy(ev_down[k]);
+        if (ev_up) cudaEventDestroy(ev_up);
+        if (ev_comp) cudaEventDestroy(ev_comp);
+        if (up) cudaStreamDestroy(up);
+        if (down) cudaStreamDestroy(down);
+    };
+#define BDM_RH_TRY(expr)                                              \
+    do {                                                              \
+        cudaError_t e__ = (expr);                                     \
+        if (e__ != cudaSuccess) {                                     \
+            res = cuda_fail(e__, #expr);                              \
+            cleanup();                                                \
+            return res;                                               \
+        }                                                             \
+    } while (0)
+    BDM_RH_TRY(cudaStreamCreateWithFlags(&up, cudaStreamNonBlocking));
+    BDM_RH_TRY(cudaStreamCreateWithFlags(&down, cudaStreamNonBlocking));
+    BDM_RH_TRY(cudaEventCreateWithFlags(&ev_up, cudaEventDisableTiming));
+    BDM_RH_TRY(cudaEventCreateWithFlags(&ev_comp, cudaEventDisableTiming));
+    for (int k = 0; k < chunks; ++k) BDM_RH_TRY(cudaEventCreateWithFlags(&ev_down[k], cudaEventDisableTiming));
+    // the compute stream's earlier work (the caller's) precedes the first upload
+    BDM_RH_TRY(cudaEventRecord(ev_comp, st));
+    BDM_RH_TRY(cudaStreamWaitEvent(up, ev_comp, 0));
+    for (int32_t t = 0; t < steps; ++t) {
+        for (int k = 0; k < chunks; ++k) {
+            const int64_t a = n * k / chunks, b = n * (k + 1) / chunks;
+            if (b == a) continue;
+            const size_t m = (size_t)(b - a);
+            if (t > 0) BDM_RH_TRY(cudaStreamWaitEvent(up, ev_down[k], 0));
+            BDM_RH_TRY(cudaMemcpyAsync(dev->x + a, host->x + a, m * 8, cudaMemcpyHostToDevice, up));
+            BDM_RH_TRY(cudaMemcpyAsync(dev->y + a, host->y + a, m * 8, cudaMemcpyHostToDevice, up));
+            BDM_RH_TRY(cudaMemcpyAsync(dev->z + a, host->z + a, m * 8, cudaMemcpyHostToDevice, up));
+            BDM_RH_TRY(cudaMemcpyAsync(dev->diameter + a, host->diameter + a, m * 8, cudaMemcpyHostToDevice, up));
+            BDM_RH_TRY(cudaMemcpyAsync(dev->id + a, host->id + a, m * 4, cudaMemcpyHostToDevice, up));
+            BDM_RH_TRY(cudaMemcpyAsync(dev->flags + a, host->flags + a, m * 4, cudaMemcpyHostToDevice, up));
+        }
+        BDM_RH_TRY(cudaEventRecord(ev_up, up));
+        BDM_RH_TRY(cudaStreamWaitEvent(st, ev_up, 0));
+        c->fused_valid = false;  // the device arrays were overwritten from the host
+        const bdm_status s = bdm_step(h, dev, p, stream);
+        if (s != BDM_OK) {
+            cleanup();
+            return s;
+        }
+        // a step that kept the input order (option sort_every) leaves d and id in place
+        const bool all = !c->keep_order;
+        BDM_RH_TRY(cudaEventRecord(ev_comp, st));
+        BDM_RH_TRY(cudaStreamWaitEvent(down, ev_comp, 0));
+        for (int k = 0; k < chunks; ++k) {
+            const int64_t a = n * k / chunks, b = n * (k + 1) / chunks;
+            const size_t m = (size_t)(b - a);
+            if (m) {
+                BDM_RH_TRY(cudaMemcpyAsync(host->x + a, dev->x + a, m * 8, cudaMemcpyDeviceToHost, down));
+                BDM_RH_TRY(cudaMemcpyAsync(host->y + a, dev->y + a, m * 8, cudaMemcpyDeviceToHost, down));
+                BDM_RH_TRY(cudaMemcpyAsync(host->z + a, dev->z + a, m * 8, cudaMemcpyDeviceToHost, down));
+                BDM_RH_TRY(cudaMemcpyAsync(host->flags + a, dev->flags + a, m * 4, cudaMemcpyDeviceToHost, down));
+                if (all) {
+                    BDM_RH_TRY(cudaMemcpyAsync(host->diameter + a, dev->diameter + a, m * 8,
+                                               cudaMemcpyDeviceToHost, down));
+                    BDM_RH_TRY(cudaMemcpyAsync(host->id + a, dev->id + a, m * 4, cudaMemcpyDeviceToHost, down));
+                }
+            }
+            BDM_RH_TRY(cudaEventRecord(ev_down[k], down));
+        }
+    }
+    // the caller's stream resumes after the last download
+    BDM_RH_TRY(cudaEventRecord(ev_comp, down));
+    BDM_RH_TRY(cudaStreamWaitEvent(st, ev_comp, 0));
+#undef BDM_RH_TRY
+    cleanup();
     return bdm_sync(h, stream);
 }
 

@@ -50,6 +50,7 @@ struct DevScalars {
     unsigned int tile_next;   // tile kernel work counter (tiles taken)
     uint32_t scan_epoch;      // tag of the slot scan's look-back words (k_zero_counts bumps
                               // it on the device, so graph replays get fresh tags)
+    double torus_side;        // > 0: the grid is the toroidal lattice of [0, side)^3 (R52)
     double dmax_prev;      // max diameter of the grid build's input (the step keeps it)
     int32_t tile_order;    // option "tile_order" (row f1): 0 row-major tiles, 1 blocked Hilbert
     uint16_t hilb[512];    // blocked Hilbert: local tile (x | y<<3 | z<<6) -> curve position
@@ -118,6 +119,8 @@ struct Ctx {
     int64_t block_sums_cap = 0;
     unsigned long long *scan_state = nullptr;  // single-pass slot scan: per-tile look-back words
     int64_t scan_state_cap = 0;
+    double torus_side = 0.0;   // bdm_step with boundary 2 builds the grid on this torus (R52)
+    double grid_torus = 0.0;   // the torus side the current grid was built on (0: none)
     // misc
     unsigned long long *pair_count = nullptr;
     DevScalars *sc = nullptr;       // device

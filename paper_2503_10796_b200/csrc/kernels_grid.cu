@@ -122,9 +122,43 @@ __global__ void __launch_bounds__(256) k_reduce(int64_t n, const double *__restr
 // all-reduced minimum corner and largest diameter of every rank) and the local
 // extent only fixes the lattice offset and dims.
 __global__ void k_setup(DevScalars *sc, double radius, const double *__restrict__ frame,
-                        int reset_after) {
+                        int reset_after, double torus_side) {
     if (threadIdx.x != 0) return;
     const double R = radius > 0.0 ? radius : (frame ? -frame[3] : dec_double(sc->enc_dmax));
+    sc->torus_side = torus_side;
+    if (torus_side > 0.0) {
+        // toroidal lattice of [0, side)^3 (R52, as R19): D = floor(side / R) >= 3 boxes of
+        // edge L = side / D per axis, origin 0; boxes are clamped to D - 1 in k_key (R20)
+        const double Dd = floor(torus_side / R);
+        const bool bad = !(R > 0.0) || !(Dd >= 3.0) || !(Dd < 1.0e6);
+        const int D = bad ? 3 : (int)Dd;
+        sc->R = R;
+        sc->R2 = R * R;
+        sc->L = torus_side / (double)D;
+        long long ns = 64;
+        for (int a = 0; a < 3; ++a) {
+            sc->o[a] = 0.0;
+            sc->hi[a] = torus_side;
+            sc->boff[a] = 0;
+            sc->dims[a] = D;
+            sc->T[a] = (D + 3) >> 2;
+            if (sc->tile_order) sc->T[a] = (sc->T[a] + 7) & ~7;
+            ns *= (long long)sc->T[a];
+        }
+        sc->nslots = ns;
+        if (bad) sc->overflow = 6;  // not a valid torus for this R: nothing is computed
+        else if (ns >= 0xFFFFFFFFll || ns > sc->slot_cap) sc->overflow = 1;
+        sc->has_frame = 0;
+        sc->dmax_prev = dec_double(sc->enc_dmax);
+        if (reset_after) {
+            for (int a = 0; a < 3; ++a) {
+                sc->enc_lo[a] = enc_double(INFINITY);
+                sc->enc_hi[a] = enc_double(-INFINITY);
+            }
+            sc->enc_dmax = enc_double(-INFINITY);
+        }
+        return;
+    }
     const double L = R * (1.0 + 0x1p-20);
     sc->R = R;
     sc->R2 = R * R;
@@ -175,7 +209,7 @@ bdm_status launch_grid_geometry(Ctx *c, const bdm_agents *a, const bdm_agents *g
         k_reduce<<<(unsigned)blocks, 256, 0, st>>>(s->n, s->x, s->y, s->z, s->diameter, c->sc);
         c->launches += 1;
     }
-    k_setup<<<1, 32, 0, st>>>(c->sc, radius, c->frame, c->fuse_reduce ? 1 : 0);
+    k_setup<<<1, 32, 0, st>>>(c->sc, radius, c->frame, c->fuse_reduce ? 1 : 0, c->torus_side);
     c->launches += reuse ? 1 : 2;
     c->fused_valid = false;
     BDM_LAUNCH_CHECK("grid geometry");
@@ -216,6 +250,8 @@ __global__ void __launch_bounds__(kGridThreads) k_key(Src S, const DevScalars *_
     const double L = sc->L, o0 = sc->o[0], o1 = sc->o[1], o2 = sc->o[2];
     const int f0 = sc->boff[0], f1 = sc->boff[1], f2 = sc->boff[2], T0 = sc->T[0], T1 = sc->T[1];
     const uint16_t *const hilb = sc_hilb(sc);
+    const bool torus = sc->torus_side > 0.0;
+    const int Dm0 = sc->dims[0] - 1, Dm1 = sc->dims[1] - 1, Dm2 = sc->dims[2] - 1;
     uint32_t k[kGridIlp], r[kGridIlp];
 #pragma unroll
     for (int q = 0; q < kGridIlp; ++q) {
@@ -226,9 +262,14 @@ __global__ void __launch_bounds__(kGridThreads) k_key(Src S, const DevScalars *_
             const int64_t j = gh ? i - S.nl : i;
             const double px = gh ? S.gx[j] : S.x[j], py = gh ? S.gy[j] : S.y[j],
                          pz = gh ? S.gz[j] : S.z[j];
-            const int bx = (int)floor((px - o0) / L) - f0;
-            const int by = (int)floor((py - o1) / L) - f1;
-            const int bz = (int)floor((pz - o2) / L) - f2;
+            int bx = (int)floor((px - o0) / L) - f0;
+            int by = (int)floor((py - o1) / L) - f1;
+            int bz = (int)floor((pz - o2) / L) - f2;
+            if (torus) {  // x == side (R20) and rounding at the faces: the edge boxes
+                bx = bx < 0 ? 0 : (bx > Dm0 ? Dm0 : bx);
+                by = by < 0 ? 0 : (by > Dm1 ? Dm1 : by);
+                bz = bz < 0 ? 0 : (bz > Dm2 ? Dm2 : bz);
+            }
             k[q] = box_key(bx, by, bz, T0, T1, hilb);
         }
     }

@@ -31,6 +31,18 @@ __global__ void __launch_bounds__(256) k_mech(MechArgs A, DevScalars *__restrict
     flush_counts<kStats>(c, sc, A.fuse);
 }
 
+// Toroidal mechanics (boundary 2, R52): thread per agent on the periodic lattice.
+template <bool kStats>
+__global__ void __launch_bounds__(256) k_mech_torus(MechArgs A, DevScalars *__restrict__ sc) {
+    if (sc->overflow) return;
+    const GridView g = load_grid(sc);
+    const double side = sc->torus_side;
+    Counts c;
+    const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (s < A.n) mech_agent_torus(A, g, s, side, c);
+    flush_counts<kStats>(c, sc, A.fuse);
+}
+
 // ============================================================== tile kernel
 // One CTA per 4x4x4-box tile (persistent, strided over tiles).  The 6x6x6 boxes of
 // the tile and its one-box halo are staged in shared memory in row-major box order
@@ -1836,6 +1848,14 @@ bdm_status launch_mech(Ctx *c, bdm_agents *a, const bdm_params *p, cudaStream_t 
     A.hi0 = p->hi[0]; A.hi1 = p->hi[1]; A.hi2 = p->hi[2];
     if (p->collect_stats)
         BDM_CUDA_TRY(cudaMemsetAsync(c->sc->stats, 0, sizeof(c->sc->stats), st));
+    if (p->boundary == 2) {  // toroidal: the reference formulation on the periodic lattice
+        const unsigned nb = (unsigned)((a->n + 255) / 256);
+        if (p->collect_stats) k_mech_torus<true><<<nb, 256, 0, st>>>(A, c->sc);
+        else k_mech_torus<false><<<nb, 256, 0, st>>>(A, c->sc);
+        c->launches += 1;
+        BDM_LAUNCH_CHECK("toroidal mechanics");
+        return BDM_OK;
+    }
     const bool dense = c->dense && (c->mech_kernel == 0 || c->mech_kernel >= 3);
     A.dense_list = dense ? c->dense_list : nullptr;
     A.dense_perm = nullptr;
@@ -1858,8 +1878,8 @@ bdm_status launch_mech(Ctx *c, bdm_agents *a, const bdm_params *p, cudaStream_t 
     if (c->tile_depth == 0 && c->mech_kernel == 5) {  // auto may switch: set both up now
         tile6_per_sm<false, 6, false, 1, true>(c);
         tile6_per_sm<true, 6, false, 1, true>(c);
-        tile6_per_sm<false, 4, false, 2, true>(c);
-        tile6_per_sm<true, 4, false, 2, true>(c);
+        tile6_per_sm<false, 5, false, 2, true>(c);
+        tile6_per_sm<true, 5, false, 2, true>(c);
     }
     if (c->tile_depth == 0 && c->mech_kernel == 0) {  // auto may switch: set both up now
         tile6_per_sm<false, 5, false, 1>(c);
@@ -1868,8 +1888,8 @@ bdm_status launch_mech(Ctx *c, bdm_agents *a, const bdm_params *p, cudaStream_t 
         tile6_per_sm<true, 4, false, 2>(c);
     }
     if (c->mech_kernel == 5 && depth == 2) {  // tile7 batches (contact prefilter), two-tile units
-        const bdm_status s = p->collect_stats ? launch_tile6<true, 4, false, 2, true>(c, A, st)
-                                              : launch_tile6<false, 4, false, 2, true>(c, A, st);
+        const bdm_status s = p->collect_stats ? launch_tile6<true, 5, false, 2, true>(c, A, st)
+                                              : launch_tile6<false, 5, false, 2, true>(c, A, st);
         if (s != BDM_OK) return s;
     } else if (c->mech_kernel == 5) {  // tile7 batches (contact prefilter)
         const bdm_status s = p->collect_stats ? launch_tile6<true, 6, false, 1, true>(c, A, st)

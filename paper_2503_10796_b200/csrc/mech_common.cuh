@@ -95,6 +95,13 @@ __device__ __forceinline__ void finish_agent(const MechArgs &A, int64_t s, doubl
         nx = nx < A.lo0 ? A.lo0 : (nx > A.hi0 ? A.hi0 : nx);
         ny = ny < A.lo1 ? A.lo1 : (ny > A.hi1 ? A.hi1 : ny);
         nz = nz < A.lo2 ? A.lo2 : (nz > A.hi2 ? A.hi2 : nz);
+    } else if (A.boundary == 2) {  // toroidal [0, hi0)^3: Alg. 9's literal wrap (R20, R52)
+        double r = fmod(nx, A.hi0);
+        nx = r < 0.0 ? A.hi0 + r : r;
+        r = fmod(ny, A.hi0);
+        ny = r < 0.0 ? A.hi0 + r : r;
+        r = fmod(nz, A.hi0);
+        nz = r < 0.0 ? A.hi0 + r : r;
     }
     const bool moved = (Dx != 0.0 || Dy != 0.0 || Dz != 0.0);
     c.moved += moved ? 1u : 0u;
@@ -196,6 +203,85 @@ __device__ __forceinline__ void mech_agent_global(const MechArgs &A, const GridV
                 }
             }
         }
+    }
+    finish_agent(A, s, xi, yi, zi, Fx, Fy, Fz, is_static, nnz, c);
+}
+
+// Toroidal mechanics (boundary 2, R52) for agent s: the reference formulation on the
+// periodic lattice of [0, side)^3 -- the 27 boxes wrap modulo D in canonical order
+// (dz, dy, dx), ascending id in a box (R9); every difference is the minimum image
+// (own - other, +-side beyond side/2) before D and f_ij.
+__device__ __forceinline__ double torus_image(double v, double side, double half) {
+    return v > half ? v - side : (v < -half ? v + side : v);
+}
+__device__ __forceinline__ int torus_wrap(int c, int D) { return c < 0 ? c + D : (c >= D ? c - D : c); }
+__device__ __forceinline__ void mech_agent_torus(const MechArgs &A, const GridView &g, int64_t s,
+                                                 double side, Counts &c) {
+    const uint32_t fi = A.sflags[s];
+    if (fi & kGhost) return;
+    const double half = side * 0.5;
+    const double xi = A.sx[s], yi = A.sy[s], zi = A.sz[s], di = A.sd[s];
+    const double ri = di * 0.5;
+    int bx = (int)floor(xi / g.L), by = (int)floor(yi / g.L), bz = (int)floor(zi / g.L);
+    bx = bx < 0 ? 0 : (bx > g.D0 - 1 ? g.D0 - 1 : bx);
+    by = by < 0 ? 0 : (by > g.D1 - 1 ? g.D1 - 1 : by);
+    bz = bz < 0 ? 0 : (bz > g.D2 - 1 ? g.D2 - 1 : bz);
+    const int nnz_in = (int)((fi >> BDM_FLAG_NNZ_SHIFT) & 3u);
+    bool is_static = false;
+    if (A.detect_static && !(fi & kChanged) && nnz_in <= 1) {
+        is_static = true;
+        for (int dz = -1; dz <= 1 && is_static; ++dz)
+            for (int dy = -1; dy <= 1 && is_static; ++dy)
+                for (int dx = -1; dx <= 1 && is_static; ++dx) {
+                    const uint32_t key = box_key(torus_wrap(bx + dx, g.D0), torus_wrap(by + dy, g.D1),
+                                                 torus_wrap(bz + dz, g.D2), g.T0, g.T1, g.hilb);
+                    const uint32_t b0 = A.box_start[key], b1 = A.box_start[key + 1];
+                    for (uint32_t t = b0; t < b1; ++t) {
+                        if (t == (uint32_t)s) continue;
+                        const double ex = torus_image(xi - A.sx[t], side, half);
+                        const double ey = torus_image(yi - A.sy[t], side, half);
+                        const double ez = torus_image(zi - A.sz[t], side, half);
+                        const double D = fma(ez, ez, fma(ey, ey, ex * ex));
+                        if (D <= g.R2 && (A.sflags[t] & kChanged)) {
+                            is_static = false;
+                            break;
+                        }
+                    }
+                }
+    }
+    double Fx = 0.0, Fy = 0.0, Fz = 0.0;
+    int nnz = nnz_in;
+    if (!is_static) {
+        nnz = 0;
+        for (int dz = -1; dz <= 1; ++dz)
+            for (int dy = -1; dy <= 1; ++dy)
+                for (int dx = -1; dx <= 1; ++dx) {
+                    const uint32_t key = box_key(torus_wrap(bx + dx, g.D0), torus_wrap(by + dy, g.D1),
+                                                 torus_wrap(bz + dz, g.D2), g.T0, g.T1, g.hilb);
+                    const uint32_t b0 = A.box_start[key], b1 = A.box_start[key + 1];
+                    for (uint32_t t = b0; t < b1; ++t) {
+                        if (t == (uint32_t)s) continue;
+                        ++c.cand;
+                        const double ex = torus_image(xi - A.sx[t], side, half);
+                        const double ey = torus_image(yi - A.sy[t], side, half);
+                        const double ez = torus_image(zi - A.sz[t], side, half);
+                        const double D = fma(ez, ez, fma(ey, ey, ex * ex));
+                        if (!(D <= g.R2)) continue;
+                        ++c.nbr;
+                        const double dist = sqrt(D);
+                        const double rj = A.sd[t] * 0.5;
+                        const double delta = (ri + rj) - dist;
+                        if (!(delta > 0.0 && dist > 0.0)) continue;
+                        ++c.cont;
+                        const double rbar = (ri * rj) / (ri + rj);
+                        const double Fn = A.k * delta - A.gamma * sqrt(rbar * delta);
+                        const double sc_ = Fn / dist;
+                        Fx = fma(sc_, ex, Fx);
+                        Fy = fma(sc_, ey, Fy);
+                        Fz = fma(sc_, ez, Fz);
+                        if (Fn != 0.0 && nnz < 2) ++nnz;
+                    }
+                }
     }
     finish_agent(A, s, xi, yi, zi, Fx, Fy, Fz, is_static, nnz, c);
 }
