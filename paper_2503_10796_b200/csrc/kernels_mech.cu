@@ -474,6 +474,7 @@ struct Tile6SmemT {
     int lo_box[3], hi_box[3];               // boxes that can hold a new extremum (see below)
     uint32_t start[TileGeo<kTZ>::kNB];
     uint32_t off[TileGeo<kTZ>::kNB + 4];
+    uint32_t wsum[kT6Warps];                // box-table scan: warp totals
     Fp32Stage<kPair, kMM> f;
     double X[kMM], Y[kMM], Z[kMM], Rr[kMM];
     uint32_t F[kV7 ? 1 : kMM];              // flags (kV7 reads them from global memory)
@@ -818,6 +819,61 @@ __device__ __forceinline__ void tile6_batch(const MechArgs &A, const Tile6SmemT<
 }
 
 
+#ifndef BDM_WALK_OLD
+// The flattened walk of one lane over its trimmed runs (see tile7_batch); returns the
+// number of survivors (saturated at kK6Max, which the caller treats as a full list),
+// listed (byte offsets m << 4) in Wp.u.a.lst[.][lane].
+// Per candidate step: one LDS.128 of the staged (x, y, z, r') as two packed f32x2
+// words, the distance and reach in packed fp32 (sub/mul.rn.f32x2 on (x, y) and (z, r')
+// with the lane's r' negated, so the second difference is r'_i + r'_j; signs of the
+// differences do not matter once squared), a predicated survivor store, the run step.
+// The test is the same conservative contact (or neighbour) test as before with the
+// squared distance summed as (dx^2 + dy^2) + dz^2: five roundings instead of the fma
+// chain's three, 2^-21.7 relative, still far inside the margin of tile7_batch's note.
+template <bool kStats, bool kMin, int kTZ>
+__device__ __forceinline__ int tile7_walk(const Tile6SmemT<false, kTZ, true> &S, Warp7 &Wp, int lane,
+                                          float4 pi, int cmax, int M, float R2f) {
+    const char *const pb = reinterpret_cast<const char *>(&S.f.P[0]);
+    const uint32_t mlast = (uint32_t)M << 4;
+    const uint32_t la0 = (uint32_t)__cvta_generic_to_shared(&Wp.u.a.lst[0][lane]);
+    const uint32_t lim = la0 + 64u * (uint32_t)kK6Max;  // a full list stops growing
+    uint32_t la = la0;
+    const char *rp = reinterpret_cast<const char *>(&Wp.u.a.run[0][lane]);
+    const uint32_t cur = *reinterpret_cast<const uint32_t *>(rp);
+    uint32_t mo = cur & 0xFFFFu, eo = cur >> 16;
+    rp += 128;
+    uint32_t nxt = *reinterpret_cast<const uint32_t *>(rp);
+    const unsigned long long pxy = pk2(pi.x, pi.y), pzw = pk2(pi.z, -pi.w);
+#pragma unroll 4
+    for (int it = 0; it < cmax; ++it) {
+        const ulonglong2 q = *reinterpret_cast<const ulonglong2 *>(pb + min(mo, mlast));
+        unsigned long long e1, e2;
+        asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(e1) : "l"(q.x), "l"(pxy));
+        asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(e2) : "l"(q.y), "l"(pzw));
+        asm("mul.rn.f32x2 %0, %1, %1;" : "=l"(e1) : "l"(e1));
+        asm("mul.rn.f32x2 %0, %1, %1;" : "=l"(e2) : "l"(e2));
+        float dx2, dy2, dz2, sr2;
+        asm("mov.b64 {%0, %1}, %2;" : "=f"(dx2), "=f"(dy2) : "l"(e1));
+        asm("mov.b64 {%0, %1}, %2;" : "=f"(dz2), "=f"(sr2) : "l"(e2));
+        const float d = __fadd_rn(__fadd_rn(dx2, dy2), dz2);
+        bool pass;
+        if (kStats) pass = d <= R2f;
+        else pass = kMin ? d <= fminf(sr2, R2f) : d <= sr2;
+        if (pass && la < lim) {
+            asm volatile("st.shared.u16 [%0], %1;" ::"r"(la), "h"((unsigned short)mo));
+            la += 64u;
+        }
+        mo += 16u;
+        if (mo == eo) {
+            mo = nxt & 0xFFFFu;
+            eo = nxt >> 16;
+            rp += 128;
+        }
+        nxt = *reinterpret_cast<const uint32_t *>(rp);
+    }
+    return (int)((la - la0) >> 6);
+}
+#else
 // The flattened walk of one lane over its trimmed runs (see tile7_batch); returns the
 // number of survivors, listed (byte offsets m << 4) in Wp.u.a.lst[.][lane].
 template <bool kStats, bool kMin, int kTZ>
@@ -856,6 +912,7 @@ __device__ __forceinline__ int tile7_walk(const Tile6SmemT<false, kTZ, true> &S,
     }
     return cnt >> 5;
 }
+#endif
 
 // Version 7 of the batch (option mech_kernel 5; the staging and tiles of k_mech_tile6):
 // the walk's conservative fp32 test is the contact test
@@ -878,13 +935,16 @@ __device__ __forceinline__ void tile7_batch(const MechArgs &A, const Tile6SmemT<
     const int k = klo + lane;
     const uint32_t gk = k < n0 ? g0 + (uint32_t)k : g1 + (uint32_t)(k - n0);
     int mi = M, nr = 0, walk = 0, ca = 0;
-    uint32_t fi = 0;
+    uint32_t fi = 0, idk = 0;
+    double dk = 0.0;
     bool active = false, cand_static = false;
     float4 pi = make_float4(-kSentinel, -kSentinel, -kSentinel, 0.f);
     if (lane < na) {
         mi = (int)S.kmi[k];
         const int lbi = (int)S.mbox[mi];
         fi = A.sflags[gk];
+        idk = A.sid[gk];  // for the write-back: the loads' latency hides behind the batch
+        dk = A.sd[gk];
         active = !(fi & kGhost);
         if (active) {
             cand_static = A.detect_static && !(fi & kChanged) && ((fi >> BDM_FLAG_NNZ_SHIFT) & 3u) <= 1u;
@@ -1050,7 +1110,7 @@ __device__ __forceinline__ void tile7_batch(const MechArgs &A, const Tile6SmemT<
         } else {
             nnz = (int)((fi >> BDM_FLAG_NNZ_SHIFT) & 3u);
         }
-        finish_agent(A, gk, xi, yi, zi, Fx, Fy, Fz, is_static, nnz, c, sides != 0);
+        finish_agent(A, gk, xi, yi, zi, Fx, Fy, Fz, is_static, nnz, c, sides != 0, dk, idk);
     }
     merge_counts<kStats>(c, Wp, sides, lane);
 }
@@ -1104,71 +1164,81 @@ __global__ void __launch_bounds__(kT6Threads, kMinBlocks) k_mech_tile6(MechArgs 
     int tx, ty, tz;
 
     const uint16_t *const hilb = S.g.hilb, *const hilb_inv = S.g.hilb_inv;
-    // tiles are taken from a device counter: no tail imbalance between the persistent
-    // CTAs (a static stride left 8 % on the table at cfg2); the broadcast slot
-    // alternates so a slow warp still reads this tile's number while the next is drawn
-    // Thread 0 draws each unit one tile ahead (the atomic's latency hides behind a whole
-    // tile) and decodes it for the CTA at the top of the iteration.
+    // Units are taken from a device counter: no tail imbalance between the persistent
+    // CTAs (a static stride left 8 % on the table at cfg2).  Thread 0 draws each unit one
+    // ahead (the atomic's latency hides behind a whole unit) and publishes unit it + 1
+    // in slot (it + 1) & 1 right after the CTA has read unit it: the iteration's own
+    // barriers make it visible, so the loop needs no barrier of its own (the slot it
+    // overwrites was last read before them).
     int t_next = tid == 0 ? (int)atomicAdd(&sc->tile_next, 1u) : 0;
-    for (int it = 0;; ++it) {
-        if (tid == 0) {
-            int *const ti = S.tinfo[it & 1];
-            const int t = t_next;
-            if (t < ntiles) t_next = (int)atomicAdd(&sc->tile_next, 1u);
-            int x = 0, y = 0, z = 0;
-            uint32_t a = (uint32_t)t, b = 0xFFFFFFFFu;  // the unit's tiles (slot numbers)
-            if (t < ntiles) {
-                if constexpr (kTZ == 1) {
-                    tile_xyz((uint32_t)t, T0, T1, hilb_inv, x, y, z);
-                } else {
-                    x = t % T0;
-                    y = (t / T0) % T1;
-                    z = kTZ * (t / (T0 * T1));
-                    a = tile_rank(x, y, z, T0, T1, hilb);
-                    if (z + 1 < S.g.T2) b = tile_rank(x, y, z + 1, T0, T1, hilb);
-                }
+    auto draw = [&](int slot) {
+        int *const ti = S.tinfo[slot];
+        const int t = t_next;
+        if (t < ntiles) t_next = (int)atomicAdd(&sc->tile_next, 1u);
+        int x = 0, y = 0, z = 0;
+        uint32_t a = (uint32_t)t, b = 0xFFFFFFFFu;  // the unit's tiles (slot numbers)
+        if (t < ntiles) {
+            if constexpr (kTZ == 1) {
+                tile_xyz((uint32_t)t, T0, T1, hilb_inv, x, y, z);
+            } else {
+                x = t % T0;
+                y = (t / T0) % T1;
+                z = kTZ * (t / (T0 * T1));
+                a = tile_rank(x, y, z, T0, T1, hilb);
+                if (z + 1 < S.g.T2) b = tile_rank(x, y, z + 1, T0, T1, hilb);
             }
-            ti[0] = t, ti[1] = x, ti[2] = y, ti[3] = z, ti[4] = (int)a, ti[5] = (int)b;
         }
-        __syncthreads();
+        ti[0] = t, ti[1] = x, ti[2] = y, ti[3] = z, ti[4] = (int)a, ti[5] = (int)b;
+    };
+    constexpr int kBI = (kNB + kT6Threads - 1) / kT6Threads;
+    if (tid == 0) draw(0);
+    __syncthreads();
+    for (int it = 0;; ++it) {
         const int *const ti = S.tinfo[it & 1];
         const int t = ti[0];
         if (t >= ntiles) break;
         tx = ti[1], ty = ti[2], tz = ti[3];
         const uint32_t ta = (uint32_t)ti[4], tb = (uint32_t)ti[5];
+        if (tid == 0) draw((it + 1) & 1);
+        // the unit's own range and the region's box table: every load is issued before
+        // the first is used (one global round trip, not one per item)
         const uint32_t g0 = A.box_start[ta * 64u];
-        const int n0 = (int)(A.box_start[ta * 64u + 64u] - g0);
-        uint32_t g1 = 0;
-        int n1 = 0;
+        const uint32_t e0 = A.box_start[ta * 64u + 64u];
+        uint32_t g1 = 0, e1 = 0;
         if (kTZ == 2 && tb != 0xFFFFFFFFu) {
             g1 = A.box_start[tb * 64u];
-            n1 = (int)(A.box_start[tb * 64u + 64u] - g1);
+            e1 = A.box_start[tb * 64u + 64u];
         }
-        const int nc = n0 + n1;
-        if (nc == 0) continue;  // uniform across the CTA
         const int bx0 = 4 * tx - 1, by0 = 4 * ty - 1, bz0 = 4 * tz - 1;
-        // ---- box table of the region (out-of-grid boxes are empty)
-        for (int lb = tid; lb < kNB; lb += kT6Threads) {
-            const uint32_t v = S.lbxyz[lb];
-            const int gx = bx0 + (int)(v & 7u), gy = by0 + (int)((v >> 3) & 7u),
-                      gz = bz0 + (int)((v >> 6) & 15u);
-            uint32_t st = 0, cn = 0;
-            if (gx >= 0 && gy >= 0 && gz >= 0 && gx < S.g.D0 && gy < S.g.D1 && gz < S.g.D2) {
-                const uint32_t key = box_key(gx, gy, gz, T0, T1, hilb);
-                st = A.box_start[key];
-                cn = A.box_start[key + 1] - st;
-            }
-            S.start[lb] = st;
-            S.off[lb] = cn;
-        }
-        __syncthreads();
-        if (w == 0) {  // exclusive scan of the kNB counts (kSQ per lane)
-            uint32_t v[kSQ], sum = 0;
+        uint32_t st[kBI], en[kBI];
 #pragma unroll
-            for (int q = 0; q < kSQ; ++q) {
-                const int lb = lane * kSQ + q;
-                v[q] = lb < kNB ? S.off[lb] : 0u;
-                sum += v[q];
+        for (int q = 0; q < kBI; ++q) {
+            const int lb = tid * kBI + q;
+            st[q] = en[q] = 0;
+            if (lb < kNB) {
+                const uint32_t v = S.lbxyz[lb];
+                const int gx = bx0 + (int)(v & 7u), gy = by0 + (int)((v >> 3) & 7u),
+                          gz = bz0 + (int)((v >> 6) & 15u);
+                if (gx >= 0 && gy >= 0 && gz >= 0 && gx < S.g.D0 && gy < S.g.D1 && gz < S.g.D2) {
+                    const uint32_t key = box_key(gx, gy, gz, T0, T1, hilb);
+                    st[q] = A.box_start[key];
+                    en[q] = A.box_start[key + 1];
+                }
+            }
+        }
+        do {  // one unit; a `break` ends it early
+        // ---- box table of the region (out-of-grid boxes are empty) and the exclusive
+        // scan of its counts: thread t owns the kBI consecutive boxes t kBI.. (all its
+        // box_start loads in flight together), a warp scan of the thread sums, then the
+        // warp totals (one barrier)
+        uint32_t run = 0;
+        {
+            uint32_t sum = 0;
+#pragma unroll
+            for (int q = 0; q < kBI; ++q) {
+                const int lb = tid * kBI + q;
+                if (lb < kNB) S.start[lb] = st[q];
+                sum += en[q] - st[q];
             }
             uint32_t inc = sum;
 #pragma unroll
@@ -1176,16 +1246,18 @@ __global__ void __launch_bounds__(kT6Threads, kMinBlocks) k_mech_tile6(MechArgs 
                 const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
                 if (lane >= o) inc += y;
             }
-            uint32_t run = inc - sum;
+            if (lane == 31) S.wsum[w] = inc;
+            __syncthreads();
+            run = inc - sum;
 #pragma unroll
-            for (int q = 0; q < kSQ; ++q) {
-                const int lb = lane * kSQ + q;
-                if (lb <= kNB) S.off[lb] = run;
-                run += v[q];
-            }
+            for (int q = 0; q < kT6Warps - 1; ++q) run += q < w ? S.wsum[q] : 0u;
         }
-        __syncthreads();
-        const int M = (int)S.off[kNB];
+        int M = 0;
+#pragma unroll
+        for (int q = 0; q < kT6Warps; ++q) M += (int)S.wsum[q];
+        const int n0 = (int)(e0 - g0), n1 = (int)(e1 - g1);
+        const int nc = n0 + n1;
+        if (nc == 0) break;  // uniform across the CTA
         if (M > Smem::kMM && S.use_pf && A.dense_list) {  // dense region: the dense-box kernel
             if (tid == 0) {  // entries are half tiles (tile << 1 | x-half), see k_mech_dense
                 const unsigned q = atomicAdd(&sc->n_dense, (kTZ == 2 && tb != 0xFFFFFFFFu) ? 4u : 2u);
@@ -1196,8 +1268,7 @@ __global__ void __launch_bounds__(kT6Threads, kMinBlocks) k_mech_tile6(MechArgs 
                     A.dense_list[q + 3] = (tb << 1) | 1u;
                 }
             }
-            __syncthreads();
-            continue;
+            break;
         }
         if (M > Smem::kMM || !S.use_pf) {
             // over-full region or |coordinates| / L >= 2^30: reference formulation
@@ -1208,15 +1279,25 @@ __global__ void __launch_bounds__(kT6Threads, kMinBlocks) k_mech_tile6(MechArgs 
                     mech_agent_global(A, S.g, k < n0 ? g0 + k : g1 + (k - n0), c);
                 merge_counts<kStats>(c, S.W[w], A.fuse ? 0x7F : 0, lane);
             }
-            __syncthreads();
-            continue;
+            break;
         }
-        // ---- staged index -> box, tile agent -> staged index
+        const double X0 = S.g.o0 + (double)(bx0 + S.g.b0) * S.g.L, Y0 = S.g.o1 + (double)(by0 + S.g.b1) * S.g.L,
+                     Z0 = S.g.o2 + (double)(bz0 + S.g.b2) * S.g.L;
+        const double hpad = 0x1p-16 * S.g.L;  // r' pad of the tile7 contact prefilter
+        // ---- staged offsets, staged index -> box, tile agent -> staged index (a thread
+        // per box, strided; measured faster than each thread mapping its own contiguous
+        // boxes from registers without the barrier: 1.74 vs 1.80 ms at cfg2)
+#pragma unroll
+        for (int q = 0; q < kBI; ++q) {
+            const int lb = tid * kBI + q;
+            if (lb <= kNB) S.off[lb] = run;
+            run += en[q] - st[q];
+        }
+        __syncthreads();
         for (int lb = tid; lb < kNB; lb += kT6Threads) {
             const uint32_t o = S.off[lb], n = S.off[lb + 1] - o;
             const uint32_t v = S.lbxyz[lb];
             const bool inner = (v >> 10) != 0u;
-            // own agents: the first tile's in box order, then the second's (lz 5..8)
             const uint32_t kb = (kTZ == 2 && ((v >> 6) & 15u) > 4u) ? (uint32_t)n0 + (S.start[lb] - g1)
                                                                    : S.start[lb] - g0;
             for (uint32_t u = 0; u < n; ++u) {
@@ -1226,11 +1307,7 @@ __global__ void __launch_bounds__(kT6Threads, kMinBlocks) k_mech_tile6(MechArgs 
         }
         __syncthreads();
         // ---- stage the region (row-major boxes, ascending id in a box)
-        {
-            const double L = S.g.L;
-            const double X0 = S.g.o0 + (double)(bx0 + S.g.b0) * L, Y0 = S.g.o1 + (double)(by0 + S.g.b1) * L,
-                         Z0 = S.g.o2 + (double)(bz0 + S.g.b2) * L;
-            const double hpad = 0x1p-16 * L;  // r' pad of the tile7 contact prefilter
+        if constexpr (!kPair) {
             for (int m = tid; m < M; m += kT6Threads) {
                 const int lb = S.mbox[m];
                 const uint32_t gi = S.start[lb] + ((uint32_t)m - S.off[lb]);
@@ -1240,25 +1317,34 @@ __global__ void __launch_bounds__(kT6Threads, kMinBlocks) k_mech_tile6(MechArgs 
                 S.Z[m] = z;
                 S.Rr[m] = d * 0.5;
                 if constexpr (!kV7) S.F[m] = A.sflags[gi];
+                S.f.P[m] = make_float4((float)(x - X0), (float)(y - Y0), (float)(z - Z0), (float)(d * 0.5 + hpad));
+            }
+            if (tid == 0) S.f.P[M] = make_float4(kSentinel, kSentinel, kSentinel, 0.f);  // sentinel agent
+        } else {
+            // ---- stage the region (row-major boxes, ascending id in a box): the packed
+            // pair layout of the f32x2 walk (mech_kernel 3)
+            for (int m = tid; m < M; m += kT6Threads) {
+                const int lb = S.mbox[m];
+                const uint32_t gi = S.start[lb] + ((uint32_t)m - S.off[lb]);
+                const double x = A.sx[gi], y = A.sy[gi], z = A.sz[gi], d = A.sd[gi];
+                S.X[m] = x;
+                S.Y[m] = y;
+                S.Z[m] = z;
+                S.Rr[m] = d * 0.5;
+                S.F[m] = A.sflags[gi];
                 const float xr = (float)(x - X0), yr = (float)(y - Y0), zr = (float)(z - Z0);
-                if constexpr (kPair) {
-                    float *xy = reinterpret_cast<float *>(&S.f.XY[0]);
-                    float *zz = reinterpret_cast<float *>(&S.f.ZZ[0]);
-                    xy[4 * m + 0] = xr;
-                    xy[4 * m + 2] = yr;
-                    zz[2 * m + 0] = zr;
-                    if (m > 0) {
-                        xy[4 * (m - 1) + 1] = xr;
-                        xy[4 * (m - 1) + 3] = yr;
-                        zz[2 * (m - 1) + 1] = zr;
-                    }
-                } else {
-                    S.f.P[m] = make_float4(xr, yr, zr, (float)(d * 0.5 + hpad));
+                float *xy = reinterpret_cast<float *>(&S.f.XY[0]);
+                float *zz = reinterpret_cast<float *>(&S.f.ZZ[0]);
+                xy[4 * m + 0] = xr;
+                xy[4 * m + 2] = yr;
+                zz[2 * m + 0] = zr;
+                if (m > 0) {
+                    xy[4 * (m - 1) + 1] = xr;
+                    xy[4 * (m - 1) + 3] = yr;
+                    zz[2 * (m - 1) + 1] = zr;
                 }
             }
-        }
-        if (tid == 0) {  // sentinel agent at M (both halves of its pair, and M's half of M-1)
-            if constexpr (kPair) {
+            if (tid == 0) {  // sentinel agent at M (both halves of its pair, and M's half of M-1)
                 float *xy = reinterpret_cast<float *>(&S.f.XY[0]);
                 float *zz = reinterpret_cast<float *>(&S.f.ZZ[0]);
                 S.f.XY[M] = make_float4(kSentinel, kSentinel, kSentinel, kSentinel);
@@ -1268,8 +1354,6 @@ __global__ void __launch_bounds__(kT6Threads, kMinBlocks) k_mech_tile6(MechArgs 
                     xy[4 * (M - 1) + 3] = kSentinel;
                     zz[2 * (M - 1) + 1] = kSentinel;
                 }
-            } else {
-                S.f.P[M] = make_float4(kSentinel, kSentinel, kSentinel, 0.f);
             }
         }
         __syncthreads();
@@ -1297,7 +1381,8 @@ __global__ void __launch_bounds__(kT6Threads, kMinBlocks) k_mech_tile6(MechArgs 
             else
                 tile6_batch<kStats, kPair, kTZ>(A, S, S.W[w], lane, g0, n0, g1, klo, khi - klo, M, sides);
         }
-        __syncthreads();  // before the next tile overwrites the staged region
+        } while (0);
+        __syncthreads();  // before the next unit overwrites the staged region (and wsum)
     }
     // per-warp accumulators -> device scalars
     const auto &Wp = S.W[w];

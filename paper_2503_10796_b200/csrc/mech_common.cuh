@@ -68,11 +68,12 @@ struct Counts {
 };
 
 // a8 + a9 + write-back for one agent (shared by both kernels); s is the sorted slot,
-// the output goes to lrank[s] when ghosts are present.
+// the output goes to lrank[s] when ghosts are present.  di and idi are the agent's
+// diameter and id (the tile kernels have them in registers before the step's work).
 __device__ __forceinline__ void finish_agent(const MechArgs &A, int64_t s, double xi, double yi,
                                              double zi, double Fx, double Fy, double Fz,
-                                             bool is_static, int nnz, Counts &c,
-                                             bool track = true) {
+                                             bool is_static, int nnz, Counts &c, bool track,
+                                             double di, uint32_t idi) {
     const int64_t o = A.lrank ? (int64_t)A.lrank[s] : s;
     double Dx = 0.0, Dy = 0.0, Dz = 0.0;
     if (!is_static) {
@@ -109,17 +110,24 @@ __device__ __forceinline__ void finish_agent(const MechArgs &A, int64_t s, doubl
         c.lo0 = fmin(c.lo0, nx); c.hi0 = fmax(c.hi0, nx);
         c.lo1 = fmin(c.lo1, ny); c.hi1 = fmax(c.hi1, ny);
         c.lo2 = fmin(c.lo2, nz); c.hi2 = fmax(c.hi2, nz);
-        c.dmax = fmax(c.dmax, A.sd[s]);
+        c.dmax = fmax(c.dmax, di);
     }
     c.stat += is_static ? 1u : 0u;
     A.ox[o] = nx;
     A.oy[o] = ny;
     A.oz[o] = nz;
-    A.od[o] = A.sd[s];
-    A.oid[o] = A.sid[s];
+    A.od[o] = di;
+    A.oid[o] = idi;
     if (A.ovol) A.ovol[o] = A.svol[s];
     A.oflags[o] = (moved ? BDM_FLAG_MOVED : 0u) | (is_static ? BDM_FLAG_STATIC : 0u) |
                   ((uint32_t)nnz << BDM_FLAG_NNZ_SHIFT);
+}
+
+__device__ __forceinline__ void finish_agent(const MechArgs &A, int64_t s, double xi, double yi,
+                                             double zi, double Fx, double Fy, double Fz,
+                                             bool is_static, int nnz, Counts &c,
+                                             bool track = true) {
+    finish_agent(A, s, xi, yi, zi, Fx, Fy, Fz, is_static, nnz, c, track, A.sd[s], A.sid[s]);
 }
 
 // The whole step for agent s of the sorted order, reading neighbours from global
