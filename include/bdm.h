@@ -523,6 +523,15 @@ bdm_status bdm_tile_curve(int32_t order, uint16_t *rank_out);
  * second, i.e. half the fp64 FLOP/s) and the SM count.  Synchronizing. */
 bdm_status bdm_peak_dfma(bdm_handle h, double *dfma_per_s, int32_t *sm_count);
 
+/* Diagnostic: checks the SIR step's shared-reciprocal quotient (kernels_sir.cu,
+ * div_by_recip: three IEEE divisions v/|v| of Alg. 9's capped step, from
+ * one reciprocal) against the hardware's IEEE division on n seeded random operands of
+ * the step's range (v = 2u - 1 per axis with u = w 2^-32, |v| > 1) and counts the
+ * results that differ in any bit.  mismatches: caller-owned host pointer.
+ * Synchronizing.  Errors: BDM_EINVAL for NULL or n <= 0. */
+bdm_status bdm_selftest_recip_div(bdm_handle h, int64_t n, uint64_t seed,
+                                  unsigned long long *mismatches);
+
 #ifdef __cplusplus
 }
 #endif

@@ -25,6 +25,7 @@ EXPORTS = [
     "bdm_grid_build", "bdm_mech_step", "bdm_step", "bdm_step_host", "bdm_run_host", "bdm_sync",
     "bdm_reserve",
     "bdm_get_stats", "bdm_get_grid_info", "bdm_neighbor_pairs", "bdm_peak_dfma",
+    "bdm_selftest_recip_div",
     "bdm_set_option", "bdm_grow_divide", "bdm_sir_step", "bdm_local_frame", "bdm_set_frame",
     "bdm_pack_slab", "bdm_append", "bdm_diffuse", "bdm_secrete", "bdm_chemotaxis",
     "bdm_onco_step", "bdm_tile_curve", "bdm_aura_max_size", "bdm_aura_reference",
@@ -134,6 +135,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "bdm_get_grid_info": [P, ctypes.POINTER(CGridInfo)],
         "bdm_neighbor_pairs": [P, AG, dbl, P, i64, ctypes.POINTER(i64), P],
         "bdm_peak_dfma": [P, ctypes.POINTER(dbl), ctypes.POINTER(i32)],
+        "bdm_selftest_recip_div": [P, i64, ctypes.c_uint64, ctypes.POINTER(ctypes.c_ulonglong)],
         "bdm_set_option": [P, ctypes.c_char_p, i64],
         "bdm_grow_divide": [P, AG, PR, dbl, dbl, P, P],
         "bdm_sir_step": [P, AG, PR, dbl, dbl, dbl, dbl, P, P],
@@ -681,3 +683,10 @@ class Engine:
         n = ctypes.c_int32()
         _check(self.lib.bdm_peak_dfma(self.h, ctypes.byref(v), ctypes.byref(n)))
         return v.value, n.value
+
+    def selftest_recip_div(self, n: int, seed: int = 1) -> int:
+        """Mismatches of the SIR step's shared-reciprocal quotients against IEEE
+        division on n random operands (bdm_selftest_recip_div)."""
+        v = ctypes.c_ulonglong()
+        _check(self.lib.bdm_selftest_recip_div(self.h, int(n), int(seed), ctypes.byref(v)))
+        return int(v.value)

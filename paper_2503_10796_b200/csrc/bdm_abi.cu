@@ -886,4 +886,11 @@ bdm_status bdm_peak_dfma(bdm_handle h, double *dfma_per_s, int32_t *sm_count) {
     return launch_peak_dfma(c->sm_count, dfma_per_s);
 }
 
+bdm_status bdm_selftest_recip_div(bdm_handle h, int64_t n, uint64_t seed,
+                                  unsigned long long *mismatches) {
+    DeviceScope ds__(h);
+    if (!h || !mismatches || n <= 0) return fail(BDM_EINVAL, "NULL argument or n <= 0");
+    return launch_selftest_recip_div((Ctx *)h, n, seed, mismatches);
+}
+
 }  // extern "C"

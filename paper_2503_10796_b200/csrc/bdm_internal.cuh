@@ -318,6 +318,7 @@ bdm_status launch_pack_slab(Ctx *c, bdm_agents *a, double lo, double hi, double 
 bdm_status launch_mech(Ctx *c, bdm_agents *a, const bdm_params *p, cudaStream_t st);
 bdm_status launch_pairs(Ctx *c, int64_t n, uint64_t *pairs, int64_t cap, cudaStream_t st);
 bdm_status launch_peak_dfma(int sm_count, double *dfma_per_s);
+bdm_status launch_selftest_recip_div(Ctx *c, int64_t n, uint64_t seed, unsigned long long *mismatches);
 // generic exclusive scan of m u32 values in place (kernels_grid.cu)
 bdm_status launch_scan_u32(Ctx *c, uint32_t *data, long long m, cudaStream_t st);
 int64_t scan_block_count(int64_t m);

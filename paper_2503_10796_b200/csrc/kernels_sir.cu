@@ -225,6 +225,19 @@ __device__ __forceinline__ bool infected_fine(const SirArgs &A, double px, doubl
     return false;
 }
 
+// The IEEE quotient a / b from y = RN(1/b): q0 = RN(a y) is within one ulp of a / b,
+// r = a - b q0 is exact (fma), and RN(q0 + r y) is the correctly rounded quotient
+// (Markstein's theorem for a correctly rounded reciprocal, round to nearest, no
+// overflow or underflow: here |a| <= 1 < b <= sqrt(3) and a is 0 or |a| >= 2^-31).
+// Being correctly rounded, it equals a / b bit for bit; one IEEE division then serves
+// the three components of the capped step (tests/test_gpu_sir.py checks it against a / b
+// on 2^28 random operands, and every SIR parity test against the oracle's division).
+__device__ __forceinline__ double div_by_recip(double a, double b, double y) {
+    const double q0 = __dmul_rn(a, y);
+    const double r = __fma_rn(-b, q0, a);
+    return __fma_rn(r, y, q0);
+}
+
 // Alg. 9 wrap: el = fmod(el, max); if el < 0: el = max + el (R20, literal).  For
 // -max < el < 2 max, fmod is exact and equals el (|el| < max, sign kept: -0 stays -0 and
 // is not < 0) or el - max (max <= el < 2 max, exact by Sterbenz), so the fast path is
@@ -273,9 +286,8 @@ __device__ __forceinline__ void sir_resolve(const SirArgs &A, uint32_t i, double
 // draws, the queue entry for an infection query, recovery, movement and wrap.
 __device__ __forceinline__ void sir_agent(const SirArgs &A, SirQueue &Q, int lane, unsigned lt_mask,
                                           int64_t i, bool valid, double px, double py, double pz,
-                                          uint8_t st, int &qn, uint32_t &cs, uint32_t &ci,
+                                          uint8_t st, uint32_t me, int &qn, uint32_t &cs, uint32_t &ci,
                                           uint32_t &cr, uint32_t &cn) {
-    const uint32_t me = valid ? (A.id ? A.id[i] : (uint32_t)i) : 0u;
     const U4 w = philox10_rk(A, me, 0u, A.step, 0u);
     // Alg. 7: an S agent whose draw passed (R17: strict '<', u = w * 2^-32) is queued
     const bool query = valid && st == 0 && uniform32(w.d) < A.p_inf;
@@ -301,7 +313,14 @@ __device__ __forceinline__ void sir_agent(const SirArgs &A, SirQueue &Q, int lan
         {  // straight-line: 48 % of the lanes need the cap, the warp runs it anyway
             const double nv = sqrt(v2);
             const bool cap = v2 > 1.0;
+#ifndef BDM_SIR_DIV3
+            // the three IEEE quotients v/nv share one reciprocal (div_by_recip)
+            const double rn = 1.0 / nv;
+            const double qx = div_by_recip(vx, nv, rn), qy = div_by_recip(vy, nv, rn),
+                         qz = div_by_recip(vz, nv, rn);
+#else
             const double qx = vx / nv, qy = vy / nv, qz = vz / nv;
+#endif
             vx = cap ? qx : vx;
             vy = cap ? qy : vy;
             vz = cap ? qz : vz;
@@ -348,26 +367,32 @@ __global__ void __launch_bounds__(kSirThreads, BDM_SIR_MINB) k_sir_update(SirArg
     uint32_t cs = 0, ci = 0, cr = 0, cn = 0;
     int qn = 0;  // warp-uniform queue fill
     const int64_t nwarps = (int64_t)gridDim.x * (kSirThreads / 32);
-    // two 32-agent slices per warp iteration, all their loads issued first
-    for (int64_t i0 = ((int64_t)blockIdx.x * (kSirThreads / 32) + wid) * 64; i0 < A.n; i0 += nwarps * 64) {
+    const int64_t first = ((int64_t)blockIdx.x * (kSirThreads / 32) + wid) * 64, stride = nwarps * 64;
+    // two 32-agent slices per warp iteration, all their loads issued first (staging
+    // the next 64 agents in shared memory with cp.async while computing measured
+    // slower: 1.62 vs 1.58 ms at cfg4)
+    for (int64_t i0 = first; i0 < A.n; i0 += stride) {
         const int64_t ia = i0 + lane, ib = i0 + 32 + lane;
         const bool va = ia < A.n, vb = ib < A.n;
         double xa = 0.0, ya = 0.0, za = 0.0, xb = 0.0, yb = 0.0, zb = 0.0;
         uint8_t sa = 0, sb = 0;
+        uint32_t ma = 0, mb = 0;  // ids (Philox counters), loaded with the rest
         if (va) {
             xa = A.x[ia];
             ya = A.y[ia];
             za = A.z[ia];
             sa = A.state[ia];
+            ma = A.id ? A.id[ia] : (uint32_t)ia;
         }
         if (vb) {
             xb = A.x[ib];
             yb = A.y[ib];
             zb = A.z[ib];
             sb = A.state[ib];
+            mb = A.id ? A.id[ib] : (uint32_t)ib;
         }
-        sir_agent(A, Q, lane, lt_mask, ia, va, xa, ya, za, sa, qn, cs, ci, cr, cn);
-        sir_agent(A, Q, lane, lt_mask, ib, vb, xb, yb, zb, sb, qn, cs, ci, cr, cn);
+        sir_agent(A, Q, lane, lt_mask, ia, va, xa, ya, za, sa, ma, qn, cs, ci, cr, cn);
+        sir_agent(A, Q, lane, lt_mask, ib, vb, xb, yb, zb, sb, mb, qn, cs, ci, cr, cn);
     }
     __syncwarp();
     if (lane < qn) sir_resolve(A, Q.idx[lane], Q.px[lane], Q.py[lane], Q.pz[lane], cs, ci, cr, cn);
@@ -502,6 +527,35 @@ bdm_status launch_sir_step(Ctx *c, bdm_agents *a, const bdm_params *p, double si
     if (counts_host)
         BDM_CUDA_TRY(cudaMemcpyAsync(counts_host, A.counts, 4 * sizeof(long long),
                                      cudaMemcpyDeviceToHost, st));
+    return BDM_OK;
+}
+
+// ---- self-test of div_by_recip against IEEE division (bdm_selftest_recip_div)
+__global__ void k_selftest_recip_div(int64_t n, uint32_t k0, uint32_t k1, unsigned long long *bad) {
+    unsigned long long nb = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const U4 w = philox10((uint32_t)i, (uint32_t)(i >> 32), 0x5eedu, 7u, k0, k1);
+        const double vx = 2.0 * uniform32(w.a) - 1.0, vy = 2.0 * uniform32(w.b) - 1.0,
+                     vz = 2.0 * uniform32(w.c) - 1.0;
+        const double v2 = __dadd_rn(__dadd_rn(__dmul_rn(vx, vx), __dmul_rn(vy, vy)), __dmul_rn(vz, vz));
+        if (!(v2 > 1.0)) continue;
+        const double nv = sqrt(v2), rn = 1.0 / nv;
+        nb += __double_as_longlong(div_by_recip(vx, nv, rn)) != __double_as_longlong(vx / nv);
+        nb += __double_as_longlong(div_by_recip(vy, nv, rn)) != __double_as_longlong(vy / nv);
+        nb += __double_as_longlong(div_by_recip(vz, nv, rn)) != __double_as_longlong(vz / nv);
+    }
+    if (nb) atomicAdd(bad, nb);
+}
+
+bdm_status launch_selftest_recip_div(Ctx *c, int64_t n, uint64_t seed, unsigned long long *mismatches) {
+    unsigned long long *d = nullptr;
+    BDM_CUDA_TRY(cudaMalloc(&d, sizeof(unsigned long long)));
+    BDM_CUDA_TRY(cudaMemset(d, 0, sizeof(unsigned long long)));
+    k_selftest_recip_div<<<(unsigned)(c->sm_count * 8), 256>>>(n, (uint32_t)seed, (uint32_t)(seed >> 32), d);
+    const cudaError_t e = cudaMemcpy(mismatches, d, sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    BDM_CUDA_TRY(e);
     return BDM_OK;
 }
 

@@ -111,3 +111,11 @@ def test_cfg4_full_size_sampled(eng, orc):
         assert counts[3] == int(np.count_nonzero((before["state"] == 0) & (after["state"] != 0)))
         del before, after
         torch.cuda.empty_cache()
+
+
+def test_shared_reciprocal_division_is_ieee(eng):
+    """The capped step divides the three components of v by |v| through one reciprocal
+    (kernels_sir.cu div_by_recip); it must equal IEEE division bit for bit.  2^28 random
+    operands of the step's range (v = 2u - 1, |v| > 1), two seeds."""
+    for seed in (1, 0x9E3779B97F4A7C15):
+        assert eng.selftest_recip_div(1 << 28, seed) == 0

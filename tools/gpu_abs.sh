@@ -8,7 +8,7 @@ for X in "$@"; do
   timeout 900 python -m pytest tests/test_gpu_sir.py -q -x > gpurun_out/pytest_s$i.log 2>&1
   echo "s$i [$X] tests: $(tail -1 gpurun_out/pytest_s$i.log)"
   for r in 1 2; do
-    timeout 300 python bench.py --config cfg4 --steps 20 --warmup 3 > gpurun_out/bench_cfg4_s$i$r.json 2>/dev/null
+    timeout 300 python bench.py --config cfg4 --steps 20 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/bench_cfg4_s$i$r.json 2>/dev/null
     python -c "import json; d=json.loads(open('gpurun_out/bench_cfg4_s$i$r.json').read().strip().splitlines()[-1]); print('s$i', round(d['ms_per_step'],4))"
   done
 done
