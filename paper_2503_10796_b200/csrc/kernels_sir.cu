@@ -15,8 +15,9 @@
 //   k_sir_collect  snapshot of the infected agents: positions, hash insert, bitmap
 //   k_sir_update   per agent, in place: infection query, recovery, movement, wrap,
 //                  S/I/R counts.  A warp handles two 32-agent slices per iteration
-//                  (loads first); infection queries are compacted into a per-warp queue
-//                  and resolved one per lane
+//                  (loads first); infection queries are compacted into a per-warp queue,
+//                  32 at a time take the coarse test one per lane, and each that passes
+//                  is searched by the whole warp (one of the 27 boxes per lane)
 #include <cuda_runtime.h>
 #include <math.h>
 
@@ -282,6 +283,88 @@ __device__ __forceinline__ void sir_resolve(const SirArgs &A, uint32_t i, double
     cr += st == 2;
 }
 
+// Whether box (bx+dx, by+dy, bz+dz) (periodic) holds a snapshot-I agent within R of p
+// (minimum image): the same box formula, key, hash probe and chain walk as
+// infected_fine, for one box.
+__device__ __forceinline__ bool infected_in_box(const SirArgs &A, double px, double py, double pz, int bx,
+                                                int by, int bz, int dx, int dy, int dz) {
+    const int D = A.D;
+    int cx = bx + dx, cy = by + dy, cz = bz + dz;
+    cx = cx < 0 ? cx + D : (cx >= D ? cx - D : cx);
+    cy = cy < 0 ? cy + D : (cy >= D ? cy - D : cy);
+    cz = cz < 0 ? cz + D : (cz >= D ? cz - D : cz);
+    const unsigned long long key =
+        ((unsigned long long)cz * D + (unsigned long long)cy) * D + (unsigned long long)cx;
+    const unsigned long long skey = (A.stamp << kStampShift) | key;
+    unsigned long long h = box_hash(key, A.tbits);
+    uint32_t head = kNone;
+    for (;;) {
+        const unsigned long long k = A.keys[h];
+        if ((k >> kStampShift) != A.stamp) break;  // empty this step
+        if (k == skey) {
+            head = (uint32_t)A.heads[h];
+            break;
+        }
+        h = (h + 1) & A.tmask;
+    }
+    for (uint32_t j = head; j != kNone; j = A.next[j]) {
+        const double ex = min_image(px - A.ix[j], A.side, A.half);
+        const double ey = min_image(py - A.iy[j], A.side, A.half);
+        const double ez = min_image(pz - A.iz[j], A.side, A.half);
+        const double Dd = ex * ex + ey * ey + ez * ez;
+        if (Dd <= A.R2) return true;
+    }
+    return false;
+}
+
+// The queued queries Q[0, nq) of a warp (nq <= 32, warp-uniform), one per lane: the
+// coarse test per lane, then each query that passes it is searched by the whole warp,
+// lane b < 27 taking box b of the 27 (their hash probes and chains in parallel instead
+// of one lane walking all 27 boxes while the others wait).  "Any snapshot-I agent within
+// R" does not depend on the order of the boxes, so the result is the same.
+__device__ __forceinline__ void sir_resolve_warp(const SirArgs &A, const SirQueue &Q, int lane, int nq,
+                                                 uint32_t &cs, uint32_t &ci, uint32_t &cr, uint32_t &cn) {
+    const bool act = lane < nq;
+    uint32_t i = 0;
+    double px = 0.0, py = 0.0, pz = 0.0;
+    if (act) {
+        i = Q.idx[lane];
+        px = Q.px[lane];
+        py = Q.py[lane];
+        pz = Q.pz[lane];
+    }
+    unsigned hm = __ballot_sync(0xffffffffu, act && coarse_hit(A, px, py, pz));
+    bool inf = false;
+    const int ddx = lane % 3 - 1, ddy = (lane / 3) % 3 - 1, ddz = lane / 9 - 1;
+    while (hm) {  // warp-uniform
+        const int q = __ffs(hm) - 1;
+        hm &= hm - 1;
+        const double qx = __shfl_sync(0xffffffffu, px, q), qy = __shfl_sync(0xffffffffu, py, q),
+                     qz = __shfl_sync(0xffffffffu, pz, q);
+        bool found = false;
+        if (lane < 27) {
+            const int bx = sir_box(qx, A.L, A.D), by = sir_box(qy, A.L, A.D), bz = sir_box(qz, A.L, A.D);
+            found = infected_in_box(A, qx, qy, qz, bx, by, bz, ddx, ddy, ddz);
+        }
+        const bool any = __any_sync(0xffffffffu, found);
+        if (lane == q) inf = any;
+    }
+    if (act) {
+        uint8_t st = 0;
+        if (inf) {
+            st = 1;
+            ++cn;
+            const uint32_t me = A.id ? A.id[i] : i;
+            const U4 r = philox10_rk(A, me, 0u, A.step, 1u);
+            if (uniform32(r.a) < A.p_rec) st = 2;  // Alg. 8 in sequence (R18)
+        }
+        A.state[i] = st;
+        cs += st == 0;
+        ci += st == 1;
+        cr += st == 2;
+    }
+}
+
 // One agent of the update (its start-of-step x, y, z, state already loaded): Philox
 // draws, the queue entry for an infection query, recovery, movement and wrap.
 __device__ __forceinline__ void sir_agent(const SirArgs &A, SirQueue &Q, int lane, unsigned lt_mask,
@@ -341,7 +424,11 @@ __device__ __forceinline__ void sir_agent(const SirArgs &A, SirQueue &Q, int lan
     qn += __popc(qb);
     if (qn >= 32) {  // warp-uniform: resolve 32 queries, one per lane
         __syncwarp();
+#ifdef BDM_SIR_LANE_SEARCH
         sir_resolve(A, Q.idx[lane], Q.px[lane], Q.py[lane], Q.pz[lane], cs, ci, cr, cn);
+#else
+        sir_resolve_warp(A, Q, lane, 32, cs, ci, cr, cn);
+#endif
         __syncwarp();
         qn -= 32;
         if (lane < qn) {
@@ -395,7 +482,11 @@ __global__ void __launch_bounds__(kSirThreads, BDM_SIR_MINB) k_sir_update(SirArg
         sir_agent(A, Q, lane, lt_mask, ib, vb, xb, yb, zb, sb, mb, qn, cs, ci, cr, cn);
     }
     __syncwarp();
+#ifdef BDM_SIR_LANE_SEARCH
     if (lane < qn) sir_resolve(A, Q.idx[lane], Q.px[lane], Q.py[lane], Q.pz[lane], cs, ci, cr, cn);
+#else
+    sir_resolve_warp(A, Q, lane, qn, cs, ci, cr, cn);
+#endif
     // block reduction of the counters, one atomic each per block
     __shared__ unsigned long long red[4][kSirThreads / 32];
     unsigned long long v[4] = {cs, ci, cr, cn};  // warp sums in 64 bits
