@@ -1271,11 +1271,14 @@ def run_slabs_python(args, ws, rank, local):
         dist.destroy_process_group()
 
 
-def measure_e2e(eng, cfg, params, stream, steps: int = 7):
+def measure_e2e(eng, cfg, params, stream, steps: int = 20):
     """Same metric end to end on a pinned host state: every step copies the agents host
     -> device, runs the step and copies the new state device -> host.  The value is
     bdm_run_host over `steps` steps (the download of step k and the upload of step k+1
-    overlap chunk by chunk, full-duplex PCIe), host clock around the whole call; the
+    overlap chunk by chunk, full-duplex PCIe: 8.2 ms for both directions at once against
+    12.7 ms one after the other, tools/pcie_duplex.py), host clock around the whole call
+    (20 steps, so the first upload and the last download, which overlap nothing, weigh
+    what they weigh in a long run rather than a seventh of the time each); the
     per-call bdm_step_host median is reported next to it.  The warm-up call sorts the
     host arrays into the grid order; the timed steps run in place with option
     sort_every = 0 (row f1), so the order stays and only x, y, z, flags come back (d and

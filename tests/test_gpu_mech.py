@@ -389,12 +389,15 @@ def test_cfg2_bench_instance_teacher_forced(orc):
 
 
 @pytest.mark.parametrize("case", ["cfg2@20011", "dense_all", "dense_cluster_static", "dense_groups",
-                                  "crowded25", "crowded90", "cap"])
+                                  "crowded18", "crowded19", "crowded20", "crowded25", "crowded90",
+                                  "cap"])
 def test_counters_off_bit_exact(eng, orc, case):
     """The timed instances run without counters (collect_stats = 0): there the tile7 and
     dense kernels test contacts only in fp32 (r'_i + r'_j) for every lane that needs no
     more, and trim boxes at the contact reach.  Same populations as the counting tests,
-    state bit-exact after every step."""
+    state bit-exact after every step; crowded18/19/20 put the central agent's survivor
+    list (its contacts and itself) right at the tile7 walk's list capacity (20 entries:
+    a list that reaches it sends the batch to the reference formulation)."""
     from paper_2503_10796_b200 import Agents
     if case.startswith("cfg2"):
         cfg = W.cfg2_scaled(20011)
