@@ -1461,13 +1461,13 @@ static bdm_status launch_tile(Ctx *c, const MechArgs &A, cudaStream_t st) {
 //            corner of the agent's box, |x - C| <= 2L), survivors as one bitmask per lane
 //   queue    the lanes' survivors are concatenated (warp scan of the popcounts) into a
 //            queue in owner-major, candidate-ascending (= canonical) order
-//   phase 2a lane-parallel over the queue (chunks of 192): exact fp64 test D <= R^2, self
-//            excluded, static pull flags, contact pre-test and compaction (as k_mech_tile6);
-//            a queued contact keeps its exact differences x_i - x_j
-//   phase 2b lane-parallel Eq. 4.1/4.2 over the compacted contacts, s = F_N / dist
-//   phase 3  each lane adds its own contacts of the chunk in order with fma (the
-//            contacts of one word concentrate on few lanes, so this loop is kept to
-//            loads and three fma)
+//   phase 2  lane-parallel over the queue (chunks of 192), two survivors per lane: exact
+//            fp64 test D <= R^2, self excluded, static pull flags, and Eq. 4.1/4.2 (as
+//            k_mech_tile6's version 7: in these regions the survivors are nearly all
+//            contacts, so a separate contact compaction cost more than it saved; a
+//            non-contact runs on stand-in operands and gets s = 0)
+//   phase 3  each lane adds its own survivors of the chunk in order with fma,
+//            recomputing x_i - x_j from the staged word (s = 0 adds exactly nothing)
 // The static decision needs every neighbour's flags, so forces of a candidate static
 // agent are computed and dropped when it turns out static (a5 result unchanged).
 constexpr int kDWarps = 4;
@@ -1486,10 +1486,7 @@ struct DenseWarp {
     uint32_t os[32];                        // their sorted index
     uint32_t nbrc[32];                      // neighbours per owner (stats)
     uint16_t Q[32 * 32];                    // survivor queue: j | owner << 8
-    uint16_t cpre[kDQ + 1];                 // contacts before survivor p (chunk-relative)
-    double cq[kDQ];                         // D, then s
-    double cx[kDQ], cy[kDQ], cz[kDQ];       // x_i - x_j of the contact
-    uint16_t ce[kDQ];                       // contact -> survivor entry (j | owner << 8)
+    double cq[kDQ];                         // s = F_N / dist per survivor (0: no contact)
     uint8_t cf[kDQ];                        // bit1 contact, bit0 F_N != 0
     uint8_t chg[32];
     // carry: kept candidates of a staging round past the word's 32 slots
@@ -1499,7 +1496,10 @@ struct DenseWarp {
 };
 
 template <bool kStats>
-__global__ void __launch_bounds__(32 * kDWarps, 4) k_mech_dense(MechArgs A, DevScalars *__restrict__ sc) {
+#ifndef BDM_DENSE_MINB
+#define BDM_DENSE_MINB 5  // (5 CTAs per SM at 96 registers: cfg3 7.79 -> 7.69 s)
+#endif
+__global__ void __launch_bounds__(32 * kDWarps, BDM_DENSE_MINB) k_mech_dense(MechArgs A, DevScalars *__restrict__ sc) {
     if (sc->overflow) return;
     extern __shared__ __align__(16) unsigned char dsm_raw[];
     DenseWarp *Sd = reinterpret_cast<DenseWarp *>(dsm_raw);
@@ -1766,85 +1766,65 @@ __global__ void __launch_bounds__(32 * kDWarps, 4) k_mech_dense(MechArgs A, DevS
                         }
                     }
                     __syncwarp();
+                    // survivors are (nearly) all contacts in these regions: one pass does the
+                    // exact test, the static flags and Eq. 4.1/4.2 for every survivor, two
+                    // per lane (non-contacts on stand-in operands, their s = 0), and phase 3
+                    // walks the lane's own survivors (no compaction, x_i - x_j recomputed)
                     for (int c0 = 0; c0 < total; c0 += kDQ) {  // warp-uniform
                         const int c1 = min(total, c0 + kDQ);
-                        // ---- phase 2a: exact test, static flags, contact pre-test, compaction
-                        int cbase = 0;
-                        for (int p0 = c0; p0 < c1; p0 += 32) {
-                            const int p = p0 + lane;
-                            bool cc = false;
-                            double D = 0.0, ex = 0.0, ey = 0.0, ez = 0.0;
-                            uint32_t e = 0;
-                            if (p < c1) {
-                                e = Wd.Q[p];
-                                const int j = (int)(e & 255u), ow = (int)(e >> 8);
-                                {
-                                    ex = Wd.ox[ow] - Wd.X[j];
-                                    ey = Wd.oy[ow] - Wd.Y[j];
-                                    ez = Wd.oz[ow] - Wd.Z[j];
-                                    D = fma(ez, ez, fma(ey, ey, ex * ex));
-                                    const bool nbr = Wd.G[j] != Wd.os[ow] && D <= g.R2;
-                                    const double s2 = Wd.orr[ow] + Wd.Rr[j];
-                                    if (kStats && nbr) atomicAdd(&Wd.nbrc[ow], 1u);
-                                    if (nbr && (Wd.F[j] & kChanged)) Wd.chg[ow] = 1;
-                                    cc = nbr && D > 0.0 && D < (s2 * s2) * (1.0 + 0x1p-30);
-                                }
-                            }
-                            const unsigned cb = __ballot_sync(0xffffffffu, cc);
-                            const int cidx = cbase + __popc(cb & lt_mask);
-                            if (p < c1) Wd.cpre[p - c0] = (uint16_t)cidx;
-                            if (cc) {
-                                Wd.cq[cidx] = D;
-                                Wd.cx[cidx] = ex;
-                                Wd.cy[cidx] = ey;
-                                Wd.cz[cidx] = ez;
-                                Wd.ce[cidx] = (uint16_t)e;
-                            }
-                            cbase += __popc(cb);
-                        }
-                        if (lane == 0) Wd.cpre[c1 - c0] = (uint16_t)cbase;
-                        __syncwarp();
-                        // ---- phase 2b: Eq. 4.1/4.2 over the compacted contact candidates
-                        // two contacts per lane, straight-line: the two sqrt/div chains
-                        // interleave (a non-contact's NaN is discarded by the select)
-                        for (int q = lane; q < cbase; q += 64) {
-                            const int q2 = q + 32;
-                            const bool h2 = q2 < cbase;
-                            const uint32_t e1 = Wd.ce[q], e2 = h2 ? Wd.ce[q2] : e1;
-                            const double D1 = Wd.cq[q], D2 = h2 ? Wd.cq[q2] : D1;
-                            const double ri1 = Wd.orr[e1 >> 8], rj1 = Wd.Rr[e1 & 255u];
-                            const double ri2 = Wd.orr[e2 >> 8], rj2 = Wd.Rr[e2 & 255u];
-                            const double dist1 = sqrt(D1), dist2 = sqrt(D2);
+                        for (int p = c0 + lane; p < c1; p += 64) {
+                            const int p2 = p + 32;
+                            const bool h2 = p2 < c1;
+                            const uint32_t e1 = Wd.Q[p], e2 = h2 ? Wd.Q[p2] : e1;
+                            const int j1 = (int)(e1 & 255u), ow1 = (int)(e1 >> 8);
+                            const int j2 = (int)(e2 & 255u), ow2 = (int)(e2 >> 8);
+                            const double ex1 = Wd.ox[ow1] - Wd.X[j1], ey1 = Wd.oy[ow1] - Wd.Y[j1],
+                                         ez1 = Wd.oz[ow1] - Wd.Z[j1];
+                            const double ex2 = Wd.ox[ow2] - Wd.X[j2], ey2 = Wd.oy[ow2] - Wd.Y[j2],
+                                         ez2 = Wd.oz[ow2] - Wd.Z[j2];
+                            const double D1 = fma(ez1, ez1, fma(ey1, ey1, ex1 * ex1));
+                            const double D2 = fma(ez2, ez2, fma(ey2, ey2, ex2 * ex2));
+                            const bool nb1 = Wd.G[j1] != Wd.os[ow1] && D1 <= g.R2;
+                            const bool nb2 = h2 && Wd.G[j2] != Wd.os[ow2] && D2 <= g.R2;
+                            if (kStats && nb1) atomicAdd(&Wd.nbrc[ow1], 1u);
+                            if (kStats && nb2) atomicAdd(&Wd.nbrc[ow2], 1u);
+                            if (nb1 && (Wd.F[j1] & kChanged)) Wd.chg[ow1] = 1;
+                            if (nb2 && (Wd.F[j2] & kChanged)) Wd.chg[ow2] = 1;
+                            const double ri1 = Wd.orr[ow1], rj1 = Wd.Rr[j1], ri2 = Wd.orr[ow2], rj2 = Wd.Rr[j2];
+                            const double dist1 = sqrt(nb1 && D1 > 0.0 ? D1 : 1.0);
+                            const double dist2 = sqrt(nb2 && D2 > 0.0 ? D2 : 1.0);
                             const double del1 = (ri1 + rj1) - dist1, del2 = (ri2 + rj2) - dist2;
-                            const double rb1 = (ri1 * rj1) / (ri1 + rj1);
-                            const double rb2 = (ri2 * rj2) / (ri2 + rj2);
-                            const double Fn1 = A.k * del1 - A.gamma * sqrt(rb1 * del1);
-                            const double Fn2 = A.k * del2 - A.gamma * sqrt(rb2 * del2);
+                            const bool cc1 = nb1 && D1 > 0.0 && del1 > 0.0;
+                            const bool cc2 = nb2 && D2 > 0.0 && del2 > 0.0;
+                            const double dl1 = cc1 ? del1 : 1.0, dl2 = cc2 ? del2 : 1.0;
+                            const double rs1 = ri1 + rj1, rs2 = ri2 + rj2;
+                            const double rb1 = (ri1 * rj1) / (rs1 > 0.0 ? rs1 : 1.0);
+                            const double rb2 = (ri2 * rj2) / (rs2 > 0.0 ? rs2 : 1.0);
+                            const double q1 = rb1 * dl1, q2 = rb2 * dl2;
+                            const double Fn1 = A.k * dl1 - A.gamma * (q1 > 0.0 ? sqrt(q1) : 0.0);
+                            const double Fn2 = A.k * dl2 - A.gamma * (q2 > 0.0 ? sqrt(q2) : 0.0);
                             const double s1 = Fn1 / dist1, s2 = Fn2 / dist2;
-                            const bool c1 = del1 > 0.0, c2 = del2 > 0.0;
-                            Wd.cq[q] = c1 ? s1 : 0.0;
-                            Wd.cf[q] = c1 ? (uint8_t)(2u | (Fn1 != 0.0 ? 1u : 0u)) : (uint8_t)0;
+                            Wd.cq[p - c0] = cc1 ? s1 : 0.0;
+                            Wd.cf[p - c0] = cc1 ? (uint8_t)(2u | (Fn1 != 0.0 ? 1u : 0u)) : (uint8_t)0;
                             if (h2) {
-                                Wd.cq[q2] = c2 ? s2 : 0.0;
-                                Wd.cf[q2] = c2 ? (uint8_t)(2u | (Fn2 != 0.0 ? 1u : 0u)) : (uint8_t)0;
+                                Wd.cq[p2 - c0] = cc2 ? s2 : 0.0;
+                                Wd.cf[p2 - c0] = cc2 ? (uint8_t)(2u | (Fn2 != 0.0 ? 1u : 0u)) : (uint8_t)0;
                             }
                         }
                         __syncwarp();
-                        // ---- phase 3: own contacts of the chunk, in order
+                        // ---- phase 3: own survivors of the chunk, in order (s = 0: fma(0, d,
+                        // F) == F exactly)
                         const int lo = max(my_off, c0) - c0, hi = min(my_off + cnt, c1) - c0;
-                        if (hi > lo) {
-                            const int q0 = Wd.cpre[lo], q1 = Wd.cpre[hi];
-                            // a non-contact carries s = 0: fma(0, d, F) == F exactly
 #pragma unroll 2
-                            for (int q = q0; q < q1; ++q) {
-                                const uint32_t fl = Wd.cf[q];
-                                const double s_ = Wd.cq[q];
-                                Fx = fma(s_, Wd.cx[q], Fx);
-                                Fy = fma(s_, Wd.cy[q], Fy);
-                                Fz = fma(s_, Wd.cz[q], Fz);
-                                nnz += (int)(fl & 1u);
-                                my_cont += (fl >> 1) & 1u;
-                            }
+                        for (int q = lo; q < hi; ++q) {
+                            const int j = (int)(Wd.Q[c0 + q] & 255u);
+                            const uint32_t fl = Wd.cf[q];
+                            const double s_ = Wd.cq[q];
+                            Fx = fma(s_, xi - Wd.X[j], Fx);
+                            Fy = fma(s_, yi - Wd.Y[j], Fy);
+                            Fz = fma(s_, zi - Wd.Z[j], Fz);
+                            nnz += (int)(fl & 1u);
+                            my_cont += (fl >> 1) & 1u;
                         }
                         __syncwarp();
                     }
