@@ -40,6 +40,7 @@ struct SirArgs {
     uint8_t *__restrict__ state;
     const uint32_t *__restrict__ id;  // nullable: id = index
     double side, L, R2, half, p_inf, p_rec;
+    unsigned long long t_inf, t_rec;  // uniform32(w) < p  <=>  w < t = ceil(p 2^32) (host)
     double Rq, invC;                  // coarse test: padded radius, 1 / (16 L)
     int D, B, cf;                     // fine boxes / coarse blocks per axis; boxes per block
     uint32_t k0, k1, step;
@@ -85,6 +86,32 @@ __device__ __forceinline__ U4 philox10_rk(const SirArgs &A, uint32_t c0, uint32_
         c3 = lo0;
     }
     return U4{c0, c1, c2, c3};
+}
+
+// Alg. 7/8 draws: uniform32(w) < p.  u = w 2^-32 is exact, so u < p <=> w < p 2^32 (exact
+// scaling) <=> w < ceil(p 2^32): one integer comparison with the host's threshold
+#ifndef BDM_SIR_INTCMP
+#define BDM_SIR_INTCMP 1
+#endif
+__device__ __forceinline__ bool draw_below(uint32_t w, double p, unsigned long long t) {
+#if BDM_SIR_INTCMP
+    return (unsigned long long)w < t;
+#else
+    return uniform32(w) < p;
+#endif
+}
+// Alg. 9's component 2 u - 1 with u = w 2^-32: 2u = w 2^-31 is exact, so the single
+// rounding of fma(w, 2^-31, -1) is the rounding of 2u - 1 (bit-identical, no
+// contraction of an inexact product)
+#ifndef BDM_SIR_FMAV
+#define BDM_SIR_FMAV 1
+#endif
+__device__ __forceinline__ double unit_comp(uint32_t w) {
+#if BDM_SIR_FMAV
+    return __fma_rn((double)w, 0x1p-31, -1.0);
+#else
+    return 2.0 * uniform32(w) - 1.0;
+#endif
 }
 
 __device__ __forceinline__ double min_image(double d, double side, double half) {
@@ -252,6 +279,15 @@ __device__ __forceinline__ double wrap_alg9(double el, double max_bound) {
     const double r = fmod_slow(el, max_bound);
     return r < 0.0 ? max_bound + r : r;
 }
+__device__ __forceinline__ bool wrap_fast_ok(double el, double max_bound) {
+    return el > -max_bound && el < 2.0 * max_bound;
+}
+// The fast path of wrap_alg9 as one subtraction: el - (-max) = max + el (the same IEEE
+// sum), el - max, or el - 0 = el exactly (-0 stays -0)
+__device__ __forceinline__ double wrap_fast(double el, double max_bound) {
+    const double t = el < 0.0 ? -max_bound : (el >= max_bound ? max_bound : 0.0);
+    return el - t;
+}
 
 // Infection queries (S agents whose draw passed, ~p_inf of them) are compacted into a
 // per-warp queue with their start-of-step position and resolved 32 at a time, one per
@@ -265,9 +301,35 @@ struct SirQueue {
     double px[kSirQ], py[kSirQ], pz[kSirQ];
 };
 
+// Per-thread S/I/R counts of the final states.  Packed: one 64-bit add per agent,
+// S | I << 21 | R << 42 (a thread counts fewer than 2^21 agents; launch_sir_step checks
+// the bound)
+#ifndef BDM_SIR_PACKED
+#define BDM_SIR_PACKED 1
+#endif
+struct SirCnt {
+#if BDM_SIR_PACKED
+    unsigned long long pk = 0;
+    __device__ __forceinline__ void add(uint32_t st) { pk += 1ull << (21u * st); }
+    __device__ __forceinline__ uint32_t s() const { return (uint32_t)(pk & 0x1FFFFFull); }
+    __device__ __forceinline__ uint32_t i() const { return (uint32_t)((pk >> 21) & 0x1FFFFFull); }
+    __device__ __forceinline__ uint32_t r() const { return (uint32_t)(pk >> 42); }
+#else
+    uint32_t cs = 0, ci = 0, cr = 0;
+    __device__ __forceinline__ void add(uint32_t st) {
+        cs += st == 0;
+        ci += st == 1;
+        cr += st == 2;
+    }
+    __device__ __forceinline__ uint32_t s() const { return cs; }
+    __device__ __forceinline__ uint32_t i() const { return ci; }
+    __device__ __forceinline__ uint32_t r() const { return cr; }
+#endif
+};
+
 // The final state of a queried S agent and its counters.
 __device__ __forceinline__ void sir_resolve(const SirArgs &A, uint32_t i, double px, double py,
-                                            double pz, uint32_t &cs, uint32_t &ci, uint32_t &cr,
+                                            double pz, SirCnt &cc,
                                             uint32_t &cn) {
     uint8_t st = 0;
     if (infected_within(A, px, py, pz)) {
@@ -275,12 +337,10 @@ __device__ __forceinline__ void sir_resolve(const SirArgs &A, uint32_t i, double
         ++cn;
         const uint32_t me = A.id ? A.id[i] : i;
         const U4 r = philox10_rk(A, me, 0u, A.step, 1u);
-        if (uniform32(r.a) < A.p_rec) st = 2;  // Alg. 8 in sequence (R18)
+        if (draw_below(r.a, A.p_rec, A.t_rec)) st = 2;  // Alg. 8 in sequence (R18)
     }
     A.state[i] = st;
-    cs += st == 0;
-    ci += st == 1;
-    cr += st == 2;
+    cc.add(st);
 }
 
 // Whether box (bx+dx, by+dy, bz+dz) (periodic) holds a snapshot-I agent within R of p
@@ -323,7 +383,7 @@ __device__ __forceinline__ bool infected_in_box(const SirArgs &A, double px, dou
 // of one lane walking all 27 boxes while the others wait).  "Any snapshot-I agent within
 // R" does not depend on the order of the boxes, so the result is the same.
 __device__ __forceinline__ void sir_resolve_warp(const SirArgs &A, const SirQueue &Q, int lane, int nq,
-                                                 uint32_t &cs, uint32_t &ci, uint32_t &cr, uint32_t &cn) {
+                                                 SirCnt &cc, uint32_t &cn) {
     const bool act = lane < nq;
     uint32_t i = 0;
     double px = 0.0, py = 0.0, pz = 0.0;
@@ -356,42 +416,38 @@ __device__ __forceinline__ void sir_resolve_warp(const SirArgs &A, const SirQueu
             ++cn;
             const uint32_t me = A.id ? A.id[i] : i;
             const U4 r = philox10_rk(A, me, 0u, A.step, 1u);
-            if (uniform32(r.a) < A.p_rec) st = 2;  // Alg. 8 in sequence (R18)
+            if (draw_below(r.a, A.p_rec, A.t_rec)) st = 2;  // Alg. 8 in sequence (R18)
         }
         A.state[i] = st;
-        cs += st == 0;
-        ci += st == 1;
-        cr += st == 2;
+        cc.add(st);
     }
 }
 
 // One agent of the update (its start-of-step x, y, z, state already loaded): Philox
 // draws, the queue entry for an infection query, recovery, movement and wrap.
+template <typename I>
 __device__ __forceinline__ void sir_agent(const SirArgs &A, SirQueue &Q, int lane, unsigned lt_mask,
-                                          int64_t i, bool valid, double px, double py, double pz,
-                                          uint8_t st, uint32_t me, int &qn, uint32_t &cs, uint32_t &ci,
-                                          uint32_t &cr, uint32_t &cn) {
+                                          I i, bool valid, double px, double py, double pz,
+                                          uint8_t st, uint32_t me, int &qn, SirCnt &cc, uint32_t &cn) {
     const U4 w = philox10_rk(A, me, 0u, A.step, 0u);
     // Alg. 7: an S agent whose draw passed (R17: strict '<', u = w * 2^-32) is queued
-    const bool query = valid && st == 0 && uniform32(w.d) < A.p_inf;
+    const bool query = valid && st == 0 && draw_below(w.d, A.p_inf, A.t_inf);
     if (valid && !query) {
         // Alg. 8: recovery (own state in sequence, R18)
         if (st == 1) {
             const U4 r = philox10_rk(A, me, 0u, A.step, 1u);
-            if (uniform32(r.a) < A.p_rec) {
+            if (draw_below(r.a, A.p_rec, A.t_rec)) {
                 st = 2;
                 A.state[i] = st;
             }
         }
-        cs += st == 0;
-        ci += st == 1;
-        cr += st == 2;
+        cc.add(st);
     }
     // Alg. 9: movement capped at unit length (R16), toroidal wrap (R20)
     if (valid) {
-        double vx = 2.0 * uniform32(w.a) - 1.0;
-        double vy = 2.0 * uniform32(w.b) - 1.0;
-        double vz = 2.0 * uniform32(w.c) - 1.0;
+        double vx = unit_comp(w.a);
+        double vy = unit_comp(w.b);
+        double vz = unit_comp(w.c);
         const double v2 = vx * vx + vy * vy + vz * vz;
         {  // straight-line: 48 % of the lanes need the cap, the warp runs it anyway
             const double nv = sqrt(v2);
@@ -408,9 +464,23 @@ __device__ __forceinline__ void sir_agent(const SirArgs &A, SirQueue &Q, int lan
             vy = cap ? qy : vy;
             vz = cap ? qz : vz;
         }
+#ifndef BDM_SIR_OLDWRAP
+        // one range test for the three coordinates (the literal fmod form only off it)
+        const double ex = px + vx, ey = py + vy, ez = pz + vz;
+        if (wrap_fast_ok(ex, A.side) && wrap_fast_ok(ey, A.side) && wrap_fast_ok(ez, A.side)) {
+            A.x[i] = wrap_fast(ex, A.side);
+            A.y[i] = wrap_fast(ey, A.side);
+            A.z[i] = wrap_fast(ez, A.side);
+        } else {
+            A.x[i] = wrap_alg9(ex, A.side);
+            A.y[i] = wrap_alg9(ey, A.side);
+            A.z[i] = wrap_alg9(ez, A.side);
+        }
+#else
         A.x[i] = wrap_alg9(px + vx, A.side);
         A.y[i] = wrap_alg9(py + vy, A.side);
         A.z[i] = wrap_alg9(pz + vz, A.side);
+#endif
     }
     // queue the infection queries (start-of-step positions)
     const unsigned qb = __ballot_sync(0xffffffffu, query);
@@ -425,9 +495,9 @@ __device__ __forceinline__ void sir_agent(const SirArgs &A, SirQueue &Q, int lan
     if (qn >= 32) {  // warp-uniform: resolve 32 queries, one per lane
         __syncwarp();
 #ifdef BDM_SIR_LANE_SEARCH
-        sir_resolve(A, Q.idx[lane], Q.px[lane], Q.py[lane], Q.pz[lane], cs, ci, cr, cn);
+        sir_resolve(A, Q.idx[lane], Q.px[lane], Q.py[lane], Q.pz[lane], cc, cn);
 #else
-        sir_resolve_warp(A, Q, lane, 32, cs, ci, cr, cn);
+        sir_resolve_warp(A, Q, lane, 32, cc, cn);
 #endif
         __syncwarp();
         qn -= 32;
@@ -444,6 +514,12 @@ __device__ __forceinline__ void sir_agent(const SirArgs &A, SirQueue &Q, int lan
 #ifndef BDM_SIR_MINB
 #define BDM_SIR_MINB 4  // resident blocks per SM the register budget is set for
 #endif
+#ifndef BDM_SIR_IDPF
+#define BDM_SIR_IDPF 0
+#endif
+// I: the agent index type, uint32_t when n + the grid stride < 2^32 (32-bit address
+// arithmetic; the queue holds 32-bit indices in either case), else int64_t
+template <typename I>
 __global__ void __launch_bounds__(kSirThreads, BDM_SIR_MINB) k_sir_update(SirArgs A, DevScalars *__restrict__ sc) {
     if (sc->overflow) return;
     __shared__ SirQueue Qs[kSirThreads / 32];
@@ -451,18 +527,50 @@ __global__ void __launch_bounds__(kSirThreads, BDM_SIR_MINB) k_sir_update(SirArg
     SirQueue &Q = Qs[wid];
     const unsigned lt_mask = (1u << lane) - 1u;
     // per-thread counters: a thread sees at most n / (grid threads) agents (< 2^32)
-    uint32_t cs = 0, ci = 0, cr = 0, cn = 0;
+    SirCnt cc;
+    uint32_t cn = 0;
     int qn = 0;  // warp-uniform queue fill
-    const int64_t nwarps = (int64_t)gridDim.x * (kSirThreads / 32);
-    const int64_t first = ((int64_t)blockIdx.x * (kSirThreads / 32) + wid) * 64, stride = nwarps * 64;
+    const I nwarps = (I)gridDim.x * (I)(kSirThreads / 32);
+    const I first = ((I)blockIdx.x * (I)(kSirThreads / 32) + (I)wid) * (I)64, stride = nwarps * (I)64;
+    const I n = (I)A.n;
     // two 32-agent slices per warp iteration, all their loads issued first (staging
     // the next 64 agents in shared memory with cp.async while computing measured
     // slower: 1.62 vs 1.58 ms at cfg4)
-    for (int64_t i0 = first; i0 < A.n; i0 += stride) {
-        const int64_t ia = i0 + lane, ib = i0 + 32 + lane;
-        const bool va = ia < A.n, vb = ib < A.n;
+#if BDM_SIR_IDPF
+    // the ids (Philox counters) are loaded one iteration ahead: the first Philox round of
+    // an iteration no longer waits on this iteration's loads
+    uint32_t na = 0, nb = 0;
+    {
+        const I ia = first + (I)lane, ib = first + (I)(32 + lane);
+        if (ia < n) na = A.id ? A.id[ia] : (uint32_t)ia;
+        if (ib < n) nb = A.id ? A.id[ib] : (uint32_t)ib;
+    }
+#endif
+    for (I i0 = first; i0 < n; i0 += stride) {
+        const I ia = i0 + (I)lane, ib = i0 + (I)(32 + lane);
+        const bool va = ia < n, vb = ib < n;
         double xa = 0.0, ya = 0.0, za = 0.0, xb = 0.0, yb = 0.0, zb = 0.0;
         uint8_t sa = 0, sb = 0;
+#if BDM_SIR_IDPF
+        const uint32_t ma = na, mb = nb;
+        {
+            const I ja = ia + stride, jb = ib + stride;
+            if (ja < n) na = A.id ? A.id[ja] : (uint32_t)ja;
+            if (jb < n) nb = A.id ? A.id[jb] : (uint32_t)jb;
+        }
+        if (va) {
+            xa = A.x[ia];
+            ya = A.y[ia];
+            za = A.z[ia];
+            sa = A.state[ia];
+        }
+        if (vb) {
+            xb = A.x[ib];
+            yb = A.y[ib];
+            zb = A.z[ib];
+            sb = A.state[ib];
+        }
+#else
         uint32_t ma = 0, mb = 0;  // ids (Philox counters), loaded with the rest
         if (va) {
             xa = A.x[ia];
@@ -478,18 +586,19 @@ __global__ void __launch_bounds__(kSirThreads, BDM_SIR_MINB) k_sir_update(SirArg
             sb = A.state[ib];
             mb = A.id ? A.id[ib] : (uint32_t)ib;
         }
-        sir_agent(A, Q, lane, lt_mask, ia, va, xa, ya, za, sa, ma, qn, cs, ci, cr, cn);
-        sir_agent(A, Q, lane, lt_mask, ib, vb, xb, yb, zb, sb, mb, qn, cs, ci, cr, cn);
+#endif
+        sir_agent(A, Q, lane, lt_mask, ia, va, xa, ya, za, sa, ma, qn, cc, cn);
+        sir_agent(A, Q, lane, lt_mask, ib, vb, xb, yb, zb, sb, mb, qn, cc, cn);
     }
     __syncwarp();
 #ifdef BDM_SIR_LANE_SEARCH
-    if (lane < qn) sir_resolve(A, Q.idx[lane], Q.px[lane], Q.py[lane], Q.pz[lane], cs, ci, cr, cn);
+    if (lane < qn) sir_resolve(A, Q.idx[lane], Q.px[lane], Q.py[lane], Q.pz[lane], cc, cn);
 #else
-    sir_resolve_warp(A, Q, lane, qn, cs, ci, cr, cn);
+    sir_resolve_warp(A, Q, lane, qn, cc, cn);
 #endif
     // block reduction of the counters, one atomic each per block
     __shared__ unsigned long long red[4][kSirThreads / 32];
-    unsigned long long v[4] = {cs, ci, cr, cn};  // warp sums in 64 bits
+    unsigned long long v[4] = {cc.s(), cc.i(), cc.r(), cn};  // warp sums in 64 bits
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
         unsigned long long t = v[q];
@@ -583,6 +692,16 @@ bdm_status launch_sir_step(Ctx *c, bdm_agents *a, const bdm_params *p, double si
     A.half = side * 0.5;
     A.p_inf = p_inf;
     A.p_rec = p_rec;
+    {
+        auto thr = [](double q) -> unsigned long long {
+            const double sc = q * 4294967296.0;  // exact (power-of-two scaling)
+            if (!(sc > 0.0)) return 0ull;        // never (incl. NaN: u < NaN is false)
+            if (sc >= 4294967296.0) return 4294967296ull;  // always
+            return (unsigned long long)ceil(sc);
+        };
+        A.t_inf = thr(p_inf);
+        A.t_rec = thr(p_rec);
+    }
     A.D = D;
     A.B = B;
     A.k0 = (uint32_t)p->seed;
@@ -604,14 +723,25 @@ bdm_status launch_sir_step(Ctx *c, bdm_agents *a, const bdm_params *p, double si
     BDM_CUDA_TRY(cudaMemsetAsync(W.bitmap, 0, ((int64_t)B * B * B + 31) / 32 * 4, st));
     BDM_CUDA_TRY(cudaMemsetAsync(W.misc, 0, 64, st));
     if (a->n > 0) {
-        const unsigned nb = (unsigned)(((a->n + 15) / 16 + 255) / 256);
-        k_sir_collect<<<nb, 256, 0, st>>>(A, c->sc);
         int64_t ub = (a->n + 255) / 256;
         // one resident wave (4 blocks per SM, the launch bounds) striding over the
         // agents: no partial last wave (1.99 -> 1.96 ms/step at cfg4)
         const int64_t maxb = (int64_t)c->sm_count * 4;
         if (ub > maxb) ub = maxb;
-        k_sir_update<<<(unsigned)ub, kSirThreads, 0, st>>>(A, c->sc);
+        // packed per-thread S/I/R counts (SirCnt): at most 4 ceil(n / threads) per thread
+        if (4 * ((a->n + ub * kSirThreads - 1) / (ub * kSirThreads)) >= (1ll << 21)) {
+            set_error("SIR population too large for the per-thread counters of this GPU");
+            return BDM_EINVAL;
+        }
+        const unsigned nb = (unsigned)(((a->n + 15) / 16 + 255) / 256);
+        k_sir_collect<<<nb, 256, 0, st>>>(A, c->sc);
+#ifndef BDM_SIR_FORCE64
+#define BDM_SIR_FORCE64 0
+#endif
+        if (!BDM_SIR_FORCE64 && a->n + ub * kSirThreads * 2 < (1ll << 32))
+            k_sir_update<uint32_t><<<(unsigned)ub, kSirThreads, 0, st>>>(A, c->sc);
+        else
+            k_sir_update<int64_t><<<(unsigned)ub, kSirThreads, 0, st>>>(A, c->sc);
         c->launches += 2;
         BDM_LAUNCH_CHECK("SIR kernels");
     }
