@@ -119,6 +119,28 @@ typedef struct bdm_ctx *bdm_handle;
  * Synchronizing.  Errors: BDM_EINVAL (max_agents < 0, bad device), BDM_ECUDA. */
 bdm_status bdm_create(bdm_handle *out, int device, int64_t max_agents);
 
+/* Caller-supplied device allocator (the caller, e.g. torch's caching
+ * allocator, owns the device memory pool; the paper's engine likewise takes its agent
+ * memory from one pool allocator).  `alloc` returns a device pointer to at
+ * least `bytes` bytes aligned to 256 B, usable on `stream` (NULL: any stream, the
+ * device is idle), or NULL on failure; `release` takes a pointer `alloc` returned.
+ * `user` is passed through unchanged. */
+typedef void *(*bdm_alloc_fn)(size_t bytes, void *stream, void *user);
+typedef void (*bdm_free_fn)(void *ptr, void *stream, void *user);
+
+/* bdm_create with the workspace sized for `max_agents` local agents plus `max_ghosts`
+ * aura agents (bdm_grid_build sorts locals and ghosts together, section 8(e)) and,
+ * when `alloc`/`release` are both non-NULL, every per-agent, grid (box starts, scan
+ * sums) and slab-exchange buffer taken from and returned to them: at creation, at
+ * capacity growth and in bdm_destroy, never inside a step of steady size.  The few
+ * context scalars (< 1 KB), the dense kernel's scratch and the first-use workspaces of
+ * the SIR, oncology and aura-codec rows use cudaMalloc.  The callbacks must stay valid
+ * until bdm_destroy returns and are called from the thread that calls the library.
+ * Synchronizing.  Errors: BDM_EINVAL (negative sizes, bad device, only one of the two
+ * callbacks given), BDM_ECAPACITY (`alloc` returned NULL), BDM_ECUDA. */
+bdm_status bdm_create_ex(bdm_handle *out, int device, int64_t max_agents, int64_t max_ghosts,
+                         bdm_alloc_fn alloc, bdm_free_fn release, void *user);
+
 /* Free the context and its workspace.  Synchronizing.  NULL is a no-op. */
 bdm_status bdm_destroy(bdm_handle h);
 

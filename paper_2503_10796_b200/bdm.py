@@ -21,7 +21,7 @@ NNZ_SHIFT = 4
 
 # Every symbol include/bdm.h declares (checked by tests/test_abi.py).
 EXPORTS = [
-    "bdm_create", "bdm_destroy", "bdm_last_error", "bdm_version", "bdm_init_spheres",
+    "bdm_create", "bdm_create_ex", "bdm_destroy", "bdm_last_error", "bdm_version", "bdm_init_spheres",
     "bdm_grid_build", "bdm_mech_step", "bdm_step", "bdm_step_host", "bdm_run_host", "bdm_sync",
     "bdm_reserve",
     "bdm_get_stats", "bdm_get_grid_info", "bdm_neighbor_pairs", "bdm_peak_dfma",
@@ -122,6 +122,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     PR = ctypes.POINTER(CParams)
     sig = {
         "bdm_create": [ctypes.POINTER(P), ctypes.c_int, i64],
+        "bdm_create_ex": [ctypes.POINTER(P), ctypes.c_int, i64, i64, ALLOC_FN, FREE_FN, P],
         "bdm_destroy": [P],
         "bdm_init_spheres": [P, AG, i64, i64, u64, dbl, dbl, dbl, i32, P],
         "bdm_grid_build": [P, AG, AG, dbl, P],
@@ -314,13 +315,61 @@ def _stream_ptr(stream):
     return ctypes.c_void_p(stream.cuda_stream)
 
 
-class Engine:
-    """Owns a bdm_handle (library workspace on one device)."""
+# bdm_alloc_fn / bdm_free_fn of include/bdm.h
+ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p)
+FREE_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p)
 
-    def __init__(self, device: int = 0, max_agents: int = 1):
+
+class TorchAllocator:
+    """bdm_create_ex callbacks backed by torch's CUDA caching allocator, so the library's
+    per-agent, grid and exchange buffers come out of (and return to) the pool the
+    caller's tensors live in.  Keeps the counts a test can check."""
+
+    def __init__(self, device: int):
+        import torch
+        self.device = int(device)
+        self.live = {}
+        self.n_alloc = self.n_free = 0
+        self.bytes_live = self.bytes_peak = 0
+
+        def _alloc(nbytes, stream, _user):
+            try:
+                st = stream if stream else torch.cuda.current_stream(self.device).cuda_stream
+                p = torch.cuda.caching_allocator_alloc(int(nbytes), self.device, st)
+            except Exception:  # out of memory: the library reports BDM_ECAPACITY
+                return None
+            self.live[p] = int(nbytes)
+            self.n_alloc += 1
+            self.bytes_live += int(nbytes)
+            self.bytes_peak = max(self.bytes_peak, self.bytes_live)
+            return p
+
+        def _free(p, _stream, _user):
+            nb = self.live.pop(p, None)
+            if nb is None:
+                return
+            self.n_free += 1
+            self.bytes_live -= nb
+            torch.cuda.caching_allocator_delete(p)
+
+        self.alloc_cb, self.free_cb = ALLOC_FN(_alloc), FREE_FN(_free)
+
+
+class Engine:
+    """Owns a bdm_handle (library workspace on one device).  With `allocator` (e.g. a
+    TorchAllocator) the workspace is taken from the caller's pool (bdm_create_ex)."""
+
+    def __init__(self, device: int = 0, max_agents: int = 1, max_ghosts: int = 0, allocator=None):
         self.lib = load_library()
         h = ctypes.c_void_p()
-        _check(self.lib.bdm_create(ctypes.byref(h), int(device), int(max_agents)))
+        self.allocator = allocator  # keeps the callbacks alive as long as the handle
+        if allocator is None and max_ghosts == 0:
+            _check(self.lib.bdm_create(ctypes.byref(h), int(device), int(max_agents)))
+        else:
+            _check(self.lib.bdm_create_ex(
+                ctypes.byref(h), int(device), int(max_agents), int(max_ghosts),
+                allocator.alloc_cb if allocator else ALLOC_FN(0),
+                allocator.free_cb if allocator else FREE_FN(0), None))
         self.h = h
         self.device = device
 

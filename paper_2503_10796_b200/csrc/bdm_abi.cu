@@ -28,15 +28,15 @@ static bdm_status fail(bdm_status s, const std::string &msg) {
 }
 
 template <class T>
-static bdm_status dalloc(T **p, int64_t count) {
-    if (*p) cudaFree(*p);
+static bdm_status dalloc(Ctx *c, T **p, int64_t count) {
+    if (*p) ctx_free(c, *p);
     *p = nullptr;
     if (count <= 0) count = 1;
-    cudaError_t e = cudaMalloc((void **)p, (size_t)count * sizeof(T));
+    cudaError_t e = ctx_malloc(c, (void **)p, (size_t)count * sizeof(T));
     if (e != cudaSuccess) {
         *p = nullptr;
         cudaGetLastError();
-        return fail(BDM_ECAPACITY, std::string("cudaMalloc of ") +
+        return fail(BDM_ECAPACITY, std::string("allocation of ") +
                                        std::to_string((long long)count * sizeof(T)) +
                                        " bytes failed: " + cudaGetErrorString(e));
     }
@@ -51,15 +51,15 @@ static bdm_status grow_agents(Ctx *c, int64_t n) {
     // optional buffers are re-allocated at the new size on their next use
     void *opt[] = {c->svol, c->div_rank, c->lrank, c->cls, c->cls2, c->perm};
     for (void *p : opt)
-        if (p) cudaFree(p);
+        if (p) ctx_free(c, p);
     c->svol = nullptr;
     c->div_rank = c->lrank = c->cls = c->cls2 = c->perm = nullptr;
     bdm_status s;
-    if ((s = dalloc(&c->key, cap)) || (s = dalloc(&c->rank, cap)) ||
-        (s = dalloc(&c->perm_tmp, cap)) || (s = dalloc(&c->skey, cap)) ||
-        (s = dalloc(&c->sid, cap)) || (s = dalloc(&c->sx, cap)) ||
-        (s = dalloc(&c->sy, cap)) || (s = dalloc(&c->sz, cap)) || (s = dalloc(&c->sd, cap)) ||
-        (s = dalloc(&c->sidf, cap)) || (s = dalloc(&c->sflags, cap))) {
+    if ((s = dalloc(c, &c->key, cap)) || (s = dalloc(c, &c->rank, cap)) ||
+        (s = dalloc(c, &c->perm_tmp, cap)) || (s = dalloc(c, &c->skey, cap)) ||
+        (s = dalloc(c, &c->sid, cap)) || (s = dalloc(c, &c->sx, cap)) ||
+        (s = dalloc(c, &c->sy, cap)) || (s = dalloc(c, &c->sz, cap)) || (s = dalloc(c, &c->sd, cap)) ||
+        (s = dalloc(c, &c->sidf, cap)) || (s = dalloc(c, &c->sflags, cap))) {
         c->agent_cap = 0;
         return s;
     }
@@ -68,7 +68,7 @@ static bdm_status grow_agents(Ctx *c, int64_t n) {
     // the scan block sums serve both the slot scan and the agent-indexed scans
     const int64_t nb = scan_block_count(cap > c->slot_cap ? cap : c->slot_cap) + 1;
     if (nb > c->block_sums_cap) {
-        if ((s = dalloc(&c->block_sums, nb))) return s;
+        if ((s = dalloc(c, &c->block_sums, nb))) return s;
         c->block_sums_cap = nb;
     }
     return BDM_OK;
@@ -78,13 +78,13 @@ static bdm_status grow_slots(Ctx *c, int64_t nslots) {
     if (nslots <= c->slot_cap) return BDM_OK;
     BDM_CUDA_TRY(cudaDeviceSynchronize());
     bdm_status s;
-    if ((s = dalloc(&c->box_start, nslots + 1)) || (s = dalloc(&c->dense_list, 2 * (nslots / 64) + 2))) {
+    if ((s = dalloc(c, &c->box_start, nslots + 1)) || (s = dalloc(c, &c->dense_list, 2 * (nslots / 64) + 2))) {
         c->slot_cap = 0;
         return s;
     }
     const int64_t nb = scan_block_count(nslots > c->agent_cap ? nslots : c->agent_cap) + 1;
     if (nb > c->block_sums_cap) {
-        if ((s = dalloc(&c->block_sums, nb))) { c->slot_cap = 0; return s; }
+        if ((s = dalloc(c, &c->block_sums, nb))) { c->slot_cap = 0; return s; }
         c->block_sums_cap = nb;
     }
     c->slot_cap = nslots;
@@ -205,9 +205,18 @@ const char *bdm_last_error(void) { return g_err.c_str(); }
 const char *bdm_version(void) { return "bdm 0.1.0 sm_100a"; }
 
 bdm_status bdm_create(bdm_handle *out, int device, int64_t max_agents) {
+    return bdm_create_ex(out, device, max_agents, 0, nullptr, nullptr, nullptr);
+}
+
+bdm_status bdm_create_ex(bdm_handle *out, int device, int64_t max_agents, int64_t max_ghosts,
+                         bdm_alloc_fn alloc, bdm_free_fn release, void *user) {
     if (!out) return fail(BDM_EINVAL, "out is NULL");
     *out = nullptr;
-    if (max_agents < 0) return fail(BDM_EINVAL, "max_agents < 0");
+    if (max_agents < 0 || max_ghosts < 0) return fail(BDM_EINVAL, "max_agents < 0 or max_ghosts < 0");
+    if ((alloc == nullptr) != (release == nullptr))
+        return fail(BDM_EINVAL, "alloc and release must both be given or both be NULL");
+    if (max_agents + max_ghosts > 0xFFFFFFFFll - 1)
+        return fail(BDM_EINVAL, "max_agents + max_ghosts exceeds 2^32 - 2 agents per context");
     int ndev = 0;
     BDM_CUDA_TRY(cudaGetDeviceCount(&ndev));
     if (device < 0 || device >= ndev || device >= kMaxDevices)
@@ -215,6 +224,10 @@ bdm_status bdm_create(bdm_handle *out, int device, int64_t max_agents) {
     BDM_CUDA_TRY(cudaSetDevice(device));
     Ctx *c = new Ctx();
     c->device = device;
+    c->alloc_fn = alloc;
+    c->free_fn = release;
+    c->alloc_ctx = user;
+    c->max_ghosts = max_ghosts;
     cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device);
     if (cudaMalloc(&c->sc, sizeof(DevScalars)) != cudaSuccess ||
         cudaMallocHost(&c->sc_host, sizeof(DevScalars)) != cudaSuccess ||
@@ -228,7 +241,7 @@ bdm_status bdm_create(bdm_handle *out, int device, int64_t max_agents) {
     }
     cudaMemset(c->sc, 0, sizeof(DevScalars));
     c->dims_hint[0] = c->dims_hint[1] = c->dims_hint[2] = 0;
-    bdm_status s = grow_agents(c, max_agents > 0 ? max_agents : 1);
+    bdm_status s = grow_agents(c, max_agents + max_ghosts > 0 ? max_agents + max_ghosts : 1);
     if (s != BDM_OK) {
         bdm_destroy((bdm_handle)c);
         return s;
@@ -251,7 +264,7 @@ bdm_status bdm_destroy(bdm_handle h) {
                     c->block_sums, c->scan_state, c->pair_count, c->n_new, c->lrank, c->cls, c->cls2,
                     c->pack_counts, c->sc};
     for (void *p : bufs)
-        if (p) cudaFree(p);
+        if (p) ctx_free(c, p);
     void *sbufs[] = {c->sir.keys, c->sir.heads, c->sir.next, c->sir.bitmap, c->sir.ix, c->sir.iy,
                      c->sir.iz, c->sir.misc};
     for (void *q : sbufs)
@@ -551,7 +564,7 @@ bdm_status bdm_onco_step(bdm_handle h, bdm_agents *a, uint32_t *age, int64_t age
     const int64_t nb = scan_block_count(id_next + 1) + 1;
     if (nb > c->block_sums_cap) {
         BDM_CUDA_TRY(cudaDeviceSynchronize());
-        if ((s = dalloc(&c->block_sums, nb)) != BDM_OK) return s;
+        if ((s = dalloc(c, &c->block_sums, nb)) != BDM_OK) return s;
         c->block_sums_cap = nb;
     }
     c->grid_valid = false;
@@ -795,8 +808,8 @@ bdm_status bdm_set_option(bdm_handle h, const char *name, int64_t value) {
         BDM_CUDA_TRY(cudaMemcpy(&c->sc->tile_order, &v, sizeof(v), cudaMemcpyHostToDevice));
         c->tile_order = (int)value;
         // the slot layout changes: the next build re-sizes the slot array from its geometry
-        if (c->box_start) cudaFree(c->box_start);
-        if (c->dense_list) cudaFree(c->dense_list);
+        ctx_free(c, c->box_start);
+        ctx_free(c, c->dense_list);
         c->box_start = nullptr;
         c->dense_list = nullptr;
         c->slot_cap = 0;

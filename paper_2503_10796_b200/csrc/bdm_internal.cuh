@@ -9,6 +9,7 @@
 #include <stdint.h>
 
 #include <string>
+#include <unordered_set>
 
 #include "bdm.h"
 
@@ -159,17 +160,51 @@ struct Ctx {
     SirWs sir;
     AuraWs aura;
     Dist *dist = nullptr;  // bdm_dist_init / bdm_dist_init_virtual
+    // bdm_create_ex: the caller's allocator for the per-agent, grid and exchange buffers
+    // (NULL: cudaMalloc / cudaFree), and the blocks it handed out
+    bdm_alloc_fn alloc_fn = nullptr;
+    bdm_free_fn free_fn = nullptr;
+    void *alloc_ctx = nullptr;
+    std::unordered_set<void *> user_blocks;
+    int64_t max_ghosts = 0;
 };
+
+// Library-owned device memory of the step path: through the caller's allocator when
+// bdm_create_ex was given one, else cudaMalloc / cudaFree.  Called at creation and capacity
+// growth (after a device synchronization; stream NULL) and when an exchange buffer grows
+// (after the exchange's host synchronization, with the exchange's stream), never inside a
+// step of steady size.
+inline cudaError_t ctx_malloc(Ctx *c, void **p, size_t bytes, cudaStream_t st = nullptr) {
+    if (c && c->alloc_fn) {
+        void *q = c->alloc_fn(bytes ? bytes : 1, (void *)st, c->alloc_ctx);
+        if (!q) {
+            *p = nullptr;
+            return cudaErrorMemoryAllocation;
+        }
+        c->user_blocks.insert(q);
+        *p = q;
+        return cudaSuccess;
+    }
+    return cudaMalloc(p, bytes ? bytes : 1);
+}
+inline void ctx_free(Ctx *c, void *p) {
+    if (!p) return;
+    if (c && c->free_fn && c->user_blocks.erase(p)) {
+        c->free_fn(p, nullptr, c->alloc_ctx);
+        return;
+    }
+    cudaFree(p);
+}
 
 // An optional per-agent buffer (agent_cap + 1 entries), allocated on first use.
 template <class T>
 inline bdm_status need_agent_buf(Ctx *c, T **p) {
     if (*p) return BDM_OK;
-    const cudaError_t e = cudaMalloc((void **)p, (size_t)(c->agent_cap + 1) * sizeof(T));
+    const cudaError_t e = ctx_malloc(c, (void **)p, (size_t)(c->agent_cap + 1) * sizeof(T));
     if (e != cudaSuccess) {
         *p = nullptr;
         cudaGetLastError();
-        return cuda_fail(e, "cudaMalloc of an optional per-agent buffer");
+        return cuda_fail(e, "allocation of an optional per-agent buffer");
     }
     return BDM_OK;
 }

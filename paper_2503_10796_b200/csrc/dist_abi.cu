@@ -94,20 +94,20 @@ struct XBuf {  // library-owned SoA agent buffer
     int64_t cap = 0;
 };
 
-static void xbuf_free(XBuf &b) {
+static void xbuf_free(Ctx *c, XBuf &b) {
     void *p[] = {b.x, b.y, b.z, b.d, b.v, b.id, b.f};
     for (void *q : p)
-        if (q) cudaFree(q);
+        if (q) ctx_free(c, q);
     b = XBuf();
 }
 
-static bdm_status xbuf_reserve(XBuf &b, int64_t n, bool vol) {
+static bdm_status xbuf_reserve(Ctx *c, cudaStream_t st, XBuf &b, int64_t n, bool vol) {
     if (n <= b.cap && (!vol || b.v)) return BDM_OK;
     const int64_t cap = n > b.cap ? n + n / 4 + 1024 : b.cap;
-    xbuf_free(b);
+    xbuf_free(c, b);
     cudaError_t e = cudaSuccess;
     auto al = [&](void **p, size_t sz) {
-        if (e == cudaSuccess) e = cudaMalloc(p, (size_t)cap * sz);
+        if (e == cudaSuccess) e = ctx_malloc(c, p, (size_t)cap * sz, st);
     };
     al((void **)&b.x, 8);
     al((void **)&b.y, 8);
@@ -117,7 +117,7 @@ static bdm_status xbuf_reserve(XBuf &b, int64_t n, bool vol) {
     al((void **)&b.f, 4);
     if (vol) al((void **)&b.v, 8);
     if (e != cudaSuccess) {
-        xbuf_free(b);
+        xbuf_free(c, b);
         cudaGetLastError();
         return cuda_fail(e, "allocation of an exchange buffer");
     }
@@ -161,8 +161,8 @@ void free_dist(Ctx *c) {
     Dist *D = c->dist;
     if (!D) return;
     for (int k = 0; k < 4; ++k) {
-        xbuf_free(D->send[k]);
-        xbuf_free(D->recv[k]);
+        xbuf_free(c, D->send[k]);
+        xbuf_free(c, D->recv[k]);
     }
     void *p[] = {D->cnt, D->ctr, D->enc, D->frame, D->holes, D->fillers, D->vframes};
     for (void *q : p)
@@ -383,7 +383,7 @@ static bdm_status x_pack(Ctx *c, Dist *D, bdm_agents *a, cudaStream_t st) {
     }
     const bool vol = a->volume != nullptr;
     for (int k = 0; k < 4; ++k) {
-        bdm_status s = xbuf_reserve(D->send[k], 1, vol);
+        bdm_status s = xbuf_reserve(c, st, D->send[k], 1, vol);
         if (s != BDM_OK) return s;
     }
     BDM_CUDA_TRY(cudaMemsetAsync(D->ctr, 0, 10 * sizeof(unsigned long long), st));
@@ -453,7 +453,7 @@ static bdm_status x_after_counts(Ctx *c, Dist *D, bdm_agents *a, cudaStream_t st
     if (h[9]) {  // a send buffer was too small: grow and pack again (stream order)
         const bool vol = a->volume != nullptr;
         for (int k = 0; k < 4; ++k) {
-            bdm_status s = xbuf_reserve(D->send[k], h[k], vol);
+            bdm_status s = xbuf_reserve(c, st, D->send[k], h[k], vol);
             if (s != BDM_OK) return s;
         }
         bdm_status s = x_pack(c, D, a, st);
@@ -468,7 +468,7 @@ static bdm_status x_after_counts(Ctx *c, Dist *D, bdm_agents *a, cudaStream_t st
     D->in_aura[1] = h[7];
     const bool vol = a->volume != nullptr;
     for (int k = 0; k < 4; ++k) {
-        bdm_status s = xbuf_reserve(D->recv[k], h[4 + k] > 0 ? h[4 + k] : 1, vol);
+        bdm_status s = xbuf_reserve(c, st, D->recv[k], h[4 + k] > 0 ? h[4 + k] : 1, vol);
         if (s != BDM_OK) return s;
     }
     return BDM_OK;
