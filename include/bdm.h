@@ -514,7 +514,7 @@ bdm_status bdm_set_option(bdm_handle h, const char *name, int64_t value);
  * agents (host-only; -1 for negative sizes). */
 int64_t bdm_aura_max_size(int64_t nref, int64_t n);
 
-/* ref := msg sorted by ascending id (R46; CUB radix sort + gather).  ref->capacity >=
+/* ref := msg sorted by ascending id (R46; hand-written LSD radix sort of (id, index) pairs, four 8-bit passes, + gather).  ref->capacity >=
  * msg->n; sets ref->n.  Asynchronous on `stream`.  Errors: BDM_EINVAL (NULL arrays),
  * BDM_ECAPACITY. */
 bdm_status bdm_aura_reference(bdm_handle h, const bdm_agents *msg, bdm_agents *ref, void *stream);

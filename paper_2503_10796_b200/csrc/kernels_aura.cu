@@ -28,7 +28,6 @@
 #include <stdint.h>
 #include <string.h>
 
-#include <cub/device/device_radix_sort.cuh>
 #include <vector>
 
 #include "bdm_internal.cuh"
@@ -434,9 +433,69 @@ __global__ void k_aura_unfill(const uint8_t *__restrict__ pay, int64_t nref, int
 }
 
 // ------------------------------------------------------------------ reference (R46)
-__global__ void k_iota(int64_t n, uint32_t *__restrict__ v) {
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i < n) v[i] = (uint32_t)i;
+// ------------------------------------------------------------------ radix sort by id
+// The reference order of a message (ascending id) as a least-significant-
+// digit radix sort of (id, index) pairs: four stable passes over 8-bit digits.  A block
+// owns a tile of kRsTile consecutive pairs.  k_rs_hist counts its digits into
+// hist[digit * nblocks + block]; the exclusive scan of that table (digit-major) is each
+// block's first output slot per digit; k_rs_scatter ranks the tile's pairs stably (round
+// by round of 256 consecutive pairs: earlier rounds, earlier warps, lower lanes with the
+// same digit, found with match.any) and moves them.  Ids are unique, so the result does
+// not depend on stability between equal keys, only between equal digits.
+constexpr int kRsThreads = 256;
+constexpr int kRsRounds = 8;
+constexpr int kRsTile = kRsThreads * kRsRounds;
+
+__global__ void __launch_bounds__(kRsThreads) k_rs_hist(int64_t n, const uint32_t *__restrict__ key,
+                                                        int shift, uint32_t *__restrict__ hist,
+                                                        int64_t nblocks) {
+    __shared__ uint32_t cnt[256];
+    cnt[threadIdx.x] = 0u;
+    __syncthreads();
+    const int64_t base = blockIdx.x * (int64_t)kRsTile;
+#pragma unroll
+    for (int r = 0; r < kRsRounds; ++r) {
+        const int64_t i = base + r * kRsThreads + threadIdx.x;
+        if (i < n) atomicAdd(&cnt[(key[i] >> shift) & 255u], 1u);
+    }
+    __syncthreads();
+    hist[threadIdx.x * nblocks + blockIdx.x] = cnt[threadIdx.x];
+    if (blockIdx.x == 0 && threadIdx.x == 0) hist[256 * nblocks] = 0u;
+}
+
+__global__ void __launch_bounds__(kRsThreads) k_rs_scatter(
+    int64_t n, const uint32_t *__restrict__ key, const uint32_t *__restrict__ val /* NULL: index */,
+    int shift, const uint32_t *__restrict__ offs, int64_t nblocks, uint32_t *__restrict__ key_out,
+    uint32_t *__restrict__ val_out) {
+    __shared__ uint32_t wcnt[kRsThreads / 32][256];
+    __shared__ uint32_t running[256];
+    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    running[t] = offs[t * nblocks + blockIdx.x];
+    const int64_t base = blockIdx.x * (int64_t)kRsTile;
+    for (int r = 0; r < kRsRounds; ++r) {
+#pragma unroll
+        for (int q = 0; q < kRsThreads / 32; ++q) wcnt[q][t] = 0u;
+        __syncthreads();  // (also orders the previous round's update of `running`)
+        const int64_t i = base + r * kRsThreads + t;
+        const bool on = i < n;
+        const uint32_t k = on ? key[i] : 0u;
+        const uint32_t d = on ? (k >> shift) & 255u : 256u + (uint32_t)lane;  // idle lanes match nobody
+        const unsigned peers = __match_any_sync(0xffffffffu, d);
+        const uint32_t below = __popc(peers & ((1u << lane) - 1u));
+        if (on && below == 0u) wcnt[w][d] = __popc(peers);
+        __syncthreads();
+        if (on) {
+            uint32_t pos = running[d] + below;
+            for (int q = 0; q < w; ++q) pos += wcnt[q][d];
+            key_out[pos] = k;
+            val_out[pos] = val ? val[i] : (uint32_t)i;
+        }
+        __syncthreads();
+        uint32_t tot = 0;
+#pragma unroll
+        for (int q = 0; q < kRsThreads / 32; ++q) tot += wcnt[q][t];
+        running[t] += tot;
+    }
 }
 
 __global__ void k_aura_gather(int64_t n, const uint32_t *__restrict__ perm, AuraView m, AuraOut o,
@@ -469,10 +528,10 @@ static bdm_status ensure_scan(Ctx *c, int64_t m) {
     const int64_t nb = scan_block_count(m) + 1;
     if (nb <= c->block_sums_cap) return BDM_OK;
     BDM_CUDA_TRY(cudaDeviceSynchronize());
-    if (c->block_sums) cudaFree(c->block_sums);
+    ctx_free(c, c->block_sums);  // (allocated through the context's allocator, bdm_create_ex)
     c->block_sums = nullptr;
     c->block_sums_cap = 0;
-    BDM_CUDA_TRY(cudaMalloc(&c->block_sums, (size_t)nb * sizeof(uint32_t)));
+    BDM_CUDA_TRY(ctx_malloc(c, (void **)&c->block_sums, (size_t)nb * sizeof(uint32_t)));
     c->block_sums_cap = nb;
     return BDM_OK;
 }
@@ -498,17 +557,24 @@ bdm_status launch_aura_reference(Ctx *c, const bdm_agents *m, bdm_agents *r, cud
     bdm_status s;
     if ((s = ensure(&W.u32a, W.u32a_cap, 2 * n + 2)) != BDM_OK) return s;
     if ((s = ensure(&W.u32b, W.u32b_cap, 2 * n + 2)) != BDM_OK) return s;
-    uint32_t *keys_out = W.u32a + n + 1, *vals_in = W.u32b, *vals_out = W.u32b + n + 1;
+    uint32_t *const kb[2] = {W.u32a, W.u32a + n + 1}, *const vb[2] = {W.u32b, W.u32b + n + 1};
+    uint32_t *keys_out = kb[1], *vals_out = vb[1];  // four passes end in buffer 1
     if (n > 0) {
-        k_iota<<<nblk(n, 256), 256, 0, st>>>(n, vals_in);
-        size_t tb = 0;
-        BDM_CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, tb, m->id, keys_out, vals_in,
-                                                     vals_out, (int)n, 0, 32, st));
-        if ((s = ensure(&W.tmp, W.tmp_cap, (int64_t)tb)) != BDM_OK) return s;
-        BDM_CUDA_TRY(cub::DeviceRadixSort::SortPairs(W.tmp, tb, m->id, keys_out, vals_in,
-                                                     vals_out, (int)n, 0, 32, st));
+        const int64_t nb = (n + kRsTile - 1) / kRsTile;
+        if ((s = ensure(&W.tmp, W.tmp_cap, (256 * nb + 1) * (int64_t)sizeof(uint32_t))) != BDM_OK) return s;
+        if ((s = ensure_scan(c, 256 * nb + 1)) != BDM_OK) return s;
+        uint32_t *const hist = reinterpret_cast<uint32_t *>(W.tmp);
+        for (int pass = 0; pass < 4; ++pass) {
+            const uint32_t *kin = pass == 0 ? m->id : kb[(pass + 1) & 1];
+            const uint32_t *vin = pass == 0 ? nullptr : vb[(pass + 1) & 1];
+            k_rs_hist<<<(unsigned)nb, kRsThreads, 0, st>>>(n, kin, 8 * pass, hist, nb);
+            if ((s = launch_scan_u32(c, hist, 256 * nb + 1, st)) != BDM_OK) return s;
+            k_rs_scatter<<<(unsigned)nb, kRsThreads, 0, st>>>(n, kin, vin, 8 * pass, hist, nb,
+                                                              kb[pass & 1], vb[pass & 1]);
+            c->launches += 2;
+        }
         k_aura_gather<<<nblk(n, 256), 256, 0, st>>>(n, vals_out, view(m), outv(r), keys_out);
-        c->launches += 2;  // iota, gather (the radix sort is CUB's)
+        c->launches += 1;
         BDM_LAUNCH_CHECK("aura reference");
     }
     r->n = n;

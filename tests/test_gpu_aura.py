@@ -93,6 +93,32 @@ def test_reference_is_id_order(eng, orc):
     _same(_host(r), orc.aura_reference(msg))
 
 
+@pytest.mark.parametrize("n", [0, 1, 31, 2048, 2049, 70_001, 1_000_003])
+def test_reference_radix_sort_full_id_range(eng, n):
+    """The hand-written LSD radix sort behind bdm_aura_reference: unique ids drawn over
+    the whole 32-bit range (every digit of every pass is exercised), sizes around the
+    2,048-pair tile and many tiles with a ragged tail; every field follows its id.
+    Expected values from numpy's argsort (ids are unique, so the order is unique)."""
+    from paper_2503_10796_b200 import Agents
+    rng = np.random.default_rng(100 + n)
+    pool = np.unique(rng.integers(0, 2 ** 32, int(1.1 * n) + 8, dtype=np.uint64).astype(np.uint32))
+    pool = pool[(pool != 0) & (pool != 0xFFFFFFFF)]
+    ids = rng.permutation(pool)[:n]
+    if n > 2:
+        ids[0], ids[1] = np.uint32(0xFFFFFFFF), np.uint32(0)   # both ends of the key range
+    ids = rng.permutation(ids)
+    assert len(ids) == n
+    msg = {"x": rng.uniform(0, 9, n), "y": rng.uniform(0, 9, n), "z": rng.uniform(0, 9, n),
+           "d": rng.uniform(8, 12, n), "id": ids, "flags": rng.integers(0, 2 ** 32, n, dtype=np.uint64).astype(np.uint32)}
+    r = Agents.empty(max(n, 1))
+    eng.aura_reference(_dev(msg, capacity=max(n, 1)), r)
+    got = _host(r)
+    order = np.argsort(ids, kind="stable")
+    assert r.n == n
+    for k in FIELDS:
+        assert np.array_equal(np.asarray(got[k])[:n].view(np.uint8), np.ascontiguousarray(msg[k][order]).view(np.uint8)), k
+
+
 @pytest.mark.parametrize("case", ["moved", "identical", "no_reference", "empty_message", "churn"])
 def test_stream_bytes_equal_oracle_and_round_trip(eng, orc, case):
     before, after = _slab_aura(orc, 30000, 2)
