@@ -473,7 +473,10 @@ bdm_status bdm_neighbor_pairs(bdm_handle h, const bdm_agents *a, double radius,
  *   "tile_depth"   0 (default) auto: two-tile work units when the first grid build of the
  *                  context had at most one agent per box, else one; 1 or 2 force it.
  *                  Two tiles stacked in z share one staged 6x6x10-box region, so sparse
- *                  populations fill the 32-lane batches (cfg5: -18 % k_mech).
+ *                  populations fill the 32-lane batches (cfg5: -18 % k_mech).  3 (default
+ *                  kernel only): two-tile units for denser populations, 8 warps sharing
+ *                  a region of up to 672 staged agents, 3 CTAs per SM (same result; as
+ *                  fast as depth 1 at cfg2, so never chosen automatically).
  *   "tile_order"   0 (default) row-major 4x4x4-box tiles; 1 blocked Hilbert: super-tiles
  *                  of 8^3 tiles row-major, the tiles inside one along a 3-D Hilbert
  *                  curve (the paper's Hilbert variant of agent

@@ -817,7 +817,7 @@ bdm_status bdm_set_option(bdm_handle h, const char *name, int64_t value) {
         return BDM_OK;
     }
     if (strcmp(name, "tile_depth") == 0) {
-        if (value < 0 || value > 2) return fail(BDM_EINVAL, "tile_depth must be 0, 1 or 2");
+        if (value < 0 || value > 3) return fail(BDM_EINVAL, "tile_depth must be 0, 1, 2 or 3");
         c->tile_depth = (int)value;
         return BDM_OK;
     }

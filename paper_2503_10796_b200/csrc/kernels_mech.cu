@@ -427,7 +427,7 @@ struct Warp6 {
 // global memory this is what lets six CTAs share an SM
 constexpr int kQ7Cap = 240;   // survivors per batch (mean ~4 contacts per agent)
 struct Warp7 {
-    uint32_t pr[kQ7Cap];                    // survivor: m | mo << 9 | owner << 18, flags << 24
+    uint32_t pr[kQ7Cap];                    // survivor: m | mo << 10 | owner << 20, flags << 25
     union {
         struct {
             uint32_t run[10][32];           // per lane: trimmed runs (start | end << 16)
@@ -462,9 +462,11 @@ struct TileGeo {
     static constexpr int kSQ = (kNB + 31) / 32;      // scan items per lane
     using MBox = typename std::conditional<(kNB > 255), uint16_t, uint8_t>::type;
 };
-template <bool kPair, int kTZ = 1, bool kV7 = false>
+template <bool kPair, int kTZ = 1, bool kV7 = false, int kThreads = kT6Threads, int kMMo = 0>
 struct Tile6SmemT {
-    static constexpr int kMM = kV7 ? 404 : kM6Max;  // staged agents per region (6 CTAs/SM)
+    // staged agents per region (404: 6 CTAs/SM; kMMo: the 8-warp two-tile units)
+    static constexpr int kMM = kMMo ? kMMo : (kV7 ? 404 : kM6Max);
+    static constexpr int kWarps = kThreads / 32;
     using WarpT = typename std::conditional<kV7, Warp7, Warp6>::type;
     GridView g;
     float R2f, Lf;
@@ -474,14 +476,14 @@ struct Tile6SmemT {
     int lo_box[3], hi_box[3];               // boxes that can hold a new extremum (see below)
     uint32_t start[TileGeo<kTZ>::kNB];
     uint32_t off[TileGeo<kTZ>::kNB + 4];
-    uint32_t wsum[kT6Warps];                // box-table scan: warp totals
+    uint32_t wsum[kWarps];                  // box-table scan: warp totals
     Fp32Stage<kPair, kMM> f;
     double X[kMM], Y[kMM], Z[kMM], Rr[kMM];
     uint32_t F[kV7 ? 1 : kMM];              // flags (kV7 reads them from global memory)
     uint16_t kmi[kMM];                      // tile agent k -> staged index
     uint16_t lbxyz[TileGeo<kTZ>::kNB];      // region box -> x | y << 3 | z << 6 | inner << 10
     typename TileGeo<kTZ>::MBox mbox[kMM];  // staged index -> region box
-    WarpT W[kT6Warps];
+    WarpT W[kWarps];
 };
 using Tile6Smem = Tile6SmemT<false>;
 
@@ -830,8 +832,8 @@ __device__ __forceinline__ void tile6_batch(const MechArgs &A, const Tile6SmemT<
 // The test is the same conservative contact (or neighbour) test as before with the
 // squared distance summed as (dx^2 + dy^2) + dz^2: five roundings instead of the fma
 // chain's three, 2^-21.7 relative, still far inside the margin of tile7_batch's note.
-template <bool kStats, bool kMin, int kTZ>
-__device__ __forceinline__ int tile7_walk(const Tile6SmemT<false, kTZ, true> &S, Warp7 &Wp, int lane,
+template <bool kStats, bool kMin, int kTZ, typename SmemT>
+__device__ __forceinline__ int tile7_walk(const SmemT &S, Warp7 &Wp, int lane,
                                           float4 pi, int cmax, int M, float R2f) {
     const char *const pb = reinterpret_cast<const char *>(&S.f.P[0]);
     const uint32_t mlast = (uint32_t)M << 4;
@@ -876,8 +878,8 @@ __device__ __forceinline__ int tile7_walk(const Tile6SmemT<false, kTZ, true> &S,
 #else
 // The flattened walk of one lane over its trimmed runs (see tile7_batch); returns the
 // number of survivors, listed (byte offsets m << 4) in Wp.u.a.lst[.][lane].
-template <bool kStats, bool kMin, int kTZ>
-__device__ __forceinline__ int tile7_walk(const Tile6SmemT<false, kTZ, true> &S, Warp7 &Wp, int lane,
+template <bool kStats, bool kMin, int kTZ, typename SmemT>
+__device__ __forceinline__ int tile7_walk(const SmemT &S, Warp7 &Wp, int lane,
                                           float4 pi, int cmax, int M, float R2f) {
     int cnt = 0;
     const char *pb = reinterpret_cast<const char *>(&S.f.P[0]);
@@ -927,8 +929,8 @@ __device__ __forceinline__ int tile7_walk(const Tile6SmemT<false, kTZ, true> &S,
 // 2^-19 L)^2 (1 + 2^-22); a counted contact has rho < (r_i + r_j)(1 + 2^-49) and rho <=
 // R(1 + 2^-50), while the threshold is >= (r_i + r_j + 2^-15 L)^2 (1 - 2^-21.4): at
 // least 8x margin whenever r_i + r_j <= L, and beyond that rho <= R bounds it.
-template <bool kStats, int kTZ>
-__device__ __forceinline__ void tile7_batch(const MechArgs &A, const Tile6SmemT<false, kTZ, true> &S,
+template <bool kStats, int kTZ, typename SmemT>
+__device__ __forceinline__ void tile7_batch(const MechArgs &A, const SmemT &S,
                                             Warp7 &Wp, int lane, uint32_t g0, int n0, uint32_t g1,
                                             int klo, int na, int M, int sides) {
     const float R2f = S.R2f, Lf = S.Lf;
@@ -989,8 +991,8 @@ __device__ __forceinline__ void tile7_batch(const MechArgs &A, const Tile6SmemT<
     __syncwarp();
     // ---- phase 1: the flattened walk with the contact (or neighbour) test; the min with
     // R2f only matters for static candidates (r'_i = inf), so warps without one skip it
-    int cnt = cs_mask ? tile7_walk<kStats, true, kTZ>(S, Wp, lane, pi, cmax, M, R2f)
-                      : tile7_walk<kStats, false, kTZ>(S, Wp, lane, pi, cmax, M, R2f);
+    int cnt = cs_mask ? tile7_walk<kStats, true, kTZ, SmemT>(S, Wp, lane, pi, cmax, M, R2f)
+                      : tile7_walk<kStats, false, kTZ, SmemT>(S, Wp, lane, pi, cmax, M, R2f);
     if (active) --cnt;  // the agent itself (D32 = 0) is always among the survivors
     int cincl = cnt;
 #pragma unroll
@@ -1008,7 +1010,7 @@ __device__ __forceinline__ void tile7_batch(const MechArgs &A, const Tile6SmemT<
         return;
     }
     {
-        const uint32_t tag = ((uint32_t)mi << 9) | ((uint32_t)lane << 18);
+        const uint32_t tag = ((uint32_t)mi << 10) | ((uint32_t)lane << 20);
         const uint32_t self = (uint32_t)mi << 4;
         const int cmx = __reduce_max_sync(0xffffffffu, active ? cnt + 1 : cnt);
         int wo = my_off;
@@ -1024,9 +1026,9 @@ __device__ __forceinline__ void tile7_batch(const MechArgs &A, const Tile6SmemT<
     if (cs_mask) {
         for (int p = lane; p < total; p += 32) {
             const uint32_t e = Wp.pr[p];
-            const int ow = (int)((e >> 18) & 31u);
+            const int ow = (int)((e >> 20) & 31u);
             if (!((cs_mask >> ow) & 1u)) continue;
-            const int m = (int)(e & 511u), mo = (int)((e >> 9) & 511u);
+            const int m = (int)(e & 1023u), mo = (int)((e >> 10) & 1023u);
             const double ex = S.X[mo] - S.X[m], ey = S.Y[mo] - S.Y[m], ez = S.Z[mo] - S.Z[m];
             const double D = fma(ez, ez, fma(ey, ey, ex * ex));
             if (D <= R2 && m != mo) {
@@ -1040,21 +1042,21 @@ __device__ __forceinline__ void tile7_batch(const MechArgs &A, const Tile6SmemT<
     const unsigned stat_mask = __ballot_sync(0xffffffffu, is_static);
     // ---- phase 2: exact test + Eq. 4.1/4.2 for every survivor of a non-static owner,
     // two per lane in straight-line code; s goes to u.b.sq, the flags (bit0 F_N != 0,
-    // bit1 contact, bit2 neighbour) to bits 24-26 of the entry
+    // bit1 contact, bit2 neighbour) to bits 25-27 of the entry
     double *const sq = Wp.u.c.sq;
     for (int p = lane; p < total; p += 64) {  // (u.a is no longer needed)
         const int p2 = p + 32;
         const bool h2 = p2 < total;
         const uint32_t e1 = Wp.pr[p], e2 = h2 ? Wp.pr[p2] : e1;
-        const int m1 = (int)(e1 & 511u), mo1 = (int)((e1 >> 9) & 511u);
-        const int m2 = (int)(e2 & 511u), mo2 = (int)((e2 >> 9) & 511u);
+        const int m1 = (int)(e1 & 1023u), mo1 = (int)((e1 >> 10) & 1023u);
+        const int m2 = (int)(e2 & 1023u), mo2 = (int)((e2 >> 10) & 1023u);
         const double ex1 = S.X[mo1] - S.X[m1], ey1 = S.Y[mo1] - S.Y[m1], ez1 = S.Z[mo1] - S.Z[m1];
         const double ex2 = S.X[mo2] - S.X[m2], ey2 = S.Y[mo2] - S.Y[m2], ez2 = S.Z[mo2] - S.Z[m2];
         const double D1 = fma(ez1, ez1, fma(ey1, ey1, ex1 * ex1));
         const double D2 = fma(ez2, ez2, fma(ey2, ey2, ex2 * ex2));
         const double ri1 = S.Rr[mo1], rj1 = S.Rr[m1], ri2 = S.Rr[mo2], rj2 = S.Rr[m2];
-        const bool w1 = !((stat_mask >> ((e1 >> 18) & 31u)) & 1u);
-        const bool w2 = !((stat_mask >> ((e2 >> 18) & 31u)) & 1u);
+        const bool w1 = !((stat_mask >> ((e1 >> 20) & 31u)) & 1u);
+        const bool w2 = !((stat_mask >> ((e2 >> 20) & 31u)) & 1u);
         const bool nb1 = D1 <= R2 && m1 != mo1, nb2 = D2 <= R2 && m2 != mo2;
         // non-contacts (the agent itself, D = 0, overlap <= 0) run on harmless stand-in
         // operands: no NaN or zero reaches the IEEE sqrt/div, so they stay on their fast
@@ -1074,10 +1076,10 @@ __device__ __forceinline__ void tile7_batch(const MechArgs &A, const Tile6SmemT<
         const uint32_t f1 = (nb1 ? 4u : 0u) | (c1 ? (2u | (Fn1 != 0.0 ? 1u : 0u)) : 0u);
         const uint32_t f2 = (nb2 ? 4u : 0u) | (c2 ? (2u | (Fn2 != 0.0 ? 1u : 0u)) : 0u);
         sq[p] = c1 ? s1 : 0.0;
-        Wp.pr[p] = (e1 & 0x00FFFFFFu) | (f1 << 24);
+        Wp.pr[p] = (e1 & 0x01FFFFFFu) | (f1 << 25);
         if (h2) {
             sq[p2] = c2 ? s2 : 0.0;
-            Wp.pr[p2] = (e2 & 0x00FFFFFFu) | (f2 << 24);
+            Wp.pr[p2] = (e2 & 0x01FFFFFFu) | (f2 << 25);
         }
     }
     __syncwarp();
@@ -1091,14 +1093,14 @@ __device__ __forceinline__ void tile7_batch(const MechArgs &A, const Tile6SmemT<
 #pragma unroll 2
         for (int q = my_off; q < my_off + cnt; ++q) {
             const uint32_t ev = Wp.pr[q];
-            const int m = (int)(ev & 511u);
+            const int m = (int)(ev & 1023u);
             const double s_ = sq[q];
             Fx = fma(s_, xi - S.X[m], Fx);
             Fy = fma(s_, yi - S.Y[m], Fy);
             Fz = fma(s_, zi - S.Z[m], Fz);
-            nnz += (int)((ev >> 24) & 1u);
-            my_cont += (ev >> 25) & 1u;
-            my_nbr += (ev >> 26) & 1u;
+            nnz += (int)((ev >> 25) & 1u);
+            my_cont += (ev >> 26) & 1u;
+            my_nbr += (ev >> 27) & 1u;
         }
         nnz = nnz < 2 ? nnz : 2;
         if (!is_static) {
@@ -1115,13 +1117,15 @@ __device__ __forceinline__ void tile7_batch(const MechArgs &A, const Tile6SmemT<
     merge_counts<kStats>(c, Wp, sides, lane);
 }
 
-template <bool kStats, int kMinBlocks, bool kPair, int kTZ = 1, bool kV7 = false>
-__global__ void __launch_bounds__(kT6Threads, kMinBlocks) k_mech_tile6(MechArgs A, DevScalars *__restrict__ sc,
+template <bool kStats, int kMinBlocks, bool kPair, int kTZ = 1, bool kV7 = false, int kThreads = kT6Threads,
+          int kMMo = 0>
+__global__ void __launch_bounds__(kThreads, kMinBlocks) k_mech_tile6(MechArgs A, DevScalars *__restrict__ sc,
                                                                       int allow_prefilter) {
     if (sc->overflow) return;
     constexpr int kNB = TileGeo<kTZ>::kNB, kSQ = TileGeo<kTZ>::kSQ;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    using Smem = Tile6SmemT<kPair, kTZ, kV7>;
+    using Smem = Tile6SmemT<kPair, kTZ, kV7, kThreads, kMMo>;
+    constexpr int kWarps = kThreads / 32;
     Smem &S = *reinterpret_cast<Smem *>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     if (tid == 0) {
@@ -1149,7 +1153,7 @@ __global__ void __launch_bounds__(kT6Threads, kMinBlocks) k_mech_tile6(MechArgs 
             if (blockIdx.x == 0) atomicMax(&sc->enc_dmax, enc_double(sc->dmax_prev));
         }
     }
-    for (int lb = tid; lb < kNB; lb += kT6Threads) {
+    for (int lb = tid; lb < kNB; lb += kThreads) {
         const uint32_t lx = lb % 6, ly = (lb / 6) % 6, lz = lb / 36;
         const uint32_t inner =
             lx >= 1 && lx <= 4 && ly >= 1 && ly <= 4 && lz >= 1 && lz <= (uint32_t)(4 * kTZ);
@@ -1190,7 +1194,7 @@ __global__ void __launch_bounds__(kT6Threads, kMinBlocks) k_mech_tile6(MechArgs 
         }
         ti[0] = t, ti[1] = x, ti[2] = y, ti[3] = z, ti[4] = (int)a, ti[5] = (int)b;
     };
-    constexpr int kBI = (kNB + kT6Threads - 1) / kT6Threads;
+    constexpr int kBI = (kNB + kThreads - 1) / kThreads;
     if (tid == 0) draw(0);
     __syncthreads();
     for (int it = 0;; ++it) {
@@ -1250,11 +1254,11 @@ __global__ void __launch_bounds__(kT6Threads, kMinBlocks) k_mech_tile6(MechArgs 
             __syncthreads();
             run = inc - sum;
 #pragma unroll
-            for (int q = 0; q < kT6Warps - 1; ++q) run += q < w ? S.wsum[q] : 0u;
+            for (int q = 0; q < kWarps - 1; ++q) run += q < w ? S.wsum[q] : 0u;
         }
         int M = 0;
 #pragma unroll
-        for (int q = 0; q < kT6Warps; ++q) M += (int)S.wsum[q];
+        for (int q = 0; q < kWarps; ++q) M += (int)S.wsum[q];
         const int n0 = (int)(e0 - g0), n1 = (int)(e1 - g1);
         const int nc = n0 + n1;
         if (nc == 0) break;  // uniform across the CTA
@@ -1272,7 +1276,7 @@ __global__ void __launch_bounds__(kT6Threads, kMinBlocks) k_mech_tile6(MechArgs 
         }
         if (M > Smem::kMM || !S.use_pf) {
             // over-full region or |coordinates| / L >= 2^30: reference formulation
-            for (int k0 = 32 * w; k0 < nc; k0 += kT6Threads) {
+            for (int k0 = 32 * w; k0 < nc; k0 += kThreads) {
                 Counts c;
                 const int k = k0 + lane;
                 if (k < nc)
@@ -1294,7 +1298,7 @@ __global__ void __launch_bounds__(kT6Threads, kMinBlocks) k_mech_tile6(MechArgs 
             run += en[q] - st[q];
         }
         __syncthreads();
-        for (int lb = tid; lb < kNB; lb += kT6Threads) {
+        for (int lb = tid; lb < kNB; lb += kThreads) {
             const uint32_t o = S.off[lb], n = S.off[lb + 1] - o;
             const uint32_t v = S.lbxyz[lb];
             const bool inner = (v >> 10) != 0u;
@@ -1308,7 +1312,7 @@ __global__ void __launch_bounds__(kT6Threads, kMinBlocks) k_mech_tile6(MechArgs 
         __syncthreads();
         // ---- stage the region (row-major boxes, ascending id in a box)
         if constexpr (!kPair) {
-            for (int m = tid; m < M; m += kT6Threads) {  // (2 or 4 items per thread with
+            for (int m = tid; m < M; m += kThreads) {  // (2 or 4 items per thread with
                 // their loads in flight together measured slower: 1.80, 1.83 vs 1.75 ms)
                 const int lb = S.mbox[m];
                 const uint32_t gi = S.start[lb] + ((uint32_t)m - S.off[lb]);
@@ -1324,7 +1328,7 @@ __global__ void __launch_bounds__(kT6Threads, kMinBlocks) k_mech_tile6(MechArgs 
         } else {
             // ---- stage the region (row-major boxes, ascending id in a box): the packed
             // pair layout of the f32x2 walk (mech_kernel 3)
-            for (int m = tid; m < M; m += kT6Threads) {
+            for (int m = tid; m < M; m += kThreads) {
                 const int lb = S.mbox[m];
                 const uint32_t gi = S.start[lb] + ((uint32_t)m - S.off[lb]);
                 const double x = A.sx[gi], y = A.sy[gi], z = A.sz[gi], d = A.sd[gi];
@@ -1372,14 +1376,14 @@ __global__ void __launch_bounds__(kT6Threads, kMinBlocks) k_mech_tile6(MechArgs 
         // full 32-lane batches: a tile of <= 96 agents keeps a warp idle rather than
         // four warps 3/4 full (-1.2 % at cfg2 against max(min(4, n), ceil(n/32)))
         const int B = (nc + 31) >> 5;
-        for (int bb = w; bb < B; bb += kT6Warps) {  // warp-uniform
+        for (int bb = w; bb < B; bb += kWarps) {  // warp-uniform
             // floor(bb nc / B): B <= 14, so the quotient is >= 1/14 from the next integer
             // and the fp32 quotient (bb nc < 2^24) floors exactly
             const int klo = (int)__fdividef((float)(bb * nc), (float)B);
             const int khi = (int)__fdividef((float)((bb + 1) * nc), (float)B);
             // (batch bb = agents bb, bb + B, ... measured slower: 1.78 vs 1.75 ms)
             if constexpr (kV7 && !kPair)
-                tile7_batch<kStats, kTZ>(A, S, S.W[w], lane, g0, n0, g1, klo, khi - klo, M, sides);
+                tile7_batch<kStats, kTZ, Smem>(A, S, S.W[w], lane, g0, n0, g1, klo, khi - klo, M, sides);
             else
                 tile6_batch<kStats, kPair, kTZ>(A, S, S.W[w], lane, g0, n0, g1, klo, khi - klo, M, sides);
         }
@@ -1398,17 +1402,18 @@ __global__ void __launch_bounds__(kT6Threads, kMinBlocks) k_mech_tile6(MechArgs 
 
 // One-time per-device setup of a tile-kernel instance (shared-memory attribute, CTAs
 // per SM); returns the CTAs per SM.
-template <bool kStats, int kMinBlocks, bool kPair, int kTZ, bool kV7 = false>
+template <bool kStats, int kMinBlocks, bool kPair, int kTZ, bool kV7 = false, int kThreads = kT6Threads,
+          int kMMo = 0>
 static int tile6_per_sm(Ctx *c) {
     static int per_sm_dev[kMaxDevices] = {};
     int &per_sm = per_sm_dev[c->device];
     if (!per_sm) {
-        const int smem = (int)sizeof(Tile6SmemT<kPair, kTZ, kV7>);
+        const int smem = (int)sizeof(Tile6SmemT<kPair, kTZ, kV7, kThreads, kMMo>);
         int v = 0;
-        if (cudaFuncSetAttribute(k_mech_tile6<kStats, kMinBlocks, kPair, kTZ, kV7>,
+        if (cudaFuncSetAttribute(k_mech_tile6<kStats, kMinBlocks, kPair, kTZ, kV7, kThreads, kMMo>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess ||
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-                &v, k_mech_tile6<kStats, kMinBlocks, kPair, kTZ, kV7>, kT6Threads, smem) != cudaSuccess) {
+                &v, k_mech_tile6<kStats, kMinBlocks, kPair, kTZ, kV7, kThreads, kMMo>, kThreads, smem) != cudaSuccess) {
             cudaGetLastError();
             return 0;
         }
@@ -1417,16 +1422,17 @@ static int tile6_per_sm(Ctx *c) {
     return per_sm;
 }
 
-template <bool kStats, int kMinBlocks, bool kPair, int kTZ = 1, bool kV7 = false>
+template <bool kStats, int kMinBlocks, bool kPair, int kTZ = 1, bool kV7 = false, int kThreads = kT6Threads,
+          int kMMo = 0>
 static bdm_status launch_tile6(Ctx *c, const MechArgs &A, cudaStream_t st) {
-    const int per_sm = tile6_per_sm<kStats, kMinBlocks, kPair, kTZ, kV7>(c);
+    const int per_sm = tile6_per_sm<kStats, kMinBlocks, kPair, kTZ, kV7, kThreads, kMMo>(c);
     if (!per_sm) {
         set_error("tile kernel setup failed");
         return BDM_ECUDA;
     }
-    const int smem = (int)sizeof(Tile6SmemT<kPair, kTZ, kV7>);
-    k_mech_tile6<kStats, kMinBlocks, kPair, kTZ, kV7>
-        <<<(unsigned)(c->sm_count * per_sm), kT6Threads, smem, st>>>(A, c->sc, c->prefilter);
+    const int smem = (int)sizeof(Tile6SmemT<kPair, kTZ, kV7, kThreads, kMMo>);
+    k_mech_tile6<kStats, kMinBlocks, kPair, kTZ, kV7, kThreads, kMMo>
+        <<<(unsigned)(c->sm_count * per_sm), kThreads, smem, st>>>(A, c->sc, c->prefilter);
     return BDM_OK;
 }
 
@@ -1954,7 +1960,14 @@ bdm_status launch_mech(Ctx *c, bdm_agents *a, const bdm_params *p, cudaStream_t 
         tile6_per_sm<false, 4, false, 2>(c);
         tile6_per_sm<true, 4, false, 2>(c);
     }
-    if (c->mech_kernel == 5 && depth == 2) {  // tile7 batches (contact prefilter), two-tile units
+    if (c->mech_kernel == 5 && depth == 3) {
+        // tile7 batches, two-tile units for populations above one agent per box: 8 warps
+        // share one staged 6x6x10-box region of up to 672 agents, 3 CTAs per SM (option
+        // tile_depth 3; measured equal to the default at cfg2, DESIGN 7.1, so not the default)
+        const bdm_status s = p->collect_stats ? launch_tile6<true, 3, false, 2, true, 256, 672>(c, A, st)
+                                              : launch_tile6<false, 3, false, 2, true, 256, 672>(c, A, st);
+        if (s != BDM_OK) return s;
+    } else if (c->mech_kernel == 5 && depth == 2) {  // tile7 batches (contact prefilter), two-tile units
         const bdm_status s = p->collect_stats ? launch_tile6<true, 5, false, 2, true>(c, A, st)
                                               : launch_tile6<false, 5, false, 2, true>(c, A, st);
         if (s != BDM_OK) return s;

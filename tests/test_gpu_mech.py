@@ -17,12 +17,13 @@ REL_TOL = 1e-9  # north_star tolerance for fp64 positions
 
 
 @pytest.fixture(scope="module", params=[(0, 1), (1, 1), (2, 1), (3, 1), (0, 2), (0, 0), (4, 0),
-                                        (5, 1), (5, 2)],
+                                        (5, 1), (5, 2), (5, 3)],
                 ids=["tile", "reference", "tile_v1", "tile_4cta", "tile_depth2", "tile_auto", "row",
-                     "tile7", "tile7_depth2"])
+                     "tile7", "tile7_depth2", "tile7_big"])
 def eng(request):
     """Every mechanics kernel: the tile kernel (default; also with two-tile work units,
-    option tile_depth 2), the per-agent reference and the other tile variants."""
+    option tile_depth 2, and the 8-warp two-tile units of dense populations, tile_depth 3),
+    the per-agent reference and the other tile variants."""
     import torch
     if not torch.cuda.is_available():
         pytest.skip("no GPU")
