@@ -237,7 +237,10 @@ struct Src {
 
 // kGridIlp agents per thread (strided by the block size, so every load and store stays
 // coalesced): the per-agent atomics' round trips overlap instead of one per thread
-constexpr int kGridIlp = 4;
+#ifndef BDM_GRID_ILP
+#define BDM_GRID_ILP 4
+#endif
+constexpr int kGridIlp = BDM_GRID_ILP;
 constexpr int kGridThreads = 256;
 
 __global__ void __launch_bounds__(kGridThreads) k_key(Src S, const DevScalars *__restrict__ sc,
@@ -549,7 +552,10 @@ __global__ void __launch_bounds__(kGridThreads) k_scatter(Src S, const uint32_t 
 // local agents (scanned afterwards into their output index).
 // kFixIlp slots per thread (strided by the block size): their dependent chains (key ->
 // box range -> id rank -> source -> SoA) overlap.
-constexpr int kFixIlp = 2;
+#ifndef BDM_FIX_ILP
+#define BDM_FIX_ILP 2
+#endif
+constexpr int kFixIlp = BDM_FIX_ILP;
 __global__ void __launch_bounds__(kGridThreads) k_fix_gather(
     Src S, const uint32_t *__restrict__ skey, const uint32_t *__restrict__ sid,
     const uint32_t *__restrict__ perm_tmp, const uint32_t *__restrict__ box_start,
