@@ -365,7 +365,10 @@ bdm_status bdm_onco_step(bdm_handle h, bdm_agents *a, uint32_t *age, int64_t age
 #define BDM_PACK_AURA 2     /* x < lo + margin -> left, x >= hi - margin -> right; copy */
 
 /* A new NCCL unique id (128 bytes) for bdm_dist_init; rank 0 makes it, the caller
- * broadcasts it (e.g. torch.distributed).  Errors: BDM_ENCCL (no libnccl.so.2). */
+ * broadcasts it (e.g. torch.distributed).  The library links no NCCL: it resolves the
+ * nine entry points it uses from the process's libnccl.so.2 (torch's, if loaded), or
+ * from the library named by the environment variable BDM_NCCL_LIB when that is set
+ * (another NCCL build; the tests' stand-in).  Errors: BDM_ENCCL (no such library). */
 bdm_status bdm_nccl_unique_id(uint8_t id[128]);
 
 /* Join the N-rank x-slab group (NCCL communicator from the 128-byte unique id; N = 1

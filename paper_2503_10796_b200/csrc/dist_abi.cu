@@ -26,6 +26,7 @@
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nccl.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <string>
@@ -57,7 +58,17 @@ static const NcclApi *nccl_api(std::string &why) {
     static int state = 0;  // 0 untried, 1 ok, -1 failed
     static std::string err;
     if (state == 0) {
-        void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+        // BDM_NCCL_LIB names the library to use instead (another NCCL build; the tests'
+        // file-based stand-in that runs two ranks on one GPU, tests/nccl_shim/)
+        const char *over = getenv("BDM_NCCL_LIB");
+        void *h = over && *over ? dlopen(over, RTLD_NOW | RTLD_LOCAL) : nullptr;
+        if (over && *over && !h) {
+            err = std::string("BDM_NCCL_LIB: ") + dlerror();
+            state = -1;
+            why = err;
+            return nullptr;
+        }
+        if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
         if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
         if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
         state = -1;
