@@ -698,7 +698,10 @@ def _traffic(kernel, alg_bytes):
     except (OSError, KeyError, ValueError):
         return None
     return {"dram_bytes_per_launch": t["dram_bytes_per_launch"],
-            **{k: t[k] for k in ("issue_active_pct", "fp64_pipe_active_pct") if k in t},
+            **{k: t[k] for k in ("issue_active_pct", "fp64_pipe_active_pct", "warp_inst_per_launch",
+                                 "warp_inst_per_agent", "fp64_thread_inst_per_agent",
+                                 "shared_wavefronts_per_launch", "shared_bank_conflict_wavefronts_per_launch",
+                                 "warps_active_pct") if k in t},
             "alg_bytes_per_launch": alg_bytes,
             "ratio": t["dram_bytes_per_launch"] / alg_bytes if alg_bytes else None,
             "source": t["source"], "capture_workload": t["workload"]}
