@@ -1,6 +1,6 @@
 #!/bin/bash
 # session 4: HEAD health check (full GPU suite, smoke, default bench line, cfg5 with depth 2/auto)
-O=gpurun_out/s4g; mkdir -p $O
+O=gpurun_out/${BDM_OUT:-s4g}; mkdir -p $O
 python -c "import __graft_entry__ as g; g.build()" > $O/build.log 2>&1; echo build=$?
 timeout 1800 python -m pytest tests -m gpu -q -p no:cacheprovider > $O/pytest_gpu.log 2>&1; echo pytest=$?; tail -2 $O/pytest_gpu.log
 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo smoke=$?; tail -1 $O/smoke.log
