@@ -414,7 +414,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_apply(uint32_t *__restric
     }
 }
 
-// Single-pass exclusive scan of the slot counts (decoupled look-back): tile b (4096
+// Single-pass exclusive scan of the slot counts (decoupled look-back): tile b (kS1Tile
 // counts, blockIdx order) publishes its aggregate, then its inclusive prefix once the
 // prefixes before it are known; warp 0 looks back over the predecessors 32 at a time.
 // One word per tile: epoch << 34 | status << 32 | value (status 1 = aggregate, 2 =
@@ -423,6 +423,15 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_apply(uint32_t *__restric
 // graph tags every scan afresh).  Counts sum to the agent count (< 2^32).  Relies on tiles being dispatched in
 // blockIdx order, so a tile only waits for tiles that are resident or done.
 constexpr unsigned long long kScanAgg = 1ull, kScanInc = 2ull;
+// Its tiles hold kS1Items counts per thread: the look-back is a serial chain of one L2
+// round trip per 32 tiles, so the time falls with the tile count (8,192-count tiles:
+// 812 tiles at cfg2 instead of 1,623; ncu 34.3 -> see profiles/r02/s4/ab_session4.txt).
+#ifndef BDM_S1_ITEMS
+#define BDM_S1_ITEMS 16
+#endif
+constexpr int kS1Items = BDM_S1_ITEMS;
+constexpr int kS1Tile = kScanThreads * kS1Items;
+static_assert(kS1Items % 4 == 0, "vector path moves 4 counts at a time");
 __device__ __forceinline__ unsigned long long scan_word(uint32_t epoch, unsigned long long st,
                                                         uint32_t v) {
     return ((unsigned long long)epoch << 34) | (st << 32) | v;
@@ -433,23 +442,24 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_single(uint32_t *__restri
     if (sc->overflow) return;
     const uint32_t epoch = sc->scan_epoch;  // 1 .. 2^30 - 1 (0 = never written)
     const long long m = sc->nslots + 1;
-    const long long base = (long long)blockIdx.x * kScanTile;
+    const long long base = (long long)blockIdx.x * kS1Tile;
     if (base >= m) return;
-    uint32_t v[kScanItems];
-    const long long i0 = base + (long long)threadIdx.x * kScanItems;
-    const bool full = i0 + kScanItems <= m;
+    uint32_t v[kS1Items];
+    const long long i0 = base + (long long)threadIdx.x * kS1Items;
+    const bool full = i0 + kS1Items <= m;
     if (full) {
-        const uint4 a = *reinterpret_cast<const uint4 *>(cnt + i0);
-        const uint4 b = *reinterpret_cast<const uint4 *>(cnt + i0 + 4);
-        v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
-        v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+#pragma unroll
+        for (int q = 0; q < kS1Items / 4; ++q) {
+            const uint4 a = *reinterpret_cast<const uint4 *>(cnt + i0 + 4 * q);
+            v[4 * q] = a.x; v[4 * q + 1] = a.y; v[4 * q + 2] = a.z; v[4 * q + 3] = a.w;
+        }
     } else {
 #pragma unroll
-        for (int k = 0; k < kScanItems; ++k) v[k] = (i0 + k < m) ? cnt[i0 + k] : 0u;
+        for (int k = 0; k < kS1Items; ++k) v[k] = (i0 + k < m) ? cnt[i0 + k] : 0u;
     }
     uint32_t s = 0;
 #pragma unroll
-    for (int k = 0; k < kScanItems; ++k) s += v[k];
+    for (int k = 0; k < kS1Items; ++k) s += v[k];
     uint32_t tot;
     const uint32_t before = block_excl_scan(s, &tot);
     __shared__ uint32_t tile_prefix;
@@ -495,18 +505,19 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_single(uint32_t *__restri
     }
     __syncthreads();
     uint32_t run = tile_prefix + before;
-    uint32_t o[kScanItems];
+    uint32_t o[kS1Items];
 #pragma unroll
-    for (int k = 0; k < kScanItems; ++k) {
+    for (int k = 0; k < kS1Items; ++k) {
         o[k] = run;
         run += v[k];
     }
     if (full) {
-        *reinterpret_cast<uint4 *>(cnt + i0) = make_uint4(o[0], o[1], o[2], o[3]);
-        *reinterpret_cast<uint4 *>(cnt + i0 + 4) = make_uint4(o[4], o[5], o[6], o[7]);
+#pragma unroll
+        for (int q = 0; q < kS1Items / 4; ++q)
+            *reinterpret_cast<uint4 *>(cnt + i0 + 4 * q) = make_uint4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
     } else {
 #pragma unroll
-        for (int k = 0; k < kScanItems; ++k)
+        for (int k = 0; k < kS1Items; ++k)
             if (i0 + k < m) cnt[i0 + k] = o[k];
     }
 }
@@ -642,7 +653,7 @@ bdm_status launch_grid_sort(Ctx *c, const bdm_agents *a, const bdm_agents *g, cu
     if (c->keep_order && (s = need_agent_buf(c, &c->perm)) != BDM_OK) return s;
     const unsigned nbi = (unsigned)((n + kGridThreads * kGridIlp - 1) / (kGridThreads * kGridIlp));
     k_key<<<nbi, kGridThreads, 0, st>>>(S, c->sc, c->key, c->rank, c->box_start);
-    const unsigned sb = (unsigned)((c->slot_cap + 1 + kScanTile - 1) / kScanTile);
+    const unsigned sb = (unsigned)((c->slot_cap + 1 + kS1Tile - 1) / kS1Tile);
     if (c->scan_state_cap < (int64_t)sb) {
         if (c->scan_state) cudaFree(c->scan_state);
         c->scan_state = nullptr;
