@@ -221,9 +221,14 @@ __global__ void k_zero_counts(uint32_t *__restrict__ counts, DevScalars *__restr
     if (sc->overflow) return;
     if (blockIdx.x == 0 && threadIdx.x == 0) sc->scan_epoch = sc->scan_epoch % 0x3FFFFFFFu + 1u;
     const long long m = sc->nslots + 1;
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < m;
+    // 16-byte stores (the array is 256-byte aligned): with 4-byte stores the kernel was
+    // bound by its own instruction issue (77 %), not by the 27 MB it writes at cfg2
+    const long long m4 = m >> 2;
+    uint4 *const c4 = reinterpret_cast<uint4 *>(counts);
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < m4;
          i += (long long)gridDim.x * blockDim.x)
-        counts[i] = 0u;
+        c4[i] = make_uint4(0u, 0u, 0u, 0u);
+    if (blockIdx.x == 0 && threadIdx.x < (m & 3)) counts[4 * m4 + threadIdx.x] = 0u;
 }
 
 // Agents [0, nl) are local, [nl, nl + ng) are the ghosts (aura) of this build.
