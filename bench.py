@@ -411,8 +411,9 @@ def run_ours(args, ws, rank, local):
         "roofline": {"bound": "alu", "kernel": "k_mech (a5-a9)",
                      "achieved": achieved / 1e12, "peak": fp64_peak / 1e12,
                      "unit": "T fp64-inst/s", "frac": achieved / fp64_peak,
-                     **_traffic_keys(_traffic("k_mech_tile6", MECH_ALG_BYTES_PER_AGENT * cfg.n)
-                                     if cfg.name == "cfg2" else None),
+                     **_traffic_keys(_traffic("k_mech_tile6" if cfg.name == "cfg2" else "k_mech_tile6_cfg5",
+                                              MECH_ALG_BYTES_PER_AGENT * cfg.n)
+                                     if cfg.name in ("cfg2", "cfg5") else None),
                      "peak_source": f"{sm_count} SMs x 64 fp64 lanes x {max_mhz:.0f} MHz "
                                     f"(guide unit counts, max clock); measured DFMA "
                                     f"{dfma_meas / 1e12:.2f} T/s",
