@@ -642,8 +642,11 @@ bdm_status launch_grid_sort(Ctx *c, const bdm_agents *a, const bdm_agents *g, cu
     S.gflags = g ? g->flags : nullptr;
     const int64_t n = S.nl + S.ng;
     {
-        int64_t zb = (c->slot_cap + 1 + 1023) / 1024;
-        const int64_t maxb = (int64_t)c->sm_count * 16;
+#ifndef BDM_ZERO_BLOCKS_PER_SM
+#define BDM_ZERO_BLOCKS_PER_SM 4
+#endif
+        int64_t zb = ((c->slot_cap + 1) / 4 + 1 + 1023) / 1024;  // one 16-byte store per thread and pass
+        const int64_t maxb = (int64_t)c->sm_count * BDM_ZERO_BLOCKS_PER_SM;
         if (zb > maxb) zb = maxb;
         k_zero_counts<<<(unsigned)zb, 1024, 0, st>>>(c->box_start, c->sc);
     }
